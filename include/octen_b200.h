@@ -1,0 +1,158 @@
+/* octen_b200.h -- C-ABI of the B200-native OCTen per-batch pipeline.
+ *
+ * Drop-in boundary for the reference library `cpstream`
+ * (/root/reference/proj, C++20 + Eigen).  The reference exposes no FFI; its
+ * boundary is the C++ API of the static library (proj/src/CMakeLists.txt:1-13).
+ * Each entry point below replaces the reference function cited beside it and
+ * takes plain pointers in the reference's own layouts:
+ *   - matrices: column-major fp64 (Eigen::MatrixXd default);
+ *   - tensors:  first index fastest (proj/include/cpstream/tensor.hpp:32-34);
+ *   - per-replica blocks are stacked replica-major.
+ * No torch types cross this boundary.
+ *
+ * Errors follow proj/include/cpstream/errors.hpp: every call returns
+ * OCTEN_OK or the status of the exception the reference would throw; the
+ * message (the reference's text) is available from octen_last_error() in the
+ * calling thread.  A stream handle is not thread-safe (one ingest at a time,
+ * SPEC.md:453); distinct handles are independent.
+ */
+#ifndef OCTEN_B200_H
+#define OCTEN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OCTEN_OK 0
+#define OCTEN_ERR_CONFIG 2   /* cpstream::ConfigError  */
+#define OCTEN_ERR_NUMERIC 3  /* cpstream::NumericError */
+#define OCTEN_ERR_IO 4       /* cpstream::IoError      */
+#define OCTEN_ERR_CUDA 5     /* device failure          */
+#define OCTEN_ERR_INTERNAL 6
+
+#define OCTEN_F64 0 /* batch element type */
+#define OCTEN_F32 1
+#define OCTEN_HOST 0 /* batch location */
+#define OCTEN_DEVICE 1
+
+/* cpstream::AlsConfig (proj/include/cpstream/cp_als.hpp:25-31) */
+typedef struct octen_als_config {
+    int32_t rank;
+    int32_t max_iters;
+    double rel_tol;
+    int32_t n_restarts;
+    uint64_t seed;
+} octen_als_config;
+
+/* cpstream::StreamConfig (proj/include/cpstream/streaming.hpp:15-27) */
+typedef struct octen_stream_config {
+    int32_t rank;
+    int32_t p;
+    int32_t q;
+    int32_t shared;
+    int32_t temporal_mode; /* -1: last mode */
+    octen_als_config als;
+    uint64_t seed;
+    int32_t enforce_bounds;
+    int32_t workers; /* accepted for API parity; the device path is schedule-free */
+    int32_t strict;
+    double residual_warning;
+    int32_t device; /* CUDA ordinal */
+} octen_stream_config;
+
+/* cpstream::BatchRecord (proj/include/cpstream/streaming.hpp:31-42) */
+typedef struct octen_batch_record {
+    int64_t batch_index;
+    int64_t t_new;
+    double temporal_residual;
+    double min_match_similarity;
+    double max_offdiag_similarity;
+    int32_t warned;
+    double compress_seconds;
+    double als_seconds;
+    double recover_seconds;
+    double total_seconds;
+} octen_batch_record;
+
+typedef struct octen_stream octen_stream;
+
+/* Message of the last failed call in this thread (empty if none). */
+const char* octen_last_error(void);
+/* Library version string. */
+const char* octen_version(void);
+
+/* init_stream (proj/include/cpstream/streaming.hpp:64; src/streaming.cpp:181-256).
+ * data: I x J x t0 batch, first index fastest, dtype OCTEN_F64/F32 at
+ * location OCTEN_HOST/DEVICE; dims[order].  On success *out owns the stream. */
+int octen_stream_init(const octen_stream_config* cfg, const void* data, int dtype, int location, int order,
+                      const int64_t* dims, octen_stream** out);
+
+/* ingest_batch (streaming.hpp:70; src/streaming.cpp:258-346). */
+int octen_stream_ingest(octen_stream* s, const void* data, int dtype, int location, int order,
+                        const int64_t* dims);
+
+void octen_stream_destroy(octen_stream* s);
+
+/* Stream state accessors (StreamState, streaming.hpp:48-59).
+ * info[0..7] = order, I, J, K(slices_seen), rank, p, q, batches_seen. */
+int octen_stream_info(const octen_stream* s, int64_t* info);
+/* KruskalModel factor `mode` (dim x rank, col-major) and lambda (rank). */
+int octen_stream_get_factor(const octen_stream* s, int mode, double* out);
+int octen_stream_get_lambda(const octen_stream* s, double* out);
+/* BatchRecord of log entry `index` (0 = init). */
+int octen_stream_get_record(const octen_stream* s, int64_t index, octen_batch_record* out);
+/* SummaryState: y (p x Q^3) and history (p x Q x rank). */
+int octen_stream_get_summaries(const octen_stream* s, double* y);
+int octen_stream_get_history(const octen_stream* s, double* h);
+/* The per-replica CP-ALS models of the last batch: factors p x 3 x Q x rank,
+ * lambda p x rank. */
+int octen_stream_get_replica_models(const octen_stream* s, double* factors, double* lambda);
+
+/* ---- stage-level entry points (the reference's L2 API, batched over replicas) ---- */
+
+/* compress (proj/include/cpstream/compression.hpp:82-83; src/compression.cpp:108-130)
+ * for all replicas: z[r] = x x1 U_r^T x2 V_r^T x3 W_r^T.
+ * u: p x I x Q, v: p x J x Q, w: p x t x Q (col-major per replica), x: I x J x t
+ * (dtype OCTEN_F64 or OCTEN_F32, host); z: p x Q^3 (host, overwritten). */
+int octen_compress(int p, int q, int shared, int64_t I, int64_t J, int64_t t, const double* u, const double* v,
+                   const double* w, const void* x, int dtype, double* z);
+
+/* cp_als (proj/include/cpstream/cp_als.hpp:48; src/cp_als.cpp:240-359) on p
+ * cubic Q^3 tensors (host, p x Q^3) with seeds[p]; cfg->seed is ignored.
+ * factors: p x 3 x Q x rank, lambda: p x rank, fit: p, iterations: p. */
+int octen_cp_als_batched(int p, int q, const double* y, const octen_als_config* cfg, const uint64_t* seeds,
+                         double* factors, double* lambda, double* fit, int32_t* iterations);
+
+/* align_replicas (proj/include/cpstream/recovery.hpp:43; src/recovery.cpp:106-291).
+ * models: factors p x 3 x Q x R, lambda p x R; u/v: p x I x Q / p x J x Q;
+ * tgram: shared x shared temporal_shared_gram.  stacks: 3 x (pQ x R),
+ * perms: p x R, scales: p x 3 x R, sims[2] = {min_match, max_offdiag}. */
+int octen_align_replicas(int p, int q, int shared, int rank, int64_t I, int64_t J, const double* u,
+                         const double* v, const double* tgram, const double* factors, const double* lambda,
+                         double* stacks, int32_t* perms, double* scales, double* sims);
+
+/* recover_nontemporal (recovery.hpp:54; src/recovery.cpp:315-319) for mode
+ * 0 (proj = stacked U^T) or 1 (stacked V^T): out = argmin |P~ out - stack|.
+ * proj_blocks: p x d x Q, stack: pQ x R, out: d x R. */
+int octen_recover_nontemporal(int p, int q, int64_t d, int rank, int mode, const double* proj_blocks,
+                              const double* stack, double* out);
+
+/* temporal_stack_from_summaries (recovery.hpp:98-99; src/recovery.cpp:429-462).
+ * y: p x Q^3; u, v as above; a: I x R, b: J x R; out: pQ x R. */
+int octen_temporal_stack_from_summaries(int p, int q, int rank, int64_t I, int64_t J, const double* y,
+                                        const double* u, const double* v, const double* a, const double* b,
+                                        double* out);
+
+/* recover_temporal_append (recovery.hpp:85-88; src/recovery.cpp:341-427),
+ * without column weights.  w: p x t x Q; history: p x Q x R (in/out, zero on
+ * the first batch); new_rows: t x R; residual: relative solve residual. */
+int octen_recover_temporal_append(int p, int q, int rank, int64_t t, const double* temporal_stack,
+                                  const double* w, double* history, double* new_rows, double* residual);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OCTEN_B200_H */

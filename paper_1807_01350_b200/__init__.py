@@ -1,0 +1,373 @@
+"""B200-native OCTen per-batch pipeline (arXiv 1807.01350) -- Python mirror of
+the reference library's hot-path API (cpstream: init_stream / ingest_batch /
+compress / cp_als / align_replicas / recover_*), calling the sm_100a kernels
+through the C-ABI in include/octen_b200.h.
+
+Tensors follow the reference layout (first index fastest,
+proj/include/cpstream/tensor.hpp:32-34): a numpy array of shape (I, J, t) is
+read in Fortran order; a torch CUDA tensor must be Fortran-contiguous
+(strides (1, I, I*J)), e.g. ``torch.empty(t, J, I).permute(2, 1, 0)``.
+Matrices are column-major float64.  Errors raise ConfigError / NumericError
+with the reference's message text.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _capi as C
+
+__all__ = ["ConfigError", "NumericError", "IoError", "CudaError", "AlsConfig", "StreamConfig", "BatchRecord",
+           "KruskalModel", "StreamState", "init_stream", "ingest_batch", "compress", "cp_als_batched",
+           "align_replicas", "recover_nontemporal", "temporal_stack_from_summaries", "recover_temporal_append",
+           "version"]
+
+
+class Error(RuntimeError):
+    """errors.hpp:9-12."""
+
+
+class ConfigError(Error):
+    """errors.hpp:14-17."""
+
+
+class NumericError(Error):
+    """errors.hpp:19-22."""
+
+
+class IoError(Error):
+    """errors.hpp:24-27."""
+
+
+class CudaError(Error):
+    """Device failure (no reference counterpart)."""
+
+
+def _check(status: int) -> None:
+    if status == C.OCTEN_OK:
+        return
+    msg = C.LIB.octen_last_error().decode()
+    if status == C.OCTEN_ERR_CONFIG:
+        raise ConfigError(msg)
+    if status == C.OCTEN_ERR_NUMERIC:
+        raise NumericError(msg)
+    if status == C.OCTEN_ERR_IO:
+        raise IoError(msg)
+    if status == C.OCTEN_ERR_CUDA:
+        raise CudaError(msg)
+    raise Error(msg)
+
+
+def version() -> str:
+    return C.LIB.octen_version().decode()
+
+
+@dataclass
+class AlsConfig:
+    """cp_als.hpp:25-31."""
+    rank: int = 1
+    max_iters: int = 100
+    rel_tol: float = 1e-8
+    n_restarts: int = 3
+    seed: int = 0
+
+    def _c(self) -> C.AlsConfigC:
+        return C.AlsConfigC(self.rank, self.max_iters, self.rel_tol, self.n_restarts, self.seed)
+
+
+@dataclass
+class StreamConfig:
+    """streaming.hpp:15-27."""
+    rank: int = 1
+    p: int = 1
+    q: int = 1
+    shared: int = 0
+    temporal_mode: int = -1
+    als: AlsConfig = field(default_factory=AlsConfig)
+    seed: int = 0
+    enforce_bounds: bool = False
+    workers: int = 0
+    strict: bool = False
+    residual_warning: float = 1e-3
+    device: int = 0
+
+    def _c(self) -> C.StreamConfigC:
+        return C.StreamConfigC(self.rank, self.p, self.q, self.shared, self.temporal_mode, self.als._c(), self.seed,
+                               int(self.enforce_bounds), self.workers, int(self.strict), self.residual_warning,
+                               self.device)
+
+
+@dataclass
+class BatchRecord:
+    """streaming.hpp:31-42."""
+    batch_index: int
+    t_new: int
+    temporal_residual: float
+    min_match_similarity: float
+    max_offdiag_similarity: float
+    warned: bool
+    compress_seconds: float
+    als_seconds: float
+    recover_seconds: float
+    total_seconds: float
+
+
+@dataclass
+class KruskalModel:
+    """cp_als.hpp:12-23."""
+    factors: List[np.ndarray]
+    lambda_: np.ndarray
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.P_dbl)
+
+
+def _f64(a) -> np.ndarray:
+    """Column-major contiguous float64 copy/view."""
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _batch_args(batch):
+    """-> (keepalive, void*, dtype, location, dims)."""
+    try:
+        import torch
+    except Exception:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(batch, torch.Tensor):
+        if batch.dim() < 1:
+            raise ConfigError("octen: batch must be a tensor")
+        dims = list(batch.shape)
+        expect = []
+        s = 1
+        for d in dims:
+            expect.append(s)
+            s *= d
+        if [st for st, d in zip(batch.stride(), dims) if d > 1] != [e for e, d in zip(expect, dims) if d > 1]:
+            raise ConfigError("octen: torch batch must be first-index-fastest (Fortran-contiguous)")
+        if batch.dtype == torch.float32:
+            dt = C.OCTEN_F32
+        elif batch.dtype == torch.float64:
+            dt = C.OCTEN_F64
+        else:
+            raise ConfigError("octen: batch dtype must be float32 or float64")
+        loc = C.OCTEN_DEVICE if batch.is_cuda else C.OCTEN_HOST
+        return batch, ctypes.c_void_p(batch.data_ptr()), dt, loc, dims
+    a = np.asarray(batch)
+    if a.dtype == np.float32:
+        dt = C.OCTEN_F32
+    else:
+        a = a.astype(np.float64, copy=False)
+        dt = C.OCTEN_F64
+    a = np.asfortranarray(a)
+    return a, ctypes.c_void_p(a.ctypes.data), dt, C.OCTEN_HOST, list(a.shape)
+
+
+class StreamState:
+    """streaming.hpp:48-59, device resident.  Use init_stream()."""
+
+    def __init__(self, handle, config: StreamConfig):
+        self._h = handle
+        self.config = config
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            C.LIB.octen_stream_destroy(h)
+            self._h = None
+
+    def _info(self):
+        info = (C.c_i64 * 8)()
+        _check(C.LIB.octen_stream_info(self._h, info))
+        return list(info)
+
+    @property
+    def slices_seen(self) -> int:
+        return self._info()[3]
+
+    @property
+    def batches_seen(self) -> int:
+        return self._info()[7]
+
+    @property
+    def model(self) -> KruskalModel:
+        info = self._info()
+        dims, rank = info[1:4], info[4]
+        factors = []
+        for m in range(3):
+            f = np.zeros((dims[m], rank), order="F")
+            _check(C.LIB.octen_stream_get_factor(self._h, m, _dptr(f)))
+            factors.append(f)
+        lam = np.zeros(rank)
+        _check(C.LIB.octen_stream_get_lambda(self._h, _dptr(lam)))
+        return KruskalModel(factors, lam)
+
+    @property
+    def log(self) -> List[BatchRecord]:
+        out = []
+        n = self._info()[7]
+        for i in range(n):
+            r = C.BatchRecordC()
+            _check(C.LIB.octen_stream_get_record(self._h, i, ctypes.byref(r)))
+            out.append(BatchRecord(r.batch_index, r.t_new, r.temporal_residual, r.min_match_similarity,
+                                   r.max_offdiag_similarity, bool(r.warned), r.compress_seconds, r.als_seconds,
+                                   r.recover_seconds, r.total_seconds))
+        return out
+
+    def summaries(self):
+        """SummaryState.y as a list of Q^3 tensors and history (p x Q x R)."""
+        info = self._info()
+        rank, p, q = info[4], info[5], info[6]
+        y = np.zeros(p * q * q * q)
+        _check(C.LIB.octen_stream_get_summaries(self._h, _dptr(y)))
+        h = np.zeros(p * q * rank)
+        _check(C.LIB.octen_stream_get_history(self._h, _dptr(h)))
+        ys = [y[i * q ** 3:(i + 1) * q ** 3].reshape((q, q, q), order="F") for i in range(p)]
+        hs = [h[i * q * rank:(i + 1) * q * rank].reshape((q, rank), order="F") for i in range(p)]
+        return ys, hs
+
+    def replica_models(self) -> List[KruskalModel]:
+        info = self._info()
+        rank, p, q = info[4], info[5], info[6]
+        f = np.zeros(p * 3 * q * rank)
+        lam = np.zeros(p * rank)
+        _check(C.LIB.octen_stream_get_replica_models(self._h, _dptr(f), _dptr(lam)))
+        out = []
+        for i in range(p):
+            fs = [f[(i * 3 + n) * q * rank:(i * 3 + n + 1) * q * rank].reshape((q, rank), order="F").copy()
+                  for n in range(3)]
+            out.append(KruskalModel(fs, lam[i * rank:(i + 1) * rank].copy()))
+        return out
+
+
+def init_stream(first_batch, cfg: StreamConfig) -> StreamState:
+    """streaming.hpp:64 / streaming.cpp:181-256."""
+    keep, ptr, dt, loc, dims = _batch_args(first_batch)
+    d = (C.c_i64 * len(dims))(*dims)
+    h = ctypes.c_void_p()
+    c = cfg._c()
+    _check(C.LIB.octen_stream_init(ctypes.byref(c), ptr, dt, loc, len(dims), d, ctypes.byref(h)))
+    del keep
+    return StreamState(h, cfg)
+
+
+def ingest_batch(state: StreamState, batch) -> None:
+    """streaming.hpp:70 / streaming.cpp:258-346."""
+    keep, ptr, dt, loc, dims = _batch_args(batch)
+    d = (C.c_i64 * len(dims))(*dims)
+    _check(C.LIB.octen_stream_ingest(state._h, ptr, dt, loc, len(dims), d))
+    del keep
+
+
+def compress(batch, u: List[np.ndarray], v: List[np.ndarray], w: List[np.ndarray], shared: int) -> List[np.ndarray]:
+    """compression.cpp:108-130 for every replica: z_r = x x1 U_r^T x2 V_r^T x3 W_r^T.
+    u[r]: I x Q, v[r]: J x Q, w[r]: t x Q (temporal rows of this batch)."""
+    p = len(u)
+    q = u[0].shape[1]
+    x = np.asarray(batch)
+    I, J, t = x.shape
+    if x.dtype == np.float32:
+        xa, dt = np.asfortranarray(x), C.OCTEN_F32
+    else:
+        xa, dt = np.asfortranarray(x, dtype=np.float64), C.OCTEN_F64
+    U = np.concatenate([_f64(a).ravel(order="F") for a in u])
+    V = np.concatenate([_f64(a).ravel(order="F") for a in v])
+    W = np.concatenate([_f64(a).ravel(order="F") for a in w])
+    z = np.zeros(p * q ** 3)
+    _check(C.LIB.octen_compress(p, q, shared, I, J, t, _dptr(U), _dptr(V), _dptr(W),
+                                ctypes.c_void_p(xa.ctypes.data), dt, _dptr(z)))
+    return [z[r * q ** 3:(r + 1) * q ** 3].reshape((q, q, q), order="F") for r in range(p)]
+
+
+def cp_als_batched(tensors: List[np.ndarray], cfg: AlsConfig, seeds: List[int]):
+    """cp_als (cp_als.cpp:240-359) on several Q x Q x Q tensors, seeds per
+    tensor.  Returns (models, fits, iterations)."""
+    p = len(tensors)
+    q = tensors[0].shape[0]
+    y = np.concatenate([_f64(t).ravel(order="F") for t in tensors])
+    f = np.zeros(p * 3 * q * cfg.rank)
+    lam = np.zeros(p * cfg.rank)
+    fit = np.zeros(p)
+    it = np.zeros(p, dtype=np.int32)
+    sd = (C.c_u64 * p)(*seeds)
+    c = cfg._c()
+    _check(C.LIB.octen_cp_als_batched(p, q, _dptr(y), ctypes.byref(c), sd, _dptr(f), _dptr(lam), _dptr(fit),
+                                      it.ctypes.data_as(C.P_i32)))
+    r = cfg.rank
+    models = []
+    for i in range(p):
+        fs = [f[(i * 3 + n) * q * r:(i * 3 + n + 1) * q * r].reshape((q, r), order="F").copy() for n in range(3)]
+        models.append(KruskalModel(fs, lam[i * r:(i + 1) * r].copy()))
+    return models, fit, it
+
+
+def align_replicas(models: List[KruskalModel], u: List[np.ndarray], v: List[np.ndarray], tgram: np.ndarray,
+                   shared: int):
+    """recovery.cpp:106-291.  Returns (stacks[3] (pQ x R), perms (p x R),
+    scales (p x 3 x R), min_match, max_offdiag)."""
+    p = len(models)
+    q, rank = models[0].factors[0].shape
+    I, J = u[0].shape[0], v[0].shape[0]
+    U = np.concatenate([_f64(a).ravel(order="F") for a in u])
+    V = np.concatenate([_f64(a).ravel(order="F") for a in v])
+    F = np.concatenate([_f64(f).ravel(order="F") for m in models for f in m.factors])
+    L = np.concatenate([np.asarray(m.lambda_, dtype=np.float64) for m in models])
+    tg = _f64(tgram if shared > 0 else np.zeros((0, 0))).ravel(order="F")
+    if tg.size == 0:
+        tg = np.zeros(1)
+    stacks = np.zeros(3 * p * q * rank)
+    perms = np.zeros(p * rank, dtype=np.int32)
+    scales = np.zeros(p * 3 * rank)
+    sims = np.zeros(2)
+    _check(C.LIB.octen_align_replicas(p, q, shared, rank, I, J, _dptr(U), _dptr(V), _dptr(tg), _dptr(F), _dptr(L),
+                                      _dptr(stacks), perms.ctypes.data_as(C.P_i32), _dptr(scales), _dptr(sims)))
+    st = [stacks[n * p * q * rank:(n + 1) * p * q * rank].reshape((p * q, rank), order="F") for n in range(3)]
+    return st, perms.reshape((p, rank)), scales.reshape((p, 3, rank)), float(sims[0]), float(sims[1])
+
+
+def recover_nontemporal(stack: np.ndarray, proj_blocks: List[np.ndarray], mode: int) -> np.ndarray:
+    """recovery.cpp:315-319 with P~ = [B_1^T; ...; B_p^T], B_r = proj_blocks[r] (d x Q)."""
+    p = len(proj_blocks)
+    d, q = proj_blocks[0].shape
+    rank = stack.shape[1]
+    Bk = np.concatenate([_f64(a).ravel(order="F") for a in proj_blocks])
+    S = _f64(stack)
+    out = np.zeros((d, rank), order="F")
+    _check(C.LIB.octen_recover_nontemporal(p, q, d, rank, mode, _dptr(Bk), _dptr(S), _dptr(out)))
+    return out
+
+
+def temporal_stack_from_summaries(ys: List[np.ndarray], u, v, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """recovery.cpp:429-462."""
+    p = len(ys)
+    q = ys[0].shape[0]
+    rank = a.shape[1]
+    Y = np.concatenate([_f64(y).ravel(order="F") for y in ys])
+    U = np.concatenate([_f64(x).ravel(order="F") for x in u])
+    V = np.concatenate([_f64(x).ravel(order="F") for x in v])
+    A, B = _f64(a), _f64(b)
+    out = np.zeros((p * q, rank), order="F")
+    _check(C.LIB.octen_temporal_stack_from_summaries(p, q, rank, A.shape[0], B.shape[0], _dptr(Y), _dptr(U), _dptr(V),
+                                                     _dptr(A), _dptr(B), _dptr(out)))
+    return out
+
+
+def recover_temporal_append(temporal_stack: np.ndarray, w: List[np.ndarray], history: List[np.ndarray]):
+    """recovery.cpp:341-427 (no column weights).  history is updated in place
+    (list of Q x R).  Returns (new_rows, residual)."""
+    p = len(w)
+    t, q = w[0].shape
+    rank = temporal_stack.shape[1]
+    W = np.concatenate([_f64(x).ravel(order="F") for x in w])
+    H = np.concatenate([_f64(h if h.size else np.zeros((q, rank))).ravel(order="F") for h in history])
+    S = _f64(temporal_stack)
+    rows = np.zeros((t, rank), order="F")
+    res = ctypes.c_double(0.0)
+    _check(C.LIB.octen_recover_temporal_append(p, q, rank, t, _dptr(S), _dptr(W), _dptr(H), _dptr(rows),
+                                               ctypes.byref(res)))
+    for i in range(p):
+        history[i] = H[i * q * rank:(i + 1) * q * rank].reshape((q, rank), order="F").copy()
+    return rows, res.value

@@ -1,0 +1,1005 @@
+// Stage 2: batched CP-ALS over every (replica, restart) problem.
+//
+// Restates cp_als (reference proj/src/cp_als.cpp:240-359) with
+//   * the GEVD warm start (cp_als.cpp:46-190): thin-U of the mode-0/1
+//     unfoldings from the Gram eigenbasis (Jacobi), slice mixtures w ~ U(-1,1)
+//     from derive(restart_seed,{11,attempt}) (host RNG, bit-exact), R x R
+//     pencil eigen-decomposition (orthes+hqr2), COD solve, rank-1 peel;
+//   * cyclic mode updates with the Hadamard-of-Grams solve, per-update
+//     normalization into lambda and the seeded column rescue (device
+//     mt19937_64, cp_als.cpp:293,309-319);
+//   * fit from the cached last-mode MTTKRP and the |dfit| < rel_tol stop
+//     (cp_als.cpp:325-345); best of n_restarts with first-wins ties.
+// MTTKRPs use a dimension tree: T = Y x3 C is shared by the mode-0 and mode-1
+// updates (C does not change between them), mode 2 contracts Y_(2) with the
+// Khatri-Rao product of the new A, B.  All restarts of a replica share every
+// read of Y_p.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+
+#include "engine.hpp"
+#include "gemm_simt.cuh"
+#include "rng_host.hpp"
+#include "small_linalg.cuh"
+
+namespace octen {
+
+namespace {
+
+constexpr double kDegenerateNorm = 1e-14;  // cp_als.cpp:17
+constexpr double kEps = 2.220446049250313e-16;
+
+struct AlsDev {
+    int P, S, Q, R, NP, max_iters;
+    double rel_tol;
+    const double* Y;
+    double* normx2;
+    double* F;
+    double* G;
+    double* lam;
+    double* T;
+    double* KR;
+    double* Mb;
+    double* fit_hist;
+    double* res_hist;
+    AlsState* state;
+    DevStatus* err;
+    Mt64* rngs;
+    const std::uint64_t* rescue_seed;
+    int* active_count;
+    // GEVD
+    double* Gev;
+    double* EV;
+    double* Ur;
+    double* Wmix;
+    double* Smix;
+    double* Tmp6;
+    double* Pm;
+    double* Hh;
+    double* gscr;
+    int* usable;
+    int* att_start;
+    int* att_used;
+    int* todo;
+    int* peel_fail;
+    __device__ size_t q3() const { return (size_t)Q * Q * Q; }
+    __device__ size_t q2() const { return (size_t)Q * Q; }
+    __device__ double* f(int prob, int n) const { return F + ((size_t)prob * 3 + n) * Q * R; }
+    __device__ double* g(int prob, int n) const { return G + ((size_t)prob * 3 + n) * R * R; }
+};
+
+__device__ double block_sum(double v, double* red) {
+    // deterministic block reduction (fixed tree)
+    red[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    const double out = red[0];
+    __syncthreads();
+    return out;
+}
+
+// ||Y_p||_F^2 per replica.
+__global__ void als_norm_kernel(AlsDev d) {
+    __shared__ double red[256];
+    const double* y = d.Y + (size_t)blockIdx.x * d.q3();
+    double s = 0.0;
+    for (size_t i = threadIdx.x; i < d.q3(); i += blockDim.x) s += y[i] * y[i];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) d.normx2[blockIdx.x] = s;
+}
+
+// ---------------- GEVD init ----------------
+
+// Jacobi eigen-decomposition of the two Gram matrices of replica p, top-R
+// eigenvectors into Ur[p][which] (descending eigenvalue), usability flag.
+__global__ void gevd_eig_sym_kernel(AlsDev d) {
+    extern __shared__ double sm[];
+    const int p = blockIdx.x / 2, which = blockIdx.x % 2;
+    const int Q = d.Q, R = d.R;
+    double* A = sm;                      // Q*Q
+    double* cs = A + (size_t)Q * Q;      // 2*(Q+2)
+    int* flag = (int*)(cs + 2 * (Q + 2));
+    int* order = flag + 4;               // Q
+    const double* src = d.Gev + ((size_t)p * 2 + which) * Q * Q;
+    double* V = d.EV + ((size_t)p * 2 + which) * Q * Q;
+    for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) A[i] = src[i];
+    __syncthreads();
+    TeamDev team;
+    jacobi_eig_sym(team, Q, A, V, cs, flag);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // order by descending eigenvalue (stable: lower index first on ties)
+        for (int i = 0; i < Q; ++i) order[i] = i;
+        for (int i = 1; i < Q; ++i) {
+            const int key = order[i];
+            const double kv = A[key + (size_t)Q * key];
+            int j = i - 1;
+            while (j >= 0 && A[order[j] + (size_t)Q * order[j]] < kv) {
+                order[j + 1] = order[j];
+                --j;
+            }
+            order[j + 1] = key;
+        }
+        const double lmax = A[order[0] + (size_t)Q * order[0]];
+        // nonzero singular values: eigenvalues above the rounding floor
+        int nz = 0;
+        for (int i = 0; i < Q; ++i)
+            if (A[order[i] + (size_t)Q * order[i]] > kEps * Q * lmax && lmax > 0.0) ++nz;
+        if (which == 0) atomicAnd(&d.usable[p], nz >= R ? 1 : 0);
+        if (which == 1) atomicAnd(&d.usable[p], nz >= R ? 1 : 0);
+    }
+    __syncthreads();
+    double* ur = d.Ur + ((size_t)p * 2 + which) * Q * R;
+    for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
+        const int i = e % Q, r = e / Q;
+        ur[i + (size_t)Q * r] = V[i + (size_t)Q * order[r]];
+    }
+}
+
+// Per problem: pick the first GEVD attempt whose pencil is invertible, has a
+// real Schur form and gives non-degenerate a1 columns (cp_als.cpp:110-150).
+__global__ void gevd_pencil_kernel(AlsDev d) {
+    const int prob = blockIdx.x;
+    if (!d.todo[prob]) return;
+    const int p = prob / d.S;
+    const int Q = d.Q, R = d.R;
+    extern __shared__ double sm[];
+    double* asub = sm;                  // R*R
+    double* nrm = asub + R * R;         // R
+    __shared__ int ok, att;
+    double* scr = d.gscr + (size_t)prob * (6 * R * R + 4 * R);
+    double* m_inv = scr;
+    double* m_pen = m_inv + R * R;
+    double* m_h = m_pen + R * R;
+    double* m_v = m_h + R * R;
+    double* wr = m_v + R * R;
+    double* wi = wr + R;
+    double* ort = wi + R;
+    int* rowp = (int*)(ort + R);  // 2R ints = R doubles; total 4R^2 + 4R of the 6R^2 + 4R scratch
+    int* colp = rowp + R;
+    const double* ur = d.Ur + ((size_t)p * 2 + 0) * Q * R;
+    double* a1 = d.f(prob, 0);
+    if (threadIdx.x == 0) att = -1;
+    __syncthreads();
+    for (int a = d.att_start[prob]; a < 3; ++a) {
+        if (threadIdx.x == 0) {
+            ok = 0;
+            const double* p1 = d.Pm + (((size_t)prob * 6) + a * 2 + 0) * R * R;
+            const double* p2 = d.Pm + (((size_t)prob * 6) + a * 2 + 1) * R * R;
+            for (int i = 0; i < R * R; ++i) m_h[i] = p2[i];
+            if (lu_fullpiv_inverse(R, m_h, R, m_inv, R, rowp, colp)) {
+                for (int j = 0; j < R; ++j)
+                    for (int i = 0; i < R; ++i) {
+                        double s = 0.0;
+                        for (int k = 0; k < R; ++k) s += p1[i + R * k] * m_inv[k + R * j];
+                        m_pen[i + R * j] = s;
+                    }
+                if (eig_real(R, m_pen, m_v, wr, wi, ort)) {
+                    int c = 0;
+                    while (c < R) {
+                        if (fabs(wi[c]) > 1e-9 * fabs(wr[c]) && c + 1 < R) {
+                            for (int i = 0; i < R; ++i) {
+                                asub[i + R * c] = m_v[i + R * c];
+                                asub[i + R * (c + 1)] = m_v[i + R * (c + 1)];
+                            }
+                            c += 2;
+                        } else {
+                            // real part of eigenvector c; for the second member of a
+                            // conjugate pair (wi < 0) that is column c-1 of the hqr2 layout
+                            const int src = (wi[c] < 0.0 && c > 0) ? c - 1 : c;
+                            for (int i = 0; i < R; ++i) asub[i + R * c] = m_v[i + R * src];
+                            c += 1;
+                        }
+                    }
+                    ok = 1;
+                }
+            }
+        }
+        __syncthreads();
+        if (!ok) continue;
+        // a1 = U_r a_sub, column norms
+        for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
+            const int i = e % Q, c = e / Q;
+            double s = 0.0;
+            for (int k = 0; k < R; ++k) s += ur[i + (size_t)Q * k] * asub[k + R * c];
+            a1[i + (size_t)Q * c] = s;
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < R; c += blockDim.x) {
+            double s = 0.0;
+            for (int i = 0; i < Q; ++i) s += dsq(a1[i + (size_t)Q * c]);
+            nrm[c] = sqrt(s);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int c = 0; c < R; ++c)
+                if (nrm[c] < kDegenerateNorm) ok = 0;
+        }
+        __syncthreads();
+        if (!ok) continue;
+        for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
+            const int c = e / Q;
+            a1[e] /= nrm[c];
+        }
+        if (threadIdx.x == 0) att = a;
+        __syncthreads();
+        break;
+    }
+    if (threadIdx.x == 0) d.att_used[prob] = att;
+}
+
+// h = (a1^T a1)^-1 (a1^T Y_(0)) in place on Hh (R x Q^2), per problem.
+__global__ void gevd_hsolve_kernel(AlsDev d) {
+    const int prob = blockIdx.x;
+    if (!d.todo[prob] || d.att_used[prob] < 0) return;
+    const int Q = d.Q, R = d.R;
+    extern __shared__ double sm[];
+    double* Lf = sm;           // R*R
+    double* Vp = Lf + R * R;   // R*R (pinv fallback)
+    double* cs = Vp + R * R;   // 2(R+2)
+    int* flag = (int*)(cs + 2 * (R + 2));
+    __shared__ int rank;
+    const double* a1 = d.f(prob, 0);
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+        const int i = e % R, j = e / R;
+        double s = 0.0;
+        for (int q = 0; q < Q; ++q) s += a1[q + (size_t)Q * i] * a1[q + (size_t)Q * j];
+        Lf[e] = s;
+        Vp[e] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) rank = chol_semidef(R, Lf, R, kEps * R);
+    __syncthreads();
+    double* h = d.Hh + (size_t)prob * R * d.q2();
+    if (rank == R) {
+        for (size_t k = threadIdx.x; k < d.q2(); k += blockDim.x) chol_solve_vec(R, Lf, R, h + (size_t)R * k, 1);
+    } else {
+        // minimum-norm fallback: pseudo-inverse from the eigen-decomposition
+        double* Ev = d.gscr + (size_t)prob * (6 * R * R + 4 * R);
+        TeamDev team;
+        jacobi_eig_sym(team, R, Vp, Ev, cs, flag);
+        __syncthreads();
+        double wmax = 0.0;
+        for (int i = 0; i < R; ++i) wmax = fmax(wmax, fabs(Vp[i + R * i]));
+        const double thr = kEps * R * wmax;
+        for (size_t k = threadIdx.x; k < d.q2(); k += blockDim.x) {
+            double x[64], y[64];
+            for (int i = 0; i < R; ++i) x[i] = h[(size_t)R * k + i];
+            for (int i = 0; i < R; ++i) y[i] = 0.0;
+            for (int e = 0; e < R; ++e) {
+                const double w = Vp[e + R * e];
+                if (!(w > thr)) continue;
+                double dot = 0.0;
+                for (int i = 0; i < R; ++i) dot += Ev[i + R * e] * x[i];
+                dot /= w;
+                for (int i = 0; i < R; ++i) y[i] += Ev[i + R * e] * dot;
+            }
+            for (int i = 0; i < R; ++i) h[(size_t)R * k + i] = y[i];
+        }
+    }
+}
+
+// Rank-1 peel of every h row (cp_als.cpp:168-173): H_r(b,c) = h(r, b + Q c).
+__global__ void gevd_peel_kernel(AlsDev d) {
+    const int prob = blockIdx.x / d.R, r = blockIdx.x % d.R;
+    if (!d.todo[prob] || d.att_used[prob] < 0) return;
+    const int Q = d.Q, R = d.R;
+    extern __shared__ double sm[];
+    double* H = sm;                     // Q*Q
+    double* u = H + (size_t)Q * Q;      // Q
+    double* v = u + Q;                  // Q
+    double* red = v + Q;                // blockDim + 2 + Q
+    const double* h = d.Hh + (size_t)prob * R * d.q2();
+    for (int e = threadIdx.x; e < Q * Q; e += blockDim.x) H[e] = h[r + (size_t)R * e];
+    __syncthreads();
+    TeamDev team;
+    const double sigma = top_singular_pair(team, Q, Q, H, u, v, red);
+    double* fb = d.f(prob, 1);
+    double* fc = d.f(prob, 2);
+    int bad = 0;
+    for (int i = threadIdx.x; i < Q; i += blockDim.x) {
+        fb[i + (size_t)Q * r] = u[i];
+        const double cv = sigma * v[i];
+        fc[i + (size_t)Q * r] = cv;
+        if (!isfinite(u[i]) || !isfinite(cv)) bad = 1;
+    }
+    if (bad) atomicOr(&d.peel_fail[prob], 1);
+}
+
+// Grams of the initial factors, lambda = 1, fresh sweep state.
+__global__ void als_init_state_kernel(AlsDev d) {
+    const int prob = blockIdx.x;
+    const int Q = d.Q, R = d.R;
+    for (int n = 0; n < 3; ++n) {
+        const double* f = d.f(prob, n);
+        double* g = d.g(prob, n);
+        for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+            const int i = e % R, j = e / R;
+            double s = 0.0;
+            for (int q = 0; q < Q; ++q) s += f[q + (size_t)Q * i] * f[q + (size_t)Q * j];
+            g[e] = s;
+        }
+    }
+    for (int c = threadIdx.x; c < R; c += blockDim.x) d.lam[(size_t)prob * R + c] = 1.0;
+    if (threadIdx.x == 0) {
+        AlsState s;
+        s.prev_fit = 0.0;
+        s.active = 1;
+        s.iterations = 0;
+        s.rescued = 0;
+        s.rng_init = 0;
+        s.failed = 0;
+        s.pad = 0;
+        d.state[prob] = s;
+        d.err[prob].code = kOk;
+    }
+}
+
+// ---------------- sweeps ----------------
+
+// MTTKRP of mode 0 (a,r) = sum_b T(a,b,r) B(b,r) and of mode 1
+// (b,r) = sum_a T(a,b,r) A(a,r), from T = Y x3 C.
+__global__ void als_mttkrp_T_kernel(AlsDev d, int mode) {
+    const int prob = blockIdx.x;
+    if (!d.state[prob].active) return;
+    const int p = prob / d.S, s = prob % d.S;
+    const int Q = d.Q, R = d.R;
+    const double* T = d.T + (size_t)p * d.q2() * d.S * R;
+    double* M = d.Mb + (size_t)prob * Q * R;
+    if (mode == 0) {
+        const double* B = d.f(prob, 1);
+        for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
+            const int a = e % Q, r = e / Q;
+            const double* tcol = T + (size_t)d.q2() * (s * R + r);
+            double acc = 0.0;
+            for (int b = 0; b < Q; ++b) acc += tcol[a + (size_t)Q * b] * B[b + (size_t)Q * r];
+            M[a + (size_t)Q * r] = acc;
+        }
+    } else {
+        const double* A = d.f(prob, 0);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int e = warp; e < Q * R; e += nw) {
+            const int b = e % Q, r = e / Q;
+            const double* tcol = T + (size_t)d.q2() * (s * R + r) + (size_t)Q * b;
+            double acc = 0.0;
+            for (int a = lane; a < Q; a += 32) acc += tcol[a] * A[a + (size_t)Q * r];
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) M[b + (size_t)Q * r] = acc;
+        }
+    }
+}
+
+// KR[p][(a + Q b), s R + r] = A(a,r) B(b,r)
+__global__ void als_kr_kernel(AlsDev d) {
+    const int prob = blockIdx.y;
+    const int p = prob / d.S, s = prob % d.S;
+    const int Q = d.Q, R = d.R;
+    const double* A = d.f(prob, 0);
+    const double* B = d.f(prob, 1);
+    double* K = d.KR + (size_t)p * d.q2() * d.S * R;
+    const size_t total = (size_t)d.q2() * R;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const int r = (int)(e / d.q2());
+        const int m = (int)(e % d.q2());
+        const int a = m % Q, b = m / Q;
+        K[m + d.q2() * (size_t)(s * R + r)] = A[a + (size_t)Q * r] * B[b + (size_t)Q * r];
+    }
+}
+
+// One mode update per problem: raw = M V^-1 (COD of the Hadamard Gram),
+// non-finite check, normalize into lambda with seeded rescue, new Gram;
+// after mode 2 the fit and the convergence test.
+__global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
+    const int prob = blockIdx.x;
+    AlsState* st = d.state + prob;
+    if (!st->active) return;
+    const int Q = d.Q, R = d.R;
+    extern __shared__ double sm[];
+    double* V = sm;                 // R*R
+    double* Lf = V + R * R;         // R*R
+    double* Ev = Lf + R * R;        // R*R
+    double* raw = Ev + R * R;       // Q*R
+    double* nrm = raw + Q * R;      // R
+    double* cs = nrm + R;           // 2(R+2)
+    double* red = cs + 2 * (R + 2); // blockDim
+    int* flag = (int*)(red + blockDim.x);
+    __shared__ int rank, bad;
+    const double* M = d.Mb + (size_t)prob * Q * R;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+        double v = 1.0;
+        for (int k = 0; k < 3; ++k)
+            if (k != mode) v *= d.g(prob, k)[e];
+        V[e] = v;
+        Lf[e] = v;
+    }
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) rank = chol_semidef(R, Lf, R, kEps * R);
+    __syncthreads();
+    if (rank == R) {
+        for (int q = threadIdx.x; q < Q; q += blockDim.x) {
+            double x[64];
+            for (int c = 0; c < R; ++c) x[c] = M[q + (size_t)Q * c];
+            chol_solve_vec(R, Lf, R, x, 1);
+            for (int c = 0; c < R; ++c) raw[q + Q * c] = x[c];
+        }
+    } else {
+        TeamDev team;
+        jacobi_eig_sym(team, R, V, Ev, cs, flag);
+        __syncthreads();
+        double wmax = 0.0;
+        for (int i = 0; i < R; ++i) wmax = fmax(wmax, fabs(V[i + R * i]));
+        const double thr = kEps * R * wmax;
+        for (int q = threadIdx.x; q < Q; q += blockDim.x) {
+            double x[64], y[64];
+            for (int c = 0; c < R; ++c) {
+                x[c] = M[q + (size_t)Q * c];
+                y[c] = 0.0;
+            }
+            for (int e = 0; e < R; ++e) {
+                const double w = V[e + R * e];
+                if (!(w > thr)) continue;
+                double dot = 0.0;
+                for (int i = 0; i < R; ++i) dot += Ev[i + R * e] * x[i];
+                dot /= w;
+                for (int i = 0; i < R; ++i) y[i] += Ev[i + R * e] * dot;
+            }
+            for (int c = 0; c < R; ++c) raw[q + Q * c] = y[c];
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < Q * R; e += blockDim.x)
+        if (!isfinite(raw[e])) bad = 1;
+    __syncthreads();
+    if (bad) {
+        if (threadIdx.x == 0) {
+            d.err[prob].code = kAlsNonFiniteFactor;
+            d.err[prob].problem = prob;
+            d.err[prob].a = sweep + 1;
+            d.err[prob].b = mode + 1;
+            st->active = 0;
+            st->failed = 1;
+        }
+        return;
+    }
+    for (int c = threadIdx.x; c < R; c += blockDim.x) {
+        double s = 0.0;
+        for (int q = 0; q < Q; ++q) s += raw[q + Q * c] * raw[q + Q * c];
+        nrm[c] = sqrt(s);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < R; ++c) {
+            if (nrm[c] < kDegenerateNorm) {
+                Mt64* g = d.rngs + prob;
+                if (!st->rng_init) {
+                    g->seed(d.rescue_seed[prob]);
+                    st->rng_init = 1;
+                }
+                double s = 0.0;
+                for (int q = 0; q < Q; ++q) {
+                    raw[q + Q * c] = g->uniform01();
+                    s += raw[q + Q * c] * raw[q + Q * c];
+                }
+                nrm[c] = sqrt(s);
+                st->rescued = 1;
+            }
+            d.lam[(size_t)prob * R + c] = nrm[c];
+        }
+    }
+    __syncthreads();
+    double* f = d.f(prob, mode);
+    for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
+        const double v = raw[e] / nrm[e / Q];
+        raw[e] = v;
+        f[e] = v;
+    }
+    __syncthreads();
+    double* g = d.g(prob, mode);
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+        const int i = e % R, j = e / R;
+        double s = 0.0;
+        for (int q = 0; q < Q; ++q) s += raw[q + Q * i] * raw[q + Q * j];
+        g[e] = s;
+    }
+    __syncthreads();
+    if (mode != 2) return;
+    // fit (cp_als.cpp:325-345)
+    const double* lam = d.lam + (size_t)prob * R;
+    double part = 0.0;
+    for (int e = threadIdx.x; e < Q * R; e += blockDim.x) part += M[e] * raw[e] * lam[e / Q];
+    const double inner = block_sum(part, red);
+    double part2 = 0.0;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+        const int i = e % R, j = e / R;
+        part2 += lam[i] * (d.g(prob, 0)[e] * d.g(prob, 1)[e] * d.g(prob, 2)[e]) * lam[j];
+    }
+    const double norm_m_sq = block_sum(part2, red);
+    if (threadIdx.x == 0) {
+        const int p = prob / d.S;
+        const double nx2 = d.normx2[p];
+        const double norm_x = sqrt(nx2);
+        const double res_sq = fmax(0.0, nx2 - 2.0 * inner + norm_m_sq);
+        const double residual = sqrt(res_sq);
+        const double fit = 1.0 - residual / norm_x;
+        if (!isfinite(fit)) {
+            d.err[prob].code = kAlsNonFiniteFit;
+            d.err[prob].problem = prob;
+            d.err[prob].a = sweep + 1;
+            st->active = 0;
+            st->failed = 1;
+            return;
+        }
+        d.fit_hist[(size_t)prob * d.max_iters + sweep] = fit;
+        d.res_hist[(size_t)prob * d.max_iters + sweep] = residual;
+        bool stop = false;
+        if (sweep > 0 && fabs(fit - st->prev_fit) < d.rel_tol) stop = true;
+        st->prev_fit = fit;
+        if (stop || sweep + 1 >= d.max_iters) {
+            st->iterations = sweep + 1;
+            st->active = 0;
+        } else {
+            atomicAdd(d.active_count, 1);
+        }
+    }
+}
+
+// Best restart per replica (strictly greater final fit wins; cp_als.cpp:347-356).
+__global__ void als_select_kernel(AlsDev d, double* Mf, double* Mlam, int* best_out) {
+    const int p = blockIdx.x;
+    __shared__ int best;
+    if (threadIdx.x == 0) {
+        double bf = -INFINITY;
+        best = 0;
+        for (int s = 0; s < d.S; ++s) {
+            const int prob = p * d.S + s;
+            const AlsState& st = d.state[prob];
+            const double ff = st.iterations > 0 ? d.fit_hist[(size_t)prob * d.max_iters + st.iterations - 1] : -INFINITY;
+            if (ff > bf) {
+                bf = ff;
+                best = s;
+            }
+        }
+        best_out[p] = best;
+    }
+    __syncthreads();
+    const int prob = p * d.S + best;
+    const size_t fsz = (size_t)3 * d.Q * d.R;
+    for (size_t e = threadIdx.x; e < fsz; e += blockDim.x) Mf[(size_t)p * fsz + e] = d.F[(size_t)prob * fsz + e];
+    for (int c = threadIdx.x; c < d.R; c += blockDim.x) Mlam[(size_t)p * d.R + c] = d.lam[(size_t)prob * d.R + c];
+}
+
+// ---- GEMM functors ----
+struct YmatA {  // A(p, m, k) = Y[p][m + Q^2 k]   (Y as Q^2 x Q)
+    const double* Y;
+    size_t q3, q2;
+    int S;
+    bool per_problem;
+    __device__ double operator()(int b, int m, int k) const {
+        const int p = per_problem ? b / S : b;
+        return Y[(size_t)p * q3 + m + q2 * k];
+    }
+};
+struct FacB {  // B(p, k, n) = F[(p S + n / R)][mode][k + Q (n % R)]
+    const double* F;
+    int S, Q, R, mode;
+    __device__ double operator()(int p, int k, int n) const {
+        const int prob = p * S + n / R;
+        return F[((size_t)prob * 3 + mode) * Q * R + k + (size_t)Q * (n % R)];
+    }
+};
+struct TStore {  // T[p][m + Q^2 n]
+    double* T;
+    size_t q2;
+    int SR;
+    __device__ void operator()(int p, int m, int n, double v) const { T[(size_t)p * q2 * SR + m + q2 * n] = v; }
+};
+struct YtA {  // A(p, c, k) = Y[p][k + Q^2 c]   (Y_(2)^T rows)
+    const double* Y;
+    size_t q3, q2;
+    __device__ double operator()(int p, int c, int k) const { return Y[(size_t)p * q3 + k + q2 * c]; }
+};
+struct KRB {  // B(p, k, n) = KR[p][k + Q^2 n]
+    const double* K;
+    size_t q2;
+    int SR;
+    __device__ double operator()(int p, int k, int n) const { return K[(size_t)p * q2 * SR + k + q2 * n]; }
+};
+struct M2Store {  // -> Mb[p S + n/R][c + Q (n%R)]
+    double* M;
+    int S, Q, R;
+    __device__ void operator()(int p, int c, int n, double v) const {
+        const int prob = p * S + n / R;
+        M[(size_t)prob * Q * R + c + (size_t)Q * (n % R)] = v;
+    }
+};
+// GEVD Grams
+struct Y0A {  // A(p, a, k) = Y[p][a + Q k]   (Y_(0): Q x Q^2)
+    const double* Y;
+    size_t q3;
+    int Q;
+    __device__ double operator()(int p, int a, int k) const { return Y[(size_t)p * q3 + a + (size_t)Q * k]; }
+};
+struct Y0B {  // B(p, k, a') = Y[p][a' + Q k]
+    const double* Y;
+    size_t q3;
+    int Q;
+    __device__ double operator()(int p, int k, int a) const { return Y[(size_t)p * q3 + a + (size_t)Q * k]; }
+};
+struct Y1A {  // A(p, b, k), k = a + Q c -> Y[a + Q b + Q^2 c]   (Y_(1))
+    const double* Y;
+    size_t q3;
+    int Q;
+    __device__ double operator()(int p, int b, int k) const {
+        const int a = k % Q, c = k / Q;
+        return Y[(size_t)p * q3 + a + (size_t)Q * b + (size_t)Q * Q * c];
+    }
+};
+struct Y1B {
+    const double* Y;
+    size_t q3;
+    int Q;
+    __device__ double operator()(int p, int k, int b) const {
+        const int a = k % Q, c = k / Q;
+        return Y[(size_t)p * q3 + a + (size_t)Q * b + (size_t)Q * Q * c];
+    }
+};
+struct GevStore {
+    double* G;
+    int Q, which;
+    __device__ void operator()(int p, int i, int j, double v) const {
+        G[((size_t)p * 2 + which) * Q * Q + i + (size_t)Q * j] = v;
+    }
+};
+// mixtures
+struct MixB {  // B(prob, c, j) = Wmix[prob][j][c]
+    const double* W;
+    int Q;
+    __device__ double operator()(int prob, int c, int j) const { return W[((size_t)prob * 6 + j) * Q + c]; }
+};
+struct MixStore {
+    double* S;
+    size_t q2;
+    __device__ void operator()(int prob, int m, int j, double v) const { S[((size_t)prob * 6 + j) * q2 + m] = v; }
+};
+struct SmA {  // A(bj, a, b) = Smix[bj][a + Q b]
+    const double* S;
+    int Q;
+    __device__ double operator()(int bj, int a, int b) const { return S[(size_t)bj * Q * Q + a + (size_t)Q * b]; }
+};
+struct UrB {  // B(bj, b, r) = Ur[p][which][b + Q r], p = (bj/6)/S
+    const double* Ur;
+    int Q, R, S, which;
+    __device__ double operator()(int bj, int b, int r) const {
+        const int p = (bj / 6) / S;
+        return Ur[((size_t)p * 2 + which) * Q * R + b + (size_t)Q * r];
+    }
+};
+struct Tmp6Store {
+    double* T;
+    int Q, R;
+    __device__ void operator()(int bj, int a, int r, double v) const { T[(size_t)bj * Q * R + a + (size_t)Q * r] = v; }
+};
+struct UrTA {  // A(bj, i, a) = Ur[p][0][a + Q i]
+    const double* Ur;
+    int Q, R, S;
+    __device__ double operator()(int bj, int i, int a) const {
+        const int p = (bj / 6) / S;
+        return Ur[((size_t)p * 2) * Q * R + a + (size_t)Q * i];
+    }
+};
+struct Tmp6B {
+    const double* T;
+    int Q, R;
+    __device__ double operator()(int bj, int a, int r) const { return T[(size_t)bj * Q * R + a + (size_t)Q * r]; }
+};
+struct PmStore {
+    double* Pm;
+    int R;
+    __device__ void operator()(int bj, int i, int r, double v) const { Pm[(size_t)bj * R * R + i + (size_t)R * r] = v; }
+};
+// h = a1^T Y_(0)
+struct A1tA {  // A(prob, r, a) = F[prob][0][a + Q r]
+    const double* F;
+    int Q, R;
+    __device__ double operator()(int prob, int r, int a) const { return F[((size_t)prob * 3) * Q * R + a + (size_t)Q * r]; }
+};
+struct Y0Bp {  // B(prob, a, k) = Y[p][a + Q k]
+    const double* Y;
+    size_t q3;
+    int Q, S;
+    __device__ double operator()(int prob, int a, int k) const {
+        return Y[(size_t)(prob / S) * q3 + a + (size_t)Q * k];
+    }
+};
+struct HStore {
+    double* H;
+    int R;
+    size_t q2;
+    __device__ void operator()(int prob, int r, int k, double v) const { H[(size_t)prob * R * q2 + r + (size_t)R * k] = v; }
+};
+
+}  // namespace
+
+void AlsEngine::alloc(int P, int S, int Q, int R, int max_iters) {
+    const size_t NP = (size_t)P * S, q2 = (size_t)Q * Q;
+    P_ = P;
+    S_ = S;
+    Q_ = Q;
+    R_ = R;
+    I_ = max_iters;
+    normx2.reserve(P);
+    F.reserve(NP * 3 * Q * R);
+    G.reserve(NP * 3 * R * R);
+    lam.reserve(NP * R);
+    T.reserve((size_t)P * q2 * S * R);
+    KR.reserve((size_t)P * q2 * S * R);
+    Mb.reserve(NP * Q * R);
+    fit_hist.reserve(NP * max_iters);
+    res_hist.reserve(NP * max_iters);
+    state.reserve(NP);
+    err.reserve(NP);
+    rngs.reserve(NP);
+    rescue_seed.reserve(NP);
+    active_count.reserve(1);
+    Gev.reserve((size_t)P * 2 * q2);
+    EV.reserve((size_t)P * 2 * q2);
+    Ur.reserve((size_t)P * 2 * Q * R);
+    Wmix.reserve(NP * 6 * Q);
+    Smix.reserve(NP * 6 * q2);
+    Tmp6.reserve(NP * 6 * Q * R);
+    Pm.reserve(NP * 6 * R * R);
+    Hh.reserve(NP * R * q2);
+    gscr.reserve(NP * (6 * R * R + 4 * R));
+    usable.reserve(P);
+    att_start.reserve(NP);
+    att_used.reserve(NP);
+    todo.reserve(NP);
+    peel_fail.reserve(NP);
+    Mf.reserve((size_t)P * 3 * Q * R);
+    Mlam.reserve((size_t)P * R);
+}
+
+void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, const double* dY,
+                    const std::vector<std::uint64_t>& seeds, cudaStream_t st) {
+    if (R < 1) throw ConfigError("cp_als: rank must be >= 1");
+    if (max_iters < 1) throw ConfigError("cp_als: max_iters must be >= 1");
+    if (!(rel_tol > 0.0)) throw ConfigError("cp_als: rel_tol must be > 0");
+    if (S < 1) throw ConfigError("cp_als: n_restarts must be >= 1");
+    if ((long long)R > (long long)Q * Q)
+        throw ConfigError("cp_als: rank " + std::to_string(R) + " exceeds solvability bound for mode 1");
+    if (R > 64) throw ConfigError("octen: device CP-ALS supports rank <= 64");
+    if (Q > 256) throw ConfigError("octen: device CP-ALS supports Q <= 256");
+    alloc(P, S, Q, R, max_iters);
+    const int NP = P * S;
+    const size_t q2 = (size_t)Q * Q, q3 = q2 * Q;
+
+    AlsDev d;
+    d.P = P;
+    d.S = S;
+    d.Q = Q;
+    d.R = R;
+    d.NP = NP;
+    d.max_iters = max_iters;
+    d.rel_tol = rel_tol;
+    d.Y = dY;
+    d.normx2 = normx2.p;
+    d.F = F.p;
+    d.G = G.p;
+    d.lam = lam.p;
+    d.T = T.p;
+    d.KR = KR.p;
+    d.Mb = Mb.p;
+    d.fit_hist = fit_hist.p;
+    d.res_hist = res_hist.p;
+    d.state = state.p;
+    d.err = err.p;
+    d.rngs = rngs.p;
+    d.rescue_seed = rescue_seed.p;
+    d.active_count = active_count.p;
+    d.Gev = Gev.p;
+    d.EV = EV.p;
+    d.Ur = Ur.p;
+    d.Wmix = Wmix.p;
+    d.Smix = Smix.p;
+    d.Tmp6 = Tmp6.p;
+    d.Pm = Pm.p;
+    d.Hh = Hh.p;
+    d.gscr = gscr.p;
+    d.usable = usable.p;
+    d.att_start = att_start.p;
+    d.att_used = att_used.p;
+    d.todo = todo.p;
+    d.peel_fail = peel_fail.p;
+    host_syncs = 0;
+
+    // ---- norms, zero-tensor check (cp_als.cpp:255-256)
+    als_norm_kernel<<<P, 256, 0, st>>>(d);
+    OCTEN_CUDA(cudaGetLastError());
+    std::vector<double> hn = normx2.to_host(P, st);
+    ++host_syncs;
+    for (int p = 0; p < P; ++p)
+        if (hn[p] == 0.0) throw NumericError("cp_als: input tensor is identically zero");
+
+    // ---- host RNG: restart seeds, GEVD mixtures, rescue seeds
+    std::vector<std::uint64_t> restart_seed(NP), hres(NP);
+    std::vector<double> hw((size_t)NP * 6 * Q);
+    for (int p = 0; p < P; ++p)
+        for (int s = 0; s < S; ++s) {
+            const int prob = p * S + s;
+            restart_seed[prob] = rng::derive(seeds[p], {rng::kAlsRestart, (std::uint64_t)s});
+            hres[prob] = rng::derive(restart_seed[prob], {rng::kAlsRescue});
+            for (int a = 0; a < 3; ++a) {
+                rng::Substream ws(rng::derive(restart_seed[prob], {rng::kAlsGevd, (std::uint64_t)a}));
+                double* w1 = hw.data() + ((size_t)prob * 6 + a * 2 + 0) * Q;
+                double* w2 = hw.data() + ((size_t)prob * 6 + a * 2 + 1) * Q;
+                for (int i = 0; i < Q; ++i) w1[i] = ws.uniform01() * 2 - 1;
+                for (int i = 0; i < Q; ++i) w2[i] = ws.uniform01() * 2 - 1;
+            }
+        }
+    Wmix.upload(hw.data(), hw.size(), st);
+    rescue_seed.upload(hres.data(), NP, st);
+
+    // ---- GEVD init (usable when Q >= R and Q >= 2; cp_als.cpp:64)
+    std::vector<int> used(NP, -1);
+    const bool shape_ok = (Q >= R) && (Q >= 2);
+    if (shape_ok) {
+        std::vector<int> ones(P, 1);
+        usable.upload(ones.data(), P, st);
+        const int ks = pick_ksplit(P, Q, Q, (int)q2);
+        ws.reserve((size_t)P * ks * q2);
+        gemm_simt<double, double, false, false>(P, Q, Q, (int)q2, Y0A{dY, q3, Q}, Y0B{dY, q3, Q},
+                                                GevStore{Gev.p, Q, 0}, st, ks, ws.p);
+        gemm_simt<double, double, true, true>(P, Q, Q, (int)q2, Y1A{dY, q3, Q}, Y1B{dY, q3, Q}, GevStore{Gev.p, Q, 1},
+                                              st, ks, ws.p);
+        const size_t smem_eig = q2 * sizeof(double) + 2 * (Q + 2) * sizeof(double) + (4 + Q) * sizeof(int) + 64;
+        OCTEN_CUDA(cudaFuncSetAttribute(gevd_eig_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eig));
+        gevd_eig_sym_kernel<<<P * 2, 256, smem_eig, st>>>(d);
+        OCTEN_CUDA(cudaGetLastError());
+        // mixtures -> p1/p2 for all attempts
+        gemm_simt<double, double, false, true>(NP, (int)q2, 6, Q, YmatA{dY, q3, q2, S, true}, MixB{Wmix.p, Q},
+                                               MixStore{Smix.p, q2}, st);
+        gemm_simt<double, double, false, false>(NP * 6, Q, R, Q, SmA{Smix.p, Q}, UrB{Ur.p, Q, R, S, 1},
+                                                Tmp6Store{Tmp6.p, Q, R}, st);
+        gemm_simt<double, double, true, false>(NP * 6, R, R, Q, UrTA{Ur.p, Q, R, S}, Tmp6B{Tmp6.p, Q, R},
+                                               PmStore{Pm.p, R}, st);
+        std::vector<int> hus = usable.to_host(P, st);
+        ++host_syncs;
+        std::vector<int> start(NP, 0), td(NP, 0);
+        for (int prob = 0; prob < NP; ++prob) td[prob] = hus[prob / S] ? 1 : 0;
+        for (int round = 0; round < 3; ++round) {
+            bool any = false;
+            for (int prob = 0; prob < NP; ++prob) any |= td[prob] != 0;
+            if (!any) break;
+            att_start.upload(start.data(), NP, st);
+            todo.upload(td.data(), NP, st);
+            peel_fail.zero(NP, st);
+            const size_t smem_pen = (size_t)(R * R + R) * sizeof(double);
+            gevd_pencil_kernel<<<NP, 128, smem_pen, st>>>(d);
+            OCTEN_CUDA(cudaGetLastError());
+            gemm_simt<double, double, false, false>(NP, R, (int)q2, Q, A1tA{F.p, Q, R}, Y0Bp{dY, q3, Q, S},
+                                                    HStore{Hh.p, R, q2}, st);
+            const size_t smem_h = (size_t)(2 * R * R + 2 * (R + 2)) * sizeof(double) + 16;
+            gevd_hsolve_kernel<<<NP, 256, smem_h, st>>>(d);
+            OCTEN_CUDA(cudaGetLastError());
+            const int peel_threads = 128;
+            const size_t smem_peel = (q2 + 2 * Q + peel_threads + 2 + Q) * sizeof(double);
+            OCTEN_CUDA(cudaFuncSetAttribute(gevd_peel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_peel));
+            gevd_peel_kernel<<<NP * R, peel_threads, smem_peel, st>>>(d);
+            OCTEN_CUDA(cudaGetLastError());
+            std::vector<int> au = att_used.to_host(NP, st);
+            std::vector<int> pf = peel_fail.to_host(NP, st);
+            ++host_syncs;
+            for (int prob = 0; prob < NP; ++prob) {
+                if (!td[prob]) continue;
+                if (au[prob] < 0) {  // exhausted: random fallback
+                    td[prob] = 0;
+                    used[prob] = -1;
+                } else if (pf[prob]) {  // non-finite peel: next attempt
+                    start[prob] = au[prob] + 1;
+                    if (start[prob] >= 3) {
+                        td[prob] = 0;
+                        used[prob] = -1;
+                    }
+                } else {
+                    td[prob] = 0;
+                    used[prob] = au[prob];
+                }
+            }
+        }
+    }
+    // random fallback factors (cp_als.cpp:275-283)
+    {
+        std::vector<double> fac((size_t)3 * Q * R);
+        for (int prob = 0; prob < NP; ++prob) {
+            if (used[prob] >= 0) continue;
+            for (int n = 0; n < 3; ++n) {
+                rng::Substream rs(rng::derive(restart_seed[prob], {rng::kAlsFactor, (std::uint64_t)n}));
+                rs.fill_uniform(fac.data() + (size_t)n * Q * R, Q, R, Q);
+            }
+            OCTEN_CUDA(cudaMemcpyAsync(F.p + (size_t)prob * 3 * Q * R, fac.data(), fac.size() * sizeof(double),
+                                       cudaMemcpyHostToDevice, st));
+            OCTEN_CUDA(cudaStreamSynchronize(st));
+        }
+    }
+    als_init_state_kernel<<<NP, 128, 0, st>>>(d);
+    OCTEN_CUDA(cudaGetLastError());
+
+    // ---- sweeps
+    const int SR = S * R;
+    const int ks_m2 = pick_ksplit(P, Q, SR, (int)q2);
+    ws.reserve(std::max<size_t>(ws.n, (size_t)P * ks_m2 * Q * SR));
+    const int upd_threads = 128;
+    const size_t smem_upd = (size_t)(3 * R * R + Q * R + R + 2 * (R + 2) + upd_threads) * sizeof(double) + 16;
+    OCTEN_CUDA(cudaFuncSetAttribute(als_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_upd));
+    int* hcount = nullptr;
+    OCTEN_CUDA(cudaMallocHost(&hcount, sizeof(int)));
+    int sweep = 0;
+    for (; sweep < max_iters; ++sweep) {
+        active_count.zero(1, st);
+        // T = Y x3 C  (Q^2 x SR per replica)
+        gemm_simt<double, double, false, true>(P, (int)q2, SR, Q, YmatA{dY, q3, q2, S, false}, FacB{F.p, S, Q, R, 2},
+                                               TStore{T.p, q2, SR}, st);
+        als_mttkrp_T_kernel<<<NP, 256, 0, st>>>(d, 0);
+        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 0, sweep);
+        als_mttkrp_T_kernel<<<NP, 256, 0, st>>>(d, 1);
+        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 1, sweep);
+        {
+            dim3 g((unsigned)std::min<size_t>((q2 * R + 255) / 256, 1024), NP);
+            als_kr_kernel<<<g, 256, 0, st>>>(d);
+        }
+        gemm_simt<double, double, true, true>(P, Q, SR, (int)q2, YtA{dY, q3, q2}, KRB{KR.p, q2, SR},
+                                              M2Store{Mb.p, S, Q, R}, st, ks_m2, ws.p);
+        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 2, sweep);
+        OCTEN_CUDA(cudaGetLastError());
+        OCTEN_CUDA(cudaMemcpyAsync(hcount, active_count.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+        ++host_syncs;
+        if (*hcount == 0) {
+            ++sweep;
+            break;
+        }
+    }
+    last_sweeps = sweep;
+    cudaFreeHost(hcount);
+
+    // ---- errors (lowest replica, then restart, wins)
+    std::vector<DevStatus> he = err.to_host(NP, st);
+    std::vector<AlsState> hs = state.to_host(NP, st);
+    for (int prob = 0; prob < NP; ++prob) {
+        if (!hs[prob].failed) continue;
+        const DevStatus& e = he[prob];
+        if (e.code == kAlsNonFiniteFactor)
+            throw NumericError("cp_als: non-finite factor at sweep " + std::to_string(e.a) + ", mode " +
+                               std::to_string(e.b));
+        if (e.code == kAlsNonFiniteFit) throw NumericError("cp_als: non-finite fit at sweep " + std::to_string(e.a));
+    }
+    DevBuf<int> best;
+    best.reserve(P);
+    als_select_kernel<<<P, 256, 0, st>>>(d, Mf.p, Mlam.p, best.p);
+    OCTEN_CUDA(cudaGetLastError());
+    std::vector<int> hb = best.to_host(P, st);
+    std::vector<double> fh = fit_hist.to_host((size_t)NP * max_iters, st);
+    std::vector<double> rh = res_hist.to_host((size_t)NP * max_iters, st);
+    results.assign(P, AlsReplicaResult{});
+    for (int p = 0; p < P; ++p) {
+        const int prob = p * S + hb[p];
+        AlsReplicaResult& r = results[p];
+        r.restart = hb[p];
+        r.iterations = hs[prob].iterations;
+        r.rescued = hs[prob].rescued != 0;
+        r.gevd_attempt = used[prob];
+        r.fit_history.assign(fh.begin() + (size_t)prob * max_iters, fh.begin() + (size_t)prob * max_iters + r.iterations);
+        r.residual_history.assign(rh.begin() + (size_t)prob * max_iters,
+                                  rh.begin() + (size_t)prob * max_iters + r.iterations);
+        r.fit = r.fit_history.empty() ? -INFINITY : r.fit_history.back();
+    }
+}
+
+}  // namespace octen

@@ -1,0 +1,333 @@
+// C-ABI (include/octen_b200.h): exceptions -> status codes + thread-local
+// message carrying the reference's error text.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/octen_b200.h"
+#include "engine.hpp"
+#include "errors.hpp"
+#include "stream.hpp"
+
+struct octen_stream {
+    std::unique_ptr<octen::Stream> s;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    g_err.clear();
+    try {
+        f();
+        return OCTEN_OK;
+    } catch (const octen::ConfigError& e) {
+        g_err = e.what();
+        return OCTEN_ERR_CONFIG;
+    } catch (const octen::NumericError& e) {
+        g_err = e.what();
+        return OCTEN_ERR_NUMERIC;
+    } catch (const octen::IoError& e) {
+        g_err = e.what();
+        return OCTEN_ERR_IO;
+    } catch (const octen::CudaError& e) {
+        g_err = e.what();
+        return OCTEN_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return OCTEN_ERR_INTERNAL;
+    } catch (...) {
+        g_err = "unknown error";
+        return OCTEN_ERR_INTERNAL;
+    }
+}
+
+octen::StreamCfg to_cfg(const octen_stream_config* c) {
+    octen::StreamCfg s;
+    s.rank = c->rank;
+    s.p = c->p;
+    s.q = c->q;
+    s.shared = c->shared;
+    s.temporal_mode = c->temporal_mode;
+    s.als_max_iters = c->als.max_iters;
+    s.als_n_restarts = c->als.n_restarts;
+    s.als_rel_tol = c->als.rel_tol;
+    s.seed = c->seed;
+    s.enforce_bounds = c->enforce_bounds != 0;
+    s.strict = c->strict != 0;
+    s.workers = c->workers;
+    s.residual_warning = c->residual_warning;
+    s.device = c->device;
+    return s;
+}
+
+void check_dtype(int dtype, int location) {
+    if (dtype != OCTEN_F64 && dtype != OCTEN_F32) throw octen::ConfigError("octen: unknown dtype");
+    if (location != OCTEN_HOST && location != OCTEN_DEVICE) throw octen::ConfigError("octen: unknown location");
+}
+
+// history: stacked (pQ x R) <-> per replica (p x Q x R)
+void hist_to_blocks(const std::vector<double>& stk, int P, int Q, int R, double* out) {
+    const size_t PQ = (size_t)P * Q;
+    for (int p = 0; p < P; ++p)
+        for (int r = 0; r < R; ++r)
+            for (int a = 0; a < Q; ++a) out[(size_t)p * Q * R + a + (size_t)Q * r] = stk[(size_t)p * Q + a + PQ * r];
+}
+std::vector<double> blocks_to_hist(const double* in, int P, int Q, int R) {
+    const size_t PQ = (size_t)P * Q;
+    std::vector<double> stk(PQ * R);
+    for (int p = 0; p < P; ++p)
+        for (int r = 0; r < R; ++r)
+            for (int a = 0; a < Q; ++a) stk[(size_t)p * Q + a + PQ * r] = in[(size_t)p * Q * R + a + (size_t)Q * r];
+    return stk;
+}
+
+struct ScopedStream {
+    cudaStream_t st = nullptr;
+    ScopedStream() { OCTEN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); }
+    ~ScopedStream() {
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* octen_last_error(void) { return g_err.c_str(); }
+
+const char* octen_version(void) { return "octen_b200 0.1 (sm_100a)"; }
+
+int octen_stream_init(const octen_stream_config* cfg, const void* data, int dtype, int location, int order,
+                      const int64_t* dims, octen_stream** out) {
+    return guard([&] {
+        if (!cfg || !data || !dims || !out) throw octen::ConfigError("octen_stream_init: null argument");
+        check_dtype(dtype, location);
+        auto h = std::make_unique<octen_stream>();
+        h->s = std::make_unique<octen::Stream>(to_cfg(cfg));
+        h->s->init(data, dtype, location, order, dims);
+        *out = h.release();
+    });
+}
+
+int octen_stream_ingest(octen_stream* s, const void* data, int dtype, int location, int order,
+                        const int64_t* dims) {
+    return guard([&] {
+        if (!s || !data || !dims) throw octen::ConfigError("octen_stream_ingest: null argument");
+        check_dtype(dtype, location);
+        s->s->ingest(data, dtype, location, order, dims);
+    });
+}
+
+void octen_stream_destroy(octen_stream* s) { delete s; }
+
+int octen_stream_info(const octen_stream* s, int64_t* info) {
+    return guard([&] {
+        const auto& x = *s->s;
+        info[0] = 3;
+        info[1] = x.I;
+        info[2] = x.J;
+        info[3] = x.K;
+        info[4] = x.cfg.rank;
+        info[5] = x.cfg.p;
+        info[6] = x.cfg.q;
+        info[7] = x.batches_seen;
+    });
+}
+
+int octen_stream_get_factor(const octen_stream* s, int mode, double* out) {
+    return guard([&] { s->s->get_factor(mode, out); });
+}
+
+int octen_stream_get_lambda(const octen_stream* s, double* out) {
+    return guard([&] {
+        auto& x = *s->s;
+        x.lam.download(out, x.cfg.rank, x.st);
+        OCTEN_CUDA(cudaStreamSynchronize(x.st));
+    });
+}
+
+int octen_stream_get_record(const octen_stream* s, int64_t index, octen_batch_record* out) {
+    return guard([&] {
+        const auto& x = *s->s;
+        if (index < 0 || index >= (int64_t)x.log.size()) throw octen::ConfigError("octen_stream_get_record: index");
+        const auto& r = x.log[(size_t)index];
+        out->batch_index = r.batch_index;
+        out->t_new = r.t_new;
+        out->temporal_residual = r.temporal_residual;
+        out->min_match_similarity = r.min_match_similarity;
+        out->max_offdiag_similarity = r.max_offdiag_similarity;
+        out->warned = r.warned;
+        out->compress_seconds = r.compress_seconds;
+        out->als_seconds = r.als_seconds;
+        out->recover_seconds = r.recover_seconds;
+        out->total_seconds = r.total_seconds;
+    });
+}
+
+int octen_stream_get_summaries(const octen_stream* s, double* y) {
+    return guard([&] {
+        auto& x = *s->s;
+        const size_t n = (size_t)x.cfg.p * x.cfg.q * x.cfg.q * x.cfg.q;
+        x.Y.download(y, n, x.st);
+        OCTEN_CUDA(cudaStreamSynchronize(x.st));
+    });
+}
+
+int octen_stream_get_history(const octen_stream* s, double* h) {
+    return guard([&] {
+        auto& x = *s->s;
+        const int P = x.cfg.p, Q = x.cfg.q, R = x.cfg.rank;
+        std::vector<double> stk = x.hist.to_host((size_t)P * Q * R, x.st);
+        hist_to_blocks(stk, P, Q, R, h);
+    });
+}
+
+int octen_stream_get_replica_models(const octen_stream* s, double* factors, double* lambda) {
+    return guard([&] {
+        auto& x = *s->s;
+        const int P = x.cfg.p, Q = x.cfg.q, R = x.cfg.rank;
+        x.als.Mf.download(factors, (size_t)P * 3 * Q * R, x.st);
+        x.als.Mlam.download(lambda, (size_t)P * R, x.st);
+        OCTEN_CUDA(cudaStreamSynchronize(x.st));
+    });
+}
+
+int octen_compress(int p, int q, int shared, int64_t I, int64_t J, int64_t t, const double* u, const double* v,
+                   const double* w, const void* x, int dtype, double* z) {
+    return guard([&] {
+        check_dtype(dtype, OCTEN_HOST);
+        if (p < 1 || q < 1 || shared < 0 || shared > q || I < 1 || J < 1 || t < 1)
+            throw octen::ConfigError("octen_compress: bad shape");
+        ScopedStream ss;
+        octen::CompressEngine e;
+        e.set_projections(p, q, shared, I, J, u, v, ss.st);
+        octen::DevBuf<double> dW, dY;
+        dW.upload(w, (size_t)p * t * q, ss.st);
+        const size_t q3 = (size_t)q * q * q;
+        dY.reserve((size_t)p * q3);
+        dY.zero((size_t)p * q3, ss.st);
+        const size_t n = (size_t)I * J * t;
+        if (dtype == OCTEN_F32) {
+            octen::DevBuf<float> dX;
+            dX.upload((const float*)x, n, ss.st);
+            e.compress_f32(dX.p, t, dW.p, dY.p, ss.st);
+            dY.download(z, (size_t)p * q3, ss.st);
+            OCTEN_CUDA(cudaStreamSynchronize(ss.st));
+        } else {
+            octen::DevBuf<double> dX;
+            dX.upload((const double*)x, n, ss.st);
+            e.compress_f64(dX.p, t, dW.p, dY.p, ss.st);
+            dY.download(z, (size_t)p * q3, ss.st);
+            OCTEN_CUDA(cudaStreamSynchronize(ss.st));
+        }
+    });
+}
+
+int octen_cp_als_batched(int p, int q, const double* y, const octen_als_config* cfg, const uint64_t* seeds,
+                         double* factors, double* lambda, double* fit, int32_t* iterations) {
+    return guard([&] {
+        ScopedStream ss;
+        octen::DevBuf<double> dY;
+        dY.upload(y, (size_t)p * q * q * q, ss.st);
+        octen::AlsEngine als;
+        std::vector<std::uint64_t> sd(seeds, seeds + p);
+        als.run(p, cfg->n_restarts, q, cfg->rank, cfg->max_iters, cfg->rel_tol, dY.p, sd, ss.st);
+        als.Mf.download(factors, (size_t)p * 3 * q * cfg->rank, ss.st);
+        als.Mlam.download(lambda, (size_t)p * cfg->rank, ss.st);
+        OCTEN_CUDA(cudaStreamSynchronize(ss.st));
+        for (int r = 0; r < p; ++r) {
+            if (fit) fit[r] = als.results[r].fit;
+            if (iterations) iterations[r] = als.results[r].iterations;
+        }
+    });
+}
+
+int octen_align_replicas(int p, int q, int shared, int rank, int64_t I, int64_t J, const double* u,
+                         const double* v, const double* tgram, const double* factors, const double* lambda,
+                         double* stacks, int32_t* perms, double* scales, double* sims) {
+    return guard([&] {
+        ScopedStream ss;
+        octen::MergeEngine m;
+        m.set_projections(p, q, shared, rank, I, J, u, v, ss.st);
+        octen::DevBuf<double> dF, dL;
+        dF.upload(factors, (size_t)p * 3 * q * rank, ss.st);
+        dL.upload(lambda, (size_t)p * rank, ss.st);
+        std::vector<double> tg(tgram, tgram + (size_t)shared * shared);
+        octen::AlignResultHost ar;
+        m.align(dF.p, dL.p, tg, ss.st, &ar);
+        m.stacks.download(stacks, (size_t)3 * p * q * rank, ss.st);
+        OCTEN_CUDA(cudaStreamSynchronize(ss.st));
+        for (size_t i = 0; i < ar.perms.size(); ++i) perms[i] = ar.perms[i];
+        for (size_t i = 0; i < ar.scales.size(); ++i) scales[i] = ar.scales[i];
+        sims[0] = ar.min_match;
+        sims[1] = ar.max_offdiag;
+    });
+}
+
+int octen_recover_nontemporal(int p, int q, int64_t d, int rank, int mode, const double* proj_blocks,
+                              const double* stack, double* out) {
+    return guard([&] {
+        if (mode != 0 && mode != 1) throw octen::ConfigError("octen_recover_nontemporal: mode must be 0 or 1");
+        ScopedStream ss;
+        octen::MergeEngine m;
+        // the other mode is a 1-row placeholder projection
+        std::vector<double> other((size_t)p * q, 1.0);
+        if (mode == 0)
+            m.set_projections(p, q, 0, rank, d, 1, proj_blocks, other.data(), ss.st);
+        else
+            m.set_projections(p, q, 0, rank, 1, d, other.data(), proj_blocks, ss.st);
+        octen::DevBuf<double> dS, dO;
+        dS.upload(stack, (size_t)p * q * rank, ss.st);
+        dO.reserve((size_t)d * rank);
+        m.solve_nontemporal(mode, dS.p, dO.p, ss.st);
+        dO.download(out, (size_t)d * rank, ss.st);
+        OCTEN_CUDA(cudaStreamSynchronize(ss.st));
+    });
+}
+
+int octen_temporal_stack_from_summaries(int p, int q, int rank, int64_t I, int64_t J, const double* y,
+                                        const double* u, const double* v, const double* a, const double* b,
+                                        double* out) {
+    return guard([&] {
+        ScopedStream ss;
+        octen::MergeEngine m;
+        m.set_projections(p, q, 0, rank, I, J, u, v, ss.st);
+        octen::DevBuf<double> dY, dA, dB, dO;
+        dY.upload(y, (size_t)p * q * q * q, ss.st);
+        dA.upload(a, (size_t)I * rank, ss.st);
+        dB.upload(b, (size_t)J * rank, ss.st);
+        dO.reserve((size_t)p * q * rank);
+        m.temporal_stack(dY.p, dA.p, dB.p, dO.p, ss.st);
+        dO.download(out, (size_t)p * q * rank, ss.st);
+        OCTEN_CUDA(cudaStreamSynchronize(ss.st));
+    });
+}
+
+int octen_recover_temporal_append(int p, int q, int rank, int64_t t, const double* temporal_stack,
+                                  const double* w, double* history, double* new_rows, double* residual) {
+    return guard([&] {
+        ScopedStream ss;
+        octen::MergeEngine m;
+        m.P = p;
+        m.Q = q;
+        m.R = rank;
+        octen::DevBuf<double> dT, dW, dH, dR;
+        dT.upload(temporal_stack, (size_t)p * q * rank, ss.st);
+        dW.upload(w, (size_t)p * t * q, ss.st);
+        std::vector<double> stk = blocks_to_hist(history, p, q, rank);
+        dH.upload(stk.data(), stk.size(), ss.st);
+        dR.reserve((size_t)t * rank);
+        m.temporal_append(dT.p, dW.p, t, dH.p, dR.p, residual, ss.st);
+        dR.download(new_rows, (size_t)t * rank, ss.st);
+        std::vector<double> h2 = dH.to_host(stk.size(), ss.st);
+        hist_to_blocks(h2, p, q, rank, history);
+    });
+}
+
+}  // extern "C"

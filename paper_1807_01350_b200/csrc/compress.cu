@@ -1,0 +1,169 @@
+// Stage 1: multi-replica compression of one temporal batch into the summaries
+// (reference compress + update_summaries, proj/src/compression.cpp:108-153,
+// mode products of tensor.cpp:168-178).
+//
+//   GEMM1  Z1 = A X_(1)          A = deduplicated [U_1 ... U_P]^T (Meff x I):
+//                                the `shared` leading columns are identical in
+//                                every replica (compression.cpp:43-60), so they
+//                                are contracted once: Meff = shared + P (Q - shared)
+//   GEMM2  Z2_p(:,:,k) = Z1_p(:,:,k) V_p      per (replica, slice)
+//   GEMM3  Y_p += Z2_p (Q^2 x t) W_p          fp64 accumulate (update_summaries)
+//
+// The batch is processed in chunks of temporal slices so Z1 stays bounded.
+// fp32 input: GEMM1 runs on the tensor cores (tcgen05, split-TF32) when the
+// sm_100a kernel is available, else this SIMT path; fp64 input: SIMT fp64.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "engine.hpp"
+#include "gemm_simt.cuh"
+#include "tc_gemm.hpp"
+
+namespace octen {
+
+namespace {
+
+template <typename T>
+struct G1A {  // A(0, m, i) = A[m*I + i]   (row-major, K contiguous)
+    const T* A;
+    long long I;
+    __device__ T operator()(int, int m, int i) const { return A[(size_t)m * I + i]; }
+};
+template <typename T>
+struct G1B {  // B(0, i, n) = X[i + I n]
+    const T* X;
+    long long I;
+    __device__ T operator()(int, int i, int n) const { return X[(size_t)i + (size_t)I * n]; }
+};
+template <typename T>
+struct G1C {  // Z1[m*N + n]
+    T* Z;
+    long long N;
+    __device__ void operator()(int, int m, int n, T v) const { Z[(size_t)m * N + n] = v; }
+};
+template <typename T>
+struct G2A {  // batch bt = p*tc + k : A(bt, a, j) = Z1[row(p,a)*N1 + k*J + j]
+    const T* Z1;
+    const int* rowmap;
+    long long N1, J;
+    int tc, Q;
+    __device__ T operator()(int bt, int a, int j) const {
+        const int p = bt / tc, k = bt % tc;
+        return Z1[(size_t)rowmap[p * Q + a] * N1 + (size_t)k * J + j];
+    }
+};
+template <typename T>
+struct G2B {  // B(bt, j, b) = V[p][j + J b]
+    const T* V;
+    long long J;
+    int tc, Q;
+    __device__ T operator()(int bt, int j, int b) const {
+        const int p = bt / tc;
+        return V[(size_t)p * J * Q + j + (size_t)J * b];
+    }
+};
+template <typename T>
+struct G2C {  // Z2[p][(a + Q b) + Q^2 k]
+    T* Z2;
+    int tc, Q;
+    __device__ void operator()(int bt, int a, int b, T v) const {
+        const int p = bt / tc, k = bt % tc;
+        const size_t q2 = (size_t)Q * Q;
+        Z2[(size_t)p * q2 * tc + a + (size_t)Q * b + q2 * k] = v;
+    }
+};
+template <typename T>
+struct G3A {  // A(p, m, k) = Z2[p][m + Q^2 k]
+    const T* Z2;
+    int tc, Q;
+    __device__ double operator()(int p, int m, int k) const {
+        const size_t q2 = (size_t)Q * Q;
+        return (double)Z2[(size_t)p * q2 * tc + m + q2 * k];
+    }
+};
+struct G3B {  // B(p, k, c) = W[p][(k0 + k) + t c]
+    const double* W;
+    long long t, k0;
+    int Q;
+    __device__ double operator()(int p, int k, int c) const { return W[(size_t)p * t * Q + (k0 + k) + (size_t)t * c]; }
+};
+struct G3C {  // Y[p][m + Q^2 c] += v
+    double* Y;
+    int Q;
+    __device__ void operator()(int p, int m, int c, double v) const {
+        const size_t q2 = (size_t)Q * Q;
+        Y[(size_t)p * q2 * Q + m + q2 * c] += v;
+    }
+};
+
+template <typename T>
+void run_compress(CompressEngine& e, const T* dX, std::int64_t t, const double* dW, double* dY, T* Z1, T* Z2,
+                  const T* A, const T* V, std::int64_t tc_max, cudaStream_t st, bool use_tc) {
+    const int Q = e.Q, P = e.P;
+    for (std::int64_t k0 = 0; k0 < t; k0 += tc_max) {
+        const int tc = (int)std::min<std::int64_t>(tc_max, t - k0);
+        const long long N1 = e.J * tc;
+        const T* Xc = dX + (size_t)e.I * e.J * k0;
+        bool done = false;
+        if constexpr (std::is_same<T, float>::value) {
+            if (use_tc) done = tc_gemm_f32_nt(A, Xc, Z1, (int)e.Meff, (long long)N1, (int)e.I, st);
+        }
+        if (!done)
+            gemm_simt<T, T, true, true>(1, (int)e.Meff, (int)N1, (int)e.I, G1A<T>{A, e.I}, G1B<T>{Xc, e.I},
+                                        G1C<T>{Z1, N1}, st);
+        gemm_simt<T, T, true, false>(P * tc, Q, Q, (int)e.J, G2A<T>{Z1, e.rowmap.p, N1, e.J, tc, Q},
+                                     G2B<T>{V, e.J, tc, Q}, G2C<T>{Z2, tc, Q}, st);
+        gemm_simt<double, double, false, true>(P, Q * Q, Q, tc, G3A<T>{Z2, tc, Q}, G3B{dW, t, k0, Q}, G3C{dY, Q}, st);
+    }
+    OCTEN_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+void CompressEngine::set_projections(int P_, int Q_, int shared_, std::int64_t I_, std::int64_t J_, const double* hU,
+                                     const double* hV, cudaStream_t st) {
+    P = P_;
+    Q = Q_;
+    shared = shared_;
+    I = I_;
+    J = J_;
+    Meff = shared + (std::int64_t)P * (Q - shared);
+    std::vector<int> rm((size_t)P * Q);
+    std::vector<double> a64((size_t)Meff * I);
+    for (int p = 0; p < P; ++p)
+        for (int a = 0; a < Q; ++a) {
+            const std::int64_t row = a < shared ? a : shared + (std::int64_t)p * (Q - shared) + (a - shared);
+            rm[(size_t)p * Q + a] = (int)row;
+            if (a < shared && p > 0) continue;
+            const double* u = hU + (size_t)p * I * Q + (size_t)I * a;
+            for (std::int64_t i = 0; i < I; ++i) a64[(size_t)row * I + i] = u[i];
+        }
+    std::vector<float> a32(a64.begin(), a64.end());
+    std::vector<float> v32(hV, hV + (size_t)P * J * Q);
+    rowmap.upload(rm.data(), rm.size(), st);
+    A64.upload(a64.data(), a64.size(), st);
+    A32.upload(a32.data(), a32.size(), st);
+    V64.upload(hV, (size_t)P * J * Q, st);
+    V32.upload(v32.data(), v32.size(), st);
+    // Z1 chunk of about 1 GiB
+    chunk_slices = std::max<std::int64_t>(1, (std::int64_t)((1ULL << 28) / (unsigned long long)std::max<std::int64_t>(1, Meff * J)));
+    OCTEN_CUDA(cudaStreamSynchronize(st));
+}
+
+void CompressEngine::compress_f32(const float* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st) {
+    const std::int64_t tc = std::min(t, chunk_slices);
+    Z1f.reserve((size_t)Meff * J * tc);
+    Z2f.reserve((size_t)P * Q * Q * tc);
+    run_compress<float>(*this, dX, t, dW, dY, Z1f.p, Z2f.p, A32.p, V32.p, tc, st, true);
+}
+
+void CompressEngine::compress_f64(const double* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st) {
+    const std::int64_t tc = std::min(t, chunk_slices);
+    Z1d.reserve((size_t)Meff * J * tc);
+    Z2d.reserve((size_t)P * Q * Q * tc);
+    run_compress<double>(*this, dX, t, dW, dY, Z1d.p, Z2d.p, A64.p, V64.p, tc, st, false);
+}
+
+}  // namespace octen

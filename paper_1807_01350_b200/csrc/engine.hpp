@@ -1,0 +1,145 @@
+// Device engines for the three stages of the per-batch OCTen pipeline.
+// All matrices are column-major fp64 unless noted (Eigen's default, as in the
+// reference); tensors are first-index-fastest (tensor.hpp:32-34).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "devbuf.hpp"
+#include "errors.hpp"
+#include "octen_common.cuh"
+#include "small_linalg.cuh"
+
+namespace octen {
+
+// ---------------------------------------------------------------------------
+// Stage 2: batched CP-ALS over the P replica summaries (cp_als.cpp:240-359),
+// all n_restarts restarts of every replica run concurrently.
+// ---------------------------------------------------------------------------
+struct AlsReplicaResult {
+    double fit = 0.0;
+    int iterations = 0;
+    int restart = 0;
+    int gevd_attempt = -1;  // -1: random init
+    bool rescued = false;
+    std::vector<double> fit_history, residual_history;
+};
+
+struct AlsState {  // per (replica, restart) problem, device resident
+    double prev_fit;
+    int active;
+    int iterations;
+    int rescued;
+    int rng_init;
+    int failed;
+    int pad;
+};
+
+class AlsEngine {
+public:
+    // Y: P x Q^3 device summaries.  seeds: per replica AlsConfig.seed.
+    void run(int P, int S, int Q, int R, int max_iters, double rel_tol, const double* dY,
+             const std::vector<std::uint64_t>& seeds, cudaStream_t st);
+
+    // Results: factors P x 3 x Q x R, lambda P x R (device).
+    DevBuf<double> Mf, Mlam;
+    std::vector<AlsReplicaResult> results;
+    int last_sweeps = 0;
+    int host_syncs = 0;
+
+private:
+    void alloc(int P, int S, int Q, int R, int max_iters);
+    int P_ = 0, S_ = 0, Q_ = 0, R_ = 0, I_ = 0;
+    DevBuf<double> normx2, F, G, lam, T, KR, Mb, fit_hist, res_hist, ws;
+    DevBuf<double> Gev, EV, Ur, Wmix, Smix, Tmp6, Pm, Hh, gscr;
+    DevBuf<int> usable, att_start, att_used, todo, peel_fail, active_count;
+    DevBuf<AlsState> state;
+    DevBuf<DevStatus> err;
+    DevBuf<Mt64> rngs;
+    DevBuf<std::uint64_t> rescue_seed;
+};
+
+// ---------------------------------------------------------------------------
+// Stage 1: compression of one temporal batch into the P summaries,
+// Y_p += X x1 U_p^T x2 V_p^T x3 W_p^T (compression.cpp:108-153).
+// ---------------------------------------------------------------------------
+class CompressEngine {
+public:
+    // Projections (host, column-major per replica: U_p I x Q, V_p J x Q).
+    void set_projections(int P, int Q, int shared, std::int64_t I, std::int64_t J, const double* hU,
+                         const double* hV, cudaStream_t st);
+    // Accumulate the compression of batch X (I x J x t, first index fastest,
+    // device) with temporal rows W (P x t x Q col-major per replica, device)
+    // into Y (P x Q^3, device).  X is fp32 or fp64.
+    void compress_f32(const float* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st);
+    void compress_f64(const double* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st);
+
+    int P = 0, Q = 0, shared = 0;
+    std::int64_t I = 0, J = 0, Meff = 0;
+    DevBuf<float> A32;   // Meff x I row-major (deduplicated shared columns)
+    DevBuf<double> A64;  // Meff x I row-major
+    DevBuf<float> V32;   // P x J x Q
+    DevBuf<double> V64;  // P x J x Q
+    DevBuf<int> rowmap;  // P x Q -> row of A
+    DevBuf<float> Z1f, Z2f;
+    DevBuf<double> Z1d, Z2d;
+    std::int64_t chunk_slices = 0;
+};
+
+// ---------------------------------------------------------------------------
+// Stage 3: alignment and merge (recovery.cpp / streaming.cpp:89-177).
+// ---------------------------------------------------------------------------
+struct AlignResultHost {
+    std::vector<int> perms;       // P x R
+    std::vector<double> scales;   // P x 3 x R
+    double min_match = 1.0, max_offdiag = 0.0;
+    int ambiguous = 0;
+};
+
+class MergeEngine {
+public:
+    // Fixed-for-the-stream projections (host col-major, per replica).
+    void set_projections(int P, int Q, int shared, int R, std::int64_t I, std::int64_t J, const double* hU,
+                         const double* hV, cudaStream_t st);
+
+    // Align replica models (device: factors P x 3 x Q x R, lambda P x R).
+    // tgram: shared x shared temporal_shared_gram (host).
+    void align(const double* dMf, const double* dMlam, const std::vector<double>& tgram, cudaStream_t st,
+               AlignResultHost* out);
+    // Full recover_batch: solves, refinement, gauge match, temporal append.
+    // Y: P x Q^3; dW: P x t x Q; hist: PQ x R stacked (updated);
+    // stored (device) nontemporal factors or null on the first batch.
+    // Outputs A_fin (I x R), B_fin (J x R), new_rows (t x R), residual.
+    void recover(const double* dY, const double* dW, std::int64_t t, double* dHist, const double* dStoredA,
+                 const double* dStoredB, double* dAfin, double* dBfin, double* dRows, double* residual,
+                 cudaStream_t st);
+
+    // Stage-level helpers (also exposed through the C-ABI for parity tests).
+    void solve_nontemporal(int n, const double* dStack, double* dOut, cudaStream_t st);
+    void temporal_stack(const double* dY, const double* dA, const double* dB, double* dTstack, cudaStream_t st);
+    void temporal_append(const double* dTstack, const double* dW, std::int64_t t, double* dHist, double* dRows,
+                         double* residual, cudaStream_t st);
+
+    int P = 0, Q = 0, shared = 0, R = 0;
+    std::int64_t dims[2] = {0, 0};
+    DevBuf<double> stacks;   // 3 x (PQ x R)
+    DevBuf<double> Ud[2];    // P x d x Q
+    DevBuf<double> Gp[2];    // P x d x d
+    DevBuf<double> Lsum[2];  // d x d (Cholesky of sum_p G_p)
+    int sum_rank[2] = {0, 0};
+    DevBuf<double> Lw[2];    // shared x shared whitener (non-temporal modes)
+    int white_ok[2] = {0, 0};
+    DevBuf<double> Lp[2];    // P x Q x Q chol(U_p^T U_p)
+    DevBuf<int> lp_ok[2];    // P
+    bool pair_solve = false;
+    DevBuf<double> solved[2], Gw, rhs, tmp, tg, red, sw, maxdiag, RF, SC, sims, tscr;
+    DevBuf<int> ranks, perms, iscr;
+    DevBuf<DevStatus> err;
+    std::vector<int> last_perm;
+};
+
+}  // namespace octen

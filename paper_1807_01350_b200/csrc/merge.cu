@@ -1,0 +1,1104 @@
+// Stage 3: replica alignment and merge into the running factors, fp64.
+//
+// Restates (reference paths relative to /root/reference/proj):
+//   align_replicas               recovery.cpp:106-291
+//   stack_projections            recovery.cpp:293-313 (never materialized:
+//                                the stacked P~ enters only through
+//                                G_p = U_p U_p^T and U_cat products)
+//   recover_nontemporal          recovery.cpp:315-319  (normal equations on
+//                                the cached Cholesky of sum_p G_p)
+//   refine_stack                 recovery.cpp:464-529
+//   recover_nontemporal_weighted recovery.cpp:321-339  (per column r:
+//                                Gram sum_p w_pr^2 G_p, batched Cholesky)
+//   match_columns                recovery.cpp:559-588
+//   temporal_stack_from_summaries recovery.cpp:429-462
+//   recover_temporal_append      recovery.cpp:341-427  (shared t x t Gram of
+//                                the stacked W rows, Schur complement for the
+//                                history-gauge column)
+//   recover_batch                streaming.cpp:89-160
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "chol_batched.cuh"
+#include "engine.hpp"
+#include "gemm_simt.cuh"
+#include "small_linalg.cuh"
+
+namespace octen {
+
+namespace {
+
+constexpr double kRankTol = 1e-10;        // recovery.cpp:12
+constexpr double kDegenerateRow = 1e-12;  // recovery.cpp:13
+constexpr double kGramRankTol = 1e-14;    // pivot^2 relative threshold
+constexpr double kEps = 2.220446049250313e-16;
+
+// ---- GEMM functors ----
+struct UcatA {  // A(b, i, k) = U[b*bs + i + d k]   (U_p stacked: d x PQ, or per replica)
+    const double* U;
+    long long d;
+    long long bs;
+    __device__ double operator()(int b, int i, int k) const { return U[(size_t)b * bs + i + (size_t)d * k]; }
+};
+struct UcatB {  // B(b, k, j) = U[b*bs + j + d k]
+    const double* U;
+    long long d;
+    long long bs;
+    __device__ double operator()(int b, int k, int j) const { return U[(size_t)b * bs + j + (size_t)d * k]; }
+};
+struct UtA {  // A(p, a, i) = U[p*d*Q + i + d a]   (U_p^T rows)
+    const double* U;
+    long long d;
+    int Q;
+    __device__ double operator()(int p, int a, int i) const { return U[(size_t)p * d * Q + i + (size_t)d * a]; }
+};
+struct ColB {  // B(b, k, r) = X[b*bs + k + ld r]
+    const double* X;
+    long long ld;
+    long long bs;
+    __device__ double operator()(int b, int k, int r) const { return X[(size_t)b * bs + k + (size_t)ld * r]; }
+};
+struct StoreCM {  // C(b, i, j) -> X[b*bs + i + ld j]
+    double* X;
+    long long ld;
+    long long bs;
+    __device__ void operator()(int b, int i, int j, double v) const { X[(size_t)b * bs + i + (size_t)ld * j] = v; }
+};
+struct AccumCM {
+    double* X;
+    long long ld;
+    long long bs;
+    __device__ void operator()(int b, int i, int j, double v) const { X[(size_t)b * bs + i + (size_t)ld * j] += v; }
+};
+struct KrB {  // B(p, k = a + Q b, r) = Ut(a, r) * Vt(b, r), Ut/Vt: P x Q x R
+    const double* Ut;
+    const double* Vt;
+    int Q, R;
+    __device__ double operator()(int p, int k, int r) const {
+        const int a = k % Q, b = k / Q;
+        return Ut[(size_t)p * Q * R + a + (size_t)Q * r] * Vt[(size_t)p * Q * R + b + (size_t)Q * r];
+    }
+};
+struct YtA2 {  // A(p, c, k) = Y[p][k + Q^2 c]
+    const double* Y;
+    size_t q3, q2;
+    __device__ double operator()(int p, int c, int k) const { return Y[(size_t)p * q3 + k + q2 * c]; }
+};
+
+__device__ void set_err(DevStatus* e, int code, int problem, int a, int b, int c, double d = 0.0) {
+    e->code = code;
+    e->problem = problem;
+    e->a = a;
+    e->b = b;
+    e->c = c;
+    e->d = d;
+}
+
+// chol of the shared-column Gram of a projection block (Eigen LLT semantics:
+// fails on a non-positive pivot).  Gram from the leading `sh` columns of U
+// (d x Q col-major).
+__global__ void whitener_kernel(const double* U, long long d, int sh, double* L, int* ok) {
+    extern __shared__ double g[];
+    for (int e = threadIdx.x; e < sh * sh; e += blockDim.x) {
+        const int i = e % sh, j = e / sh;
+        double s = 0.0;
+        for (long long k = 0; k < d; ++k) s += U[k + d * i] * U[k + d * j];
+        g[e] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *ok = (chol_semidef(sh, g, sh, 0.0) == sh) ? 1 : 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < sh * sh; e += blockDim.x) L[e] = g[e];
+}
+
+__global__ void chol_small_from_host_kernel(double* G, int n, int* ok) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *ok = (chol_semidef(n, G, n, 0.0) == n) ? 1 : 0;
+}
+
+// chol(U_p^T U_p) per replica (refine_stack's LLT, recovery.cpp:486-487).
+__global__ void lp_kernel(const double* U, long long d, int Q, double* Lp, int* ok) {
+    extern __shared__ double g[];
+    const int p = blockIdx.x;
+    const double* u = U + (size_t)p * d * Q;
+    for (int e = threadIdx.x; e < Q * Q; e += blockDim.x) {
+        const int i = e % Q, j = e / Q;
+        double s = 0.0;
+        for (long long k = 0; k < d; ++k) s += u[k + d * i] * u[k + d * j];
+        g[e] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) ok[p] = (chol_semidef(Q, g, Q, 0.0) == Q) ? 1 : 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < Q * Q; e += blockDim.x) Lp[(size_t)p * Q * Q + e] = g[e];
+}
+
+struct AlignDev {
+    int P, Q, sh, R, order;
+    const double* Mf;   // P x 3 x Q x R
+    const double* Mlam; // P x R
+    const double* Lw0;  // sh x sh
+    const double* Lw1;
+    const double* Lwt;
+    const int* wok;     // 3 flags
+    double* RF;         // P x 3 x Q x R
+    double* SC;         // P x 3 x sh x R
+    double* stacks;     // 3 x PQ x R
+    const double* rms;  // P x R x R (pair-solve)
+    int pair;
+    int* perms;         // P x R
+    double* scales;     // P x 3 x R
+    double* minsim;     // P
+    double* maxoff;     // P
+    int* ambig;         // P
+    DevStatus* err;     // P + 1 (slot 0: reference)
+};
+
+// lambda^(1/N) spread and whitened shared coordinates (recovery.cpp:121-184).
+__global__ void align_prep_kernel(AlignDev a) {
+    const int p = blockIdx.x;
+    const int Q = a.Q, R = a.R, sh = a.sh;
+    const double inv_order = 1.0 / 3.0;
+    for (int n = 0; n < 3; ++n) {
+        const double* f = a.Mf + ((size_t)p * 3 + n) * Q * R;
+        double* rf = a.RF + ((size_t)p * 3 + n) * Q * R;
+        for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
+            const double lam = a.Mlam[(size_t)p * R + e / Q];
+            rf[e] = f[e] * pow(fmax(lam, 0.0), inv_order);
+        }
+    }
+    __syncthreads();
+    for (int n = 0; n < 3; ++n) {
+        const double* L = n == 0 ? a.Lw0 : (n == 1 ? a.Lw1 : a.Lwt);
+        const bool white = a.P >= 2 && a.wok[n];
+        const double* rf = a.RF + ((size_t)p * 3 + n) * Q * R;
+        double* sc = a.SC + ((size_t)p * 3 + n) * sh * R;
+        for (int r = threadIdx.x; r < R; r += blockDim.x) {
+            double* x = sc + (size_t)sh * r;
+            for (int i = 0; i < sh; ++i) x[i] = rf[i + (size_t)Q * r];
+            if (white) trsv_lower(sh, L, sh, x, 1);
+        }
+    }
+    __syncthreads();
+    if (p == 0 && a.P >= 2 && threadIdx.x == 0) {
+        for (int n = 0; n < 3; ++n) {
+            const double* sc = a.SC + (size_t)n * sh * R;
+            for (int c = 0; c < R; ++c) {
+                double s = 0.0;
+                for (int i = 0; i < sh; ++i) s += dsq(sc[i + (size_t)sh * c]);
+                if (sqrt(s) < kDegenerateRow) {
+                    set_err(a.err, kAlignDegenerateRef, -1, n + 1, 0, 0);
+                    return;
+                }
+            }
+        }
+    }
+}
+
+// Similarity, greedy matching, shared-row scales, stack blocks (recovery.cpp:196-289).
+__global__ void align_match_kernel(AlignDev a) {
+    const int p = blockIdx.x;
+    const int Q = a.Q, R = a.R, sh = a.sh, PQ = a.P * a.Q;
+    extern __shared__ double sm[];
+    double* sim = sm;            // R*R
+    double* cn = sim + R * R;    // R (candidate norms)
+    double* rn = cn + R;         // R (reference norms)
+    __shared__ int perm[64];
+    __shared__ unsigned char ru[64], cu[64];
+    __shared__ int bad;
+    DevStatus* err = a.err + 1 + p;
+    if (p == 0) {
+        for (int n = 0; n < 3; ++n) {
+            const double* rf = a.RF + (size_t)n * Q * R;
+            double* stk = a.stacks + (size_t)n * PQ * R;
+            for (int e = threadIdx.x; e < Q * R; e += blockDim.x) stk[(e % Q) + (size_t)PQ * (e / Q)] = rf[e];
+        }
+        for (int e = threadIdx.x; e < R; e += blockDim.x) {
+            a.perms[e] = e;
+            for (int n = 0; n < 3; ++n) a.scales[(size_t)n * R + e] = 1.0;
+        }
+        return;
+    }
+    if (threadIdx.x == 0) bad = 0;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) sim[e] = 1.0;
+    __syncthreads();
+    if (a.pair) {
+        for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+            const double rho = sqrt(a.rms[(size_t)p * R * R + e] / 2.0);
+            sim[e] = 1.0 - fmin(1.0, rho);
+        }
+        __syncthreads();
+    } else {
+        for (int n = 0; n < 3; ++n) {
+            const double* sr = a.SC + (size_t)n * sh * R;
+            const double* sc = a.SC + ((size_t)p * 3 + n) * sh * R;
+            for (int c = threadIdx.x; c < R; c += blockDim.x) {
+                double s1 = 0.0, s2 = 0.0;
+                for (int i = 0; i < sh; ++i) {
+                    s1 += dsq(sc[i + (size_t)sh * c]);
+                    s2 += dsq(sr[i + (size_t)sh * c]);
+                }
+                cn[c] = sqrt(s1);
+                rn[c] = sqrt(s2);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int c = 0; c < R; ++c)
+                    if (cn[c] < kDegenerateRow) {
+                        set_err(err, kAlignDegenerateRep, p, p + 1, n + 1, 0);
+                        bad = 1;
+                        break;
+                    }
+            }
+            __syncthreads();
+            if (bad) return;
+            for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+                const int i = e % R, j = e / R;
+                double dot = 0.0;
+                for (int k = 0; k < sh; ++k) {
+                    const double x = rn[i] > 0.0 ? sr[k + (size_t)sh * i] / rn[i] : sr[k + (size_t)sh * i];
+                    const double y = cn[j] > 0.0 ? sc[k + (size_t)sh * j] / cn[j] : sc[k + (size_t)sh * j];
+                    dot += x * y;
+                }
+                sim[e] *= fabs(dot);
+            }
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) {
+        unsigned char* ru_ = ru;
+        unsigned char* cu_ = cu;
+        a.ambig[p] = greedy_match(R, sim, R, 1e-9, perm, ru_, cu_);
+        double mn = 1.0, mx = 0.0;
+        for (int i = 0; i < R; ++i) {
+            mn = fmin(mn, sim[i + R * perm[i]]);
+            for (int j = 0; j < R; ++j)
+                if (j != perm[i]) mx = fmax(mx, sim[i + R * j]);
+        }
+        a.minsim[p] = mn;
+        a.maxoff[p] = mx;
+        for (int i = 0; i < R; ++i) a.perms[(size_t)p * R + i] = perm[i];
+    }
+    __syncthreads();
+    // scales per mode (in mode order, then column order, as the reference)
+    for (int n = 0; n < 3; ++n) {
+        const double* sr = a.SC + (size_t)n * sh * R;
+        const double* sc = a.SC + ((size_t)p * 3 + n) * sh * R;
+        for (int i = threadIdx.x; i < R; i += blockDim.x) {
+            const int j = perm[i];
+            double den = 0.0, num = 0.0;
+            for (int k = 0; k < sh; ++k) {
+                den += dsq(sc[k + (size_t)sh * j]);
+                num += sr[k + (size_t)sh * i] * sc[k + (size_t)sh * j];
+            }
+            cn[i] = den > 0.0 ? num / den : 0.0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int i = 0; i < R; ++i)
+                if (!isfinite(cn[i]) || cn[i] == 0.0) {
+                    set_err(err, kAlignDegenerateScale, p, p + 1, n + 1, 0);
+                    bad = 1;
+                    break;
+                }
+        }
+        __syncthreads();
+        if (bad) return;
+        const double* rf = a.RF + ((size_t)p * 3 + n) * Q * R;
+        double* stk = a.stacks + (size_t)n * PQ * R;
+        for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
+            const int q = e % Q, i = e / Q;
+            stk[(size_t)p * Q + q + (size_t)PQ * i] = cn[i] * rf[q + (size_t)Q * perm[i]];
+        }
+        for (int i = threadIdx.x; i < R; i += blockDim.x) a.scales[((size_t)p * 3 + n) * R + i] = cn[i];
+        __syncthreads();
+    }
+}
+
+// Pair-solve similarity (recovery.cpp:203-246) in normal-equation form:
+// residual^2 = |rhs|^2 - g^T (J^T J)^-1 g with g = U_ref rb_i + s U_rep cb_j.
+// Inputs per (p, n): Y1 = Gj^-1 g1 (d x R), Y2 = Gj^-1 g2 (d x R).
+__global__ void pair_rms_kernel(int P, int Q, int sh, int R, long long d, int n, const double* g1,
+                                const double* Y1, const double* g2, const double* Y2, const double* RF,
+                                const double* SC, double* rms) {
+    const int p = blockIdx.x + 1;
+    const double* y1 = Y1 + (size_t)p * d * R;
+    const double* gg2 = g2 + (size_t)p * d * R;
+    const double* y2 = Y2 + (size_t)p * d * R;
+    const double* rb = RF + ((size_t)0 * 3 + n) * Q * R;
+    const double* cb = RF + ((size_t)p * 3 + n) * Q * R;
+    const double* sr = SC + ((size_t)0 * 3 + n) * sh * R;
+    const double* sc = SC + ((size_t)p * 3 + n) * sh * R;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+        const int i = e % R, j = e / R;
+        double zz = 0.0, zr = 0.0;
+        for (int k = 0; k < sh; ++k) {
+            zz += dsq(sc[k + (size_t)sh * j]);
+            zr += sr[k + (size_t)sh * i] * sc[k + (size_t)sh * j];
+        }
+        const double s = zz > 0.0 ? zr / zz : 0.0;
+        double rb2 = 0.0, cb2 = 0.0;
+        for (int q = 0; q < Q; ++q) {
+            rb2 += dsq(rb[q + (size_t)Q * i]);
+            cb2 += dsq(cb[q + (size_t)Q * j]);
+        }
+        double a11 = 0.0, a12 = 0.0, a22 = 0.0;
+        for (long long k = 0; k < d; ++k) {
+            a11 += g1[k + d * i] * y1[k + d * i];
+            a12 += g1[k + d * i] * y2[k + d * j];
+            a22 += gg2[k + d * j] * y2[k + d * j];
+        }
+        const double rhs2 = rb2 + s * s * cb2;
+        const double proj = a11 + 2.0 * s * a12 + s * s * a22;
+        const double res2 = fmax(0.0, rhs2 - proj);
+        const double rel = sqrt(res2) / fmax(sqrt(rhs2), 1e-300);
+        rms[(size_t)p * R * R + e] += rel * rel;
+    }
+}
+
+// refine_stack per replica (recovery.cpp:475-517): whitened per-column scale,
+// cosine agreement, in-place stack rescale, weights ((a-0.5)/0.5)^2.
+__global__ void refine_kernel(int P, int Q, int R, int PQ, const double* tg, double* stacks, const double* Lp0,
+                              const double* Lp1, const int* ok0, const int* ok1, double* weights) {
+    const int p = blockIdx.x;
+    extern __shared__ double sm[];
+    double* zt = sm;             // Q*R
+    double* zb = zt + Q * R;     // Q*R
+    double* agr = zb + Q * R;    // R
+    for (int r = threadIdx.x; r < R; r += blockDim.x) agr[r] = 1.0;
+    __syncthreads();
+    for (int n = 0; n < 2; ++n) {
+        const double* L = (n == 0 ? Lp0 : Lp1) + (size_t)p * Q * Q;
+        const bool white = (n == 0 ? ok0 : ok1)[p] != 0;
+        const double* t = tg + ((size_t)p * 2 + n) * Q * R;
+        double* stk = stacks + (size_t)n * PQ * R;
+        for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
+            zt[e] = t[e];
+            zb[e] = stk[(size_t)p * Q + (e % Q) + (size_t)PQ * (e / Q)];
+        }
+        __syncthreads();
+        if (white)
+            for (int c = threadIdx.x; c < 2 * R; c += blockDim.x)
+                trsv_lower(Q, L, Q, (c < R ? zt : zb) + (size_t)Q * (c % R), 1);
+        __syncthreads();
+        for (int r = threadIdx.x; r < R; r += blockDim.x) {
+            double bb = 0.0, bt = 0.0, tt = 0.0;
+            for (int q = 0; q < Q; ++q) {
+                const double b = zb[q + Q * r], x = zt[q + Q * r];
+                bb += b * b;
+                bt += b * x;
+                tt += x * x;
+            }
+            const double scale = bb > 0.0 ? bt / bb : 0.0;
+            const double cosine = (bb > 0.0 && tt > 0.0) ? bt / sqrt(bb * tt) : 0.0;
+            if (!isfinite(scale) || fabs(scale) < 1e-3 || fabs(scale) > 1e3) {
+                agr[r] = 0.0;
+                continue;
+            }
+            for (int q = 0; q < Q; ++q) stk[(size_t)p * Q + q + (size_t)PQ * r] *= scale;
+            agr[r] *= fabs(cosine);
+        }
+        __syncthreads();
+    }
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        const double av = agr[r];
+        weights[(size_t)p + (size_t)P * r] = av <= 0.5 ? 0.0 : ((av - 0.5) / 0.5) * ((av - 0.5) / 0.5);
+    }
+}
+
+// Keep every column solvable (recovery.cpp:519-527).
+__global__ void weight_mass_kernel(int P, int Q, int R, long long max_dim, double* w) {
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        double mass = 0.0;
+        for (int p = 0; p < P; ++p) mass += w[(size_t)p + (size_t)P * r] > 0.0 ? Q : 0;
+        if (mass < (double)max_dim + 1)
+            for (int p = 0; p < P; ++p) w[(size_t)p + (size_t)P * r] = 1.0;
+    }
+}
+
+// Gw[r](i,j) = sum_p w_pr^2 G_p(i,j), lower triangle.
+__global__ void weighted_gram_kernel(int P, int R, long long d, const double* Gp, const double* w, double* Gw) {
+    const size_t total = (size_t)d * d;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const long long i = (long long)(e % d), j = (long long)(e / d);
+        if (i < j) continue;
+        double g[64];
+        for (int p = 0; p < P; ++p) g[p] = Gp[(size_t)p * total + e];
+        for (int r = 0; r < R; ++r) {
+            double s = 0.0;
+            for (int p = 0; p < P; ++p) {
+                const double wv = w[(size_t)p + (size_t)P * r];
+                s += wv * wv * g[p];
+            }
+            Gw[(size_t)r * total + e] = s;
+        }
+    }
+}
+
+// SW(k, r) = w_{k/Q, r}^2 * stack(k, r)
+__global__ void scale_stack_kernel(int P, int Q, int R, const double* stack, const double* w, double* sw) {
+    const size_t PQ = (size_t)P * Q, total = PQ * R;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const size_t k = e % PQ, r = e / PQ;
+        const double wv = w[k / Q + (size_t)P * r];
+        sw[e] = wv * wv * stack[e];
+    }
+}
+
+// match_columns (recovery.cpp:559-588) on the two non-temporal factors.
+__global__ void match_columns_kernel(int R, long long d0, long long d1, const double* cur0, const double* cur1,
+                                     const double* sto0, const double* sto1, int* perm_out, double* signs_out,
+                                     double* sim_out) {
+    extern __shared__ double sm[];
+    double* sim = sm;               // R*R
+    double* nc = sim + R * R;       // 2R
+    double* ns = nc + 2 * R;        // 2R
+    __shared__ int perm[64];
+    __shared__ unsigned char ru[64], cu[64];
+    for (int e = threadIdx.x; e < 2 * R; e += blockDim.x) {
+        const int n = e / R, c = e % R;
+        const long long d = n ? d1 : d0;
+        const double* cur = (n ? cur1 : cur0) + (size_t)d * c;
+        const double* sto = (n ? sto1 : sto0) + (size_t)d * c;
+        double a = 0.0, b = 0.0;
+        for (long long i = 0; i < d; ++i) {
+            a += cur[i] * cur[i];
+            b += sto[i] * sto[i];
+        }
+        nc[e] = sqrt(a);
+        ns[e] = sqrt(b);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+        const int i = e % R, j = e / R;  // i: stored, j: current
+        double s = 1.0;
+        for (int n = 0; n < 2; ++n) {
+            const long long d = n ? d1 : d0;
+            const double* cur = (n ? cur1 : cur0) + (size_t)d * j;
+            const double* sto = (n ? sto1 : sto0) + (size_t)d * i;
+            const double a = nc[n * R + j] > 0.0 ? nc[n * R + j] : 1.0;
+            const double b = ns[n * R + i] > 0.0 ? ns[n * R + i] : 1.0;
+            double dot = 0.0;
+            for (long long k = 0; k < d; ++k) dot += (sto[k] / b) * (cur[k] / a);
+            s *= fabs(dot);
+        }
+        sim[e] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) greedy_match(R, sim, R, 1e-9, perm, ru, cu);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 2 * R; e += blockDim.x) {
+        const int n = e / R, i = e % R, j = perm[i];
+        const long long d = n ? d1 : d0;
+        const double* cur = (n ? cur1 : cur0) + (size_t)d * j;
+        const double* sto = (n ? sto1 : sto0) + (size_t)d * i;
+        const double a = nc[n * R + j] > 0.0 ? nc[n * R + j] : 1.0;
+        const double b = ns[n * R + i] > 0.0 ? ns[n * R + i] : 1.0;
+        double dot = 0.0;
+        for (long long k = 0; k < d; ++k) dot += (sto[k] / b) * (cur[k] / a);
+        signs_out[(size_t)n * R + i] = dot < 0.0 ? -1.0 : 1.0;
+    }
+    for (int i = threadIdx.x; i < R; i += blockDim.x) perm_out[i] = perm[i];
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) sim_out[e] = sim[e];
+}
+
+// fin.col(i) = solved.col(perm[i]) * sign(i) / |solved.col(perm[i])|  (streaming.cpp:136-148)
+__global__ void finalize_kernel(int R, long long d, const double* solved, const int* perm, const double* signs,
+                                double* fin, DevStatus* err, int mode_slot) {
+    __shared__ double red[256];
+    const int i = blockIdx.x;
+    const int j = perm[i];
+    const double* s = solved + (size_t)d * j;
+    double acc = 0.0;
+    for (long long k = threadIdx.x; k < d; k += blockDim.x) acc += s[k] * s[k];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if ((int)threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+        __syncthreads();
+    }
+    const double nrm = sqrt(red[0]);
+    if (!(nrm > 0.0)) {
+        if (threadIdx.x == 0) set_err(err, kRecoverZeroColumn, mode_slot, 0, 0, 0);
+        return;
+    }
+    const double f = (signs ? signs[i] : 1.0) / nrm;
+    for (long long k = threadIdx.x; k < d; k += blockDim.x) fin[k + (size_t)d * i] = s[k] * f;
+}
+
+// Per replica: C~_p = M_p Gram_p^-1 with Gram_p = (Ut^T Ut) .* (Vt^T Vt)
+// (COD solve of recovery.cpp:456-459; pseudo-inverse fallback when singular).
+__global__ void tstack_solve_kernel(int P, int Q, int R, const double* Ut, const double* Vt, const double* Mt,
+                                    double* tstack) {
+    const int p = blockIdx.x;
+    extern __shared__ double sm[];
+    double* Gm = sm;           // R*R
+    double* Lf = Gm + R * R;   // R*R
+    double* Ev = Lf + R * R;   // R*R
+    double* cs = Ev + R * R;   // 2(R+2)
+    int* flag = (int*)(cs + 2 * (R + 2));
+    __shared__ int rank;
+    const double* ut = Ut + (size_t)p * Q * R;
+    const double* vt = Vt + (size_t)p * Q * R;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+        const int i = e % R, j = e / R;
+        double a = 0.0, b = 0.0;
+        for (int q = 0; q < Q; ++q) {
+            a += ut[q + (size_t)Q * i] * ut[q + (size_t)Q * j];
+            b += vt[q + (size_t)Q * i] * vt[q + (size_t)Q * j];
+        }
+        Gm[e] = a * b;
+        Lf[e] = a * b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) rank = chol_semidef(R, Lf, R, kEps * R);
+    __syncthreads();
+    const double* m = Mt + (size_t)p * Q * R;
+    const size_t PQ = (size_t)P * Q;
+    if (rank == R) {
+        for (int c = threadIdx.x; c < Q; c += blockDim.x) {
+            double x[64];
+            for (int r = 0; r < R; ++r) x[r] = m[c + (size_t)Q * r];
+            chol_solve_vec(R, Lf, R, x, 1);
+            for (int r = 0; r < R; ++r) tstack[(size_t)p * Q + c + PQ * r] = x[r];
+        }
+    } else {
+        TeamDev team;
+        jacobi_eig_sym(team, R, Gm, Ev, cs, flag);
+        __syncthreads();
+        double wmax = 0.0;
+        for (int i = 0; i < R; ++i) wmax = fmax(wmax, fabs(Gm[i + R * i]));
+        const double thr = 1e-16 * wmax;  // COD threshold 1e-8 on the chain's pivots
+        for (int c = threadIdx.x; c < Q; c += blockDim.x) {
+            double x[64], y[64];
+            for (int r = 0; r < R; ++r) {
+                x[r] = m[c + (size_t)Q * r];
+                y[r] = 0.0;
+            }
+            for (int e = 0; e < R; ++e) {
+                const double w = Gm[e + R * e];
+                if (!(w > thr)) continue;
+                double dot = 0.0;
+                for (int i = 0; i < R; ++i) dot += Ev[i + R * e] * x[i];
+                dot /= w;
+                for (int i = 0; i < R; ++i) y[i] += Ev[i + R * e] * dot;
+            }
+            for (int r = 0; r < R; ++r) tstack[(size_t)p * Q + c + PQ * r] = y[r];
+        }
+    }
+}
+
+// per column r: hh = |h_r|^2, hr = h_r . rhs_r, rr = |rhs_r|^2
+__global__ void append_dots_kernel(long long PQ, const double* tstack, const double* hist, double* dots) {
+    __shared__ double r1[256], r2[256], r3[256];
+    const int r = blockIdx.x;
+    const double* x = tstack + (size_t)PQ * r;
+    const double* h = hist + (size_t)PQ * r;
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (long long k = threadIdx.x; k < PQ; k += blockDim.x) {
+        a += h[k] * h[k];
+        b += h[k] * x[k];
+        c += x[k] * x[k];
+    }
+    r1[threadIdx.x] = a;
+    r2[threadIdx.x] = b;
+    r3[threadIdx.x] = c;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) {
+            r1[threadIdx.x] += r1[threadIdx.x + s];
+            r2[threadIdx.x] += r2[threadIdx.x + s];
+            r3[threadIdx.x] += r3[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        dots[3 * r + 0] = r1[0];
+        dots[3 * r + 1] = r2[0];
+        dots[3 * r + 2] = r3[0];
+    }
+}
+
+// Per-column solve decisions of recover_temporal_append (recovery.cpp:375-418).
+// Z holds Gc^-1 [bv | hv] (t x 2R).  Writes rows (t x R), gauge/hsel per column.
+__global__ void append_decide_kernel(int R, long long t, int rank_c, const double* dots, const double* hv,
+                                     const double* Z, const double* maxdiag, double* rows, double* coef,
+                                     DevStatus* err, int tmode) {
+    const int r = blockIdx.x;
+    __shared__ double red[256];
+    __shared__ int path;  // 0 plain, 1 joint accepted, 2 joint rejected (gauge 1)
+    __shared__ double gauge;
+    const double hh = dots[3 * r], hr = dots[3 * r + 1], rr = dots[3 * r + 2];
+    const double* z = Z + (size_t)t * r;
+    const double* y = Z + (size_t)t * (R + r);
+    const double* hvr = hv + (size_t)t * r;
+    const double hn = sqrt(hh), rn = sqrt(rr);
+    if (hn <= kRankTol * fmax(1.0, rn)) {
+        if (threadIdx.x == 0) {
+            path = 0;
+            gauge = 1.0;
+            if (rank_c < t) set_err(err + r, kRecoverRankDeficient, r, tmode + 1, rank_c, (int)t);
+        }
+    } else {
+        double a = 0.0, b = 0.0;
+        for (long long k = threadIdx.x; k < t; k += blockDim.x) {
+            a += hvr[k] * y[k];
+            b += hvr[k] * z[k];
+        }
+        red[threadIdx.x] = a;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+            __syncthreads();
+        }
+        const double hvy = red[0];
+        __syncthreads();
+        red[threadIdx.x] = b;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+            __syncthreads();
+        }
+        const double hvz = red[0];
+        if (threadIdx.x == 0) {
+            const double schur = hh - hvy;
+            const double scale = fmax(*maxdiag, hh);
+            if (rank_c < t || !(schur > kGramRankTol * scale)) {
+                set_err(err + r, kAppendRankDeficient, r, 0, 0, 0);
+                path = -1;
+            } else {
+                double g = (hr - hvz) / schur;
+                if (!isfinite(g)) {
+                    set_err(err + r, kAppendNonFiniteGauge, r, 0, 0, 0);
+                    path = -1;
+                } else if (fabs(g - 1.0) > 0.5) {
+                    path = 2;
+                    gauge = 1.0;
+                } else {
+                    path = 1;
+                    gauge = g;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (path < 0) return;
+    double* out = rows + (size_t)t * r;
+    for (long long k = threadIdx.x; k < t; k += blockDim.x) {
+        double v;
+        if (path == 0)
+            v = z[k];
+        else if (path == 2)
+            v = z[k] - y[k];
+        else
+            v = (z[k] - y[k] * gauge) / gauge;
+        out[k] = v;
+    }
+    if (threadIdx.x == 0) {
+        coef[2 * r] = gauge;
+        coef[2 * r + 1] = path == 0 ? 0.0 : 1.0;
+    }
+}
+
+// fitted residual norms: f = rhs - g (hsel h + Ps), per column
+__global__ void append_resid_kernel(long long PQ, const double* tstack, const double* hist, const double* Ps,
+                                    const double* coef, double* out) {
+    __shared__ double red[256];
+    const int r = blockIdx.x;
+    const double g = coef[2 * r], hs = coef[2 * r + 1];
+    double a = 0.0;
+    for (long long k = threadIdx.x; k < PQ; k += blockDim.x) {
+        const size_t e = (size_t)PQ * r + k;
+        const double f = tstack[e] - g * (hs * hist[e] + Ps[e]);
+        a += f * f;
+    }
+    red[threadIdx.x] = a;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[r] = red[0];
+}
+
+__global__ void add_kernel(size_t n, const double* a, double* b) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        b[i] += a[i];
+}
+
+int grid_for(size_t n, int threads = 256) {
+    size_t b = (n + threads - 1) / threads;
+    if (b > 148 * 8) b = 148 * 8;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+void throw_status(const DevStatus& e) {
+    switch (e.code) {
+        case kAlignDegenerateRef:
+            throw NumericError("align_replicas: degenerate shared rows in reference, mode " + std::to_string(e.a));
+        case kAlignDegenerateRep:
+            throw NumericError("align_replicas: degenerate shared rows in replica " + std::to_string(e.a) + ", mode " +
+                               std::to_string(e.b));
+        case kAlignDegenerateScale:
+            throw NumericError("align_replicas: degenerate scale for replica " + std::to_string(e.a) + ", mode " +
+                               std::to_string(e.b));
+        case kRecoverRankDeficient:
+            throw NumericError("recover: rank-deficient projection on mode " + std::to_string(e.a) + " (rank " +
+                               std::to_string(e.b) + " of " + std::to_string(e.c) + ")");
+        case kRecoverZeroColumn:
+            throw NumericError("recover: zero column in recovered factor");
+        case kAppendRankDeficient:
+            throw NumericError("recover_temporal_append: rank-deficient joint system");
+        case kAppendNonFiniteGauge:
+            throw NumericError("recover_temporal_append: non-finite history gauge");
+        default:
+            throw NumericError("octen: device error code " + std::to_string(e.code));
+    }
+}
+
+void check_errs(DevBuf<DevStatus>& err, int count, cudaStream_t st) {
+    std::vector<DevStatus> h = err.to_host(count, st);
+    for (int i = 0; i < count; ++i)
+        if (h[i].code != kOk) throw_status(h[i]);
+}
+
+}  // namespace
+
+void MergeEngine::set_projections(int P_, int Q_, int sh, int R_, std::int64_t I, std::int64_t J, const double* hU,
+                                  const double* hV, cudaStream_t st) {
+    P = P_;
+    Q = Q_;
+    shared = sh;
+    R = R_;
+    dims[0] = I;
+    dims[1] = J;
+    if (R > 64) throw ConfigError("octen: device merge supports rank <= 64");
+    if (P > 64) throw ConfigError("octen: device merge supports p <= 64");
+    const long long PQ = (long long)P * Q;
+    for (int n = 0; n < 2; ++n) {
+        const long long d = dims[n];
+        Ud[n].upload(n == 0 ? hU : hV, (size_t)P * d * Q, st);
+        Gp[n].reserve((size_t)P * d * d);
+        gemm_simt<double, double, false, false>(P, (int)d, (int)d, Q, UcatA{Ud[n].p, d, d * Q}, UcatB{Ud[n].p, d, d * Q},
+                                                StoreCM{Gp[n].p, d, d * d}, st);
+        Lsum[n].reserve((size_t)d * d);
+        gemm_simt<double, double, false, false>(1, (int)d, (int)d, (int)PQ, UcatA{Ud[n].p, d, 0}, UcatB{Ud[n].p, d, 0},
+                                                StoreCM{Lsum[n].p, d, 0}, st);
+        maxdiag.reserve(128);
+        ranks.reserve(128);
+        chol_batched(Lsum[n].p, (int)d, (int)d, 0, 1, kGramRankTol, maxdiag.p, ranks.p, st);
+        sum_rank[n] = ranks.to_host(1, st)[0];
+        // whitener of the shared block (reference replica; the block is shared)
+        DevBuf<int> okb;
+        okb.reserve(1);
+        Lw[n].reserve((size_t)std::max(1, sh * sh));
+        white_ok[n] = 0;
+        if (sh > 0) {
+            whitener_kernel<<<1, 256, (size_t)sh * sh * sizeof(double), st>>>(Ud[n].p, d, sh, Lw[n].p, okb.p);
+            OCTEN_CUDA(cudaGetLastError());
+            white_ok[n] = okb.to_host(1, st)[0];
+        }
+        Lp[n].reserve((size_t)P * Q * Q);
+        lp_ok[n].reserve(P);
+        const size_t smem = (size_t)Q * Q * sizeof(double);
+        OCTEN_CUDA(cudaFuncSetAttribute(lp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        lp_kernel<<<P, 256, smem, st>>>(Ud[n].p, d, Q, Lp[n].p, lp_ok[n].p);
+        OCTEN_CUDA(cudaGetLastError());
+    }
+    pair_solve = P >= 2;
+    for (int n = 0; n < 2; ++n)
+        if (2LL * Q < dims[n] + 1) pair_solve = false;
+    stacks.reserve((size_t)3 * PQ * R);
+    OCTEN_CUDA(cudaStreamSynchronize(st));
+}
+
+void MergeEngine::align(const double* dMf, const double* dMlam, const std::vector<double>& tgram, cudaStream_t st,
+                        AlignResultHost* out) {
+    const int sh = shared;
+    const size_t PQ = (size_t)P * Q;
+    if (P >= 2 && sh < 1) throw ConfigError("align_replicas: shared columns required to align multiple replicas");
+    RF.reserve((size_t)P * 3 * Q * R);
+    SC.reserve((size_t)P * 3 * std::max(sh, 1) * R);
+    err.reserve(P + 1 + 64);
+    err.zero(P + 1, st);
+    perms.reserve((size_t)P * R);
+    red.reserve((size_t)P * 3 * R + 3 * P);
+    iscr.reserve(P + 8);
+    // temporal whitener
+    DevBuf<double> Lwt;
+    Lwt.reserve((size_t)std::max(1, sh * sh));
+    iscr.zero(8, st);
+    if (sh > 0 && (int)tgram.size() == sh * sh) {
+        OCTEN_CUDA(cudaMemcpyAsync(Lwt.p, tgram.data(), sizeof(double) * sh * sh, cudaMemcpyHostToDevice, st));
+        chol_small_from_host_kernel<<<1, 32, 0, st>>>(Lwt.p, sh, iscr.p + 2);
+    }
+    std::vector<int> wok = {white_ok[0], white_ok[1], 0};
+    OCTEN_CUDA(cudaMemcpyAsync(iscr.p, wok.data(), 2 * sizeof(int), cudaMemcpyHostToDevice, st));
+    double* scales_d = red.p;
+    double* minsim_d = red.p + (size_t)P * 3 * R;
+    double* maxoff_d = minsim_d + P;
+    DevBuf<int> ambig;
+    ambig.reserve(P);
+    ambig.zero(P, st);
+
+    AlignDev a;
+    a.P = P;
+    a.Q = Q;
+    a.sh = sh;
+    a.R = R;
+    a.order = 3;
+    a.Mf = dMf;
+    a.Mlam = dMlam;
+    a.Lw0 = Lw[0].p;
+    a.Lw1 = Lw[1].p;
+    a.Lwt = Lwt.p;
+    a.wok = iscr.p;
+    a.RF = RF.p;
+    a.SC = SC.p;
+    a.stacks = stacks.p;
+    a.pair = pair_solve ? 1 : 0;
+    a.perms = perms.p;
+    a.scales = scales_d;
+    a.minsim = minsim_d;
+    a.maxoff = maxoff_d;
+    a.ambig = ambig.p;
+    a.err = err.p;
+    align_prep_kernel<<<P, 128, 0, st>>>(a);
+    OCTEN_CUDA(cudaGetLastError());
+    check_errs(err, 1, st);
+    DevBuf<double> rmsb;
+    if (pair_solve) {
+        // per non-temporal mode: Gj_p = G_0 + G_p, g1 = U_0 rb, g2 = U_p cb, solves
+        rmsb.reserve((size_t)P * R * R);
+        rmsb.zero((size_t)P * R * R, st);
+        for (int n = 0; n < 2; ++n) {
+            const long long d = dims[n];
+            DevBuf<double> Gj, g1, g2, Y1, Y2, md;
+            DevBuf<int> rk;
+            Gj.reserve((size_t)P * d * d);
+            g1.reserve((size_t)d * R);
+            g2.reserve((size_t)P * d * R);
+            Y1.reserve((size_t)P * d * R);
+            Y2.reserve((size_t)P * d * R);
+            md.reserve(P);
+            rk.reserve(P);
+            for (int p = 0; p < P; ++p) {
+                OCTEN_CUDA(cudaMemcpyAsync(Gj.p + (size_t)p * d * d, Gp[n].p, sizeof(double) * d * d,
+                                           cudaMemcpyDeviceToDevice, st));
+                add_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>((size_t)d * d, Gp[n].p + (size_t)p * d * d,
+                                                                     Gj.p + (size_t)p * d * d);
+            }
+            chol_batched(Gj.p, (int)d, (int)d, d * d, P, 1e-15, md.p, rk.p, st);
+            // g1 = U_0 RF_0[n]  (d x R)
+            gemm_simt<double, double, false, true>(1, (int)d, R, Q, UcatA{Ud[n].p, d, 0},
+                                                   ColB{RF.p + (size_t)n * Q * R, Q, 0}, StoreCM{g1.p, d, 0}, st);
+            // g2_p = U_p RF_p[n]
+            gemm_simt<double, double, false, true>(P, (int)d, R, Q, UcatA{Ud[n].p, d, d * Q},
+                                                   ColB{RF.p + (size_t)n * Q * R, Q, 3LL * Q * R},
+                                                   StoreCM{g2.p, d, d * R}, st);
+            for (int p = 0; p < P; ++p)
+                OCTEN_CUDA(cudaMemcpyAsync(Y1.p + (size_t)p * d * R, g1.p, sizeof(double) * d * R,
+                                           cudaMemcpyDeviceToDevice, st));
+            OCTEN_CUDA(cudaMemcpyAsync(Y2.p, g2.p, sizeof(double) * P * d * R, cudaMemcpyDeviceToDevice, st));
+            chol_solve_batched(Gj.p, (int)d, (int)d, d * d, Y1.p, (int)d, d * R, R, P, st);
+            chol_solve_batched(Gj.p, (int)d, (int)d, d * d, Y2.p, (int)d, d * R, R, P, st);
+            if (P > 1)
+                pair_rms_kernel<<<P - 1, 256, 0, st>>>(P, Q, sh, R, d, n, g1.p, Y1.p, g2.p, Y2.p, RF.p, SC.p, rmsb.p);
+            OCTEN_CUDA(cudaGetLastError());
+            OCTEN_CUDA(cudaStreamSynchronize(st));
+        }
+        a.rms = rmsb.p;
+    } else {
+        a.rms = nullptr;
+    }
+    const size_t smem = (size_t)(R * R + 2 * R) * sizeof(double);
+    align_match_kernel<<<P, 128, smem, st>>>(a);
+    OCTEN_CUDA(cudaGetLastError());
+    check_errs(err, P + 1, st);
+    if (out) {
+        out->perms = perms.to_host((size_t)P * R, st);
+        out->scales = red.to_host((size_t)P * 3 * R, st);
+        std::vector<double> mm = red.to_host((size_t)P * 3 * R + 2 * P, st);
+        std::vector<int> am = ambig.to_host(P, st);
+        out->min_match = 1.0;
+        out->max_offdiag = 0.0;
+        out->ambiguous = 0;
+        for (int p = 1; p < P; ++p) {
+            out->min_match = std::min(out->min_match, mm[(size_t)P * 3 * R + p]);
+            out->max_offdiag = std::max(out->max_offdiag, mm[(size_t)P * 3 * R + P + p]);
+            out->ambiguous += am[p];
+        }
+    }
+}
+
+void MergeEngine::solve_nontemporal(int n, const double* dStack, double* dOut, cudaStream_t st) {
+    const long long d = dims[n], PQ = (long long)P * Q;
+    if (PQ < d)
+        throw NumericError("recover: mode " + std::to_string(n + 1) + " projection is " + std::to_string(PQ) + "x" +
+                           std::to_string(d) + "; p*Q must reach the mode extent (raise p per the replica bound)");
+    if (sum_rank[n] < d)
+        throw NumericError("recover: rank-deficient projection on mode " + std::to_string(n + 1) + " (rank " +
+                           std::to_string(sum_rank[n]) + " of " + std::to_string(d) + ")");
+    gemm_simt<double, double, false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{dStack, PQ, 0},
+                                           StoreCM{dOut, d, 0}, st);
+    chol_solve_batched(Lsum[n].p, (int)d, (int)d, 0, dOut, (int)d, 0, R, 1, st);
+}
+
+void MergeEngine::temporal_stack(const double* dY, const double* dA, const double* dB, double* dTstack,
+                                 cudaStream_t st) {
+    const size_t q2 = (size_t)Q * Q, q3 = q2 * Q;
+    tg.reserve((size_t)P * 2 * Q * R);
+    double* Ut = tg.p;
+    double* Vt = tg.p + (size_t)P * Q * R;
+    gemm_simt<double, double, true, true>(P, Q, R, (int)dims[0], UtA{Ud[0].p, dims[0], Q}, ColB{dA, dims[0], 0},
+                                          StoreCM{Ut, Q, (long long)Q * R}, st);
+    gemm_simt<double, double, true, true>(P, Q, R, (int)dims[1], UtA{Ud[1].p, dims[1], Q}, ColB{dB, dims[1], 0},
+                                          StoreCM{Vt, Q, (long long)Q * R}, st);
+    tmp.reserve((size_t)P * Q * R);
+    const int ks = pick_ksplit(P, Q, R, (int)q2);
+    tscr.reserve((size_t)P * ks * Q * R);
+    gemm_simt<double, double, true, true>(P, Q, R, (int)q2, YtA2{dY, q3, q2}, KrB{Ut, Vt, Q, R},
+                                          StoreCM{tmp.p, Q, (long long)Q * R}, st, ks, tscr.p);
+    const size_t smem = (size_t)(3 * R * R + 2 * (R + 2)) * sizeof(double) + 16;
+    tstack_solve_kernel<<<P, 128, smem, st>>>(P, Q, R, Ut, Vt, tmp.p, dTstack);
+    OCTEN_CUDA(cudaGetLastError());
+}
+
+void MergeEngine::temporal_append(const double* dTstack, const double* dW, std::int64_t t, double* dHist,
+                                  double* dRows, double* residual, cudaStream_t st) {
+    const long long PQ = (long long)P * Q;
+    if (PQ < t + 1) throw NumericError("recover_temporal_append: p*Q too small for the batch extent");
+    DevBuf<double> Gc, BZ, md, dots, coef, Ps, res;
+    DevBuf<int> rk;
+    Gc.reserve((size_t)t * t);
+    BZ.reserve((size_t)t * 2 * R);
+    md.reserve(1);
+    rk.reserve(1);
+    dots.reserve((size_t)3 * R);
+    coef.reserve((size_t)2 * R);
+    Ps.reserve((size_t)PQ * R);
+    res.reserve(R);
+    err.reserve(P + 1 + 64);
+    err.zero(R, st);
+    // Gc = Pc^T Pc = sum_{(p,a)} W_p[:,a] W_p[:,a]^T ; W as t x PQ col-major
+    gemm_simt<double, double, false, false>(1, (int)t, (int)t, (int)PQ, UcatA{dW, t, 0}, UcatB{dW, t, 0},
+                                            StoreCM{Gc.p, t, 0}, st);
+    chol_batched(Gc.p, (int)t, (int)t, 0, 1, kGramRankTol, md.p, rk.p, st);
+    // [bv | hv] = Pc^T [tstack | hist]
+    gemm_simt<double, double, false, true>(1, (int)t, R, (int)PQ, UcatA{dW, t, 0}, ColB{dTstack, PQ, 0},
+                                           StoreCM{BZ.p, t, 0}, st);
+    gemm_simt<double, double, false, true>(1, (int)t, R, (int)PQ, UcatA{dW, t, 0}, ColB{dHist, PQ, 0},
+                                           StoreCM{BZ.p + (size_t)t * R, t, 0}, st);
+    DevBuf<double> hv;
+    hv.reserve((size_t)t * R);
+    OCTEN_CUDA(cudaMemcpyAsync(hv.p, BZ.p + (size_t)t * R, sizeof(double) * t * R, cudaMemcpyDeviceToDevice, st));
+    append_dots_kernel<<<R, 256, 0, st>>>(PQ, dTstack, dHist, dots.p);
+    chol_solve_batched(Gc.p, (int)t, (int)t, 0, BZ.p, (int)t, 0, 2 * R, 1, st);
+    const int rank_c = rk.to_host(1, st)[0];
+    append_decide_kernel<<<R, 256, 0, st>>>(R, t, rank_c, dots.p, hv.p, BZ.p, md.p, dRows, coef.p, err.p,
+                                            2 /* temporal mode */);
+    OCTEN_CUDA(cudaGetLastError());
+    check_errs(err, R, st);
+    // Ps = Pc * rows (PQ x R)
+    gemm_simt<double, double, true, true>(1, (int)PQ, R, (int)t, UtA{dW, t, (int)PQ}, ColB{dRows, t, 0},
+                                          StoreCM{Ps.p, PQ, 0}, st);
+    append_resid_kernel<<<R, 256, 0, st>>>(PQ, dTstack, dHist, Ps.p, coef.p, res.p);
+    std::vector<double> hr = res.to_host(R, st);
+    std::vector<double> hd = dots.to_host((size_t)3 * R, st);
+    double res_sq = 0.0, rhs_sq = 0.0;
+    for (int r = 0; r < R; ++r) {
+        res_sq += hr[r];
+        rhs_sq += hd[3 * r + 2];
+    }
+    *residual = rhs_sq > 0.0 ? std::sqrt(res_sq / rhs_sq) : 0.0;
+    add_kernel<<<grid_for((size_t)PQ * R), 256, 0, st>>>((size_t)PQ * R, Ps.p, dHist);
+    OCTEN_CUDA(cudaGetLastError());
+}
+
+void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, double* dHist, const double* dStoredA,
+                          const double* dStoredB, double* dAfin, double* dBfin, double* dRows, double* residual,
+                          cudaStream_t st) {
+    const long long PQ = (long long)P * Q;
+    for (int n = 0; n < 2; ++n) {
+        solved[n].reserve((size_t)dims[n] * R);
+        solve_nontemporal(n, stacks.p + (size_t)n * PQ * R, solved[n].p, st);
+    }
+    // two refinement passes (streaming.cpp:107-120)
+    DevBuf<double> w;
+    w.reserve((size_t)P * R);
+    tg.reserve((size_t)P * 2 * Q * R);
+    sw.reserve((size_t)PQ * R);
+    rhs.reserve((size_t)std::max(dims[0], dims[1]) * R);
+    maxdiag.reserve(128);
+    ranks.reserve(128);
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int n = 0; n < 2; ++n) {
+            const long long d = dims[n];
+            // tg[p][n] = U_p^T solved_n  (Q x R)
+            gemm_simt<double, double, true, true>(P, Q, R, (int)d, UtA{Ud[n].p, d, Q}, ColB{solved[n].p, d, 0},
+                                                  StoreCM{tg.p + (size_t)n * Q * R, Q, 2LL * Q * R}, st);
+        }
+        const size_t smem = (size_t)(2 * Q * R + R) * sizeof(double);
+        OCTEN_CUDA(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        refine_kernel<<<P, 128, smem, st>>>(P, Q, R, (int)PQ, tg.p, stacks.p, Lp[0].p, Lp[1].p, lp_ok[0].p,
+                                            lp_ok[1].p, w.p);
+        weight_mass_kernel<<<1, 64, 0, st>>>(P, Q, R, std::max(dims[0], dims[1]), w.p);
+        OCTEN_CUDA(cudaGetLastError());
+        for (int n = 0; n < 2; ++n) {
+            const long long d = dims[n];
+            if (PQ < d)
+                throw NumericError("recover: mode " + std::to_string(n + 1) + " projection is " + std::to_string(PQ) +
+                                   "x" + std::to_string(d) +
+                                   "; p*Q must reach the mode extent (raise p per the replica bound)");
+            Gw.reserve((size_t)R * d * d);
+            weighted_gram_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>(P, R, d, Gp[n].p, w.p, Gw.p);
+            chol_batched(Gw.p, (int)d, (int)d, d * d, R, kGramRankTol, maxdiag.p, ranks.p, st);
+            scale_stack_kernel<<<grid_for((size_t)PQ * R), 256, 0, st>>>(P, Q, R, stacks.p + (size_t)n * PQ * R, w.p,
+                                                                        sw.p);
+            gemm_simt<double, double, false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{sw.p, PQ, 0},
+                                                   StoreCM{solved[n].p, d, 0}, st);
+            std::vector<int> rk = ranks.to_host(R, st);
+            for (int r = 0; r < R; ++r)
+                if (rk[r] < d)
+                    throw NumericError("recover: rank-deficient projection on mode " + std::to_string(n + 1) +
+                                       " (rank " + std::to_string(rk[r]) + " of " + std::to_string(d) + ")");
+            // each column r against its own factor
+            chol_solve_batched(Gw.p, (int)d, (int)d, d * d, solved[n].p, (int)d, d, 1, R, st);
+        }
+    }
+    // gauge to the stored factors
+    DevBuf<int> perm;
+    DevBuf<double> signs, simb;
+    perm.reserve(R);
+    signs.reserve((size_t)2 * R);
+    simb.reserve((size_t)R * R);
+    err.reserve(P + 1 + 64);
+    err.zero(2, st);
+    if (dStoredA && dStoredB) {
+        const size_t smem = (size_t)(R * R + 4 * R) * sizeof(double);
+        match_columns_kernel<<<1, 256, smem, st>>>(R, dims[0], dims[1], solved[0].p, solved[1].p, dStoredA, dStoredB,
+                                                   perm.p, signs.p, simb.p);
+        finalize_kernel<<<R, 256, 0, st>>>(R, dims[0], solved[0].p, perm.p, signs.p, dAfin, err.p, 0);
+        finalize_kernel<<<R, 256, 0, st>>>(R, dims[1], solved[1].p, perm.p, signs.p + R, dBfin, err.p + 1, 1);
+        last_perm = perm.to_host(R, st);
+    } else {
+        std::vector<int> id(R);
+        for (int i = 0; i < R; ++i) id[i] = i;
+        perm.upload(id.data(), R, st);
+        finalize_kernel<<<R, 256, 0, st>>>(R, dims[0], solved[0].p, perm.p, nullptr, dAfin, err.p, 0);
+        finalize_kernel<<<R, 256, 0, st>>>(R, dims[1], solved[1].p, perm.p, nullptr, dBfin, err.p + 1, 1);
+        last_perm = id;
+    }
+    OCTEN_CUDA(cudaGetLastError());
+    check_errs(err, 2, st);
+    // temporal stack from the summaries, then the append
+    DevBuf<double> tstack;
+    tstack.reserve((size_t)PQ * R);
+    temporal_stack(dY, dAfin, dBfin, tstack.p, st);
+    temporal_append(tstack.p, dW, t, dHist, dRows, residual, st);
+}
+
+}  // namespace octen

@@ -1,0 +1,65 @@
+// Common definitions for the OCTen B200 kernels and their host-side twins.
+//
+// OCTEN_HD marks routines compiled both for the device (nvcc, inside the
+// kernels of this library) and for the host (g++, only by the CPU test
+// harness tests/cpu_harness/small_linalg_host.cpp, which checks the small
+// dense solvers against numpy without a GPU).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define OCTEN_HD __host__ __device__
+#define OCTEN_DEV __device__
+#else
+#define OCTEN_HD
+#define OCTEN_DEV
+#endif
+
+namespace octen {
+
+// A "team" is the set of threads cooperating on one small problem: a CUDA
+// thread block on the device, a single thread on the host.  Team-parallel
+// routines only use tid()/size()/sync() and block-strided loops, so the
+// one-thread host instantiation executes exactly the same arithmetic.
+#if defined(__CUDACC__)
+struct TeamDev {
+    __device__ int tid() const { return (int)threadIdx.x; }
+    __device__ int size() const { return (int)blockDim.x; }
+    __device__ void sync() const { __syncthreads(); }
+};
+#endif
+struct TeamHost {
+    int tid() const { return 0; }
+    int size() const { return 1; }
+    void sync() const {}
+};
+
+// Device-side error record. Kernels that detect a reference error condition
+// write the first (lowest problem index wins) record; the host turns it into
+// the reference exception text.
+enum StatusCode : int {
+    kOk = 0,
+    kAlsNonFiniteFactor = 1,   // a = sweep, b = mode            (cp_als.cpp:305-307)
+    kAlsNonFiniteFit = 2,      // a = sweep                      (cp_als.cpp:335-336)
+    kAlignDegenerateRef = 3,   // a = mode                       (recovery.cpp:181-183)
+    kAlignDegenerateRep = 4,   // a = replica, b = mode          (recovery.cpp:253-255)
+    kAlignDegenerateScale = 5, // a = replica, b = mode          (recovery.cpp:279-281)
+    kRecoverRankDeficient = 6, // a = mode, b = rank, c = cols   (recovery.cpp:34-36)
+    kRecoverZeroColumn = 7,    //                                 (streaming.cpp:143-144)
+    kAppendRankDeficient = 8,  //                                 (recovery.cpp:398-399)
+    kAppendNonFiniteGauge = 9, //                                 (recovery.cpp:402-403)
+    kGevdFailed = 10,          // internal: GEVD init exhausted -> random fallback
+};
+
+struct DevStatus {
+    int code;
+    int problem;  // ordering key: lowest wins
+    int a, b, c;
+    double d;
+};
+
+OCTEN_HD inline double dsq(double x) { return x * x; }
+
+}  // namespace octen

@@ -1,0 +1,877 @@
+// Small dense linear algebra used inside the OCTen kernels: one problem per
+// thread block ("team"), matrices resident in shared memory.  Every routine
+// is OCTEN_HD so tests/cpu_harness can run the exact same code on the host
+// (one-thread team) against numpy.
+//
+// These replace the Eigen decompositions the reference calls on small
+// matrices (reference paths relative to /root/reference/proj):
+//   * jacobi_eig_sym      -- BDCSVD thin-U of the unfoldings (cp_als.cpp:96-100)
+//                            via the Gram eigenbasis; also the pseudo-inverse
+//                            fallback for rank-deficient COD solves
+//   * eig_real (orthes+hqr2) -- Eigen::EigenSolver on the R x R GEVD pencil
+//                            (cp_als.cpp:126-140)
+//   * lu_fullpiv_*        -- Eigen::FullPivLU isInvertible/inverse (cp_als.cpp:122-124)
+//   * chol_semidef        -- LLT / rank-revealing solves (recovery.cpp:26-38,151-173,486)
+//   * greedy_match        -- recovery.cpp:42-85
+//   * top_singular_pair   -- JacobiSVD rank-1 peel (cp_als.cpp:24-36)
+//   * Mt64                -- std::mt19937_64 for the ALS column rescue stream
+//                            (cp_als.cpp:293,311-316; rng.hpp:51-85)
+#pragma once
+
+#include "octen_common.cuh"
+
+namespace octen {
+
+// ---------------------------------------------------------------------------
+// std::mt19937_64 (published definition), 53-bit uniforms as rng.hpp:56.
+// ---------------------------------------------------------------------------
+struct Mt64 {
+    uint64_t mt[312];
+    int idx;
+
+    OCTEN_HD void seed(uint64_t s) {
+        mt[0] = s;
+        for (int i = 1; i < 312; ++i)
+            mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+        idx = 312;
+    }
+    OCTEN_HD void twist() {
+        const uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL, A = 0xB5026F5AA96619E9ULL;
+        for (int i = 0; i < 312; ++i) {
+            uint64_t x = (mt[i] & UM) | (mt[(i + 1) % 312] & LM);
+            uint64_t xa = x >> 1;
+            if (x & 1ULL) xa ^= A;
+            mt[i] = mt[(i + 156) % 312] ^ xa;
+        }
+        idx = 0;
+    }
+    OCTEN_HD uint64_t next() {
+        if (idx >= 312) twist();
+        uint64_t y = mt[idx++];
+        y ^= (y >> 29) & 0x5555555555555555ULL;
+        y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+        y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+        y ^= y >> 43;
+        return y;
+    }
+    OCTEN_HD double uniform01() { return (double)(next() >> 11) * 0x1.0p-53; }
+};
+
+OCTEN_HD inline uint64_t splitmix(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// ---------------------------------------------------------------------------
+// Greedy column matching (recovery.cpp:42-85).  sim is r x r column-major
+// with leading dimension ld; perm[ref] = cand.  Returns the number of steps
+// that saw more than one candidate within tie_tol (the reference logs these).
+// Single thread.
+// ---------------------------------------------------------------------------
+OCTEN_HD inline int greedy_match(int r, const double* sim, int ld, double tie_tol, int* perm,
+                                 unsigned char* ref_used, unsigned char* cand_used) {
+    int ambiguous = 0;
+    for (int i = 0; i < r; ++i) {
+        perm[i] = -1;
+        ref_used[i] = 0;
+        cand_used[i] = 0;
+    }
+    for (int step = 0; step < r; ++step) {
+        double best = -INFINITY;
+        for (int i = 0; i < r; ++i) {
+            if (ref_used[i]) continue;
+            for (int j = 0; j < r; ++j) {
+                if (cand_used[j]) continue;
+                const double v = sim[i + (size_t)ld * j];
+                best = v > best ? v : best;
+            }
+        }
+        int bi = -1, bj = -1, ties = 0;
+        for (int i = 0; i < r && bi < 0; ++i) {
+            if (ref_used[i]) continue;
+            for (int j = 0; j < r; ++j) {
+                if (cand_used[j]) continue;
+                if (sim[i + (size_t)ld * j] >= best - tie_tol) {
+                    bi = i;
+                    bj = j;
+                    break;
+                }
+            }
+        }
+        for (int i = 0; i < r; ++i) {
+            if (ref_used[i]) continue;
+            for (int j = 0; j < r; ++j)
+                if (!cand_used[j] && sim[i + (size_t)ld * j] >= best - tie_tol) ++ties;
+        }
+        if (ties > 1) ++ambiguous;
+        if (bi < 0) {  // NaN similarities: take the first free pair
+            for (int i = 0; i < r && bi < 0; ++i)
+                if (!ref_used[i])
+                    for (int j = 0; j < r; ++j)
+                        if (!cand_used[j]) {
+                            bi = i;
+                            bj = j;
+                            break;
+                        }
+        }
+        perm[bi] = bj;
+        ref_used[bi] = 1;
+        cand_used[bj] = 1;
+    }
+    return ambiguous;
+}
+
+// ---------------------------------------------------------------------------
+// Semi-definite Cholesky, in place, lower triangle of a column-major n x n
+// matrix.  A pivot <= tol * max_diag(A) marks the column deficient: it is
+// zeroed and skipped (exact for PSD input, whose Schur complement then has a
+// zero row/column).  Returns the numerical rank.  Single thread.
+// ---------------------------------------------------------------------------
+OCTEN_HD inline int chol_semidef(int n, double* a, int lda, double tol) {
+    double maxd = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double v = a[i + (size_t)lda * i];
+        maxd = v > maxd ? v : maxd;
+    }
+    const double thr = tol * maxd;
+    int rank = 0;
+    for (int k = 0; k < n; ++k) {
+        double d = a[k + (size_t)lda * k];
+        for (int p = 0; p < k; ++p) d -= dsq(a[k + (size_t)lda * p]);
+        if (!(d > thr) || maxd <= 0.0) {
+            for (int i = k; i < n; ++i) a[i + (size_t)lda * k] = 0.0;
+            continue;
+        }
+        ++rank;
+        const double lkk = sqrt(d);
+        a[k + (size_t)lda * k] = lkk;
+        for (int i = k + 1; i < n; ++i) {
+            double s = a[i + (size_t)lda * k];
+            for (int p = 0; p < k; ++p) s -= a[i + (size_t)lda * p] * a[k + (size_t)lda * p];
+            a[i + (size_t)lda * k] = s / lkk;
+        }
+    }
+    return rank;
+}
+
+// Solve L L^T x = b in place for one vector (full-rank factor from chol_semidef).
+OCTEN_HD inline void chol_solve_vec(int n, const double* l, int ldl, double* x, int incx) {
+    for (int i = 0; i < n; ++i) {
+        double s = x[(size_t)incx * i];
+        for (int p = 0; p < i; ++p) s -= l[i + (size_t)ldl * p] * x[(size_t)incx * p];
+        x[(size_t)incx * i] = s / l[i + (size_t)ldl * i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        double s = x[(size_t)incx * i];
+        for (int p = i + 1; p < n; ++p) s -= l[p + (size_t)ldl * i] * x[(size_t)incx * p];
+        x[(size_t)incx * i] = s / l[i + (size_t)ldl * i];
+    }
+}
+
+// Forward substitution L y = b (lower, non-unit).  Single thread.
+OCTEN_HD inline void trsv_lower(int n, const double* l, int ldl, double* x, int incx) {
+    for (int i = 0; i < n; ++i) {
+        double s = x[(size_t)incx * i];
+        for (int p = 0; p < i; ++p) s -= l[i + (size_t)ldl * p] * x[(size_t)incx * p];
+        x[(size_t)incx * i] = s / l[i + (size_t)ldl * i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Full-pivot LU (Eigen::FullPivLU semantics): rank counts pivots
+// > epsilon * n * |maxpivot|.  On return `inv` holds the inverse when the
+// matrix is invertible.  a is destroyed.  Single thread.  perm scratch: 2n ints.
+// ---------------------------------------------------------------------------
+OCTEN_HD inline bool lu_fullpiv_inverse(int n, double* a, int lda, double* inv, int ldi, int* rowp,
+                                        int* colp) {
+    double maxpiv = 0.0;
+    double piv_abs[64];
+    for (int k = 0; k < n; ++k) {
+        int bi = k, bj = k;
+        double best = -1.0;
+        for (int j = k; j < n; ++j)
+            for (int i = k; i < n; ++i) {
+                const double v = fabs(a[i + (size_t)lda * j]);
+                if (v > best) {
+                    best = v;
+                    bi = i;
+                    bj = j;
+                }
+            }
+        rowp[k] = bi;
+        colp[k] = bj;
+        if (bi != k)
+            for (int j = 0; j < n; ++j) {
+                const double t = a[k + (size_t)lda * j];
+                a[k + (size_t)lda * j] = a[bi + (size_t)lda * j];
+                a[bi + (size_t)lda * j] = t;
+            }
+        if (bj != k)
+            for (int i = 0; i < n; ++i) {
+                const double t = a[i + (size_t)lda * k];
+                a[i + (size_t)lda * k] = a[i + (size_t)lda * bj];
+                a[i + (size_t)lda * bj] = t;
+            }
+        const double p = a[k + (size_t)lda * k];
+        piv_abs[k] = fabs(p);
+        if (fabs(p) > maxpiv) maxpiv = fabs(p);
+        if (p != 0.0) {
+            for (int i = k + 1; i < n; ++i) a[i + (size_t)lda * k] /= p;
+            for (int j = k + 1; j < n; ++j) {
+                const double u = a[k + (size_t)lda * j];
+                for (int i = k + 1; i < n; ++i) a[i + (size_t)lda * j] -= a[i + (size_t)lda * k] * u;
+            }
+        }
+    }
+    const double thr = 2.220446049250313e-16 * (double)n * maxpiv;
+    int rank = 0;
+    for (int k = 0; k < n; ++k)
+        if (piv_abs[k] > thr) ++rank;
+    if (rank < n) return false;
+    // inverse: solve (P A Q) = L U  ->  A^-1 = Q U^-1 L^-1 P
+    for (int c = 0; c < n; ++c) {
+        double* x = inv + (size_t)ldi * c;
+        for (int i = 0; i < n; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+        for (int k = 0; k < n; ++k)  // apply row swaps P
+            if (rowp[k] != k) {
+                const double t = x[k];
+                x[k] = x[rowp[k]];
+                x[rowp[k]] = t;
+            }
+        for (int i = 0; i < n; ++i)  // L y = Pb (unit lower)
+            for (int p = 0; p < i; ++p) x[i] -= a[i + (size_t)lda * p] * x[p];
+        for (int i = n - 1; i >= 0; --i) {  // U z = y
+            for (int p = i + 1; p < n; ++p) x[i] -= a[i + (size_t)lda * p] * x[p];
+            x[i] /= a[i + (size_t)lda * i];
+        }
+        for (int k = n - 1; k >= 0; --k)  // undo column swaps Q
+            if (colp[k] != k) {
+                const double t = x[k];
+                x[k] = x[colp[k]];
+                x[colp[k]] = t;
+            }
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// Real nonsymmetric eigen-decomposition: Householder reduction to Hessenberg
+// form (EISPACK orthes) followed by the shifted double-step QR iteration with
+// eigenvector back-substitution (EISPACK hqr2), as in Eigen's EigenSolver
+// (RealSchur + complex back-substitution).  Eigenvalues come back as (wr, wi);
+// complex pairs are adjacent with the positive imaginary part first and their
+// eigenvector stored as [Re | Im] in columns (c, c+1) -- the layout the
+// reference turns into a_sub (cp_als.cpp:128-140).  Eigenvectors are not
+// normalized (the reference normalizes each a1 column afterwards, which makes
+// the scale irrelevant).  h and v are n x n column-major (ld n), ort is n
+// scratch.  Returns false if the QR iteration does not converge within 40n
+// steps (Eigen's maxIterations).  Single thread.
+// ---------------------------------------------------------------------------
+namespace detail {
+OCTEN_HD inline void cdiv(double xr, double xi, double yr, double yi, double& cr, double& ci) {
+    double r, d;
+    if (fabs(yr) > fabs(yi)) {
+        r = yi / yr;
+        d = yr + r * yi;
+        cr = (xr + r * xi) / d;
+        ci = (xi - r * xr) / d;
+    } else {
+        r = yr / yi;
+        d = yi + r * yr;
+        cr = (r * xr + xi) / d;
+        ci = (r * xi - xr) / d;
+    }
+}
+}  // namespace detail
+
+OCTEN_HD inline bool eig_real(int nn, double* hm, double* vm, double* wr, double* wi, double* ort) {
+#define H_(i, j) hm[(i) + (size_t)nn * (j)]
+#define V_(i, j) vm[(i) + (size_t)nn * (j)]
+    const int low = 0, high = nn - 1;
+    // --- orthes ---
+    for (int m = low + 1; m <= high - 1; ++m) {
+        double scale = 0.0;
+        for (int i = m; i <= high; ++i) scale += fabs(H_(i, m - 1));
+        if (scale != 0.0) {
+            double h = 0.0;
+            for (int i = high; i >= m; --i) {
+                ort[i] = H_(i, m - 1) / scale;
+                h += ort[i] * ort[i];
+            }
+            double g = sqrt(h);
+            if (ort[m] > 0) g = -g;
+            h = h - ort[m] * g;
+            ort[m] = ort[m] - g;
+            for (int j = m; j < nn; ++j) {
+                double f = 0.0;
+                for (int i = high; i >= m; --i) f += ort[i] * H_(i, j);
+                f = f / h;
+                for (int i = m; i <= high; ++i) H_(i, j) -= f * ort[i];
+            }
+            for (int i = 0; i <= high; ++i) {
+                double f = 0.0;
+                for (int j = high; j >= m; --j) f += ort[j] * H_(i, j);
+                f = f / h;
+                for (int j = m; j <= high; ++j) H_(i, j) -= f * ort[j];
+            }
+            ort[m] = scale * ort[m];
+            H_(m, m - 1) = scale * g;
+        }
+    }
+    for (int i = 0; i < nn; ++i)
+        for (int j = 0; j < nn; ++j) V_(i, j) = (i == j) ? 1.0 : 0.0;
+    for (int m = high - 1; m >= low + 1; --m) {
+        if (H_(m, m - 1) != 0.0) {
+            for (int i = m + 1; i <= high; ++i) ort[i] = H_(i, m - 1);
+            for (int j = m; j <= high; ++j) {
+                double g = 0.0;
+                for (int i = m; i <= high; ++i) g += ort[i] * V_(i, j);
+                g = (g / ort[m]) / H_(m, m - 1);
+                for (int i = m; i <= high; ++i) V_(i, j) += g * ort[i];
+            }
+        }
+    }
+    // --- hqr2 ---
+    int n = nn - 1;
+    const double eps = 2.220446049250313e-16;
+    double exshift = 0.0, p = 0, q = 0, r = 0, s = 0, z = 0, t, w, x, y;
+    double norm = 0.0;
+    for (int i = 0; i < nn; ++i) {
+        if (i < low || i > high) {
+            wr[i] = H_(i, i);
+            wi[i] = 0.0;
+        }
+        for (int j = (i - 1 > 0 ? i - 1 : 0); j < nn; ++j) norm += fabs(H_(i, j));
+    }
+    int iter = 0, total_iter = 0;
+    const int max_total = 40 * nn;
+    while (n >= low) {
+        int l = n;
+        while (l > low) {
+            s = fabs(H_(l - 1, l - 1)) + fabs(H_(l, l));
+            if (s == 0.0) s = norm;
+            if (fabs(H_(l, l - 1)) < eps * s) break;
+            l--;
+        }
+        if (l == n) {
+            H_(n, n) = H_(n, n) + exshift;
+            wr[n] = H_(n, n);
+            wi[n] = 0.0;
+            n--;
+            iter = 0;
+        } else if (l == n - 1) {
+            w = H_(n, n - 1) * H_(n - 1, n);
+            p = (H_(n - 1, n - 1) - H_(n, n)) / 2.0;
+            q = p * p + w;
+            z = sqrt(fabs(q));
+            H_(n, n) = H_(n, n) + exshift;
+            H_(n - 1, n - 1) = H_(n - 1, n - 1) + exshift;
+            x = H_(n, n);
+            if (q >= 0) {
+                z = (p >= 0) ? p + z : p - z;
+                wr[n - 1] = x + z;
+                wr[n] = wr[n - 1];
+                if (z != 0.0) wr[n] = x - w / z;
+                wi[n - 1] = 0.0;
+                wi[n] = 0.0;
+                x = H_(n, n - 1);
+                s = fabs(x) + fabs(z);
+                p = x / s;
+                q = z / s;
+                r = sqrt(p * p + q * q);
+                p = p / r;
+                q = q / r;
+                for (int j = n - 1; j < nn; ++j) {
+                    z = H_(n - 1, j);
+                    H_(n - 1, j) = q * z + p * H_(n, j);
+                    H_(n, j) = q * H_(n, j) - p * z;
+                }
+                for (int i = 0; i <= n; ++i) {
+                    z = H_(i, n - 1);
+                    H_(i, n - 1) = q * z + p * H_(i, n);
+                    H_(i, n) = q * H_(i, n) - p * z;
+                }
+                for (int i = low; i <= high; ++i) {
+                    z = V_(i, n - 1);
+                    V_(i, n - 1) = q * z + p * V_(i, n);
+                    V_(i, n) = q * V_(i, n) - p * z;
+                }
+            } else {
+                wr[n - 1] = x + p;
+                wr[n] = x + p;
+                wi[n - 1] = z;
+                wi[n] = -z;
+            }
+            n = n - 2;
+            iter = 0;
+        } else {
+            x = H_(n, n);
+            y = 0.0;
+            w = 0.0;
+            if (l < n) {
+                y = H_(n - 1, n - 1);
+                w = H_(n, n - 1) * H_(n - 1, n);
+            }
+            if (iter == 10) {
+                exshift += x;
+                for (int i = low; i <= n; ++i) H_(i, i) -= x;
+                s = fabs(H_(n, n - 1)) + fabs(H_(n - 1, n - 2));
+                x = y = 0.75 * s;
+                w = -0.4375 * s * s;
+            }
+            if (iter == 30) {
+                s = (y - x) / 2.0;
+                s = s * s + w;
+                if (s > 0) {
+                    s = sqrt(s);
+                    if (y < x) s = -s;
+                    s = x - w / ((y - x) / 2.0 + s);
+                    for (int i = low; i <= n; ++i) H_(i, i) -= s;
+                    exshift += s;
+                    x = y = w = 0.964;
+                }
+            }
+            iter = iter + 1;
+            if (++total_iter > max_total) return false;
+            int m = n - 2;
+            while (m >= l) {
+                z = H_(m, m);
+                r = x - z;
+                s = y - z;
+                p = (r * s - w) / H_(m + 1, m) + H_(m, m + 1);
+                q = H_(m + 1, m + 1) - z - r - s;
+                r = H_(m + 2, m + 1);
+                s = fabs(p) + fabs(q) + fabs(r);
+                p = p / s;
+                q = q / s;
+                r = r / s;
+                if (m == l) break;
+                if (fabs(H_(m, m - 1)) * (fabs(q) + fabs(r)) <
+                    eps * (fabs(p) * (fabs(H_(m - 1, m - 1)) + fabs(z) + fabs(H_(m + 1, m + 1)))))
+                    break;
+                m--;
+            }
+            for (int i = m + 2; i <= n; ++i) {
+                H_(i, i - 2) = 0.0;
+                if (i > m + 2) H_(i, i - 3) = 0.0;
+            }
+            for (int k = m; k <= n - 1; ++k) {
+                const bool notlast = (k != n - 1);
+                if (k != m) {
+                    p = H_(k, k - 1);
+                    q = H_(k + 1, k - 1);
+                    r = notlast ? H_(k + 2, k - 1) : 0.0;
+                    x = fabs(p) + fabs(q) + fabs(r);
+                    if (x == 0.0) continue;
+                    p = p / x;
+                    q = q / x;
+                    r = r / x;
+                }
+                s = sqrt(p * p + q * q + r * r);
+                if (p < 0) s = -s;
+                if (s != 0) {
+                    if (k != m)
+                        H_(k, k - 1) = -s * x;
+                    else if (l != m)
+                        H_(k, k - 1) = -H_(k, k - 1);
+                    p = p + s;
+                    x = p / s;
+                    y = q / s;
+                    z = r / s;
+                    q = q / p;
+                    r = r / p;
+                    for (int j = k; j < nn; ++j) {
+                        p = H_(k, j) + q * H_(k + 1, j);
+                        if (notlast) {
+                            p = p + r * H_(k + 2, j);
+                            H_(k + 2, j) = H_(k + 2, j) - p * z;
+                        }
+                        H_(k, j) = H_(k, j) - p * x;
+                        H_(k + 1, j) = H_(k + 1, j) - p * y;
+                    }
+                    const int imax = (n < k + 3) ? n : k + 3;
+                    for (int i = 0; i <= imax; ++i) {
+                        p = x * H_(i, k) + y * H_(i, k + 1);
+                        if (notlast) {
+                            p = p + z * H_(i, k + 2);
+                            H_(i, k + 2) = H_(i, k + 2) - p * r;
+                        }
+                        H_(i, k) = H_(i, k) - p;
+                        H_(i, k + 1) = H_(i, k + 1) - p * q;
+                    }
+                    for (int i = low; i <= high; ++i) {
+                        p = x * V_(i, k) + y * V_(i, k + 1);
+                        if (notlast) {
+                            p = p + z * V_(i, k + 2);
+                            V_(i, k + 2) = V_(i, k + 2) - p * r;
+                        }
+                        V_(i, k) = V_(i, k) - p;
+                        V_(i, k + 1) = V_(i, k + 1) - p * q;
+                    }
+                }
+            }
+        }
+    }
+    // back-substitution
+    if (norm == 0.0) return true;
+    for (n = nn - 1; n >= 0; n--) {
+        p = wr[n];
+        q = wi[n];
+        if (q == 0) {
+            int l = n;
+            H_(n, n) = 1.0;
+            for (int i = n - 1; i >= 0; i--) {
+                w = H_(i, i) - p;
+                r = 0.0;
+                for (int j = l; j <= n; j++) r = r + H_(i, j) * H_(j, n);
+                if (wi[i] < 0.0) {
+                    z = w;
+                    s = r;
+                } else {
+                    l = i;
+                    if (wi[i] == 0.0) {
+                        if (w != 0.0)
+                            H_(i, n) = -r / w;
+                        else
+                            H_(i, n) = -r / (eps * norm);
+                    } else {
+                        x = H_(i, i + 1);
+                        y = H_(i + 1, i);
+                        q = (wr[i] - p) * (wr[i] - p) + wi[i] * wi[i];
+                        t = (x * s - z * r) / q;
+                        H_(i, n) = t;
+                        if (fabs(x) > fabs(z))
+                            H_(i + 1, n) = (-r - w * t) / x;
+                        else
+                            H_(i + 1, n) = (-s - y * t) / z;
+                    }
+                    t = fabs(H_(i, n));
+                    if ((eps * t) * t > 1)
+                        for (int j = i; j <= n; j++) H_(j, n) = H_(j, n) / t;
+                }
+            }
+        } else if (q < 0) {
+            int l = n - 1;
+            double cr, ci;
+            if (fabs(H_(n, n - 1)) > fabs(H_(n - 1, n))) {
+                H_(n - 1, n - 1) = q / H_(n, n - 1);
+                H_(n - 1, n) = -(H_(n, n) - p) / H_(n, n - 1);
+            } else {
+                detail::cdiv(0.0, -H_(n - 1, n), H_(n - 1, n - 1) - p, q, cr, ci);
+                H_(n - 1, n - 1) = cr;
+                H_(n - 1, n) = ci;
+            }
+            H_(n, n - 1) = 0.0;
+            H_(n, n) = 1.0;
+            for (int i = n - 2; i >= 0; i--) {
+                double ra = 0.0, sa = 0.0, vr, vi;
+                for (int j = l; j <= n; j++) {
+                    ra = ra + H_(i, j) * H_(j, n - 1);
+                    sa = sa + H_(i, j) * H_(j, n);
+                }
+                w = H_(i, i) - p;
+                if (wi[i] < 0.0) {
+                    z = w;
+                    r = ra;
+                    s = sa;
+                } else {
+                    l = i;
+                    if (wi[i] == 0) {
+                        detail::cdiv(-ra, -sa, w, q, cr, ci);
+                        H_(i, n - 1) = cr;
+                        H_(i, n) = ci;
+                    } else {
+                        x = H_(i, i + 1);
+                        y = H_(i + 1, i);
+                        vr = (wr[i] - p) * (wr[i] - p) + wi[i] * wi[i] - q * q;
+                        vi = (wr[i] - p) * 2.0 * q;
+                        if (vr == 0.0 && vi == 0.0)
+                            vr = eps * norm * (fabs(w) + fabs(q) + fabs(x) + fabs(y) + fabs(z));
+                        detail::cdiv(x * r - z * ra + q * sa, x * s - z * sa - q * ra, vr, vi, cr, ci);
+                        H_(i, n - 1) = cr;
+                        H_(i, n) = ci;
+                        if (fabs(x) > (fabs(z) + fabs(q))) {
+                            H_(i + 1, n - 1) = (-ra - w * H_(i, n - 1) + q * H_(i, n)) / x;
+                            H_(i + 1, n) = (-sa - w * H_(i, n) - q * H_(i, n - 1)) / x;
+                        } else {
+                            detail::cdiv(-r - y * H_(i, n - 1), -s - y * H_(i, n), z, q, cr, ci);
+                            H_(i + 1, n - 1) = cr;
+                            H_(i + 1, n) = ci;
+                        }
+                    }
+                    t = fmax(fabs(H_(i, n - 1)), fabs(H_(i, n)));
+                    if ((eps * t) * t > 1)
+                        for (int j = i; j <= n; j++) {
+                            H_(j, n - 1) = H_(j, n - 1) / t;
+                            H_(j, n) = H_(j, n) / t;
+                        }
+                }
+            }
+        }
+    }
+    for (int j = nn - 1; j >= low; j--)
+        for (int i = low; i <= high; i++) {
+            z = 0.0;
+            const int kmax = j < high ? j : high;
+            for (int k = low; k <= kmax; k++) z = z + V_(i, k) * H_(k, j);
+            V_(i, j) = z;
+        }
+    return true;
+#undef H_
+#undef V_
+}
+
+// ---------------------------------------------------------------------------
+// Team-parallel cyclic Jacobi eigen-decomposition of a symmetric n x n matrix
+// held column-major (ld n) in `a` (shared memory on the device).  Rotations
+// of one round-robin round act on disjoint index pairs, so every 2x2 block of
+// A' = G^T A G and every row pair of V' = V G updates independently.  On
+// return the diagonal of `a` holds the eigenvalues and the columns of `v`
+// (ld n) the eigenvectors.  scratch: 2*(n+1) doubles + 1 int (shared).
+// ---------------------------------------------------------------------------
+template <class Team>
+OCTEN_HD void jacobi_eig_sym(const Team& team, int n, double* a, double* v, double* cs, int* flag,
+                             int max_sweeps = 40) {
+    const int m = (n % 2) ? n + 1 : n;  // padded player count (index n is a dummy)
+    const int half = m / 2;
+    for (int idx = team.tid(); idx < n * n; idx += team.size())
+        v[idx] = ((idx % n) == (idx / n)) ? 1.0 : 0.0;
+    team.sync();
+    double* cc = cs;
+    double* ss = cs + half;
+    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+        if (team.tid() == 0) *flag = 0;
+        team.sync();
+        for (int round = 0; round < m - 1; ++round) {
+            // pair k: k==0 -> (round, m-1); else ((round+k) % (m-1), (round-k+m-1) % (m-1))
+            for (int k = team.tid(); k < half; k += team.size()) {
+                int p, q;
+                if (k == 0) {
+                    p = round;
+                    q = m - 1;
+                } else {
+                    p = (round + k) % (m - 1);
+                    q = (round - k + m - 1) % (m - 1);
+                }
+                if (p > q) {
+                    const int tt = p;
+                    p = q;
+                    q = tt;
+                }
+                double c = 1.0, s = 0.0;
+                if (q < n) {
+                    const double apq = a[p + n * q];
+                    const double app = a[p + n * p], aqq = a[q + n * q];
+                    if (fabs(apq) > 1e-300 && fabs(apq) > 1e-17 * sqrt(fabs(app) * fabs(aqq))) {
+                        const double theta = (aqq - app) / (2.0 * apq);
+                        double t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
+                        if (theta < 0.0) t = -t;
+                        c = 1.0 / sqrt(t * t + 1.0);
+                        s = t * c;
+                        *flag = 1;
+                    }
+                }
+                cc[k] = c;
+                ss[k] = s;
+            }
+            team.sync();
+            // A' = G^T A G on 2x2 blocks (pair k1 rows, pair k2 cols)
+            for (int blk = team.tid(); blk < half * half; blk += team.size()) {
+                const int k1 = blk % half, k2 = blk / half;
+                int p1, q1, p2, q2;
+                if (k1 == 0) {
+                    p1 = round;
+                    q1 = m - 1;
+                } else {
+                    p1 = (round + k1) % (m - 1);
+                    q1 = (round - k1 + m - 1) % (m - 1);
+                }
+                if (p1 > q1) {
+                    const int tt = p1;
+                    p1 = q1;
+                    q1 = tt;
+                }
+                if (k2 == 0) {
+                    p2 = round;
+                    q2 = m - 1;
+                } else {
+                    p2 = (round + k2) % (m - 1);
+                    q2 = (round - k2 + m - 1) % (m - 1);
+                }
+                if (p2 > q2) {
+                    const int tt = p2;
+                    p2 = q2;
+                    q2 = tt;
+                }
+                const double c1 = cc[k1], s1 = ss[k1], c2 = cc[k2], s2 = ss[k2];
+                if (q1 < n && q2 < n) {
+                    const double b00 = a[p1 + n * p2], b01 = a[p1 + n * q2];
+                    const double b10 = a[q1 + n * p2], b11 = a[q1 + n * q2];
+                    // rows: r_p = c1 b_p - s1 b_q ; r_q = s1 b_p + c1 b_q
+                    const double r00 = c1 * b00 - s1 * b10, r01 = c1 * b01 - s1 * b11;
+                    const double r10 = s1 * b00 + c1 * b10, r11 = s1 * b01 + c1 * b11;
+                    // cols: c_p = c2 r_p - s2 r_q ; c_q = s2 r_p + c2 r_q
+                    double n00 = c2 * r00 - s2 * r01, n01 = s2 * r00 + c2 * r01;
+                    double n10 = c2 * r10 - s2 * r11, n11 = s2 * r10 + c2 * r11;
+                    if (k1 == k2 && s1 != 0.0) {
+                        // diagonal block: exact annihilation, NR-style diagonal update
+                        const double t = s1 / c1;
+                        n00 = b00 - t * b01;
+                        n11 = b11 + t * b01;
+                        n01 = 0.0;
+                        n10 = 0.0;
+                    }
+                    a[p1 + n * p2] = n00;
+                    a[p1 + n * q2] = n01;
+                    a[q1 + n * p2] = n10;
+                    a[q1 + n * q2] = n11;
+                } else if (q1 < n) {  // column pair is the dummy: rows only on real column p2
+                    const double b0 = a[p1 + n * p2], b1 = a[q1 + n * p2];
+                    a[p1 + n * p2] = c1 * b0 - s1 * b1;
+                    a[q1 + n * p2] = s1 * b0 + c1 * b1;
+                } else if (q2 < n) {  // row pair is the dummy: columns only on real row p1
+                    const double b0 = a[p1 + n * p2], b1 = a[p1 + n * q2];
+                    a[p1 + n * p2] = c2 * b0 - s2 * b1;
+                    a[p1 + n * q2] = s2 * b0 + c2 * b1;
+                }
+            }
+            // V' = V G : columns (p,q) of every row
+            for (int e = team.tid(); e < n * half; e += team.size()) {
+                const int row = e % n, k = e / n;
+                int p, q;
+                if (k == 0) {
+                    p = round;
+                    q = m - 1;
+                } else {
+                    p = (round + k) % (m - 1);
+                    q = (round - k + m - 1) % (m - 1);
+                }
+                if (p > q) {
+                    const int tt = p;
+                    p = q;
+                    q = tt;
+                }
+                if (q >= n) continue;
+                const double c = cc[k], s = ss[k];
+                const double vp = v[row + n * p], vq = v[row + n * q];
+                v[row + n * p] = c * vp - s * vq;
+                v[row + n * q] = s * vp + c * vq;
+            }
+            team.sync();
+        }
+        const int any = *flag;
+        team.sync();
+        if (!any) break;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Top singular triplet of an m x n matrix (column-major, ld m) by power
+// iteration on A^T A: returns sigma, u (m), v (n) with A v = sigma u.  Stops
+// when the right vector moves by <= 1e-14 or after max_iter.
+// Replaces the rank-1 JacobiSVD peel (cp_als.cpp:24-36).  Team-parallel;
+// scratch `red` (shared): team.size() + 2 + n doubles.
+// ---------------------------------------------------------------------------
+template <class Team>
+OCTEN_HD double team_reduce_sum(const Team& team, double v, double* red) {
+    // deterministic: every thread writes, thread 0 sums in index order
+    red[team.tid()] = v;
+    team.sync();
+    if (team.tid() == 0) {
+        double s = 0.0;
+        for (int i = 0; i < team.size(); ++i) s += red[i];
+        red[team.size()] = s;
+    }
+    team.sync();
+    const double out = red[team.size()];
+    team.sync();
+    return out;
+}
+
+template <class Team>
+OCTEN_HD double top_singular_pair(const Team& team, int m, int n, const double* a, double* u, double* v,
+                                  double* red, int max_iter = 500) {
+    // start: the row of A with the largest norm (transposed)
+    if (team.tid() == 0) {
+        int best = 0;
+        double bn = -1.0;
+        for (int i = 0; i < m; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < n; ++j) s += dsq(a[i + (size_t)m * j]);
+            if (s > bn) {
+                bn = s;
+                best = i;
+            }
+        }
+        red[team.size() + 1] = (double)best;
+    }
+    team.sync();
+    const int row = (int)red[team.size() + 1];
+    team.sync();
+    double loc = 0.0;
+    for (int j = team.tid(); j < n; j += team.size()) {
+        v[j] = a[row + (size_t)m * j];
+        loc += v[j] * v[j];
+    }
+    double vn = sqrt(team_reduce_sum(team, loc, red));
+    if (vn == 0.0) {
+        for (int i = team.tid(); i < m; i += team.size()) u[i] = 0.0;
+        team.sync();
+        return 0.0;
+    }
+    for (int j = team.tid(); j < n; j += team.size()) v[j] /= vn;
+    team.sync();
+    double sigma = 0.0;
+    for (int it = 0; it < max_iter; ++it) {
+        // u = A v / |A v|
+        loc = 0.0;
+        for (int i = team.tid(); i < m; i += team.size()) {
+            double s = 0.0;
+            for (int j = 0; j < n; ++j) s += a[i + (size_t)m * j] * v[j];
+            u[i] = s;
+            loc += s * s;
+        }
+        sigma = sqrt(team_reduce_sum(team, loc, red));
+        if (sigma == 0.0) break;
+        for (int i = team.tid(); i < m; i += team.size()) u[i] /= sigma;
+        team.sync();
+        // w = A^T u ; v_new = w / |w| ; diff = |v_new - v|
+        double l2 = 0.0;
+        for (int j = team.tid(); j < n; j += team.size()) {
+            double s = 0.0;
+            for (int i = 0; i < m; ++i) s += a[i + (size_t)m * j] * u[i];
+            red[team.size() + 2 + j] = s;  // staged in the tail of red (size >= size+2+n)
+            l2 += s * s;
+        }
+        const double wn = sqrt(team_reduce_sum(team, l2, red));
+        loc = 0.0;
+        for (int j = team.tid(); j < n; j += team.size()) {
+            const double nv = red[team.size() + 2 + j] / wn;
+            loc += dsq(nv - v[j]);
+            v[j] = nv;
+        }
+        const double diff = sqrt(team_reduce_sum(team, loc, red));
+        if (diff <= 1e-14) {
+            sigma = wn;  // |A^T u| = sigma at convergence
+            break;
+        }
+        sigma = wn;
+    }
+    // final consistent pair: u = A v / sigma
+    loc = 0.0;
+    for (int i = team.tid(); i < m; i += team.size()) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) s += a[i + (size_t)m * j] * v[j];
+        u[i] = s;
+        loc += s * s;
+    }
+    sigma = sqrt(team_reduce_sum(team, loc, red));
+    if (sigma > 0.0)
+        for (int i = team.tid(); i < m; i += team.size()) u[i] /= sigma;
+    team.sync();
+    return sigma;
+}
+
+}  // namespace octen

@@ -1,0 +1,429 @@
+// Host orchestrator of the per-batch pipeline: init_stream / ingest_batch
+// (reference proj/src/streaming.cpp:181-346) over device-resident state.
+//
+// Host work is limited to what the reference's determinism contract pins to
+// the host: the seeded projection draws (gen_replicas / extend_temporal,
+// compression.cpp:22-99) and the stage sequencing.  Summaries Y_p, history
+// accumulators M_p, the model factors and every contraction/solve live on the
+// device.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "errors.hpp"
+#include "rng_host.hpp"
+#include "stream.hpp"
+
+namespace octen {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double seconds_since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+__global__ void nonfinite_f32_kernel(const float* x, size_t n, int* flag) {
+    int bad = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        if (!isfinite(x[i])) bad = 1;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+__global__ void nonfinite_f64_kernel(const double* x, size_t n, int* flag) {
+    int bad = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        if (!isfinite(x[i])) bad = 1;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+// C_raw = C * diag(lambda) for the first K rows (ld = cap)
+__global__ void scale_cols_kernel(double* C, long long K, long long cap, int R, const double* lam) {
+    const size_t total = (size_t)K * R;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const long long k = (long long)(e % K);
+        const int r = (int)(e / K);
+        C[k + (size_t)cap * r] *= lam[r];
+    }
+}
+// append t new rows (t x R col-major) at row offset K of C (ld = cap)
+__global__ void append_rows_kernel(double* C, long long K, long long cap, int R, const double* rows, long long t) {
+    const size_t total = (size_t)t * R;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const long long k = (long long)(e % t);
+        const int r = (int)(e / t);
+        C[(K + k) + (size_t)cap * r] = rows[k + (size_t)t * r];
+    }
+}
+// KruskalModel::normalize over (A, B, C) for column r (cp_als.cpp:216-228).
+__global__ void normalize_model_kernel(double* A, long long I, double* B, long long J, double* C, long long K,
+                                       long long capC, double* lam) {
+    __shared__ double red[256];
+    const int r = blockIdx.x;
+    double l = 1.0;
+    for (int f = 0; f < 3; ++f) {
+        double* col = f == 0 ? A + (size_t)I * r : (f == 1 ? B + (size_t)J * r : C + (size_t)capC * r);
+        const long long n = f == 0 ? I : (f == 1 ? J : K);
+        double s = 0.0;
+        for (long long i = threadIdx.x; i < n; i += blockDim.x) s += col[i] * col[i];
+        red[threadIdx.x] = s;
+        __syncthreads();
+        for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+            if ((int)threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+            __syncthreads();
+        }
+        const double nrm = sqrt(red[0]);
+        __syncthreads();
+        if (nrm > 0.0) {
+            for (long long i = threadIdx.x; i < n; i += blockDim.x) col[i] /= nrm;
+            l *= nrm;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) lam[r] = l;
+}
+
+int grid1d(size_t n) {
+    size_t b = (n + 255) / 256;
+    if (b > 148 * 8) b = 148 * 8;
+    return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+Stream::Stream(const StreamCfg& c) : cfg(c) {
+    OCTEN_CUDA(cudaSetDevice(cfg.device));
+    OCTEN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    OCTEN_CUDA(cudaEventCreate(&ev0));
+    OCTEN_CUDA(cudaEventCreate(&ev1));
+}
+
+Stream::~Stream() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (st) cudaStreamDestroy(st);
+}
+
+void Stream::validate(int order) {
+    // streaming.cpp:23-34
+    if (order < 3) throw ConfigError("stream: tensor order must be >= 3");
+    if (cfg.rank < 1) throw ConfigError("stream: rank must be >= 1");
+    if (cfg.p < 1) throw ConfigError("stream: p must be >= 1");
+    if (cfg.q < 1) throw ConfigError("stream: Q must be >= 1");
+    if (cfg.shared < 0 || cfg.shared >= cfg.q) throw ConfigError("stream: shared must lie in [0, Q)");
+    if (cfg.temporal_mode >= order) throw ConfigError("stream: temporal mode out of range");
+    if (cfg.p >= 2 && cfg.shared < 1) throw ConfigError("stream: alignment across replicas needs shared >= 1");
+    if (order != 3 || cfg.temporal_mode != 2)
+        throw ConfigError("octen: the device path supports order-3 streams with the temporal mode last");
+}
+
+void Stream::gen_replicas() {
+    // compression.cpp:22-70 (host RNG, bit-exact draws)
+    const int P = cfg.p, Q = cfg.q, sh = cfg.shared;
+    const std::int64_t dimv[2] = {I, J};
+    std::vector<double>* dst[2] = {&hU, &hV};
+    for (int m = 0; m < 2; ++m) {
+        const std::int64_t d = dimv[m];
+        std::vector<double> shared_block((size_t)d * sh);
+        rng::Substream s(rng::derive(cfg.seed, {rng::kNontemporalShared, (std::uint64_t)m}));
+        s.fill_uniform(shared_block.data(), d, sh, d);
+        dst[m]->assign((size_t)P * d * Q, 0.0);
+        for (int r = 0; r < P; ++r) {
+            double* mat = dst[m]->data() + (size_t)r * d * Q;
+            for (size_t i = 0; i < shared_block.size(); ++i) mat[i] = shared_block[i];
+            if (Q > sh) {
+                rng::Substream s2(
+                    rng::derive(cfg.seed, {rng::kNontemporalPrivate, (std::uint64_t)m, (std::uint64_t)r}));
+                s2.fill_uniform(mat + (size_t)d * sh, d, Q - sh, d);
+            }
+        }
+    }
+    tgram.assign((size_t)sh * sh, 0.0);
+    batches_drawn = 0;
+}
+
+void Stream::extend_temporal(std::int64_t t_new) {
+    // compression.cpp:72-99
+    const int P = cfg.p, Q = cfg.q, sh = cfg.shared;
+    const std::uint64_t key = (std::uint64_t)batches_drawn;
+    std::vector<double> shared_rows((size_t)t_new * sh);
+    {
+        rng::Substream s(rng::derive(cfg.seed, {rng::kTemporalShared, key}));
+        s.fill_uniform(shared_rows.data(), t_new, sh, t_new);
+    }
+    for (int i = 0; i < sh; ++i)
+        for (int j = 0; j < sh; ++j) {
+            double acc = 0.0;
+            for (std::int64_t k = 0; k < t_new; ++k)
+                acc += shared_rows[k + (size_t)t_new * i] * shared_rows[k + (size_t)t_new * j];
+            tgram[i + (size_t)sh * j] += acc;
+        }
+    hW.assign((size_t)P * t_new * Q, 0.0);
+    for (int r = 0; r < P; ++r) {
+        double* w = hW.data() + (size_t)r * t_new * Q;
+        for (size_t i = 0; i < shared_rows.size(); ++i) w[i] = shared_rows[i];
+        if (Q > sh) {
+            rng::Substream s2(rng::derive(cfg.seed, {rng::kTemporalPrivate, key, (std::uint64_t)r}));
+            s2.fill_uniform(w + (size_t)t_new * sh, t_new, Q - sh, t_new);
+        }
+    }
+    dW.upload(hW.data(), hW.size(), st);
+    ++batches_drawn;
+}
+
+const void* Stream::stage_input(const void* data, int dtype, int location, size_t n) {
+    if (location == 1) return data;
+    if (dtype == 1) {
+        X32.reserve(n);
+        OCTEN_CUDA(cudaMemcpyAsync(X32.p, data, n * sizeof(float), cudaMemcpyHostToDevice, st));
+        return X32.p;
+    }
+    X64.reserve(n);
+    OCTEN_CUDA(cudaMemcpyAsync(X64.p, data, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    return X64.p;
+}
+
+void Stream::check_finite(const void* dX, int dtype, size_t n) {
+    flag.reserve(1);
+    flag.zero(1, st);
+    if (dtype == 1)
+        nonfinite_f32_kernel<<<grid1d(n), 256, 0, st>>>((const float*)dX, n, flag.p);
+    else
+        nonfinite_f64_kernel<<<grid1d(n), 256, 0, st>>>((const double*)dX, n, flag.p);
+    OCTEN_CUDA(cudaGetLastError());
+    if (flag.to_host(1, st)[0]) throw NumericError("DenseTensor: non-finite value");
+}
+
+void Stream::compress_stage(const void* dX, int dtype, std::int64_t t) {
+    if (dtype == 1)
+        comp.compress_f32((const float*)dX, t, dW.p, Y.p, st);
+    else
+        comp.compress_f64((const double*)dX, t, dW.p, Y.p, st);
+    ++batches_seen;
+}
+
+void Stream::als_stage(std::int64_t batch_index) {
+    std::vector<std::uint64_t> seeds(cfg.p);
+    for (int r = 0; r < cfg.p; ++r)
+        seeds[r] = rng::derive(cfg.seed, {rng::kStreamAls, (std::uint64_t)r, (std::uint64_t)batch_index});
+    als.run(cfg.p, cfg.als_n_restarts, cfg.q, cfg.rank, cfg.als_max_iters, cfg.als_rel_tol, Y.p, seeds, st);
+}
+
+void Stream::ensure_c_capacity(std::int64_t rows) {
+    if (rows <= capC && C.p) return;
+    std::int64_t cap = std::max<std::int64_t>(capC * 2, rows);
+    cap = std::max<std::int64_t>(cap, 64);
+    DevBuf<double> nc;
+    nc.reserve((size_t)cap * cfg.rank);
+    if (C.p && K > 0)
+        OCTEN_CUDA(cudaMemcpy2DAsync(nc.p, cap * sizeof(double), C.p, capC * sizeof(double), K * sizeof(double),
+                                     cfg.rank, cudaMemcpyDeviceToDevice, st));
+    OCTEN_CUDA(cudaStreamSynchronize(st));
+    std::swap(C.p, nc.p);
+    std::swap(C.n, nc.n);
+    capC = cap;
+}
+
+void Stream::recover_stage(std::int64_t t_new, bool first, BatchRecordC& rec) {
+    AlignResultHost ar;
+    merge.align(als.Mf.p, als.Mlam.p, tgram, st, &ar);
+    rec.min_match_similarity = ar.min_match;
+    rec.max_offdiag_similarity = ar.max_offdiag;
+    const int R = cfg.rank;
+    Anew.reserve((size_t)I * R);
+    Bnew.reserve((size_t)J * R);
+    rows.reserve((size_t)t_new * R);
+    double residual = 0.0;
+    merge.recover(Y.p, dW.p, t_new, hist.p, first ? nullptr : A.p, first ? nullptr : B.p, Anew.p, Bnew.p, rows.p,
+                  &residual, st);
+    rec.temporal_residual = residual;
+    rec.warned = residual > cfg.residual_warning ? 1 : 0;
+    if (rec.warned && cfg.strict) {
+        if (first)
+            throw NumericError("init_stream: temporal solve residual " + std::to_string(residual) +
+                               " exceeds strict threshold");
+        throw NumericError("temporal solve residual " + std::to_string(residual) + " exceeds strict threshold");
+    }
+    // assemble_model (streaming.cpp:162-177): C_raw = [C diag(lambda); rows]
+    ensure_c_capacity(K + t_new);
+    if (!first && K > 0) scale_cols_kernel<<<grid1d((size_t)K * R), 256, 0, st>>>(C.p, K, capC, R, lam.p);
+    append_rows_kernel<<<grid1d((size_t)t_new * R), 256, 0, st>>>(C.p, K, capC, R, rows.p, t_new);
+    std::swap(A.p, Anew.p);
+    std::swap(A.n, Anew.n);
+    std::swap(B.p, Bnew.p);
+    std::swap(B.n, Bnew.n);
+    normalize_model_kernel<<<R, 256, 0, st>>>(A.p, I, B.p, J, C.p, K + t_new, capC, lam.p);
+    OCTEN_CUDA(cudaGetLastError());
+    K += t_new;
+}
+
+void Stream::init(const void* data, int dtype, int location, int order, const std::int64_t* dims) {
+    if (cfg.temporal_mode < 0) cfg.temporal_mode = order - 1;
+    validate(order);
+    const std::int64_t t0 = dims[2];
+    if (t0 < 1) throw ConfigError("init_stream: first batch has no temporal extent");
+    I = dims[0];
+    J = dims[1];
+    if (cfg.enforce_bounds) {
+        // replica_bound_nmode (recovery.cpp:548-557) and kruskal_check (recovery.cpp:531-541)
+        if (cfg.q <= cfg.shared) throw ConfigError("replica_bound: requires Q > shared");
+        double worst = (double)(I - cfg.shared) / (double)(cfg.q - cfg.shared);
+        worst = std::max(worst, (double)J / cfg.q);
+        worst = std::max(worst, (double)t0 / cfg.q);
+        const std::int64_t need = (std::int64_t)std::ceil(worst);
+        if (cfg.p < need)
+            throw ConfigError("init_stream: p=" + std::to_string(cfg.p) + " below the replica bound; need p >= " +
+                              std::to_string(need));
+        long sum = 0;
+        for (int n = 0; n < 3; ++n) sum += std::min<std::int64_t>(cfg.q, std::min<std::int64_t>(dims[n], cfg.rank));
+        if (sum < 2L * cfg.rank + 2)
+            throw ConfigError("init_stream: compressed decomposition fails the identifiability bound");
+    }
+    const auto t_start = Clock::now();
+    gen_replicas();
+    const int P = cfg.p, Q = cfg.q, R = cfg.rank;
+    comp.set_projections(P, Q, cfg.shared, I, J, hU.data(), hV.data(), st);
+    merge.set_projections(P, Q, cfg.shared, R, I, J, hU.data(), hV.data(), st);
+    const size_t q3 = (size_t)Q * Q * Q;
+    Y.reserve((size_t)P * q3);
+    Y.zero((size_t)P * q3, st);
+    hist.reserve((size_t)P * Q * R);
+    hist.zero((size_t)P * Q * R, st);
+    lam.reserve(R);
+    A.reserve((size_t)I * R);
+    B.reserve((size_t)J * R);
+    K = 0;
+    batches_seen = 0;
+
+    BatchRecordC rec{};
+    rec.batch_index = 0;
+    rec.t_new = t0;
+    auto tc = Clock::now();
+    const size_t n = (size_t)I * J * t0;
+    const void* dX = stage_input(data, dtype, location, n);
+    check_finite(dX, dtype, n);
+    extend_temporal(t0);
+    compress_stage(dX, dtype, t0);
+    OCTEN_CUDA(cudaStreamSynchronize(st));
+    rec.compress_seconds = seconds_since(tc);
+    auto ta = Clock::now();
+    als_stage(0);
+    rec.als_seconds = seconds_since(ta);
+    auto tr = Clock::now();
+    recover_stage(t0, true, rec);
+    OCTEN_CUDA(cudaStreamSynchronize(st));
+    rec.recover_seconds = seconds_since(tr);
+    rec.total_seconds = seconds_since(t_start);
+    log.push_back(rec);
+    initialized = true;
+}
+
+void Stream::snapshot(Snapshot& s) {
+    const int P = cfg.p, Q = cfg.q, R = cfg.rank;
+    const size_t q3 = (size_t)Q * Q * Q;
+    s.Y.reserve((size_t)P * q3);
+    OCTEN_CUDA(cudaMemcpyAsync(s.Y.p, Y.p, sizeof(double) * P * q3, cudaMemcpyDeviceToDevice, st));
+    s.hist.reserve((size_t)P * Q * R);
+    OCTEN_CUDA(cudaMemcpyAsync(s.hist.p, hist.p, sizeof(double) * P * Q * R, cudaMemcpyDeviceToDevice, st));
+    s.A.reserve((size_t)I * R);
+    OCTEN_CUDA(cudaMemcpyAsync(s.A.p, A.p, sizeof(double) * I * R, cudaMemcpyDeviceToDevice, st));
+    s.B.reserve((size_t)J * R);
+    OCTEN_CUDA(cudaMemcpyAsync(s.B.p, B.p, sizeof(double) * J * R, cudaMemcpyDeviceToDevice, st));
+    s.C.reserve((size_t)capC * R);
+    OCTEN_CUDA(cudaMemcpyAsync(s.C.p, C.p, sizeof(double) * capC * R, cudaMemcpyDeviceToDevice, st));
+    s.lam.reserve(R);
+    OCTEN_CUDA(cudaMemcpyAsync(s.lam.p, lam.p, sizeof(double) * R, cudaMemcpyDeviceToDevice, st));
+    s.capC = capC;
+    s.K = K;
+    s.batches_seen = batches_seen;
+    s.batches_drawn = batches_drawn;
+    s.tgram = tgram;
+    s.log_len = log.size();
+    OCTEN_CUDA(cudaStreamSynchronize(st));
+}
+
+void Stream::restore(Snapshot& s) {
+    std::swap(Y.p, s.Y.p);
+    std::swap(Y.n, s.Y.n);
+    std::swap(hist.p, s.hist.p);
+    std::swap(hist.n, s.hist.n);
+    std::swap(A.p, s.A.p);
+    std::swap(A.n, s.A.n);
+    std::swap(B.p, s.B.p);
+    std::swap(B.n, s.B.n);
+    std::swap(C.p, s.C.p);
+    std::swap(C.n, s.C.n);
+    std::swap(lam.p, s.lam.p);
+    std::swap(lam.n, s.lam.n);
+    capC = s.capC;
+    K = s.K;
+    batches_seen = s.batches_seen;
+    batches_drawn = s.batches_drawn;
+    tgram = s.tgram;
+    log.resize(s.log_len);
+}
+
+void Stream::ingest(const void* data, int dtype, int location, int order, const std::int64_t* dims) {
+    // streaming.cpp:258-346
+    if (order != 3)
+        throw ConfigError("ingest_batch: batch order mismatch at batch " + std::to_string(batches_seen));
+    if (dims[0] != I)
+        throw ConfigError("ingest_batch: extent mismatch on mode 1 at batch " + std::to_string(batches_seen));
+    if (dims[1] != J)
+        throw ConfigError("ingest_batch: extent mismatch on mode 2 at batch " + std::to_string(batches_seen));
+    const std::int64_t t_new = dims[2];
+    if (t_new < 1) throw ConfigError("ingest_batch: batch has no temporal extent");
+    Snapshot backup;
+    if (cfg.strict) snapshot(backup);
+    const std::string context = "batch " + std::to_string(batches_seen) + ": ";
+    try {
+        const auto t_start = Clock::now();
+        BatchRecordC rec{};
+        rec.batch_index = batches_seen;
+        rec.t_new = t_new;
+        auto tc = Clock::now();
+        const size_t n = (size_t)I * J * t_new;
+        const void* dX = stage_input(data, dtype, location, n);
+        check_finite(dX, dtype, n);
+        extend_temporal(t_new);
+        compress_stage(dX, dtype, t_new);
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+        rec.compress_seconds = seconds_since(tc);
+        auto ta = Clock::now();
+        als_stage(rec.batch_index);
+        rec.als_seconds = seconds_since(ta);
+        auto tr = Clock::now();
+        recover_stage(t_new, false, rec);
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+        rec.recover_seconds = seconds_since(tr);
+        rec.total_seconds = seconds_since(t_start);
+        log.push_back(rec);
+    } catch (const ConfigError& e) {
+        if (cfg.strict) restore(backup);
+        throw ConfigError(context + e.what());
+    } catch (const NumericError& e) {
+        if (cfg.strict) restore(backup);
+        throw NumericError(context + e.what());
+    } catch (...) {
+        if (cfg.strict) restore(backup);
+        throw;
+    }
+}
+
+void Stream::get_factor(int mode, double* out) {
+    const int R = cfg.rank;
+    if (mode == 0)
+        OCTEN_CUDA(cudaMemcpyAsync(out, A.p, sizeof(double) * I * R, cudaMemcpyDeviceToHost, st));
+    else if (mode == 1)
+        OCTEN_CUDA(cudaMemcpyAsync(out, B.p, sizeof(double) * J * R, cudaMemcpyDeviceToHost, st));
+    else if (mode == 2)
+        OCTEN_CUDA(cudaMemcpy2DAsync(out, K * sizeof(double), C.p, capC * sizeof(double), K * sizeof(double), R,
+                                     cudaMemcpyDeviceToHost, st));
+    else
+        throw ConfigError("octen_stream_get_factor: mode out of range");
+    OCTEN_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace octen

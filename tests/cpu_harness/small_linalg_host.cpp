@@ -1,0 +1,51 @@
+// Host (g++) instantiation of the device small-linear-algebra routines, so
+// tests/test_small_linalg_cpu.py can check the exact kernel code against
+// numpy on a machine without a GPU.  Test infrastructure only.
+#include <cstring>
+#include <vector>
+
+#include "../../paper_1807_01350_b200/csrc/small_linalg.cuh"
+
+using namespace octen;
+
+extern "C" {
+
+void h_jacobi_eig(int n, const double* a, double* w, double* v) {
+    std::vector<double> am(a, a + (size_t)n * n), cs(2 * (n + 2));
+    int flag = 0;
+    TeamHost team;
+    jacobi_eig_sym(team, n, am.data(), v, cs.data(), &flag);
+    for (int i = 0; i < n; ++i) w[i] = am[i + (size_t)n * i];
+}
+
+int h_eig_real(int n, const double* a, double* wr, double* wi, double* v) {
+    std::vector<double> h(a, a + (size_t)n * n), ort(n);
+    return eig_real(n, h.data(), v, wr, wi, ort.data()) ? 1 : 0;
+}
+
+int h_lu_inverse(int n, const double* a, double* inv) {
+    std::vector<double> m(a, a + (size_t)n * n);
+    std::vector<int> rp(n), cp(n);
+    return lu_fullpiv_inverse(n, m.data(), n, inv, n, rp.data(), cp.data()) ? 1 : 0;
+}
+
+int h_chol_semidef(int n, double* a, double tol) { return chol_semidef(n, a, n, tol); }
+
+int h_greedy(int r, const double* sim, double tie, int* perm) {
+    std::vector<unsigned char> a(r), b(r);
+    return greedy_match(r, sim, r, tie, perm, a.data(), b.data());
+}
+
+double h_top_sv(int m, int n, const double* a, double* u, double* v) {
+    std::vector<double> red(1 + 2 + n + 8);
+    TeamHost team;
+    return top_singular_pair(team, m, n, a, u, v, red.data());
+}
+
+void h_mt64(unsigned long long seed, int n, double* out) {
+    Mt64 g;
+    g.seed(seed);
+    for (int i = 0; i < n; ++i) out[i] = g.uniform01();
+}
+
+}  // extern "C"
