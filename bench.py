@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""bench.py -- OCTen per-batch update throughput on B200.
+
+One step = one ingest_batch (compress -> per-replica CP-ALS -> align/merge)
+of a temporal batch on the BASELINE c3 workload: dense fp32 1000x1000 slices,
+batches of 100 slices after an initial block of K0=1000, Q=100, P=16
+replicas, rank R=20, shared=25, CP-ALS 30 sweeps x 3 restarts, rel_tol 1e-8
+(SURVEY.md §8(d)).  Metric: tensor entries streamed per second per batch
+update (I*J*t / step time).  Inputs are synthetic (rank-20 U(0,1) factors +
+1% Gaussian noise, generated on the device) and each 400 MB batch exceeds the
+126 MB L2, so no flush is needed.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N>1 (torchrun): every rank runs an independent stream on its own GPU
+("replicas only", weak scaling); value = all ranks'
+entries / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: I, J, K0, t, Q, P, R, shared, als_iters
+    "c3": dict(I=1000, J=1000, K0=1000, t=100, Q=100, P=16, R=20, shared=25, iters=30, restarts=3),
+    "c2": dict(I=500, J=500, K0=500, t=50, Q=50, P=8, R=10, shared=12, iters=30, restarts=3),
+    "small": dict(I=200, J=200, K0=100, t=20, Q=20, P=16, R=5, shared=5, iters=30, restarts=3),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# synthetic data (device)
+# ---------------------------------------------------------------------------
+
+class Synth:
+    """Rank-R U(0,1) factors + N(0, sigma) noise with sigma = 1% of the clean
+    RMS (BASELINE.json c3), generated on the device in fp64 and rounded to
+    fp32; batches are Fortran-ordered (I, J, t) views of (t, J, I) storage."""
+
+    def __init__(self, torch, dev, I, J, K, R, seed):
+        self.torch = torch
+        self.dev = dev
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        self.g = g
+        self.A = torch.rand((I, R), generator=g, device=dev, dtype=torch.float64)
+        self.B = torch.rand((J, R), generator=g, device=dev, dtype=torch.float64)
+        self.C = torch.rand((K, R), generator=g, device=dev, dtype=torch.float64)
+        clean = torch.einsum("kr,jr,ir->kji", self.C[:10], self.B, self.A)
+        self.sigma = 0.01 * float(clean.pow(2).mean().sqrt())
+        del clean
+
+    def batch(self, k0, t, out=None):
+        torch = self.torch
+        if out is None:
+            out = torch.empty((t, self.B.shape[0], self.A.shape[0]), device=self.dev, dtype=torch.float32)
+        step = 50
+        for s in range(0, t, step):
+            e = min(t, s + step)
+            x = torch.einsum("kr,jr,ir->kji", self.C[k0 + s:k0 + e], self.B, self.A)
+            x += self.sigma * torch.randn(x.shape, generator=self.g, device=self.dev, dtype=torch.float64)
+            out[s:e].copy_(x)
+            del x
+        return out.permute(2, 1, 0)
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port on the host cores, staged sample
+# ---------------------------------------------------------------------------
+
+def cpu_sample(cfg, seed=7, slices=5, replicas=1, cols=2):
+    """Time the oracle (numpy/LAPACK restatement of the reference) on a bounded
+    sample of one c3 batch update and scale to the full batch:
+      compress: `slices` of the t slices for `replicas` of the P replicas;
+      CP-ALS:   `replicas` of the P replicas (full sweeps/restarts);
+      merge:    align + the unweighted solve + `cols` of the R weighted
+                column solves per non-temporal mode + the temporal append.
+    Returns (seconds_per_batch_estimate, detail)."""
+    from oracle import octen_oracle as O
+    from oracle import rng as R_
+    I, J, t, Q, P, R, sh = cfg["I"], cfg["J"], cfg["t"], cfg["Q"], cfg["P"], cfg["R"], cfg["shared"]
+    g = np.random.default_rng(seed)
+    rs = O.gen_replicas([I, J], Q, P, sh, seed)
+    O.extend_temporal(rs, t)
+    x = g.random((I, J, slices)).astype(np.float32).astype(np.float64)
+    x = np.asfortranarray(x)
+    # compression
+    t0 = time.perf_counter()
+    zs = [O.compress(x, rs, r, 0, slices) for r in range(replicas)]
+    tc = (time.perf_counter() - t0) * (t / slices) * (P / replicas)
+    # CP-ALS on a realistic summary (rank-R signal)
+    del zs
+    fa = [g.random((d, R)) for d in (I, J, t)]
+    y = None
+    for r in range(replicas):
+        ct = [rs.replicas[r].nontemporal[0].T @ fa[0], rs.replicas[r].nontemporal[1].T @ fa[1],
+              rs.replicas[r].temporal.T @ fa[2]]
+        y = O.reconstruct_fast(O.KruskalModel(ct, np.ones(R)))
+        y = y + 0.01 * np.sqrt(np.mean(y ** 2)) * g.standard_normal(y.shape)
+    t0 = time.perf_counter()
+    models = []
+    for r in range(replicas):
+        models.append(O.cp_als(y, O.AlsConfig(R, cfg["iters"], 1e-8, cfg["restarts"],
+                                              R_.derive(seed, [8, r, 1]))).model)
+    ta = (time.perf_counter() - t0) * (P / replicas)
+    # merge
+    proj = O.stack_projections(rs, 0)
+    stack = proj @ fa[0] + 1e-3 * g.standard_normal((P * Q, R))
+    t0 = time.perf_counter()
+    O.recover_nontemporal(stack, proj, 0)
+    t_solve1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    w = np.ones((P, R))
+    w[0, :cols] = 0.7
+    O.recover_nontemporal_weighted(stack[:, :cols], proj, 0, Q, w[:, :cols])
+    t_wcol = (time.perf_counter() - t0) / cols
+    summ = O.init_summaries(rs)
+    t0 = time.perf_counter()
+    O.recover_temporal_append(g.random((P * Q, R)), rs, summ, np.zeros((0, R)), t)
+    t_app = time.perf_counter() - t0
+    tm = 2 * (t_solve1 + 2 * R * t_wcol) + t_app
+    total = tc + ta + tm
+    detail = ("oracle port, 1 batch of %dx%dx%d estimated from: compress %d/%d slices x %d/%d replicas, "
+              "CP-ALS %d/%d replicas, merge 1+%d/%d column solves per mode + temporal append"
+              % (I, J, t, slices, t, replicas, P, replicas, P, cols, 2 * R))
+    return total, {"compress_s": tc, "als_s": ta, "merge_s": tm}, detail
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    import os as _os
+    entries = cfg["I"] * cfg["J"] * cfg["t"]
+    cores = _os.cpu_count()
+    for _ in range(args.warmup):
+        cpu_sample(cfg, slices=2, cols=1)
+    times = []
+    det = None
+    for _ in range(args.steps):
+        tot, parts, det = cpu_sample(cfg, slices=2, cols=1)
+        times.append(tot)
+    sec = float(np.mean(times))
+    v = entries / sec
+    line = {"metric": "tensor entries streamed/sec per batch update", "value": v, "unit": "entries/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.config, **cfg},
+            "cpu_baseline": {"value": v, "unit": "entries/s", "cores": cores, "kind": "port", "sample": det},
+            "e2e": {"value": v, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# own arm
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="octen", choices=["octen", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    import paper_1807_01350_b200 as ob
+    I, J, K0, t, Q, P, R, sh = (cfg[k] for k in ("I", "J", "K0", "t", "Q", "P", "R", "shared"))
+    nb = args.warmup + args.steps + args.e2e_steps
+    syn = Synth(torch, dev, I, J, K0 + nb * t, R, seed=1234 + rank)
+    first = syn.batch(0, K0)
+    scfg = ob.StreamConfig(rank=R, p=P, q=Q, shared=sh, seed=7 * 1234 + 3 + rank,
+                           als=ob.AlsConfig(max_iters=cfg["iters"], rel_tol=1e-8, n_restarts=cfg["restarts"]),
+                           device=local)
+    torch.cuda.synchronize()
+    t_init = time.perf_counter()
+    st = ob.init_stream(first, scfg)
+    t_init = time.perf_counter() - t_init
+    del first
+    batches = [syn.batch(K0 + i * t, t) for i in range(args.warmup + args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.warmup):
+        ob.ingest_batch(st, batches[i])
+    times0 = (ctypes_stage_times(ob, st))
+    l0 = ob._capi.LIB.octen_launch_count()
+    clk = ClockSampler(local)
+    clk.start()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        ob.ingest_batch(st, batches[args.warmup + i])
+    e1.record()
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = ob._capi.LIB.octen_launch_count() - l0
+    times1 = ctypes_stage_times(ob, st)
+    dt = [b - a for a, b in zip(times0, times1)]
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    entries = I * J * t
+    value = world * entries / (ms * 1e-3)
+
+    # e2e through the C-ABI with pinned host buffers (H2D inside the timed region)
+    e2e = None
+    if args.e2e_steps > 0:
+        hb = []
+        for i in range(args.e2e_steps):
+            d = syn.batch(K0 + (args.warmup + args.steps + i) * t, t)
+            h = torch.empty((t, J, I), dtype=torch.float32, pin_memory=True)
+            h.copy_(d.permute(2, 1, 0))
+            hb.append(h.permute(2, 1, 0))
+        torch.cuda.synchronize()
+        barrier()
+        tw = time.perf_counter()
+        d2h = 0
+        for h in hb:
+            ob.ingest_batch(st, h)
+            m = st.model  # D2H of the updated model (factors + lambda)
+            d2h = sum(f.nbytes for f in m.factors) + m.lambda_.nbytes
+        barrier()
+        e2e_s = (time.perf_counter() - tw) / args.e2e_steps
+        if world > 1:
+            tt = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        e2e = {"value": world * entries / e2e_s, "unit": "entries/s", "h2d_bytes_per_step": entries * 4,
+               "d2h_bytes_per_step": int(d2h)}
+
+    hbm, bf16, peak_kind = peaks()
+    tf32_peak = bf16 / 2.0
+    g1_ms = dt[3] / max(dt[5], 1)  # per launch
+    g1_flops = dt[4] / max(dt[5], 1)
+    achieved = g1_flops / (g1_ms * 1e-3) / 1e12 if g1_ms > 0 else 0.0
+    roofline = {"kernel": "compression mode-1 contraction (GEMM1)", "bound": "tensor", "achieved": achieved,
+                "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak, "traffic": None,
+                "peak_source": "%s bf16 %.1f TF/s / 2 (dense TF32)" % (peak_kind, bf16),
+                "flops_per_launch": g1_flops, "ms_per_launch": g1_ms}
+    stage = {"compress_ms": dt[0] / args.steps, "als_ms": dt[1] / args.steps, "merge_ms": dt[2] / args.steps,
+             "gemm1_ms": dt[3] / args.steps, "init_s": t_init}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sec, parts, det = cpu_sample(cfg)
+            cpu = {"value": entries / sec, "unit": "entries/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": det, "stages_s": parts}
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": "entries/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": "failed: %r" % (exc,)}
+
+    if rank == 0:
+        line = {"metric": "tensor entries streamed/sec per batch update", "value": value, "unit": "entries/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32 compress (split-TF32/FP32) + f64 CP-ALS/merge", "data": "synthetic",
+                "config": {"workload": args.config, **cfg, "l2": "inputs larger than L2 (400 MB fp32 batch)",
+                           "parallelism": "replicas only" if world > 1 else "single"},
+                "stages": stage, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ctypes_stage_times(ob, st):
+    import ctypes
+    out = (ctypes.c_double * 6)()
+    ob._check(ob._capi.LIB.octen_stream_get_stage_times(st._h, out))
+    return list(out)
+
+
+if __name__ == "__main__":
+    main()

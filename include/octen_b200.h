@@ -82,6 +82,8 @@ typedef struct octen_stream octen_stream;
 const char* octen_last_error(void);
 /* Library version string. */
 const char* octen_version(void);
+/* Number of kernels this library has launched in this process. */
+int64_t octen_launch_count(void);
 
 /* init_stream (proj/include/cpstream/streaming.hpp:64; src/streaming.cpp:181-256).
  * data: I x J x t0 batch, first index fastest, dtype OCTEN_F64/F32 at
@@ -109,6 +111,11 @@ int octen_stream_get_history(const octen_stream* s, double* h);
 /* The per-replica CP-ALS models of the last batch: factors p x 3 x Q x rank,
  * lambda p x rank. */
 int octen_stream_get_replica_models(const octen_stream* s, double* factors, double* lambda);
+/* Cumulative device time (CUDA events on the stream's own CUDA stream), ms:
+ * out[0] compress stage, out[1] CP-ALS stage, out[2] merge stage,
+ * out[3] mode-1 contraction kernels; out[4] their algorithmic flops,
+ * out[5] their launch count. */
+int octen_stream_get_stage_times(const octen_stream* s, double* out);
 
 /* ---- stage-level entry points (the reference's L2 API, batched over replicas) ---- */
 

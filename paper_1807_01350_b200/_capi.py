@@ -53,6 +53,8 @@ class BatchRecordC(ctypes.Structure):
 SIGNATURES = {
     "octen_last_error": (ctypes.c_char_p, []),
     "octen_version": (ctypes.c_char_p, []),
+    "octen_launch_count": (ctypes.c_int64, []),
+    "octen_stream_get_stage_times": (ctypes.c_int, [ctypes.c_void_p, P_dbl]),
     "octen_stream_init": (ctypes.c_int, [ctypes.POINTER(StreamConfigC), ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, P_i64, ctypes.POINTER(ctypes.c_void_p)]),
     "octen_stream_ingest": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
@@ -92,4 +94,17 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     return lib
 
 
-LIB = load()
+class _LazyLib:
+    """Loads the native library on first use (so `python -m
+    paper_1807_01350_b200.build` can run before it exists); any call without
+    the library raises ImportError -- there is no fallback."""
+
+    _lib = None
+
+    def __getattr__(self, name):
+        if _LazyLib._lib is None:
+            _LazyLib._lib = load()
+        return getattr(_LazyLib._lib, name)
+
+
+LIB = _LazyLib()

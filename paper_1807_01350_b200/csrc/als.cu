@@ -820,7 +820,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     host_syncs = 0;
 
     // ---- norms, zero-tensor check (cp_als.cpp:255-256)
-    als_norm_kernel<<<P, 256, 0, st>>>(d);
+    als_norm_kernel<<<P, 256, 0, st>>>(d); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     std::vector<double> hn = normx2.to_host(P, st);
     ++host_syncs;
@@ -860,7 +860,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
                                               st, ks, ws.p);
         const size_t smem_eig = q2 * sizeof(double) + 2 * (Q + 2) * sizeof(double) + (4 + Q) * sizeof(int) + 64;
         OCTEN_CUDA(cudaFuncSetAttribute(gevd_eig_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eig));
-        gevd_eig_sym_kernel<<<P * 2, 256, smem_eig, st>>>(d);
+        gevd_eig_sym_kernel<<<P * 2, 256, smem_eig, st>>>(d); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
         // mixtures -> p1/p2 for all attempts
         gemm_simt<double, double, false, true>(NP, (int)q2, 6, Q, YmatA{dY, q3, q2, S, true}, MixB{Wmix.p, Q},
@@ -881,17 +881,17 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             todo.upload(td.data(), NP, st);
             peel_fail.zero(NP, st);
             const size_t smem_pen = (size_t)(R * R + R) * sizeof(double);
-            gevd_pencil_kernel<<<NP, 128, smem_pen, st>>>(d);
+            gevd_pencil_kernel<<<NP, 128, smem_pen, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
             gemm_simt<double, double, false, false>(NP, R, (int)q2, Q, A1tA{F.p, Q, R}, Y0Bp{dY, q3, Q, S},
                                                     HStore{Hh.p, R, q2}, st);
             const size_t smem_h = (size_t)(2 * R * R + 2 * (R + 2)) * sizeof(double) + 16;
-            gevd_hsolve_kernel<<<NP, 256, smem_h, st>>>(d);
+            gevd_hsolve_kernel<<<NP, 256, smem_h, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
             const int peel_threads = 128;
             const size_t smem_peel = (q2 + 2 * Q + peel_threads + 2 + Q) * sizeof(double);
             OCTEN_CUDA(cudaFuncSetAttribute(gevd_peel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_peel));
-            gevd_peel_kernel<<<NP * R, peel_threads, smem_peel, st>>>(d);
+            gevd_peel_kernel<<<NP * R, peel_threads, smem_peel, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
             std::vector<int> au = att_used.to_host(NP, st);
             std::vector<int> pf = peel_fail.to_host(NP, st);
@@ -928,7 +928,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             OCTEN_CUDA(cudaStreamSynchronize(st));
         }
     }
-    als_init_state_kernel<<<NP, 128, 0, st>>>(d);
+    als_init_state_kernel<<<NP, 128, 0, st>>>(d); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
 
     // ---- sweeps
@@ -946,17 +946,17 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         // T = Y x3 C  (Q^2 x SR per replica)
         gemm_simt<double, double, false, true>(P, (int)q2, SR, Q, YmatA{dY, q3, q2, S, false}, FacB{F.p, S, Q, R, 2},
                                                TStore{T.p, q2, SR}, st);
-        als_mttkrp_T_kernel<<<NP, 256, 0, st>>>(d, 0);
-        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 0, sweep);
-        als_mttkrp_T_kernel<<<NP, 256, 0, st>>>(d, 1);
-        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 1, sweep);
+        als_mttkrp_T_kernel<<<NP, 256, 0, st>>>(d, 0); OCTEN_LAUNCHED(1);
+        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 0, sweep); OCTEN_LAUNCHED(1);
+        als_mttkrp_T_kernel<<<NP, 256, 0, st>>>(d, 1); OCTEN_LAUNCHED(1);
+        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 1, sweep); OCTEN_LAUNCHED(1);
         {
             dim3 g((unsigned)std::min<size_t>((q2 * R + 255) / 256, 1024), NP);
-            als_kr_kernel<<<g, 256, 0, st>>>(d);
+            als_kr_kernel<<<g, 256, 0, st>>>(d); OCTEN_LAUNCHED(1);
         }
         gemm_simt<double, double, true, true>(P, Q, SR, (int)q2, YtA{dY, q3, q2}, KRB{KR.p, q2, SR},
                                               M2Store{Mb.p, S, Q, R}, st, ks_m2, ws.p);
-        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 2, sweep);
+        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 2, sweep); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
         OCTEN_CUDA(cudaMemcpyAsync(hcount, active_count.p, sizeof(int), cudaMemcpyDeviceToHost, st));
         OCTEN_CUDA(cudaStreamSynchronize(st));
@@ -982,7 +982,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     }
     DevBuf<int> best;
     best.reserve(P);
-    als_select_kernel<<<P, 256, 0, st>>>(d, Mf.p, Mlam.p, best.p);
+    als_select_kernel<<<P, 256, 0, st>>>(d, Mf.p, Mlam.p, best.p); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     std::vector<int> hb = best.to_host(P, st);
     std::vector<double> fh = fit_hist.to_host((size_t)NP * max_iters, st);

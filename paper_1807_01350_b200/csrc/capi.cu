@@ -103,6 +103,17 @@ const char* octen_last_error(void) { return g_err.c_str(); }
 
 const char* octen_version(void) { return "octen_b200 0.1 (sm_100a)"; }
 
+int64_t octen_launch_count(void) { return (int64_t)octen::launch_counter().load(); }
+
+int octen_stream_get_stage_times(const octen_stream* s, double* out) {
+    return guard([&] {
+        const auto& x = *s->s;
+        for (int i = 0; i < 4; ++i) out[i] = x.dev_ms[i];
+        out[4] = x.gemm1_flops;
+        out[5] = (double)x.gemm1_launches;
+    });
+}
+
 int octen_stream_init(const octen_stream_config* cfg, const void* data, int dtype, int location, int order,
                       const int64_t* dims, octen_stream** out) {
     return guard([&] {

@@ -135,14 +135,14 @@ struct CholTrailC {
 inline void chol_batched(double* A, int n, int lda, long long sA, int batch, double tol, double* maxdiag,
                          int* rank, cudaStream_t st) {
     if (batch <= 0 || n <= 0) return;
-    chol_maxdiag_kernel<<<batch, 256, 0, st>>>(A, n, lda, sA, maxdiag, rank);
+    chol_maxdiag_kernel<<<batch, 256, 0, st>>>(A, n, lda, sA, maxdiag, rank); OCTEN_LAUNCHED(1);
     for (int k0 = 0; k0 < n; k0 += kCholNB) {
-        chol_diag_kernel<<<batch, 256, 0, st>>>(A, n, lda, sA, k0, tol, maxdiag, rank);
+        chol_diag_kernel<<<batch, 256, 0, st>>>(A, n, lda, sA, k0, tol, maxdiag, rank); OCTEN_LAUNCHED(1);
         const int nb = min(kCholNB, n - k0);
         const int rows = n - k0 - nb;
         if (rows <= 0) break;
         dim3 g((rows + 127) / 128, batch);
-        chol_panel_kernel<<<g, 128, 0, st>>>(A, n, lda, sA, k0);
+        chol_panel_kernel<<<g, 128, 0, st>>>(A, n, lda, sA, k0); OCTEN_LAUNCHED(1);
         const int r0 = k0 + nb;
         gemm_simt<double, double, false, false>(batch, rows, rows, nb, CholTrailA{A, lda, sA, r0, k0},
                                                 CholTrailB{A, lda, sA, r0, k0}, CholTrailC{A, lda, sA, r0},
@@ -221,7 +221,7 @@ inline void chol_solve_batched(const double* L, int n, int ldl, long long sL, do
     dim3 g(nrhs, batch);
     const size_t smem = (size_t)n * sizeof(double);
     if (smem > 48 * 1024) cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    chol_solve_kernel<<<g, 256, smem, st>>>(L, n, ldl, sL, X, ldx, sX);
+    chol_solve_kernel<<<g, 256, smem, st>>>(L, n, ldl, sL, X, ldx, sX); OCTEN_LAUNCHED(1);
 }
 
 }  // namespace octen

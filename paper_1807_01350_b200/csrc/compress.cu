@@ -107,12 +107,17 @@ void run_compress(CompressEngine& e, const T* dX, std::int64_t t, const double* 
         const long long N1 = e.J * tc;
         const T* Xc = dX + (size_t)e.I * e.J * k0;
         bool done = false;
+        OCTEN_CUDA(cudaEventRecord(e.event(2 * e.g1_used), st));
         if constexpr (std::is_same<T, float>::value) {
             if (use_tc) done = tc_gemm_f32_nt(A, Xc, Z1, (int)e.Meff, (long long)N1, (int)e.I, st);
         }
         if (!done)
             gemm_simt<T, T, true, true>(1, (int)e.Meff, (int)N1, (int)e.I, G1A<T>{A, e.I}, G1B<T>{Xc, e.I},
                                         G1C<T>{Z1, N1}, st);
+        OCTEN_CUDA(cudaEventRecord(e.event(2 * e.g1_used + 1), st));
+        ++e.g1_used;
+        ++e.gemm1_launches;
+        e.gemm1_flops += 2.0 * (double)e.Meff * (double)N1 * (double)e.I;
         gemm_simt<T, T, true, false>(P * tc, Q, Q, (int)e.J, G2A<T>{Z1, e.rowmap.p, N1, e.J, tc, Q},
                                      G2B<T>{V, e.J, tc, Q}, G2C<T>{Z2, tc, Q}, st);
         gemm_simt<double, double, false, true>(P, Q * Q, Q, tc, G3A<T>{Z2, tc, Q}, G3B{dW, t, k0, Q}, G3C{dY, Q}, st);
@@ -121,6 +126,30 @@ void run_compress(CompressEngine& e, const T* dX, std::int64_t t, const double* 
 }
 
 }  // namespace
+
+cudaEvent_t CompressEngine::event(int i) {
+    while ((int)g1_events.size() <= i) {
+        cudaEvent_t ev;
+        OCTEN_CUDA(cudaEventCreate(&ev));
+        g1_events.push_back(ev);
+    }
+    return g1_events[i];
+}
+
+double CompressEngine::collect_gemm1_ms() {
+    double ms = 0.0;
+    for (int i = 0; i < g1_used; ++i) {
+        float t = 0.f;
+        OCTEN_CUDA(cudaEventElapsedTime(&t, g1_events[2 * i], g1_events[2 * i + 1]));
+        ms += t;
+    }
+    g1_used = 0;
+    return ms;
+}
+
+CompressEngine::~CompressEngine() {
+    for (cudaEvent_t e : g1_events) cudaEventDestroy(e);
+}
 
 void CompressEngine::set_projections(int P_, int Q_, int shared_, std::int64_t I_, std::int64_t J_, const double* hU,
                                      const double* hV, cudaStream_t st) {

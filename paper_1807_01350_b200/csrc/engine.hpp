@@ -88,6 +88,14 @@ public:
     DevBuf<float> Z1f, Z2f;
     DevBuf<double> Z1d, Z2d;
     std::int64_t chunk_slices = 0;
+    // device time of the mode-1 contraction (the dominant compression kernel)
+    std::vector<cudaEvent_t> g1_events;  // pairs, reused
+    int g1_used = 0;
+    long long gemm1_launches = 0;
+    double gemm1_flops = 0.0;  // algorithmic, accumulated
+    double collect_gemm1_ms();  // call after the stream is synchronized
+    cudaEvent_t event(int i);
+    ~CompressEngine();
 };
 
 // ---------------------------------------------------------------------------

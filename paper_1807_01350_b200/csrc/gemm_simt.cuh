@@ -120,12 +120,12 @@ void gemm_simt(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaStream
     constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
     dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batches * ksplit);
     gemm_simt_kernel<TIn, Acc, BM, BN, BK, TM, TN, A_KFAST, B_KFAST>
-        <<<grid, (BM / TM) * (BN / TN), 0, st>>>(M, N, K, ksplit, kchunk, af, bf, cf, workspace);
+        <<<grid, (BM / TM) * (BN / TN), 0, st>>>(M, N, K, ksplit, kchunk, af, bf, cf, workspace); OCTEN_LAUNCHED(1);
     if (ksplit > 1) {
         const size_t total = (size_t)batches * M * N;
         int blocks = (int)((total + 255) / 256);
         if (blocks > 148 * 16) blocks = 148 * 16;
-        gemm_splitk_reduce<Acc><<<blocks, 256, 0, st>>>(batches, M, N, ksplit, workspace, cf);
+        gemm_splitk_reduce<Acc><<<blocks, 256, 0, st>>>(batches, M, N, ksplit, workspace, cf); OCTEN_LAUNCHED(1);
     }
 }
 

@@ -33,7 +33,7 @@ namespace {
 
 constexpr double kRankTol = 1e-10;        // recovery.cpp:12
 constexpr double kDegenerateRow = 1e-12;  // recovery.cpp:13
-constexpr double kGramRankTol = 1e-14;    // pivot^2 relative threshold
+constexpr double kGramRankTol = 1e-11;    // pivot^2 relative threshold
 constexpr double kEps = 2.220446049250313e-16;
 
 // ---- GEMM functors ----
@@ -797,7 +797,7 @@ void MergeEngine::set_projections(int P_, int Q_, int sh, int R_, std::int64_t I
         Lw[n].reserve((size_t)std::max(1, sh * sh));
         white_ok[n] = 0;
         if (sh > 0) {
-            whitener_kernel<<<1, 256, (size_t)sh * sh * sizeof(double), st>>>(Ud[n].p, d, sh, Lw[n].p, okb.p);
+            whitener_kernel<<<1, 256, (size_t)sh * sh * sizeof(double), st>>>(Ud[n].p, d, sh, Lw[n].p, okb.p); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
             white_ok[n] = okb.to_host(1, st)[0];
         }
@@ -805,7 +805,7 @@ void MergeEngine::set_projections(int P_, int Q_, int sh, int R_, std::int64_t I
         lp_ok[n].reserve(P);
         const size_t smem = (size_t)Q * Q * sizeof(double);
         OCTEN_CUDA(cudaFuncSetAttribute(lp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        lp_kernel<<<P, 256, smem, st>>>(Ud[n].p, d, Q, Lp[n].p, lp_ok[n].p);
+        lp_kernel<<<P, 256, smem, st>>>(Ud[n].p, d, Q, Lp[n].p, lp_ok[n].p); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
     }
     pair_solve = P >= 2;
@@ -833,7 +833,7 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
     iscr.zero(8, st);
     if (sh > 0 && (int)tgram.size() == sh * sh) {
         OCTEN_CUDA(cudaMemcpyAsync(Lwt.p, tgram.data(), sizeof(double) * sh * sh, cudaMemcpyHostToDevice, st));
-        chol_small_from_host_kernel<<<1, 32, 0, st>>>(Lwt.p, sh, iscr.p + 2);
+        chol_small_from_host_kernel<<<1, 32, 0, st>>>(Lwt.p, sh, iscr.p + 2); OCTEN_LAUNCHED(1);
     }
     std::vector<int> wok = {white_ok[0], white_ok[1], 0};
     OCTEN_CUDA(cudaMemcpyAsync(iscr.p, wok.data(), 2 * sizeof(int), cudaMemcpyHostToDevice, st));
@@ -866,7 +866,7 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
     a.maxoff = maxoff_d;
     a.ambig = ambig.p;
     a.err = err.p;
-    align_prep_kernel<<<P, 128, 0, st>>>(a);
+    align_prep_kernel<<<P, 128, 0, st>>>(a); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     check_errs(err, 1, st);
     DevBuf<double> rmsb;
@@ -889,7 +889,7 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
                 OCTEN_CUDA(cudaMemcpyAsync(Gj.p + (size_t)p * d * d, Gp[n].p, sizeof(double) * d * d,
                                            cudaMemcpyDeviceToDevice, st));
                 add_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>((size_t)d * d, Gp[n].p + (size_t)p * d * d,
-                                                                     Gj.p + (size_t)p * d * d);
+                                                                     Gj.p + (size_t)p * d * d); OCTEN_LAUNCHED(1);
             }
             chol_batched(Gj.p, (int)d, (int)d, d * d, P, 1e-15, md.p, rk.p, st);
             // g1 = U_0 RF_0[n]  (d x R)
@@ -905,8 +905,10 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
             OCTEN_CUDA(cudaMemcpyAsync(Y2.p, g2.p, sizeof(double) * P * d * R, cudaMemcpyDeviceToDevice, st));
             chol_solve_batched(Gj.p, (int)d, (int)d, d * d, Y1.p, (int)d, d * R, R, P, st);
             chol_solve_batched(Gj.p, (int)d, (int)d, d * d, Y2.p, (int)d, d * R, R, P, st);
-            if (P > 1)
+            if (P > 1) {
                 pair_rms_kernel<<<P - 1, 256, 0, st>>>(P, Q, sh, R, d, n, g1.p, Y1.p, g2.p, Y2.p, RF.p, SC.p, rmsb.p);
+                OCTEN_LAUNCHED(1);
+            }
             OCTEN_CUDA(cudaGetLastError());
             OCTEN_CUDA(cudaStreamSynchronize(st));
         }
@@ -915,7 +917,7 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
         a.rms = nullptr;
     }
     const size_t smem = (size_t)(R * R + 2 * R) * sizeof(double);
-    align_match_kernel<<<P, 128, smem, st>>>(a);
+    align_match_kernel<<<P, 128, smem, st>>>(a); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     check_errs(err, P + 1, st);
     if (out) {
@@ -963,7 +965,7 @@ void MergeEngine::temporal_stack(const double* dY, const double* dA, const doubl
     gemm_simt<double, double, true, true>(P, Q, R, (int)q2, YtA2{dY, q3, q2}, KrB{Ut, Vt, Q, R},
                                           StoreCM{tmp.p, Q, (long long)Q * R}, st, ks, tscr.p);
     const size_t smem = (size_t)(3 * R * R + 2 * (R + 2)) * sizeof(double) + 16;
-    tstack_solve_kernel<<<P, 128, smem, st>>>(P, Q, R, Ut, Vt, tmp.p, dTstack);
+    tstack_solve_kernel<<<P, 128, smem, st>>>(P, Q, R, Ut, Vt, tmp.p, dTstack); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
 }
 
@@ -995,17 +997,17 @@ void MergeEngine::temporal_append(const double* dTstack, const double* dW, std::
     DevBuf<double> hv;
     hv.reserve((size_t)t * R);
     OCTEN_CUDA(cudaMemcpyAsync(hv.p, BZ.p + (size_t)t * R, sizeof(double) * t * R, cudaMemcpyDeviceToDevice, st));
-    append_dots_kernel<<<R, 256, 0, st>>>(PQ, dTstack, dHist, dots.p);
+    append_dots_kernel<<<R, 256, 0, st>>>(PQ, dTstack, dHist, dots.p); OCTEN_LAUNCHED(1);
     chol_solve_batched(Gc.p, (int)t, (int)t, 0, BZ.p, (int)t, 0, 2 * R, 1, st);
     const int rank_c = rk.to_host(1, st)[0];
     append_decide_kernel<<<R, 256, 0, st>>>(R, t, rank_c, dots.p, hv.p, BZ.p, md.p, dRows, coef.p, err.p,
-                                            2 /* temporal mode */);
+                                            2 /* temporal mode */); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     check_errs(err, R, st);
     // Ps = Pc * rows (PQ x R)
     gemm_simt<double, double, true, true>(1, (int)PQ, R, (int)t, UtA{dW, t, (int)PQ}, ColB{dRows, t, 0},
                                           StoreCM{Ps.p, PQ, 0}, st);
-    append_resid_kernel<<<R, 256, 0, st>>>(PQ, dTstack, dHist, Ps.p, coef.p, res.p);
+    append_resid_kernel<<<R, 256, 0, st>>>(PQ, dTstack, dHist, Ps.p, coef.p, res.p); OCTEN_LAUNCHED(1);
     std::vector<double> hr = res.to_host(R, st);
     std::vector<double> hd = dots.to_host((size_t)3 * R, st);
     double res_sq = 0.0, rhs_sq = 0.0;
@@ -1014,7 +1016,7 @@ void MergeEngine::temporal_append(const double* dTstack, const double* dW, std::
         rhs_sq += hd[3 * r + 2];
     }
     *residual = rhs_sq > 0.0 ? std::sqrt(res_sq / rhs_sq) : 0.0;
-    add_kernel<<<grid_for((size_t)PQ * R), 256, 0, st>>>((size_t)PQ * R, Ps.p, dHist);
+    add_kernel<<<grid_for((size_t)PQ * R), 256, 0, st>>>((size_t)PQ * R, Ps.p, dHist); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
 }
 
@@ -1044,8 +1046,8 @@ void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, do
         const size_t smem = (size_t)(2 * Q * R + R) * sizeof(double);
         OCTEN_CUDA(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         refine_kernel<<<P, 128, smem, st>>>(P, Q, R, (int)PQ, tg.p, stacks.p, Lp[0].p, Lp[1].p, lp_ok[0].p,
-                                            lp_ok[1].p, w.p);
-        weight_mass_kernel<<<1, 64, 0, st>>>(P, Q, R, std::max(dims[0], dims[1]), w.p);
+                                            lp_ok[1].p, w.p); OCTEN_LAUNCHED(1);
+        weight_mass_kernel<<<1, 64, 0, st>>>(P, Q, R, std::max(dims[0], dims[1]), w.p); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
         for (int n = 0; n < 2; ++n) {
             const long long d = dims[n];
@@ -1054,10 +1056,10 @@ void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, do
                                    "x" + std::to_string(d) +
                                    "; p*Q must reach the mode extent (raise p per the replica bound)");
             Gw.reserve((size_t)R * d * d);
-            weighted_gram_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>(P, R, d, Gp[n].p, w.p, Gw.p);
+            weighted_gram_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>(P, R, d, Gp[n].p, w.p, Gw.p); OCTEN_LAUNCHED(1);
             chol_batched(Gw.p, (int)d, (int)d, d * d, R, kGramRankTol, maxdiag.p, ranks.p, st);
             scale_stack_kernel<<<grid_for((size_t)PQ * R), 256, 0, st>>>(P, Q, R, stacks.p + (size_t)n * PQ * R, w.p,
-                                                                        sw.p);
+                                                                        sw.p); OCTEN_LAUNCHED(1);
             gemm_simt<double, double, false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{sw.p, PQ, 0},
                                                    StoreCM{solved[n].p, d, 0}, st);
             std::vector<int> rk = ranks.to_host(R, st);
@@ -1080,16 +1082,16 @@ void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, do
     if (dStoredA && dStoredB) {
         const size_t smem = (size_t)(R * R + 4 * R) * sizeof(double);
         match_columns_kernel<<<1, 256, smem, st>>>(R, dims[0], dims[1], solved[0].p, solved[1].p, dStoredA, dStoredB,
-                                                   perm.p, signs.p, simb.p);
-        finalize_kernel<<<R, 256, 0, st>>>(R, dims[0], solved[0].p, perm.p, signs.p, dAfin, err.p, 0);
-        finalize_kernel<<<R, 256, 0, st>>>(R, dims[1], solved[1].p, perm.p, signs.p + R, dBfin, err.p + 1, 1);
+                                                   perm.p, signs.p, simb.p); OCTEN_LAUNCHED(1);
+        finalize_kernel<<<R, 256, 0, st>>>(R, dims[0], solved[0].p, perm.p, signs.p, dAfin, err.p, 0); OCTEN_LAUNCHED(1);
+        finalize_kernel<<<R, 256, 0, st>>>(R, dims[1], solved[1].p, perm.p, signs.p + R, dBfin, err.p + 1, 1); OCTEN_LAUNCHED(1);
         last_perm = perm.to_host(R, st);
     } else {
         std::vector<int> id(R);
         for (int i = 0; i < R; ++i) id[i] = i;
         perm.upload(id.data(), R, st);
-        finalize_kernel<<<R, 256, 0, st>>>(R, dims[0], solved[0].p, perm.p, nullptr, dAfin, err.p, 0);
-        finalize_kernel<<<R, 256, 0, st>>>(R, dims[1], solved[1].p, perm.p, nullptr, dBfin, err.p + 1, 1);
+        finalize_kernel<<<R, 256, 0, st>>>(R, dims[0], solved[0].p, perm.p, nullptr, dAfin, err.p, 0); OCTEN_LAUNCHED(1);
+        finalize_kernel<<<R, 256, 0, st>>>(R, dims[1], solved[1].p, perm.p, nullptr, dBfin, err.p + 1, 1); OCTEN_LAUNCHED(1);
         last_perm = id;
     }
     OCTEN_CUDA(cudaGetLastError());

@@ -6,6 +6,7 @@
 // dense solvers against numpy without a GPU).
 #pragma once
 
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 
@@ -17,7 +18,16 @@
 #define OCTEN_DEV
 #endif
 
+#define OCTEN_LAUNCHED(n) ::octen::launch_counter().fetch_add((n), std::memory_order_relaxed)
+
 namespace octen {
+
+// Number of kernels this library has launched (reported by bench.py as
+// gpu_launches).
+inline std::atomic<long long>& launch_counter() {
+    static std::atomic<long long> c{0};
+    return c;
+}
 
 // A "team" is the set of threads cooperating on one small problem: a CUDA
 // thread block on the device, a single thread on the host.  Team-parallel

@@ -98,11 +98,14 @@ Stream::Stream(const StreamCfg& c) : cfg(c) {
     OCTEN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     OCTEN_CUDA(cudaEventCreate(&ev0));
     OCTEN_CUDA(cudaEventCreate(&ev1));
+    for (auto& e : evs) OCTEN_CUDA(cudaEventCreate(&e));
 }
 
 Stream::~Stream() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    for (auto& e : evs)
+        if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
 }
 
@@ -192,6 +195,7 @@ void Stream::check_finite(const void* dX, int dtype, size_t n) {
         nonfinite_f32_kernel<<<grid1d(n), 256, 0, st>>>((const float*)dX, n, flag.p);
     else
         nonfinite_f64_kernel<<<grid1d(n), 256, 0, st>>>((const double*)dX, n, flag.p);
+    OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     if (flag.to_host(1, st)[0]) throw NumericError("DenseTensor: non-finite value");
 }
@@ -248,13 +252,16 @@ void Stream::recover_stage(std::int64_t t_new, bool first, BatchRecordC& rec) {
     }
     // assemble_model (streaming.cpp:162-177): C_raw = [C diag(lambda); rows]
     ensure_c_capacity(K + t_new);
-    if (!first && K > 0) scale_cols_kernel<<<grid1d((size_t)K * R), 256, 0, st>>>(C.p, K, capC, R, lam.p);
-    append_rows_kernel<<<grid1d((size_t)t_new * R), 256, 0, st>>>(C.p, K, capC, R, rows.p, t_new);
+    if (!first && K > 0) {
+        scale_cols_kernel<<<grid1d((size_t)K * R), 256, 0, st>>>(C.p, K, capC, R, lam.p);
+        OCTEN_LAUNCHED(1);
+    }
+    append_rows_kernel<<<grid1d((size_t)t_new * R), 256, 0, st>>>(C.p, K, capC, R, rows.p, t_new); OCTEN_LAUNCHED(1);
     std::swap(A.p, Anew.p);
     std::swap(A.n, Anew.n);
     std::swap(B.p, Bnew.p);
     std::swap(B.n, Bnew.n);
-    normalize_model_kernel<<<R, 256, 0, st>>>(A.p, I, B.p, J, C.p, K + t_new, capC, lam.p);
+    normalize_model_kernel<<<R, 256, 0, st>>>(A.p, I, B.p, J, C.p, K + t_new, capC, lam.p); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     K += t_new;
 }
@@ -305,15 +312,21 @@ void Stream::init(const void* data, int dtype, int location, int order, const st
     const void* dX = stage_input(data, dtype, location, n);
     check_finite(dX, dtype, n);
     extend_temporal(t0);
+    OCTEN_CUDA(cudaEventRecord(evs[0], st));
     compress_stage(dX, dtype, t0);
+    OCTEN_CUDA(cudaEventRecord(evs[1], st));
     OCTEN_CUDA(cudaStreamSynchronize(st));
     rec.compress_seconds = seconds_since(tc);
     auto ta = Clock::now();
+    OCTEN_CUDA(cudaEventRecord(evs[2], st));
     als_stage(0);
+    OCTEN_CUDA(cudaEventRecord(evs[3], st));
     rec.als_seconds = seconds_since(ta);
     auto tr = Clock::now();
     recover_stage(t0, true, rec);
+    OCTEN_CUDA(cudaEventRecord(evs[4], st));
     OCTEN_CUDA(cudaStreamSynchronize(st));
+    accumulate_stage_times();
     rec.recover_seconds = seconds_since(tr);
     rec.total_seconds = seconds_since(t_start);
     log.push_back(rec);
@@ -388,15 +401,21 @@ void Stream::ingest(const void* data, int dtype, int location, int order, const 
         const void* dX = stage_input(data, dtype, location, n);
         check_finite(dX, dtype, n);
         extend_temporal(t_new);
+        OCTEN_CUDA(cudaEventRecord(evs[0], st));
         compress_stage(dX, dtype, t_new);
+        OCTEN_CUDA(cudaEventRecord(evs[1], st));
         OCTEN_CUDA(cudaStreamSynchronize(st));
         rec.compress_seconds = seconds_since(tc);
         auto ta = Clock::now();
+        OCTEN_CUDA(cudaEventRecord(evs[2], st));
         als_stage(rec.batch_index);
+        OCTEN_CUDA(cudaEventRecord(evs[3], st));
         rec.als_seconds = seconds_since(ta);
         auto tr = Clock::now();
         recover_stage(t_new, false, rec);
+        OCTEN_CUDA(cudaEventRecord(evs[4], st));
         OCTEN_CUDA(cudaStreamSynchronize(st));
+        accumulate_stage_times();
         rec.recover_seconds = seconds_since(tr);
         rec.total_seconds = seconds_since(t_start);
         log.push_back(rec);
@@ -410,6 +429,19 @@ void Stream::ingest(const void* data, int dtype, int location, int order, const 
         if (cfg.strict) restore(backup);
         throw;
     }
+}
+
+void Stream::accumulate_stage_times() {
+    float t = 0.f;
+    OCTEN_CUDA(cudaEventElapsedTime(&t, evs[0], evs[1]));
+    dev_ms[0] += t;
+    OCTEN_CUDA(cudaEventElapsedTime(&t, evs[2], evs[3]));
+    dev_ms[1] += t;
+    OCTEN_CUDA(cudaEventElapsedTime(&t, evs[3], evs[4]));
+    dev_ms[2] += t;
+    dev_ms[3] += comp.collect_gemm1_ms();
+    gemm1_flops = comp.gemm1_flops;
+    gemm1_launches = comp.gemm1_launches;
 }
 
 void Stream::get_factor(int mode, double* out) {

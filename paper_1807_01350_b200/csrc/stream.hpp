@@ -56,6 +56,11 @@ public:
     DevBuf<float> X32;
     DevBuf<int> flag;
     std::vector<BatchRecordC> log;
+    // cumulative device milliseconds: compress, als, recover, gemm1 (mode-1 contraction)
+    double dev_ms[4] = {0, 0, 0, 0};
+    double gemm1_flops = 0.0;
+    long long gemm1_launches = 0;
+    cudaEvent_t evs[6] = {};
 
 private:
     struct Snapshot {
@@ -73,6 +78,7 @@ private:
     void als_stage(std::int64_t batch_index);
     void recover_stage(std::int64_t t_new, bool first, BatchRecordC& rec);
     void ensure_c_capacity(std::int64_t rows);
+    void accumulate_stage_times();
     void snapshot(Snapshot& s);
     void restore(Snapshot& s);
 };
