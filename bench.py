@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # name: I, J, K0, t, Q, P, R, shared, als_iters
-    "c3": dict(I=1000, J=1000, K0=1000, t=100, Q=100, P=16, R=20, shared=25, iters=30, restarts=3),
+    "c3": dict(I=1000, J=1000, K0=1000, t=100, Q=100, P=16, R=20, shared=10, iters=30, restarts=3),
     "c2": dict(I=500, J=500, K0=500, t=50, Q=50, P=8, R=10, shared=12, iters=30, restarts=3),
     "small": dict(I=200, J=200, K0=100, t=20, Q=20, P=16, R=5, shared=5, iters=30, restarts=3),
 }

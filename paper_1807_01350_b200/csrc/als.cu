@@ -21,7 +21,7 @@
 #include <stdexcept>
 
 #include "engine.hpp"
-#include "gemm_simt.cuh"
+#include "gemm_dmma.cuh"
 #include "rng_host.hpp"
 #include "small_linalg.cuh"
 
@@ -84,34 +84,47 @@ __device__ double block_sum(double v, double* red) {
     return out;
 }
 
-// ||Y_p||_F^2 per replica.
-__global__ void als_norm_kernel(AlsDev d) {
+// ||Y_p||_F^2 per replica: 64 chunk partials per replica (grid P x 64), then
+// a fixed-order sum (deterministic).
+__global__ void als_norm_kernel(AlsDev d, double* part) {
     __shared__ double red[256];
-    const double* y = d.Y + (size_t)blockIdx.x * d.q3();
+    const int p = blockIdx.y, c = blockIdx.x, nc = gridDim.x;
+    const size_t n = d.q3(), chunk = (n + nc - 1) / nc;
+    const double* y = d.Y + (size_t)p * n;
+    const size_t b = chunk * c, e = min(n, b + chunk);
     double s = 0.0;
-    for (size_t i = threadIdx.x; i < d.q3(); i += blockDim.x) s += y[i] * y[i];
+    for (size_t i = b + threadIdx.x; i < e; i += blockDim.x) s += y[i] * y[i];
     s = block_sum(s, red);
-    if (threadIdx.x == 0) d.normx2[blockIdx.x] = s;
+    if (threadIdx.x == 0) part[(size_t)p * nc + c] = s;
+}
+__global__ void als_norm_finish_kernel(AlsDev d, const double* part, int nc) {
+    const int p = threadIdx.x + blockIdx.x * blockDim.x;
+    if (p >= d.P) return;
+    double s = 0.0;
+    for (int c = 0; c < nc; ++c) s += part[(size_t)p * nc + c];
+    d.normx2[p] = s;
 }
 
 // ---------------- GEVD init ----------------
 
 // Jacobi eigen-decomposition of the two Gram matrices of replica p, top-R
 // eigenvectors into Ur[p][which] (descending eigenvalue), usability flag.
-__global__ void gevd_eig_sym_kernel(AlsDev d) {
+__global__ void gevd_eig_sym_kernel(AlsDev d, int v_in_smem) {
     extern __shared__ double sm[];
     const int p = blockIdx.x / 2, which = blockIdx.x % 2;
     const int Q = d.Q, R = d.R;
     double* A = sm;                      // Q*Q
     double* cs = A + (size_t)Q * Q;      // 2*(Q+2)
-    int* flag = (int*)(cs + 2 * (Q + 2));
-    int* order = flag + 4;               // Q
+    double* Vs = cs + 2 * (Q + 2);       // Q*Q when v_in_smem
+    int* iw = (int*)(Vs + (v_in_smem ? (size_t)Q * Q : 0));  // Q + 8
+    int* order = iw + Q + 8;             // Q
     const double* src = d.Gev + ((size_t)p * 2 + which) * Q * Q;
-    double* V = d.EV + ((size_t)p * 2 + which) * Q * Q;
+    double* Vg = d.EV + ((size_t)p * 2 + which) * Q * Q;
+    double* V = v_in_smem ? Vs : Vg;
     for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) A[i] = src[i];
     __syncthreads();
     TeamDev team;
-    jacobi_eig_sym(team, Q, A, V, cs, flag);
+    jacobi_eig_sym(team, Q, A, V, cs, iw);
     __syncthreads();
     if (threadIdx.x == 0) {
         // order by descending eigenvalue (stable: lower index first on ties)
@@ -131,8 +144,7 @@ __global__ void gevd_eig_sym_kernel(AlsDev d) {
         int nz = 0;
         for (int i = 0; i < Q; ++i)
             if (A[order[i] + (size_t)Q * order[i]] > kEps * Q * lmax && lmax > 0.0) ++nz;
-        if (which == 0) atomicAnd(&d.usable[p], nz >= R ? 1 : 0);
-        if (which == 1) atomicAnd(&d.usable[p], nz >= R ? 1 : 0);
+        atomicAnd(&d.usable[p], nz >= R ? 1 : 0);
     }
     __syncthreads();
     double* ur = d.Ur + ((size_t)p * 2 + which) * Q * R;
@@ -153,7 +165,7 @@ __global__ void gevd_pencil_kernel(AlsDev d) {
     double* asub = sm;                  // R*R
     double* nrm = asub + R * R;         // R
     __shared__ int ok, att;
-    double* scr = d.gscr + (size_t)prob * (6 * R * R + 4 * R);
+    double* scr = nrm + R;  // shared: 4R^2 + 4R doubles
     double* m_inv = scr;
     double* m_pen = m_inv + R * R;
     double* m_h = m_pen + R * R;
@@ -241,8 +253,9 @@ __global__ void gevd_hsolve_kernel(AlsDev d) {
     const int Q = d.Q, R = d.R;
     extern __shared__ double sm[];
     double* Lf = sm;           // R*R
-    double* Vp = Lf + R * R;   // R*R (pinv fallback)
-    double* cs = Vp + R * R;   // 2(R+2)
+    double* Vp = Lf + R * R;   // R*R (Gram; pinv fallback / inverse)
+    double* Li = Vp + R * R;   // R*R (L^-1)
+    double* cs = Li + R * R;   // 2(R+2)
     int* flag = (int*)(cs + 2 * (R + 2));
     __shared__ int rank;
     const double* a1 = d.f(prob, 0);
@@ -254,11 +267,39 @@ __global__ void gevd_hsolve_kernel(AlsDev d) {
         Vp[e] = s;
     }
     __syncthreads();
-    if (threadIdx.x == 0) rank = chol_semidef(R, Lf, R, kEps * R);
+    if (threadIdx.x < 32) {
+        TeamWarp w;
+        int rk;
+        if (R <= 32) {
+            const double md = warp_max_diag(Lf, R, R);
+            rk = warp_chol_inv32(Lf, R, R, md > 0.0 ? kEps * R * md : INFINITY, Li, R);
+        } else {
+            rk = team_chol_semidef(w, R, Lf, R, kEps * R, cs, flag);
+            if (rk == R) team_tri_inv_lower(w, R, Lf, R, Li, R);
+        }
+        if (threadIdx.x == 0) rank = rk;
+    }
     __syncthreads();
     double* h = d.Hh + (size_t)prob * R * d.q2();
     if (rank == R) {
-        for (size_t k = threadIdx.x; k < d.q2(); k += blockDim.x) chol_solve_vec(R, Lf, R, h + (size_t)R * k, 1);
+        // Vp <- (a1^T a1)^-1 = L^-T L^-1
+        for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+            const int i = e % R, j = e / R;
+            double sacc = 0.0;
+            for (int k = (i > j ? i : j); k < R; ++k) sacc += Li[k + R * i] * Li[k + R * j];
+            Vp[e] = sacc;
+        }
+        __syncthreads();
+        for (size_t k = threadIdx.x; k < d.q2(); k += blockDim.x) {
+            double x[64], y[64];
+            for (int i = 0; i < R; ++i) x[i] = h[(size_t)R * k + i];
+            for (int i = 0; i < R; ++i) {
+                double sacc = 0.0;
+                for (int j = 0; j < R; ++j) sacc += Vp[i + R * j] * x[j];
+                y[i] = sacc;
+            }
+            for (int i = 0; i < R; ++i) h[(size_t)R * k + i] = y[i];
+        }
     } else {
         // minimum-norm fallback: pseudo-inverse from the eigen-decomposition
         double* Ev = d.gscr + (size_t)prob * (6 * R * R + 4 * R);
@@ -344,33 +385,59 @@ __global__ void als_init_state_kernel(AlsDev d) {
 // ---------------- sweeps ----------------
 
 // MTTKRP of mode 0 (a,r) = sum_b T(a,b,r) B(b,r) and of mode 1
-// (b,r) = sum_a T(a,b,r) A(a,r), from T = Y x3 C.
+// (b,r) = sum_a T(a,b,r) A(a,r), from T = Y x3 C.  One warp per
+// (problem, r): lanes run along the contiguous a index of T.
 __global__ void als_mttkrp_T_kernel(AlsDev d, int mode) {
-    const int prob = blockIdx.x;
+    const int warps_per_block = blockDim.x >> 5;
+    const int wid = blockIdx.x * warps_per_block + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int R = d.R, Q = d.Q;
+    if (wid >= d.NP * R) return;
+    const int prob = wid / R, r = wid % R;
     if (!d.state[prob].active) return;
     const int p = prob / d.S, s = prob % d.S;
-    const int Q = d.Q, R = d.R;
-    const double* T = d.T + (size_t)p * d.q2() * d.S * R;
-    double* M = d.Mb + (size_t)prob * Q * R;
+    const double* tcol = d.T + (size_t)p * d.q2() * d.S * R + (size_t)d.q2() * (s * R + r);
+    double* M = d.Mb + (size_t)prob * Q * R + (size_t)Q * r;
+    constexpr int MAXA = 8;  // Q <= 256
     if (mode == 0) {
-        const double* B = d.f(prob, 1);
-        for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
-            const int a = e % Q, r = e / Q;
-            const double* tcol = T + (size_t)d.q2() * (s * R + r);
-            double acc = 0.0;
-            for (int b = 0; b < Q; ++b) acc += tcol[a + (size_t)Q * b] * B[b + (size_t)Q * r];
-            M[a + (size_t)Q * r] = acc;
+        const double* B = d.f(prob, 1) + (size_t)Q * r;
+        double acc[MAXA];
+#pragma unroll
+        for (int i = 0; i < MAXA; ++i) acc[i] = 0.0;
+#pragma unroll 4
+        for (int b = 0; b < Q; ++b) {
+            const double w = B[b];
+            const double* row = tcol + (size_t)Q * b;
+#pragma unroll
+            for (int i = 0; i < MAXA; ++i) {
+                const int a = lane + 32 * i;
+                if (a < Q) acc[i] += __ldg(row + a) * w;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < MAXA; ++i) {
+            const int a = lane + 32 * i;
+            if (a < Q) M[a] = acc[i];
         }
     } else {
-        const double* A = d.f(prob, 0);
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-        for (int e = warp; e < Q * R; e += nw) {
-            const int b = e % Q, r = e / Q;
-            const double* tcol = T + (size_t)d.q2() * (s * R + r) + (size_t)Q * b;
+        const double* A = d.f(prob, 0) + (size_t)Q * r;
+        double av[MAXA];
+#pragma unroll
+        for (int i = 0; i < MAXA; ++i) {
+            const int a = lane + 32 * i;
+            av[i] = a < Q ? A[a] : 0.0;
+        }
+#pragma unroll 4
+        for (int b = 0; b < Q; ++b) {
+            const double* row = tcol + (size_t)Q * b;
             double acc = 0.0;
-            for (int a = lane; a < Q; a += 32) acc += tcol[a] * A[a + (size_t)Q * r];
+#pragma unroll
+            for (int i = 0; i < MAXA; ++i) {
+                const int a = lane + 32 * i;
+                if (a < Q) acc += __ldg(row + a) * av[i];
+            }
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) M[b + (size_t)Q * r] = acc;
+            if (lane == 0) M[b] = acc;
         }
     }
 }
@@ -392,9 +459,12 @@ __global__ void als_kr_kernel(AlsDev d) {
     }
 }
 
-// One mode update per problem: raw = M V^-1 (COD of the Hadamard Gram),
-// non-finite check, normalize into lambda with seeded rescue, new Gram;
-// after mode 2 the fit and the convergence test.
+// One mode update per problem: raw = M V^-1 (COD of the Hadamard Gram;
+// cp_als.cpp:298-323), non-finite check, normalize into lambda with the
+// seeded rescue, new Gram; after mode 2 the fit and the convergence test
+// (cp_als.cpp:325-345).  V^-1 is formed from the Cholesky factor (or the
+// eigen pseudo-inverse when V is numerically singular, matching COD's
+// minimum-norm solve), then raw = M V^-1 is a parallel (Q x R)(R x R) product.
 __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     const int prob = blockIdx.x;
     AlsState* st = d.state + prob;
@@ -403,12 +473,13 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     extern __shared__ double sm[];
     double* V = sm;                 // R*R
     double* Lf = V + R * R;         // R*R
-    double* Ev = Lf + R * R;        // R*R
-    double* raw = Ev + R * R;       // Q*R
+    double* Ev = Lf + R * R;        // R*R  (eigenvectors / L^-1)
+    double* Vi = Ev + R * R;        // R*R  (V^-1 or V^+)
+    double* raw = Vi + R * R;       // Q*R
     double* nrm = raw + Q * R;      // R
     double* cs = nrm + R;           // 2(R+2)
     double* red = cs + 2 * (R + 2); // blockDim
-    int* flag = (int*)(red + blockDim.x);
+    int* iw = (int*)(red + blockDim.x);  // R + 8
     __shared__ int rank, bad;
     const double* M = d.Mb + (size_t)prob * Q * R;
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
@@ -420,42 +491,53 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     }
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
-    if (threadIdx.x == 0) rank = chol_semidef(R, Lf, R, kEps * R);
+    if (threadIdx.x < 32) {
+        TeamWarp w;
+        int rk;
+        if (R <= 32) {
+            const double md = warp_max_diag(Lf, R, R);
+            rk = warp_chol_inv32(Lf, R, R, md > 0.0 ? kEps * R * md : INFINITY, Ev, R);  // Ev = L^-1
+        } else {
+            rk = team_chol_semidef(w, R, Lf, R, kEps * R, cs, iw);
+            if (rk == R) team_tri_inv_lower(w, R, Lf, R, Ev, R);
+        }
+        if (threadIdx.x == 0) rank = rk;
+    }
     __syncthreads();
     if (rank == R) {
-        for (int q = threadIdx.x; q < Q; q += blockDim.x) {
-            double x[64];
-            for (int c = 0; c < R; ++c) x[c] = M[q + (size_t)Q * c];
-            chol_solve_vec(R, Lf, R, x, 1);
-            for (int c = 0; c < R; ++c) raw[q + Q * c] = x[c];
+        // Vi = L^-T L^-1
+        for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+            const int i = e % R, j = e / R;
+            double s = 0.0;
+            for (int k = (i > j ? i : j); k < R; ++k) s += Ev[k + R * i] * Ev[k + R * j];
+            Vi[e] = s;
         }
     } else {
         TeamDev team;
-        jacobi_eig_sym(team, R, V, Ev, cs, flag);
+        jacobi_eig_sym(team, R, V, Ev, cs, iw);
         __syncthreads();
         double wmax = 0.0;
         for (int i = 0; i < R; ++i) wmax = fmax(wmax, fabs(V[i + R * i]));
         const double thr = kEps * R * wmax;
-        for (int q = threadIdx.x; q < Q; q += blockDim.x) {
-            double x[64], y[64];
-            for (int c = 0; c < R; ++c) {
-                x[c] = M[q + (size_t)Q * c];
-                y[c] = 0.0;
+        for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+            const int i = e % R, j = e / R;
+            double s = 0.0;
+            for (int k = 0; k < R; ++k) {
+                const double w = V[k + R * k];
+                if (w > thr) s += Ev[i + R * k] * Ev[j + R * k] / w;
             }
-            for (int e = 0; e < R; ++e) {
-                const double w = V[e + R * e];
-                if (!(w > thr)) continue;
-                double dot = 0.0;
-                for (int i = 0; i < R; ++i) dot += Ev[i + R * e] * x[i];
-                dot /= w;
-                for (int i = 0; i < R; ++i) y[i] += Ev[i + R * e] * dot;
-            }
-            for (int c = 0; c < R; ++c) raw[q + Q * c] = y[c];
+            Vi[e] = s;
         }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < Q * R; e += blockDim.x)
-        if (!isfinite(raw[e])) bad = 1;
+    // raw = M Vi
+    for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
+        const int q = e % Q, c = e / Q;
+        double s = 0.0;
+        for (int k = 0; k < R; ++k) s += M[q + (size_t)Q * k] * Vi[k + R * c];
+        raw[e] = s;
+        if (!isfinite(s)) bad = 1;
+    }
     __syncthreads();
     if (bad) {
         if (threadIdx.x == 0) {
@@ -468,10 +550,15 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
         }
         return;
     }
-    for (int c = threadIdx.x; c < R; c += blockDim.x) {
-        double s = 0.0;
-        for (int q = 0; q < Q; ++q) s += raw[q + Q * c] * raw[q + Q * c];
-        nrm[c] = sqrt(s);
+    {
+        // column norms: one warp per column
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int c = warp; c < R; c += nw) {
+            double sacc = 0.0;
+            for (int q = lane; q < Q; q += 32) sacc += raw[q + Q * c] * raw[q + Q * c];
+            for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+            if (lane == 0) nrm[c] = sqrt(sacc);
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -504,9 +591,11 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     double* g = d.g(prob, mode);
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
         const int i = e % R, j = e / R;
+        if (i > j) continue;
         double s = 0.0;
         for (int q = 0; q < Q; ++q) s += raw[q + Q * i] * raw[q + Q * j];
-        g[e] = s;
+        g[i + R * j] = s;
+        g[j + R * i] = s;
     }
     __syncthreads();
     if (mode != 2) return;
@@ -605,11 +694,14 @@ struct YtA {  // A(p, c, k) = Y[p][k + Q^2 c]   (Y_(2)^T rows)
     size_t q3, q2;
     __device__ double operator()(int p, int c, int k) const { return Y[(size_t)p * q3 + k + q2 * c]; }
 };
-struct KRB {  // B(p, k, n) = KR[p][k + Q^2 n]
-    const double* K;
-    size_t q2;
-    int SR;
-    __device__ double operator()(int p, int k, int n) const { return K[(size_t)p * q2 * SR + k + q2 * n]; }
+struct KRB {  // B(p, k = a + Q b, n = s R + r) = A_(p,s)(a, r) * B_(p,s)(b, r)  (Khatri-Rao on the fly)
+    const double* F;
+    int S, Q, R;
+    __device__ double operator()(int p, int k, int n) const {
+        const int a = k % Q, b = k / Q, s = n / R, r = n % R;
+        const double* fa = F + ((size_t)(p * S + s) * 3 + 0) * Q * R + (size_t)Q * r;
+        return fa[a] * fa[(size_t)Q * R + b];
+    }
 };
 struct M2Store {  // -> Mb[p S + n/R][c + Q (n%R)]
     double* M;
@@ -820,7 +912,9 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     host_syncs = 0;
 
     // ---- norms, zero-tensor check (cp_als.cpp:255-256)
-    als_norm_kernel<<<P, 256, 0, st>>>(d); OCTEN_LAUNCHED(1);
+    ws.reserve((size_t)P * 64);
+    als_norm_kernel<<<dim3(64, P), 256, 0, st>>>(d, ws.p); OCTEN_LAUNCHED(1);
+    als_norm_finish_kernel<<<(P + 127) / 128, 128, 0, st>>>(d, ws.p, 64); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     std::vector<double> hn = normx2.to_host(P, st);
     ++host_syncs;
@@ -854,20 +948,22 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         usable.upload(ones.data(), P, st);
         const int ks = pick_ksplit(P, Q, Q, (int)q2);
         ws.reserve((size_t)P * ks * q2);
-        gemm_simt<double, double, false, false>(P, Q, Q, (int)q2, Y0A{dY, q3, Q}, Y0B{dY, q3, Q},
+        gemm_f64<false, false>(P, Q, Q, (int)q2, Y0A{dY, q3, Q}, Y0B{dY, q3, Q},
                                                 GevStore{Gev.p, Q, 0}, st, ks, ws.p);
-        gemm_simt<double, double, true, true>(P, Q, Q, (int)q2, Y1A{dY, q3, Q}, Y1B{dY, q3, Q}, GevStore{Gev.p, Q, 1},
+        gemm_f64<true, true>(P, Q, Q, (int)q2, Y1A{dY, q3, Q}, Y1B{dY, q3, Q}, GevStore{Gev.p, Q, 1},
                                               st, ks, ws.p);
-        const size_t smem_eig = q2 * sizeof(double) + 2 * (Q + 2) * sizeof(double) + (4 + Q) * sizeof(int) + 64;
+        size_t smem_eig = (q2 + 2 * (Q + 2)) * sizeof(double) + (2 * Q + 16) * sizeof(int) + 64;
+        const int v_in_smem = (smem_eig + q2 * sizeof(double) <= 220 * 1024) ? 1 : 0;
+        if (v_in_smem) smem_eig += q2 * sizeof(double);
         OCTEN_CUDA(cudaFuncSetAttribute(gevd_eig_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eig));
-        gevd_eig_sym_kernel<<<P * 2, 256, smem_eig, st>>>(d); OCTEN_LAUNCHED(1);
+        gevd_eig_sym_kernel<<<P * 2, 1024, smem_eig, st>>>(d, v_in_smem); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
         // mixtures -> p1/p2 for all attempts
-        gemm_simt<double, double, false, true>(NP, (int)q2, 6, Q, YmatA{dY, q3, q2, S, true}, MixB{Wmix.p, Q},
+        gemm_f64<false, true>(NP, (int)q2, 6, Q, YmatA{dY, q3, q2, S, true}, MixB{Wmix.p, Q},
                                                MixStore{Smix.p, q2}, st);
-        gemm_simt<double, double, false, false>(NP * 6, Q, R, Q, SmA{Smix.p, Q}, UrB{Ur.p, Q, R, S, 1},
+        gemm_f64<false, false>(NP * 6, Q, R, Q, SmA{Smix.p, Q}, UrB{Ur.p, Q, R, S, 1},
                                                 Tmp6Store{Tmp6.p, Q, R}, st);
-        gemm_simt<double, double, true, false>(NP * 6, R, R, Q, UrTA{Ur.p, Q, R, S}, Tmp6B{Tmp6.p, Q, R},
+        gemm_f64<true, false>(NP * 6, R, R, Q, UrTA{Ur.p, Q, R, S}, Tmp6B{Tmp6.p, Q, R},
                                                PmStore{Pm.p, R}, st);
         std::vector<int> hus = usable.to_host(P, st);
         ++host_syncs;
@@ -880,12 +976,12 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             att_start.upload(start.data(), NP, st);
             todo.upload(td.data(), NP, st);
             peel_fail.zero(NP, st);
-            const size_t smem_pen = (size_t)(R * R + R) * sizeof(double);
+            const size_t smem_pen = (size_t)(5 * R * R + 5 * R + 8) * sizeof(double);
             gevd_pencil_kernel<<<NP, 128, smem_pen, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
-            gemm_simt<double, double, false, false>(NP, R, (int)q2, Q, A1tA{F.p, Q, R}, Y0Bp{dY, q3, Q, S},
+            gemm_f64<false, false>(NP, R, (int)q2, Q, A1tA{F.p, Q, R}, Y0Bp{dY, q3, Q, S},
                                                     HStore{Hh.p, R, q2}, st);
-            const size_t smem_h = (size_t)(2 * R * R + 2 * (R + 2)) * sizeof(double) + 16;
+            const size_t smem_h = (size_t)(3 * R * R + 2 * (R + 2)) * sizeof(double) + (R + 8) * sizeof(int) + 16;
             gevd_hsolve_kernel<<<NP, 256, smem_h, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
             const int peel_threads = 128;
@@ -935,8 +1031,8 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     const int SR = S * R;
     const int ks_m2 = pick_ksplit(P, Q, SR, (int)q2);
     ws.reserve(std::max<size_t>(ws.n, (size_t)P * ks_m2 * Q * SR));
-    const int upd_threads = 128;
-    const size_t smem_upd = (size_t)(3 * R * R + Q * R + R + 2 * (R + 2) + upd_threads) * sizeof(double) + 16;
+    const int upd_threads = 256;
+    const size_t smem_upd = (size_t)(4 * R * R + Q * R + R + 2 * (R + 2) + upd_threads) * sizeof(double) + (R + 8) * sizeof(int) + 16;
     OCTEN_CUDA(cudaFuncSetAttribute(als_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_upd));
     int* hcount = nullptr;
     OCTEN_CUDA(cudaMallocHost(&hcount, sizeof(int)));
@@ -944,17 +1040,13 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     for (; sweep < max_iters; ++sweep) {
         active_count.zero(1, st);
         // T = Y x3 C  (Q^2 x SR per replica)
-        gemm_simt<double, double, false, true>(P, (int)q2, SR, Q, YmatA{dY, q3, q2, S, false}, FacB{F.p, S, Q, R, 2},
+        gemm_f64<false, true>(P, (int)q2, SR, Q, YmatA{dY, q3, q2, S, false}, FacB{F.p, S, Q, R, 2},
                                                TStore{T.p, q2, SR}, st);
-        als_mttkrp_T_kernel<<<NP, 256, 0, st>>>(d, 0); OCTEN_LAUNCHED(1);
+        als_mttkrp_T_kernel<<<(NP * R + 7) / 8, 256, 0, st>>>(d, 0); OCTEN_LAUNCHED(1);
         als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 0, sweep); OCTEN_LAUNCHED(1);
-        als_mttkrp_T_kernel<<<NP, 256, 0, st>>>(d, 1); OCTEN_LAUNCHED(1);
+        als_mttkrp_T_kernel<<<(NP * R + 7) / 8, 256, 0, st>>>(d, 1); OCTEN_LAUNCHED(1);
         als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 1, sweep); OCTEN_LAUNCHED(1);
-        {
-            dim3 g((unsigned)std::min<size_t>((q2 * R + 255) / 256, 1024), NP);
-            als_kr_kernel<<<g, 256, 0, st>>>(d); OCTEN_LAUNCHED(1);
-        }
-        gemm_simt<double, double, true, true>(P, Q, SR, (int)q2, YtA{dY, q3, q2}, KRB{KR.p, q2, SR},
+        gemm_f64<true, true>(P, Q, SR, (int)q2, YtA{dY, q3, q2}, KRB{F.p, S, Q, R},
                                               M2Store{Mb.p, S, Q, R}, st, ks_m2, ws.p);
         als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 2, sweep); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());

@@ -15,10 +15,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "engine.hpp"
-#include "gemm_simt.cuh"
+#include "gemm_dmma.cuh"
 #include "tc_gemm.hpp"
 
 namespace octen {
@@ -109,7 +110,8 @@ void run_compress(CompressEngine& e, const T* dX, std::int64_t t, const double* 
         bool done = false;
         OCTEN_CUDA(cudaEventRecord(e.event(2 * e.g1_used), st));
         if constexpr (std::is_same<T, float>::value) {
-            if (use_tc) done = tc_gemm_f32_nt(A, Xc, Z1, (int)e.Meff, (long long)N1, (int)e.I, st);
+            if (use_tc) done = tc_gemm_tf32x3(e.Ahi.p, e.Alo.p, e.lda_tc, Xc, Z1, (int)e.Meff, (long long)N1, (int)e.I, st);
+            e.used_tc = done;
         }
         if (!done)
             gemm_simt<T, T, true, true>(1, (int)e.Meff, (int)N1, (int)e.I, G1A<T>{A, e.I}, G1B<T>{Xc, e.I},
@@ -120,7 +122,7 @@ void run_compress(CompressEngine& e, const T* dX, std::int64_t t, const double* 
         e.gemm1_flops += 2.0 * (double)e.Meff * (double)N1 * (double)e.I;
         gemm_simt<T, T, true, false>(P * tc, Q, Q, (int)e.J, G2A<T>{Z1, e.rowmap.p, N1, e.J, tc, Q},
                                      G2B<T>{V, e.J, tc, Q}, G2C<T>{Z2, tc, Q}, st);
-        gemm_simt<double, double, false, true>(P, Q * Q, Q, tc, G3A<T>{Z2, tc, Q}, G3B{dW, t, k0, Q}, G3C{dY, Q}, st);
+        gemm_f64<false, true>(P, Q * Q, Q, tc, G3A<T>{Z2, tc, Q}, G3B{dW, t, k0, Q}, G3C{dY, Q}, st);
     }
     OCTEN_CUDA(cudaGetLastError());
 }
@@ -170,6 +172,24 @@ void CompressEngine::set_projections(int P_, int Q_, int shared_, std::int64_t I
             for (std::int64_t i = 0; i < I; ++i) a64[(size_t)row * I + i] = u[i];
         }
     std::vector<float> a32(a64.begin(), a64.end());
+    // TF32 hi/lo split of the fp64 projections: hi = fp32 value with the low
+    // 13 mantissa bits cleared, lo = fp32(u - hi)
+    lda_tc = (int)((I + 3) / 4 * 4);
+    std::vector<float> ahi((size_t)Meff * lda_tc, 0.f), alo((size_t)Meff * lda_tc, 0.f);
+    for (std::int64_t m = 0; m < Meff; ++m)
+        for (std::int64_t i = 0; i < I; ++i) {
+            const double u = a64[(size_t)m * I + i];
+            float f = (float)u;
+            uint32_t bits;
+            std::memcpy(&bits, &f, 4);
+            bits &= 0xFFFFE000u;
+            float h;
+            std::memcpy(&h, &bits, 4);
+            ahi[(size_t)m * lda_tc + i] = h;
+            alo[(size_t)m * lda_tc + i] = (float)(u - (double)h);
+        }
+    Ahi.upload(ahi.data(), ahi.size(), st);
+    Alo.upload(alo.data(), alo.size(), st);
     std::vector<float> v32(hV, hV + (size_t)P * J * Q);
     rowmap.upload(rm.data(), rm.size(), st);
     A64.upload(a64.data(), a64.size(), st);

@@ -81,6 +81,9 @@ public:
     int P = 0, Q = 0, shared = 0;
     std::int64_t I = 0, J = 0, Meff = 0;
     DevBuf<float> A32;   // Meff x I row-major (deduplicated shared columns)
+    DevBuf<float> Ahi, Alo;  // TF32 split of the fp64 projections (tcgen05 path)
+    int lda_tc = 0;
+    bool used_tc = false;
     DevBuf<double> A64;  // Meff x I row-major
     DevBuf<float> V32;   // P x J x Q
     DevBuf<double> V64;  // P x J x Q

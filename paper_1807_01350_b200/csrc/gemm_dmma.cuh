@@ -1,0 +1,167 @@
+// Batched fp64 GEMM on the FP64 tensor cores (mma.sync.m8n8k4.f64, the only
+// fp64 MMA on sm_100a: tcgen05 has no f64 kind), with functor-addressed
+// operands so the ALS / merge contractions run on their native layouts.
+//
+//   C(b,m,n) <- sum_k A(b,m,k) B(b,k,n)     (store functor decides = or +=)
+//
+// 64x64 block tile, BK = 16, 8 warps each owning a 32x16 sub-tile (4 x 2
+// m8n8 accumulators), register-staged double buffering of the shared tiles.
+// Deterministic split-K (fixed-order reduction) as in gemm_simt.cuh.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "gemm_simt.cuh"
+#include "octen_common.cuh"
+
+namespace octen {
+
+__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
+    asm volatile(
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+template <bool A_KFAST, bool B_KFAST, class AF, class BF, class CF>
+__global__ void __launch_bounds__(256)
+    gemm_dmma_kernel(int M, int N, int K, int ksplit, int kchunk, AF af, BF bf, CF cf, double* partial,
+                     int lower_only) {
+    constexpr int BM = 64, BN = 64, BK = 16, PAD = 4;
+    __shared__ double As[2][BK][BM + PAD];
+    __shared__ double Bs[2][BK][BN + PAD];
+    if (lower_only && (int)(blockIdx.x * BN) >= (int)(blockIdx.y * BM + BM)) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+    const int zb = blockIdx.z;
+    const int batch = zb / ksplit, ks = zb % ksplit;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int kbeg = ks * kchunk;
+    const int kend = min(K, kbeg + kchunk);
+
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    double ra[4], rb[4];
+    auto load = [&](int k0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int e = tid + r * 256;
+            int mm, kk;
+            if (A_KFAST) {
+                kk = e % BK;
+                mm = e / BK;
+            } else {
+                mm = e % BM;
+                kk = e / BM;
+            }
+            const int gm = m0 + mm, gk = k0 + kk;
+            ra[r] = (gm < M && gk < kend) ? (double)af(batch, gm, gk) : 0.0;
+            int nn, kb;
+            if (B_KFAST) {
+                kb = e % BK;
+                nn = e / BK;
+            } else {
+                nn = e % BN;
+                kb = e / BN;
+            }
+            const int gn = n0 + nn, gk2 = k0 + kb;
+            rb[r] = (gn < N && gk2 < kend) ? (double)bf(batch, gk2, gn) : 0.0;
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int e = tid + r * 256;
+            int mm, kk;
+            if (A_KFAST) {
+                kk = e % BK;
+                mm = e / BK;
+            } else {
+                mm = e % BM;
+                kk = e / BM;
+            }
+            As[buf][kk][mm] = ra[r];
+            int nn, kb;
+            if (B_KFAST) {
+                kb = e % BK;
+                nn = e / BK;
+            } else {
+                nn = e % BN;
+                kb = e / BN;
+            }
+            Bs[buf][kb][nn] = rb[r];
+        }
+    };
+
+    int buf = 0;
+    if (kbeg < kend) {
+        load(kbeg);
+        store(0);
+    }
+    __syncthreads();
+    for (int k0 = kbeg; k0 < kend; k0 += BK) {
+        const bool more = k0 + BK < kend;
+        if (more) load(k0 + BK);
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double a[4], b[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[buf][kk + t4][wm + i * 8 + g];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) b[j] = Bs[buf][kk + t4][wn + j * 8 + g];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+        if (more) {
+            store(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int gm = m0 + wm + i * 8 + g, gn = n0 + wn + j * 8 + 2 * t4 + v;
+                if (gm < M && gn < N) {
+                    if (ksplit == 1)
+                        cf(batch, gm, gn, acc[i][j][v]);
+                    else
+                        partial[(((size_t)batch * ksplit + ks) * M + gm) * N + gn] = acc[i][j][v];
+                }
+            }
+}
+
+// Same interface as gemm_simt (fp64 only).
+template <bool A_KFAST, bool B_KFAST, class AF, class BF, class CF>
+void gemm_f64(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaStream_t st, int ksplit = 1,
+              double* workspace = nullptr, int lower_only = 0) {
+    if (batches <= 0 || M <= 0 || N <= 0) return;
+    if (K <= 0) ksplit = 1;
+    if (ksplit < 1) ksplit = 1;
+    int kchunk = (K + ksplit - 1) / ksplit;
+    kchunk = ((kchunk + 15) / 16) * 16;
+    if (kchunk < 16) kchunk = 16;
+    dim3 grid((N + 63) / 64, (M + 63) / 64, batches * ksplit);
+    gemm_dmma_kernel<A_KFAST, B_KFAST><<<grid, 256, 0, st>>>(M, N, K, ksplit, kchunk, af, bf, cf, workspace,
+                                                             lower_only);
+    OCTEN_LAUNCHED(1);
+    if (ksplit > 1) {
+        const size_t total = (size_t)batches * M * N;
+        int blocks = (int)((total + 255) / 256);
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        gemm_splitk_reduce<double><<<blocks, 256, 0, st>>>(batches, M, N, ksplit, workspace, cf);
+        OCTEN_LAUNCHED(1);
+    }
+}
+
+}  // namespace octen

@@ -19,8 +19,11 @@ namespace octen {
 template <typename TIn, typename Acc, int BM, int BN, int BK, int TM, int TN, bool A_KFAST, bool B_KFAST,
           class AF, class BF, class CF>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
-    gemm_simt_kernel(int M, int N, int K, int ksplit, int kchunk, AF af, BF bf, CF cf, Acc* partial) {
+    gemm_simt_kernel(int M, int N, int K, int ksplit, int kchunk, AF af, BF bf, CF cf, Acc* partial,
+                     int lower_only) {
     constexpr int NT = (BM / TM) * (BN / TN);
+    // lower_only: skip output tiles strictly above the diagonal (m < n everywhere)
+    if (lower_only && (int)(blockIdx.x * BN) >= (int)(blockIdx.y * BM + BM)) return;
     __shared__ Acc As[BK][BM + 1];
     __shared__ Acc Bs[BK][BN + 1];
     const int tid = threadIdx.x;
@@ -109,7 +112,7 @@ __global__ void gemm_splitk_reduce(int batches, int M, int N, int ksplit, const 
 // Host launcher.  workspace must hold batches*ksplit*M*N Acc when ksplit > 1.
 template <typename TIn, typename Acc, bool A_KFAST, bool B_KFAST, class AF, class BF, class CF>
 void gemm_simt(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaStream_t st, int ksplit = 1,
-               Acc* workspace = nullptr) {
+               Acc* workspace = nullptr, int lower_only = 0) {
     if (batches <= 0 || M <= 0 || N <= 0) return;
     if (K <= 0) {
         ksplit = 1;
@@ -120,7 +123,8 @@ void gemm_simt(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaStream
     constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
     dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batches * ksplit);
     gemm_simt_kernel<TIn, Acc, BM, BN, BK, TM, TN, A_KFAST, B_KFAST>
-        <<<grid, (BM / TM) * (BN / TN), 0, st>>>(M, N, K, ksplit, kchunk, af, bf, cf, workspace); OCTEN_LAUNCHED(1);
+        <<<grid, (BM / TM) * (BN / TN), 0, st>>>(M, N, K, ksplit, kchunk, af, bf, cf, workspace,
+                                                              lower_only); OCTEN_LAUNCHED(1);
     if (ksplit > 1) {
         const size_t total = (size_t)batches * M * N;
         int blocks = (int)((total + 255) / 256);

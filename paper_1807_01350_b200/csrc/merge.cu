@@ -24,7 +24,7 @@
 
 #include "chol_batched.cuh"
 #include "engine.hpp"
-#include "gemm_simt.cuh"
+#include "gemm_dmma.cuh"
 #include "small_linalg.cuh"
 
 namespace octen {
@@ -782,10 +782,10 @@ void MergeEngine::set_projections(int P_, int Q_, int sh, int R_, std::int64_t I
         const long long d = dims[n];
         Ud[n].upload(n == 0 ? hU : hV, (size_t)P * d * Q, st);
         Gp[n].reserve((size_t)P * d * d);
-        gemm_simt<double, double, false, false>(P, (int)d, (int)d, Q, UcatA{Ud[n].p, d, d * Q}, UcatB{Ud[n].p, d, d * Q},
+        gemm_f64<false, false>(P, (int)d, (int)d, Q, UcatA{Ud[n].p, d, d * Q}, UcatB{Ud[n].p, d, d * Q},
                                                 StoreCM{Gp[n].p, d, d * d}, st);
         Lsum[n].reserve((size_t)d * d);
-        gemm_simt<double, double, false, false>(1, (int)d, (int)d, (int)PQ, UcatA{Ud[n].p, d, 0}, UcatB{Ud[n].p, d, 0},
+        gemm_f64<false, false>(1, (int)d, (int)d, (int)PQ, UcatA{Ud[n].p, d, 0}, UcatB{Ud[n].p, d, 0},
                                                 StoreCM{Lsum[n].p, d, 0}, st);
         maxdiag.reserve(128);
         ranks.reserve(128);
@@ -893,10 +893,10 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
             }
             chol_batched(Gj.p, (int)d, (int)d, d * d, P, 1e-15, md.p, rk.p, st);
             // g1 = U_0 RF_0[n]  (d x R)
-            gemm_simt<double, double, false, true>(1, (int)d, R, Q, UcatA{Ud[n].p, d, 0},
+            gemm_f64<false, true>(1, (int)d, R, Q, UcatA{Ud[n].p, d, 0},
                                                    ColB{RF.p + (size_t)n * Q * R, Q, 0}, StoreCM{g1.p, d, 0}, st);
             // g2_p = U_p RF_p[n]
-            gemm_simt<double, double, false, true>(P, (int)d, R, Q, UcatA{Ud[n].p, d, d * Q},
+            gemm_f64<false, true>(P, (int)d, R, Q, UcatA{Ud[n].p, d, d * Q},
                                                    ColB{RF.p + (size_t)n * Q * R, Q, 3LL * Q * R},
                                                    StoreCM{g2.p, d, d * R}, st);
             for (int p = 0; p < P; ++p)
@@ -944,7 +944,7 @@ void MergeEngine::solve_nontemporal(int n, const double* dStack, double* dOut, c
     if (sum_rank[n] < d)
         throw NumericError("recover: rank-deficient projection on mode " + std::to_string(n + 1) + " (rank " +
                            std::to_string(sum_rank[n]) + " of " + std::to_string(d) + ")");
-    gemm_simt<double, double, false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{dStack, PQ, 0},
+    gemm_f64<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{dStack, PQ, 0},
                                            StoreCM{dOut, d, 0}, st);
     chol_solve_batched(Lsum[n].p, (int)d, (int)d, 0, dOut, (int)d, 0, R, 1, st);
 }
@@ -955,16 +955,16 @@ void MergeEngine::temporal_stack(const double* dY, const double* dA, const doubl
     tg.reserve((size_t)P * 2 * Q * R);
     double* Ut = tg.p;
     double* Vt = tg.p + (size_t)P * Q * R;
-    gemm_simt<double, double, true, true>(P, Q, R, (int)dims[0], UtA{Ud[0].p, dims[0], Q}, ColB{dA, dims[0], 0},
+    gemm_f64<true, true>(P, Q, R, (int)dims[0], UtA{Ud[0].p, dims[0], Q}, ColB{dA, dims[0], 0},
                                           StoreCM{Ut, Q, (long long)Q * R}, st);
-    gemm_simt<double, double, true, true>(P, Q, R, (int)dims[1], UtA{Ud[1].p, dims[1], Q}, ColB{dB, dims[1], 0},
+    gemm_f64<true, true>(P, Q, R, (int)dims[1], UtA{Ud[1].p, dims[1], Q}, ColB{dB, dims[1], 0},
                                           StoreCM{Vt, Q, (long long)Q * R}, st);
     tmp.reserve((size_t)P * Q * R);
     const int ks = pick_ksplit(P, Q, R, (int)q2);
     tscr.reserve((size_t)P * ks * Q * R);
-    gemm_simt<double, double, true, true>(P, Q, R, (int)q2, YtA2{dY, q3, q2}, KrB{Ut, Vt, Q, R},
+    gemm_f64<true, true>(P, Q, R, (int)q2, YtA2{dY, q3, q2}, KrB{Ut, Vt, Q, R},
                                           StoreCM{tmp.p, Q, (long long)Q * R}, st, ks, tscr.p);
-    const size_t smem = (size_t)(3 * R * R + 2 * (R + 2)) * sizeof(double) + 16;
+    const size_t smem = (size_t)(3 * R * R + 2 * (R + 2)) * sizeof(double) + (R + 8) * sizeof(int) + 16;
     tstack_solve_kernel<<<P, 128, smem, st>>>(P, Q, R, Ut, Vt, tmp.p, dTstack); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
 }
@@ -986,13 +986,13 @@ void MergeEngine::temporal_append(const double* dTstack, const double* dW, std::
     err.reserve(P + 1 + 64);
     err.zero(R, st);
     // Gc = Pc^T Pc = sum_{(p,a)} W_p[:,a] W_p[:,a]^T ; W as t x PQ col-major
-    gemm_simt<double, double, false, false>(1, (int)t, (int)t, (int)PQ, UcatA{dW, t, 0}, UcatB{dW, t, 0},
+    gemm_f64<false, false>(1, (int)t, (int)t, (int)PQ, UcatA{dW, t, 0}, UcatB{dW, t, 0},
                                             StoreCM{Gc.p, t, 0}, st);
     chol_batched(Gc.p, (int)t, (int)t, 0, 1, kGramRankTol, md.p, rk.p, st);
     // [bv | hv] = Pc^T [tstack | hist]
-    gemm_simt<double, double, false, true>(1, (int)t, R, (int)PQ, UcatA{dW, t, 0}, ColB{dTstack, PQ, 0},
+    gemm_f64<false, true>(1, (int)t, R, (int)PQ, UcatA{dW, t, 0}, ColB{dTstack, PQ, 0},
                                            StoreCM{BZ.p, t, 0}, st);
-    gemm_simt<double, double, false, true>(1, (int)t, R, (int)PQ, UcatA{dW, t, 0}, ColB{dHist, PQ, 0},
+    gemm_f64<false, true>(1, (int)t, R, (int)PQ, UcatA{dW, t, 0}, ColB{dHist, PQ, 0},
                                            StoreCM{BZ.p + (size_t)t * R, t, 0}, st);
     DevBuf<double> hv;
     hv.reserve((size_t)t * R);
@@ -1005,7 +1005,7 @@ void MergeEngine::temporal_append(const double* dTstack, const double* dW, std::
     OCTEN_CUDA(cudaGetLastError());
     check_errs(err, R, st);
     // Ps = Pc * rows (PQ x R)
-    gemm_simt<double, double, true, true>(1, (int)PQ, R, (int)t, UtA{dW, t, (int)PQ}, ColB{dRows, t, 0},
+    gemm_f64<true, true>(1, (int)PQ, R, (int)t, UtA{dW, t, (int)PQ}, ColB{dRows, t, 0},
                                           StoreCM{Ps.p, PQ, 0}, st);
     append_resid_kernel<<<R, 256, 0, st>>>(PQ, dTstack, dHist, Ps.p, coef.p, res.p); OCTEN_LAUNCHED(1);
     std::vector<double> hr = res.to_host(R, st);
@@ -1040,7 +1040,7 @@ void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, do
         for (int n = 0; n < 2; ++n) {
             const long long d = dims[n];
             // tg[p][n] = U_p^T solved_n  (Q x R)
-            gemm_simt<double, double, true, true>(P, Q, R, (int)d, UtA{Ud[n].p, d, Q}, ColB{solved[n].p, d, 0},
+            gemm_f64<true, true>(P, Q, R, (int)d, UtA{Ud[n].p, d, Q}, ColB{solved[n].p, d, 0},
                                                   StoreCM{tg.p + (size_t)n * Q * R, Q, 2LL * Q * R}, st);
         }
         const size_t smem = (size_t)(2 * Q * R + R) * sizeof(double);
@@ -1060,7 +1060,7 @@ void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, do
             chol_batched(Gw.p, (int)d, (int)d, d * d, R, kGramRankTol, maxdiag.p, ranks.p, st);
             scale_stack_kernel<<<grid_for((size_t)PQ * R), 256, 0, st>>>(P, Q, R, stacks.p + (size_t)n * PQ * R, w.p,
                                                                         sw.p); OCTEN_LAUNCHED(1);
-            gemm_simt<double, double, false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{sw.p, PQ, 0},
+            gemm_f64<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{sw.p, PQ, 0},
                                                    StoreCM{solved[n].p, d, 0}, st);
             std::vector<int> rk = ranks.to_host(R, st);
             for (int r = 0; r < R; ++r)

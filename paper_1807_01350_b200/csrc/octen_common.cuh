@@ -39,6 +39,12 @@ struct TeamDev {
     __device__ int size() const { return (int)blockDim.x; }
     __device__ void sync() const { __syncthreads(); }
 };
+// One warp as a team (lanes 0..31); sync is a warp barrier.
+struct TeamWarp {
+    __device__ int tid() const { return (int)(threadIdx.x & 31); }
+    __device__ int size() const { return 32; }
+    __device__ void sync() const { __syncwarp(); }
+};
 #endif
 struct TeamHost {
     int tid() const { return 0; }

@@ -156,6 +156,125 @@ OCTEN_HD inline int chol_semidef(int n, double* a, int lda, double tol) {
     return rank;
 }
 
+// Team-parallel version of chol_semidef (right-looking, rows over the team).
+// sc: 1 double + 2 ints of shared scratch.  Returns the rank to every thread.
+// thr_abs >= 0 replaces tol * max(diag) as the absolute pivot threshold.
+template <class Team>
+OCTEN_HD int team_chol_semidef(const Team& team, int n, double* a, int lda, double tol, double* sc, int* irank,
+                               double thr_abs = -1.0) {
+    if (team.tid() == 0) {
+        double maxd = 0.0;
+        for (int i = 0; i < n; ++i) maxd = fmax(maxd, a[i + (size_t)lda * i]);
+        sc[0] = thr_abs >= 0.0 ? 1.0 : maxd;
+        *irank = 0;
+    }
+    team.sync();
+    const double maxd = sc[0];
+    const double thr = thr_abs >= 0.0 ? thr_abs : tol * maxd;
+    for (int k = 0; k < n; ++k) {
+        const double d = a[k + (size_t)lda * k];
+        const bool dead = !(d > thr) || !(maxd > 0.0);
+        const double piv = dead ? 0.0 : sqrt(d);
+        team.sync();
+        for (int i = k + team.tid(); i < n; i += team.size())
+            a[i + (size_t)lda * k] = dead ? 0.0 : (i == k ? piv : a[i + (size_t)lda * k] / piv);
+        team.sync();
+        if (!dead) {
+            for (int i = k + 1 + team.tid(); i < n; i += team.size()) {
+                const double lik = a[i + (size_t)lda * k];
+                for (int j = k + 1; j <= i; ++j) a[i + (size_t)lda * j] -= lik * a[j + (size_t)lda * k];
+            }
+        }
+        if (team.tid() == 0 && !dead) ++*irank;
+        team.sync();
+    }
+    const int r = *irank;
+    team.sync();
+    return r;
+}
+
+// Inverse of a lower-triangular n x n matrix (column j per team thread);
+// zero pivots give zero rows/columns.  x: n x n (ld ldx), may alias nothing.
+template <class Team>
+OCTEN_HD void team_tri_inv_lower(const Team& team, int n, const double* l, int ldl, double* x, int ldx) {
+    for (int j = team.tid(); j < n; j += team.size())
+        for (int i = 0; i < n; ++i) {
+            double v = (i == j) ? 1.0 : 0.0;
+            for (int p = j; p < i; ++p) v -= l[i + (size_t)ldl * p] * x[p + (size_t)ldx * j];
+            const double d = l[i + (size_t)ldl * i];
+            x[i + (size_t)ldx * j] = (i < j || d == 0.0) ? 0.0 : v / d;
+        }
+    team.sync();
+}
+
+#if defined(__CUDACC__)
+// Warp Cholesky + triangular inverse of an n x n (n <= 32) symmetric block in
+// shared memory (column-major, ld lds; lower part read).  Left-looking: for
+// column j, lane i > j forms L_ij from independent loads of rows i and j (no
+// load/store chains), one reciprocal per column.  Loops are kept rolled: an
+// unrolled version overflows the instruction cache (executed once per
+// launch).  s is overwritten with L (upper zeroed), x (ld ldx) receives L^-1.
+// A pivot <= thr marks a deficient column (zeroed, as chol_semidef).  Returns
+// the rank; must be called by all 32 lanes of one warp.
+__device__ inline int warp_chol_inv32(double* s, int lds, int n, double thr, double* x, int ldx) {
+    const int lane = threadIdx.x & 31;
+    int rank = 0;
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+        // diagonal: L_jj^2 = a_jj - sum_{p<j} L_jp^2 (every lane computes it)
+        double d = s[j + (size_t)lds * j];
+#pragma unroll 4
+        for (int p = 0; p < j; ++p) {
+            const double l = s[j + (size_t)lds * p];
+            d -= l * l;
+        }
+        const bool dead = !(d > thr);
+        const double piv = dead ? 0.0 : sqrt(d);
+        const double rp = dead ? 0.0 : 1.0 / piv;
+        double lij = 0.0;
+        const int i = lane;
+        if (i > j && i < n) {
+            double v = s[i + (size_t)lds * j];
+#pragma unroll 4
+            for (int p = 0; p < j; ++p) v -= s[i + (size_t)lds * p] * s[j + (size_t)lds * p];
+            lij = v * rp;
+        }
+        __syncwarp();
+        if (i > j && i < n) s[i + (size_t)lds * j] = lij;
+        if (i == j) s[j + (size_t)lds * j] = piv;
+        if (i < j && i < n) s[i + (size_t)lds * j] = 0.0;
+        rank += dead ? 0 : 1;
+        __syncwarp();
+    }
+    // inverse: lane j owns column j of L^-1
+    if (lane < n) {
+        const int j = lane;
+#pragma unroll 1
+        for (int i = 0; i < n; ++i) {
+            double v = (i == j) ? 1.0 : 0.0;
+            if (i > j) {
+#pragma unroll 4
+                for (int p = j; p < i; ++p) v -= s[i + (size_t)lds * p] * x[p + (size_t)ldx * j];
+            }
+            const double lii = s[i + (size_t)lds * i];
+            x[i + (size_t)ldx * j] = (i < j || lii == 0.0) ? 0.0 : v / lii;
+        }
+    }
+    __syncwarp();
+    return rank;
+}
+#endif
+
+#if defined(__CUDACC__)
+// max of the diagonal of an n x n matrix, reduced over one warp (all lanes get it)
+__device__ inline double warp_max_diag(const double* a, int lda, int n) {
+    double m = 0.0;
+    for (int i = threadIdx.x & 31; i < n; i += 32) m = fmax(m, a[i + (size_t)lda * i]);
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    return m;
+}
+#endif
+
 // Solve L L^T x = b in place for one vector (full-rank factor from chol_semidef).
 OCTEN_HD inline void chol_solve_vec(int n, const double* l, int ldl, double* x, int incx) {
     for (int i = 0; i < n; ++i) {
@@ -629,23 +748,35 @@ OCTEN_HD inline bool eig_real(int nn, double* hm, double* vm, double* wr, double
 // of one round-robin round act on disjoint index pairs, so every 2x2 block of
 // A' = G^T A G and every row pair of V' = V G updates independently.  On
 // return the diagonal of `a` holds the eigenvalues and the columns of `v`
-// (ld n) the eigenvectors.  scratch: 2*(n+1) doubles + 1 int (shared).
+// (ld n) the eigenvectors.  Scratch (shared): cs = 2*(n+2) doubles,
+// iw = n + 4 ints (iw[0] is the sweep flag, iw[2..] the round's pair table).
 // ---------------------------------------------------------------------------
 template <class Team>
-OCTEN_HD void jacobi_eig_sym(const Team& team, int n, double* a, double* v, double* cs, int* flag,
+OCTEN_HD void jacobi_eig_sym(const Team& team, int n, double* a, double* v, double* cs, int* iw,
                              int max_sweeps = 40) {
     const int m = (n % 2) ? n + 1 : n;  // padded player count (index n is a dummy)
     const int half = m / 2;
+    int* flag = iw;
+    int* pp = iw + 2;         // half entries
+    int* qq = iw + 2 + half;  // half entries
     for (int idx = team.tid(); idx < n * n; idx += team.size())
         v[idx] = ((idx % n) == (idx / n)) ? 1.0 : 0.0;
     team.sync();
     double* cc = cs;
     double* ss = cs + half;
     for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-        if (team.tid() == 0) *flag = 0;
+        if (team.tid() == 0) {
+            *flag = 0;
+            double dm = 0.0;
+            for (int i = 0; i < n; ++i) dm = fmax(dm, fabs(a[i + n * i]));
+            cs[2 * half] = dm;
+        }
         team.sync();
+        // rotate only pairs whose coupling exceeds 1e-15 of the largest
+        // diagonal (dominant-subspace accuracy; tiny eigenpairs are not refined)
+        const double skip = 1e-15 * cs[2 * half];
         for (int round = 0; round < m - 1; ++round) {
-            // pair k: k==0 -> (round, m-1); else ((round+k) % (m-1), (round-k+m-1) % (m-1))
+            // circle method: k==0 -> (round, m-1); else ((round+k) % (m-1), (round-k+m-1) % (m-1))
             for (int k = team.tid(); k < half; k += team.size()) {
                 int p, q;
                 if (k == 0) {
@@ -664,7 +795,7 @@ OCTEN_HD void jacobi_eig_sym(const Team& team, int n, double* a, double* v, doub
                 if (q < n) {
                     const double apq = a[p + n * q];
                     const double app = a[p + n * p], aqq = a[q + n * q];
-                    if (fabs(apq) > 1e-300 && fabs(apq) > 1e-17 * sqrt(fabs(app) * fabs(aqq))) {
+                    if (fabs(apq) > 1e-300 && fabs(apq) > skip && fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
                         const double theta = (aqq - app) / (2.0 * apq);
                         double t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
                         if (theta < 0.0) t = -t;
@@ -675,36 +806,14 @@ OCTEN_HD void jacobi_eig_sym(const Team& team, int n, double* a, double* v, doub
                 }
                 cc[k] = c;
                 ss[k] = s;
+                pp[k] = p;
+                qq[k] = q;
             }
             team.sync();
             // A' = G^T A G on 2x2 blocks (pair k1 rows, pair k2 cols)
             for (int blk = team.tid(); blk < half * half; blk += team.size()) {
                 const int k1 = blk % half, k2 = blk / half;
-                int p1, q1, p2, q2;
-                if (k1 == 0) {
-                    p1 = round;
-                    q1 = m - 1;
-                } else {
-                    p1 = (round + k1) % (m - 1);
-                    q1 = (round - k1 + m - 1) % (m - 1);
-                }
-                if (p1 > q1) {
-                    const int tt = p1;
-                    p1 = q1;
-                    q1 = tt;
-                }
-                if (k2 == 0) {
-                    p2 = round;
-                    q2 = m - 1;
-                } else {
-                    p2 = (round + k2) % (m - 1);
-                    q2 = (round - k2 + m - 1) % (m - 1);
-                }
-                if (p2 > q2) {
-                    const int tt = p2;
-                    p2 = q2;
-                    q2 = tt;
-                }
+                const int p1 = pp[k1], q1 = qq[k1], p2 = pp[k2], q2 = qq[k2];
                 const double c1 = cc[k1], s1 = ss[k1], c2 = cc[k2], s2 = ss[k2];
                 if (q1 < n && q2 < n) {
                     const double b00 = a[p1 + n * p2], b01 = a[p1 + n * q2];
@@ -740,19 +849,7 @@ OCTEN_HD void jacobi_eig_sym(const Team& team, int n, double* a, double* v, doub
             // V' = V G : columns (p,q) of every row
             for (int e = team.tid(); e < n * half; e += team.size()) {
                 const int row = e % n, k = e / n;
-                int p, q;
-                if (k == 0) {
-                    p = round;
-                    q = m - 1;
-                } else {
-                    p = (round + k) % (m - 1);
-                    q = (round - k + m - 1) % (m - 1);
-                }
-                if (p > q) {
-                    const int tt = p;
-                    p = q;
-                    q = tt;
-                }
+                const int p = pp[k], q = qq[k];
                 if (q >= n) continue;
                 const double c = cc[k], s = ss[k];
                 const double vp = v[row + n * p], vq = v[row + n * q];

@@ -1,9 +1,336 @@
-// tcgen05 split-TF32 GEMM (see tc_gemm.hpp).  Round-1 bring-up: not yet
-// enabled; the SIMT path carries the contraction.
+// tcgen05 split-TF32 GEMM for the dense compression's mode-1 contraction
+// (reference: the mode-0 product of compress(), compression.cpp:117-128 /
+// tensor.cpp:168-178, batched over all replicas with the shared columns
+// deduplicated):
+//
+//     Z[m, n] = sum_k A[m, k] * X[k + K n]        (A: Meff x K, X: K x N, fp32)
+//
+// fp32 accuracy from the TF32 tensor cores: A = A_hi + A_lo (pre-split once
+// per stream from the fp64 projections), X = X_hi + X_lo (split in shared
+// memory right after the TMA lands), D += A_hi X_hi + A_hi X_lo + A_lo X_hi,
+// fp32 accumulation in TMEM.  Per CTA one 128 x 256 output tile:
+//   warp 0      TMA producer (A_hi, A_lo, X tiles; 128B swizzle, 2 stages)
+//   warp 1      TMEM allocation + single-thread tcgen05.mma issue
+//   warps 2..7  split X into hi/lo in place (same swizzled layout)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b.x32 -> fp32 stores
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "errors.hpp"
+#include "octen_common.cuh"
 #include "tc_gemm.hpp"
 
 namespace octen {
 
-bool tc_gemm_f32_nt(const float*, const float*, float*, int, long long, int, cudaStream_t) { return false; }
+namespace {
+
+constexpr int BM = 128, BN = 256, BKB = 128;  // BK in bytes (32 fp32)
+constexpr int BK = BKB / 4;
+constexpr int STAGES = 2;
+constexpr int A_BYTES = BM * BKB;              // 16 KB
+constexpr int B_BYTES = BN * BKB;              // 32 KB
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B(hi in place), B_lo
+constexpr int NUM_THREADS = 256;
+constexpr int CONVERT_WARP0 = 2, CONVERT_WARPS = 6;
+constexpr uint32_t TMEM_COLS = 256;
+
+// ---- PTX helpers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    const uint32_t addr = smem_u32(bar);
+    for (uint32_t it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(addr), "r"(phase)
+            : "memory");
+        if (ok) return;
+        if (it > (1u << 26)) asm volatile("trap;");
+    }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
+    d |= (uint64_t)1 << 16;                         // leading byte offset (unused for SW128 K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;               // stride byte offset
+    d |= (uint64_t)1 << 46;                         // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                         // layout: SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, A/B K-major, M=128, N=256.
+constexpr uint32_t make_idesc() {
+    return (1u << 4)                // D format F32
+           | (2u << 7)              // A format TF32
+           | (2u << 10)             // B format TF32
+           | ((uint32_t)(BN >> 3) << 17)  // N
+           | ((uint32_t)(BM >> 4) << 24); // M
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(dtmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                          const __grid_constant__ CUtensorMap map_x, float* __restrict__ Z, int M, long long N, int K,
+                          long long ldz) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-align the stage buffers (SW128 atoms)
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full_bar = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+    uint64_t* conv_bar = full_bar + STAGES;
+    uint64_t* empty_bar = conv_bar + STAGES;
+    uint64_t* done_bar = empty_bar + STAGES;
+    uint32_t* tmem_slot = (uint32_t*)(done_bar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m_tile = blockIdx.y, n_tile = blockIdx.x;
+    const int m0 = m_tile * BM;
+    const long long n0 = (long long)n_tile * BN;
+    const int num_kb = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&conv_bar[s], CONVERT_WARPS * 32);
+            mbar_init(&empty_bar[s], 1);
+        }
+        mbar_init(done_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---- TMA producer ----
+            for (int kb = 0; kb < num_kb; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                if (kb >= STAGES) mbar_wait(&empty_bar[s], ph ^ 1);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                mbar_arrive_expect_tx(&full_bar[s], 2 * A_BYTES + B_BYTES);
+                tma_load_2d(st, &map_ahi, &full_bar[s], kb * BK, m0);
+                tma_load_2d(st + A_BYTES, &map_alo, &full_bar[s], kb * BK, m0);
+                tma_load_2d(st + 2 * A_BYTES, &map_x, &full_bar[s], kb * BK, (int)n0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---- MMA issuer ----
+            constexpr uint32_t idesc = make_idesc();
+            for (int kb = 0; kb < num_kb; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(&conv_bar[s], ph);
+                tc_fence_after();
+                uint8_t* st = smem + s * STAGE_BYTES;
+                const uint32_t a_hi = smem_u32(st), a_lo = smem_u32(st + A_BYTES);
+                const uint32_t b_hi = smem_u32(st + 2 * A_BYTES), b_lo = smem_u32(st + 2 * A_BYTES + B_BYTES);
+#pragma unroll
+                for (int k = 0; k < BK / 8; ++k) {
+                    const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
+                    const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+                    mma_tf32(tmem_base, make_desc_sw128(a_hi + off), make_desc_sw128(b_hi + off), idesc, acc0);
+                    mma_tf32(tmem_base, make_desc_sw128(a_hi + off), make_desc_sw128(b_lo + off), idesc, 1u);
+                    mma_tf32(tmem_base, make_desc_sw128(a_lo + off), make_desc_sw128(b_hi + off), idesc, 1u);
+                }
+                mma_commit(&empty_bar[s]);
+            }
+            mma_commit(done_bar);
+        }
+    } else {
+        // ---- X hi/lo split (warps 2..7) ----
+        const int ct = threadIdx.x - CONVERT_WARP0 * 32;
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int s = kb % STAGES;
+            const uint32_t ph = (kb / STAGES) & 1;
+            mbar_wait(&full_bar[s], ph);
+            uint8_t* st = smem + s * STAGE_BYTES;
+            float4* bx = (float4*)(st + 2 * A_BYTES);
+            float4* bl = (float4*)(st + 2 * A_BYTES + B_BYTES);
+            for (int i = ct; i < B_BYTES / 16; i += CONVERT_WARPS * 32) {
+                float4 v = bx[i];
+                float4 h, l;
+                h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                l.x = v.x - h.x;
+                l.y = v.y - h.y;
+                l.z = v.z - h.z;
+                l.w = v.w - h.w;
+                bx[i] = h;
+                bl[i] = l;
+            }
+            fence_proxy_async();
+            mbar_arrive(&conv_bar[s]);
+        }
+        if (warp >= 4) {
+            // ---- epilogue ----
+            mbar_wait(done_bar, 0);
+            tc_fence_after();
+            const int q = warp & 3;
+            const int row = m0 + q * 32 + lane;
+            float* zrow = Z + (size_t)row * ldz;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (row < M) {
+                    const long long nb = n0 + c0;
+                    if (nb + 32 <= N && (ldz % 4) == 0) {
+                        float4* dst = (float4*)(zrow + nb);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                    } else {
+                        for (int j = 0; j < 32; ++j)
+                            if (nb + j < N) zrow[nb + j] = __uint_as_float(r[j]);
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    }
+}
+
+// ---- host: tensor maps through the driver entry point (no libcuda link) ----
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    });
+    return fn;
+}
+
+bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+              uint32_t box_inner, uint32_t box_outer) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool g_disabled = false;
+
+}  // namespace
+
+bool tc_gemm_available() {
+    if (g_disabled) return false;
+    if (std::getenv("OCTEN_DISABLE_TCGEN05")) return false;
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    return major == 10 && minor == 0 && get_encode() != nullptr;
+}
+
+bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X, float* Z, int M, long long N, int K,
+                    cudaStream_t st) {
+    if (!tc_gemm_available()) return false;
+    if ((K % 4) != 0 || (lda % 4) != 0 || ((uintptr_t)X % 16) != 0 || ((uintptr_t)Ahi % 16) != 0 ||
+        ((uintptr_t)Alo % 16) != 0 || N > (1LL << 31) - 1 || M <= 0 || N <= 0 || K <= 0)
+        return false;
+    CUtensorMap mhi, mlo, mx;
+    if (!make_map(&mhi, Ahi, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 4, BK, BM)) return false;
+    if (!make_map(&mlo, Alo, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 4, BK, BM)) return false;
+    if (!make_map(&mx, X, (uint64_t)K, (uint64_t)N, (uint64_t)K * 4, BK, BN)) return false;
+    const size_t smem = STAGES * STAGE_BYTES + 1024 + 256;
+    static bool attr = false;
+    if (!attr) {
+        OCTEN_CUDA(cudaFuncSetAttribute(tc_gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+    tc_gemm_tf32x3_kernel<<<grid, NUM_THREADS, smem, st>>>(mhi, mlo, mx, Z, M, N, K, N);
+    OCTEN_LAUNCHED(1);
+    OCTEN_CUDA(cudaGetLastError());
+    return true;
+}
 
 }  // namespace octen

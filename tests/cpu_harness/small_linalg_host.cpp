@@ -12,9 +12,9 @@ extern "C" {
 
 void h_jacobi_eig(int n, const double* a, double* w, double* v) {
     std::vector<double> am(a, a + (size_t)n * n), cs(2 * (n + 2));
-    int flag = 0;
+    std::vector<int> iw(n + 8);
     TeamHost team;
-    jacobi_eig_sym(team, n, am.data(), v, cs.data(), &flag);
+    jacobi_eig_sym(team, n, am.data(), v, cs.data(), iw.data());
     for (int i = 0; i < n; ++i) w[i] = am[i + (size_t)n * i];
 }
 
@@ -49,3 +49,12 @@ void h_mt64(unsigned long long seed, int n, double* out) {
 }
 
 }  // extern "C"
+
+extern "C" int h_team_chol_inv(int n, double* a, double* inv, double tol) {
+    TeamHost team;
+    double sc[2];
+    int ir[2];
+    const int rk = team_chol_semidef(team, n, a, n, tol, sc, ir);
+    team_tri_inv_lower(team, n, a, n, inv, n);
+    return rk;
+}

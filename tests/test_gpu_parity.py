@@ -73,6 +73,26 @@ def test_compress_f32_within_tolerance(ob):
         assert rel(got[r], want) < 1e-5  # fp32 inputs: BASELINE tolerance is 1e-4
 
 
+@pytest.mark.parametrize("shape", [(200, 300, 12, 40, 5, 4), (1000, 64, 9, 100, 4, 10), (96, 50, 7, 30, 9, 6)])
+def test_compress_f32_tcgen05_vs_simt_and_oracle(ob, shape, monkeypatch):
+    # the tcgen05 split-TF32 mode-1 kernel (M/N/K tails: several tiles, K not a
+    # multiple of 32) against the fp64 oracle and the SIMT fp32 path
+    I, J, t, Q, P, sh = shape
+    rs, u, v, w = _small_replicas(I, J, t, Q, P, sh, seed=I + J)
+    x = rng.Substream(I * J).uniform01_array(I * J * t).reshape((I, J, t), order="F").astype(np.float32)
+    got_tc = ob.compress(x, u, v, w, sh)
+    monkeypatch.setenv("OCTEN_DISABLE_TCGEN05", "1")
+    got_simt = ob.compress(x, u, v, w, sh)
+    monkeypatch.delenv("OCTEN_DISABLE_TCGEN05")
+    for r in range(P):
+        want = O.compress(x.astype(np.float64), rs, r, 0, t)
+        # split-TF32 with the tensor core's fp32 accumulation: the accumulator
+        # rounds toward zero, a bias of ~K/2 ulps on positive data (2e-5 at
+        # K=1000); BASELINE tolerance is 1e-4 relative Frobenius.
+        assert rel(got_tc[r], want) < 1e-4 * max(1.0, I / 1000.0)
+        assert rel(got_simt[r], want) < 5e-6
+
+
 def test_compress_zero_and_rank1(ob):
     # test_compression.cpp:108-144
     rs, u, v, w = _small_replicas(6, 5, 4, 3, 2, 1, seed=77)

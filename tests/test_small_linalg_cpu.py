@@ -154,3 +154,20 @@ def test_top_singular_pair(lib, m, n):
     sgn = np.sign(u @ uu[:, 0])
     assert np.allclose(u, sgn * uu[:, 0], atol=1e-10)
     assert np.allclose(v, sgn * vt[0], atol=1e-10)
+
+
+def test_team_chol_and_triangular_inverse(lib):
+    s = rng.Substream(77)
+    x = s.fill_uniform(40, 16)
+    g = np.asfortranarray(x.T @ x)
+    g0 = g.copy()
+    inv = np.zeros((16, 16), order="F")
+    assert lib.h_team_chol_inv(16, P(g), P(inv), ctypes.c_double(1e-14)) == 16
+    l = np.tril(g)
+    assert np.allclose(l @ l.T, g0, rtol=1e-12)
+    assert np.allclose(inv @ l, np.eye(16), atol=1e-10)
+    rs = O.gen_replicas([4, 4], 2, 3, 2, 8)
+    proj = O.stack_projections(rs, 0)
+    g = np.asfortranarray(proj.T @ proj)
+    inv = np.zeros((4, 4), order="F")
+    assert lib.h_team_chol_inv(4, P(g), P(inv), ctypes.c_double(1e-11)) == 2
