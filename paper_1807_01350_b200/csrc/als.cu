@@ -385,28 +385,27 @@ __global__ void als_init_state_kernel(AlsDev d) {
 // ---------------- sweeps ----------------
 
 // MTTKRP of mode 0 (a,r) = sum_b T(a,b,r) B(b,r) and of mode 1
-// (b,r) = sum_a T(a,b,r) A(a,r), from T = Y x3 C.  One warp per
-// (problem, r): lanes run along the contiguous a index of T.
-__global__ void als_mttkrp_T_kernel(AlsDev d, int mode) {
-    const int warps_per_block = blockDim.x >> 5;
-    const int wid = blockIdx.x * warps_per_block + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
+// (b,r) = sum_a T(a,b,r) A(a,r), from T = Y x3 C.  One block per
+// (problem, r); the 8 warps split the b range, lanes run along the contiguous
+// a index of T; mode 0 partials are combined across warps in fixed order.
+__global__ void __launch_bounds__(256) als_mttkrp_T_kernel(AlsDev d, int mode) {
     const int R = d.R, Q = d.Q;
-    if (wid >= d.NP * R) return;
-    const int prob = wid / R, r = wid % R;
+    const int prob = blockIdx.x / R, r = blockIdx.x % R;
     if (!d.state[prob].active) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int p = prob / d.S, s = prob % d.S;
     const double* tcol = d.T + (size_t)p * d.q2() * d.S * R + (size_t)d.q2() * (s * R + r);
     double* M = d.Mb + (size_t)prob * Q * R + (size_t)Q * r;
     constexpr int MAXA = 8;  // Q <= 256
+    __shared__ double part[8][257];
     if (mode == 0) {
         const double* B = d.f(prob, 1) + (size_t)Q * r;
         double acc[MAXA];
 #pragma unroll
         for (int i = 0; i < MAXA; ++i) acc[i] = 0.0;
-#pragma unroll 4
-        for (int b = 0; b < Q; ++b) {
-            const double w = B[b];
+#pragma unroll 2
+        for (int b = warp; b < Q; b += nw) {
+            const double w = __ldg(B + b);
             const double* row = tcol + (size_t)Q * b;
 #pragma unroll
             for (int i = 0; i < MAXA; ++i) {
@@ -417,7 +416,13 @@ __global__ void als_mttkrp_T_kernel(AlsDev d, int mode) {
 #pragma unroll
         for (int i = 0; i < MAXA; ++i) {
             const int a = lane + 32 * i;
-            if (a < Q) M[a] = acc[i];
+            if (a < Q) part[warp][a] = acc[i];
+        }
+        __syncthreads();
+        for (int a = threadIdx.x; a < Q; a += blockDim.x) {
+            double sum = 0.0;
+            for (int w = 0; w < nw; ++w) sum += part[w][a];
+            M[a] = sum;
         }
     } else {
         const double* A = d.f(prob, 0) + (size_t)Q * r;
@@ -425,10 +430,10 @@ __global__ void als_mttkrp_T_kernel(AlsDev d, int mode) {
 #pragma unroll
         for (int i = 0; i < MAXA; ++i) {
             const int a = lane + 32 * i;
-            av[i] = a < Q ? A[a] : 0.0;
+            av[i] = a < Q ? __ldg(A + a) : 0.0;
         }
-#pragma unroll 4
-        for (int b = 0; b < Q; ++b) {
+#pragma unroll 2
+        for (int b = warp; b < Q; b += nw) {
             const double* row = tcol + (size_t)Q * b;
             double acc = 0.0;
 #pragma unroll
@@ -444,19 +449,15 @@ __global__ void als_mttkrp_T_kernel(AlsDev d, int mode) {
 
 // KR[p][(a + Q b), s R + r] = A(a,r) B(b,r)
 __global__ void als_kr_kernel(AlsDev d) {
-    const int prob = blockIdx.y;
-    const int p = prob / d.S, s = prob % d.S;
+    // grid (Q [b], R, NP), block >= Q threads [a]: no index division
+    const int b = blockIdx.x, r = blockIdx.y, prob = blockIdx.z;
+    const int a = threadIdx.x;
     const int Q = d.Q, R = d.R;
-    const double* A = d.f(prob, 0);
-    const double* B = d.f(prob, 1);
-    double* K = d.KR + (size_t)p * d.q2() * d.S * R;
-    const size_t total = (size_t)d.q2() * R;
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-        const int r = (int)(e / d.q2());
-        const int m = (int)(e % d.q2());
-        const int a = m % Q, b = m / Q;
-        K[m + d.q2() * (size_t)(s * R + r)] = A[a + (size_t)Q * r] * B[b + (size_t)Q * r];
-    }
+    if (a >= Q) return;
+    const int p = prob / d.S, s = prob % d.S;
+    const double bv = d.f(prob, 1)[b + (size_t)Q * r];
+    double* K = d.KR + (size_t)p * d.q2() * d.S * R + d.q2() * (size_t)(s * R + r) + (size_t)Q * b;
+    K[a] = d.f(prob, 0)[a + (size_t)Q * r] * bv;
 }
 
 // One mode update per problem: raw = M V^-1 (COD of the Hadamard Gram;
@@ -476,12 +477,17 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     double* Ev = Lf + R * R;        // R*R  (eigenvectors / L^-1)
     double* Vi = Ev + R * R;        // R*R  (V^-1 or V^+)
     double* raw = Vi + R * R;       // Q*R
-    double* nrm = raw + Q * R;      // R
+    double* Ms = raw + Q * R;       // Q*R  (staged MTTKRP)
+    double* nrm = Ms + Q * R;       // R
     double* cs = nrm + R;           // 2(R+2)
     double* red = cs + 2 * (R + 2); // blockDim
     int* iw = (int*)(red + blockDim.x);  // R + 8
     __shared__ int rank, bad;
-    const double* M = d.Mb + (size_t)prob * Q * R;
+    const double* M = Ms;
+    {
+        const double* Mg = d.Mb + (size_t)prob * Q * R;
+        for (int e = threadIdx.x; e < Q * R; e += blockDim.x) Ms[e] = Mg[e];
+    }
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
         double v = 1.0;
         for (int k = 0; k < 3; ++k)
@@ -694,14 +700,11 @@ struct YtA {  // A(p, c, k) = Y[p][k + Q^2 c]   (Y_(2)^T rows)
     size_t q3, q2;
     __device__ double operator()(int p, int c, int k) const { return Y[(size_t)p * q3 + k + q2 * c]; }
 };
-struct KRB {  // B(p, k = a + Q b, n = s R + r) = A_(p,s)(a, r) * B_(p,s)(b, r)  (Khatri-Rao on the fly)
-    const double* F;
-    int S, Q, R;
-    __device__ double operator()(int p, int k, int n) const {
-        const int a = k % Q, b = k / Q, s = n / R, r = n % R;
-        const double* fa = F + ((size_t)(p * S + s) * 3 + 0) * Q * R + (size_t)Q * r;
-        return fa[a] * fa[(size_t)Q * R + b];
-    }
+struct KRB {  // B(p, k, n) = KR[p][k + Q^2 n]  (materialized Khatri-Rao product)
+    const double* K;
+    size_t q2;
+    int SR;
+    __device__ double operator()(int p, int k, int n) const { return K[(size_t)p * q2 * SR + k + q2 * n]; }
 };
 struct M2Store {  // -> Mb[p S + n/R][c + Q (n%R)]
     double* M;
@@ -1032,7 +1035,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     const int ks_m2 = pick_ksplit(P, Q, SR, (int)q2);
     ws.reserve(std::max<size_t>(ws.n, (size_t)P * ks_m2 * Q * SR));
     const int upd_threads = 256;
-    const size_t smem_upd = (size_t)(4 * R * R + Q * R + R + 2 * (R + 2) + upd_threads) * sizeof(double) + (R + 8) * sizeof(int) + 16;
+    const size_t smem_upd = (size_t)(4 * R * R + 2 * Q * R + R + 2 * (R + 2) + upd_threads) * sizeof(double) + (R + 8) * sizeof(int) + 16;
     OCTEN_CUDA(cudaFuncSetAttribute(als_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_upd));
     int* hcount = nullptr;
     OCTEN_CUDA(cudaMallocHost(&hcount, sizeof(int)));
@@ -1042,11 +1045,13 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         // T = Y x3 C  (Q^2 x SR per replica)
         gemm_f64<false, true>(P, (int)q2, SR, Q, YmatA{dY, q3, q2, S, false}, FacB{F.p, S, Q, R, 2},
                                                TStore{T.p, q2, SR}, st);
-        als_mttkrp_T_kernel<<<(NP * R + 7) / 8, 256, 0, st>>>(d, 0); OCTEN_LAUNCHED(1);
+        als_mttkrp_T_kernel<<<NP * R, 256, 0, st>>>(d, 0); OCTEN_LAUNCHED(1);
         als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 0, sweep); OCTEN_LAUNCHED(1);
-        als_mttkrp_T_kernel<<<(NP * R + 7) / 8, 256, 0, st>>>(d, 1); OCTEN_LAUNCHED(1);
+        als_mttkrp_T_kernel<<<NP * R, 256, 0, st>>>(d, 1); OCTEN_LAUNCHED(1);
         als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 1, sweep); OCTEN_LAUNCHED(1);
-        gemm_f64<true, true>(P, Q, SR, (int)q2, YtA{dY, q3, q2}, KRB{F.p, S, Q, R},
+        als_kr_kernel<<<dim3(Q, R, NP), (Q + 31) / 32 * 32, 0, st>>>(d);
+        OCTEN_LAUNCHED(1);
+        gemm_f64<true, true>(P, Q, SR, (int)q2, YtA{dY, q3, q2}, KRB{KR.p, q2, SR},
                                               M2Store{Mb.p, S, Q, R}, st, ks_m2, ws.p);
         als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 2, sweep); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());

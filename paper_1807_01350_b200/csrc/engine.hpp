@@ -141,13 +141,14 @@ public:
     DevBuf<double> Ud[2];    // P x d x Q
     DevBuf<double> Gp[2];    // P x d x d
     DevBuf<double> Lsum[2];  // d x d (Cholesky of sum_p G_p)
+    DevBuf<double> Lsum_inv[2], Gw_inv;  // diagonal-block inverses of the factors
     int sum_rank[2] = {0, 0};
     DevBuf<double> Lw[2];    // shared x shared whitener (non-temporal modes)
     int white_ok[2] = {0, 0};
     DevBuf<double> Lp[2];    // P x Q x Q chol(U_p^T U_p)
     DevBuf<int> lp_ok[2];    // P
     bool pair_solve = false;
-    DevBuf<double> solved[2], Gw, rhs, tmp, tg, red, sw, maxdiag, RF, SC, sims, tscr;
+    DevBuf<double> solved[2], Gw, rhs, tmp, tg, red, sw, sw2, maxdiag, RF, SC, sims, tscr;
     DevBuf<int> ranks, perms, iscr;
     DevBuf<DevStatus> err;
     std::vector<int> last_perm;

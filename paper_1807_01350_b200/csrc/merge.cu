@@ -132,7 +132,10 @@ __global__ void lp_kernel(const double* U, long long d, int Q, double* Lp, int* 
     __syncthreads();
     if (threadIdx.x == 0) ok[p] = (chol_semidef(Q, g, Q, 0.0) == Q) ? 1 : 0;
     __syncthreads();
-    for (int e = threadIdx.x; e < Q * Q; e += blockDim.x) Lp[(size_t)p * Q * Q + e] = g[e];
+    // store L^-1 (refine_stack whitens with L^-1; a matrix product instead of
+    // per-column triangular solves on the hot path)
+    TeamDev team;
+    team_tri_inv_lower(team, Q, g, Q, Lp + (size_t)p * Q * Q, Q);
 }
 
 struct AlignDev {
@@ -366,7 +369,9 @@ __global__ void refine_kernel(int P, int Q, int R, int PQ, const double* tg, dou
     extern __shared__ double sm[];
     double* zt = sm;             // Q*R
     double* zb = zt + Q * R;     // Q*R
-    double* agr = zb + Q * R;    // R
+    double* tt0 = zb + Q * R;    // Q*R raw target
+    double* bb0 = tt0 + Q * R;   // Q*R raw block
+    double* agr = bb0 + Q * R;   // R
     for (int r = threadIdx.x; r < R; r += blockDim.x) agr[r] = 1.0;
     __syncthreads();
     for (int n = 0; n < 2; ++n) {
@@ -375,13 +380,27 @@ __global__ void refine_kernel(int P, int Q, int R, int PQ, const double* tg, dou
         const double* t = tg + ((size_t)p * 2 + n) * Q * R;
         double* stk = stacks + (size_t)n * PQ * R;
         for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
-            zt[e] = t[e];
-            zb[e] = stk[(size_t)p * Q + (e % Q) + (size_t)PQ * (e / Q)];
+            tt0[e] = t[e];
+            bb0[e] = stk[(size_t)p * Q + (e % Q) + (size_t)PQ * (e / Q)];
         }
         __syncthreads();
-        if (white)
-            for (int c = threadIdx.x; c < 2 * R; c += blockDim.x)
-                trsv_lower(Q, L, Q, (c < R ? zt : zb) + (size_t)Q * (c % R), 1);
+        // whitened coordinates: z = L^-1 x (L points at L^-1, lower)
+        for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
+            const int i = e % Q, r = e / Q;
+            if (white) {
+                double a = 0.0, b = 0.0;
+                for (int k = 0; k <= i; ++k) {
+                    const double l = L[i + (size_t)Q * k];
+                    a += l * tt0[k + Q * r];
+                    b += l * bb0[k + Q * r];
+                }
+                zt[e] = a;
+                zb[e] = b;
+            } else {
+                zt[e] = tt0[e];
+                zb[e] = bb0[e];
+            }
+        }
         __syncthreads();
         for (int r = threadIdx.x; r < R; r += blockDim.x) {
             double bb = 0.0, bt = 0.0, tt = 0.0;
@@ -478,11 +497,16 @@ __global__ void match_columns_kernel(int R, long long d0, long long d1, const do
             const long long d = n ? d1 : d0;
             const double* cur = (n ? cur1 : cur0) + (size_t)d * j;
             const double* sto = (n ? sto1 : sto0) + (size_t)d * i;
-            const double a = nc[n * R + j] > 0.0 ? nc[n * R + j] : 1.0;
-            const double b = ns[n * R + i] > 0.0 ? ns[n * R + i] : 1.0;
-            double dot = 0.0;
-            for (long long k = 0; k < d; ++k) dot += (sto[k] / b) * (cur[k] / a);
-            s *= fabs(dot);
+            const double a = nc[n * R + j] > 0.0 ? 1.0 / nc[n * R + j] : 1.0;
+            const double b = ns[n * R + i] > 0.0 ? 1.0 / ns[n * R + i] : 1.0;
+            double d0s = 0.0, d1s = 0.0;
+            long long k = 0;
+            for (; k + 1 < d; k += 2) {
+                d0s += sto[k] * cur[k];
+                d1s += sto[k + 1] * cur[k + 1];
+            }
+            if (k < d) d0s += sto[k] * cur[k];
+            s *= fabs((d0s + d1s) * a * b);
         }
         sim[e] = s;
     }
@@ -497,7 +521,7 @@ __global__ void match_columns_kernel(int R, long long d0, long long d1, const do
         const double a = nc[n * R + j] > 0.0 ? nc[n * R + j] : 1.0;
         const double b = ns[n * R + i] > 0.0 ? ns[n * R + i] : 1.0;
         double dot = 0.0;
-        for (long long k = 0; k < d; ++k) dot += (sto[k] / b) * (cur[k] / a);
+        for (long long k = 0; k < d; ++k) dot += sto[k] * cur[k];  // sign of the cosine (norms > 0)
         signs_out[(size_t)n * R + i] = dot < 0.0 ? -1.0 : 1.0;
     }
     for (int i = threadIdx.x; i < R; i += blockDim.x) perm_out[i] = perm[i];
@@ -789,7 +813,7 @@ void MergeEngine::set_projections(int P_, int Q_, int sh, int R_, std::int64_t I
                                                 StoreCM{Lsum[n].p, d, 0}, st);
         maxdiag.reserve(128);
         ranks.reserve(128);
-        chol_batched(Lsum[n].p, (int)d, (int)d, 0, 1, kGramRankTol, maxdiag.p, ranks.p, st);
+        chol_batched(Lsum[n].p, (int)d, (int)d, 0, 1, kGramRankTol, maxdiag.p, ranks.p, Lsum_inv[n], st);
         sum_rank[n] = ranks.to_host(1, st)[0];
         // whitener of the shared block (reference replica; the block is shared)
         DevBuf<int> okb;
@@ -891,7 +915,8 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
                 add_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>((size_t)d * d, Gp[n].p + (size_t)p * d * d,
                                                                      Gj.p + (size_t)p * d * d); OCTEN_LAUNCHED(1);
             }
-            chol_batched(Gj.p, (int)d, (int)d, d * d, P, 1e-15, md.p, rk.p, st);
+            DevBuf<double> linvj;
+            chol_batched(Gj.p, (int)d, (int)d, d * d, P, 1e-15, md.p, rk.p, linvj, st);
             // g1 = U_0 RF_0[n]  (d x R)
             gemm_f64<false, true>(1, (int)d, R, Q, UcatA{Ud[n].p, d, 0},
                                                    ColB{RF.p + (size_t)n * Q * R, Q, 0}, StoreCM{g1.p, d, 0}, st);
@@ -903,8 +928,8 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
                 OCTEN_CUDA(cudaMemcpyAsync(Y1.p + (size_t)p * d * R, g1.p, sizeof(double) * d * R,
                                            cudaMemcpyDeviceToDevice, st));
             OCTEN_CUDA(cudaMemcpyAsync(Y2.p, g2.p, sizeof(double) * P * d * R, cudaMemcpyDeviceToDevice, st));
-            chol_solve_batched(Gj.p, (int)d, (int)d, d * d, Y1.p, (int)d, d * R, R, P, st);
-            chol_solve_batched(Gj.p, (int)d, (int)d, d * d, Y2.p, (int)d, d * R, R, P, st);
+            chol_solve_blocked(Gj.p, (int)d, (int)d, d * d, linvj, Y1.p, (int)d, d * R, R, P, st);
+            chol_solve_blocked(Gj.p, (int)d, (int)d, d * d, linvj, Y2.p, (int)d, d * R, R, P, st);
             if (P > 1) {
                 pair_rms_kernel<<<P - 1, 256, 0, st>>>(P, Q, sh, R, d, n, g1.p, Y1.p, g2.p, Y2.p, RF.p, SC.p, rmsb.p);
                 OCTEN_LAUNCHED(1);
@@ -946,7 +971,7 @@ void MergeEngine::solve_nontemporal(int n, const double* dStack, double* dOut, c
                            std::to_string(sum_rank[n]) + " of " + std::to_string(d) + ")");
     gemm_f64<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{dStack, PQ, 0},
                                            StoreCM{dOut, d, 0}, st);
-    chol_solve_batched(Lsum[n].p, (int)d, (int)d, 0, dOut, (int)d, 0, R, 1, st);
+    chol_solve_blocked(Lsum[n].p, (int)d, (int)d, 0, Lsum_inv[n], dOut, (int)d, 0, R, 1, st);
 }
 
 void MergeEngine::temporal_stack(const double* dY, const double* dA, const double* dB, double* dTstack,
@@ -988,7 +1013,8 @@ void MergeEngine::temporal_append(const double* dTstack, const double* dW, std::
     // Gc = Pc^T Pc = sum_{(p,a)} W_p[:,a] W_p[:,a]^T ; W as t x PQ col-major
     gemm_f64<false, false>(1, (int)t, (int)t, (int)PQ, UcatA{dW, t, 0}, UcatB{dW, t, 0},
                                             StoreCM{Gc.p, t, 0}, st);
-    chol_batched(Gc.p, (int)t, (int)t, 0, 1, kGramRankTol, md.p, rk.p, st);
+    DevBuf<double> linvc;
+    chol_batched(Gc.p, (int)t, (int)t, 0, 1, kGramRankTol, md.p, rk.p, linvc, st);
     // [bv | hv] = Pc^T [tstack | hist]
     gemm_f64<false, true>(1, (int)t, R, (int)PQ, UcatA{dW, t, 0}, ColB{dTstack, PQ, 0},
                                            StoreCM{BZ.p, t, 0}, st);
@@ -998,7 +1024,7 @@ void MergeEngine::temporal_append(const double* dTstack, const double* dW, std::
     hv.reserve((size_t)t * R);
     OCTEN_CUDA(cudaMemcpyAsync(hv.p, BZ.p + (size_t)t * R, sizeof(double) * t * R, cudaMemcpyDeviceToDevice, st));
     append_dots_kernel<<<R, 256, 0, st>>>(PQ, dTstack, dHist, dots.p); OCTEN_LAUNCHED(1);
-    chol_solve_batched(Gc.p, (int)t, (int)t, 0, BZ.p, (int)t, 0, 2 * R, 1, st);
+    chol_solve_blocked(Gc.p, (int)t, (int)t, 0, linvc, BZ.p, (int)t, 0, 2 * R, 1, st);
     const int rank_c = rk.to_host(1, st)[0];
     append_decide_kernel<<<R, 256, 0, st>>>(R, t, rank_c, dots.p, hv.p, BZ.p, md.p, dRows, coef.p, err.p,
                                             2 /* temporal mode */); OCTEN_LAUNCHED(1);
@@ -1043,9 +1069,9 @@ void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, do
             gemm_f64<true, true>(P, Q, R, (int)d, UtA{Ud[n].p, d, Q}, ColB{solved[n].p, d, 0},
                                                   StoreCM{tg.p + (size_t)n * Q * R, Q, 2LL * Q * R}, st);
         }
-        const size_t smem = (size_t)(2 * Q * R + R) * sizeof(double);
+        const size_t smem = (size_t)(4 * Q * R + R) * sizeof(double);
         OCTEN_CUDA(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        refine_kernel<<<P, 128, smem, st>>>(P, Q, R, (int)PQ, tg.p, stacks.p, Lp[0].p, Lp[1].p, lp_ok[0].p,
+        refine_kernel<<<P, 256, smem, st>>>(P, Q, R, (int)PQ, tg.p, stacks.p, Lp[0].p, Lp[1].p, lp_ok[0].p,
                                             lp_ok[1].p, w.p); OCTEN_LAUNCHED(1);
         weight_mass_kernel<<<1, 64, 0, st>>>(P, Q, R, std::max(dims[0], dims[1]), w.p); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
@@ -1055,20 +1081,45 @@ void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, do
                 throw NumericError("recover: mode " + std::to_string(n + 1) + " projection is " + std::to_string(PQ) +
                                    "x" + std::to_string(d) +
                                    "; p*Q must reach the mode extent (raise p per the replica bound)");
-            Gw.reserve((size_t)R * d * d);
-            weighted_gram_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>(P, R, d, Gp[n].p, w.p, Gw.p); OCTEN_LAUNCHED(1);
-            chol_batched(Gw.p, (int)d, (int)d, d * d, R, kGramRankTol, maxdiag.p, ranks.p, st);
-            scale_stack_kernel<<<grid_for((size_t)PQ * R), 256, 0, st>>>(P, Q, R, stacks.p + (size_t)n * PQ * R, w.p,
-                                                                        sw.p); OCTEN_LAUNCHED(1);
-            gemm_f64<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{sw.p, PQ, 0},
-                                                   StoreCM{solved[n].p, d, 0}, st);
-            std::vector<int> rk = ranks.to_host(R, st);
-            for (int r = 0; r < R; ++r)
-                if (rk[r] < d)
-                    throw NumericError("recover: rank-deficient projection on mode " + std::to_string(n + 1) +
-                                       " (rank " + std::to_string(rk[r]) + " of " + std::to_string(d) + ")");
+        }
+        // Both modes' R weighted systems in one batched factorization when the
+        // extents agree (2R matrices per launch halves the latency-bound steps).
+        const bool fused = dims[0] == dims[1];
+        const int groups = fused ? 1 : 2;
+        for (int gi = 0; gi < groups; ++gi) {
+            const long long d = dims[fused ? 0 : gi];
+            const int nmodes = fused ? 2 : 1;
+            const int nb = nmodes * R;
+            Gw.reserve((size_t)nb * d * d);
+            sw2.reserve((size_t)d * nb);
+            for (int mi = 0; mi < nmodes; ++mi) {
+                const int n = fused ? mi : gi;
+                weighted_gram_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>(P, R, d, Gp[n].p, w.p,
+                                                                              Gw.p + (size_t)mi * R * d * d);
+                OCTEN_LAUNCHED(1);
+                scale_stack_kernel<<<grid_for((size_t)PQ * R), 256, 0, st>>>(P, Q, R, stacks.p + (size_t)n * PQ * R,
+                                                                            w.p, sw.p);
+                OCTEN_LAUNCHED(1);
+                gemm_f64<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{sw.p, PQ, 0},
+                                      StoreCM{sw2.p + (size_t)mi * R * d, d, 0}, st);
+            }
+            chol_batched(Gw.p, (int)d, (int)d, d * d, nb, kGramRankTol, maxdiag.p, ranks.p, Gw_inv, st);
+            std::vector<int> rk = ranks.to_host(nb, st);
+            for (int mi = 0; mi < nmodes; ++mi) {
+                const int n = fused ? mi : gi;
+                for (int r = 0; r < R; ++r)
+                    if (rk[mi * R + r] < d)
+                        throw NumericError("recover: rank-deficient projection on mode " + std::to_string(n + 1) +
+                                           " (rank " + std::to_string(rk[mi * R + r]) + " of " + std::to_string(d) +
+                                           ")");
+            }
             // each column r against its own factor
-            chol_solve_batched(Gw.p, (int)d, (int)d, d * d, solved[n].p, (int)d, d, 1, R, st);
+            chol_solve_blocked(Gw.p, (int)d, (int)d, d * d, Gw_inv, sw2.p, (int)d, d, 1, nb, st);
+            for (int mi = 0; mi < nmodes; ++mi) {
+                const int n = fused ? mi : gi;
+                OCTEN_CUDA(cudaMemcpyAsync(solved[n].p, sw2.p + (size_t)mi * R * d, sizeof(double) * d * R,
+                                           cudaMemcpyDeviceToDevice, st));
+            }
         }
     }
     // gauge to the stored factors
@@ -1081,7 +1132,7 @@ void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, do
     err.zero(2, st);
     if (dStoredA && dStoredB) {
         const size_t smem = (size_t)(R * R + 4 * R) * sizeof(double);
-        match_columns_kernel<<<1, 256, smem, st>>>(R, dims[0], dims[1], solved[0].p, solved[1].p, dStoredA, dStoredB,
+        match_columns_kernel<<<1, 1024, smem, st>>>(R, dims[0], dims[1], solved[0].p, solved[1].p, dStoredA, dStoredB,
                                                    perm.p, signs.p, simb.p); OCTEN_LAUNCHED(1);
         finalize_kernel<<<R, 256, 0, st>>>(R, dims[0], solved[0].p, perm.p, signs.p, dAfin, err.p, 0); OCTEN_LAUNCHED(1);
         finalize_kernel<<<R, 256, 0, st>>>(R, dims[1], solved[1].p, perm.p, signs.p + R, dBfin, err.p + 1, 1); OCTEN_LAUNCHED(1);

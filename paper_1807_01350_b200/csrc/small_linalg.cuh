@@ -221,23 +221,41 @@ __device__ inline int warp_chol_inv32(double* s, int lds, int n, double thr, dou
     int rank = 0;
 #pragma unroll 1
     for (int j = 0; j < n; ++j) {
-        // diagonal: L_jj^2 = a_jj - sum_{p<j} L_jp^2 (every lane computes it)
-        double d = s[j + (size_t)lds * j];
-#pragma unroll 4
-        for (int p = 0; p < j; ++p) {
-            const double l = s[j + (size_t)lds * p];
-            d -= l * l;
+        // diagonal: L_jj^2 = a_jj - sum_{p<j} L_jp^2 (every lane computes it);
+        // four independent partial sums break the FMA dependency chain
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+        int p = 0;
+#pragma unroll 1
+        for (; p + 3 < j; p += 4) {
+            const double l0 = s[j + (size_t)lds * p], l1 = s[j + (size_t)lds * (p + 1)];
+            const double l2 = s[j + (size_t)lds * (p + 2)], l3 = s[j + (size_t)lds * (p + 3)];
+            d0 += l0 * l0;
+            d1 += l1 * l1;
+            d2 += l2 * l2;
+            d3 += l3 * l3;
         }
+        for (; p < j; ++p) {
+            const double l = s[j + (size_t)lds * p];
+            d0 += l * l;
+        }
+        const double d = s[j + (size_t)lds * j] - ((d0 + d1) + (d2 + d3));
         const bool dead = !(d > thr);
         const double piv = dead ? 0.0 : sqrt(d);
         const double rp = dead ? 0.0 : 1.0 / piv;
         double lij = 0.0;
         const int i = lane;
         if (i > j && i < n) {
-            double v = s[i + (size_t)lds * j];
-#pragma unroll 4
-            for (int p = 0; p < j; ++p) v -= s[i + (size_t)lds * p] * s[j + (size_t)lds * p];
-            lij = v * rp;
+            double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+            int q = 0;
+#pragma unroll 1
+            for (; q + 3 < j; q += 4) {
+                v0 += s[i + (size_t)lds * q] * s[j + (size_t)lds * q];
+                v1 += s[i + (size_t)lds * (q + 1)] * s[j + (size_t)lds * (q + 1)];
+                v2 += s[i + (size_t)lds * (q + 2)] * s[j + (size_t)lds * (q + 2)];
+                v3 += s[i + (size_t)lds * (q + 3)] * s[j + (size_t)lds * (q + 3)];
+            }
+            for (; q < j; ++q) v0 += s[i + (size_t)lds * q] * s[j + (size_t)lds * q];
+            lij = (s[i + (size_t)lds * j] - ((v0 + v1) + (v2 + v3))) * rp;
         }
         __syncwarp();
         if (i > j && i < n) s[i + (size_t)lds * j] = lij;
@@ -251,13 +269,20 @@ __device__ inline int warp_chol_inv32(double* s, int lds, int n, double thr, dou
         const int j = lane;
 #pragma unroll 1
         for (int i = 0; i < n; ++i) {
-            double v = (i == j) ? 1.0 : 0.0;
+            double v0 = (i == j) ? 1.0 : 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
             if (i > j) {
-#pragma unroll 4
-                for (int p = j; p < i; ++p) v -= s[i + (size_t)lds * p] * x[p + (size_t)ldx * j];
+                int p = j;
+#pragma unroll 1
+                for (; p + 3 < i; p += 4) {
+                    v0 -= s[i + (size_t)lds * p] * x[p + (size_t)ldx * j];
+                    v1 -= s[i + (size_t)lds * (p + 1)] * x[p + 1 + (size_t)ldx * j];
+                    v2 -= s[i + (size_t)lds * (p + 2)] * x[p + 2 + (size_t)ldx * j];
+                    v3 -= s[i + (size_t)lds * (p + 3)] * x[p + 3 + (size_t)ldx * j];
+                }
+                for (; p < i; ++p) v0 -= s[i + (size_t)lds * p] * x[p + (size_t)ldx * j];
             }
             const double lii = s[i + (size_t)lds * i];
-            x[i + (size_t)ldx * j] = (i < j || lii == 0.0) ? 0.0 : v / lii;
+            x[i + (size_t)ldx * j] = (i < j || lii == 0.0) ? 0.0 : ((v0 + v1) + (v2 + v3)) / lii;
         }
     }
     __syncwarp();
@@ -873,6 +898,20 @@ OCTEN_HD void jacobi_eig_sym(const Team& team, int n, double* a, double* v, doub
 // ---------------------------------------------------------------------------
 template <class Team>
 OCTEN_HD double team_reduce_sum(const Team& team, double v, double* red) {
+#if defined(__CUDA_ARCH__)
+    // device: warp shuffle tree, then warp partials summed in warp order
+    // (fixed order, deterministic); requires blockDim.x % 32 == 0
+    if (team.size() > 1) {
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const int nw = team.size() >> 5;
+        if ((team.tid() & 31) == 0) red[team.tid() >> 5] = v;
+        team.sync();
+        double s = 0.0;
+        for (int i = 0; i < nw; ++i) s += red[i];
+        team.sync();
+        return s;
+    }
+#endif
     // deterministic: every thread writes, thread 0 sums in index order
     red[team.tid()] = v;
     team.sync();
@@ -969,6 +1008,180 @@ OCTEN_HD double top_singular_pair(const Team& team, int m, int n, const double* 
         for (int i = team.tid(); i < m; i += team.size()) u[i] /= sigma;
     team.sync();
     return sigma;
+}
+
+// ---------------------------------------------------------------------------
+// Top-k eigenpairs of a symmetric positive semidefinite n x n matrix `a`
+// (column-major, ld n, read only) by block subspace (orthogonal) iteration:
+// a block of m >= k columns, each product W = A U re-orthonormalised by
+// classical Gram-Schmidt run twice (CGS2), with a Rayleigh-Ritz projection
+// H = U^T A U whose Ritz values give the convergence rate
+// rho = theta_{m-1} / theta_{k-1}.  The iteration stops once rho^products
+// <= 1e-18; it gives up (returns 0, the caller falls back to the full Jacobi
+// solver) when that needs more than max_products, when the block collapses
+// (A U has a zero column) or when theta_{k-1} <= 0.  The Gram spectrum of a
+// compressed low-rank replica has a gap of ~1e-4 at k = rank, so a handful of
+// products replace the O(n^3)-per-sweep Jacobi solve of the whole matrix.
+// Same role as jacobi_eig_sym: the BDCSVD thin-U of the unfoldings
+// (cp_als.cpp:96-100), top-k only.
+// On success: u (n x m) columns 0..k-1 = eigenvectors by descending
+// eigenvalue, theta[0..m) = Ritz values descending.
+// Scratch: w n*m, h m*m, hv m*m, cs 2*(m+2) + team.size() + 2 doubles,
+// iw 2*m + 8 ints.
+// ---------------------------------------------------------------------------
+template <class Team>
+OCTEN_HD void team_symm_block(const Team& team, int n, const double* a, int m, const double* u,
+                              double* w) {
+    for (int e = team.tid(); e < n * m; e += team.size()) {
+        const int i = e % n, j = e / n;
+        const double* uj = u + (size_t)n * j;
+        double s = 0.0;
+        for (int l = 0; l < n; ++l) s += a[i + (size_t)n * l] * uj[l];
+        w[e] = s;
+    }
+    team.sync();
+}
+
+// coefficients cf[i] = <w_i, w_j>, i < j
+template <class Team>
+OCTEN_HD void team_cgs_coeffs(const Team& team, int n, int j, const double* w, double* cf) {
+    const double* wj = w + (size_t)n * j;
+#if defined(__CUDA_ARCH__)
+    if (team.size() >= 64) {
+        const int lane = team.tid() & 31, wid = team.tid() >> 5, nw = team.size() >> 5;
+        for (int i = wid; i < j; i += nw) {
+            const double* wi = w + (size_t)n * i;
+            double s = 0.0;
+            for (int r = lane; r < n; r += 32) s += wi[r] * wj[r];
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) cf[i] = s;
+        }
+        team.sync();
+        return;
+    }
+#endif
+    for (int i = team.tid(); i < j; i += team.size()) {
+        const double* wi = w + (size_t)n * i;
+        double s = 0.0;
+        for (int r = 0; r < n; ++r) s += wi[r] * wj[r];
+        cf[i] = s;
+    }
+    team.sync();
+}
+
+// orthonormalise the m columns of w in place (CGS2); 0 if a column vanishes
+template <class Team>
+OCTEN_HD int team_cgs2(const Team& team, int n, int m, double* w, double* cf, double* red) {
+    for (int j = 0; j < m; ++j) {
+        double* wj = w + (size_t)n * j;
+        if (j > 0) {
+            for (int pass = 0; pass < 2; ++pass) {
+                team_cgs_coeffs(team, n, j, w, cf);
+                for (int r = team.tid(); r < n; r += team.size()) {
+                    double s = wj[r];
+                    for (int i = 0; i < j; ++i) s -= cf[i] * w[r + (size_t)n * i];
+                    wj[r] = s;
+                }
+                team.sync();
+            }
+        }
+        double loc = 0.0;
+        for (int r = team.tid(); r < n; r += team.size()) loc += wj[r] * wj[r];
+        const double nrm2 = team_reduce_sum(team, loc, red);
+        if (!(nrm2 > 0.0) || !(nrm2 < 1e300)) return 0;
+        const double inv = 1.0 / sqrt(nrm2);
+        for (int r = team.tid(); r < n; r += team.size()) wj[r] *= inv;
+        team.sync();
+    }
+    return 1;
+}
+
+template <class Team>
+OCTEN_HD int subspace_eig_top(const Team& team, int n, const double* a, int k, int m, double* u,
+                              double* w, double* h, double* hv, double* theta, double* cs, int* iw,
+                              int max_products = 24) {
+    double* cf = cs;                 // m (also Jacobi scratch 2*(m+2))
+    double* red = cs + 2 * (m + 2);  // team.size() + 2
+    int* order = iw + m + 8;         // m
+    double* const u0 = u;
+    // deterministic start block, entries uniform in [-1, 1)
+    for (int e = team.tid(); e < n * m; e += team.size())
+        u[e] = (double)(splitmix(0x5eedULL + (uint64_t)e) >> 11) * 0x1.0p-52 - 1.0;
+    team.sync();
+    if (!team_cgs2(team, n, m, u, cf, red)) return 0;
+    int products = 0, target = 3;
+    for (;;) {
+        team_symm_block(team, n, a, m, u, w);  // W = A U
+        ++products;
+        if (products >= target) {
+            // Rayleigh-Ritz: H = U^T W (symmetrised), H = Hv diag(theta) Hv^T
+            for (int e = team.tid(); e < m * m; e += team.size()) {
+                const int i = e % m, j = e / m;
+                if (i > j) continue;
+                double s1 = 0.0, s2 = 0.0;
+                for (int r = 0; r < n; ++r) {
+                    s1 += u[r + (size_t)n * i] * w[r + (size_t)n * j];
+                    s2 += u[r + (size_t)n * j] * w[r + (size_t)n * i];
+                }
+                const double hij = 0.5 * (s1 + s2);
+                h[i + (size_t)m * j] = hij;
+                h[j + (size_t)m * i] = hij;
+            }
+            team.sync();
+            jacobi_eig_sym(team, m, h, hv, cs, iw);
+            team.sync();
+            if (team.tid() == 0) {
+                for (int i = 0; i < m; ++i) order[i] = i;
+                for (int i = 1; i < m; ++i) {
+                    const int key = order[i];
+                    const double kv = h[key + (size_t)m * key];
+                    int j = i - 1;
+                    while (j >= 0 && h[order[j] + (size_t)m * order[j]] < kv) {
+                        order[j + 1] = order[j];
+                        --j;
+                    }
+                    order[j + 1] = key;
+                }
+                for (int i = 0; i < m; ++i) theta[i] = h[order[i] + (size_t)m * order[i]];
+                // products needed for rho^N <= 1e-18
+                const double tk = theta[k - 1], tm = fabs(theta[m - 1]);
+                int need = max_products + 1;
+                if (tk > 0.0 && theta[0] > 0.0) {
+                    const double rho = fmax(tm / tk, 1e-300);
+                    if (rho < 1.0) {
+                        const double nn = ceil(log(1e-18) / log(rho));
+                        need = nn < (double)(max_products + 1) ? (int)nn : max_products + 1;
+                    }
+                }
+                iw[m + 4] = need;
+            }
+            team.sync();
+            const int need = iw[m + 4];
+            team.sync();
+            if (need > max_products) return 0;
+            if (products >= need) break;
+            target = need;
+        }
+        if (!team_cgs2(team, n, m, w, cf, red)) return 0;
+        double* t = u;
+        u = w;
+        w = t;
+    }
+    // Ritz vectors: column c = U hv[:, order[c]], c < k; computed into the
+    // buffer not holding U, then moved to the caller's u if needed
+    for (int e = team.tid(); e < n * k; e += team.size()) {
+        const int r = e % n, c = e / n;
+        const double* hc = hv + (size_t)m * order[c];
+        double s = 0.0;
+        for (int l = 0; l < m; ++l) s += u[r + (size_t)n * l] * hc[l];
+        w[e] = s;
+    }
+    team.sync();
+    if (w != u0) {
+        for (int e = team.tid(); e < n * k; e += team.size()) u0[e] = w[e];
+        team.sync();
+    }
+    return 1;
 }
 
 }  // namespace octen

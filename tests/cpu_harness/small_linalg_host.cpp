@@ -58,3 +58,14 @@ extern "C" int h_team_chol_inv(int n, double* a, double* inv, double tol) {
     team_tri_inv_lower(team, n, a, n, inv, n);
     return rk;
 }
+
+extern "C" int h_subspace_eig_top(int n, const double* a, int k, int m, double* u, double* theta) {
+    std::vector<double> w((size_t)n * m), h((size_t)m * m), hv((size_t)m * m), cs(2 * (m + 2) + 1 + 2);
+    std::vector<double> ub((size_t)n * m);
+    std::vector<int> iw(2 * m + 8);
+    TeamHost team;
+    const int ok = subspace_eig_top(team, n, a, k, m, ub.data(), w.data(), h.data(), hv.data(), theta,
+                                    cs.data(), iw.data());
+    for (size_t e = 0; e < (size_t)n * k; ++e) u[e] = ub[e];
+    return ok;
+}

@@ -171,3 +171,39 @@ def test_team_chol_and_triangular_inverse(lib):
     g = np.asfortranarray(proj.T @ proj)
     inv = np.zeros((4, 4), order="F")
     assert lib.h_team_chol_inv(4, P(g), P(inv), ctypes.c_double(1e-11)) == 2
+
+
+def _gram_with_gap(n, k, seed, gap):
+    s = rng.Substream(seed)
+    q, _ = np.linalg.qr(s.fill_uniform(n, n) - 0.5)
+    lam = np.concatenate([np.logspace(0, -10, k), gap * 1e-10 * s.uniform01_array(n - k)])
+    return np.asfortranarray((q * lam) @ q.T), q[:, :k]
+
+
+@pytest.mark.parametrize("n,k,m", [(100, 20, 28), (64, 8, 16), (120, 20, 28)])
+def test_subspace_eig_top(lib, n, k, m):
+    a, _ = _gram_with_gap(n, k, n + k, 1e-4)
+    u = np.zeros((n, k), order="F")
+    theta = np.zeros(m)
+    assert lib.h_subspace_eig_top(n, P(a), k, m, P(u), P(theta)) == 1
+    w, v = np.linalg.eigh(a)
+    w, v = w[::-1], v[:, ::-1]
+    assert np.allclose(u.T @ u, np.eye(k), atol=1e-12)
+    # Ritz values and the top-k subspace agree with LAPACK (to the Gram floor)
+    assert np.allclose(theta[:k], w[:k], rtol=1e-6, atol=1e-14 * w[0])
+    sv = np.linalg.svd(v[:, :k].T @ u, compute_uv=False)
+    assert sv.min() > 1 - 1e-8
+    # leading (well separated) eigenvectors individually
+    for c in range(3):
+        assert abs(abs(u[:, c] @ v[:, c]) - 1) < 1e-10
+
+
+def test_subspace_eig_top_gives_up_without_gap(lib):
+    s = rng.Substream(3)
+    x = s.fill_uniform(60, 60)
+    a = np.asfortranarray(x @ x.T)  # slowly decaying spectrum: no gap at k
+    u = np.zeros((60, 10), order="F")
+    theta = np.zeros(16)
+    assert lib.h_subspace_eig_top(60, P(a), 10, 16, P(u), P(theta)) == 0
+    z = np.zeros((40, 40), order="F")
+    assert lib.h_subspace_eig_top(40, P(z), 4, 8, P(np.zeros((40, 4), order="F")), P(np.zeros(8))) == 0
