@@ -4,7 +4,7 @@
 One step = one ingest_batch (compress -> per-replica CP-ALS -> align/merge)
 of a temporal batch on the BASELINE c3 workload: dense fp32 1000x1000 slices,
 batches of 100 slices after an initial block of K0=1000, Q=100, P=16
-replicas, rank R=20, shared=25, CP-ALS 30 sweeps x 3 restarts, rel_tol 1e-8
+replicas, rank R=20, shared=10, CP-ALS 30 sweeps x 3 restarts, rel_tol 1e-8
 (SURVEY.md §8(d)).  Metric: tensor entries streamed per second per batch
 update (I*J*t / step time).  Inputs are synthetic (rank-20 U(0,1) factors +
 1% Gaussian noise, generated on the device) and each 400 MB batch exceeds the

@@ -109,21 +109,40 @@ __global__ void als_norm_finish_kernel(AlsDev d, const double* part, int nc) {
 
 // Jacobi eigen-decomposition of the two Gram matrices of replica p, top-R
 // eigenvectors into Ur[p][which] (descending eigenvalue), usability flag.
-__global__ void gevd_eig_sym_kernel(AlsDev d, int v_in_smem) {
+__global__ void __launch_bounds__(1024) gevd_eig_sym_kernel(AlsDev d, int v_in_smem, int mblk) {
     extern __shared__ double sm[];
     const int p = blockIdx.x / 2, which = blockIdx.x % 2;
     const int Q = d.Q, R = d.R;
     double* A = sm;                      // Q*Q
-    double* cs = A + (size_t)Q * Q;      // 2*(Q+2)
-    double* Vs = cs + 2 * (Q + 2);       // Q*Q when v_in_smem
-    int* iw = (int*)(Vs + (v_in_smem ? (size_t)Q * Q : 0));  // Q + 8
+    double* cs = A + (size_t)Q * Q;      // 2*(Q+2) (+ reduction scratch)
+    double* Vs = cs + 2 * (Q + 2) + blockDim.x / 32 + 4;  // Q*Q when v_in_smem
+    int* iw = (int*)(Vs + (v_in_smem ? (size_t)Q * Q : 0));  // 2Q + 16
     int* order = iw + Q + 8;             // Q
     const double* src = d.Gev + ((size_t)p * 2 + which) * Q * Q;
     double* Vg = d.EV + ((size_t)p * 2 + which) * Q * Q;
     double* V = v_in_smem ? Vs : Vg;
+    double* ur = d.Ur + ((size_t)p * 2 + which) * Q * R;
     for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) A[i] = src[i];
     __syncthreads();
     TeamDev team;
+    if (mblk > 0) {
+        // top-R by subspace iteration; the V region holds U, W, H, Hv, theta
+        const int m = mblk;
+        double* U = V;
+        double* W = U + (size_t)Q * m;
+        double* H = W + (size_t)Q * m;
+        double* Hv = H + (size_t)m * m;
+        double* th = Hv + (size_t)m * m;
+        const int ok = subspace_eig_top(team, Q, A, R, m, U, W, H, Hv, th, cs, iw);
+        if (ok) {
+            for (int e = threadIdx.x; e < Q * R; e += blockDim.x) ur[e] = U[e];
+            // nonzero singular values: top-R Ritz values above the rounding floor
+            if (threadIdx.x == 0)
+                atomicAnd(&d.usable[p], (th[0] > 0.0 && th[R - 1] > kEps * Q * th[0]) ? 1 : 0);
+            return;
+        }
+        // no usable gap at R: full Jacobi below (A is untouched)
+    }
     jacobi_eig_sym(team, Q, A, V, cs, iw);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -147,7 +166,6 @@ __global__ void gevd_eig_sym_kernel(AlsDev d, int v_in_smem) {
         atomicAnd(&d.usable[p], nz >= R ? 1 : 0);
     }
     __syncthreads();
-    double* ur = d.Ur + ((size_t)p * 2 + which) * Q * R;
     for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
         const int i = e % Q, r = e / Q;
         ur[i + (size_t)Q * r] = V[i + (size_t)Q * order[r]];
@@ -955,11 +973,15 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
                                                 GevStore{Gev.p, Q, 0}, st, ks, ws.p);
         gemm_f64<true, true>(P, Q, Q, (int)q2, Y1A{dY, q3, Q}, Y1B{dY, q3, Q}, GevStore{Gev.p, Q, 1},
                                               st, ks, ws.p);
-        size_t smem_eig = (q2 + 2 * (Q + 2)) * sizeof(double) + (2 * Q + 16) * sizeof(int) + 64;
+        size_t smem_eig = (q2 + 2 * (Q + 2) + 1024 / 32 + 4) * sizeof(double) + (2 * Q + 16) * sizeof(int) + 64;
         const int v_in_smem = (smem_eig + q2 * sizeof(double) <= 220 * 1024) ? 1 : 0;
         if (v_in_smem) smem_eig += q2 * sizeof(double);
+        // subspace iteration for the top-R block when the matrix is large
+        // enough for it to pay and its scratch fits the V region
+        const int mblk = std::min(Q, R + 8);
+        const int use_sub = (Q >= 2 * mblk && (size_t)2 * Q * mblk + 2 * mblk * mblk + mblk <= q2) ? mblk : 0;
         OCTEN_CUDA(cudaFuncSetAttribute(gevd_eig_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eig));
-        gevd_eig_sym_kernel<<<P * 2, 1024, smem_eig, st>>>(d, v_in_smem); OCTEN_LAUNCHED(1);
+        gevd_eig_sym_kernel<<<P * 2, 1024, smem_eig, st>>>(d, v_in_smem, use_sub); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
         // mixtures -> p1/p2 for all attempts
         gemm_f64<false, true>(NP, (int)q2, 6, Q, YmatA{dY, q3, q2, S, true}, MixB{Wmix.p, Q},
