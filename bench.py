@@ -12,9 +12,11 @@ update (I*J*t / step time).  Inputs are synthetic (rank-20 U(0,1) factors +
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-N>1 (torchrun): every rank runs an independent stream on its own GPU
-("replicas only", weak scaling); value = all ranks'
-entries / max-over-ranks time.
+N>1 (torchrun): by default ONE stream sharded by replica over the ranks
+(rank g compresses into and decomposes replicas [p0, p0+p_local), the merge
+runs redundantly after NCCL all-gathers of the replica models and temporal
+rows; strong scaling, value = batch entries / max-over-ranks step time).
+--multi replicas runs N independent streams instead (weak scaling).
 """
 from __future__ import annotations
 
@@ -237,6 +239,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--multi", default="sharded", choices=["sharded", "replicas"],
+                    help="N>1: one replica-sharded stream over all ranks (NCCL all-gathers, strong scaling) "
+                         "or N independent streams (weak scaling)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
@@ -262,20 +267,30 @@ def main():
     import paper_1807_01350_b200 as ob
     I, J, K0, t, Q, P, R, sh = (cfg[k] for k in ("I", "J", "K0", "t", "Q", "P", "R", "shared"))
     nb = args.warmup + args.steps + args.e2e_steps
-    syn = Synth(torch, dev, I, J, K0 + nb * t, R, seed=1234 + rank)
+    sharded = world > 1 and args.multi == "sharded"
+    # sharded: every rank sees the same batches and seeds (one stream);
+    # replicas: independent streams with per-rank data
+    dseed = 1234 if sharded else 1234 + rank
+    syn = Synth(torch, dev, I, J, K0 + nb * t, R, seed=dseed)
     first = syn.batch(0, K0)
-    scfg = ob.StreamConfig(rank=R, p=P, q=Q, shared=sh, seed=7 * 1234 + 3 + rank,
+    scfg = ob.StreamConfig(rank=R, p=P, q=Q, shared=sh, seed=7 * dseed + 3,
                            als=ob.AlsConfig(max_iters=cfg["iters"], rel_tol=1e-8, n_restarts=cfg["restarts"]),
                            device=local)
     torch.cuda.synchronize()
     t_init = time.perf_counter()
-    st = ob.init_stream(first, scfg)
+    if sharded:
+        st = ob.ShardedStream(scfg, rank, world, lambda snd, rcv: dist.all_gather_into_tensor(rcv, snd))
+        st.ingest(first)
+        ingest = st.ingest
+    else:
+        st = ob.init_stream(first, scfg)
+        ingest = lambda b: ob.ingest_batch(st, b)  # noqa: E731
     t_init = time.perf_counter() - t_init
     del first
     batches = [syn.batch(K0 + i * t, t) for i in range(args.warmup + args.steps)]
     torch.cuda.synchronize()
     for i in range(args.warmup):
-        ob.ingest_batch(st, batches[i])
+        ingest(batches[i])
     times0 = (ctypes_stage_times(ob, st))
     l0 = ob._capi.LIB.octen_launch_count()
     clk = ClockSampler(local)
@@ -285,7 +300,7 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
-        ob.ingest_batch(st, batches[args.warmup + i])
+        ingest(batches[args.warmup + i])
     e1.record()
     barrier()
     clocks = clk.stop()
@@ -298,7 +313,8 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     entries = I * J * t
-    value = world * entries / (ms * 1e-3)
+    jobs = 1 if sharded else world  # batches the whole job processes per step
+    value = jobs * entries / (ms * 1e-3)
 
     # e2e through the C-ABI with pinned host buffers (H2D inside the timed region)
     e2e = None
@@ -314,7 +330,7 @@ def main():
         tw = time.perf_counter()
         d2h = 0
         for h in hb:
-            ob.ingest_batch(st, h)
+            ingest(h)
             m = st.model  # D2H of the updated model (factors + lambda)
             d2h = sum(f.nbytes for f in m.factors) + m.lambda_.nbytes
         barrier()
@@ -323,7 +339,7 @@ def main():
             tt = torch.tensor([e2e_s], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_s = float(tt.item())
-        e2e = {"value": world * entries / e2e_s, "unit": "entries/s", "h2d_bytes_per_step": entries * 4,
+        e2e = {"value": jobs * entries / e2e_s, "unit": "entries/s", "h2d_bytes_per_step": entries * 4,
                "d2h_bytes_per_step": int(d2h)}
 
     hbm, bf16, peak_kind = peaks()
@@ -351,10 +367,12 @@ def main():
     if rank == 0:
         line = {"metric": "tensor entries streamed/sec per batch update", "value": value, "unit": "entries/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
                 "dtype": "f32 compress (split-TF32/FP32) + f64 CP-ALS/merge", "data": "synthetic",
                 "config": {"workload": args.config, **cfg, "l2": "inputs larger than L2 (400 MB fp32 batch)",
-                           "parallelism": "replicas only" if world > 1 else "single"},
+                           "parallelism": ("replica-sharded x%d (NCCL all-gather of replica models)" % world
+                                           if sharded else ("independent streams x%d" % world if world > 1
+                                                            else "single"))},
                 "stages": stage, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks}
         print(json.dumps(line), flush=True)

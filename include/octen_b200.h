@@ -105,7 +105,8 @@ int octen_stream_get_factor(const octen_stream* s, int mode, double* out);
 int octen_stream_get_lambda(const octen_stream* s, double* out);
 /* BatchRecord of log entry `index` (0 = init). */
 int octen_stream_get_record(const octen_stream* s, int64_t index, octen_batch_record* out);
-/* SummaryState: y (p x Q^3) and history (p x Q x rank). */
+/* SummaryState: y (p x Q^3; a sharded handle returns its p_local owned
+ * replicas) and history (p x Q x rank). */
 int octen_stream_get_summaries(const octen_stream* s, double* y);
 int octen_stream_get_history(const octen_stream* s, double* h);
 /* The per-replica CP-ALS models of the last batch: factors p x 3 x Q x rank,
@@ -116,6 +117,33 @@ int octen_stream_get_replica_models(const octen_stream* s, double* factors, doub
  * out[3] mode-1 contraction kernels; out[4] their algorithmic flops,
  * out[5] their launch count. */
 int octen_stream_get_stage_times(const octen_stream* s, double* out);
+
+/* ---- replica-sharded streams (multi-GPU, one process per GPU) ----
+ * The reference fans replicas out over worker threads (streaming.cpp:36-69,
+ * parallel_replicas); here rank g of `shard_world` owns replicas
+ * [p0, p0 + p_local), chunk = ceil(p / shard_world): it compresses every
+ * batch into, and runs CP-ALS on, its own replicas, then runs the alignment
+ * and merge redundantly (bit-identical on every rank) after two all-gathers
+ * that the CALLER performs between the phases over any transport (NCCL via
+ * torch.distributed in bench.py):
+ *   octen_stream_begin  -> models_out : sizes[0] doubles  (device pointer)
+ *   all-gather          -> models_all : shard_world * sizes[0], rank order
+ *   octen_stream_merge  -> rows_out   : sizes[1] doubles  (device pointer)
+ *   all-gather          -> rows_all   : shard_world * sizes[1], rank order
+ *   octen_stream_finish
+ * The first begin on a new handle performs init_stream; later ones
+ * ingest_batch.  A CP-ALS failure on one rank travels in the exchanged block
+ * so every rank raises the same NumericError in merge (no rank is left
+ * waiting in a collective).  octen_stream_init/ingest are the three phases
+ * back to back with shard_world == 1. */
+int octen_stream_create(const octen_stream_config* cfg, int shard_rank, int shard_world, octen_stream** out);
+/* sizes[0..5] = models doubles per rank, rows doubles per rank, p0, p_local,
+ * shard_rank, shard_world. */
+int octen_stream_exchange_sizes(const octen_stream* s, int64_t* sizes);
+int octen_stream_begin(octen_stream* s, const void* data, int dtype, int location, int order, const int64_t* dims,
+                       double* models_out);
+int octen_stream_merge(octen_stream* s, const double* models_all, double* rows_out);
+int octen_stream_finish(octen_stream* s, const double* rows_all);
 
 /* ---- stage-level entry points (the reference's L2 API, batched over replicas) ---- */
 

@@ -1152,6 +1152,14 @@ def validate_config(cfg: StreamConfig, order: int) -> None:
 def _recover_batch(aligned: AlignedStack, rs: ReplicaSet, summaries: SummaryState,
                    stored_nontemporal, c_old_raw, t_new: int):
     """streaming.cpp:89-160."""
+    final, weights = _recover_nontemporal_final(aligned, rs, stored_nontemporal)
+    tstack = temporal_stack_from_summaries(rs, summaries, final)
+    temporal = recover_temporal_append(tstack, rs, summaries, c_old_raw, t_new)
+    return final, temporal, weights
+
+
+def _recover_nontemporal_final(aligned: AlignedStack, rs: ReplicaSet, stored_nontemporal):
+    """streaming.cpp:89-148: solves, two refinement passes, gauge match."""
     order = rs.order()
     rank = aligned.stacks[0].shape[1]
     tmode = rs.temporal_mode
@@ -1186,9 +1194,7 @@ def _recover_batch(aligned: AlignedStack, rs: ReplicaSet, summaries: SummaryStat
                 raise NumericError("recover: zero column in recovered factor")
             fin[:, i] = s[:, j] * (signs[m][i] / nrm)
         final.append(fin)
-    tstack = temporal_stack_from_summaries(rs, summaries, final)
-    temporal = recover_temporal_append(tstack, rs, summaries, c_old_raw, t_new)
-    return final, temporal, weights
+    return final, weights
 
 
 def _assemble_model(nontemporal, temporal_raw, tmode: int) -> KruskalModel:

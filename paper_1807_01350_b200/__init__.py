@@ -19,6 +19,7 @@ from typing import List, Optional
 import numpy as np
 
 from . import _capi as C
+from . import sharding as _sharding
 
 __all__ = ["ConfigError", "NumericError", "IoError", "CudaError", "AlsConfig", "StreamConfig", "BatchRecord",
            "KruskalModel", "StreamState", "init_stream", "ingest_batch", "compress", "cp_als_batched",
@@ -260,6 +261,74 @@ def ingest_batch(state: StreamState, batch) -> None:
     d = (C.c_i64 * len(dims))(*dims)
     _check(C.LIB.octen_stream_ingest(state._h, ptr, dt, loc, len(dims), d))
     del keep
+
+
+def shard_range(p: int, world: int, rank: int):
+    """Replicas owned by `rank` of a `world`-way sharded stream: (p0, p_local)."""
+    try:
+        return _sharding.shard_range(p, world, rank)
+    except ValueError as e:
+        raise ConfigError("octen: " + str(e)) from None
+
+
+exchange_sizes = _sharding.exchange_sizes
+
+
+class ShardedStream(StreamState):
+    """One rank of a replica-sharded stream (include/octen_b200.h,
+    octen_stream_begin/merge/finish).  `allgather(send, recv)` is the
+    caller's collective on CUDA float64 tensors (recv = world x send, rank
+    order), e.g. torch.distributed.all_gather_into_tensor over NCCL."""
+
+    def __init__(self, cfg: StreamConfig, shard_rank: int, shard_world: int, allgather):
+        import torch
+        h = ctypes.c_void_p()
+        c = cfg._c()
+        _check(C.LIB.octen_stream_create(ctypes.byref(c), shard_rank, shard_world, ctypes.byref(h)))
+        super().__init__(h, cfg)
+        sz = (C.c_i64 * 6)()
+        _check(C.LIB.octen_stream_exchange_sizes(h, sz))
+        self.models_count, self.rows_count, self.p0, self.p_local = sz[0], sz[1], sz[2], sz[3]
+        self.shard_rank, self.shard_world = shard_rank, shard_world
+        dev = torch.device("cuda", cfg.device)
+        self._mo = torch.zeros(self.models_count, dtype=torch.float64, device=dev)
+        self._ma = torch.zeros(self.models_count * shard_world, dtype=torch.float64, device=dev)
+        self._ro = torch.zeros(self.rows_count, dtype=torch.float64, device=dev)
+        self._ra = torch.zeros(self.rows_count * shard_world, dtype=torch.float64, device=dev)
+        self._allgather = allgather
+
+    def summaries(self):
+        """The owned replicas' summaries (p_local Q^3 tensors) and the full
+        history (p x Q x R, kept on every rank)."""
+        ys, hs = super().summaries()
+        return ys[:self.p_local], hs
+
+    # the three phases, exposed for callers that drive the exchange themselves
+    def begin(self, batch):
+        keep, ptr, dt, loc, dims = _batch_args(batch)
+        d = (C.c_i64 * len(dims))(*dims)
+        _check(C.LIB.octen_stream_begin(self._h, ptr, dt, loc, len(dims), d, ctypes.c_void_p(self._mo.data_ptr())))
+        del keep
+        return self._mo
+
+    def merge(self, models_all):
+        _check(C.LIB.octen_stream_merge(self._h, ctypes.c_void_p(models_all.data_ptr()),
+                                        ctypes.c_void_p(self._ro.data_ptr())))
+        return self._ro
+
+    def finish(self, rows_all):
+        _check(C.LIB.octen_stream_finish(self._h, ctypes.c_void_p(rows_all.data_ptr())))
+
+    def ingest(self, batch) -> None:
+        """init_stream on the first call, ingest_batch afterwards."""
+        import torch
+        self.begin(batch)
+        self._allgather(self._mo, self._ma)
+        torch.cuda.synchronize()
+        self.merge(self._ma)
+        self._allgather(self._ro, self._ra)
+        torch.cuda.synchronize()
+        self.finish(self._ra)
 
 
 def compress(batch, u: List[np.ndarray], v: List[np.ndarray], w: List[np.ndarray], shared: int) -> List[np.ndarray]:

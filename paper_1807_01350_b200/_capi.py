@@ -60,6 +60,13 @@ SIGNATURES = {
     "octen_stream_ingest": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, P_i64]),
     "octen_stream_destroy": (None, [ctypes.c_void_p]),
+    "octen_stream_create": (ctypes.c_int, [ctypes.POINTER(StreamConfigC), ctypes.c_int, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_void_p)]),
+    "octen_stream_exchange_sizes": (ctypes.c_int, [ctypes.c_void_p, P_i64]),
+    "octen_stream_begin": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          P_i64, ctypes.c_void_p]),
+    "octen_stream_merge": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "octen_stream_finish": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "octen_stream_info": (ctypes.c_int, [ctypes.c_void_p, P_i64]),
     "octen_stream_get_factor": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, P_dbl]),
     "octen_stream_get_lambda": (ctypes.c_int, [ctypes.c_void_p, P_dbl]),

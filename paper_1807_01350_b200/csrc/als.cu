@@ -879,8 +879,16 @@ void AlsEngine::alloc(int P, int S, int Q, int R, int max_iters) {
     Mlam.reserve((size_t)P * R);
 }
 
+std::string als_failure_message(int kind, int a, int b) {
+    // cp_als.cpp:305-307 (non-finite factor), 335-336 (non-finite fit), 251 (zero input)
+    if (kind == 1) return "cp_als: input tensor is identically zero";
+    if (kind == 2) return "cp_als: non-finite factor at sweep " + std::to_string(a) + ", mode " + std::to_string(b);
+    return "cp_als: non-finite fit at sweep " + std::to_string(a);
+}
+
 void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, const double* dY,
                     const std::vector<std::uint64_t>& seeds, cudaStream_t st) {
+    failure = {};
     if (R < 1) throw ConfigError("cp_als: rank must be >= 1");
     if (max_iters < 1) throw ConfigError("cp_als: max_iters must be >= 1");
     if (!(rel_tol > 0.0)) throw ConfigError("cp_als: rel_tol must be > 0");
@@ -940,7 +948,10 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     std::vector<double> hn = normx2.to_host(P, st);
     ++host_syncs;
     for (int p = 0; p < P; ++p)
-        if (hn[p] == 0.0) throw NumericError("cp_als: input tensor is identically zero");
+        if (hn[p] == 0.0) {
+            failure = {1, 0, 0};
+            throw NumericError(als_failure_message(1, 0, 0));
+        }
 
     // ---- host RNG: restart seeds, GEVD mixtures, rescue seeds
     std::vector<std::uint64_t> restart_seed(NP), hres(NP);
@@ -1094,10 +1105,14 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     for (int prob = 0; prob < NP; ++prob) {
         if (!hs[prob].failed) continue;
         const DevStatus& e = he[prob];
-        if (e.code == kAlsNonFiniteFactor)
-            throw NumericError("cp_als: non-finite factor at sweep " + std::to_string(e.a) + ", mode " +
-                               std::to_string(e.b));
-        if (e.code == kAlsNonFiniteFit) throw NumericError("cp_als: non-finite fit at sweep " + std::to_string(e.a));
+        if (e.code == kAlsNonFiniteFactor) {
+            failure = {2, e.a, e.b};
+            throw NumericError(als_failure_message(2, e.a, e.b));
+        }
+        if (e.code == kAlsNonFiniteFit) {
+            failure = {3, e.a, 0};
+            throw NumericError(als_failure_message(3, e.a, 0));
+        }
     }
     DevBuf<int> best;
     best.reserve(P);

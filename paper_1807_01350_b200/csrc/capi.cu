@@ -91,7 +91,12 @@ struct ScopedStream {
     cudaStream_t st = nullptr;
     ScopedStream() { OCTEN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); }
     ~ScopedStream() {
-        if (st) cudaStreamDestroy(st);
+        // drain before the stream's temporaries return to the block cache
+        // (matters on error paths, where the body did not synchronize)
+        if (st) {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
     }
 };
 
@@ -136,6 +141,51 @@ int octen_stream_ingest(octen_stream* s, const void* data, int dtype, int locati
 }
 
 void octen_stream_destroy(octen_stream* s) { delete s; }
+
+int octen_stream_create(const octen_stream_config* cfg, int shard_rank, int shard_world, octen_stream** out) {
+    return guard([&] {
+        if (!cfg || !out) throw octen::ConfigError("octen_stream_create: null argument");
+        auto h = std::make_unique<octen_stream>();
+        h->s = std::make_unique<octen::Stream>(to_cfg(cfg), shard_rank, shard_world);
+        *out = h.release();
+    });
+}
+
+int octen_stream_exchange_sizes(const octen_stream* s, int64_t* sizes) {
+    return guard([&] {
+        if (!s || !sizes) throw octen::ConfigError("octen_stream_exchange_sizes: null argument");
+        const auto& x = *s->s;
+        sizes[0] = (int64_t)x.models_count();
+        sizes[1] = (int64_t)x.rows_count();
+        sizes[2] = x.p0;
+        sizes[3] = x.pl;
+        sizes[4] = x.shard_rank;
+        sizes[5] = x.shard_world;
+    });
+}
+
+int octen_stream_begin(octen_stream* s, const void* data, int dtype, int location, int order, const int64_t* dims,
+                       double* models_out) {
+    return guard([&] {
+        if (!s || !data || !dims || !models_out) throw octen::ConfigError("octen_stream_begin: null argument");
+        check_dtype(dtype, location);
+        s->s->begin(data, dtype, location, order, dims, models_out);
+    });
+}
+
+int octen_stream_merge(octen_stream* s, const double* models_all, double* rows_out) {
+    return guard([&] {
+        if (!s || !models_all || !rows_out) throw octen::ConfigError("octen_stream_merge: null argument");
+        s->s->merge_phase(models_all, rows_out);
+    });
+}
+
+int octen_stream_finish(octen_stream* s, const double* rows_all) {
+    return guard([&] {
+        if (!s || !rows_all) throw octen::ConfigError("octen_stream_finish: null argument");
+        s->s->finish(rows_all);
+    });
+}
 
 int octen_stream_info(const octen_stream* s, int64_t* info) {
     return guard([&] {
@@ -184,7 +234,7 @@ int octen_stream_get_record(const octen_stream* s, int64_t index, octen_batch_re
 int octen_stream_get_summaries(const octen_stream* s, double* y) {
     return guard([&] {
         auto& x = *s->s;
-        const size_t n = (size_t)x.cfg.p * x.cfg.q * x.cfg.q * x.cfg.q;
+        const size_t n = (size_t)x.pl * x.cfg.q * x.cfg.q * x.cfg.q;
         x.Y.download(y, n, x.st);
         OCTEN_CUDA(cudaStreamSynchronize(x.st));
     });
@@ -203,8 +253,8 @@ int octen_stream_get_replica_models(const octen_stream* s, double* factors, doub
     return guard([&] {
         auto& x = *s->s;
         const int P = x.cfg.p, Q = x.cfg.q, R = x.cfg.rank;
-        x.als.Mf.download(factors, (size_t)P * 3 * Q * R, x.st);
-        x.als.Mlam.download(lambda, (size_t)P * R, x.st);
+        x.MfAll.download(factors, (size_t)P * 3 * Q * R, x.st);
+        x.MlamAll.download(lambda, (size_t)P * R, x.st);
         OCTEN_CUDA(cudaStreamSynchronize(x.st));
     });
 }
@@ -314,7 +364,7 @@ int octen_temporal_stack_from_summaries(int p, int q, int rank, int64_t I, int64
         dA.upload(a, (size_t)I * rank, ss.st);
         dB.upload(b, (size_t)J * rank, ss.st);
         dO.reserve((size_t)p * q * rank);
-        m.temporal_stack(dY.p, dA.p, dB.p, dO.p, ss.st);
+        m.temporal_stack(dY.p, 0, p, dA.p, dB.p, dO.p, false, ss.st);
         dO.download(out, (size_t)p * q * rank, ss.st);
         OCTEN_CUDA(cudaStreamSynchronize(ss.st));
     });

@@ -1,14 +1,63 @@
-// Minimal owning device buffer.
+// Minimal owning device buffer over a per-thread, per-device block cache.
+//
+// cudaFree synchronizes the whole device, so per-batch temporaries released
+// with it would stall the pipeline between kernels.  Released blocks go to a
+// cache instead and are reused by later reservations.  Reuse is stream-safe
+// because every public entry point finishes with a stream synchronize and a
+// handle is driven from one host thread (the reference's threading contract,
+// SPEC.md:453): a cached block is never still in use by queued work of
+// another stream when it is handed out again.
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <map>
 #include <vector>
 
 #include "errors.hpp"
 
 namespace octen {
+
+struct BlockCache {
+    std::multimap<size_t, void*> free_blocks[16];  // per device ordinal (bytes -> block)
+
+    static BlockCache& get() {
+        static thread_local BlockCache* c = new BlockCache;  // never destroyed: buffers may outlive it
+        return *c;
+    }
+    void* take(size_t bytes, size_t& got) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        auto& m = free_blocks[dev & 15];
+        auto it = m.lower_bound(bytes);
+        if (it != m.end() && it->first <= 2 * bytes + (1 << 20)) {
+            void* p = it->second;
+            got = it->first;
+            m.erase(it);
+            return p;
+        }
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            trim(dev);
+            OCTEN_CUDA(cudaMalloc(&p, bytes));
+        }
+        got = bytes;
+        return p;
+    }
+    void give(void* p, size_t bytes) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        free_blocks[dev & 15].emplace(bytes, p);
+    }
+    void trim(int dev) {
+        OCTEN_CUDA(cudaDeviceSynchronize());
+        for (auto& kv : free_blocks[dev & 15]) cudaFree(kv.second);
+        free_blocks[dev & 15].clear();
+    }
+};
 
 template <class T>
 struct DevBuf {
@@ -21,7 +70,7 @@ struct DevBuf {
     ~DevBuf() { release(); }
 
     void release() {
-        if (p) cudaFree(p);
+        if (p) BlockCache::get().give(p, n * sizeof(T));
         p = nullptr;
         n = 0;
     }
@@ -30,20 +79,21 @@ struct DevBuf {
         if (count <= n && p) return p;
         release();
         if (count == 0) count = 1;
-        OCTEN_CUDA(cudaMalloc(&p, count * sizeof(T)));
-        n = count;
+        size_t got = 0;
+        p = static_cast<T*>(BlockCache::get().take(count * sizeof(T), got));
+        n = got / sizeof(T);
         return p;
     }
     // Ensure capacity, preserving the first `keep` elements.
     T* grow(size_t count, size_t keep, cudaStream_t st) {
         if (count <= n && p) return p;
-        T* q = nullptr;
-        OCTEN_CUDA(cudaMalloc(&q, count * sizeof(T)));
+        size_t got = 0;
+        T* q = static_cast<T*>(BlockCache::get().take(count * sizeof(T), got));
         if (p && keep) OCTEN_CUDA(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
         OCTEN_CUDA(cudaStreamSynchronize(st));
         release();
         p = q;
-        n = count;
+        n = got / sizeof(T);
         return p;
     }
     void zero(size_t count, cudaStream_t st) {

@@ -39,6 +39,14 @@ struct AlsState {  // per (replica, restart) problem, device resident
     int pad;
 };
 
+// NumericError text of a failed CP-ALS (kind 1 zero input, 2 non-finite
+// factor at sweep a / mode b, 3 non-finite fit at sweep a).
+std::string als_failure_message(int kind, int a, int b);
+
+struct AlsFailure {
+    int kind = 0, a = 0, b = 0;
+};
+
 class AlsEngine {
 public:
     // Y: P x Q^3 device summaries.  seeds: per replica AlsConfig.seed.
@@ -50,6 +58,7 @@ public:
     std::vector<AlsReplicaResult> results;
     int last_sweeps = 0;
     int host_syncs = 0;
+    AlsFailure failure;  // set when run() throws a NumericError
 
 private:
     void alloc(int P, int S, int Q, int R, int max_iters);
@@ -128,10 +137,16 @@ public:
     void recover(const double* dY, const double* dW, std::int64_t t, double* dHist, const double* dStoredA,
                  const double* dStoredB, double* dAfin, double* dBfin, double* dRows, double* residual,
                  cudaStream_t st);
+    // The non-temporal part of recover: solves, two refinement passes and the
+    // gauge match (streaming.cpp:89-131) -> dAfin, dBfin.
+    void recover_ab(const double* dStoredA, const double* dStoredB, double* dAfin, double* dBfin, cudaStream_t st);
 
     // Stage-level helpers (also exposed through the C-ABI for parity tests).
     void solve_nontemporal(int n, const double* dStack, double* dOut, cudaStream_t st);
-    void temporal_stack(const double* dY, const double* dA, const double* dB, double* dTstack, cudaStream_t st);
+    // temporal_stack_from_summaries for replicas [p0, p0 + pl), dY holding
+    // those pl summaries; output stacked (P*Q x R) or replica-major (pl x Q x R).
+    void temporal_stack(const double* dY, int p0, int pl, const double* dA, const double* dB, double* dOut,
+                        bool replica_major, cudaStream_t st);
     void temporal_append(const double* dTstack, const double* dW, std::int64_t t, double* dHist, double* dRows,
                          double* residual, cudaStream_t st);
 

@@ -466,47 +466,74 @@ __global__ void scale_stack_kernel(int P, int Q, int R, const double* stack, con
     }
 }
 
-// match_columns (recovery.cpp:559-588) on the two non-temporal factors.
-__global__ void match_columns_kernel(int R, long long d0, long long d1, const double* cur0, const double* cur1,
-                                     const double* sto0, const double* sto1, int* perm_out, double* signs_out,
-                                     double* sim_out) {
-    extern __shared__ double sm[];
-    double* sim = sm;               // R*R
-    double* nc = sim + R * R;       // 2R
-    double* ns = nc + 2 * R;        // 2R
+// match_columns (recovery.cpp:559-588): per mode n, the R x R dot products
+// between stored columns i and current columns j plus the column norms.
+// Block (n, j): threads stride over the rows of current column j (coalesced)
+// for 16 stored columns at a time; fixed-order block reduction.
+__global__ void __launch_bounds__(256) match_dots_kernel(int R, long long d0, long long d1, const double* cur0,
+                                                         const double* cur1, const double* sto0, const double* sto1,
+                                                         double* dots, double* nc, double* ns) {
+    __shared__ double red[8][18];
+    const int n = blockIdx.x / R, j = blockIdx.x % R;
+    const long long d = n ? d1 : d0;
+    const double* cur = (n ? cur1 : cur0) + (size_t)d * j;
+    const double* sto = n ? sto1 : sto0;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i0 = 0; i0 < R + 2; i0 += 16) {
+        double acc[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+        for (long long k = threadIdx.x; k < d; k += blockDim.x) {
+            const double x = cur[k];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const int i = i0 + c;
+                if (i < R)
+                    acc[c] += sto[k + (size_t)d * i] * x;
+                else if (i == R)
+                    acc[c] += x * x;  // |current column j|^2
+                else if (i == R + 1) {
+                    const double y = sto[k + (size_t)d * j];
+                    acc[c] += y * y;  // |stored column j|^2
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            double v = acc[c];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) red[w][c] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < 16) {
+            const int i = i0 + threadIdx.x;
+            double v = 0.0;
+            for (int ww = 0; ww < 8; ++ww) v += red[ww][threadIdx.x];
+            if (i < R)
+                dots[(size_t)n * R * R + i + (size_t)R * j] = v;
+            else if (i == R)
+                nc[n * R + j] = sqrt(v);
+            else if (i == R + 1)
+                ns[n * R + j] = sqrt(v);
+        }
+        __syncthreads();
+    }
+}
+
+// sim(i, j) = prod_n |cos(stored_i, current_j)|, greedy one-to-one match with
+// lowest-index tie-break, signs of the matched cosines (recovery.cpp:559-588).
+__global__ void match_select_kernel(int R, const double* dots, const double* nc, const double* ns, int* perm_out,
+                                    double* signs_out, double* sim_out) {
+    extern __shared__ double sim[];  // R*R
     __shared__ int perm[64];
     __shared__ unsigned char ru[64], cu[64];
-    for (int e = threadIdx.x; e < 2 * R; e += blockDim.x) {
-        const int n = e / R, c = e % R;
-        const long long d = n ? d1 : d0;
-        const double* cur = (n ? cur1 : cur0) + (size_t)d * c;
-        const double* sto = (n ? sto1 : sto0) + (size_t)d * c;
-        double a = 0.0, b = 0.0;
-        for (long long i = 0; i < d; ++i) {
-            a += cur[i] * cur[i];
-            b += sto[i] * sto[i];
-        }
-        nc[e] = sqrt(a);
-        ns[e] = sqrt(b);
-    }
-    __syncthreads();
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
         const int i = e % R, j = e / R;  // i: stored, j: current
         double s = 1.0;
         for (int n = 0; n < 2; ++n) {
-            const long long d = n ? d1 : d0;
-            const double* cur = (n ? cur1 : cur0) + (size_t)d * j;
-            const double* sto = (n ? sto1 : sto0) + (size_t)d * i;
             const double a = nc[n * R + j] > 0.0 ? 1.0 / nc[n * R + j] : 1.0;
             const double b = ns[n * R + i] > 0.0 ? 1.0 / ns[n * R + i] : 1.0;
-            double d0s = 0.0, d1s = 0.0;
-            long long k = 0;
-            for (; k + 1 < d; k += 2) {
-                d0s += sto[k] * cur[k];
-                d1s += sto[k + 1] * cur[k + 1];
-            }
-            if (k < d) d0s += sto[k] * cur[k];
-            s *= fabs((d0s + d1s) * a * b);
+            s *= fabs(dots[(size_t)n * R * R + e] * a * b);
         }
         sim[e] = s;
     }
@@ -515,14 +542,7 @@ __global__ void match_columns_kernel(int R, long long d0, long long d1, const do
     __syncthreads();
     for (int e = threadIdx.x; e < 2 * R; e += blockDim.x) {
         const int n = e / R, i = e % R, j = perm[i];
-        const long long d = n ? d1 : d0;
-        const double* cur = (n ? cur1 : cur0) + (size_t)d * j;
-        const double* sto = (n ? sto1 : sto0) + (size_t)d * i;
-        const double a = nc[n * R + j] > 0.0 ? nc[n * R + j] : 1.0;
-        const double b = ns[n * R + i] > 0.0 ? ns[n * R + i] : 1.0;
-        double dot = 0.0;
-        for (long long k = 0; k < d; ++k) dot += sto[k] * cur[k];  // sign of the cosine (norms > 0)
-        signs_out[(size_t)n * R + i] = dot < 0.0 ? -1.0 : 1.0;
+        signs_out[(size_t)n * R + i] = dots[(size_t)n * R * R + i + (size_t)R * j] < 0.0 ? -1.0 : 1.0;
     }
     for (int i = threadIdx.x; i < R; i += blockDim.x) perm_out[i] = perm[i];
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) sim_out[e] = sim[e];
@@ -554,8 +574,11 @@ __global__ void finalize_kernel(int R, long long d, const double* solved, const 
 
 // Per replica: C~_p = M_p Gram_p^-1 with Gram_p = (Ut^T Ut) .* (Vt^T Vt)
 // (COD solve of recovery.cpp:456-459; pseudo-inverse fallback when singular).
-__global__ void tstack_solve_kernel(int P, int Q, int R, const double* Ut, const double* Vt, const double* Mt,
-                                    double* tstack) {
+// Output element (replica p, row c, column r) at tstack[p*sp + c + sr*r]:
+// sp = Q, sr = P*Q for the stacked P*Q x R layout; sp = Q*R, sr = Q for
+// replica-major Q x R blocks (the all-gather layout of sharded streams).
+__global__ void tstack_solve_kernel(int Q, int R, const double* Ut, const double* Vt, const double* Mt,
+                                    double* tstack, long long sp, long long sr) {
     const int p = blockIdx.x;
     extern __shared__ double sm[];
     double* Gm = sm;           // R*R
@@ -580,13 +603,12 @@ __global__ void tstack_solve_kernel(int P, int Q, int R, const double* Ut, const
     if (threadIdx.x == 0) rank = chol_semidef(R, Lf, R, kEps * R);
     __syncthreads();
     const double* m = Mt + (size_t)p * Q * R;
-    const size_t PQ = (size_t)P * Q;
     if (rank == R) {
         for (int c = threadIdx.x; c < Q; c += blockDim.x) {
             double x[64];
             for (int r = 0; r < R; ++r) x[r] = m[c + (size_t)Q * r];
             chol_solve_vec(R, Lf, R, x, 1);
-            for (int r = 0; r < R; ++r) tstack[(size_t)p * Q + c + PQ * r] = x[r];
+            for (int r = 0; r < R; ++r) tstack[(size_t)p * sp + c + (size_t)sr * r] = x[r];
         }
     } else {
         TeamDev team;
@@ -609,7 +631,7 @@ __global__ void tstack_solve_kernel(int P, int Q, int R, const double* Ut, const
                 dot /= w;
                 for (int i = 0; i < R; ++i) y[i] += Ev[i + R * e] * dot;
             }
-            for (int r = 0; r < R; ++r) tstack[(size_t)p * Q + c + PQ * r] = y[r];
+            for (int r = 0; r < R; ++r) tstack[(size_t)p * sp + c + (size_t)sr * r] = y[r];
         }
     }
 }
@@ -974,23 +996,28 @@ void MergeEngine::solve_nontemporal(int n, const double* dStack, double* dOut, c
     chol_solve_blocked(Lsum[n].p, (int)d, (int)d, 0, Lsum_inv[n], dOut, (int)d, 0, R, 1, st);
 }
 
-void MergeEngine::temporal_stack(const double* dY, const double* dA, const double* dB, double* dTstack,
-                                 cudaStream_t st) {
+void MergeEngine::temporal_stack(const double* dY, int p0, int pl, const double* dA, const double* dB, double* dOut,
+                                 bool replica_major, cudaStream_t st) {
     const size_t q2 = (size_t)Q * Q, q3 = q2 * Q;
+    if (pl <= 0) return;
     tg.reserve((size_t)P * 2 * Q * R);
     double* Ut = tg.p;
-    double* Vt = tg.p + (size_t)P * Q * R;
-    gemm_f64<true, true>(P, Q, R, (int)dims[0], UtA{Ud[0].p, dims[0], Q}, ColB{dA, dims[0], 0},
+    double* Vt = tg.p + (size_t)pl * Q * R;
+    const double* U0 = Ud[0].p + (size_t)p0 * dims[0] * Q;
+    const double* V0 = Ud[1].p + (size_t)p0 * dims[1] * Q;
+    gemm_f64<true, true>(pl, Q, R, (int)dims[0], UtA{U0, dims[0], Q}, ColB{dA, dims[0], 0},
                                           StoreCM{Ut, Q, (long long)Q * R}, st);
-    gemm_f64<true, true>(P, Q, R, (int)dims[1], UtA{Ud[1].p, dims[1], Q}, ColB{dB, dims[1], 0},
+    gemm_f64<true, true>(pl, Q, R, (int)dims[1], UtA{V0, dims[1], Q}, ColB{dB, dims[1], 0},
                                           StoreCM{Vt, Q, (long long)Q * R}, st);
-    tmp.reserve((size_t)P * Q * R);
-    const int ks = pick_ksplit(P, Q, R, (int)q2);
-    tscr.reserve((size_t)P * ks * Q * R);
-    gemm_f64<true, true>(P, Q, R, (int)q2, YtA2{dY, q3, q2}, KrB{Ut, Vt, Q, R},
+    tmp.reserve((size_t)pl * Q * R);
+    const int ks = pick_ksplit(pl, Q, R, (int)q2);
+    tscr.reserve((size_t)pl * ks * Q * R);
+    gemm_f64<true, true>(pl, Q, R, (int)q2, YtA2{dY, q3, q2}, KrB{Ut, Vt, Q, R},
                                           StoreCM{tmp.p, Q, (long long)Q * R}, st, ks, tscr.p);
     const size_t smem = (size_t)(3 * R * R + 2 * (R + 2)) * sizeof(double) + (R + 8) * sizeof(int) + 16;
-    tstack_solve_kernel<<<P, 128, smem, st>>>(P, Q, R, Ut, Vt, tmp.p, dTstack); OCTEN_LAUNCHED(1);
+    const long long sp = replica_major ? (long long)Q * R : (long long)Q;
+    const long long sr = replica_major ? (long long)Q : (long long)P * Q;
+    tstack_solve_kernel<<<pl, 128, smem, st>>>(Q, R, Ut, Vt, tmp.p, dOut, sp, sr); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
 }
 
@@ -1049,6 +1076,16 @@ void MergeEngine::temporal_append(const double* dTstack, const double* dW, std::
 void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, double* dHist, const double* dStoredA,
                           const double* dStoredB, double* dAfin, double* dBfin, double* dRows, double* residual,
                           cudaStream_t st) {
+    recover_ab(dStoredA, dStoredB, dAfin, dBfin, st);
+    // temporal stack from the summaries, then the append
+    DevBuf<double> tstack;
+    tstack.reserve((size_t)P * Q * R);
+    temporal_stack(dY, 0, P, dAfin, dBfin, tstack.p, false, st);
+    temporal_append(tstack.p, dW, t, dHist, dRows, residual, st);
+}
+
+void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, double* dAfin, double* dBfin,
+                             cudaStream_t st) {
     const long long PQ = (long long)P * Q;
     for (int n = 0; n < 2; ++n) {
         solved[n].reserve((size_t)dims[n] * R);
@@ -1131,9 +1168,14 @@ void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, do
     err.reserve(P + 1 + 64);
     err.zero(2, st);
     if (dStoredA && dStoredB) {
-        const size_t smem = (size_t)(R * R + 4 * R) * sizeof(double);
-        match_columns_kernel<<<1, 1024, smem, st>>>(R, dims[0], dims[1], solved[0].p, solved[1].p, dStoredA, dStoredB,
-                                                   perm.p, signs.p, simb.p); OCTEN_LAUNCHED(1);
+        DevBuf<double> mdots;
+        mdots.reserve((size_t)2 * R * R + 4 * R);
+        match_dots_kernel<<<2 * R, 256, 0, st>>>(R, dims[0], dims[1], solved[0].p, solved[1].p, dStoredA, dStoredB,
+                                                 mdots.p, mdots.p + 2 * R * R, mdots.p + 2 * R * R + 2 * R);
+        OCTEN_LAUNCHED(1);
+        match_select_kernel<<<1, 128, (size_t)R * R * sizeof(double), st>>>(
+            R, mdots.p, mdots.p + 2 * R * R, mdots.p + 2 * R * R + 2 * R, perm.p, signs.p, simb.p);
+        OCTEN_LAUNCHED(1);
         finalize_kernel<<<R, 256, 0, st>>>(R, dims[0], solved[0].p, perm.p, signs.p, dAfin, err.p, 0); OCTEN_LAUNCHED(1);
         finalize_kernel<<<R, 256, 0, st>>>(R, dims[1], solved[1].p, perm.p, signs.p + R, dBfin, err.p + 1, 1); OCTEN_LAUNCHED(1);
         last_perm = perm.to_host(R, st);
@@ -1147,11 +1189,6 @@ void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, do
     }
     OCTEN_CUDA(cudaGetLastError());
     check_errs(err, 2, st);
-    // temporal stack from the summaries, then the append
-    DevBuf<double> tstack;
-    tstack.reserve((size_t)PQ * R);
-    temporal_stack(dY, dAfin, dBfin, tstack.p, st);
-    temporal_append(tstack.p, dW, t, dHist, dRows, residual, st);
 }
 
 }  // namespace octen

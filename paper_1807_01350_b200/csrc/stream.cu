@@ -93,7 +93,13 @@ int grid1d(size_t n) {
 
 }  // namespace
 
-Stream::Stream(const StreamCfg& c) : cfg(c) {
+Stream::Stream(const StreamCfg& c, int rank, int world) : cfg(c), shard_rank(rank), shard_world(world) {
+    if (world < 1 || rank < 0 || rank >= world) throw ConfigError("octen: shard rank/world out of range");
+    if (cfg.p >= 1 && world > cfg.p) throw ConfigError("octen: more shards than replicas");
+    const int P = std::max(1, cfg.p);
+    chunk = (P + world - 1) / world;
+    p0 = std::min(P, rank * chunk);
+    pl = std::max(0, std::min(P, p0 + chunk) - p0);
     OCTEN_CUDA(cudaSetDevice(cfg.device));
     OCTEN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     OCTEN_CUDA(cudaEventCreate(&ev0));
@@ -102,6 +108,7 @@ Stream::Stream(const StreamCfg& c) : cfg(c) {
 }
 
 Stream::~Stream() {
+    if (st) cudaStreamSynchronize(st);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     for (auto& e : evs)
@@ -200,21 +207,6 @@ void Stream::check_finite(const void* dX, int dtype, size_t n) {
     if (flag.to_host(1, st)[0]) throw NumericError("DenseTensor: non-finite value");
 }
 
-void Stream::compress_stage(const void* dX, int dtype, std::int64_t t) {
-    if (dtype == 1)
-        comp.compress_f32((const float*)dX, t, dW.p, Y.p, st);
-    else
-        comp.compress_f64((const double*)dX, t, dW.p, Y.p, st);
-    ++batches_seen;
-}
-
-void Stream::als_stage(std::int64_t batch_index) {
-    std::vector<std::uint64_t> seeds(cfg.p);
-    for (int r = 0; r < cfg.p; ++r)
-        seeds[r] = rng::derive(cfg.seed, {rng::kStreamAls, (std::uint64_t)r, (std::uint64_t)batch_index});
-    als.run(cfg.p, cfg.als_n_restarts, cfg.q, cfg.rank, cfg.als_max_iters, cfg.als_rel_tol, Y.p, seeds, st);
-}
-
 void Stream::ensure_c_capacity(std::int64_t rows) {
     if (rows <= capC && C.p) return;
     std::int64_t cap = std::max<std::int64_t>(capC * 2, rows);
@@ -230,43 +222,8 @@ void Stream::ensure_c_capacity(std::int64_t rows) {
     capC = cap;
 }
 
-void Stream::recover_stage(std::int64_t t_new, bool first, BatchRecordC& rec) {
-    AlignResultHost ar;
-    merge.align(als.Mf.p, als.Mlam.p, tgram, st, &ar);
-    rec.min_match_similarity = ar.min_match;
-    rec.max_offdiag_similarity = ar.max_offdiag;
-    const int R = cfg.rank;
-    Anew.reserve((size_t)I * R);
-    Bnew.reserve((size_t)J * R);
-    rows.reserve((size_t)t_new * R);
-    double residual = 0.0;
-    merge.recover(Y.p, dW.p, t_new, hist.p, first ? nullptr : A.p, first ? nullptr : B.p, Anew.p, Bnew.p, rows.p,
-                  &residual, st);
-    rec.temporal_residual = residual;
-    rec.warned = residual > cfg.residual_warning ? 1 : 0;
-    if (rec.warned && cfg.strict) {
-        if (first)
-            throw NumericError("init_stream: temporal solve residual " + std::to_string(residual) +
-                               " exceeds strict threshold");
-        throw NumericError("temporal solve residual " + std::to_string(residual) + " exceeds strict threshold");
-    }
-    // assemble_model (streaming.cpp:162-177): C_raw = [C diag(lambda); rows]
-    ensure_c_capacity(K + t_new);
-    if (!first && K > 0) {
-        scale_cols_kernel<<<grid1d((size_t)K * R), 256, 0, st>>>(C.p, K, capC, R, lam.p);
-        OCTEN_LAUNCHED(1);
-    }
-    append_rows_kernel<<<grid1d((size_t)t_new * R), 256, 0, st>>>(C.p, K, capC, R, rows.p, t_new); OCTEN_LAUNCHED(1);
-    std::swap(A.p, Anew.p);
-    std::swap(A.n, Anew.n);
-    std::swap(B.p, Bnew.p);
-    std::swap(B.n, Bnew.n);
-    normalize_model_kernel<<<R, 256, 0, st>>>(A.p, I, B.p, J, C.p, K + t_new, capC, lam.p); OCTEN_LAUNCHED(1);
-    OCTEN_CUDA(cudaGetLastError());
-    K += t_new;
-}
-
-void Stream::init(const void* data, int dtype, int location, int order, const std::int64_t* dims) {
+// ---- first-batch preparation (streaming.cpp:181-215) ----
+void Stream::prepare(int order, const std::int64_t* dims) {
     if (cfg.temporal_mode < 0) cfg.temporal_mode = order - 1;
     validate(order);
     const std::int64_t t0 = dims[2];
@@ -288,14 +245,16 @@ void Stream::init(const void* data, int dtype, int location, int order, const st
         if (sum < 2L * cfg.rank + 2)
             throw ConfigError("init_stream: compressed decomposition fails the identifiability bound");
     }
-    const auto t_start = Clock::now();
     gen_replicas();
     const int P = cfg.p, Q = cfg.q, R = cfg.rank;
-    comp.set_projections(P, Q, cfg.shared, I, J, hU.data(), hV.data(), st);
+    // compression and summaries for the owned replicas only
+    if (pl > 0)
+        comp.set_projections(pl, Q, cfg.shared, I, J, hU.data() + (size_t)p0 * I * Q, hV.data() + (size_t)p0 * J * Q,
+                             st);
     merge.set_projections(P, Q, cfg.shared, R, I, J, hU.data(), hV.data(), st);
     const size_t q3 = (size_t)Q * Q * Q;
-    Y.reserve((size_t)P * q3);
-    Y.zero((size_t)P * q3, st);
+    Y.reserve((size_t)std::max(pl, 1) * q3);
+    Y.zero((size_t)std::max(pl, 1) * q3, st);
     hist.reserve((size_t)P * Q * R);
     hist.zero((size_t)P * Q * R, st);
     lam.reserve(R);
@@ -303,41 +262,216 @@ void Stream::init(const void* data, int dtype, int location, int order, const st
     B.reserve((size_t)J * R);
     K = 0;
     batches_seen = 0;
+}
 
-    BatchRecordC rec{};
-    rec.batch_index = 0;
-    rec.t_new = t0;
-    auto tc = Clock::now();
-    const size_t n = (size_t)I * J * t0;
-    const void* dX = stage_input(data, dtype, location, n);
-    check_finite(dX, dtype, n);
-    extend_temporal(t0);
-    OCTEN_CUDA(cudaEventRecord(evs[0], st));
-    compress_stage(dX, dtype, t0);
-    OCTEN_CUDA(cudaEventRecord(evs[1], st));
-    OCTEN_CUDA(cudaStreamSynchronize(st));
-    rec.compress_seconds = seconds_since(tc);
-    auto ta = Clock::now();
-    OCTEN_CUDA(cudaEventRecord(evs[2], st));
-    als_stage(0);
-    OCTEN_CUDA(cudaEventRecord(evs[3], st));
-    rec.als_seconds = seconds_since(ta);
-    auto tr = Clock::now();
-    recover_stage(t0, true, rec);
-    OCTEN_CUDA(cudaEventRecord(evs[4], st));
-    OCTEN_CUDA(cudaStreamSynchronize(st));
-    accumulate_stage_times();
-    rec.recover_seconds = seconds_since(tr);
-    rec.total_seconds = seconds_since(t_start);
-    log.push_back(rec);
-    initialized = true;
+// ---- phase 1: stage, compress and decompose the owned replicas ----
+void Stream::begin(const void* data, int dtype, int location, int order, const std::int64_t* dims,
+                   double* models_out) {
+    if (pending) throw ConfigError("octen: the previous batch has not finished (begin/merge/finish)");
+    const bool first = !initialized;
+    if (first) {
+        prepare(order, dims);
+    } else {
+        // streaming.cpp:258-346
+        if (order != 3)
+            throw ConfigError("ingest_batch: batch order mismatch at batch " + std::to_string(batches_seen));
+        if (dims[0] != I)
+            throw ConfigError("ingest_batch: extent mismatch on mode 1 at batch " + std::to_string(batches_seen));
+        if (dims[1] != J)
+            throw ConfigError("ingest_batch: extent mismatch on mode 2 at batch " + std::to_string(batches_seen));
+        if (dims[2] < 1) throw ConfigError("ingest_batch: batch has no temporal extent");
+    }
+    const std::int64_t t = dims[2];
+    context = first ? std::string() : "batch " + std::to_string(batches_seen) + ": ";
+    if (!first && cfg.strict) snapshot(backup);
+    pending = true;
+    pending_first = first;
+    pending_t = t;
+    t_start = Clock::now();
+    prec = BatchRecordC{};
+    prec.batch_index = first ? 0 : batches_seen;
+    prec.t_new = t;
+    const int Q = cfg.q, R = cfg.rank;
+    try {
+        auto tc = Clock::now();
+        const size_t n = (size_t)I * J * t;
+        const void* dX = stage_input(data, dtype, location, n);
+        check_finite(dX, dtype, n);
+        extend_temporal(t);
+        OCTEN_CUDA(cudaEventRecord(evs[0], st));
+        if (pl > 0) {
+            const double* dWl = dW.p + (size_t)p0 * t * Q;
+            if (dtype == 1)
+                comp.compress_f32((const float*)dX, t, dWl, Y.p, st);
+            else
+                comp.compress_f64((const double*)dX, t, dWl, Y.p, st);
+        }
+        ++batches_seen;
+        OCTEN_CUDA(cudaEventRecord(evs[1], st));
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+        prec.compress_seconds = std::chrono::duration<double>(Clock::now() - tc).count();
+        auto ta = Clock::now();
+        OCTEN_CUDA(cudaEventRecord(evs[2], st));
+        double hdr[4] = {0, 0, 0, 0};
+        const size_t qr = (size_t)Q * R;
+        if (pl > 0) {
+            std::vector<std::uint64_t> seeds(pl);
+            for (int r = 0; r < pl; ++r)
+                seeds[r] = rng::derive(cfg.seed, {rng::kStreamAls, (std::uint64_t)(p0 + r), (std::uint64_t)prec.batch_index});
+            try {
+                als.run(pl, cfg.als_n_restarts, Q, R, cfg.als_max_iters, cfg.als_rel_tol, Y.p, seeds, st);
+            } catch (const NumericError&) {
+                // a replica's CP-ALS failed: every rank raises it after the exchange
+                if (als.failure.kind == 0) throw;
+                hdr[0] = als.failure.kind;
+                hdr[1] = als.failure.a;
+                hdr[2] = als.failure.b;
+            }
+            if (hdr[0] == 0.0) {
+                OCTEN_CUDA(cudaMemcpyAsync(models_out + 4, als.Mf.p, sizeof(double) * pl * 3 * qr,
+                                           cudaMemcpyDeviceToDevice, st));
+                OCTEN_CUDA(cudaMemcpyAsync(models_out + 4 + (size_t)chunk * 3 * qr, als.Mlam.p, sizeof(double) * pl * R,
+                                           cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        OCTEN_CUDA(cudaMemcpyAsync(models_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
+        OCTEN_CUDA(cudaEventRecord(evs[3], st));
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+        prec.als_seconds = std::chrono::duration<double>(Clock::now() - ta).count();
+    } catch (...) {
+        fail_pending();
+    }
+}
+
+// ---- phase 2: align, recover A and B, temporal-stack rows of the owned replicas ----
+void Stream::merge_phase(const double* models_all, double* rows_out) {
+    if (!pending) throw ConfigError("octen: merge without a begun batch");
+    try {
+        t_recover = Clock::now();
+        const int P = cfg.p, Q = cfg.q, R = cfg.rank;
+        const size_t qr = (size_t)Q * R, mc = models_count();
+        // CP-ALS failures of any rank (lowest replica first)
+        std::vector<double> hdr((size_t)shard_world * 4);
+        for (int g = 0; g < shard_world; ++g)
+            OCTEN_CUDA(cudaMemcpyAsync(hdr.data() + 4 * g, models_all + (size_t)g * mc, 4 * sizeof(double),
+                                       cudaMemcpyDeviceToHost, st));
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+        for (int g = 0; g < shard_world; ++g)
+            if (hdr[4 * g] != 0.0)
+                throw NumericError(als_failure_message((int)hdr[4 * g], (int)hdr[4 * g + 1], (int)hdr[4 * g + 2]));
+        MfAll.reserve((size_t)P * 3 * qr);
+        MlamAll.reserve((size_t)P * R);
+        for (int g = 0; g < shard_world; ++g) {
+            const int g0 = g * chunk, gl = std::max(0, std::min(P, g0 + chunk) - g0);
+            if (gl == 0) continue;
+            const double* blk = models_all + (size_t)g * mc;
+            OCTEN_CUDA(cudaMemcpyAsync(MfAll.p + (size_t)g0 * 3 * qr, blk + 4, sizeof(double) * gl * 3 * qr,
+                                       cudaMemcpyDeviceToDevice, st));
+            OCTEN_CUDA(cudaMemcpyAsync(MlamAll.p + (size_t)g0 * R, blk + 4 + (size_t)chunk * 3 * qr,
+                                       sizeof(double) * gl * R, cudaMemcpyDeviceToDevice, st));
+        }
+        AlignResultHost ar;
+        merge.align(MfAll.p, MlamAll.p, tgram, st, &ar);
+        prec.min_match_similarity = ar.min_match;
+        prec.max_offdiag_similarity = ar.max_offdiag;
+        Anew.reserve((size_t)I * R);
+        Bnew.reserve((size_t)J * R);
+        merge.recover_ab(pending_first ? nullptr : A.p, pending_first ? nullptr : B.p, Anew.p, Bnew.p, st);
+        if (pl > 0) merge.temporal_stack(Y.p, p0, pl, Anew.p, Bnew.p, rows_out, true, st);
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+        fail_pending();
+    }
+}
+
+namespace {
+// rows_all (world blocks of chunk x Q x R, replica-major) -> P*Q x R stacked
+__global__ void unpack_rows_kernel(const double* rows_all, size_t per_rank, int chunk, int P, int Q, int R,
+                                   double* tstack) {
+    const size_t total = (size_t)P * Q * R, PQ = (size_t)P * Q;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const size_t row = e % PQ;
+        const int r = (int)(e / PQ);
+        const int p = (int)(row / Q), i = (int)(row % Q);
+        const int g = p / chunk, pi = p % chunk;
+        tstack[row + PQ * r] = rows_all[(size_t)g * per_rank + (size_t)pi * Q * R + i + (size_t)Q * r];
+    }
+}
+}  // namespace
+
+// ---- phase 3: temporal append, model assembly, BatchRecord ----
+void Stream::finish(const double* rows_all) {
+    if (!pending) throw ConfigError("octen: finish without a begun batch");
+    try {
+        const int P = cfg.p, Q = cfg.q, R = cfg.rank;
+        const std::int64_t t_new = pending_t;
+        tstackAll.reserve((size_t)P * Q * R);
+        unpack_rows_kernel<<<grid1d((size_t)P * Q * R), 256, 0, st>>>(rows_all, rows_count(), chunk, P, Q, R,
+                                                                       tstackAll.p);
+        OCTEN_LAUNCHED(1);
+        rows.reserve((size_t)t_new * R);
+        double residual = 0.0;
+        merge.temporal_append(tstackAll.p, dW.p, t_new, hist.p, rows.p, &residual, st);
+        prec.temporal_residual = residual;
+        prec.warned = residual > cfg.residual_warning ? 1 : 0;
+        if (prec.warned && cfg.strict) {
+            if (pending_first)
+                throw NumericError("init_stream: temporal solve residual " + std::to_string(residual) +
+                                   " exceeds strict threshold");
+            throw NumericError("temporal solve residual " + std::to_string(residual) + " exceeds strict threshold");
+        }
+        // assemble_model (streaming.cpp:162-177): C_raw = [C diag(lambda); rows]
+        ensure_c_capacity(K + t_new);
+        if (!pending_first && K > 0) {
+            scale_cols_kernel<<<grid1d((size_t)K * R), 256, 0, st>>>(C.p, K, capC, R, lam.p);
+            OCTEN_LAUNCHED(1);
+        }
+        append_rows_kernel<<<grid1d((size_t)t_new * R), 256, 0, st>>>(C.p, K, capC, R, rows.p, t_new);
+        OCTEN_LAUNCHED(1);
+        std::swap(A.p, Anew.p);
+        std::swap(A.n, Anew.n);
+        std::swap(B.p, Bnew.p);
+        std::swap(B.n, Bnew.n);
+        normalize_model_kernel<<<R, 256, 0, st>>>(A.p, I, B.p, J, C.p, K + t_new, capC, lam.p);
+        OCTEN_LAUNCHED(1);
+        OCTEN_CUDA(cudaGetLastError());
+        OCTEN_CUDA(cudaEventRecord(evs[4], st));
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+        K += t_new;
+        accumulate_stage_times();
+        prec.recover_seconds = std::chrono::duration<double>(Clock::now() - t_recover).count();
+        prec.total_seconds = std::chrono::duration<double>(Clock::now() - t_start).count();
+        log.push_back(prec);
+        initialized = true;
+        pending = false;
+    } catch (...) {
+        fail_pending();
+    }
+}
+
+// Error inside a phase: drain the stream, roll back (strict mode), add the
+// batch context (streaming.cpp:336-345) and rethrow.
+void Stream::fail_pending() {
+    cudaStreamSynchronize(st);
+    (void)cudaGetLastError();
+    const bool had = pending;
+    pending = false;
+    const bool first = pending_first;
+    if (had && !first && cfg.strict) restore(backup);
+    try {
+        throw;
+    } catch (const ConfigError& e) {
+        throw ConfigError(context + e.what());
+    } catch (const NumericError& e) {
+        throw NumericError(context + e.what());
+    }
 }
 
 void Stream::snapshot(Snapshot& s) {
     const int P = cfg.p, Q = cfg.q, R = cfg.rank;
-    const size_t q3 = (size_t)Q * Q * Q;
-    s.Y.reserve((size_t)P * q3);
-    OCTEN_CUDA(cudaMemcpyAsync(s.Y.p, Y.p, sizeof(double) * P * q3, cudaMemcpyDeviceToDevice, st));
+    const size_t ny = (size_t)std::max(pl, 1) * Q * Q * Q;
+    s.Y.reserve(ny);
+    OCTEN_CUDA(cudaMemcpyAsync(s.Y.p, Y.p, sizeof(double) * ny, cudaMemcpyDeviceToDevice, st));
     s.hist.reserve((size_t)P * Q * R);
     OCTEN_CUDA(cudaMemcpyAsync(s.hist.p, hist.p, sizeof(double) * P * Q * R, cudaMemcpyDeviceToDevice, st));
     s.A.reserve((size_t)I * R);
@@ -378,57 +512,21 @@ void Stream::restore(Snapshot& s) {
     log.resize(s.log_len);
 }
 
+void Stream::init(const void* data, int dtype, int location, int order, const std::int64_t* dims) {
+    xmodels.reserve(models_count() * shard_world);
+    xrows.reserve(rows_count() * shard_world);
+    begin(data, dtype, location, order, dims, xmodels.p);
+    merge_phase(xmodels.p, xrows.p);
+    finish(xrows.p);
+}
+
 void Stream::ingest(const void* data, int dtype, int location, int order, const std::int64_t* dims) {
-    // streaming.cpp:258-346
-    if (order != 3)
-        throw ConfigError("ingest_batch: batch order mismatch at batch " + std::to_string(batches_seen));
-    if (dims[0] != I)
-        throw ConfigError("ingest_batch: extent mismatch on mode 1 at batch " + std::to_string(batches_seen));
-    if (dims[1] != J)
-        throw ConfigError("ingest_batch: extent mismatch on mode 2 at batch " + std::to_string(batches_seen));
-    const std::int64_t t_new = dims[2];
-    if (t_new < 1) throw ConfigError("ingest_batch: batch has no temporal extent");
-    Snapshot backup;
-    if (cfg.strict) snapshot(backup);
-    const std::string context = "batch " + std::to_string(batches_seen) + ": ";
-    try {
-        const auto t_start = Clock::now();
-        BatchRecordC rec{};
-        rec.batch_index = batches_seen;
-        rec.t_new = t_new;
-        auto tc = Clock::now();
-        const size_t n = (size_t)I * J * t_new;
-        const void* dX = stage_input(data, dtype, location, n);
-        check_finite(dX, dtype, n);
-        extend_temporal(t_new);
-        OCTEN_CUDA(cudaEventRecord(evs[0], st));
-        compress_stage(dX, dtype, t_new);
-        OCTEN_CUDA(cudaEventRecord(evs[1], st));
-        OCTEN_CUDA(cudaStreamSynchronize(st));
-        rec.compress_seconds = seconds_since(tc);
-        auto ta = Clock::now();
-        OCTEN_CUDA(cudaEventRecord(evs[2], st));
-        als_stage(rec.batch_index);
-        OCTEN_CUDA(cudaEventRecord(evs[3], st));
-        rec.als_seconds = seconds_since(ta);
-        auto tr = Clock::now();
-        recover_stage(t_new, false, rec);
-        OCTEN_CUDA(cudaEventRecord(evs[4], st));
-        OCTEN_CUDA(cudaStreamSynchronize(st));
-        accumulate_stage_times();
-        rec.recover_seconds = seconds_since(tr);
-        rec.total_seconds = seconds_since(t_start);
-        log.push_back(rec);
-    } catch (const ConfigError& e) {
-        if (cfg.strict) restore(backup);
-        throw ConfigError(context + e.what());
-    } catch (const NumericError& e) {
-        if (cfg.strict) restore(backup);
-        throw NumericError(context + e.what());
-    } catch (...) {
-        if (cfg.strict) restore(backup);
-        throw;
-    }
+    if (shard_world != 1) throw ConfigError("octen: a sharded stream ingests through begin/merge/finish");
+    xmodels.reserve(models_count());
+    xrows.reserve(rows_count());
+    begin(data, dtype, location, order, dims, xmodels.p);
+    merge_phase(xmodels.p, xrows.p);
+    finish(xrows.p);
 }
 
 void Stream::accumulate_stage_times() {

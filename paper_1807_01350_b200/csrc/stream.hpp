@@ -5,7 +5,9 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "devbuf.hpp"
@@ -31,9 +33,21 @@ struct BatchRecordC {
     double compress_seconds, als_seconds, recover_seconds, total_seconds;
 };
 
+// One stream handle.  Unsharded (world == 1) it owns every replica.  As rank
+// g of a replica-sharded stream (one process per GPU) it owns replicas
+// [p0, p0 + pl), pl <= chunk = ceil(P / world): it compresses the batch into
+// and runs CP-ALS on those replicas only, and runs the alignment/merge
+// redundantly after two all-gathers the caller performs between the phases:
+//   begin  -> models_out  (models_count() doubles: status header, chunk x 3 x Q x R
+//                          factors, chunk x R lambdas)
+//   merge  <- models_all  (world blocks, rank order) -> rows_out (rows_count():
+//                          chunk x Q x R temporal-stack rows of the owned replicas)
+//   finish <- rows_all    (world blocks)
+// init_stream / ingest_batch (streaming.cpp:181-346) are the three phases
+// back to back with internal exchange buffers.
 class Stream {
 public:
-    explicit Stream(const StreamCfg& c);
+    Stream(const StreamCfg& c, int shard_rank = 0, int shard_world = 1);
     ~Stream();
     Stream(const Stream&) = delete;
     Stream& operator=(const Stream&) = delete;
@@ -42,7 +56,14 @@ public:
     void ingest(const void* data, int dtype, int location, int order, const std::int64_t* dims);
     void get_factor(int mode, double* out);
 
+    void begin(const void* data, int dtype, int location, int order, const std::int64_t* dims, double* models_out);
+    void merge_phase(const double* models_all, double* rows_out);
+    void finish(const double* rows_all);
+    size_t models_count() const { return 4 + (size_t)chunk * (3 * (size_t)cfg.q * cfg.rank + cfg.rank); }
+    size_t rows_count() const { return (size_t)chunk * cfg.q * cfg.rank; }
+
     StreamCfg cfg;
+    int shard_rank = 0, shard_world = 1, p0 = 0, pl = 0, chunk = 0;
     cudaStream_t st = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::int64_t I = 0, J = 0, K = 0, capC = 0;
@@ -52,7 +73,9 @@ public:
     CompressEngine comp;
     AlsEngine als;
     MergeEngine merge;
+    // Y: pl x Q^3 (owned replicas); hist: P*Q x R (all replicas, kept redundantly)
     DevBuf<double> Y, hist, A, B, C, lam, dW, Anew, Bnew, rows, X64;
+    DevBuf<double> xmodels, xrows, MfAll, MlamAll, tstackAll;
     DevBuf<float> X32;
     DevBuf<int> flag;
     std::vector<BatchRecordC> log;
@@ -63,6 +86,7 @@ public:
     cudaEvent_t evs[6] = {};
 
 private:
+    using Clock = std::chrono::steady_clock;
     struct Snapshot {
         DevBuf<double> Y, hist, A, B, C, lam;
         std::int64_t capC = 0, K = 0, batches_seen = 0, batches_drawn = 0;
@@ -70,17 +94,24 @@ private:
         size_t log_len = 0;
     };
     void validate(int order);
+    void prepare(int order, const std::int64_t* dims);
     void gen_replicas();
     void extend_temporal(std::int64_t t_new);
     const void* stage_input(const void* data, int dtype, int location, size_t n);
     void check_finite(const void* dX, int dtype, size_t n);
-    void compress_stage(const void* dX, int dtype, std::int64_t t);
-    void als_stage(std::int64_t batch_index);
-    void recover_stage(std::int64_t t_new, bool first, BatchRecordC& rec);
     void ensure_c_capacity(std::int64_t rows);
     void accumulate_stage_times();
     void snapshot(Snapshot& s);
     void restore(Snapshot& s);
+    [[noreturn]] void fail_pending();
+
+    // the batch between begin and finish
+    bool pending = false, pending_first = false;
+    std::int64_t pending_t = 0;
+    BatchRecordC prec{};
+    Clock::time_point t_start, t_recover;
+    Snapshot backup;
+    std::string context;
 };
 
 }  // namespace octen

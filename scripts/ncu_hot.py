@@ -1,0 +1,20 @@
+"""Top SASS lines by warp-stall samples from an ncu report (source page).
+usage: python scripts/ncu_hot.py REPORT.ncu-rep [N]"""
+import csv
+import io
+import subprocess
+import sys
+
+rep = sys.argv[1]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+lines = out.splitlines()
+start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
+rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+tot = sum(int(r["Warp Stall Sampling (All Samples)"] or 0) for r in rows)
+print("total samples", tot, "instructions", len(rows))
+rows.sort(key=lambda r: -int(r["Warp Stall Sampling (All Samples)"] or 0))
+for r in rows[:n]:
+    s = int(r["Warp Stall Sampling (All Samples)"] or 0)
+    print("%6d %5.1f%%  %s  %s" % (s, 100.0 * s / max(tot, 1), r["Address"][-5:], r["Source"].strip()[:90]))
