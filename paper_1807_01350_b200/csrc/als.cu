@@ -515,16 +515,11 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     }
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
-    if (threadIdx.x < 32) {
-        TeamWarp w;
-        int rk;
-        if (R <= 32) {
-            const double md = warp_max_diag(Lf, R, R);
-            rk = warp_chol_inv32(Lf, R, R, md > 0.0 ? kEps * R * md : INFINITY, Ev, R);  // Ev = L^-1
-        } else {
-            rk = team_chol_semidef(w, R, Lf, R, kEps * R, cs, iw);
-            if (rk == R) team_tri_inv_lower(w, R, Lf, R, Ev, R);
-        }
+    {
+        // Lf = chol(V), Ev = Lf^-1, block-cooperative (R <= 64)
+        double md = 0.0;
+        for (int i = 0; i < R; ++i) md = fmax(md, V[i + R * i]);
+        const int rk = block_chol_inv64(V, R, R, md > 0.0 ? kEps * R * md : INFINITY, Lf, R, Ev, R, red);
         if (threadIdx.x == 0) rank = rk;
     }
     __syncthreads();

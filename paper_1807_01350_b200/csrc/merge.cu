@@ -270,10 +270,12 @@ __global__ void align_match_kernel(AlignDev a) {
             __syncthreads();
         }
     }
+    {
+        __shared__ double gscr[96];
+        const int amb = block_greedy_match(R, sim, R, 1e-9, perm, ru, cu, gscr);
+        if (threadIdx.x == 0) a.ambig[p] = amb;
+    }
     if (threadIdx.x == 0) {
-        unsigned char* ru_ = ru;
-        unsigned char* cu_ = cu;
-        a.ambig[p] = greedy_match(R, sim, R, 1e-9, perm, ru_, cu_);
         double mn = 1.0, mx = 0.0;
         for (int i = 0; i < R; ++i) {
             mn = fmin(mn, sim[i + R * perm[i]]);
@@ -538,8 +540,10 @@ __global__ void match_select_kernel(int R, const double* dots, const double* nc,
         sim[e] = s;
     }
     __syncthreads();
-    if (threadIdx.x == 0) greedy_match(R, sim, R, 1e-9, perm, ru, cu);
-    __syncthreads();
+    {
+        __shared__ double gscr[96];
+        block_greedy_match(R, sim, R, 1e-9, perm, ru, cu, gscr);
+    }
     for (int e = threadIdx.x; e < 2 * R; e += blockDim.x) {
         const int n = e / R, i = e % R, j = perm[i];
         signs_out[(size_t)n * R + i] = dots[(size_t)n * R * R + i + (size_t)R * j] < 0.0 ? -1.0 : 1.0;

@@ -291,6 +291,184 @@ __device__ inline int warp_chol_inv32(double* s, int lds, int n, double thr, dou
 #endif
 
 #if defined(__CUDACC__)
+// ---------------------------------------------------------------------------
+// greedy_match (above) with the whole block: per step one max-reduction for
+// the best free similarity, then one combined reduction for the
+// lexicographically first free pair within tie_tol of it (lowest ref, then
+// lowest candidate) and the number of such pairs.  Same result as the serial
+// routine, R steps of O(R^2 / blockDim) work.  blockDim.x % 32 == 0, r <= 64.
+// scratch: 3 * 32 doubles.  Returns the ambiguity count (all threads).
+// ---------------------------------------------------------------------------
+__device__ inline int block_greedy_match(int r, const double* sim, int ld, double tie_tol, int* perm,
+                                         unsigned char* ref_used, unsigned char* cand_used, double* scratch) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    double* rmax = scratch;        // per-warp max
+    double* rkey = scratch + 32;   // per-warp min key
+    double* rcnt = scratch + 64;   // per-warp tie count
+    for (int i = tid; i < r; i += blockDim.x) {
+        perm[i] = -1;
+        ref_used[i] = 0;
+        cand_used[i] = 0;
+    }
+    __syncthreads();
+    int ambiguous = 0;
+    const int rr = r * r;
+    for (int step = 0; step < r; ++step) {
+        double best = -INFINITY;
+        int firstfree = 0x7fffffff;
+        for (int e = tid; e < rr; e += blockDim.x) {
+            const int i = e / r, j = e % r;  // key order: ref-major
+            if (ref_used[i] || cand_used[j]) continue;
+            const double v = sim[i + (size_t)ld * j];
+            best = v > best ? v : best;
+            firstfree = min(firstfree, e);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+            firstfree = min(firstfree, __shfl_xor_sync(0xffffffffu, firstfree, o));
+        }
+        if (lane == 0) {
+            rmax[wid] = best;
+            rkey[wid] = (double)firstfree;
+        }
+        __syncthreads();
+        best = -INFINITY;
+        double ff = 2147483647.0;
+        for (int w = 0; w < nw; ++w) {
+            best = fmax(best, rmax[w]);
+            ff = fmin(ff, rkey[w]);
+        }
+        __syncthreads();
+        int key = 0x7fffffff, cnt = 0;
+        for (int e = tid; e < rr; e += blockDim.x) {
+            const int i = e / r, j = e % r;
+            if (ref_used[i] || cand_used[j]) continue;
+            if (sim[i + (size_t)ld * j] >= best - tie_tol) {
+                key = min(key, e);
+                ++cnt;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        }
+        if (lane == 0) {
+            rkey[wid] = (double)key;
+            rcnt[wid] = (double)cnt;
+        }
+        __syncthreads();
+        double kk = 2147483647.0, cc = 0.0;
+        for (int w = 0; w < nw; ++w) {
+            kk = fmin(kk, rkey[w]);
+            cc += rcnt[w];
+        }
+        if (cc > 1.0) ++ambiguous;
+        // NaN similarities: no pair qualifies -> the first free pair
+        const int pick = (kk < 2147483647.0) ? (int)kk : (int)ff;
+        __syncthreads();
+        if (tid == 0) {
+            const int bi = pick / r, bj = pick % r;
+            perm[bi] = bj;
+            ref_used[bi] = 1;
+            cand_used[bj] = 1;
+        }
+        __syncthreads();
+    }
+    return ambiguous;
+}
+#endif
+
+#if defined(__CUDACC__)
+// ---------------------------------------------------------------------------
+// Block-cooperative semi-definite Cholesky with the inverse of the factor,
+// n <= 64, blockDim.x == 256.  Every thread keeps a fixed share of the packed
+// lower triangle of A (-> L) and of B (I -> L^-1) in registers; step k
+// publishes column k of L and row k of L^-1 through shared memory and all
+// threads apply the rank-1 updates to their own elements (two barriers per
+// step, no serial warp).  A pivot <= thr is dead: column k of L and row k of
+// L^-1 become zero.  a (ld lda) is read only; l (ld ldl, lower; upper zeroed)
+// and x (ld ldx, lower; upper zeroed) are written.  scratch: 2 * 64 + 2
+// doubles of shared memory.  Returns the rank (all threads).
+// ---------------------------------------------------------------------------
+__device__ inline int block_chol_inv64(const double* a, int lda, int n, double thr, double* l, int ldl, double* x,
+                                       int ldx, double* scratch) {
+    constexpr int kPer = 9;  // ceil(64 * 65 / 2 / 256)
+    double* colk = scratch;
+    double* rowk = scratch + 64;
+    double* shv = scratch + 128;  // [0] reciprocal pivot, [1] dead count
+    const int tid = threadIdx.x;
+    double av[kPer], bv[kPer];
+    int iv[kPer], jv[kPer];
+    if (tid == 0) shv[1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < kPer; ++s) {
+        const int e = tid + 256 * s;
+        int i = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+        while ((i + 1) * (i + 2) / 2 <= e) ++i;
+        while (i * (i + 1) / 2 > e) --i;
+        const int j = e - i * (i + 1) / 2;
+        const bool ok = i < n;
+        iv[s] = ok ? i : 64;
+        jv[s] = ok ? j : 64;
+        av[s] = ok ? a[i + (size_t)lda * j] : 0.0;
+        bv[s] = (ok && i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+#pragma unroll
+        for (int s = 0; s < kPer; ++s)
+            if (iv[s] == k && jv[s] == k) {
+                const double d = av[s];
+                const bool dead = !(d > thr);
+                const double piv = dead ? 0.0 : sqrt(d);
+                av[s] = piv;
+                shv[0] = dead ? 0.0 : 1.0 / piv;
+                if (dead) shv[1] += 1.0;
+            }
+        __syncthreads();
+        const double rp = shv[0];
+#pragma unroll
+        for (int s = 0; s < kPer; ++s) {
+            if (jv[s] == k && iv[s] > k && iv[s] < 64) {
+                av[s] *= rp;
+                colk[iv[s]] = av[s];
+            }
+            if (iv[s] == k) {
+                bv[s] *= rp;
+                rowk[jv[s]] = bv[s];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < kPer; ++s) {
+            const int i = iv[s], j = jv[s];
+            if (i < 64 && i > k) {
+                if (j > k)
+                    av[s] -= colk[i] * colk[j];
+                else
+                    bv[s] -= colk[i] * rowk[j];
+            }
+        }
+    }
+    for (int e = tid; e < n * n; e += 256) {
+        const int i = e % n, j = e / n;
+        if (i < j) {
+            l[i + (size_t)ldl * j] = 0.0;
+            x[i + (size_t)ldx * j] = 0.0;
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < kPer; ++s)
+        if (iv[s] < 64) {
+            l[iv[s] + (size_t)ldl * jv[s]] = av[s];
+            x[iv[s] + (size_t)ldx * jv[s]] = bv[s];
+        }
+    __syncthreads();
+    return n - (int)shv[1];
+}
+#endif
+
+#if defined(__CUDACC__)
 // max of the diagonal of an n x n matrix, reduced over one warp (all lanes get it)
 __device__ inline double warp_max_diag(const double* a, int lda, int n) {
     double m = 0.0;

@@ -14,11 +14,13 @@ if [ -n "$LAUNCHES" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $LCMD > gpurun_out/${TAG}_ncu.log 2>&1
   echo "ncu rc=$?"
 fi
-# FULLK="k1 k2 ...": one `ncu --set full` capture (first launch) per kernel name
+# FULLK="k1 k2:skip ...": one `ncu --set full` capture per kernel name
+# (after skipping `skip` launches of it)
 if [ -n "$FULLK" ]; then
   LCMD="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline"
-  for k in $FULLK; do
-    timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 \
+  for ks in $FULLK; do
+    k=${ks%%:*}; sk=0; [ "$k" != "$ks" ] && sk=${ks##*:}
+    timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s $sk -c 1 \
       -f -o gpurun_out/${TAG}_full_$k $LCMD > gpurun_out/${TAG}_full_$k.log 2>&1
     echo "ncu full $k rc=$?"
   done
