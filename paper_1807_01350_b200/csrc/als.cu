@@ -191,26 +191,36 @@ __global__ void gevd_pencil_kernel(AlsDev d) {
     double* wr = m_v + R * R;
     double* wi = wr + R;
     double* ort = wi + R;
-    int* rowp = (int*)(ort + R);  // 2R ints = R doubles; total 4R^2 + 4R of the 6R^2 + 4R scratch
+    int* rowp = (int*)(ort + R);  // 2R ints = R doubles
     int* colp = rowp + R;
+    double* piv = ort + 2 * R;    // R
+    double* wscr = piv + R;       // 64 (team argmax scratch)
     const double* ur = d.Ur + ((size_t)p * 2 + 0) * Q * R;
     double* a1 = d.f(prob, 0);
     if (threadIdx.x == 0) att = -1;
     __syncthreads();
     for (int a = d.att_start[prob]; a < 3; ++a) {
-        if (threadIdx.x == 0) {
-            ok = 0;
-            const double* p1 = d.Pm + (((size_t)prob * 6) + a * 2 + 0) * R * R;
-            const double* p2 = d.Pm + (((size_t)prob * 6) + a * 2 + 1) * R * R;
-            for (int i = 0; i < R * R; ++i) m_h[i] = p2[i];
-            if (lu_fullpiv_inverse(R, m_h, R, m_inv, R, rowp, colp)) {
-                for (int j = 0; j < R; ++j)
-                    for (int i = 0; i < R; ++i) {
-                        double s = 0.0;
-                        for (int k = 0; k < R; ++k) s += p1[i + R * k] * m_inv[k + R * j];
-                        m_pen[i + R * j] = s;
-                    }
-                if (eig_real(R, m_pen, m_v, wr, wi, ort)) {
+        const double* p1 = d.Pm + (((size_t)prob * 6) + a * 2 + 0) * R * R;
+        const double* p2 = d.Pm + (((size_t)prob * 6) + a * 2 + 1) * R * R;
+        if (threadIdx.x < 32) {
+            // one warp: FullPivLU of p2 (cp_als.cpp:122-124), pencil p1 p2^-1,
+            // real Schur form + eigenvectors (cp_als.cpp:126-140)
+            TeamWarp w;
+            for (int i = w.tid(); i < R * R; i += 32) m_h[i] = p2[i];
+            __syncwarp();
+            bool good = lu_fullpiv_inverse_team(w, R, m_h, R, m_inv, R, rowp, colp, piv, wscr);
+            if (good) {
+                for (int e = w.tid(); e < R * R; e += 32) {
+                    const int i = e % R, j = e / R;
+                    double s = 0.0;
+                    for (int k = 0; k < R; ++k) s += p1[i + R * k] * m_inv[k + R * j];
+                    m_pen[e] = s;
+                }
+                __syncwarp();
+                good = eig_real_team(w, R, m_pen, m_v, wr, wi, ort);
+            }
+            if (good) {
+                if (w.tid() == 0) {
                     int c = 0;
                     while (c < R) {
                         if (fabs(wi[c]) > 1e-9 * fabs(wr[c]) && c + 1 < R) {
@@ -220,16 +230,14 @@ __global__ void gevd_pencil_kernel(AlsDev d) {
                             }
                             c += 2;
                         } else {
-                            // real part of eigenvector c; for the second member of a
-                            // conjugate pair (wi < 0) that is column c-1 of the hqr2 layout
                             const int src = (wi[c] < 0.0 && c > 0) ? c - 1 : c;
                             for (int i = 0; i < R; ++i) asub[i + R * c] = m_v[i + R * src];
                             c += 1;
                         }
                     }
-                    ok = 1;
                 }
             }
+            if (w.tid() == 0) ok = good ? 1 : 0;
         }
         __syncthreads();
         if (!ok) continue;
@@ -1007,7 +1015,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             att_start.upload(start.data(), NP, st);
             todo.upload(td.data(), NP, st);
             peel_fail.zero(NP, st);
-            const size_t smem_pen = (size_t)(5 * R * R + 5 * R + 8) * sizeof(double);
+            const size_t smem_pen = (size_t)(5 * R * R + 7 * R + 72) * sizeof(double);
             gevd_pencil_kernel<<<NP, 128, smem_pen, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
             gemm_f64<false, false>(NP, R, (int)q2, Q, A1tA{F.p, Q, R}, Y0Bp{dY, q3, Q, S},

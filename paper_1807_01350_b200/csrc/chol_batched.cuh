@@ -52,19 +52,31 @@ __global__ void chol_maxdiag_kernel(const double* A, int n, int lda, long long s
 // so one step costs two barriers and ~9 FMAs per thread.  A pivot
 // <= tol * maxdiag is dead: its column of L and row of L^-1 become zero and
 // the rank is decremented.
-constexpr int kDiagThreads = 256;
-constexpr int kDiagPer = (kCholNB * (kCholNB + 1) / 2 + kDiagThreads - 1) / kDiagThreads;  // 9
+constexpr int kDiagThreads = 512;
+constexpr int kDiagPer = (kCholNB * (kCholNB + 1) / 2 + kDiagThreads - 1) / kDiagThreads;  // 5
 
+// Branch-free form of the updates: colk[i] is zero for i <= k and rowk[j] is
+// zero for j > k (both start zeroed; step k zeroes colk[k] and writes rowk
+// only up to k), so every owned element applies
+//   A(i,j) -= colk[i] colk[j];  B(i,j) -= colk[i] rowk[j]
+// unconditionally and the products vanish outside the trailing / forward
+// ranges.  Unused slots point at row/column 64 (zero entries).
 __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int n, int lda, long long sA, int k0,
                                                                  double tol, const double* maxdiag, int* rank,
                                                                  double* Linv, int nblk) {
-    __shared__ double colk[kCholNB], rowk[kCholNB];
+    __shared__ double colk[kCholNB + 1], rowk[kCholNB + 1];
     __shared__ double sh_rp;
+    __shared__ int sh_dead;
     double* a = A + (size_t)blockIdx.x * sA;
     const int nb = min(kCholNB, n - k0);
     const int tid = threadIdx.x;
     double av[kDiagPer], bv[kDiagPer];
     int iv[kDiagPer], jv[kDiagPer];
+    if (tid <= kCholNB) {
+        colk[tid] = 0.0;
+        rowk[tid] = 0.0;
+    }
+    if (tid == 0) sh_dead = 0;
 #pragma unroll
     for (int s = 0; s < kDiagPer; ++s) {
         // packed lower-triangle index e -> (i, j), j <= i (row-major packing)
@@ -74,52 +86,55 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
         while (i * (i + 1) / 2 > e) --i;
         const int j = e - i * (i + 1) / 2;
         const bool ok = e < kCholNB * (kCholNB + 1) / 2 && i < nb;
-        iv[s] = ok ? i : kCholNB;  // kCholNB marks an unused slot
+        iv[s] = ok ? i : kCholNB;
         jv[s] = ok ? j : kCholNB;
         av[s] = ok ? a[(k0 + i) + (size_t)lda * (k0 + j)] : 0.0;
         bv[s] = (ok && i == j) ? 1.0 : 0.0;
     }
     const double md = maxdiag[blockIdx.x];
     const double thr = (md > 0.0) ? tol * md : INFINITY;
+    // owner of the diagonal element (k, k): packed index k(k+3)/2
+    __syncthreads();
     for (int k = 0; k < nb; ++k) {
-        // pivot (owner of (k, k))
+        const int ed = k * (k + 3) / 2;
+        if (tid == ed % kDiagThreads) {
+            const int sd = ed / kDiagThreads;
 #pragma unroll
-        for (int s = 0; s < kDiagPer; ++s)
-            if (iv[s] == k && jv[s] == k) {
-                const double d = av[s];
-                const bool dead = !(d > thr);
-                const double piv = dead ? 0.0 : sqrt(d);
-                av[s] = piv;
-                sh_rp = dead ? 0.0 : 1.0 / piv;
-                if (dead) atomicSub(&rank[blockIdx.x], 1);
-            }
-        __syncthreads();
-        const double rp = sh_rp;
-        // column k of L, row k of L^-1
-#pragma unroll
-        for (int s = 0; s < kDiagPer; ++s) {
-            if (jv[s] == k && iv[s] > k && iv[s] < kCholNB) {
-                av[s] *= rp;
-                colk[iv[s]] = av[s];
-            }
-            if (iv[s] == k) {
-                bv[s] *= rp;
-                rowk[jv[s]] = bv[s];
-            }
+            for (int s = 0; s < kDiagPer; ++s)
+                if (s == sd) {
+                    const double d = av[s];
+                    const bool dead = !(d > thr);
+                    const double piv = dead ? 0.0 : sqrt(d);
+                    av[s] = piv;
+                    sh_rp = dead ? 0.0 : 1.0 / piv;
+                    if (dead) ++sh_dead;
+                }
         }
         __syncthreads();
+        const double rp = sh_rp;
 #pragma unroll
         for (int s = 0; s < kDiagPer; ++s) {
             const int i = iv[s], j = jv[s];
-            if (i < kCholNB && i > k) {
-                if (j > k)
-                    av[s] -= colk[i] * colk[j];
-                else
-                    bv[s] -= colk[i] * rowk[j];
+            if (j == k && i > k) {  // column k of L (i < 64 for used slots)
+                av[s] *= rp;
+                colk[i] = av[s];
             }
+            if (i == k) {  // row k of L^-1
+                bv[s] *= rp;
+                rowk[j] = bv[s];
+            }
+        }
+        if (tid == 0) colk[k] = 0.0;
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < kDiagPer; ++s) {
+            const double ci = colk[iv[s]];
+            av[s] -= ci * colk[jv[s]];
+            bv[s] -= ci * rowk[jv[s]];
         }
         // the next step's first barrier orders these reads before colk/rowk are rewritten
     }
+    if (tid == 0 && sh_dead) atomicSub(&rank[blockIdx.x], sh_dead);
     double* inv = Linv + ((size_t)blockIdx.x * nblk + k0 / kCholNB) * kCholNB * kCholNB;
     for (int e = tid; e < kCholNB * kCholNB; e += kDiagThreads) {
         const int i = e % kCholNB, j = e / kCholNB;

@@ -946,6 +946,544 @@ OCTEN_HD inline bool eig_real(int nn, double* hm, double* vm, double* wr, double
 }
 
 // ---------------------------------------------------------------------------
+// Team-parallel twins of lu_fullpiv_inverse and eig_real (same arithmetic per
+// element, same pivot/shift/deflation decisions): the O(n) inner loops of
+// every O(n) step -- pivot search, row/column swaps and eliminations, the
+// Householder applications of orthes, the row/column/vector updates of each
+// Francis double-shift step, the eigenvector back-transformation -- are split
+// over the team; the scalar control flow runs redundantly in every thread
+// from shared values and every scalar store is done by thread 0 between
+// barriers.  Used by one warp per GEVD problem (TeamWarp); the host harness
+// instantiates them with TeamHost.  scratch: 2 * team.size() doubles.
+// ---------------------------------------------------------------------------
+template <class Team>
+OCTEN_HD void team_argmax_first(const Team& team, double& v, int& key, double* scratch) {
+    // max v; ties -> smallest key.  All threads receive the winner.
+#if defined(__CUDA_ARCH__)
+    if (team.size() == 32) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int ok = __shfl_xor_sync(0xffffffffu, key, o);
+            if (ov > v || (ov == v && ok < key)) {
+                v = ov;
+                key = ok;
+            }
+        }
+        return;
+    }
+#endif
+    scratch[2 * team.tid()] = v;
+    scratch[2 * team.tid() + 1] = (double)key;
+    team.sync();
+    double bv = scratch[0];
+    int bk = (int)scratch[1];
+    for (int t = 1; t < team.size(); ++t) {
+        const double ov = scratch[2 * t];
+        const int ok = (int)scratch[2 * t + 1];
+        if (ov > bv || (ov == bv && ok < bk)) {
+            bv = ov;
+            bk = ok;
+        }
+    }
+    team.sync();
+    v = bv;
+    key = bk;
+}
+
+template <class Team>
+OCTEN_HD bool lu_fullpiv_inverse_team(const Team& team, int n, double* a, int lda, double* inv, int ldi,
+                                      int* rowp, int* colp, double* piv_abs, double* scratch) {
+    const int T = team.tid(), NT = team.size();
+    double maxpiv = 0.0;
+    for (int k = 0; k < n; ++k) {
+        // first maximum in column-major scan order (as the serial routine)
+        const int m = n - k;
+        double best = -1.0;
+        int bkey = 0x7fffffff;
+        for (int e = T; e < m * m; e += NT) {
+            const int i = k + e % m, j = k + e / m;
+            const double v = fabs(a[i + (size_t)lda * j]);
+            if (v > best) {
+                best = v;
+                bkey = e;
+            }
+        }
+        team_argmax_first(team, best, bkey, scratch);
+        const int bi = k + bkey % m, bj = k + bkey / m;
+        if (T == 0) {
+            rowp[k] = bi;
+            colp[k] = bj;
+        }
+        if (bi != k)
+            for (int j = T; j < n; j += NT) {
+                const double t = a[k + (size_t)lda * j];
+                a[k + (size_t)lda * j] = a[bi + (size_t)lda * j];
+                a[bi + (size_t)lda * j] = t;
+            }
+        team.sync();
+        if (bj != k)
+            for (int i = T; i < n; i += NT) {
+                const double t = a[i + (size_t)lda * k];
+                a[i + (size_t)lda * k] = a[i + (size_t)lda * bj];
+                a[i + (size_t)lda * bj] = t;
+            }
+        team.sync();
+        const double p = a[k + (size_t)lda * k];
+        if (T == 0) piv_abs[k] = fabs(p);
+        if (fabs(p) > maxpiv) maxpiv = fabs(p);
+        if (p != 0.0) {
+            for (int i = k + 1 + T; i < n; i += NT) a[i + (size_t)lda * k] /= p;
+            team.sync();
+            const int mm = n - k - 1;
+            for (int e = T; e < mm * mm; e += NT) {
+                const int i = k + 1 + e % mm, j = k + 1 + e / mm;
+                a[i + (size_t)lda * j] -= a[i + (size_t)lda * k] * a[k + (size_t)lda * j];
+            }
+        }
+        team.sync();
+    }
+    const double thr = 2.220446049250313e-16 * (double)n * maxpiv;
+    int rank = 0;
+    for (int k = 0; k < n; ++k)
+        if (piv_abs[k] > thr) ++rank;
+    if (rank < n) return false;
+    for (int c = T; c < n; c += NT) {
+        double* x = inv + (size_t)ldi * c;
+        for (int i = 0; i < n; ++i) x[i] = (i == c) ? 1.0 : 0.0;
+        for (int k = 0; k < n; ++k)
+            if (rowp[k] != k) {
+                const double t = x[k];
+                x[k] = x[rowp[k]];
+                x[rowp[k]] = t;
+            }
+        for (int i = 0; i < n; ++i)
+            for (int p = 0; p < i; ++p) x[i] -= a[i + (size_t)lda * p] * x[p];
+        for (int i = n - 1; i >= 0; --i) {
+            for (int p = i + 1; p < n; ++p) x[i] -= a[i + (size_t)lda * p] * x[p];
+            x[i] /= a[i + (size_t)lda * i];
+        }
+        for (int k = n - 1; k >= 0; --k)
+            if (colp[k] != k) {
+                const double t = x[k];
+                x[k] = x[colp[k]];
+                x[colp[k]] = t;
+            }
+    }
+    team.sync();
+    return true;
+}
+
+template <class Team>
+OCTEN_HD bool eig_real_team(const Team& team, int nn, double* hm, double* vm, double* wr, double* wi, double* ort) {
+#define H_(i, j) hm[(i) + (size_t)nn * (j)]
+#define V_(i, j) vm[(i) + (size_t)nn * (j)]
+    const int T = team.tid(), NT = team.size();
+    const bool lead = (T == 0);
+    const int low = 0, high = nn - 1;
+    // --- orthes ---
+    for (int m = low + 1; m <= high - 1; ++m) {
+        double scale = 0.0;
+        for (int i = m; i <= high; ++i) scale += fabs(H_(i, m - 1));
+        if (scale != 0.0) {
+            double h = 0.0;
+            for (int i = high; i >= m; --i) {
+                const double o = H_(i, m - 1) / scale;
+                h += o * o;
+            }
+            double g = sqrt(h);
+            const double om = H_(m, m - 1) / scale;
+            if (om > 0) g = -g;
+            h = h - om * g;
+            for (int i = m + T; i <= high; i += NT) ort[i] = (i == m) ? om - g : H_(i, m - 1) / scale;
+            team.sync();
+            for (int j = m + T; j < nn; j += NT) {
+                double f = 0.0;
+                for (int i = high; i >= m; --i) f += ort[i] * H_(i, j);
+                f = f / h;
+                for (int i = m; i <= high; ++i) H_(i, j) -= f * ort[i];
+            }
+            team.sync();
+            for (int i = T; i <= high; i += NT) {
+                double f = 0.0;
+                for (int j = high; j >= m; --j) f += ort[j] * H_(i, j);
+                f = f / h;
+                for (int j = m; j <= high; ++j) H_(i, j) -= f * ort[j];
+            }
+            team.sync();
+            if (lead) {
+                ort[m] = scale * ort[m];
+                H_(m, m - 1) = scale * g;
+            }
+            team.sync();
+        }
+    }
+    for (int e = T; e < nn * nn; e += NT) vm[e] = ((e % nn) == (e / nn)) ? 1.0 : 0.0;
+    team.sync();
+    for (int m = high - 1; m >= low + 1; --m) {
+        if (H_(m, m - 1) != 0.0) {
+            for (int i = m + 1 + T; i <= high; i += NT) ort[i] = H_(i, m - 1);
+            team.sync();
+            for (int j = m + T; j <= high; j += NT) {
+                double g = 0.0;
+                for (int i = m; i <= high; ++i) g += ort[i] * V_(i, j);
+                g = (g / ort[m]) / H_(m, m - 1);
+                for (int i = m; i <= high; ++i) V_(i, j) += g * ort[i];
+            }
+            team.sync();
+        }
+    }
+    // --- hqr2 ---
+    int n = nn - 1;
+    const double eps = 2.220446049250313e-16;
+    double exshift = 0.0, p = 0, q = 0, r = 0, s = 0, z = 0, t, w, x, y;
+    double norm = 0.0;
+    for (int i = 0; i < nn; ++i)
+        for (int j = (i - 1 > 0 ? i - 1 : 0); j < nn; ++j) norm += fabs(H_(i, j));
+    int iter = 0, total_iter = 0;
+    const int max_total = 40 * nn;
+    while (n >= low) {
+        int l = n;
+        while (l > low) {
+            s = fabs(H_(l - 1, l - 1)) + fabs(H_(l, l));
+            if (s == 0.0) s = norm;
+            if (fabs(H_(l, l - 1)) < eps * s) break;
+            l--;
+        }
+        if (l == n) {
+            const double hv = H_(n, n) + exshift;
+            team.sync();
+            if (lead) {
+                H_(n, n) = hv;
+                wr[n] = hv;
+                wi[n] = 0.0;
+            }
+            team.sync();
+            n--;
+            iter = 0;
+        } else if (l == n - 1) {
+            w = H_(n, n - 1) * H_(n - 1, n);
+            p = (H_(n - 1, n - 1) - H_(n, n)) / 2.0;
+            q = p * p + w;
+            z = sqrt(fabs(q));
+            const double hnn = H_(n, n) + exshift, hmm = H_(n - 1, n - 1) + exshift;
+            const double hsub = H_(n, n - 1);
+            x = hnn;
+            team.sync();
+            if (lead) {
+                H_(n, n) = hnn;
+                H_(n - 1, n - 1) = hmm;
+            }
+            if (q >= 0) {
+                z = (p >= 0) ? p + z : p - z;
+                const double wa = x + z;
+                const double wb = (z != 0.0) ? x - w / z : wa;
+                if (lead) {
+                    wr[n - 1] = wa;
+                    wr[n] = wb;
+                    wi[n - 1] = 0.0;
+                    wi[n] = 0.0;
+                }
+                x = hsub;
+                s = fabs(x) + fabs(z);
+                p = x / s;
+                q = z / s;
+                r = sqrt(p * p + q * q);
+                p = p / r;
+                q = q / r;
+                team.sync();
+                for (int j = n - 1 + T; j < nn; j += NT) {
+                    const double zz = H_(n - 1, j);
+                    H_(n - 1, j) = q * zz + p * H_(n, j);
+                    H_(n, j) = q * H_(n, j) - p * zz;
+                }
+                team.sync();
+                for (int i = T; i <= n; i += NT) {
+                    const double zz = H_(i, n - 1);
+                    H_(i, n - 1) = q * zz + p * H_(i, n);
+                    H_(i, n) = q * H_(i, n) - p * zz;
+                }
+                for (int i = low + T; i <= high; i += NT) {
+                    const double zz = V_(i, n - 1);
+                    V_(i, n - 1) = q * zz + p * V_(i, n);
+                    V_(i, n) = q * V_(i, n) - p * zz;
+                }
+            } else {
+                if (lead) {
+                    wr[n - 1] = x + p;
+                    wr[n] = x + p;
+                    wi[n - 1] = z;
+                    wi[n] = -z;
+                }
+            }
+            team.sync();
+            n = n - 2;
+            iter = 0;
+        } else {
+            x = H_(n, n);
+            y = 0.0;
+            w = 0.0;
+            if (l < n) {
+                y = H_(n - 1, n - 1);
+                w = H_(n, n - 1) * H_(n - 1, n);
+            }
+            if (iter == 10) {
+                exshift += x;
+                team.sync();
+                for (int i = low + T; i <= n; i += NT) H_(i, i) -= x;
+                team.sync();
+                s = fabs(H_(n, n - 1)) + fabs(H_(n - 1, n - 2));
+                x = y = 0.75 * s;
+                w = -0.4375 * s * s;
+            }
+            if (iter == 30) {
+                s = (y - x) / 2.0;
+                s = s * s + w;
+                if (s > 0) {
+                    s = sqrt(s);
+                    if (y < x) s = -s;
+                    s = x - w / ((y - x) / 2.0 + s);
+                    team.sync();
+                    for (int i = low + T; i <= n; i += NT) H_(i, i) -= s;
+                    team.sync();
+                    exshift += s;
+                    x = y = w = 0.964;
+                }
+            }
+            iter = iter + 1;
+            if (++total_iter > max_total) return false;
+            int m = n - 2;
+            while (m >= l) {
+                z = H_(m, m);
+                r = x - z;
+                s = y - z;
+                p = (r * s - w) / H_(m + 1, m) + H_(m, m + 1);
+                q = H_(m + 1, m + 1) - z - r - s;
+                r = H_(m + 2, m + 1);
+                s = fabs(p) + fabs(q) + fabs(r);
+                p = p / s;
+                q = q / s;
+                r = r / s;
+                if (m == l) break;
+                if (fabs(H_(m, m - 1)) * (fabs(q) + fabs(r)) <
+                    eps * (fabs(p) * (fabs(H_(m - 1, m - 1)) + fabs(z) + fabs(H_(m + 1, m + 1)))))
+                    break;
+                m--;
+            }
+            team.sync();
+            for (int i = m + 2 + T; i <= n; i += NT) {
+                H_(i, i - 2) = 0.0;
+                if (i > m + 2) H_(i, i - 3) = 0.0;
+            }
+            team.sync();
+            for (int k = m; k <= n - 1; ++k) {
+                const bool notlast = (k != n - 1);
+                if (k != m) {
+                    p = H_(k, k - 1);
+                    q = H_(k + 1, k - 1);
+                    r = notlast ? H_(k + 2, k - 1) : 0.0;
+                    x = fabs(p) + fabs(q) + fabs(r);
+                    if (x == 0.0) continue;
+                    p = p / x;
+                    q = q / x;
+                    r = r / x;
+                }
+                s = sqrt(p * p + q * q + r * r);
+                if (p < 0) s = -s;
+                if (s != 0) {
+                    double hk = 0.0;
+                    bool store = false;
+                    if (k != m) {
+                        hk = -s * x;
+                        store = true;
+                    } else if (l != m) {
+                        hk = -H_(k, k - 1);
+                        store = true;
+                    }
+                    team.sync();
+                    if (lead && store) H_(k, k - 1) = hk;
+                    p = p + s;
+                    x = p / s;
+                    y = q / s;
+                    z = r / s;
+                    q = q / p;
+                    r = r / p;
+                    for (int j = k + T; j < nn; j += NT) {
+                        double pp = H_(k, j) + q * H_(k + 1, j);
+                        if (notlast) {
+                            pp = pp + r * H_(k + 2, j);
+                            H_(k + 2, j) = H_(k + 2, j) - pp * z;
+                        }
+                        H_(k, j) = H_(k, j) - pp * x;
+                        H_(k + 1, j) = H_(k + 1, j) - pp * y;
+                    }
+                    team.sync();
+                    const int imax = (n < k + 3) ? n : k + 3;
+                    for (int i = T; i <= imax; i += NT) {
+                        double pp = x * H_(i, k) + y * H_(i, k + 1);
+                        if (notlast) {
+                            pp = pp + z * H_(i, k + 2);
+                            H_(i, k + 2) = H_(i, k + 2) - pp * r;
+                        }
+                        H_(i, k) = H_(i, k) - pp;
+                        H_(i, k + 1) = H_(i, k + 1) - pp * q;
+                    }
+                    for (int i = low + T; i <= high; i += NT) {
+                        double pp = x * V_(i, k) + y * V_(i, k + 1);
+                        if (notlast) {
+                            pp = pp + z * V_(i, k + 2);
+                            V_(i, k + 2) = V_(i, k + 2) - pp * r;
+                        }
+                        V_(i, k) = V_(i, k) - pp;
+                        V_(i, k + 1) = V_(i, k + 1) - pp * q;
+                    }
+                    team.sync();
+                }
+            }
+        }
+    }
+    // back-substitution (O(n^2) per vector, redundant in every thread; the
+    // stores are thread 0's)
+    if (norm == 0.0) return true;
+    for (n = nn - 1; n >= 0; n--) {
+        p = wr[n];
+        q = wi[n];
+        if (q == 0) {
+            int l = n;
+            team.sync();
+            if (lead) H_(n, n) = 1.0;
+            team.sync();
+            for (int i = n - 1; i >= 0; i--) {
+                w = H_(i, i) - p;
+                r = 0.0;
+                for (int j = l; j <= n; j++) r = r + H_(i, j) * H_(j, n);
+                if (wi[i] < 0.0) {
+                    z = w;
+                    s = r;
+                } else {
+                    l = i;
+                    double a0, a1 = 0.0;
+                    bool two = false;
+                    if (wi[i] == 0.0) {
+                        a0 = (w != 0.0) ? -r / w : -r / (eps * norm);
+                    } else {
+                        x = H_(i, i + 1);
+                        y = H_(i + 1, i);
+                        q = (wr[i] - p) * (wr[i] - p) + wi[i] * wi[i];
+                        t = (x * s - z * r) / q;
+                        a0 = t;
+                        a1 = (fabs(x) > fabs(z)) ? (-r - w * t) / x : (-s - y * t) / z;
+                        two = true;
+                    }
+                    team.sync();
+                    if (lead) {
+                        H_(i, n) = a0;
+                        if (two) H_(i + 1, n) = a1;
+                    }
+                    team.sync();
+                    t = fabs(a0);
+                    if ((eps * t) * t > 1) {
+                        for (int j = i + T; j <= n; j += NT) H_(j, n) = H_(j, n) / t;
+                        team.sync();
+                    }
+                }
+            }
+        } else if (q < 0) {
+            int l = n - 1;
+            double cr, ci;
+            double h00, h01;
+            if (fabs(H_(n, n - 1)) > fabs(H_(n - 1, n))) {
+                h00 = q / H_(n, n - 1);
+                h01 = -(H_(n, n) - p) / H_(n, n - 1);
+            } else {
+                detail::cdiv(0.0, -H_(n - 1, n), H_(n - 1, n - 1) - p, q, cr, ci);
+                h00 = cr;
+                h01 = ci;
+            }
+            team.sync();
+            if (lead) {
+                H_(n - 1, n - 1) = h00;
+                H_(n - 1, n) = h01;
+                H_(n, n - 1) = 0.0;
+                H_(n, n) = 1.0;
+            }
+            team.sync();
+            for (int i = n - 2; i >= 0; i--) {
+                double ra = 0.0, sa = 0.0, vr, vi;
+                for (int j = l; j <= n; j++) {
+                    ra = ra + H_(i, j) * H_(j, n - 1);
+                    sa = sa + H_(i, j) * H_(j, n);
+                }
+                w = H_(i, i) - p;
+                if (wi[i] < 0.0) {
+                    z = w;
+                    r = ra;
+                    s = sa;
+                } else {
+                    l = i;
+                    double b0, b1, b2 = 0.0, b3 = 0.0;
+                    bool two = false;
+                    if (wi[i] == 0) {
+                        detail::cdiv(-ra, -sa, w, q, cr, ci);
+                        b0 = cr;
+                        b1 = ci;
+                    } else {
+                        x = H_(i, i + 1);
+                        y = H_(i + 1, i);
+                        vr = (wr[i] - p) * (wr[i] - p) + wi[i] * wi[i] - q * q;
+                        vi = (wr[i] - p) * 2.0 * q;
+                        if (vr == 0.0 && vi == 0.0)
+                            vr = eps * norm * (fabs(w) + fabs(q) + fabs(x) + fabs(y) + fabs(z));
+                        detail::cdiv(x * r - z * ra + q * sa, x * s - z * sa - q * ra, vr, vi, cr, ci);
+                        b0 = cr;
+                        b1 = ci;
+                        if (fabs(x) > (fabs(z) + fabs(q))) {
+                            b2 = (-ra - w * b0 + q * b1) / x;
+                            b3 = (-sa - w * b1 - q * b0) / x;
+                        } else {
+                            detail::cdiv(-r - y * b0, -s - y * b1, z, q, cr, ci);
+                            b2 = cr;
+                            b3 = ci;
+                        }
+                        two = true;
+                    }
+                    team.sync();
+                    if (lead) {
+                        H_(i, n - 1) = b0;
+                        H_(i, n) = b1;
+                        if (two) {
+                            H_(i + 1, n - 1) = b2;
+                            H_(i + 1, n) = b3;
+                        }
+                    }
+                    team.sync();
+                    t = fmax(fabs(b0), fabs(b1));
+                    if ((eps * t) * t > 1) {
+                        for (int j = i + T; j <= n; j += NT) {
+                            H_(j, n - 1) = H_(j, n - 1) / t;
+                            H_(j, n) = H_(j, n) / t;
+                        }
+                        team.sync();
+                    }
+                }
+            }
+        }
+    }
+    team.sync();
+    // back-transformation: each thread owns whole rows of V
+    for (int i = low + T; i <= high; i += NT)
+        for (int j = nn - 1; j >= low; j--) {
+            double zz = 0.0;
+            const int kmax = j < high ? j : high;
+            for (int k = low; k <= kmax; k++) zz = zz + V_(i, k) * H_(k, j);
+            V_(i, j) = zz;
+        }
+    team.sync();
+    return true;
+#undef H_
+#undef V_
+}
+
+// ---------------------------------------------------------------------------
 // Team-parallel cyclic Jacobi eigen-decomposition of a symmetric n x n matrix
 // held column-major (ld n) in `a` (shared memory on the device).  Rotations
 // of one round-robin round act on disjoint index pairs, so every 2x2 block of

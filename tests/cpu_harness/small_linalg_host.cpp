@@ -69,3 +69,17 @@ extern "C" int h_subspace_eig_top(int n, const double* a, int k, int m, double* 
     for (size_t e = 0; e < (size_t)n * k; ++e) u[e] = ub[e];
     return ok;
 }
+
+extern "C" int h_eig_real_team(int n, const double* a, double* wr, double* wi, double* v) {
+    std::vector<double> h(a, a + (size_t)n * n), ort(n);
+    TeamHost team;
+    return eig_real_team(team, n, h.data(), v, wr, wi, ort.data()) ? 1 : 0;
+}
+
+extern "C" int h_lu_inverse_team(int n, const double* a, double* inv) {
+    std::vector<double> m(a, a + (size_t)n * n), piv(n), scr(4);
+    std::vector<int> rp(n), cp(n);
+    TeamHost team;
+    return lu_fullpiv_inverse_team(team, n, m.data(), n, inv, n, rp.data(), cp.data(), piv.data(), scr.data()) ? 1
+                                                                                                             : 0;
+}

@@ -53,13 +53,14 @@ def test_jacobi_eig_sym(lib, n):
     assert np.allclose(a @ v, v * w[None, :], atol=1e-10 * ref.max())
 
 
+@pytest.mark.parametrize("fn", ["h_eig_real", "h_eig_real_team"])
 @pytest.mark.parametrize("n,seed", [(3, 1), (5, 2), (20, 3), (32, 4), (17, 5)])
-def test_eig_real_matches_lapack(lib, n, seed):
+def test_eig_real_matches_lapack(lib, n, seed, fn):
     s = rng.Substream(seed)
     a = np.asfortranarray(s.fill_uniform(n, n) * 2 - 1)
     wr, wi = np.zeros(n), np.zeros(n)
     v = np.zeros((n, n), order="F")
-    assert lib.h_eig_real(n, P(a), P(wr), P(wi), P(v)) == 1
+    assert getattr(lib, fn)(n, P(a), P(wr), P(wi), P(v)) == 1
     lam = wr + 1j * wi
     ref = np.linalg.eigvals(a)
     assert np.allclose(np.sort_complex(lam), np.sort_complex(ref), atol=1e-10)
@@ -77,7 +78,8 @@ def test_eig_real_matches_lapack(lib, n, seed):
             c += 1
 
 
-def test_eig_real_gevd_pencil(lib):
+@pytest.mark.parametrize("fn", ["h_eig_real", "h_eig_real_team"])
+def test_eig_real_gevd_pencil(lib, fn):
     # a pencil built the way GevdInit builds it (cp_als.cpp:117-126)
     truth = O.KruskalModel([rng.Substream(9 + k).fill_uniform(12, 4) for k in range(3)], np.ones(4))
     t = O.reconstruct(truth)
@@ -90,7 +92,7 @@ def test_eig_real_gevd_pencil(lib):
     pencil = np.asfortranarray(p1 @ np.linalg.inv(p2))
     wr, wi = np.zeros(4), np.zeros(4)
     v = np.zeros((4, 4), order="F")
-    assert lib.h_eig_real(4, P(pencil), P(wr), P(wi), P(v)) == 1
+    assert getattr(lib, fn)(4, P(pencil), P(wr), P(wi), P(v)) == 1
     assert np.allclose(wi, 0)
     ev, evec = np.linalg.eig(pencil)
     # same eigen-pairs up to order/scale
@@ -101,15 +103,16 @@ def test_eig_real_gevd_pencil(lib):
         assert abs(abs(x @ y) - 1) < 1e-9
 
 
-def test_lu_fullpiv(lib):
+@pytest.mark.parametrize("fn", ["h_lu_inverse", "h_lu_inverse_team"])
+def test_lu_fullpiv(lib, fn):
     s = rng.Substream(4)
     a = np.asfortranarray(s.fill_uniform(6, 6))
     inv = np.zeros((6, 6), order="F")
-    assert lib.h_lu_inverse(6, P(a), P(inv)) == 1
+    assert getattr(lib, fn)(6, P(a), P(inv)) == 1
     assert np.allclose(inv @ a, np.eye(6), atol=1e-10)
     sing = np.asfortranarray(np.outer(np.arange(1.0, 5), np.arange(2.0, 6)))
     inv = np.zeros((4, 4), order="F")
-    assert lib.h_lu_inverse(4, P(sing), P(inv)) == 0
+    assert getattr(lib, fn)(4, P(sing), P(inv)) == 0
     assert O.fullpiv_lu_invertible(sing) is False
 
 
@@ -207,3 +210,18 @@ def test_subspace_eig_top_gives_up_without_gap(lib):
     assert lib.h_subspace_eig_top(60, P(a), 10, 16, P(u), P(theta)) == 0
     z = np.zeros((40, 40), order="F")
     assert lib.h_subspace_eig_top(40, P(z), 4, 8, P(np.zeros((40, 4), order="F")), P(np.zeros(8))) == 0
+
+
+def test_eig_real_team_is_the_serial_arithmetic(lib):
+    # one-thread team instantiation == the serial routine, bit for bit
+    for n, seed in [(7, 11), (20, 12), (25, 13)]:
+        s = rng.Substream(seed)
+        a = np.asfortranarray(s.fill_uniform(n, n) * 2 - 1)
+        outs = []
+        for fn in ("h_eig_real", "h_eig_real_team"):
+            wr, wi = np.zeros(n), np.zeros(n)
+            v = np.zeros((n, n), order="F")
+            assert getattr(lib, fn)(n, P(a), P(wr), P(wi), P(v)) == 1
+            outs.append((wr, wi, v))
+        for x, y in zip(*outs):
+            assert np.array_equal(x, y)
