@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
                                                                  double tol, const double* maxdiag, int* rank,
                                                                  double* Linv, int nblk) {
     __shared__ double colk[kCholNB + 1], rowk[kCholNB + 1];
-    __shared__ double sh_rp;
+    __shared__ double shv_rp[2];
     __shared__ int sh_dead;
     double* a = A + (size_t)blockIdx.x * sA;
     const int nb = min(kCholNB, n - k0);
@@ -93,9 +93,10 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
     }
     const double md = maxdiag[blockIdx.x];
     const double thr = (md > 0.0) ? tol * md : INFINITY;
-    // owner of the diagonal element (k, k): packed index k(k+3)/2
-    __syncthreads();
-    for (int k = 0; k < nb; ++k) {
+    // The owner of diagonal element (k, k) (packed index k(k+3)/2) turns it
+    // into the pivot as soon as its own update of step k-1 is done, so the
+    // pivot's rsqrt overlaps the other threads' updates: two barriers a step.
+    auto pivot = [&](int k) {
         const int ed = k * (k + 3) / 2;
         if (tid == ed % kDiagThreads) {
             const int sd = ed / kDiagThreads;
@@ -104,14 +105,18 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
                 if (s == sd) {
                     const double d = av[s];
                     const bool dead = !(d > thr);
-                    const double piv = dead ? 0.0 : sqrt(d);
-                    av[s] = piv;
-                    sh_rp = dead ? 0.0 : 1.0 / piv;
+                    const double rp = dead ? 0.0 : rsqrt(d);
+                    av[s] = dead ? 0.0 : d * rp;
+                    shv_rp[k & 1] = rp;
                     if (dead) ++sh_dead;
                 }
         }
-        __syncthreads();
-        const double rp = sh_rp;
+    };
+    __syncthreads();
+    pivot(0);
+    __syncthreads();
+    for (int k = 0; k < nb; ++k) {
+        const double rp = shv_rp[k & 1];
 #pragma unroll
         for (int s = 0; s < kDiagPer; ++s) {
             const int i = iv[s], j = jv[s];
@@ -132,7 +137,8 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
             av[s] -= ci * colk[jv[s]];
             bv[s] -= ci * rowk[jv[s]];
         }
-        // the next step's first barrier orders these reads before colk/rowk are rewritten
+        if (k + 1 < nb) pivot(k + 1);
+        __syncthreads();
     }
     if (tid == 0 && sh_dead) atomicSub(&rank[blockIdx.x], sh_dead);
     double* inv = Linv + ((size_t)blockIdx.x * nblk + k0 / kCholNB) * kCholNB * kCholNB;
@@ -181,33 +187,75 @@ struct PanelC {
     }
 };
 
-struct CholTrailA {
-    double* A;
-    int lda;
-    long long sA;
-    int r0, k0;
-    __device__ double operator()(int b, int m, int k) const {
-        return A[(size_t)b * sA + (r0 + m) + (size_t)lda * (k0 + k)];
+// Trailing update of the right-looking step: for the lower triangle of the
+// trailing block (rows/columns r0..n-1)
+//   A(i, j) -= sum_k L21(i, k) L21(j, k),   L21 = A[r0:, k0:k0+nb]
+// One CTA per 64 x 64 lower tile (tile (ti, tj), ti >= tj) and matrix: both
+// panel slices are staged whole in shared memory (K = nb <= 64), the product
+// runs on the FP64 tensor cores (DMMA m8n8k4, 8 warps x 32 x 16), and the
+// result goes back through shared memory so the read-modify-write of A is
+// column-coalesced.
+constexpr int kTrailLD = kCholNB + 4;
+
+__global__ void __launch_bounds__(256) chol_trail_kernel(double* A, int n, int lda, long long sA, int r0, int k0,
+                                                         int nb) {
+    extern __shared__ double trail_smem[];
+    double* Pi = trail_smem;                       // [64 k][kTrailLD m]
+    double* Pj = trail_smem + kCholNB * kTrailLD;  // [64 k][kTrailLD m]
+    const int t = blockIdx.x;
+    int ti = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    while (ti * (ti + 1) / 2 > t) --ti;
+    const int tj = t - ti * (ti + 1) / 2;
+    double* a = A + (size_t)blockIdx.z * sA;
+    const int i0 = r0 + kCholNB * ti, j0 = r0 + kCholNB * tj;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < kCholNB * kCholNB; e += 256) {
+        const int m = e % kCholNB, kk = e / kCholNB;
+        const bool kin = kk < nb;
+        Pi[kk * kTrailLD + m] = (kin && i0 + m < n) ? a[(i0 + m) + (size_t)lda * (k0 + kk)] : 0.0;
+        Pj[kk * kTrailLD + m] = (kin && j0 + m < n) ? a[(j0 + m) + (size_t)lda * (k0 + kk)] : 0.0;
     }
-};
-struct CholTrailB {
-    double* A;
-    int lda;
-    long long sA;
-    int r0, k0;
-    __device__ double operator()(int b, int k, int nn) const {
-        return A[(size_t)b * sA + (r0 + nn) + (size_t)lda * (k0 + k)];
+    __syncthreads();
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int kend = (nb + 3) & ~3;
+    for (int kk = 0; kk < kend; kk += 4) {
+        double fa[4], fb[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) fa[i] = Pi[(kk + t4) * kTrailLD + wm + i * 8 + g];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) fb[j] = Pj[(kk + t4) * kTrailLD + wn + j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
     }
-};
-struct CholTrailC {
-    double* A;
-    int lda;
-    long long sA;
-    int r0;
-    __device__ void operator()(int b, int m, int nn, double v) const {
-        if (m >= nn) A[(size_t)b * sA + (r0 + m) + (size_t)lda * (r0 + nn)] -= v;
+    __syncthreads();
+    // stage the 64 x 64 product column-major (ld 65) over the panel buffers
+    double* Cs = trail_smem;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int m = wm + i * 8 + g, nn = wn + j * 8 + 2 * t4 + v;
+                Cs[m + (kCholNB + 1) * nn] = acc[i][j][v];
+            }
+    __syncthreads();
+    for (int e = tid; e < kCholNB * kCholNB; e += 256) {
+        const int m = e % kCholNB, nn = e / kCholNB;
+        const int gi = i0 + m, gj = j0 + nn;
+        if (gi < n && gj < n && gi >= gj) a[gi + (size_t)lda * gj] -= Cs[m + (kCholNB + 1) * nn];
     }
-};
+}
 
 // In-place batched semi-definite Cholesky.  Lower triangle holds L on return;
 // the strict upper triangle outside the diagonal blocks is left as it was
@@ -217,6 +265,13 @@ struct CholTrailC {
 inline void chol_batched(double* A, int n, int lda, long long sA, int batch, double tol, double* maxdiag,
                          int* rank, DevBuf<double>& linv, cudaStream_t st) {
     if (batch <= 0 || n <= 0) return;
+    constexpr size_t kTrailSmem = 2 * kCholNB * kTrailLD * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        OCTEN_CUDA(cudaFuncSetAttribute(chol_trail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kTrailSmem));
+        attr = true;
+    }
     const int nblk = (n + kCholNB - 1) / kCholNB;
     linv.reserve((size_t)batch * nblk * kCholNB * kCholNB);
     chol_maxdiag_kernel<<<batch, 256, 0, st>>>(A, n, lda, sA, maxdiag, rank); OCTEN_LAUNCHED(1);
@@ -229,9 +284,10 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
         const int r0 = k0 + nb;
         gemm_f64<false, true>(batch, rows, nb, nb, PanelA{A, lda, sA, r0, k0}, PanelB{linv.p, nblk, k0 / kCholNB},
                                                PanelC{A, lda, sA, r0, k0}, st);
-        gemm_f64<false, false>(batch, rows, rows, nb, CholTrailA{A, lda, sA, r0, k0},
-                                                CholTrailB{A, lda, sA, r0, k0}, CholTrailC{A, lda, sA, r0},
-                                                st, 1, nullptr, 1);
+        const int tiles = (rows + kCholNB - 1) / kCholNB;
+        chol_trail_kernel<<<dim3(tiles * (tiles + 1) / 2, 1, batch), 256, kTrailSmem, st>>>(A, n, lda, sA, r0, k0,
+                                                                                              nb);
+        OCTEN_LAUNCHED(1);
     }
 }
 

@@ -110,7 +110,11 @@ void run_compress(CompressEngine& e, const T* dX, std::int64_t t, const double* 
         bool done = false;
         OCTEN_CUDA(cudaEventRecord(e.event(2 * e.g1_used), st));
         if constexpr (std::is_same<T, float>::value) {
-            if (use_tc) done = tc_gemm_tf32x3(e.Ahi.p, e.Alo.p, e.lda_tc, Xc, Z1, (int)e.Meff, (long long)N1, (int)e.I, st);
+            // tensor-core path: GEMM1 scatters its rows replica-contiguously
+            // (P*Q x N1) for the batched tcgen05 mode-2 contraction
+            if (use_tc)
+                done = tc_gemm_tf32x3(e.Ahi.p, e.Alo.p, e.lda_tc, Xc, Z1, (int)e.Meff, (long long)N1, (int)e.I, st, P,
+                                      Q, e.shared);
             e.used_tc = done;
         }
         if (!done)
@@ -120,8 +124,15 @@ void run_compress(CompressEngine& e, const T* dX, std::int64_t t, const double* 
         ++e.g1_used;
         ++e.gemm1_launches;
         e.gemm1_flops += 2.0 * (double)e.Meff * (double)N1 * (double)e.I;
-        gemm_simt<T, T, true, false>(P * tc, Q, Q, (int)e.J, G2A<T>{Z1, e.rowmap.p, N1, e.J, tc, Q},
-                                     G2B<T>{V, e.J, tc, Q}, G2C<T>{Z2, tc, Q}, st);
+        bool done2 = false;
+        if constexpr (std::is_same<T, float>::value) {
+            if (done)
+                done2 = tc_mode2_tf32x3(Z1, N1, (int)e.J, tc, e.Vhi.p, e.Vlo.p, e.ldv_tc, P, Q, Z2, st);
+        }
+        if (!done2)
+            gemm_simt<T, T, true, false>(P * tc, Q, Q, (int)e.J,
+                                         G2A<T>{Z1, done ? e.rowmap_id.p : e.rowmap.p, N1, e.J, tc, Q},
+                                         G2B<T>{V, e.J, tc, Q}, G2C<T>{Z2, tc, Q}, st);
         gemm_f64<false, true>(P, Q * Q, Q, tc, G3A<T>{Z2, tc, Q}, G3B{dW, t, k0, Q}, G3C{dY, Q}, st);
     }
     OCTEN_CUDA(cudaGetLastError());
@@ -190,6 +201,29 @@ void CompressEngine::set_projections(int P_, int Q_, int shared_, std::int64_t I
         }
     Ahi.upload(ahi.data(), ahi.size(), st);
     Alo.upload(alo.data(), alo.size(), st);
+    // same split of V for the tensor-core mode-2 contraction: row p Q + b = V_p[:, b]
+    ldv_tc = (int)((J + 3) / 4 * 4);
+    {
+        std::vector<float> vhi((size_t)P * Q * ldv_tc, 0.f), vlo((size_t)P * Q * ldv_tc, 0.f);
+        for (int p = 0; p < P; ++p)
+            for (int b = 0; b < Q; ++b)
+                for (std::int64_t j = 0; j < J; ++j) {
+                    const double v = hV[(size_t)p * J * Q + j + (size_t)J * b];
+                    float f = (float)v;
+                    uint32_t bits;
+                    std::memcpy(&bits, &f, 4);
+                    bits &= 0xFFFFE000u;
+                    float h;
+                    std::memcpy(&h, &bits, 4);
+                    vhi[((size_t)p * Q + b) * ldv_tc + j] = h;
+                    vlo[((size_t)p * Q + b) * ldv_tc + j] = (float)(v - (double)h);
+                }
+        Vhi.upload(vhi.data(), vhi.size(), st);
+        Vlo.upload(vlo.data(), vlo.size(), st);
+        std::vector<int> rid((size_t)P * Q);
+        for (size_t i = 0; i < rid.size(); ++i) rid[i] = (int)i;
+        rowmap_id.upload(rid.data(), rid.size(), st);
+    }
     std::vector<float> v32(hV, hV + (size_t)P * J * Q);
     rowmap.upload(rm.data(), rm.size(), st);
     A64.upload(a64.data(), a64.size(), st);
@@ -197,13 +231,14 @@ void CompressEngine::set_projections(int P_, int Q_, int shared_, std::int64_t I
     V64.upload(hV, (size_t)P * J * Q, st);
     V32.upload(v32.data(), v32.size(), st);
     // Z1 chunk of about 1 GiB
-    chunk_slices = std::max<std::int64_t>(1, (std::int64_t)((1ULL << 28) / (unsigned long long)std::max<std::int64_t>(1, Meff * J)));
+    const std::int64_t zrows = std::max<std::int64_t>(Meff, (std::int64_t)P * Q);  // scattered tc layout: P*Q rows
+    chunk_slices = std::max<std::int64_t>(1, (std::int64_t)((1ULL << 28) / (unsigned long long)std::max<std::int64_t>(1, zrows * J)));
     OCTEN_CUDA(cudaStreamSynchronize(st));
 }
 
 void CompressEngine::compress_f32(const float* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st) {
     const std::int64_t tc = std::min(t, chunk_slices);
-    Z1f.reserve((size_t)Meff * J * tc);
+    Z1f.reserve((size_t)std::max<std::int64_t>(Meff, (std::int64_t)P * Q) * J * tc);
     Z2f.reserve((size_t)P * Q * Q * tc);
     run_compress<float>(*this, dX, t, dW, dY, Z1f.p, Z2f.p, A32.p, V32.p, tc, st, true);
 }

@@ -92,6 +92,9 @@ public:
     DevBuf<float> A32;   // Meff x I row-major (deduplicated shared columns)
     DevBuf<float> Ahi, Alo;  // TF32 split of the fp64 projections (tcgen05 path)
     int lda_tc = 0;
+    DevBuf<float> Vhi, Vlo;  // TF32 split of V: P*Q x ldv_tc, row p Q + b = V_p[:, b]
+    int ldv_tc = 0;
+    DevBuf<int> rowmap_id;   // identity row map (replica-contiguous Z1 of the tc path)
     bool used_tc = false;
     DevBuf<double> A64;  // Meff x I row-major
     DevBuf<float> V32;   // P x J x Q

@@ -116,10 +116,39 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+// Row scatter of the epilogue (scP > 0): output row m of the deduplicated
+// stack goes to replica rows p*Q + a -- the `sh` shared rows to every replica,
+// private row m = sh + p (Q - sh) + (a - sh) to its own -- so the next
+// contraction reads each replica's Q rows contiguously.
+__device__ __forceinline__ void store_row_chunk(float* Z, long long ldz, int row, long long nb, long long N,
+                                                const uint32_t* r, int scP, int scQ, int scSh) {
+    auto put = [&](float* zrow) {
+        if (nb + 32 <= N && (ldz % 4) == 0) {
+            float4* dst = (float4*)(zrow + nb);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                     __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        } else {
+            for (int j = 0; j < 32; ++j)
+                if (nb + j < N) zrow[nb + j] = __uint_as_float(r[j]);
+        }
+    };
+    if (scP <= 0) {
+        put(Z + (size_t)row * ldz);
+    } else if (row < scSh) {
+        for (int p = 0; p < scP; ++p) put(Z + ((size_t)p * scQ + row) * ldz);
+    } else {
+        const int pr = scQ - scSh;
+        const int p = (row - scSh) / pr, a = scSh + (row - scSh) % pr;
+        put(Z + ((size_t)p * scQ + a) * ldz);
+    }
+}
+
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                           const __grid_constant__ CUtensorMap map_x, float* __restrict__ Z, int M, long long N, int K,
-                          long long ldz) {
+                          long long ldz, int scP, int scQ, int scSh) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-align the stage buffers (SW128 atoms)
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -225,7 +254,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tc_fence_after();
             const int q = warp & 3;
             const int row = m0 + q * 32 + lane;
-            float* zrow = Z + (size_t)row * ldz;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t r[32];
@@ -240,17 +268,163 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                       "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (row < M) {
-                    const long long nb = n0 + c0;
-                    if (nb + 32 <= N && (ldz % 4) == 0) {
-                        float4* dst = (float4*)(zrow + nb);
+                if (row < M) store_row_chunk(Z, ldz, row, n0 + c0, N, r, scP, scQ, scSh);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Mode-2 contraction of the compression, batched over (replica p, slice k):
+//   Z2[p][a + Q b + Q^2 k] = sum_j Z1[p Q + a][k J + j] * V_p[j, b]
+// One CTA per (p, k): M = 128 rows of Z1 (a < Q used), N = 112 columns
+// (b < Q used), K = J in 32-wide blocks.  Z1 (replica-contiguous rows, the
+// scattered GEMM1 output) is split hi/lo in shared memory like X in GEMM1;
+// V_p comes pre-split (Vhi/Vlo, P*Q x ldv, rows b, K = j contiguous).  Rows
+// or columns past the tensors are TMA zero-filled; A columns past slice k
+// meet zero B rows (j >= J), so they contribute nothing.
+// ---------------------------------------------------------------------------
+constexpr int M2_BN = 112;
+constexpr int M2_STAGES = 3;
+constexpr int M2_A_BYTES = BM * BKB;                      // 16 KB
+constexpr int M2_B_BYTES = M2_BN * BKB;                   // 14 KB
+constexpr int M2_STAGE_BYTES = 2 * M2_A_BYTES + 2 * M2_B_BYTES;
+constexpr uint32_t M2_TMEM_COLS = 128;
+
+constexpr uint32_t make_idesc_m2() {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(M2_BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    tc_mode2_tf32x3_kernel(const __grid_constant__ CUtensorMap map_z1, const __grid_constant__ CUtensorMap map_vhi,
+                           const __grid_constant__ CUtensorMap map_vlo, float* __restrict__ Z2, int Q, int J, int tc) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full_bar = (uint64_t*)(smem + M2_STAGES * M2_STAGE_BYTES);
+    uint64_t* conv_bar = full_bar + M2_STAGES;
+    uint64_t* empty_bar = conv_bar + M2_STAGES;
+    uint64_t* done_bar = empty_bar + M2_STAGES;
+    uint32_t* tmem_slot = (uint32_t*)(done_bar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int p = blockIdx.x / tc, k = blockIdx.x % tc;
+    const int num_kb = (J + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < M2_STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&conv_bar[s], CONVERT_WARPS * 32);
+            mbar_init(&empty_bar[s], 1);
+        }
+        mbar_init(done_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(M2_TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < num_kb; ++kb) {
+                const int s = kb % M2_STAGES;
+                const uint32_t ph = (kb / M2_STAGES) & 1;
+                if (kb >= M2_STAGES) mbar_wait(&empty_bar[s], ph ^ 1);
+                uint8_t* st = smem + s * M2_STAGE_BYTES;
+                mbar_arrive_expect_tx(&full_bar[s], M2_A_BYTES + 2 * M2_B_BYTES);
+                tma_load_2d(st, &map_z1, &full_bar[s], k * J + kb * BK, p * Q);
+                tma_load_2d(st + 2 * M2_A_BYTES, &map_vhi, &full_bar[s], kb * BK, p * Q);
+                tma_load_2d(st + 2 * M2_A_BYTES + M2_B_BYTES, &map_vlo, &full_bar[s], kb * BK, p * Q);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc_m2();
+            for (int kb = 0; kb < num_kb; ++kb) {
+                const int s = kb % M2_STAGES;
+                const uint32_t ph = (kb / M2_STAGES) & 1;
+                mbar_wait(&conv_bar[s], ph);
+                tc_fence_after();
+                uint8_t* st = smem + s * M2_STAGE_BYTES;
+                const uint32_t a_hi = smem_u32(st), a_lo = smem_u32(st + M2_A_BYTES);
+                const uint32_t b_hi = smem_u32(st + 2 * M2_A_BYTES), b_lo = smem_u32(st + 2 * M2_A_BYTES + M2_B_BYTES);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-                    } else {
-                        for (int j = 0; j < 32; ++j)
-                            if (nb + j < N) zrow[nb + j] = __uint_as_float(r[j]);
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                    const uint32_t off = kk * 32;
+                    const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+                    mma_tf32(tmem_base, make_desc_sw128(a_hi + off), make_desc_sw128(b_hi + off), idesc, acc0);
+                    mma_tf32(tmem_base, make_desc_sw128(a_hi + off), make_desc_sw128(b_lo + off), idesc, 1u);
+                    mma_tf32(tmem_base, make_desc_sw128(a_lo + off), make_desc_sw128(b_hi + off), idesc, 1u);
+                }
+                mma_commit(&empty_bar[s]);
+            }
+            mma_commit(done_bar);
+        }
+    } else {
+        // ---- Z1 tile hi/lo split (warps 2..7) ----
+        const int ct = threadIdx.x - CONVERT_WARP0 * 32;
+        for (int kb = 0; kb < num_kb; ++kb) {
+            const int s = kb % M2_STAGES;
+            const uint32_t ph = (kb / M2_STAGES) & 1;
+            mbar_wait(&full_bar[s], ph);
+            uint8_t* st = smem + s * M2_STAGE_BYTES;
+            float4* ah = (float4*)st;
+            float4* al = (float4*)(st + M2_A_BYTES);
+            for (int i = ct; i < M2_A_BYTES / 16; i += CONVERT_WARPS * 32) {
+                const float4 v = ah[i];
+                float4 h, l;
+                h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                l.x = v.x - h.x;
+                l.y = v.y - h.y;
+                l.z = v.z - h.z;
+                l.w = v.w - h.w;
+                ah[i] = h;
+                al[i] = l;
+            }
+            fence_proxy_async();
+            mbar_arrive(&conv_bar[s]);
+        }
+        if (warp >= 4) {
+            // ---- epilogue: lanes are rows a; each column b is one coalesced 128 B store per warp ----
+            mbar_wait(done_bar, 0);
+            tc_fence_after();
+            const int q = warp & 3;
+            const int a = q * 32 + lane;
+            const size_t q2 = (size_t)Q * Q;
+            float* zb = Z2 + (size_t)p * q2 * tc + q2 * k;
+#pragma unroll 1
+            for (int c0 = 0; c0 < M2_BN; c0 += 32) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (a < Q) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int b = c0 + j;
+                        if (b < Q) zb[a + (size_t)Q * b] = __uint_as_float(r[j]);
                     }
                 }
             }
@@ -260,7 +434,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(M2_TMEM_COLS));
     }
 }
 
@@ -311,7 +485,7 @@ bool tc_gemm_available() {
 }
 
 bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X, float* Z, int M, long long N, int K,
-                    cudaStream_t st) {
+                    cudaStream_t st, int scatter_p, int scatter_q, int scatter_sh) {
     if (!tc_gemm_available()) return false;
     if ((K % 4) != 0 || (lda % 4) != 0 || ((uintptr_t)X % 16) != 0 || ((uintptr_t)Ahi % 16) != 0 ||
         ((uintptr_t)Alo % 16) != 0 || N > (1LL << 31) - 1 || M <= 0 || N <= 0 || K <= 0)
@@ -327,7 +501,30 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
         attr = true;
     }
     dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
-    tc_gemm_tf32x3_kernel<<<grid, NUM_THREADS, smem, st>>>(mhi, mlo, mx, Z, M, N, K, N);
+    tc_gemm_tf32x3_kernel<<<grid, NUM_THREADS, smem, st>>>(mhi, mlo, mx, Z, M, N, K, N, scatter_p, scatter_q,
+                                                           scatter_sh);
+    OCTEN_LAUNCHED(1);
+    OCTEN_CUDA(cudaGetLastError());
+    return true;
+}
+
+bool tc_mode2_tf32x3(const float* Z1, long long N1, int J, int tc, const float* Vhi, const float* Vlo, int ldv, int P,
+                     int Q, float* Z2, cudaStream_t st) {
+    if (!tc_gemm_available()) return false;
+    if (Q > M2_BN || Q < 1 || (N1 % 4) != 0 || (ldv % 4) != 0 || ((uintptr_t)Z1 % 16) != 0 ||
+        ((uintptr_t)Vhi % 16) != 0 || ((uintptr_t)Vlo % 16) != 0 || (long long)P * tc > 2147483647LL)
+        return false;
+    CUtensorMap mz, mh, ml;
+    if (!make_map(&mz, Z1, (uint64_t)N1, (uint64_t)P * Q, (uint64_t)N1 * 4, BK, BM)) return false;
+    if (!make_map(&mh, Vhi, (uint64_t)J, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, M2_BN)) return false;
+    if (!make_map(&ml, Vlo, (uint64_t)J, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, M2_BN)) return false;
+    const size_t smem = M2_STAGES * M2_STAGE_BYTES + 1024 + 256;
+    static bool attr = false;
+    if (!attr) {
+        OCTEN_CUDA(cudaFuncSetAttribute(tc_mode2_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    tc_mode2_tf32x3_kernel<<<P * tc, NUM_THREADS, smem, st>>>(mz, mh, ml, Z2, Q, J, tc);
     OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     return true;

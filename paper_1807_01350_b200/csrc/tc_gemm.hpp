@@ -13,7 +13,16 @@ namespace octen {
 bool tc_gemm_available();
 // A_hi / A_lo: M x K row-major (leading dimension lda >= K, lda % 4 == 0);
 // X: K x N column-major (K contiguous); Z: M x N row-major (ld N).
+// scatter_p > 0: output row m of the deduplicated stack is written to the
+// replica rows p * scatter_q + a (shared rows m < scatter_sh to every replica),
+// so Z is scatter_p * scatter_q x N.
 bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X, float* Z, int M, long long N, int K,
-                    cudaStream_t st);
+                    cudaStream_t st, int scatter_p = 0, int scatter_q = 0, int scatter_sh = 0);
+// Mode-2 contraction batched over (replica, slice):
+//   Z2[p][a + Q b + Q^2 k] = sum_j Z1[p Q + a][k J + j] V_p[j, b]
+// Z1: P*Q x N1 row-major (N1 = J * tc); Vhi/Vlo: TF32 hi/lo split of V,
+// P*Q x ldv row-major (row p Q + b holds V_p[:, b]).  Requires Q <= 112.
+bool tc_mode2_tf32x3(const float* Z1, long long N1, int J, int tc, const float* Vhi, const float* Vlo, int ldv, int P,
+                     int Q, float* Z2, cudaStream_t st);
 
 }  // namespace octen

@@ -20,7 +20,7 @@ if [ -n "$FULLK" ]; then
   LCMD="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline"
   for ks in $FULLK; do
     k=${ks%%:*}; sk=0; [ "$k" != "$ks" ] && sk=${ks##*:}
-    timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s $sk -c 1 \
+    timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:$k -s $sk -c 1 \
       -f -o gpurun_out/${TAG}_full_$k $LCMD > gpurun_out/${TAG}_full_$k.log 2>&1
     echo "ncu full $k rc=$?"
   done
