@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(1024) gevd_eig_sym_kernel(AlsDev d, int v_in_s
     double* Vg = d.EV + ((size_t)p * 2 + which) * Q * Q;
     double* V = v_in_smem ? Vs : Vg;
     double* ur = d.Ur + ((size_t)p * 2 + which) * Q * R;
-    for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) A[i] = src[i];
+    g2s_copy(A, src, Q * Q);
     __syncthreads();
     TeamDev team;
     if (mblk > 0) {
@@ -474,16 +474,32 @@ __global__ void __launch_bounds__(256) als_mttkrp_T_kernel(AlsDev d, int mode) {
 }
 
 // KR[p][(a + Q b), s R + r] = A(a,r) B(b,r)
-__global__ void als_kr_kernel(AlsDev d) {
-    // grid (Q [b], R, NP), block >= Q threads [a]: no index division
-    const int b = blockIdx.x, r = blockIdx.y, prob = blockIdx.z;
-    const int a = threadIdx.x;
+__global__ void __launch_bounds__(256) als_kr_kernel(AlsDev d) {
+    // one block per (r, problem): the Q^2 column of KR, coalesced writes
+    const int r = blockIdx.x, prob = blockIdx.y;
     const int Q = d.Q, R = d.R;
-    if (a >= Q) return;
+    if (!d.state[prob].active) return;
+    __shared__ double av[256], bv[256];
+    for (int i = threadIdx.x; i < Q; i += blockDim.x) {
+        av[i] = d.f(prob, 0)[i + (size_t)Q * r];
+        bv[i] = d.f(prob, 1)[i + (size_t)Q * r];
+    }
+    __syncthreads();
     const int p = prob / d.S, s = prob % d.S;
-    const double bv = d.f(prob, 1)[b + (size_t)Q * r];
-    double* K = d.KR + (size_t)p * d.q2() * d.S * R + d.q2() * (size_t)(s * R + r) + (size_t)Q * b;
-    K[a] = d.f(prob, 0)[a + (size_t)Q * r] * bv;
+    double* K = d.KR + (size_t)p * d.q2() * d.S * R + d.q2() * (size_t)(s * R + r);
+    const int q2 = Q * Q;
+    // e = a + Q b, walked as (b, a) to avoid a division per element
+    int b = threadIdx.x / Q, a = threadIdx.x % Q;
+    const int db = blockDim.x / Q, da = blockDim.x % Q;
+    for (int e = threadIdx.x; e < q2; e += blockDim.x) {
+        K[e] = av[a] * bv[b];
+        a += da;
+        b += db;
+        if (a >= Q) {
+            a -= Q;
+            ++b;
+        }
+    }
 }
 
 // One mode update per problem: raw = M V^-1 (COD of the Hadamard Gram;
@@ -511,8 +527,7 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     __shared__ int rank, bad;
     const double* M = Ms;
     {
-        const double* Mg = d.Mb + (size_t)prob * Q * R;
-        for (int e = threadIdx.x; e < Q * R; e += blockDim.x) Ms[e] = Mg[e];
+        g2s_copy(Ms, d.Mb + (size_t)prob * Q * R, Q * R);
     }
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
         double v = 1.0;
@@ -715,6 +730,32 @@ struct TStore {  // T[p][m + Q^2 n]
     size_t q2;
     int SR;
     __device__ void operator()(int p, int m, int n, double v) const { T[(size_t)p * q2 * SR + m + q2 * n] = v; }
+};
+// element-pointer twins for the pipelined DMMA GEMM (16-byte pairs along the
+// fast index; used when Q is even)
+struct YmatP {  // &Y[p][m + Q^2 k]   (M-fast)
+    const double* Y;
+    size_t q3, q2;
+    __device__ const double* operator()(int p, int m, int k) const { return Y + (size_t)p * q3 + m + q2 * k; }
+};
+struct FacP {  // &F[(p S + n / R)][mode][k + Q (n % R)]   (K-fast)
+    const double* F;
+    int S, Q, R, mode;
+    __device__ const double* operator()(int p, int k, int n) const {
+        const int prob = p * S + n / R;
+        return F + ((size_t)prob * 3 + mode) * Q * R + k + (size_t)Q * (n % R);
+    }
+};
+struct YtP {  // &Y[p][k + Q^2 c]   (K-fast)
+    const double* Y;
+    size_t q3, q2;
+    __device__ const double* operator()(int p, int c, int k) const { return Y + (size_t)p * q3 + k + q2 * c; }
+};
+struct KRP {  // &KR[p][k + Q^2 n]   (K-fast)
+    const double* K;
+    size_t q2;
+    int SR;
+    __device__ const double* operator()(int p, int k, int n) const { return K + (size_t)p * q2 * SR + k + q2 * n; }
 };
 struct YtA {  // A(p, c, k) = Y[p][k + Q^2 c]   (Y_(2)^T rows)
     const double* Y;
@@ -1075,20 +1116,31 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     OCTEN_CUDA(cudaFuncSetAttribute(als_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_upd));
     int* hcount = nullptr;
     OCTEN_CUDA(cudaMallocHost(&hcount, sizeof(int)));
+    // 16-byte pairs along every fast index need an even Q (and aligned bases)
+    const bool pipe_ok = (Q % 2 == 0) && ((uintptr_t)dY % 16 == 0) && ((uintptr_t)F.p % 16 == 0) &&
+                         ((uintptr_t)KR.p % 16 == 0);
     int sweep = 0;
     for (; sweep < max_iters; ++sweep) {
         active_count.zero(1, st);
         // T = Y x3 C  (Q^2 x SR per replica)
-        gemm_f64<false, true>(P, (int)q2, SR, Q, YmatA{dY, q3, q2, S, false}, FacB{F.p, S, Q, R, 2},
-                                               TStore{T.p, q2, SR}, st);
+        if (pipe_ok)
+            gemm_f64_pipe<false>(P, (int)q2, SR, Q, YmatP{dY, q3, q2}, FacP{F.p, S, Q, R, 2}, TStore{T.p, q2, SR},
+                                 st);
+        else
+            gemm_f64<false, true>(P, (int)q2, SR, Q, YmatA{dY, q3, q2, S, false}, FacB{F.p, S, Q, R, 2},
+                                  TStore{T.p, q2, SR}, st);
         als_mttkrp_T_kernel<<<NP * R, 256, 0, st>>>(d, 0); OCTEN_LAUNCHED(1);
         als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 0, sweep); OCTEN_LAUNCHED(1);
         als_mttkrp_T_kernel<<<NP * R, 256, 0, st>>>(d, 1); OCTEN_LAUNCHED(1);
         als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 1, sweep); OCTEN_LAUNCHED(1);
-        als_kr_kernel<<<dim3(Q, R, NP), (Q + 31) / 32 * 32, 0, st>>>(d);
+        als_kr_kernel<<<dim3(R, NP), 256, 0, st>>>(d);
         OCTEN_LAUNCHED(1);
-        gemm_f64<true, true>(P, Q, SR, (int)q2, YtA{dY, q3, q2}, KRB{KR.p, q2, SR},
-                                              M2Store{Mb.p, S, Q, R}, st, ks_m2, ws.p);
+        if (pipe_ok)
+            gemm_f64_pipe<true>(P, Q, SR, (int)q2, YtP{dY, q3, q2}, KRP{KR.p, q2, SR}, M2Store{Mb.p, S, Q, R}, st,
+                                ks_m2, ws.p);
+        else
+            gemm_f64<true, true>(P, Q, SR, (int)q2, YtA{dY, q3, q2}, KRB{KR.p, q2, SR}, M2Store{Mb.p, S, Q, R}, st,
+                                 ks_m2, ws.p);
         als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 2, sweep); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
         OCTEN_CUDA(cudaMemcpyAsync(hcount, active_count.p, sizeof(int), cudaMemcpyDeviceToHost, st));

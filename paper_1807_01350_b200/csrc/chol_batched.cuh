@@ -197,7 +197,7 @@ struct PanelC {
 // column-coalesced.
 constexpr int kTrailLD = kCholNB + 4;
 
-__global__ void __launch_bounds__(256) chol_trail_kernel(double* A, int n, int lda, long long sA, int r0, int k0,
+__global__ void __launch_bounds__(256, 2) chol_trail_kernel(double* A, int n, int lda, long long sA, int r0, int k0,
                                                          int nb) {
     extern __shared__ double trail_smem[];
     double* Pi = trail_smem;                       // [64 k][kTrailLD m]
@@ -210,11 +210,35 @@ __global__ void __launch_bounds__(256) chol_trail_kernel(double* A, int n, int l
     double* a = A + (size_t)blockIdx.z * sA;
     const int i0 = r0 + kCholNB * ti, j0 = r0 + kCholNB * tj;
     const int tid = threadIdx.x;
-    for (int e = tid; e < kCholNB * kCholNB; e += 256) {
-        const int m = e % kCholNB, kk = e / kCholNB;
-        const bool kin = kk < nb;
-        Pi[kk * kTrailLD + m] = (kin && i0 + m < n) ? a[(i0 + m) + (size_t)lda * (k0 + kk)] : 0.0;
-        Pj[kk * kTrailLD + m] = (kin && j0 + m < n) ? a[(j0 + m) + (size_t)lda * (k0 + kk)] : 0.0;
+    // C tile prefetch (lower part) into registers: its latency overlaps the
+    // panel staging and the DMMAs
+    double cv[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int e = tid + 256 * r;
+        const int m = e & (kCholNB - 1), nn = e >> 6;
+        const int gi = i0 + m, gj = j0 + nn;
+        cv[r] = (gi < n && gj < n && gi >= gj) ? a[gi + (size_t)lda * gj] : 0.0;
+    }
+    // panels: batches of loads into registers, then shared stores
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        double pi[8], pj[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = tid + 256 * (8 * h + r);
+            const int m = e & (kCholNB - 1), kk = e >> 6;
+            const bool kin = kk < nb;
+            pi[r] = (kin && i0 + m < n) ? a[(i0 + m) + (size_t)lda * (k0 + kk)] : 0.0;
+            pj[r] = (kin && j0 + m < n) ? a[(j0 + m) + (size_t)lda * (k0 + kk)] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = tid + 256 * (8 * h + r);
+            const int m = e & (kCholNB - 1), kk = e >> 6;
+            Pi[kk * kTrailLD + m] = pi[r];
+            Pj[kk * kTrailLD + m] = pj[r];
+        }
     }
     __syncthreads();
     const int lane = tid & 31, warp = tid >> 5;
@@ -250,10 +274,12 @@ __global__ void __launch_bounds__(256) chol_trail_kernel(double* A, int n, int l
                 Cs[m + (kCholNB + 1) * nn] = acc[i][j][v];
             }
     __syncthreads();
-    for (int e = tid; e < kCholNB * kCholNB; e += 256) {
-        const int m = e % kCholNB, nn = e / kCholNB;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int e = tid + 256 * r;
+        const int m = e & (kCholNB - 1), nn = e >> 6;
         const int gi = i0 + m, gj = j0 + nn;
-        if (gi < n && gj < n && gi >= gj) a[gi + (size_t)lda * gj] -= Cs[m + (kCholNB + 1) * nn];
+        if (gi < n && gj < n && gi >= gj) a[gi + (size_t)lda * gj] = cv[r] - Cs[m + (kCholNB + 1) * nn];
     }
 }
 

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -126,7 +127,8 @@ void run_compress(CompressEngine& e, const T* dX, std::int64_t t, const double* 
         e.gemm1_flops += 2.0 * (double)e.Meff * (double)N1 * (double)e.I;
         bool done2 = false;
         if constexpr (std::is_same<T, float>::value) {
-            if (done)
+            static const bool no_m2 = std::getenv("OCTEN_DISABLE_TC_MODE2") != nullptr;
+            if (done && !no_m2)
                 done2 = tc_mode2_tf32x3(Z1, N1, (int)e.J, tc, e.Vhi.p, e.Vlo.p, e.ldv_tc, P, Q, Z2, st);
         }
         if (!done2)

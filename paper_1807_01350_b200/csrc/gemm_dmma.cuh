@@ -141,6 +141,168 @@ __global__ void __launch_bounds__(256)
             }
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined variant for operands with 16-byte contiguous pairs along the
+// fast dimension: the functors return element POINTERS (A(b, m, k), B(b, k, n))
+// and tiles move by cp.async 16 B chunks through a 3-stage shared-memory
+// ring, so global latency overlaps the DMMAs.  128 x 64 CTA tile, BK = 16,
+// 8 warps of 32 x 32 (16 DMMA per 8 fragment loads).  A is M-fast
+// (A_KFAST = false: pairs (m, m+1)) or K-fast (pairs (k, k+1)); B is K-fast.
+// Requirements (checked by the caller): the pair start addresses are 16-byte
+// aligned, M (M-fast A) or K is even, the K chunk of a split is a multiple of
+// 16.  Rows/columns/k past the ranges are zero-filled (src-size 0).
+// ---------------------------------------------------------------------------
+namespace pipe {
+constexpr int BM = 128, BN = 64, BK = 16, ST = 3, PAD = 4;
+constexpr int A_M_FAST_ELEMS = BK * (BM + PAD);  // [k][m]
+constexpr int A_K_FAST_ELEMS = BM * (BK + PAD);  // [m][k]
+constexpr int B_ELEMS = BN * (BK + PAD);         // [n][k]
+template <bool A_KFAST>
+constexpr int a_elems() {
+    return A_KFAST ? A_K_FAST_ELEMS : A_M_FAST_ELEMS;
+}
+template <bool A_KFAST>
+constexpr size_t smem_bytes() {
+    return (size_t)ST * (a_elems<A_KFAST>() + B_ELEMS) * sizeof(double);
+}
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+}  // namespace pipe
+
+template <bool A_KFAST, class AF, class BF, class CF>
+__global__ void __launch_bounds__(256)
+    gemm_dmma_pipe_kernel(int M, int N, int K, int ksplit, int kchunk, AF af, BF bf, CF cf, double* partial) {
+    using namespace pipe;
+    extern __shared__ double pipe_smem[];
+    constexpr int AE = a_elems<A_KFAST>();
+    double* As = pipe_smem;                 // ST x AE
+    double* Bs = pipe_smem + ST * AE;       // ST x B_ELEMS
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+    const int zb = blockIdx.z;
+    const int batch = zb / ksplit, ks = zb % ksplit;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int kbeg = ks * kchunk;
+    const int kend = min(K, kbeg + kchunk);
+    const int ntiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+    const double* dummy = af(batch, 0, 0);
+
+    auto load = [&](int kt, int stg) {
+        const int k0 = kbeg + kt * BK;
+        double* as = As + stg * AE;
+        double* bs = Bs + stg * B_ELEMS;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int c = tid + r * 256;  // 1024 chunks
+            if (A_KFAST) {
+                const int mm = c >> 3, kk = (c & 7) * 2;
+                const int gm = m0 + mm, gk = k0 + kk;
+                const bool v = gm < M && gk < kend;
+                cp16(as + mm * (BK + PAD) + kk, v ? af(batch, gm, gk) : dummy, v);
+            } else {
+                const int kk = c >> 6, mm = (c & 63) * 2;
+                const int gm = m0 + mm, gk = k0 + kk;
+                const bool v = gm < M && gk < kend;
+                cp16(as + kk * (BM + PAD) + mm, v ? af(batch, gm, gk) : dummy, v);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int c = tid + r * 256;  // 512 chunks
+            const int nn = c >> 3, kk = (c & 7) * 2;
+            const int gn = n0 + nn, gk = k0 + kk;
+            const bool v = gn < N && gk < kend;
+            cp16(bs + nn * (BK + PAD) + kk, v ? bf(batch, gk, gn) : dummy, v);
+        }
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < ntiles) load(s, s);
+        commit();
+    }
+    for (int kt = 0; kt < ntiles; ++kt) {
+        wait<ST - 2>();
+        __syncthreads();
+        if (kt + ST - 1 < ntiles) load(kt + ST - 1, (kt + ST - 1) % ST);
+        commit();
+        const double* as = As + (kt % ST) * AE;
+        const double* bs = Bs + (kt % ST) * B_ELEMS;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double fa[4], fb[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int m = wm + i * 8 + g;
+                fa[i] = A_KFAST ? as[m * (BK + PAD) + kk + t4] : as[(kk + t4) * (BM + PAD) + m];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) fb[j] = bs[(wn + j * 8 + g) * (BK + PAD) + kk + t4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+        }
+    }
+    wait<0>();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int gm = m0 + wm + i * 8 + g, gn = n0 + wn + j * 8 + 2 * t4 + v;
+                if (gm < M && gn < N) {
+                    if (ksplit == 1)
+                        cf(batch, gm, gn, acc[i][j][v]);
+                    else
+                        partial[(((size_t)batch * ksplit + ks) * M + gm) * N + gn] = acc[i][j][v];
+                }
+            }
+}
+
+template <bool A_KFAST, class AF, class BF, class CF>
+void gemm_f64_pipe(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaStream_t st, int ksplit = 1,
+                   double* workspace = nullptr) {
+    if (batches <= 0 || M <= 0 || N <= 0) return;
+    if (K <= 0) ksplit = 1;
+    if (ksplit < 1) ksplit = 1;
+    int kchunk = (K + ksplit - 1) / ksplit;
+    kchunk = ((kchunk + pipe::BK - 1) / pipe::BK) * pipe::BK;
+    const size_t smem = pipe::smem_bytes<A_KFAST>();
+    static bool attr = false;
+    if (!attr) {
+        OCTEN_CUDA(cudaFuncSetAttribute(gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    dim3 grid((N + pipe::BN - 1) / pipe::BN, (M + pipe::BM - 1) / pipe::BM, batches * ksplit);
+    gemm_dmma_pipe_kernel<A_KFAST><<<grid, 256, smem, st>>>(M, N, K, ksplit, kchunk, af, bf, cf, workspace);
+    OCTEN_LAUNCHED(1);
+    if (ksplit > 1) {
+        const size_t total = (size_t)batches * M * N;
+        int blocks = (int)((total + 255) / 256);
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        gemm_splitk_reduce<double><<<blocks, 256, 0, st>>>(batches, M, N, ksplit, workspace, cf);
+        OCTEN_LAUNCHED(1);
+    }
+}
+
 // Same interface as gemm_simt (fp64 only).
 template <bool A_KFAST, bool B_KFAST, class AF, class BF, class CF>
 void gemm_f64(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaStream_t st, int ksplit = 1,

@@ -440,20 +440,32 @@ __global__ void weight_mass_kernel(int P, int Q, int R, long long max_dim, doubl
 }
 
 // Gw[r](i,j) = sum_p w_pr^2 G_p(i,j), lower triangle.
-__global__ void weighted_gram_kernel(int P, int R, long long d, const double* Gp, const double* w, double* Gw) {
+__global__ void __launch_bounds__(256) weighted_gram_kernel(int P, int R, long long d, const double* Gp,
+                                                            const double* w, double* Gw) {
+    // Gw[r] = sum_p w_pr^2 G_p on the lower triangle; 16 columns r per pass
+    // with the squared weights in shared memory (registers hold the partial
+    // sums, G_p is streamed once per pass)
+    __shared__ double w2[64 * 64];
+    for (int e = threadIdx.x; e < P * R; e += blockDim.x) w2[e] = w[e] * w[e];
+    __syncthreads();
     const size_t total = (size_t)d * d;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
         const long long i = (long long)(e % d), j = (long long)(e / d);
         if (i < j) continue;
-        double g[64];
-        for (int p = 0; p < P; ++p) g[p] = Gp[(size_t)p * total + e];
-        for (int r = 0; r < R; ++r) {
-            double s = 0.0;
+        for (int r0 = 0; r0 < R; r0 += 16) {
+            double acc[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) acc[c] = 0.0;
             for (int p = 0; p < P; ++p) {
-                const double wv = w[(size_t)p + (size_t)P * r];
-                s += wv * wv * g[p];
+                const double g = Gp[(size_t)p * total + e];
+                const double* wp = w2 + p;
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                    if (r0 + c < R) acc[c] += wp[(size_t)P * (r0 + c)] * g;
             }
-            Gw[(size_t)r * total + e] = s;
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                if (r0 + c < R) Gw[(size_t)(r0 + c) * total + e] = acc[c];
         }
     }
 }

@@ -78,4 +78,25 @@ struct DevStatus {
 
 OCTEN_HD inline double dsq(double x) { return x * x; }
 
+#if defined(__CUDACC__)
+// Block-wide global -> shared copy with four independent loads in flight per
+// thread.  (A plain `dst[e] = src[e]` loop through generic pointers makes
+// every load wait for the previous shared store, since the compiler cannot
+// rule out aliasing: one global latency per element per thread.)  src must
+// be read-only for the kernel's lifetime.
+__device__ __forceinline__ void g2s_copy(double* dst, const double* src, int n) {
+    const int st = blockDim.x;
+    int e = threadIdx.x;
+    for (; e + 3 * st < n; e += 4 * st) {
+        const double v0 = __ldg(src + e), v1 = __ldg(src + e + st);
+        const double v2 = __ldg(src + e + 2 * st), v3 = __ldg(src + e + 3 * st);
+        dst[e] = v0;
+        dst[e + st] = v1;
+        dst[e + 2 * st] = v2;
+        dst[e + 3 * st] = v3;
+    }
+    for (; e < n; e += st) dst[e] = __ldg(src + e);
+}
+#endif
+
 }  // namespace octen

@@ -460,6 +460,8 @@ bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
               uint32_t box_inner, uint32_t box_outer) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return false;
+    // keep every extent and stride a whole number of 16-byte units
+    if ((inner * 4) % 16 != 0 || row_bytes % 16 != 0) return false;
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {row_bytes};
     cuuint32_t box[2] = {box_inner, box_outer};
@@ -491,8 +493,10 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
         ((uintptr_t)Alo % 16) != 0 || N > (1LL << 31) - 1 || M <= 0 || N <= 0 || K <= 0)
         return false;
     CUtensorMap mhi, mlo, mx;
-    if (!make_map(&mhi, Ahi, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 4, BK, BM)) return false;
-    if (!make_map(&mlo, Alo, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 4, BK, BM)) return false;
+    // inner extents in whole 16-byte units: the zero padding of A (lda >= K)
+    // stands in for the tail (X's own extent is K, TMA zero-fills past it)
+    if (!make_map(&mhi, Ahi, (uint64_t)lda, (uint64_t)M, (uint64_t)lda * 4, BK, BM)) return false;
+    if (!make_map(&mlo, Alo, (uint64_t)lda, (uint64_t)M, (uint64_t)lda * 4, BK, BM)) return false;
     if (!make_map(&mx, X, (uint64_t)K, (uint64_t)N, (uint64_t)K * 4, BK, BN)) return false;
     const size_t smem = STAGES * STAGE_BYTES + 1024 + 256;
     static bool attr = false;
@@ -511,13 +515,16 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
 bool tc_mode2_tf32x3(const float* Z1, long long N1, int J, int tc, const float* Vhi, const float* Vlo, int ldv, int P,
                      int Q, float* Z2, cudaStream_t st) {
     if (!tc_gemm_available()) return false;
-    if (Q > M2_BN || Q < 1 || (N1 % 4) != 0 || (ldv % 4) != 0 || ((uintptr_t)Z1 % 16) != 0 ||
+    // the A box of slice k starts at column k J: TMA needs that inner
+    // coordinate on a 16-byte boundary, hence J % 4 == 0
+    if (Q > M2_BN || Q < 1 || (J % 4) != 0 || (N1 % 4) != 0 || (ldv % 4) != 0 || ((uintptr_t)Z1 % 16) != 0 ||
         ((uintptr_t)Vhi % 16) != 0 || ((uintptr_t)Vlo % 16) != 0 || (long long)P * tc > 2147483647LL)
         return false;
     CUtensorMap mz, mh, ml;
     if (!make_map(&mz, Z1, (uint64_t)N1, (uint64_t)P * Q, (uint64_t)N1 * 4, BK, BM)) return false;
-    if (!make_map(&mh, Vhi, (uint64_t)J, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, M2_BN)) return false;
-    if (!make_map(&ml, Vlo, (uint64_t)J, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, M2_BN)) return false;
+    // inner extent ldv (zero-padded past J, a whole number of 16-byte units)
+    if (!make_map(&mh, Vhi, (uint64_t)ldv, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, M2_BN)) return false;
+    if (!make_map(&ml, Vlo, (uint64_t)ldv, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, M2_BN)) return false;
     const size_t smem = M2_STAGES * M2_STAGE_BYTES + 1024 + 256;
     static bool attr = false;
     if (!attr) {
