@@ -109,7 +109,7 @@ __global__ void als_norm_finish_kernel(AlsDev d, const double* part, int nc) {
 
 // Jacobi eigen-decomposition of the two Gram matrices of replica p, top-R
 // eigenvectors into Ur[p][which] (descending eigenvalue), usability flag.
-__global__ void __launch_bounds__(1024) gevd_eig_sym_kernel(AlsDev d, int v_in_smem, int mblk) {
+__global__ void __launch_bounds__(256) gevd_eig_sym_kernel(AlsDev d, int v_in_smem, int mblk) {
     extern __shared__ double sm[];
     const int p = blockIdx.x / 2, which = blockIdx.x % 2;
     const int Q = d.Q, R = d.R;
@@ -315,19 +315,8 @@ __global__ void gevd_hsolve_kernel(AlsDev d) {
             for (int k = (i > j ? i : j); k < R; ++k) sacc += Li[k + R * i] * Li[k + R * j];
             Vp[e] = sacc;
         }
-        __syncthreads();
-        for (size_t k = threadIdx.x; k < d.q2(); k += blockDim.x) {
-            double x[64], y[64];
-            for (int i = 0; i < R; ++i) x[i] = h[(size_t)R * k + i];
-            for (int i = 0; i < R; ++i) {
-                double sacc = 0.0;
-                for (int j = 0; j < R; ++j) sacc += Vp[i + R * j] * x[j];
-                y[i] = sacc;
-            }
-            for (int i = 0; i < R; ++i) h[(size_t)R * k + i] = y[i];
-        }
     } else {
-        // minimum-norm fallback: pseudo-inverse from the eigen-decomposition
+        // minimum-norm fallback: Vp <- pseudo-inverse from the eigen-decomposition
         double* Ev = d.gscr + (size_t)prob * (6 * R * R + 4 * R);
         TeamDev team;
         jacobi_eig_sym(team, R, Vp, Ev, cs, flag);
@@ -335,20 +324,41 @@ __global__ void gevd_hsolve_kernel(AlsDev d) {
         double wmax = 0.0;
         for (int i = 0; i < R; ++i) wmax = fmax(wmax, fabs(Vp[i + R * i]));
         const double thr = kEps * R * wmax;
-        for (size_t k = threadIdx.x; k < d.q2(); k += blockDim.x) {
-            double x[64], y[64];
-            for (int i = 0; i < R; ++i) x[i] = h[(size_t)R * k + i];
-            for (int i = 0; i < R; ++i) y[i] = 0.0;
-            for (int e = 0; e < R; ++e) {
-                const double w = Vp[e + R * e];
-                if (!(w > thr)) continue;
-                double dot = 0.0;
-                for (int i = 0; i < R; ++i) dot += Ev[i + R * e] * x[i];
-                dot /= w;
-                for (int i = 0; i < R; ++i) y[i] += Ev[i + R * e] * dot;
+        for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+            const int i = e % R, j = e / R;
+            double sacc = 0.0;
+            for (int k = 0; k < R; ++k) {
+                const double w = Vp[k + R * k];
+                if (w > thr) sacc += Ev[i + R * k] * Ev[j + R * k] / w;
             }
-            for (int i = 0; i < R; ++i) h[(size_t)R * k + i] = y[i];
+            Li[e] = sacc;
         }
+        __syncthreads();
+        for (int e = threadIdx.x; e < R * R; e += blockDim.x) Vp[e] = Li[e];
+    }
+    __syncthreads();
+    // h <- Vp h, column chunks of blockDim staged in shared memory (rows of h
+    // are contiguous: coalesced loads and stores; in place per chunk)
+    double* xs = cs + 2 * (R + 2) + (R + 8);  // R x (blockDim + 1), past the Jacobi flag ints
+    const int nc = blockDim.x, ldx = nc + 1;
+    const size_t q2 = d.q2();
+    for (size_t k0 = 0; k0 < q2; k0 += nc) {
+        const int c = threadIdx.x;
+        const bool ok = k0 + c < q2;
+        for (int j = 0; j < R; ++j) xs[c + (size_t)ldx * j] = ok ? h[(size_t)j * q2 + k0 + c] : 0.0;
+        __syncthreads();
+        if (ok)
+            for (int i = 0; i < R; ++i) {
+                double s0 = 0.0, s1 = 0.0;
+                int j = 0;
+                for (; j + 1 < R; j += 2) {
+                    s0 += Vp[i + R * j] * xs[c + (size_t)ldx * j];
+                    s1 += Vp[i + R * (j + 1)] * xs[c + (size_t)ldx * (j + 1)];
+                }
+                if (j < R) s0 += Vp[i + R * j] * xs[c + (size_t)ldx * j];
+                h[(size_t)i * q2 + k0 + c] = s0 + s1;
+            }
+        __syncthreads();
     }
 }
 
@@ -363,7 +373,7 @@ __global__ void gevd_peel_kernel(AlsDev d) {
     double* v = u + Q;                  // Q
     double* red = v + Q;                // blockDim + 2 + Q
     const double* h = d.Hh + (size_t)prob * R * d.q2();
-    for (int e = threadIdx.x; e < Q * Q; e += blockDim.x) H[e] = h[r + (size_t)R * e];
+    g2s_copy(H, h + (size_t)r * d.q2(), Q * Q);
     __syncthreads();
     TeamDev team;
     const double sigma = top_singular_pair(team, Q, Q, H, u, v, red);
@@ -634,8 +644,18 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
         const int i = e % R, j = e / R;
         if (i > j) continue;
-        double s = 0.0;
-        for (int q = 0; q < Q; ++q) s += raw[q + Q * i] * raw[q + Q * j];
+        const double* ri = raw + Q * i;
+        const double* rj = raw + Q * j;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int q = 0;
+        for (; q + 3 < Q; q += 4) {
+            s0 += ri[q] * rj[q];
+            s1 += ri[q + 1] * rj[q + 1];
+            s2 += ri[q + 2] * rj[q + 2];
+            s3 += ri[q + 3] * rj[q + 3];
+        }
+        for (; q < Q; ++q) s0 += ri[q] * rj[q];
+        const double s = (s0 + s1) + (s2 + s3);
         g[i + R * j] = s;
         g[j + R * i] = s;
     }
@@ -875,11 +895,11 @@ struct Y0Bp {  // B(prob, a, k) = Y[p][a + Q k]
         return Y[(size_t)(prob / S) * q3 + a + (size_t)Q * k];
     }
 };
-struct HStore {
+struct HStore {  // H[prob][r][k]: row r of h contiguous (the peel reads H_r = h(r, :) whole)
     double* H;
     int R;
     size_t q2;
-    __device__ void operator()(int prob, int r, int k, double v) const { H[(size_t)prob * R * q2 + r + (size_t)R * k] = v; }
+    __device__ void operator()(int prob, int r, int k, double v) const { H[(size_t)prob * R * q2 + (size_t)r * q2 + k] = v; }
 };
 
 }  // namespace
@@ -1036,7 +1056,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         const int mblk = std::min(Q, R + 8);
         const int use_sub = (Q >= 2 * mblk && (size_t)2 * Q * mblk + 2 * mblk * mblk + mblk <= q2) ? mblk : 0;
         OCTEN_CUDA(cudaFuncSetAttribute(gevd_eig_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eig));
-        gevd_eig_sym_kernel<<<P * 2, 1024, smem_eig, st>>>(d, v_in_smem, use_sub); OCTEN_LAUNCHED(1);
+        gevd_eig_sym_kernel<<<P * 2, 256, smem_eig, st>>>(d, v_in_smem, use_sub); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
         // mixtures -> p1/p2 for all attempts
         gemm_f64<false, true>(NP, (int)q2, 6, Q, YmatA{dY, q3, q2, S, true}, MixB{Wmix.p, Q},
@@ -1061,7 +1081,8 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             OCTEN_CUDA(cudaGetLastError());
             gemm_f64<false, false>(NP, R, (int)q2, Q, A1tA{F.p, Q, R}, Y0Bp{dY, q3, Q, S},
                                                     HStore{Hh.p, R, q2}, st);
-            const size_t smem_h = (size_t)(3 * R * R + 2 * (R + 2)) * sizeof(double) + (R + 8) * sizeof(int) + 16;
+            const size_t smem_h = (size_t)(3 * R * R + 2 * (R + 2) + (R + 8) + (size_t)R * 257) * sizeof(double) + 16;
+            OCTEN_CUDA(cudaFuncSetAttribute(gevd_hsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_h));
             gevd_hsolve_kernel<<<NP, 256, smem_h, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
             const int peel_threads = 128;

@@ -52,8 +52,8 @@ __global__ void chol_maxdiag_kernel(const double* A, int n, int lda, long long s
 // so one step costs two barriers and ~9 FMAs per thread.  A pivot
 // <= tol * maxdiag is dead: its column of L and row of L^-1 become zero and
 // the rank is decremented.
-constexpr int kDiagThreads = 512;
-constexpr int kDiagPer = (kCholNB * (kCholNB + 1) / 2 + kDiagThreads - 1) / kDiagThreads;  // 5
+constexpr int kDiagThreads = 1024;
+constexpr int kDiagPer = (kCholNB * (kCholNB + 1) / 2 + kDiagThreads - 1) / kDiagThreads;  // 3
 
 // Branch-free form of the updates: colk[i] is zero for i <= k and rowk[j] is
 // zero for j > k (both start zeroed; step k zeroes colk[k] and writes rowk

@@ -167,6 +167,7 @@ public:
     DevBuf<int> lp_ok[2];    // P
     bool pair_solve = false;
     DevBuf<double> solved[2], Gw, rhs, tmp, tg, red, sw, sw2, maxdiag, RF, SC, sims, tscr;
+    DevBuf<double> kws;  // split-K partials
     DevBuf<int> ranks, perms, iscr;
     DevBuf<DevStatus> err;
     std::vector<int> last_perm;

@@ -88,6 +88,20 @@ struct YtA2 {  // A(p, c, k) = Y[p][k + Q^2 c]
     __device__ double operator()(int p, int c, int k) const { return Y[(size_t)p * q3 + k + q2 * c]; }
 };
 
+// Small-output, long-K GEMMs of the merge (d x R right-hand sides with
+// K = P*Q, per-replica Q x R projections with K = d): split K so the launch
+// fills the GPU; deterministic fixed-order reduction (gemm_splitk_reduce).
+template <bool A_KFAST, bool B_KFAST, class AF, class BF, class CF>
+void gemm_f64_splitk(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaStream_t st, DevBuf<double>& ws) {
+    const int ks = pick_ksplit(batches, M, N, K, 296, 64);
+    if (ks > 1) ws.reserve((size_t)batches * ks * M * N);
+    gemm_f64<A_KFAST, B_KFAST>(batches, M, N, K, af, bf, cf, st, ks, ks > 1 ? ws.p : nullptr);
+}
+
+}  // namespace
+
+namespace {
+
 __device__ void set_err(DevStatus* e, int code, int problem, int a, int b, int c, double d = 0.0) {
     e->code = code;
     e->problem = problem;
@@ -1007,8 +1021,8 @@ void MergeEngine::solve_nontemporal(int n, const double* dStack, double* dOut, c
     if (sum_rank[n] < d)
         throw NumericError("recover: rank-deficient projection on mode " + std::to_string(n + 1) + " (rank " +
                            std::to_string(sum_rank[n]) + " of " + std::to_string(d) + ")");
-    gemm_f64<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{dStack, PQ, 0},
-                                           StoreCM{dOut, d, 0}, st);
+    gemm_f64_splitk<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{dStack, PQ, 0},
+                                           StoreCM{dOut, d, 0}, st, kws);
     chol_solve_blocked(Lsum[n].p, (int)d, (int)d, 0, Lsum_inv[n], dOut, (int)d, 0, R, 1, st);
 }
 
@@ -1021,10 +1035,10 @@ void MergeEngine::temporal_stack(const double* dY, int p0, int pl, const double*
     double* Vt = tg.p + (size_t)pl * Q * R;
     const double* U0 = Ud[0].p + (size_t)p0 * dims[0] * Q;
     const double* V0 = Ud[1].p + (size_t)p0 * dims[1] * Q;
-    gemm_f64<true, true>(pl, Q, R, (int)dims[0], UtA{U0, dims[0], Q}, ColB{dA, dims[0], 0},
-                                          StoreCM{Ut, Q, (long long)Q * R}, st);
-    gemm_f64<true, true>(pl, Q, R, (int)dims[1], UtA{V0, dims[1], Q}, ColB{dB, dims[1], 0},
-                                          StoreCM{Vt, Q, (long long)Q * R}, st);
+    gemm_f64_splitk<true, true>(pl, Q, R, (int)dims[0], UtA{U0, dims[0], Q}, ColB{dA, dims[0], 0},
+                                          StoreCM{Ut, Q, (long long)Q * R}, st, kws);
+    gemm_f64_splitk<true, true>(pl, Q, R, (int)dims[1], UtA{V0, dims[1], Q}, ColB{dB, dims[1], 0},
+                                          StoreCM{Vt, Q, (long long)Q * R}, st, kws);
     tmp.reserve((size_t)pl * Q * R);
     const int ks = pick_ksplit(pl, Q, R, (int)q2);
     tscr.reserve((size_t)pl * ks * Q * R);
@@ -1059,10 +1073,10 @@ void MergeEngine::temporal_append(const double* dTstack, const double* dW, std::
     DevBuf<double> linvc;
     chol_batched(Gc.p, (int)t, (int)t, 0, 1, kGramRankTol, md.p, rk.p, linvc, st);
     // [bv | hv] = Pc^T [tstack | hist]
-    gemm_f64<false, true>(1, (int)t, R, (int)PQ, UcatA{dW, t, 0}, ColB{dTstack, PQ, 0},
-                                           StoreCM{BZ.p, t, 0}, st);
-    gemm_f64<false, true>(1, (int)t, R, (int)PQ, UcatA{dW, t, 0}, ColB{dHist, PQ, 0},
-                                           StoreCM{BZ.p + (size_t)t * R, t, 0}, st);
+    gemm_f64_splitk<false, true>(1, (int)t, R, (int)PQ, UcatA{dW, t, 0}, ColB{dTstack, PQ, 0},
+                                           StoreCM{BZ.p, t, 0}, st, kws);
+    gemm_f64_splitk<false, true>(1, (int)t, R, (int)PQ, UcatA{dW, t, 0}, ColB{dHist, PQ, 0},
+                                           StoreCM{BZ.p + (size_t)t * R, t, 0}, st, kws);
     DevBuf<double> hv;
     hv.reserve((size_t)t * R);
     OCTEN_CUDA(cudaMemcpyAsync(hv.p, BZ.p + (size_t)t * R, sizeof(double) * t * R, cudaMemcpyDeviceToDevice, st));
@@ -1119,8 +1133,8 @@ void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, dou
         for (int n = 0; n < 2; ++n) {
             const long long d = dims[n];
             // tg[p][n] = U_p^T solved_n  (Q x R)
-            gemm_f64<true, true>(P, Q, R, (int)d, UtA{Ud[n].p, d, Q}, ColB{solved[n].p, d, 0},
-                                                  StoreCM{tg.p + (size_t)n * Q * R, Q, 2LL * Q * R}, st);
+            gemm_f64_splitk<true, true>(P, Q, R, (int)d, UtA{Ud[n].p, d, Q}, ColB{solved[n].p, d, 0},
+                                                  StoreCM{tg.p + (size_t)n * Q * R, Q, 2LL * Q * R}, st, kws);
         }
         const size_t smem = (size_t)(4 * Q * R + R) * sizeof(double);
         OCTEN_CUDA(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1153,8 +1167,8 @@ void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, dou
                 scale_stack_kernel<<<grid_for((size_t)PQ * R), 256, 0, st>>>(P, Q, R, stacks.p + (size_t)n * PQ * R,
                                                                             w.p, sw.p);
                 OCTEN_LAUNCHED(1);
-                gemm_f64<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{sw.p, PQ, 0},
-                                      StoreCM{sw2.p + (size_t)mi * R * d, d, 0}, st);
+                gemm_f64_splitk<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{sw.p, PQ, 0},
+                                      StoreCM{sw2.p + (size_t)mi * R * d, d, 0}, st, kws);
             }
             chol_batched(Gw.p, (int)d, (int)d, d * d, nb, kGramRankTol, maxdiag.p, ranks.p, Gw_inv, st);
             std::vector<int> rk = ranks.to_host(nb, st);

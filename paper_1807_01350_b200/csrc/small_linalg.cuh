@@ -387,22 +387,28 @@ __device__ inline int block_greedy_match(int r, const double* sim, int ld, doubl
 // threads apply the rank-1 updates to their own elements (two barriers per
 // step, no serial warp).  A pivot <= thr is dead: column k of L and row k of
 // L^-1 become zero.  a (ld lda) is read only; l (ld ldl, lower; upper zeroed)
-// and x (ld ldx, lower; upper zeroed) are written.  scratch: 2 * 64 + 2
-// doubles of shared memory.  Returns the rank (all threads).
+// and x (ld ldx, lower; upper zeroed) are written.  Returns the rank (all
+// threads).
 // ---------------------------------------------------------------------------
-__device__ inline int block_chol_inv64(const double* a, int lda, int n, double thr, double* l, int ldl, double* x,
+template <int kPer>
+__device__ inline int block_chol_inv_t(const double* a, int lda, int n, double thr, double* l, int ldl, double* x,
                                        int ldx, double* scratch) {
-    constexpr int kPer = 9;  // ceil(64 * 65 / 2 / 256)
-    double* colk = scratch;
-    double* rowk = scratch + 64;
-    double* shv = scratch + 128;  // [0] reciprocal pivot, [1] dead count
+    // branch-free updates: colk[i] = 0 for i <= k, rowk[j] = 0 for j > k;
+    // unused slots point at the zero entries colk[64] / rowk[64]
+    double* colk = scratch;        // 65
+    double* rowk = scratch + 65;   // 65
+    double* shv = scratch + 130;   // [0..1] reciprocal pivots (double-buffered), [2] dead count
     const int tid = threadIdx.x;
     double av[kPer], bv[kPer];
     int iv[kPer], jv[kPer];
-    if (tid == 0) shv[1] = 0.0;
+    if (tid <= 64) {
+        colk[tid] = 0.0;
+        rowk[tid] = 0.0;
+    }
+    if (tid == 0) shv[2] = 0.0;
 #pragma unroll
     for (int s = 0; s < kPer; ++s) {
-        const int e = tid + 256 * s;
+        const int e = tid + (int)blockDim.x * s;
         int i = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
         while ((i + 1) * (i + 2) / 2 <= e) ++i;
         while (i * (i + 1) / 2 > e) --i;
@@ -413,44 +419,51 @@ __device__ inline int block_chol_inv64(const double* a, int lda, int n, double t
         av[s] = ok ? a[i + (size_t)lda * j] : 0.0;
         bv[s] = (ok && i == j) ? 1.0 : 0.0;
     }
+    auto pivot = [&](int k) {
+        const int ed = k * (k + 3) / 2;
+        if (tid == ed % (int)blockDim.x) {
+            const int sd = ed / (int)blockDim.x;
+#pragma unroll
+            for (int s = 0; s < kPer; ++s)
+                if (s == sd) {
+                    const double d = av[s];
+                    const bool dead = !(d > thr);
+                    const double rp = dead ? 0.0 : rsqrt(d);
+                    av[s] = dead ? 0.0 : d * rp;
+                    shv[k & 1] = rp;
+                    if (dead) shv[2] += 1.0;
+                }
+        }
+    };
+    __syncthreads();
+    if (n > 0) pivot(0);
     __syncthreads();
     for (int k = 0; k < n; ++k) {
-#pragma unroll
-        for (int s = 0; s < kPer; ++s)
-            if (iv[s] == k && jv[s] == k) {
-                const double d = av[s];
-                const bool dead = !(d > thr);
-                const double piv = dead ? 0.0 : sqrt(d);
-                av[s] = piv;
-                shv[0] = dead ? 0.0 : 1.0 / piv;
-                if (dead) shv[1] += 1.0;
-            }
-        __syncthreads();
-        const double rp = shv[0];
-#pragma unroll
-        for (int s = 0; s < kPer; ++s) {
-            if (jv[s] == k && iv[s] > k && iv[s] < 64) {
-                av[s] *= rp;
-                colk[iv[s]] = av[s];
-            }
-            if (iv[s] == k) {
-                bv[s] *= rp;
-                rowk[jv[s]] = bv[s];
-            }
-        }
-        __syncthreads();
+        const double rp = shv[k & 1];
 #pragma unroll
         for (int s = 0; s < kPer; ++s) {
             const int i = iv[s], j = jv[s];
-            if (i < 64 && i > k) {
-                if (j > k)
-                    av[s] -= colk[i] * colk[j];
-                else
-                    bv[s] -= colk[i] * rowk[j];
+            if (j == k && i > k) {
+                av[s] *= rp;
+                colk[i] = av[s];
+            }
+            if (i == k) {
+                bv[s] *= rp;
+                rowk[j] = bv[s];
             }
         }
+        if (tid == 0) colk[k] = 0.0;
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < kPer; ++s) {
+            const double ci = colk[iv[s]];
+            av[s] -= ci * colk[jv[s]];
+            bv[s] -= ci * rowk[jv[s]];
+        }
+        if (k + 1 < n) pivot(k + 1);
+        __syncthreads();
     }
-    for (int e = tid; e < n * n; e += 256) {
+    for (int e = tid; e < n * n; e += blockDim.x) {
         const int i = e % n, j = e / n;
         if (i < j) {
             l[i + (size_t)ldl * j] = 0.0;
@@ -464,7 +477,21 @@ __device__ inline int block_chol_inv64(const double* a, int lda, int n, double t
             x[iv[s] + (size_t)ldx * jv[s]] = bv[s];
         }
     __syncthreads();
-    return n - (int)shv[1];
+    return n - (int)shv[2];
+}
+
+// Block-cooperative semi-definite Cholesky with the inverse of the factor,
+// n <= 64 (see block_chol_inv_t): every thread keeps ceil(n(n+1)/2 /
+// blockDim) elements of the packed lower triangles of A (-> L) and I
+// (-> L^-1) in registers; the pivot of step k+1 is formed by its owner
+// during step k.  scratch: 133 doubles of shared memory.
+__device__ inline int block_chol_inv64(const double* a, int lda, int n, double thr, double* l, int ldl, double* x,
+                                       int ldx, double* scratch) {
+    const int per = (n * (n + 1) / 2 + (int)blockDim.x - 1) / (int)blockDim.x;
+    if (per <= 1) return block_chol_inv_t<1>(a, lda, n, thr, l, ldl, x, ldx, scratch);
+    if (per <= 3) return block_chol_inv_t<3>(a, lda, n, thr, l, ldl, x, ldx, scratch);
+    if (per <= 5) return block_chol_inv_t<5>(a, lda, n, thr, l, ldl, x, ldx, scratch);
+    return block_chol_inv_t<9>(a, lda, n, thr, l, ldl, x, ldx, scratch);
 }
 #endif
 

@@ -159,7 +159,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t* tmem_slot = (uint32_t*)(done_bar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m_tile = blockIdx.y, n_tile = blockIdx.x;
+    // m-tiles fastest: the CTAs sharing one X slab (all m-tiles of an n-tile)
+    // run back to back, so X comes from DRAM once and from L2 thereafter
+    const int m_tile = blockIdx.x, n_tile = blockIdx.y;
     const int m0 = m_tile * BM;
     const long long n0 = (long long)n_tile * BN;
     const int num_kb = (K + BK - 1) / BK;
@@ -504,7 +506,8 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
         OCTEN_CUDA(cudaFuncSetAttribute(tc_gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+    if ((N + BN - 1) / BN > 65535) return false;
+    dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
     tc_gemm_tf32x3_kernel<<<grid, NUM_THREADS, smem, st>>>(mhi, mlo, mx, Z, M, N, K, N, scatter_p, scatter_q,
                                                            scatter_sh);
     OCTEN_LAUNCHED(1);
