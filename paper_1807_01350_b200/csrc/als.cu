@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -59,6 +61,7 @@ struct AlsDev {
     double* Tmp6;
     double* Pm;
     double* Hh;
+    int* eigdbg;  // [0] subspace fallbacks to Jacobi (diagnostics)
     double* gscr;
     int* usable;
     int* att_start;
@@ -142,6 +145,7 @@ __global__ void __launch_bounds__(256) gevd_eig_sym_kernel(AlsDev d, int v_in_sm
             return;
         }
         // no usable gap at R: full Jacobi below (A is untouched)
+        if (threadIdx.x == 0) atomicAdd(&d.eigdbg[0], 1);
     }
     jacobi_eig_sym(team, Q, A, V, cs, iw);
     __syncthreads();
@@ -337,29 +341,9 @@ __global__ void gevd_hsolve_kernel(AlsDev d) {
         for (int e = threadIdx.x; e < R * R; e += blockDim.x) Vp[e] = Li[e];
     }
     __syncthreads();
-    // h <- Vp h, column chunks of blockDim staged in shared memory (rows of h
-    // are contiguous: coalesced loads and stores; in place per chunk)
-    double* xs = cs + 2 * (R + 2) + (R + 8);  // R x (blockDim + 1), past the Jacobi flag ints
-    const int nc = blockDim.x, ldx = nc + 1;
-    const size_t q2 = d.q2();
-    for (size_t k0 = 0; k0 < q2; k0 += nc) {
-        const int c = threadIdx.x;
-        const bool ok = k0 + c < q2;
-        for (int j = 0; j < R; ++j) xs[c + (size_t)ldx * j] = ok ? h[(size_t)j * q2 + k0 + c] : 0.0;
-        __syncthreads();
-        if (ok)
-            for (int i = 0; i < R; ++i) {
-                double s0 = 0.0, s1 = 0.0;
-                int j = 0;
-                for (; j + 1 < R; j += 2) {
-                    s0 += Vp[i + R * j] * xs[c + (size_t)ldx * j];
-                    s1 += Vp[i + R * (j + 1)] * xs[c + (size_t)ldx * (j + 1)];
-                }
-                if (j < R) s0 += Vp[i + R * j] * xs[c + (size_t)ldx * j];
-                h[(size_t)i * q2 + k0 + c] = s0 + s1;
-            }
-        __syncthreads();
-    }
+    // Vp to global: h <- Vp h runs next as a batched GEMM (gevd_hsolve)
+    double* vg = d.gscr + (size_t)prob * (6 * R * R + 4 * R) + 3 * R * R;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) vg[e] = Vp[e];
 }
 
 // Rank-1 peel of every h row (cp_als.cpp:168-173): H_r(b,c) = h(r, b + Q c).
@@ -372,7 +356,7 @@ __global__ void gevd_peel_kernel(AlsDev d) {
     double* u = H + (size_t)Q * Q;      // Q
     double* v = u + Q;                  // Q
     double* red = v + Q;                // blockDim + 2 + Q
-    const double* h = d.Hh + (size_t)prob * R * d.q2();
+    const double* h = d.KR + (size_t)prob * R * d.q2();  // h2 = Vp h (gevd_hsolve + GEMM)
     g2s_copy(H, h + (size_t)r * d.q2(), Q * Q);
     __syncthreads();
     TeamDev team;
@@ -895,6 +879,19 @@ struct Y0Bp {  // B(prob, a, k) = Y[p][a + Q k]
         return Y[(size_t)(prob / S) * q3 + a + (size_t)Q * k];
     }
 };
+struct VpA {  // A(prob, i, j) = Vp[prob][i + R j]   (the R x R solve operator)
+    const double* G;
+    int R;
+    __device__ double operator()(int prob, int i, int j) const {
+        return G[(size_t)prob * (6 * R * R + 4 * R) + 3 * R * R + i + (size_t)R * j];
+    }
+};
+struct HrowB {  // B(prob, j, k) = H[prob][j][k]
+    const double* H;
+    int R;
+    size_t q2;
+    __device__ double operator()(int prob, int j, int k) const { return H[(size_t)prob * R * q2 + (size_t)j * q2 + k]; }
+};
 struct HStore {  // H[prob][r][k]: row r of h contiguous (the peel reads H_r = h(r, :) whole)
     double* H;
     int R;
@@ -996,6 +993,9 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     d.Tmp6 = Tmp6.p;
     d.Pm = Pm.p;
     d.Hh = Hh.p;
+    eigdbg.reserve(4);
+    eigdbg.zero(4, st);
+    d.eigdbg = eigdbg.p;
     d.gscr = gscr.p;
     d.usable = usable.p;
     d.att_start = att_start.p;
@@ -1081,10 +1081,12 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             OCTEN_CUDA(cudaGetLastError());
             gemm_f64<false, false>(NP, R, (int)q2, Q, A1tA{F.p, Q, R}, Y0Bp{dY, q3, Q, S},
                                                     HStore{Hh.p, R, q2}, st);
-            const size_t smem_h = (size_t)(3 * R * R + 2 * (R + 2) + (R + 8) + (size_t)R * 257) * sizeof(double) + 16;
+            const size_t smem_h = (size_t)(3 * R * R + 2 * (R + 2) + (R + 8)) * sizeof(double) + 16;
             OCTEN_CUDA(cudaFuncSetAttribute(gevd_hsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_h));
             gevd_hsolve_kernel<<<NP, 256, smem_h, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
+            // h2 = Vp h into the KR scratch (same size, unused before the sweeps)
+            gemm_f64<false, false>(NP, R, (int)q2, R, VpA{gscr.p, R}, HrowB{Hh.p, R, q2}, HStore{KR.p, R, q2}, st);
             const int peel_threads = 128;
             const size_t smem_peel = (q2 + 2 * Q + peel_threads + 2 + Q) * sizeof(double);
             OCTEN_CUDA(cudaFuncSetAttribute(gevd_peel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_peel));
@@ -1173,6 +1175,10 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         }
     }
     last_sweeps = sweep;
+    if (std::getenv("OCTEN_DEBUG_ALS")) {
+        const std::vector<int> ed = eigdbg.to_host(1, st);
+        std::fprintf(stderr, "octen als: %d problems, %d sweeps, %d GEVD eigen fallbacks\n", NP, sweep, ed[0]);
+    }
     cudaFreeHost(hcount);
 
     // ---- errors (lowest replica, then restart, wins)

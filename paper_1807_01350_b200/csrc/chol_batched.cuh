@@ -42,125 +42,132 @@ __global__ void chol_maxdiag_kernel(const double* A, int n, int lda, long long s
 }
 
 // Factor the nb x nb diagonal block at offset k0 of every matrix and invert
-// it (for the panel GEMM and the blocked solves), fused in one right-looking
-// sweep.  Every thread keeps a fixed share of the packed lower triangle of
-// both the block (A -> L) and of B (I -> L^-1) in registers; step k publishes
-// column k of L and row k of L^-1 through shared memory and every thread
-// applies the rank-1 updates to its own elements:
-//   A(i,j) -= L(i,k) L(j,k)      (j > k)        -- Cholesky trailing update
-//   B(i,j) -= L(i,k) X(k,j)      (j <= k < i)   -- forward substitution
-// so one step costs two barriers and ~9 FMAs per thread.  A pivot
-// <= tol * maxdiag is dead: its column of L and row of L^-1 become zero and
-// the rank is decremented.
-constexpr int kDiagThreads = 1024;
-constexpr int kDiagPer = (kCholNB * (kCholNB + 1) / 2 + kDiagThreads - 1) / kDiagThreads;  // 3
+// it (for the panel GEMM and the blocked solves) as a 2 x 2 block of 32 x 32
+// halves:
+//   L11 = chol(A11), X11 = L11^-1            (block_chol_inv_t, registers)
+//   L21 = A21 X11^T;  A22 -= L21 L21^T        (shared-memory products)
+//   L22 = chol(A22), X22 = L22^-1
+//   X21 = -X22 L21 X11
+// The fused register factorizations cost two barriers per column and touch
+// only 528 elements (one or two per thread), so the 64 sequential steps are
+// cheap; the coupling products are fully parallel.  A pivot <= tol * maxdiag
+// is dead: its column of L and row of L^-1 become zero and the rank drops.
+constexpr int kDiagThreads = 128;
+constexpr int kHalf = kCholNB / 2;
+constexpr int kDLD = kCholNB + 1;  // shared leading dimension
+constexpr size_t kDiagSmem = (size_t)(2 * kCholNB * kDLD + kHalf * (kHalf + 1) + 160) * sizeof(double);
 
-// Branch-free form of the updates: colk[i] is zero for i <= k and rowk[j] is
-// zero for j > k (both start zeroed; step k zeroes colk[k] and writes rowk
-// only up to k), so every owned element applies
-//   A(i,j) -= colk[i] colk[j];  B(i,j) -= colk[i] rowk[j]
-// unconditionally and the products vanish outside the trailing / forward
-// ranges.  Unused slots point at row/column 64 (zero entries).
 __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int n, int lda, long long sA, int k0,
                                                                  double tol, const double* maxdiag, int* rank,
                                                                  double* Linv, int nblk) {
-    __shared__ double colk[kCholNB + 1], rowk[kCholNB + 1];
-    __shared__ double shv_rp[2];
-    __shared__ int sh_dead;
+    extern __shared__ double diag_smem[];
+    double* S = diag_smem;                  // A -> L (lower), column-major, ld kDLD
+    double* X = S + kCholNB * kDLD;         // L^-1 (lower)
+    double* T = X + kCholNB * kDLD;         // kHalf x (kHalf + 1)
+    double* scr = T + kHalf * (kHalf + 1);  // 160
     double* a = A + (size_t)blockIdx.x * sA;
     const int nb = min(kCholNB, n - k0);
     const int tid = threadIdx.x;
-    double av[kDiagPer], bv[kDiagPer];
-    int iv[kDiagPer], jv[kDiagPer];
-    if (tid <= kCholNB) {
-        colk[tid] = 0.0;
-        rowk[tid] = 0.0;
-    }
-    if (tid == 0) sh_dead = 0;
 #pragma unroll
-    for (int s = 0; s < kDiagPer; ++s) {
-        // packed lower-triangle index e -> (i, j), j <= i (row-major packing)
-        const int e = tid + kDiagThreads * s;
-        int i = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-        while ((i + 1) * (i + 2) / 2 <= e) ++i;
-        while (i * (i + 1) / 2 > e) --i;
-        const int j = e - i * (i + 1) / 2;
-        const bool ok = e < kCholNB * (kCholNB + 1) / 2 && i < nb;
-        iv[s] = ok ? i : kCholNB;
-        jv[s] = ok ? j : kCholNB;
-        av[s] = ok ? a[(k0 + i) + (size_t)lda * (k0 + j)] : 0.0;
-        bv[s] = (ok && i == j) ? 1.0 : 0.0;
+    for (int h = 0; h < 4; ++h) {
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = tid + kDiagThreads * (8 * h + r);
+            const int i = e & (kCholNB - 1), j = e >> 6;
+            v[r] = (i < nb && j < nb && i >= j) ? a[(k0 + i) + (size_t)lda * (k0 + j)] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = tid + kDiagThreads * (8 * h + r);
+            const int i = e & (kCholNB - 1), j = e >> 6;
+            S[i + kDLD * j] = v[r];
+            X[i + kDLD * j] = 0.0;
+        }
     }
     const double md = maxdiag[blockIdx.x];
     const double thr = (md > 0.0) ? tol * md : INFINITY;
-    // The owner of diagonal element (k, k) (packed index k(k+3)/2) turns it
-    // into the pivot as soon as its own update of step k-1 is done, so the
-    // pivot's rsqrt overlaps the other threads' updates: two barriers a step.
-    auto pivot = [&](int k) {
-        const int ed = k * (k + 3) / 2;
-        if (tid == ed % kDiagThreads) {
-            const int sd = ed / kDiagThreads;
-#pragma unroll
-            for (int s = 0; s < kDiagPer; ++s)
-                if (s == sd) {
-                    const double d = av[s];
-                    const bool dead = !(d > thr);
-                    const double rp = dead ? 0.0 : rsqrt(d);
-                    av[s] = dead ? 0.0 : d * rp;
-                    shv_rp[k & 1] = rp;
-                    if (dead) ++sh_dead;
-                }
-        }
-    };
     __syncthreads();
-    pivot(0);
-    __syncthreads();
-    for (int k = 0; k < nb; ++k) {
-        const double rp = shv_rp[k & 1];
-#pragma unroll
-        for (int s = 0; s < kDiagPer; ++s) {
-            const int i = iv[s], j = jv[s];
-            if (j == k && i > k) {  // column k of L (i < 64 for used slots)
-                av[s] *= rp;
-                colk[i] = av[s];
+    const int n1 = min(kHalf, nb);
+    const int rk1 = block_chol_inv_t<5, kDiagThreads>(S, kDLD, n1, thr, S, kDLD, X, kDLD, scr);
+    int dead = n1 - rk1;
+    const int n2 = nb - n1;
+    if (n2 > 0) {
+        double* A21 = S + kHalf;                 // rows 32.., cols 0..31
+        double* A22 = S + kHalf + kDLD * kHalf;  // rows 32.., cols 32..
+        double* X21 = X + kHalf;
+        double* X22 = X + kHalf + kDLD * kHalf;
+        // T = A21 X11^T   (T(i, j) = sum_{k <= j} A21(i, k) X11(j, k))
+        for (int e = tid; e < kHalf * kHalf; e += kDiagThreads) {
+            const int i = e % kHalf, j = e / kHalf;
+            double s0 = 0.0, s1 = 0.0;
+            int k = 0;
+            for (; k + 1 <= j; k += 2) {
+                s0 += A21[i + kDLD * k] * X[j + kDLD * k];
+                s1 += A21[i + kDLD * (k + 1)] * X[j + kDLD * (k + 1)];
             }
-            if (i == k) {  // row k of L^-1
-                bv[s] *= rp;
-                rowk[j] = bv[s];
-            }
+            if (k <= j) s0 += A21[i + kDLD * k] * X[j + kDLD * k];
+            T[i + (kHalf + 1) * j] = (i < n2) ? s0 + s1 : 0.0;
         }
-        if (tid == 0) colk[k] = 0.0;
         __syncthreads();
-#pragma unroll
-        for (int s = 0; s < kDiagPer; ++s) {
-            const double ci = colk[iv[s]];
-            av[s] -= ci * colk[jv[s]];
-            bv[s] -= ci * rowk[jv[s]];
+        for (int e = tid; e < kHalf * kHalf; e += kDiagThreads) {
+            const int i = e % kHalf, j = e / kHalf;
+            A21[i + kDLD * j] = T[i + (kHalf + 1) * j];  // L21
         }
-        if (k + 1 < nb) pivot(k + 1);
+        __syncthreads();
+        // A22 -= L21 L21^T (lower)
+        for (int e = tid; e < kHalf * kHalf; e += kDiagThreads) {
+            const int i = e % kHalf, j = e / kHalf;
+            if (i < j) continue;
+            double s0 = 0.0, s1 = 0.0;
+            for (int k = 0; k < kHalf; k += 2) {
+                s0 += A21[i + kDLD * k] * A21[j + kDLD * k];
+                s1 += A21[i + kDLD * (k + 1)] * A21[j + kDLD * (k + 1)];
+            }
+            A22[i + kDLD * j] -= s0 + s1;
+        }
+        __syncthreads();
+        const int rk2 = block_chol_inv_t<5, kDiagThreads>(A22, kDLD, n2, thr, A22, kDLD, X22, kDLD, scr);
+        dead += n2 - rk2;
+        // X21 = -X22 (L21 X11): T = L21 X11, then X21 = -X22 T
+        for (int e = tid; e < kHalf * kHalf; e += kDiagThreads) {
+            const int i = e % kHalf, j = e / kHalf;
+            double s0 = 0.0, s1 = 0.0;
+            int k = j;
+            for (; k + 1 < kHalf; k += 2) {
+                s0 += A21[i + kDLD * k] * X[k + kDLD * j];
+                s1 += A21[i + kDLD * (k + 1)] * X[k + 1 + kDLD * j];
+            }
+            if (k < kHalf) s0 += A21[i + kDLD * k] * X[k + kDLD * j];
+            T[i + (kHalf + 1) * j] = s0 + s1;
+        }
+        __syncthreads();
+        for (int e = tid; e < kHalf * kHalf; e += kDiagThreads) {
+            const int i = e % kHalf, j = e / kHalf;
+            double s0 = 0.0, s1 = 0.0;
+            int k = 0;
+            for (; k + 1 <= i; k += 2) {
+                s0 += X22[i + kDLD * k] * T[k + (kHalf + 1) * j];
+                s1 += X22[i + kDLD * (k + 1)] * T[k + 1 + (kHalf + 1) * j];
+            }
+            if (k <= i) s0 += X22[i + kDLD * k] * T[k + (kHalf + 1) * j];
+            X21[i + kDLD * j] = -(s0 + s1);
+        }
         __syncthreads();
     }
-    if (tid == 0 && sh_dead) atomicSub(&rank[blockIdx.x], sh_dead);
+    if (tid == 0 && dead) atomicSub(&rank[blockIdx.x], dead);
+    // write back: L (lower of the nb x nb block, upper zeroed) and L^-1
     double* inv = Linv + ((size_t)blockIdx.x * nblk + k0 / kCholNB) * kCholNB * kCholNB;
     for (int e = tid; e < kCholNB * kCholNB; e += kDiagThreads) {
-        const int i = e % kCholNB, j = e / kCholNB;
-        if (i < j) {
-            inv[e] = 0.0;
-            if (i < nb && j < nb) a[(k0 + i) + (size_t)lda * (k0 + j)] = 0.0;
-        } else if (i >= nb) {
-            inv[e] = 0.0;
-        }
-    }
-#pragma unroll
-    for (int s = 0; s < kDiagPer; ++s) {
-        const int i = iv[s], j = jv[s];
-        if (i < kCholNB) {
-            a[(k0 + i) + (size_t)lda * (k0 + j)] = av[s];
-            inv[i + kCholNB * j] = bv[s];
-        }
+        const int i = e & (kCholNB - 1), j = e >> 6;
+        const bool in = i < nb && j < nb;
+        inv[e] = (in && i >= j) ? X[i + kDLD * j] : 0.0;
+        if (in) a[(k0 + i) + (size_t)lda * (k0 + j)] = (i >= j) ? S[i + kDLD * j] : 0.0;
     }
 }
 
+// Rows below the diagonal block: L21 = A21 * L11^-T as an in-place GEMM
+// (one block owns whole rows: N = nb <= BN), dead columns come out zero.
 struct PanelA {
     double* A;
     int lda;
@@ -296,13 +303,15 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
     if (!attr) {
         OCTEN_CUDA(cudaFuncSetAttribute(chol_trail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kTrailSmem));
+        OCTEN_CUDA(cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kDiagSmem));
         attr = true;
     }
     const int nblk = (n + kCholNB - 1) / kCholNB;
     linv.reserve((size_t)batch * nblk * kCholNB * kCholNB);
     chol_maxdiag_kernel<<<batch, 256, 0, st>>>(A, n, lda, sA, maxdiag, rank); OCTEN_LAUNCHED(1);
     for (int k0 = 0; k0 < n; k0 += kCholNB) {
-        chol_diag_kernel<<<batch, kDiagThreads, 0, st>>>(A, n, lda, sA, k0, tol, maxdiag, rank, linv.p, nblk);
+        chol_diag_kernel<<<batch, kDiagThreads, kDiagSmem, st>>>(A, n, lda, sA, k0, tol, maxdiag, rank, linv.p, nblk);
         OCTEN_LAUNCHED(1);
         const int nb = min(kCholNB, n - k0);
         const int rows = n - k0 - nb;

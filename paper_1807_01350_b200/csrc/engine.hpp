@@ -65,7 +65,7 @@ private:
     int P_ = 0, S_ = 0, Q_ = 0, R_ = 0, I_ = 0;
     DevBuf<double> normx2, F, G, lam, T, KR, Mb, fit_hist, res_hist, ws;
     DevBuf<double> Gev, EV, Ur, Wmix, Smix, Tmp6, Pm, Hh, gscr;
-    DevBuf<int> usable, att_start, att_used, todo, peel_fail, active_count;
+    DevBuf<int> usable, att_start, att_used, todo, peel_fail, active_count, eigdbg;
     DevBuf<AlsState> state;
     DevBuf<DevStatus> err;
     DevBuf<Mt64> rngs;

@@ -390,9 +390,10 @@ __device__ inline int block_greedy_match(int r, const double* sim, int ld, doubl
 // and x (ld ldx, lower; upper zeroed) are written.  Returns the rank (all
 // threads).
 // ---------------------------------------------------------------------------
-template <int kPer>
+template <int kPer, int kThreads>
 __device__ inline int block_chol_inv_t(const double* a, int lda, int n, double thr, double* l, int ldl, double* x,
                                        int ldx, double* scratch) {
+    // kThreads == blockDim.x (compile time: the owner arithmetic below divides by it)
     // branch-free updates: colk[i] = 0 for i <= k, rowk[j] = 0 for j > k;
     // unused slots point at the zero entries colk[64] / rowk[64]
     double* colk = scratch;        // 65
@@ -408,7 +409,7 @@ __device__ inline int block_chol_inv_t(const double* a, int lda, int n, double t
     if (tid == 0) shv[2] = 0.0;
 #pragma unroll
     for (int s = 0; s < kPer; ++s) {
-        const int e = tid + (int)blockDim.x * s;
+        const int e = tid + kThreads * s;
         int i = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
         while ((i + 1) * (i + 2) / 2 <= e) ++i;
         while (i * (i + 1) / 2 > e) --i;
@@ -421,8 +422,8 @@ __device__ inline int block_chol_inv_t(const double* a, int lda, int n, double t
     }
     auto pivot = [&](int k) {
         const int ed = k * (k + 3) / 2;
-        if (tid == ed % (int)blockDim.x) {
-            const int sd = ed / (int)blockDim.x;
+        if (tid == ed % kThreads) {
+            const int sd = ed / kThreads;
 #pragma unroll
             for (int s = 0; s < kPer; ++s)
                 if (s == sd) {
@@ -463,7 +464,7 @@ __device__ inline int block_chol_inv_t(const double* a, int lda, int n, double t
         if (k + 1 < n) pivot(k + 1);
         __syncthreads();
     }
-    for (int e = tid; e < n * n; e += blockDim.x) {
+    for (int e = tid; e < n * n; e += kThreads) {
         const int i = e % n, j = e / n;
         if (i < j) {
             l[i + (size_t)ldl * j] = 0.0;
@@ -481,17 +482,18 @@ __device__ inline int block_chol_inv_t(const double* a, int lda, int n, double t
 }
 
 // Block-cooperative semi-definite Cholesky with the inverse of the factor,
-// n <= 64 (see block_chol_inv_t): every thread keeps ceil(n(n+1)/2 /
-// blockDim) elements of the packed lower triangles of A (-> L) and I
+// n <= 64, blockDim.x == 256 (see block_chol_inv_t): every thread keeps
+// ceil(n(n+1)/2 / 256) elements of the packed lower triangles of A (-> L) and I
 // (-> L^-1) in registers; the pivot of step k+1 is formed by its owner
 // during step k.  scratch: 133 doubles of shared memory.
 __device__ inline int block_chol_inv64(const double* a, int lda, int n, double thr, double* l, int ldl, double* x,
                                        int ldx, double* scratch) {
-    const int per = (n * (n + 1) / 2 + (int)blockDim.x - 1) / (int)blockDim.x;
-    if (per <= 1) return block_chol_inv_t<1>(a, lda, n, thr, l, ldl, x, ldx, scratch);
-    if (per <= 3) return block_chol_inv_t<3>(a, lda, n, thr, l, ldl, x, ldx, scratch);
-    if (per <= 5) return block_chol_inv_t<5>(a, lda, n, thr, l, ldl, x, ldx, scratch);
-    return block_chol_inv_t<9>(a, lda, n, thr, l, ldl, x, ldx, scratch);
+    // blockDim.x == 256 (the ALS update kernel)
+    const int per = (n * (n + 1) / 2 + 255) / 256;
+    if (per <= 1) return block_chol_inv_t<1, 256>(a, lda, n, thr, l, ldl, x, ldx, scratch);
+    if (per <= 3) return block_chol_inv_t<3, 256>(a, lda, n, thr, l, ldl, x, ldx, scratch);
+    if (per <= 5) return block_chol_inv_t<5, 256>(a, lda, n, thr, l, ldl, x, ldx, scratch);
+    return block_chol_inv_t<9, 256>(a, lda, n, thr, l, ldl, x, ldx, scratch);
 }
 #endif
 
@@ -1672,11 +1674,12 @@ OCTEN_HD double team_reduce_sum(const Team& team, double v, double* red) {
 template <class Team>
 OCTEN_HD double top_singular_pair(const Team& team, int m, int n, const double* a, double* u, double* v,
                                   double* red, int max_iter = 500) {
-    // start: the row of A with the largest norm (transposed)
-    if (team.tid() == 0) {
-        int best = 0;
+    // start: the row of A with the largest norm (transposed); first row
+    // wins ties.  Row norms in parallel, then a (max, lowest index) reduction.
+    {
         double bn = -1.0;
-        for (int i = 0; i < m; ++i) {
+        int best = 0x7fffffff;
+        for (int i = team.tid(); i < m; i += team.size()) {
             double s = 0.0;
             for (int j = 0; j < n; ++j) s += dsq(a[i + (size_t)m * j]);
             if (s > bn) {
@@ -1684,7 +1687,37 @@ OCTEN_HD double top_singular_pair(const Team& team, int m, int n, const double* 
                 best = i;
             }
         }
-        red[team.size() + 1] = (double)best;
+#if defined(__CUDA_ARCH__)
+        if (team.size() > 1) {
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bn, o);
+                const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+                if (ov > bn || (ov == bn && ob < best)) {
+                    bn = ov;
+                    best = ob;
+                }
+            }
+            const int nw = team.size() >> 5, w = team.tid() >> 5;
+            if ((team.tid() & 31) == 0) {
+                red[2 * w] = bn;
+                red[2 * w + 1] = (double)best;
+            }
+            team.sync();
+            if (team.tid() == 0) {
+                double b = red[0];
+                int bi = (int)red[1];
+                for (int q = 1; q < nw; ++q)
+                    if (red[2 * q] > b || (red[2 * q] == b && (int)red[2 * q + 1] < bi)) {
+                        b = red[2 * q];
+                        bi = (int)red[2 * q + 1];
+                    }
+                red[team.size() + 1] = (double)bi;
+            }
+        } else
+#endif
+        {
+            if (team.tid() == 0) red[team.size() + 1] = (double)best;
+        }
     }
     team.sync();
     const int row = (int)red[team.size() + 1];
@@ -1871,7 +1904,10 @@ OCTEN_HD int subspace_eig_top(const Team& team, int n, const double* a, int k, i
                 h[j + (size_t)m * i] = hij;
             }
             team.sync();
-            jacobi_eig_sym(team, m, h, hv, cs, iw);
+            // 12 sweeps: the top-k pairs converge quadratically in a few; the
+            // trailing noise-level block (|h_pq| at the rounding floor) would
+            // otherwise keep the cyclic sweeps going to the cap
+            jacobi_eig_sym(team, m, h, hv, cs, iw, 12);
             team.sync();
             if (team.tid() == 0) {
                 for (int i = 0; i < m; ++i) order[i] = i;
