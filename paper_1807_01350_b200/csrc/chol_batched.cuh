@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "devbuf.hpp"
 #include "gemm_dmma.cuh"
@@ -205,15 +206,27 @@ struct PanelC {
 constexpr int kTrailLD = kCholNB + 4;
 
 __global__ void __launch_bounds__(256, 2) chol_trail_kernel(double* A, int n, int lda, long long sA, int r0, int k0,
-                                                         int nb) {
+                                                         int nb, int part) {
     extern __shared__ double trail_smem[];
     double* Pi = trail_smem;                       // [64 k][kTrailLD m]
     double* Pj = trail_smem + kCholNB * kTrailLD;  // [64 k][kTrailLD m]
+    // part 0: every lower tile; 1: tile column tj = 0 only (the next panel
+    // column, on the critical path); 2: tile columns tj >= 1 (lookahead)
     const int t = blockIdx.x;
-    int ti = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-    while (ti * (ti + 1) / 2 > t) --ti;
-    const int tj = t - ti * (ti + 1) / 2;
+    int ti, tj;
+    if (part == 1) {
+        ti = t;
+        tj = 0;
+    } else {
+        ti = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+        while (ti * (ti + 1) / 2 > t) --ti;
+        tj = t - ti * (ti + 1) / 2;
+        if (part == 2) {
+            ++ti;
+            ++tj;
+        }
+    }
     double* a = A + (size_t)blockIdx.z * sA;
     const int i0 = r0 + kCholNB * ti, j0 = r0 + kCholNB * tj;
     const int tid = threadIdx.x;
@@ -310,20 +323,66 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
     const int nblk = (n + kCholNB - 1) / kCholNB;
     linv.reserve((size_t)batch * nblk * kCholNB * kCholNB);
     chol_maxdiag_kernel<<<batch, 256, 0, st>>>(A, n, lda, sA, maxdiag, rank); OCTEN_LAUNCHED(1);
-    for (int k0 = 0; k0 < n; k0 += kCholNB) {
-        chol_diag_kernel<<<batch, kDiagThreads, kDiagSmem, st>>>(A, n, lda, sA, k0, tol, maxdiag, rank, linv.p, nblk);
+    // Lookahead (depth 1): the trailing update of step k is split into the
+    // next block column (part 1) and the rest (part 2).  The critical chain
+    // diag -> panel -> part 1 runs on a high-priority stream, part 2 on the
+    // caller's stream, so part 2 of step k overlaps the diagonal
+    // factorization and panel of step k+1 (the scheduler hands freed SMs to
+    // the high-priority CTAs first).  Part 1 of step k+1 waits for part 2 of
+    // step k: both update block column k+2.
+    static thread_local cudaStream_t crit = nullptr;
+    static thread_local std::vector<cudaEvent_t> ev_panel, ev_rest;
+    static thread_local cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+    if (!crit) {
+        int lo = 0, hi = 0;
+        OCTEN_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        OCTEN_CUDA(cudaStreamCreateWithPriority(&crit, cudaStreamNonBlocking, hi));
+        OCTEN_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+        OCTEN_CUDA(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming));
+    }
+    while ((int)ev_panel.size() < nblk) {
+        cudaEvent_t a, b;
+        OCTEN_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        OCTEN_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        ev_panel.push_back(a);
+        ev_rest.push_back(b);
+    }
+    OCTEN_CUDA(cudaEventRecord(ev_start, st));
+    OCTEN_CUDA(cudaStreamWaitEvent(crit, ev_start, 0));
+    int pending_rest = -1;  // step whose part 2 is in flight on `st`
+    for (int kb = 0; kb < nblk; ++kb) {
+        const int k0 = kb * kCholNB;
+        chol_diag_kernel<<<batch, kDiagThreads, kDiagSmem, crit>>>(A, n, lda, sA, k0, tol, maxdiag, rank, linv.p,
+                                                                    nblk);
         OCTEN_LAUNCHED(1);
         const int nb = min(kCholNB, n - k0);
         const int rows = n - k0 - nb;
         if (rows <= 0) break;
         const int r0 = k0 + nb;
         gemm_f64<false, true>(batch, rows, nb, nb, PanelA{A, lda, sA, r0, k0}, PanelB{linv.p, nblk, k0 / kCholNB},
-                                               PanelC{A, lda, sA, r0, k0}, st);
+                                               PanelC{A, lda, sA, r0, k0}, crit);
         const int tiles = (rows + kCholNB - 1) / kCholNB;
-        chol_trail_kernel<<<dim3(tiles * (tiles + 1) / 2, 1, batch), 256, kTrailSmem, st>>>(A, n, lda, sA, r0, k0,
-                                                                                              nb);
+        if (tiles > 1) {
+            OCTEN_CUDA(cudaEventRecord(ev_panel[kb], crit));
+            OCTEN_CUDA(cudaStreamWaitEvent(st, ev_panel[kb], 0));
+        }
+        if (pending_rest >= 0) {
+            OCTEN_CUDA(cudaStreamWaitEvent(crit, ev_rest[pending_rest], 0));
+            pending_rest = -1;
+        }
+        chol_trail_kernel<<<dim3(tiles, 1, batch), 256, kTrailSmem, crit>>>(A, n, lda, sA, r0, k0, nb, 1);
         OCTEN_LAUNCHED(1);
+        if (tiles > 1) {
+            chol_trail_kernel<<<dim3((tiles - 1) * tiles / 2, 1, batch), 256, kTrailSmem, st>>>(A, n, lda, sA, r0, k0,
+                                                                                                 nb, 2);
+            OCTEN_LAUNCHED(1);
+            OCTEN_CUDA(cudaEventRecord(ev_rest[kb], st));
+            pending_rest = kb;
+        }
     }
+    // join: everything on `st` after this waits for the critical chain
+    OCTEN_CUDA(cudaEventRecord(ev_end, crit));
+    OCTEN_CUDA(cudaStreamWaitEvent(st, ev_end, 0));
 }
 
 // Blocked solves with the stored diagonal-block inverses.  Step k of the
