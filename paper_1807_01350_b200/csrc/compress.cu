@@ -67,13 +67,14 @@ struct G2B {  // B(bt, j, b) = V[p][j + J b]
     }
 };
 template <typename T>
-struct G2C {  // Z2[p][(a + Q b) + Q^2 k]
+struct G2C {  // Z2[p * zs + (a + Q b) + Q^2 k]   (zs: per-replica stride, Q^2 t for the whole batch)
     T* Z2;
+    long long zs;
     int tc, Q;
     __device__ void operator()(int bt, int a, int b, T v) const {
         const int p = bt / tc, k = bt % tc;
         const size_t q2 = (size_t)Q * Q;
-        Z2[(size_t)p * q2 * tc + a + (size_t)Q * b + q2 * k] = v;
+        Z2[(size_t)p * zs + a + (size_t)Q * b + q2 * k] = v;
     }
 };
 template <typename T>
@@ -100,14 +101,39 @@ struct G3C {  // Y[p][m + Q^2 c] += v
     }
 };
 
+__global__ void nonfinite_chunk_kernel(const float* x32, const double* x64, size_t n, int* flag) {
+    int bad = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        if (!isfinite(x32 ? (double)x32[i] : x64[i])) bad = 1;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+// Modes 1 and 2 of the compression for the whole batch, slice chunk by
+// slice chunk: Z2[p][a + Q b + Q^2 k] = (X x1 U_p^T x2 V_p^T)(a, b, k).
+// With `ready` the chunk waits for its host->device copy event first, so the
+// copies of later chunks overlap the contractions of earlier ones; with
+// `flag` every chunk is also scanned for non-finite values (the batch must
+// be rejected before the summaries change).
 template <typename T>
-void run_compress(CompressEngine& e, const T* dX, std::int64_t t, const double* dW, double* dY, T* Z1, T* Z2,
-                  const T* A, const T* V, std::int64_t tc_max, cudaStream_t st, bool use_tc) {
+void run_project(CompressEngine& e, const T* dX, std::int64_t t, T* Z1, T* Z2, const T* A, const T* V,
+                 std::int64_t tc_max, cudaStream_t st, bool use_tc, const cudaEvent_t* ready, int* flag) {
     const int Q = e.Q, P = e.P;
-    for (std::int64_t k0 = 0; k0 < t; k0 += tc_max) {
+    const long long zs = (long long)Q * Q * t;
+    for (std::int64_t k0 = 0, ci = 0; k0 < t; k0 += tc_max, ++ci) {
         const int tc = (int)std::min<std::int64_t>(tc_max, t - k0);
         const long long N1 = e.J * tc;
         const T* Xc = dX + (size_t)e.I * e.J * k0;
+        if (ready) OCTEN_CUDA(cudaStreamWaitEvent(st, ready[ci], 0));
+        if (flag) {
+            const size_t n = (size_t)e.I * e.J * tc;
+            size_t blocks = (n + 255) / 256;
+            if (blocks > 148 * 8) blocks = 148 * 8;
+            if constexpr (std::is_same<T, float>::value)
+                nonfinite_chunk_kernel<<<(int)blocks, 256, 0, st>>>(Xc, nullptr, n, flag);
+            else
+                nonfinite_chunk_kernel<<<(int)blocks, 256, 0, st>>>(nullptr, Xc, n, flag);
+            OCTEN_LAUNCHED(1);
+        }
         bool done = false;
         OCTEN_CUDA(cudaEventRecord(e.event(2 * e.g1_used), st));
         if constexpr (std::is_same<T, float>::value) {
@@ -125,18 +151,27 @@ void run_compress(CompressEngine& e, const T* dX, std::int64_t t, const double* 
         ++e.g1_used;
         ++e.gemm1_launches;
         e.gemm1_flops += 2.0 * (double)e.Meff * (double)N1 * (double)e.I;
+        T* Z2c = Z2 + (size_t)Q * Q * k0;
         bool done2 = false;
         if constexpr (std::is_same<T, float>::value) {
             static const bool no_m2 = std::getenv("OCTEN_DISABLE_TC_MODE2") != nullptr;
             if (done && !no_m2)
-                done2 = tc_mode2_tf32x3(Z1, N1, (int)e.J, tc, e.Vhi.p, e.Vlo.p, e.ldv_tc, P, Q, Z2, st);
+                done2 = tc_mode2_tf32x3(Z1, N1, (int)e.J, tc, e.Vhi.p, e.Vlo.p, e.ldv_tc, P, Q, Z2c, zs, st);
         }
         if (!done2)
             gemm_simt<T, T, true, false>(P * tc, Q, Q, (int)e.J,
                                          G2A<T>{Z1, done ? e.rowmap_id.p : e.rowmap.p, N1, e.J, tc, Q},
-                                         G2B<T>{V, e.J, tc, Q}, G2C<T>{Z2, tc, Q}, st);
-        gemm_f64<false, true>(P, Q * Q, Q, tc, G3A<T>{Z2, tc, Q}, G3B{dW, t, k0, Q}, G3C{dY, Q}, st);
+                                         G2B<T>{V, e.J, tc, Q}, G2C<T>{Z2c, zs, tc, Q}, st);
     }
+    OCTEN_CUDA(cudaGetLastError());
+}
+
+// Mode 3 for the whole batch, accumulated into the summaries (update_summaries):
+// Y_p += Z2_p (Q^2 x t) W_p (t x Q), fp64.
+template <typename T>
+void run_accumulate(CompressEngine& e, std::int64_t t, const T* Z2, const double* dW, double* dY, cudaStream_t st) {
+    const int Q = e.Q, P = e.P;
+    gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<T>{Z2, (int)t, Q}, G3B{dW, t, 0, Q}, G3C{dY, Q}, st);
     OCTEN_CUDA(cudaGetLastError());
 }
 
@@ -238,18 +273,37 @@ void CompressEngine::set_projections(int P_, int Q_, int shared_, std::int64_t I
     OCTEN_CUDA(cudaStreamSynchronize(st));
 }
 
+void CompressEngine::project(const void* dX, int dtype, std::int64_t t, cudaStream_t st, const cudaEvent_t* ready,
+                             std::int64_t ready_slices, int* flag) {
+    std::int64_t tc = std::min(t, chunk_slices);
+    if (ready) tc = ready_slices;  // chunks follow the copies
+    const size_t zrows = (size_t)std::max<std::int64_t>(Meff, (std::int64_t)P * Q);
+    if (dtype == 1) {
+        Z1f.reserve(zrows * J * tc);
+        Z2f.reserve((size_t)P * Q * Q * t);
+        run_project<float>(*this, (const float*)dX, t, Z1f.p, Z2f.p, A32.p, V32.p, tc, st, true, ready, flag);
+    } else {
+        Z1d.reserve((size_t)Meff * J * tc);
+        Z2d.reserve((size_t)P * Q * Q * t);
+        run_project<double>(*this, (const double*)dX, t, Z1d.p, Z2d.p, A64.p, V64.p, tc, st, false, ready, flag);
+    }
+}
+
+void CompressEngine::accumulate(int dtype, std::int64_t t, const double* dW, double* dY, cudaStream_t st) {
+    if (dtype == 1)
+        run_accumulate<float>(*this, t, Z2f.p, dW, dY, st);
+    else
+        run_accumulate<double>(*this, t, Z2d.p, dW, dY, st);
+}
+
 void CompressEngine::compress_f32(const float* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st) {
-    const std::int64_t tc = std::min(t, chunk_slices);
-    Z1f.reserve((size_t)std::max<std::int64_t>(Meff, (std::int64_t)P * Q) * J * tc);
-    Z2f.reserve((size_t)P * Q * Q * tc);
-    run_compress<float>(*this, dX, t, dW, dY, Z1f.p, Z2f.p, A32.p, V32.p, tc, st, true);
+    project(dX, 1, t, st, nullptr, 0, nullptr);
+    accumulate(1, t, dW, dY, st);
 }
 
 void CompressEngine::compress_f64(const double* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st) {
-    const std::int64_t tc = std::min(t, chunk_slices);
-    Z1d.reserve((size_t)Meff * J * tc);
-    Z2d.reserve((size_t)P * Q * Q * tc);
-    run_compress<double>(*this, dX, t, dW, dY, Z1d.p, Z2d.p, A64.p, V64.p, tc, st, false);
+    project(dX, 0, t, st, nullptr, 0, nullptr);
+    accumulate(0, t, dW, dY, st);
 }
 
 }  // namespace octen

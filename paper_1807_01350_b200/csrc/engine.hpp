@@ -86,6 +86,13 @@ public:
     // into Y (P x Q^3, device).  X is fp32 or fp64.
     void compress_f32(const float* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st);
     void compress_f64(const double* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st);
+    // The same in two phases.  project: modes 1-2 of the whole batch into
+    // Z2 (P x Q^2 x t), chunk by chunk; chunk c waits for ready[c] when given
+    // (ready_slices slices per chunk) and is scanned for non-finite values
+    // into *flag when flag != null.  accumulate: Y += Z2 x3 W (fp64).
+    void project(const void* dX, int dtype, std::int64_t t, cudaStream_t st, const cudaEvent_t* ready,
+                 std::int64_t ready_slices, int* flag);
+    void accumulate(int dtype, std::int64_t t, const double* dW, double* dY, cudaStream_t st);
 
     int P = 0, Q = 0, shared = 0;
     std::int64_t I = 0, J = 0, Meff = 0;

@@ -109,6 +109,11 @@ Stream::Stream(const StreamCfg& c, int rank, int world) : cfg(c), shard_rank(ran
 
 Stream::~Stream() {
     if (st) cudaStreamSynchronize(st);
+    if (cp) {
+        cudaStreamSynchronize(cp);
+        cudaStreamDestroy(cp);
+    }
+    for (cudaEvent_t e : copy_ev) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     for (auto& e : evs)
@@ -295,17 +300,50 @@ void Stream::begin(const void* data, int dtype, int location, int order, const s
     try {
         auto tc = Clock::now();
         const size_t n = (size_t)I * J * t;
-        const void* dX = stage_input(data, dtype, location, n);
-        check_finite(dX, dtype, n);
-        extend_temporal(t);
         OCTEN_CUDA(cudaEventRecord(evs[0], st));
         if (pl > 0) {
-            const double* dWl = dW.p + (size_t)p0 * t * Q;
-            if (dtype == 1)
-                comp.compress_f32((const float*)dX, t, dWl, Y.p, st);
-            else
-                comp.compress_f64((const double*)dX, t, dWl, Y.p, st);
+            // modes 1-2 chunk by chunk; a host batch is copied chunk by chunk on
+            // the copy stream so the transfer overlaps the contractions; every
+            // chunk is scanned for non-finite values before Y is touched
+            flag.reserve(1);
+            flag.zero(1, st);
+            if (location == 0) {
+                const std::int64_t sub = std::max<std::int64_t>(
+                    1, std::min<std::int64_t>(comp.chunk_slices, std::min<std::int64_t>(t, (t + 4) / 5)));
+                const std::int64_t nch = (t + sub - 1) / sub;
+                const size_t esz = dtype == 1 ? sizeof(float) : sizeof(double);
+                void* dst;
+                if (dtype == 1)
+                    dst = X32.reserve(n);
+                else
+                    dst = X64.reserve(n);
+                if (!cp) OCTEN_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+                while ((std::int64_t)copy_ev.size() < nch) {
+                    cudaEvent_t e;
+                    OCTEN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    copy_ev.push_back(e);
+                }
+                // the copy stream must not overwrite X while earlier work on st reads it
+                OCTEN_CUDA(cudaEventRecord(copy_ev[0], st));
+                OCTEN_CUDA(cudaStreamWaitEvent(cp, copy_ev[0], 0));
+                const size_t plane = (size_t)I * J;
+                for (std::int64_t c = 0; c < nch; ++c) {
+                    const std::int64_t k0 = c * sub, kc = std::min(sub, t - k0);
+                    OCTEN_CUDA(cudaMemcpyAsync((char*)dst + plane * k0 * esz, (const char*)data + plane * k0 * esz,
+                                               plane * kc * esz, cudaMemcpyHostToDevice, cp));
+                    OCTEN_CUDA(cudaEventRecord(copy_ev[c], cp));
+                }
+                comp.project(dst, dtype, t, st, copy_ev.data(), sub, flag.p);
+            } else {
+                comp.project(data, dtype, t, st, nullptr, 0, flag.p);
+            }
+            if (flag.to_host(1, st)[0]) throw NumericError("DenseTensor: non-finite value");
+        } else {
+            const void* dX = stage_input(data, dtype, location, n);
+            check_finite(dX, dtype, n);
         }
+        extend_temporal(t);
+        if (pl > 0) comp.accumulate(dtype, t, dW.p + (size_t)p0 * t * Q, Y.p, st);
         ++batches_seen;
         OCTEN_CUDA(cudaEventRecord(evs[1], st));
         OCTEN_CUDA(cudaStreamSynchronize(st));

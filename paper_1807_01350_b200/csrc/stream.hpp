@@ -65,6 +65,8 @@ public:
     StreamCfg cfg;
     int shard_rank = 0, shard_world = 1, p0 = 0, pl = 0, chunk = 0;
     cudaStream_t st = nullptr;
+    cudaStream_t cp = nullptr;           // host->device batch copies (chunked)
+    std::vector<cudaEvent_t> copy_ev;    // one per copied chunk
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::int64_t I = 0, J = 0, K = 0, capC = 0;
     std::int64_t batches_seen = 0, batches_drawn = 0;

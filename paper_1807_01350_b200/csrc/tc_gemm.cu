@@ -305,7 +305,8 @@ constexpr uint32_t make_idesc_m2() {
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_mode2_tf32x3_kernel(const __grid_constant__ CUtensorMap map_z1, const __grid_constant__ CUtensorMap map_vhi,
-                           const __grid_constant__ CUtensorMap map_vlo, float* __restrict__ Z2, int Q, int J, int tc) {
+                           const __grid_constant__ CUtensorMap map_vlo, float* __restrict__ Z2, int Q, int J, int tc,
+                           long long zstride) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full_bar = (uint64_t*)(smem + M2_STAGES * M2_STAGE_BYTES);
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int q = warp & 3;
             const int a = q * 32 + lane;
             const size_t q2 = (size_t)Q * Q;
-            float* zb = Z2 + (size_t)p * q2 * tc + q2 * k;
+            float* zb = Z2 + (size_t)p * zstride + q2 * k;
 #pragma unroll 1
             for (int c0 = 0; c0 < M2_BN; c0 += 32) {
                 uint32_t r[32];
@@ -516,7 +517,7 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
 }
 
 bool tc_mode2_tf32x3(const float* Z1, long long N1, int J, int tc, const float* Vhi, const float* Vlo, int ldv, int P,
-                     int Q, float* Z2, cudaStream_t st) {
+                     int Q, float* Z2, long long zstride, cudaStream_t st) {
     if (!tc_gemm_available()) return false;
     // the A box of slice k starts at column k J: TMA needs that inner
     // coordinate on a 16-byte boundary, hence J % 4 == 0
@@ -534,7 +535,7 @@ bool tc_mode2_tf32x3(const float* Z1, long long N1, int J, int tc, const float* 
         OCTEN_CUDA(cudaFuncSetAttribute(tc_mode2_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    tc_mode2_tf32x3_kernel<<<P * tc, NUM_THREADS, smem, st>>>(mz, mh, ml, Z2, Q, J, tc);
+    tc_mode2_tf32x3_kernel<<<P * tc, NUM_THREADS, smem, st>>>(mz, mh, ml, Z2, Q, J, tc, zstride);
     OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     return true;

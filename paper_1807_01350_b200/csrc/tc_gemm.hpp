@@ -19,10 +19,10 @@ bool tc_gemm_available();
 bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X, float* Z, int M, long long N, int K,
                     cudaStream_t st, int scatter_p = 0, int scatter_q = 0, int scatter_sh = 0);
 // Mode-2 contraction batched over (replica, slice):
-//   Z2[p][a + Q b + Q^2 k] = sum_j Z1[p Q + a][k J + j] V_p[j, b]
+//   Z2[p * zstride + a + Q b + Q^2 k] = sum_j Z1[p Q + a][k J + j] V_p[j, b]
 // Z1: P*Q x N1 row-major (N1 = J * tc); Vhi/Vlo: TF32 hi/lo split of V,
 // P*Q x ldv row-major (row p Q + b holds V_p[:, b]).  Requires Q <= 112.
 bool tc_mode2_tf32x3(const float* Z1, long long N1, int J, int tc, const float* Vhi, const float* Vlo, int ldv, int P,
-                     int Q, float* Z2, cudaStream_t st);
+                     int Q, float* Z2, long long zstride, cudaStream_t st);
 
 }  // namespace octen
