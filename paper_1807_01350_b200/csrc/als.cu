@@ -947,6 +947,15 @@ std::string als_failure_message(int kind, int a, int b) {
     return "cp_als: non-finite fit at sweep " + std::to_string(a);
 }
 
+AlsEngine::~AlsEngine() {
+    if (lane_st) {
+        cudaStreamSynchronize(lane_st);
+        cudaStreamDestroy(lane_st);
+    }
+    for (cudaEvent_t e : lane_ev)
+        if (e) cudaEventDestroy(e);
+}
+
 void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, const double* dY,
                     const std::vector<std::uint64_t>& seeds, cudaStream_t st) {
     failure = {};
@@ -1137,43 +1146,111 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     const int upd_threads = 256;
     const size_t smem_upd = (size_t)(4 * R * R + 2 * Q * R + R + 2 * (R + 2) + upd_threads) * sizeof(double) + (R + 8) * sizeof(int) + 16;
     OCTEN_CUDA(cudaFuncSetAttribute(als_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_upd));
-    int* hcount = nullptr;
-    OCTEN_CUDA(cudaMallocHost(&hcount, sizeof(int)));
     // 16-byte pairs along every fast index need an even Q (and aligned bases)
     const bool pipe_ok = (Q % 2 == 0) && ((uintptr_t)dY % 16 == 0) && ((uintptr_t)F.p % 16 == 0) &&
                          ((uintptr_t)KR.p % 16 == 0);
-    int sweep = 0;
-    for (; sweep < max_iters; ++sweep) {
-        active_count.zero(1, st);
+    // Two lanes (halves of the replicas, each on its own stream): the
+    // latency-bound per-problem kernels of one lane overlap the DMMA GEMMs of
+    // the other.  Lane 1 starts half a phase late (after lane 0's first
+    // T-GEMM) and the lanes run free: the convergence count of sweep s is
+    // read while sweep s+1 is already queued (converged problems are masked
+    // inside every kernel, so the one extra sweep is harmless).
+    const int L = (P >= 2) ? 2 : 1;
+    int lp0[2] = {0, 0}, lp1[2] = {P, P};
+    if (L == 2) {
+        lp1[0] = P / 2;
+        lp0[1] = P / 2;
+    }
+    if (!lane_st) OCTEN_CUDA(cudaStreamCreateWithFlags(&lane_st, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&lane_ev[0], &lane_ev[1], &lane_ev[2], &lane_ev[3], &lane_ev[4], &lane_ev[5]})
+        if (!*e) OCTEN_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    cudaStream_t ls[2] = {st, lane_st};
+    active_count.reserve(2);
+    ws2.reserve(ws.n);
+    AlsDev dl[2];
+    for (int l = 0; l < L; ++l) {
+        const int pb = lp0[l], pn = lp1[l] - lp0[l], qb = pb * S;
+        AlsDev& x = dl[l];
+        x = d;
+        x.P = pn;
+        x.NP = pn * S;
+        x.Y = dY + (size_t)pb * q3;
+        x.normx2 = normx2.p + pb;
+        x.F = F.p + (size_t)qb * 3 * Q * R;
+        x.G = G.p + (size_t)qb * 3 * R * R;
+        x.lam = lam.p + (size_t)qb * R;
+        x.T = T.p + (size_t)pb * q2 * SR;
+        x.KR = KR.p + (size_t)pb * q2 * SR;
+        x.Mb = Mb.p + (size_t)qb * Q * R;
+        x.fit_hist = fit_hist.p + (size_t)qb * max_iters;
+        x.res_hist = res_hist.p + (size_t)qb * max_iters;
+        x.state = state.p + qb;
+        x.err = err.p + qb;
+        x.rngs = rngs.p + qb;
+        x.rescue_seed = rescue_seed.p + qb;
+        x.active_count = active_count.p + l;
+    }
+    if (L == 2) {
+        OCTEN_CUDA(cudaEventRecord(lane_ev[0], st));
+        OCTEN_CUDA(cudaStreamWaitEvent(lane_st, lane_ev[0], 0));
+    }
+    int* hcount = nullptr;  // [parity][lane]
+    OCTEN_CUDA(cudaMallocHost(&hcount, 4 * sizeof(int)));
+    auto launch_sweep = [&](int l, int sw, bool offset_wait) {
+        const AlsDev& x = dl[l];
+        cudaStream_t ss = ls[l];
+        const int pn = x.P, npn = x.NP;
+        double* wsl = l == 0 ? ws.p : ws2.p;
+        OCTEN_CUDA(cudaMemsetAsync(x.active_count, 0, sizeof(int), ss));
+        if (offset_wait) OCTEN_CUDA(cudaStreamWaitEvent(ss, lane_ev[1], 0));
         // T = Y x3 C  (Q^2 x SR per replica)
         if (pipe_ok)
-            gemm_f64_pipe<false>(P, (int)q2, SR, Q, YmatP{dY, q3, q2}, FacP{F.p, S, Q, R, 2}, TStore{T.p, q2, SR},
-                                 st);
+            gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmatP{x.Y, q3, q2}, FacP{x.F, S, Q, R, 2}, TStore{x.T, q2, SR},
+                                 ss);
         else
-            gemm_f64<false, true>(P, (int)q2, SR, Q, YmatA{dY, q3, q2, S, false}, FacB{F.p, S, Q, R, 2},
-                                  TStore{T.p, q2, SR}, st);
-        als_mttkrp_T_kernel<<<NP * R, 256, 0, st>>>(d, 0); OCTEN_LAUNCHED(1);
-        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 0, sweep); OCTEN_LAUNCHED(1);
-        als_mttkrp_T_kernel<<<NP * R, 256, 0, st>>>(d, 1); OCTEN_LAUNCHED(1);
-        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 1, sweep); OCTEN_LAUNCHED(1);
-        als_kr_kernel<<<dim3(R, NP), 256, 0, st>>>(d);
+            gemm_f64<false, true>(pn, (int)q2, SR, Q, YmatA{x.Y, q3, q2, S, false}, FacB{x.F, S, Q, R, 2},
+                                  TStore{x.T, q2, SR}, ss);
+        if (l == 0 && sw == 0 && L == 2) OCTEN_CUDA(cudaEventRecord(lane_ev[1], ss));
+        als_mttkrp_T_kernel<<<npn * R, 256, 0, ss>>>(x, 0); OCTEN_LAUNCHED(1);
+        als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, 0, sw); OCTEN_LAUNCHED(1);
+        als_mttkrp_T_kernel<<<npn * R, 256, 0, ss>>>(x, 1); OCTEN_LAUNCHED(1);
+        als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, 1, sw); OCTEN_LAUNCHED(1);
+        als_kr_kernel<<<dim3(R, npn), 256, 0, ss>>>(x);
         OCTEN_LAUNCHED(1);
         if (pipe_ok)
-            gemm_f64_pipe<true>(P, Q, SR, (int)q2, YtP{dY, q3, q2}, KRP{KR.p, q2, SR}, M2Store{Mb.p, S, Q, R}, st,
-                                ks_m2, ws.p);
+            gemm_f64_pipe<true>(pn, Q, SR, (int)q2, YtP{x.Y, q3, q2}, KRP{x.KR, q2, SR}, M2Store{x.Mb, S, Q, R}, ss,
+                                ks_m2, wsl);
         else
-            gemm_f64<true, true>(P, Q, SR, (int)q2, YtA{dY, q3, q2}, KRB{KR.p, q2, SR}, M2Store{Mb.p, S, Q, R}, st,
-                                 ks_m2, ws.p);
-        als_update_kernel<<<NP, upd_threads, smem_upd, st>>>(d, 2, sweep); OCTEN_LAUNCHED(1);
+            gemm_f64<true, true>(pn, Q, SR, (int)q2, YtA{x.Y, q3, q2}, KRB{x.KR, q2, SR}, M2Store{x.Mb, S, Q, R}, ss,
+                                 ks_m2, wsl);
+        als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, 2, sw); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
-        OCTEN_CUDA(cudaMemcpyAsync(hcount, active_count.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-        OCTEN_CUDA(cudaStreamSynchronize(st));
-        ++host_syncs;
-        if (*hcount == 0) {
-            ++sweep;
-            break;
+        OCTEN_CUDA(cudaMemcpyAsync(hcount + 2 * (sw & 1) + l, x.active_count, sizeof(int), cudaMemcpyDeviceToHost,
+                                   ss));
+        OCTEN_CUDA(cudaEventRecord(lane_ev[2 + 2 * (sw & 1) + l], ss));
+    };
+    int sweep = 0;
+    for (; sweep < max_iters; ++sweep) {
+        for (int l = 0; l < L; ++l) launch_sweep(l, sweep, l == 1 && sweep == 0);
+        if (sweep >= 1) {
+            // problems still active after the previous sweep
+            int left = 0;
+            for (int l = 0; l < L; ++l) {
+                OCTEN_CUDA(cudaEventSynchronize(lane_ev[2 + 2 * ((sweep - 1) & 1) + l]));
+                left += hcount[2 * ((sweep - 1) & 1) + l];
+            }
+            ++host_syncs;
+            if (left == 0) {
+                ++sweep;
+                break;
+            }
         }
     }
+    if (L == 2) {
+        OCTEN_CUDA(cudaEventRecord(lane_ev[0], lane_st));
+        OCTEN_CUDA(cudaStreamWaitEvent(st, lane_ev[0], 0));
+    }
+    OCTEN_CUDA(cudaStreamSynchronize(st));
     last_sweeps = sweep;
     if (std::getenv("OCTEN_DEBUG_ALS")) {
         const std::vector<int> ed = eigdbg.to_host(1, st);

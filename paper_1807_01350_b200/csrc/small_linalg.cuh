@@ -1289,9 +1289,12 @@ OCTEN_HD bool eig_real_team(const Team& team, int nn, double* hm, double* vm, do
                 q = H_(m + 1, m + 1) - z - r - s;
                 r = H_(m + 2, m + 1);
                 s = fabs(p) + fabs(q) + fabs(r);
-                p = p / s;
-                q = q / s;
-                r = r / s;
+                {
+                    const double is = 1.0 / s;  // one division, three products
+                    p = p * is;
+                    q = q * is;
+                    r = r * is;
+                }
                 if (m == l) break;
                 if (fabs(H_(m, m - 1)) * (fabs(q) + fabs(r)) <
                     eps * (fabs(p) * (fabs(H_(m - 1, m - 1)) + fabs(z) + fabs(H_(m + 1, m + 1)))))
@@ -1312,9 +1315,10 @@ OCTEN_HD bool eig_real_team(const Team& team, int nn, double* hm, double* vm, do
                     r = notlast ? H_(k + 2, k - 1) : 0.0;
                     x = fabs(p) + fabs(q) + fabs(r);
                     if (x == 0.0) continue;
-                    p = p / x;
-                    q = q / x;
-                    r = r / x;
+                    const double ix = 1.0 / x;
+                    p = p * ix;
+                    q = q * ix;
+                    r = r * ix;
                 }
                 s = sqrt(p * p + q * q + r * r);
                 if (p < 0) s = -s;
@@ -1331,11 +1335,12 @@ OCTEN_HD bool eig_real_team(const Team& team, int nn, double* hm, double* vm, do
                     team.sync();
                     if (lead && store) H_(k, k - 1) = hk;
                     p = p + s;
-                    x = p / s;
-                    y = q / s;
-                    z = r / s;
-                    q = q / p;
-                    r = r / p;
+                    const double is = 1.0 / s, ip = 1.0 / p;
+                    x = p * is;
+                    y = q * is;
+                    z = r * is;
+                    q = q * ip;
+                    r = r * ip;
                     for (int j = k + T; j < nn; j += NT) {
                         double pp = H_(k, j) + q * H_(k + 1, j);
                         if (notlast) {

