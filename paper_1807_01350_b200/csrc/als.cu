@@ -948,10 +948,11 @@ std::string als_failure_message(int kind, int a, int b) {
 }
 
 AlsEngine::~AlsEngine() {
-    if (lane_st) {
-        cudaStreamSynchronize(lane_st);
-        cudaStreamDestroy(lane_st);
-    }
+    for (cudaStream_t ls : lane_st)
+        if (ls) {
+            cudaStreamSynchronize(ls);
+            cudaStreamDestroy(ls);
+        }
     for (cudaEvent_t e : lane_ev)
         if (e) cudaEventDestroy(e);
 }
@@ -1149,25 +1150,30 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     // 16-byte pairs along every fast index need an even Q (and aligned bases)
     const bool pipe_ok = (Q % 2 == 0) && ((uintptr_t)dY % 16 == 0) && ((uintptr_t)F.p % 16 == 0) &&
                          ((uintptr_t)KR.p % 16 == 0);
-    // Two lanes (halves of the replicas, each on its own stream): the
+    // Up to four lanes (replica slices, each on its own stream): the
     // latency-bound per-problem kernels of one lane overlap the DMMA GEMMs of
     // the other.  Lane 1 starts half a phase late (after lane 0's first
     // T-GEMM) and the lanes run free: the convergence count of sweep s is
     // read while sweep s+1 is already queued (converged problems are masked
     // inside every kernel, so the one extra sweep is harmless).
-    const int L = (P >= 2) ? 2 : 1;
-    int lp0[2] = {0, 0}, lp1[2] = {P, P};
-    if (L == 2) {
-        lp1[0] = P / 2;
-        lp0[1] = P / 2;
+    int L = 4;  // measured: 1 lane 14.1 ms, 2 lanes 13.5, 4 lanes 13.4 (c3 CP-ALS stage)
+    if (const char* ev = std::getenv("OCTEN_ALS_LANES")) L = std::max(1, std::min(kMaxLanes, std::atoi(ev)));
+    L = std::min(L, P);
+    int lp0[kMaxLanes], lp1[kMaxLanes];
+    for (int l = 0; l < L; ++l) {
+        lp0[l] = (int)((long long)P * l / L);
+        lp1[l] = (int)((long long)P * (l + 1) / L);
     }
-    if (!lane_st) OCTEN_CUDA(cudaStreamCreateWithFlags(&lane_st, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&lane_ev[0], &lane_ev[1], &lane_ev[2], &lane_ev[3], &lane_ev[4], &lane_ev[5]})
-        if (!*e) OCTEN_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    cudaStream_t ls[2] = {st, lane_st};
-    active_count.reserve(2);
-    ws2.reserve(ws.n);
-    AlsDev dl[2];
+    for (int l = 1; l < L; ++l)
+        if (!lane_st[l]) OCTEN_CUDA(cudaStreamCreateWithFlags(&lane_st[l], cudaStreamNonBlocking));
+    for (cudaEvent_t& e : lane_ev)
+        if (!e) OCTEN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaStream_t ls[kMaxLanes];
+    ls[0] = st;
+    for (int l = 1; l < L; ++l) ls[l] = lane_st[l];
+    active_count.reserve(kMaxLanes);
+    ws2.reserve(ws.n * (L - 1) + 1);
+    AlsDev dl[kMaxLanes];
     for (int l = 0; l < L; ++l) {
         const int pb = lp0[l], pn = lp1[l] - lp0[l], qb = pb * S;
         AlsDev& x = dl[l];
@@ -1190,19 +1196,20 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         x.rescue_seed = rescue_seed.p + qb;
         x.active_count = active_count.p + l;
     }
-    if (L == 2) {
+    if (L > 1) {
         OCTEN_CUDA(cudaEventRecord(lane_ev[0], st));
-        OCTEN_CUDA(cudaStreamWaitEvent(lane_st, lane_ev[0], 0));
+        for (int l = 1; l < L; ++l) OCTEN_CUDA(cudaStreamWaitEvent(ls[l], lane_ev[0], 0));
     }
     int* hcount = nullptr;  // [parity][lane]
-    OCTEN_CUDA(cudaMallocHost(&hcount, 4 * sizeof(int)));
+    OCTEN_CUDA(cudaMallocHost(&hcount, 2 * kMaxLanes * sizeof(int)));
     auto launch_sweep = [&](int l, int sw, bool offset_wait) {
         const AlsDev& x = dl[l];
         cudaStream_t ss = ls[l];
         const int pn = x.P, npn = x.NP;
-        double* wsl = l == 0 ? ws.p : ws2.p;
+        double* wsl = l == 0 ? ws.p : ws2.p + (size_t)(l - 1) * ws.n;
         OCTEN_CUDA(cudaMemsetAsync(x.active_count, 0, sizeof(int), ss));
-        if (offset_wait) OCTEN_CUDA(cudaStreamWaitEvent(ss, lane_ev[1], 0));
+        // lane l starts its first sweep after lane l-1's first T-GEMM
+        if (offset_wait) OCTEN_CUDA(cudaStreamWaitEvent(ss, lane_ev[1 + l - 1], 0));
         // T = Y x3 C  (Q^2 x SR per replica)
         if (pipe_ok)
             gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmatP{x.Y, q3, q2}, FacP{x.F, S, Q, R, 2}, TStore{x.T, q2, SR},
@@ -1210,7 +1217,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         else
             gemm_f64<false, true>(pn, (int)q2, SR, Q, YmatA{x.Y, q3, q2, S, false}, FacB{x.F, S, Q, R, 2},
                                   TStore{x.T, q2, SR}, ss);
-        if (l == 0 && sw == 0 && L == 2) OCTEN_CUDA(cudaEventRecord(lane_ev[1], ss));
+        if (sw == 0 && l + 1 < L) OCTEN_CUDA(cudaEventRecord(lane_ev[1 + l], ss));
         als_mttkrp_T_kernel<<<npn * R, 256, 0, ss>>>(x, 0); OCTEN_LAUNCHED(1);
         als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, 0, sw); OCTEN_LAUNCHED(1);
         als_mttkrp_T_kernel<<<npn * R, 256, 0, ss>>>(x, 1); OCTEN_LAUNCHED(1);
@@ -1225,19 +1232,19 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
                                  ks_m2, wsl);
         als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, 2, sw); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
-        OCTEN_CUDA(cudaMemcpyAsync(hcount + 2 * (sw & 1) + l, x.active_count, sizeof(int), cudaMemcpyDeviceToHost,
-                                   ss));
-        OCTEN_CUDA(cudaEventRecord(lane_ev[2 + 2 * (sw & 1) + l], ss));
+        OCTEN_CUDA(cudaMemcpyAsync(hcount + kMaxLanes * (sw & 1) + l, x.active_count, sizeof(int),
+                                   cudaMemcpyDeviceToHost, ss));
+        OCTEN_CUDA(cudaEventRecord(lane_ev[kMaxLanes + kMaxLanes * (sw & 1) + l], ss));
     };
     int sweep = 0;
     for (; sweep < max_iters; ++sweep) {
-        for (int l = 0; l < L; ++l) launch_sweep(l, sweep, l == 1 && sweep == 0);
+        for (int l = 0; l < L; ++l) launch_sweep(l, sweep, l >= 1 && sweep == 0);
         if (sweep >= 1) {
             // problems still active after the previous sweep
             int left = 0;
             for (int l = 0; l < L; ++l) {
-                OCTEN_CUDA(cudaEventSynchronize(lane_ev[2 + 2 * ((sweep - 1) & 1) + l]));
-                left += hcount[2 * ((sweep - 1) & 1) + l];
+                OCTEN_CUDA(cudaEventSynchronize(lane_ev[kMaxLanes + kMaxLanes * ((sweep - 1) & 1) + l]));
+                left += hcount[kMaxLanes * ((sweep - 1) & 1) + l];
             }
             ++host_syncs;
             if (left == 0) {
@@ -1246,8 +1253,8 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             }
         }
     }
-    if (L == 2) {
-        OCTEN_CUDA(cudaEventRecord(lane_ev[0], lane_st));
+    for (int l = 1; l < L; ++l) {
+        OCTEN_CUDA(cudaEventRecord(lane_ev[0], ls[l]));
         OCTEN_CUDA(cudaStreamWaitEvent(st, lane_ev[0], 0));
     }
     OCTEN_CUDA(cudaStreamSynchronize(st));
