@@ -62,6 +62,7 @@ struct AlsDev {
     double* Pm;
     double* Hh;
     int* eigdbg;  // [0] subspace fallbacks to Jacobi (diagnostics)
+    long long* tsc;  // per-phase clock64 stamps of the update kernel (diagnostics; null normally)
     double* gscr;
     int* usable;
     int* att_start;
@@ -520,6 +521,9 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     int* iw = (int*)(red + blockDim.x);  // R + 8
     __shared__ int rank, bad;
     const double* M = Ms;
+#define OCTEN_TSC(i) \
+    if (d.tsc && threadIdx.x == 0 && blockIdx.x == 0) d.tsc[(i)] = clock64();
+    OCTEN_TSC(0)
     {
         g2s_copy(Ms, d.Mb + (size_t)prob * Q * R, Q * R);
     }
@@ -532,22 +536,22 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     }
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
+    OCTEN_TSC(1)
     {
-        // Lf = chol(V), Ev = Lf^-1, block-cooperative (R <= 64)
+        // Lf = chol(V), Ev = Lf^-1, block-cooperative (R <= 64).  (A fully
+        // unrolled one-warp register version measured 3.5x slower: its
+        // straight-line code streams through the instruction cache once.)
         double md = 0.0;
         for (int i = 0; i < R; ++i) md = fmax(md, V[i + R * i]);
-        const int rk = block_chol_inv64(V, R, R, md > 0.0 ? kEps * R * md : INFINITY, Lf, R, Ev, R, red);
+        const double thr = md > 0.0 ? kEps * R * md : INFINITY;
+        const int rk = block_chol_inv64(V, R, R, thr, Lf, R, Ev, R, red);
         if (threadIdx.x == 0) rank = rk;
     }
     __syncthreads();
+    OCTEN_TSC(2)
     if (rank == R) {
-        // Vi = L^-T L^-1
-        for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-            const int i = e % R, j = e / R;
-            double s = 0.0;
-            for (int k = (i > j ? i : j); k < R; ++k) s += Ev[k + R * i] * Ev[k + R * j];
-            Vi[e] = s;
-        }
+        // Vi = L^-T L^-1 on the FP64 tensor cores: Vi(i, j) = sum_k Ev(k, i) Ev(k, j)
+        block_dmma_small(R, R, R, Ev, R, 1, Ev, 1, R, Vi, 1, R);
     } else {
         TeamDev team;
         jacobi_eig_sym(team, R, V, Ev, cs, iw);
@@ -566,15 +570,14 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
         }
     }
     __syncthreads();
-    // raw = M Vi
-    for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
-        const int q = e % Q, c = e / Q;
-        double s = 0.0;
-        for (int k = 0; k < R; ++k) s += M[q + (size_t)Q * k] * Vi[k + R * c];
-        raw[e] = s;
-        if (!isfinite(s)) bad = 1;
-    }
+    OCTEN_TSC(3)
+    // raw = M Vi on the FP64 tensor cores (Q x R x R)
+    block_dmma_small(Q, R, R, M, 1, Q, Vi, 1, R, raw, 1, Q);
     __syncthreads();
+    for (int e = threadIdx.x; e < Q * R; e += blockDim.x)
+        if (!isfinite(raw[e])) bad = 1;
+    __syncthreads();
+    OCTEN_TSC(4)
     if (bad) {
         if (threadIdx.x == 0) {
             d.err[prob].code = kAlsNonFiniteFactor;
@@ -597,7 +600,21 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    OCTEN_TSC(5)
+    // degenerate columns are re-drawn from the problem's sequential rescue
+    // stream (column order); the common case (none) skips the serial loop
+    __shared__ int any_degenerate;
+    if (threadIdx.x == 0) any_degenerate = 0;
+    __syncthreads();
+    for (int c = threadIdx.x; c < R; c += blockDim.x)
+        if (nrm[c] < kDegenerateNorm) any_degenerate = 1;
+    __syncthreads();
+    if (!any_degenerate) {
+        for (int c = threadIdx.x; c < R; c += blockDim.x) {
+            d.lam[(size_t)prob * R + c] = nrm[c];
+            cs[c] = 1.0 / nrm[c];
+        }
+    } else if (threadIdx.x == 0) {
         for (int c = 0; c < R; ++c) {
             if (nrm[c] < kDegenerateNorm) {
                 Mt64* g = d.rngs + prob;
@@ -614,36 +631,24 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
                 st->rescued = 1;
             }
             d.lam[(size_t)prob * R + c] = nrm[c];
+            cs[c] = 1.0 / nrm[c];
         }
     }
     __syncthreads();
+    OCTEN_TSC(6)
     double* f = d.f(prob, mode);
     for (int e = threadIdx.x; e < Q * R; e += blockDim.x) {
-        const double v = raw[e] / nrm[e / Q];
+        const double v = raw[e] * cs[e / Q];  // cs: 1 / column norm
         raw[e] = v;
         f[e] = v;
     }
     __syncthreads();
+    OCTEN_TSC(7)
     double* g = d.g(prob, mode);
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-        const int i = e % R, j = e / R;
-        if (i > j) continue;
-        const double* ri = raw + Q * i;
-        const double* rj = raw + Q * j;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int q = 0;
-        for (; q + 3 < Q; q += 4) {
-            s0 += ri[q] * rj[q];
-            s1 += ri[q + 1] * rj[q + 1];
-            s2 += ri[q + 2] * rj[q + 2];
-            s3 += ri[q + 3] * rj[q + 3];
-        }
-        for (; q < Q; ++q) s0 += ri[q] * rj[q];
-        const double s = (s0 + s1) + (s2 + s3);
-        g[i + R * j] = s;
-        g[j + R * i] = s;
-    }
+    // Gram of the new factor on the FP64 tensor cores: g(i, j) = sum_q raw(q, i) raw(q, j)
+    block_dmma_small(R, R, Q, raw, Q, 1, raw, 1, Q, g, 1, R);
     __syncthreads();
+    OCTEN_TSC(8)
     if (mode != 2) return;
     // fit (cp_als.cpp:325-345)
     const double* lam = d.lam + (size_t)prob * R;
@@ -683,6 +688,7 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
             atomicAdd(d.active_count, 1);
         }
     }
+#undef OCTEN_TSC
 }
 
 // Best restart per replica (strictly greater final fit wins; cp_als.cpp:347-356).
@@ -1006,6 +1012,12 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     eigdbg.reserve(4);
     eigdbg.zero(4, st);
     d.eigdbg = eigdbg.p;
+    static const bool want_tsc = std::getenv("OCTEN_DEBUG_ALS_TSC") != nullptr;
+    if (want_tsc) {
+        tscbuf.reserve(64);
+        tscbuf.zero(64, st);
+    }
+    d.tsc = want_tsc ? reinterpret_cast<long long*>(tscbuf.p) : nullptr;
     d.gscr = gscr.p;
     d.usable = usable.p;
     d.att_start = att_start.p;
@@ -1259,6 +1271,13 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     }
     OCTEN_CUDA(cudaStreamSynchronize(st));
     last_sweeps = sweep;
+    if (d.tsc) {
+        std::vector<double> raw = tscbuf.to_host(64, st);
+        const long long* t = reinterpret_cast<const long long*>(raw.data());
+        std::fprintf(stderr, "octen als update phases (cycles from start):");
+        for (int i = 1; i < 32 && t[i]; ++i) std::fprintf(stderr, " %lld", t[i] - t[0]);
+        std::fprintf(stderr, "\n");
+    }
     if (std::getenv("OCTEN_DEBUG_ALS")) {
         const std::vector<int> ed = eigdbg.to_host(1, st);
         std::fprintf(stderr, "octen als: %d problems, %d sweeps, %d GEVD eigen fallbacks\n", NP, sweep, ed[0]);

@@ -142,6 +142,39 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
+// Block-cooperative small fp64 GEMM from shared (or global) memory on the
+// FP64 tensor cores: C(m, n) = sum_k A(m, k) B(k, n) with element strides
+//   A(m, k) = A[m * sam + k * sak],  B(k, n) = B[k * sbk + n * sbn],
+//   C(m, n) = C[m * scm + n * scn].
+// The block's warps take 8 x 8 output tiles round-robin and step k by 4
+// (DMMA m8n8k4); indices past M / N / K read as zero.  For the R x R and
+// Q x R products of the ALS update (Q <= 256, R <= 64).  No barrier inside:
+// callers synchronize before reading C.
+// ---------------------------------------------------------------------------
+__device__ inline void block_dmma_small(int M, int N, int K, const double* A, int sam, int sak, const double* B,
+                                        int sbk, int sbn, double* C, int scm, int scn) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int tm = (M + 7) >> 3, tn = (N + 7) >> 3;
+    for (int tile = warp; tile < tm * tn; tile += nw) {
+        const int m0 = (tile % tm) * 8, n0 = (tile / tm) * 8;
+        double c0 = 0.0, c1 = 0.0;
+        const int am = m0 + g, bn = n0 + g;
+        for (int k0 = 0; k0 < K; k0 += 4) {
+            const int k = k0 + t4;
+            const double a = (am < M && k < K) ? A[am * sam + k * sak] : 0.0;
+            const double b = (bn < N && k < K) ? B[k * sbk + bn * sbn] : 0.0;
+            dmma_m8n8k4(c0, c1, a, b);
+        }
+        const int cm = m0 + g, cn = n0 + 2 * t4;
+        if (cm < M) {
+            if (cn < N) C[cm * scm + cn * scn] = c0;
+            if (cn + 1 < N) C[cm * scm + (cn + 1) * scn] = c1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Pipelined variant for operands with 16-byte contiguous pairs along the
 // fast dimension: the functors return element POINTERS (A(b, m, k), B(b, k, n))
 // and tiles move by cp.async 16 B chunks through a 3-stage shared-memory
