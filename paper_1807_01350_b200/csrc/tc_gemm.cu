@@ -28,11 +28,16 @@ namespace octen {
 
 namespace {
 
-constexpr int BM = 128, BN = 256, BKB = 128;  // BK in bytes (32 fp32)
+constexpr int BM = 128, BN = 256, BKB = 128;  // BK in bytes (32 fp32), 128 B swizzle (mode-2 kernel)
 constexpr int BK = BKB / 4;
-constexpr int STAGES = 2;
-constexpr int A_BYTES = BM * BKB;              // 16 KB
-constexpr int B_BYTES = BN * BKB;              // 32 KB
+// GEMM1: 16-wide k-blocks (64 B rows, 64 B swizzle) in a 4-deep ring: the
+// same 192 KB of shared memory as two 32-wide stages, but three k-blocks are
+// in flight while one is consumed, which covers the TMA latency
+constexpr int G1_BKB = 64;
+constexpr int G1_BK = G1_BKB / 4;
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * G1_BKB;           // 8 KB
+constexpr int B_BYTES = BN * G1_BKB;           // 16 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B(hi in place), B_lo
 constexpr int NUM_THREADS = 256;
 constexpr int CONVERT_WARP0 = 2, CONVERT_WARPS = 6;
@@ -81,6 +86,16 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// UMMA shared-memory descriptor: K-major, 64B swizzle, 8-row groups 512 B apart.
+__device__ __forceinline__ uint64_t make_desc_sw64(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
+    d |= (uint64_t)1 << 16;                         // leading byte offset (unused for swizzled K-major)
+    d |= (uint64_t)(512 >> 4) << 32;                // stride byte offset
+    d |= (uint64_t)1 << 46;                         // descriptor version (sm_100)
+    d |= (uint64_t)4 << 61;                         // layout: SWIZZLE_64B
+    return d;
+}
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.
 __device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
     uint64_t d = 0;
@@ -164,7 +179,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int m_tile = blockIdx.x, n_tile = blockIdx.y;
     const int m0 = m_tile * BM;
     const long long n0 = (long long)n_tile * BN;
-    const int num_kb = (K + BK - 1) / BK;
+    const int num_kb = (K + G1_BK - 1) / G1_BK;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -194,9 +209,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (kb >= STAGES) mbar_wait(&empty_bar[s], ph ^ 1);
                 uint8_t* st = smem + s * STAGE_BYTES;
                 mbar_arrive_expect_tx(&full_bar[s], 2 * A_BYTES + B_BYTES);
-                tma_load_2d(st, &map_ahi, &full_bar[s], kb * BK, m0);
-                tma_load_2d(st + A_BYTES, &map_alo, &full_bar[s], kb * BK, m0);
-                tma_load_2d(st + 2 * A_BYTES, &map_x, &full_bar[s], kb * BK, (int)n0);
+                tma_load_2d(st, &map_ahi, &full_bar[s], kb * G1_BK, m0);
+                tma_load_2d(st + A_BYTES, &map_alo, &full_bar[s], kb * G1_BK, m0);
+                tma_load_2d(st + 2 * A_BYTES, &map_x, &full_bar[s], kb * G1_BK, (int)n0);
             }
         }
     } else if (warp == 1) {
@@ -212,12 +227,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint32_t a_hi = smem_u32(st), a_lo = smem_u32(st + A_BYTES);
                 const uint32_t b_hi = smem_u32(st + 2 * A_BYTES), b_lo = smem_u32(st + 2 * A_BYTES + B_BYTES);
 #pragma unroll
-                for (int k = 0; k < BK / 8; ++k) {
+                for (int k = 0; k < G1_BK / 8; ++k) {
                     const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
                     const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
-                    mma_tf32(tmem_base, make_desc_sw128(a_hi + off), make_desc_sw128(b_hi + off), idesc, acc0);
-                    mma_tf32(tmem_base, make_desc_sw128(a_hi + off), make_desc_sw128(b_lo + off), idesc, 1u);
-                    mma_tf32(tmem_base, make_desc_sw128(a_lo + off), make_desc_sw128(b_hi + off), idesc, 1u);
+                    mma_tf32(tmem_base, make_desc_sw64(a_hi + off), make_desc_sw64(b_hi + off), idesc, acc0);
+                    mma_tf32(tmem_base, make_desc_sw64(a_hi + off), make_desc_sw64(b_lo + off), idesc, 1u);
+                    mma_tf32(tmem_base, make_desc_sw64(a_lo + off), make_desc_sw64(b_hi + off), idesc, 1u);
                 }
                 mma_commit(&empty_bar[s]);
             }
@@ -460,7 +475,8 @@ EncodeTiledFn get_encode() {
 }
 
 bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-              uint32_t box_inner, uint32_t box_outer) {
+              uint32_t box_inner, uint32_t box_outer,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return false;
     // keep every extent and stride a whole number of 16-byte units
@@ -470,7 +486,7 @@ bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -498,9 +514,12 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
     CUtensorMap mhi, mlo, mx;
     // inner extents in whole 16-byte units: the zero padding of A (lda >= K)
     // stands in for the tail (X's own extent is K, TMA zero-fills past it)
-    if (!make_map(&mhi, Ahi, (uint64_t)lda, (uint64_t)M, (uint64_t)lda * 4, BK, BM)) return false;
-    if (!make_map(&mlo, Alo, (uint64_t)lda, (uint64_t)M, (uint64_t)lda * 4, BK, BM)) return false;
-    if (!make_map(&mx, X, (uint64_t)K, (uint64_t)N, (uint64_t)K * 4, BK, BN)) return false;
+    if (!make_map(&mhi, Ahi, (uint64_t)lda, (uint64_t)M, (uint64_t)lda * 4, G1_BK, BM, CU_TENSOR_MAP_SWIZZLE_64B))
+        return false;
+    if (!make_map(&mlo, Alo, (uint64_t)lda, (uint64_t)M, (uint64_t)lda * 4, G1_BK, BM, CU_TENSOR_MAP_SWIZZLE_64B))
+        return false;
+    if (!make_map(&mx, X, (uint64_t)K, (uint64_t)N, (uint64_t)K * 4, G1_BK, BN, CU_TENSOR_MAP_SWIZZLE_64B))
+        return false;
     const size_t smem = STAGES * STAGE_BYTES + 1024 + 256;
     static bool attr = false;
     if (!attr) {
