@@ -41,6 +41,11 @@ constexpr int B_BYTES = BN * G1_BKB;           // 16 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B(hi in place), B_lo
 constexpr int NUM_THREADS = 256;
 constexpr int CONVERT_WARP0 = 2, CONVERT_WARPS = 6;
+// kind::tf32 reads the fp32 container and ignores its 13 low mantissa bits,
+// so the raw tile already is the hi part: the converters only write lo
+// (one 16 B store per 4 elements instead of two; shared memory bandwidth is
+// the converters' limit).  Set true to store the masked hi explicitly.
+constexpr bool kWriteHi = false;
 constexpr uint32_t TMEM_COLS = 256;
 
 // ---- PTX helpers ----
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 l.y = v.y - h.y;
                 l.z = v.z - h.z;
                 l.w = v.w - h.w;
-                bx[i] = h;
+                if (kWriteHi) bx[i] = h;
                 bl[i] = l;
             }
             fence_proxy_async();
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 l.y = v.y - h.y;
                 l.z = v.z - h.z;
                 l.w = v.w - h.w;
-                ah[i] = h;
+                if (kWriteHi) ah[i] = h;
                 al[i] = l;
             }
             fence_proxy_async();
