@@ -177,6 +177,37 @@ __global__ void __launch_bounds__(256) gevd_eig_sym_kernel(AlsDev d, int v_in_sm
     }
 }
 
+// GEVD slice mixtures for every attempt of every restart of replica p
+// (cp_als.cpp:117-121): Smix[prob][j][m] = sum_c Y[p][m + Q^2 c] w[prob][j][c],
+// j = 0..5 (3 attempts x 2 mixtures).  One thread per m reads Y once per
+// replica (coalesced) for all S restarts; the weights sit in shared memory.
+__global__ void __launch_bounds__(256) gevd_mix_kernel(AlsDev d) {
+    extern __shared__ double wmix[];  // S * 6 * Q
+    const int p = blockIdx.y, Q = d.Q, S = d.S;
+    const int nw = S * 6;
+    for (int e = threadIdx.x; e < nw * Q; e += blockDim.x) wmix[e] = d.Wmix[(size_t)p * S * 6 * Q + e];
+    __syncthreads();
+    const size_t q2 = d.q2();
+    const size_t m = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (m >= q2) return;
+    const double* y = d.Y + (size_t)p * d.q3() + m;
+    double acc[24];
+#pragma unroll
+    for (int j = 0; j < 24; ++j) acc[j] = 0.0;
+    for (int c = 0; c < Q; ++c) {
+        const double v = __ldg(y + q2 * c);
+#pragma unroll
+        for (int j = 0; j < 24; ++j)
+            if (j < nw) acc[j] += v * wmix[j * Q + c];
+    }
+#pragma unroll
+    for (int j = 0; j < 24; ++j)
+        if (j < nw) {
+            const int prob = p * S + j / 6, jj = j % 6;
+            d.Smix[((size_t)prob * 6 + jj) * q2 + m] = acc[j];
+        }
+}
+
 // Per problem: pick the first GEVD attempt whose pencil is invertible, has a
 // real Schur form and gives non-degenerate a1 columns (cp_als.cpp:110-150).
 __global__ void gevd_pencil_kernel(AlsDev d) {
@@ -898,6 +929,52 @@ struct HrowB {  // B(prob, j, k) = H[prob][j][k]
     size_t q2;
     __device__ double operator()(int prob, int j, int k) const { return H[(size_t)prob * R * q2 + (size_t)j * q2 + k]; }
 };
+// pointer functors for the pipelined GEVD GEMMs (Q even)
+struct Y0PA {  // &Y[p][m + Q k]   (Y_(0), M-fast)
+    const double* Y;
+    size_t q3;
+    int Q;
+    __device__ const double* operator()(int p, int m, int k) const { return Y + (size_t)p * q3 + m + (size_t)Q * k; }
+};
+struct Y0PB {  // &Y[p][n + Q k]   (Y_(0)^T, N-fast)
+    const double* Y;
+    size_t q3;
+    int Q;
+    __device__ const double* operator()(int p, int k, int n) const { return Y + (size_t)p * q3 + n + (size_t)Q * k; }
+};
+struct Y1PA {  // &Y[p][a + Q b + Q^2 c], k = a + Q c   (Y_(1), K-fast)
+    const double* Y;
+    size_t q3;
+    int Q;
+    __device__ const double* operator()(int p, int b, int k) const {
+        const int a = k % Q, c = k / Q;
+        return Y + (size_t)p * q3 + a + (size_t)Q * b + (size_t)Q * Q * c;
+    }
+};
+struct Y1PB {
+    const double* Y;
+    size_t q3;
+    int Q;
+    __device__ const double* operator()(int p, int k, int b) const {
+        const int a = k % Q, c = k / Q;
+        return Y + (size_t)p * q3 + a + (size_t)Q * b + (size_t)Q * Q * c;
+    }
+};
+struct Y0tP {  // &Y[p][k + Q m]   (Y_(0)^T rows: m = b + Q c, K = a contiguous)
+    const double* Y;
+    size_t q3;
+    int Q;
+    __device__ const double* operator()(int p, int m, int k) const { return Y + (size_t)p * q3 + k + (size_t)Q * m; }
+};
+struct HtStore {  // C(p, m, n) -> H[p S + n / R][n % R][m]
+    double* H;
+    int S, R;
+    size_t q2;
+    __device__ void operator()(int p, int m, int n, double v) const {
+        const int prob = p * S + n / R;
+        H[(size_t)prob * R * q2 + (size_t)(n % R) * q2 + m] = v;
+    }
+};
 struct HStore {  // H[prob][r][k]: row r of h contiguous (the peel reads H_r = h(r, :) whole)
     double* H;
     int R;
@@ -1066,10 +1143,18 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         usable.upload(ones.data(), P, st);
         const int ks = pick_ksplit(P, Q, Q, (int)q2);
         ws.reserve((size_t)P * ks * q2);
-        gemm_f64<false, false>(P, Q, Q, (int)q2, Y0A{dY, q3, Q}, Y0B{dY, q3, Q},
-                                                GevStore{Gev.p, Q, 0}, st, ks, ws.p);
-        gemm_f64<true, true>(P, Q, Q, (int)q2, Y1A{dY, q3, Q}, Y1B{dY, q3, Q}, GevStore{Gev.p, Q, 1},
-                                              st, ks, ws.p);
+        const bool gpipe = (Q % 2 == 0) && ((uintptr_t)dY % 16 == 0);
+        if (gpipe) {
+            gemm_f64_pipe<false, Y0PA, Y0PB, GevStore, false>(P, Q, Q, (int)q2, Y0PA{dY, q3, Q}, Y0PB{dY, q3, Q},
+                                                              GevStore{Gev.p, Q, 0}, st, ks, ws.p);
+            gemm_f64_pipe<true>(P, Q, Q, (int)q2, Y1PA{dY, q3, Q}, Y1PB{dY, q3, Q}, GevStore{Gev.p, Q, 1}, st, ks,
+                                ws.p);
+        } else {
+            gemm_f64<false, false>(P, Q, Q, (int)q2, Y0A{dY, q3, Q}, Y0B{dY, q3, Q}, GevStore{Gev.p, Q, 0}, st, ks,
+                                   ws.p);
+            gemm_f64<true, true>(P, Q, Q, (int)q2, Y1A{dY, q3, Q}, Y1B{dY, q3, Q}, GevStore{Gev.p, Q, 1}, st, ks,
+                                 ws.p);
+        }
         size_t smem_eig = (q2 + 2 * (Q + 2) + 1024 / 32 + 4) * sizeof(double) + (2 * Q + 16) * sizeof(int) + 64;
         const int v_in_smem = (smem_eig + q2 * sizeof(double) <= 220 * 1024) ? 1 : 0;
         if (v_in_smem) smem_eig += q2 * sizeof(double);
@@ -1081,8 +1166,17 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         gevd_eig_sym_kernel<<<P * 2, 256, smem_eig, st>>>(d, v_in_smem, use_sub); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
         // mixtures -> p1/p2 for all attempts
-        gemm_f64<false, true>(NP, (int)q2, 6, Q, YmatA{dY, q3, q2, S, true}, MixB{Wmix.p, Q},
-                                               MixStore{Smix.p, q2}, st);
+        if (S <= 4) {
+            const size_t smem_mix = (size_t)S * 6 * Q * sizeof(double);
+            if (smem_mix > 48 * 1024)
+                OCTEN_CUDA(cudaFuncSetAttribute(gevd_mix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem_mix));
+            gevd_mix_kernel<<<dim3((unsigned)((q2 + 255) / 256), P), 256, smem_mix, st>>>(d);
+            OCTEN_LAUNCHED(1);
+        } else {
+            gemm_f64<false, true>(NP, (int)q2, 6, Q, YmatA{dY, q3, q2, S, true}, MixB{Wmix.p, Q}, MixStore{Smix.p, q2},
+                                  st);
+        }
         gemm_f64<false, false>(NP * 6, Q, R, Q, SmA{Smix.p, Q}, UrB{Ur.p, Q, R, S, 1},
                                                 Tmp6Store{Tmp6.p, Q, R}, st);
         gemm_f64<true, false>(NP * 6, R, R, Q, UrTA{Ur.p, Q, R, S}, Tmp6B{Tmp6.p, Q, R},
@@ -1101,8 +1195,14 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             const size_t smem_pen = (size_t)(5 * R * R + 7 * R + 72) * sizeof(double);
             gevd_pencil_kernel<<<NP, 128, smem_pen, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
-            gemm_f64<false, false>(NP, R, (int)q2, Q, A1tA{F.p, Q, R}, Y0Bp{dY, q3, Q, S},
-                                                    HStore{Hh.p, R, q2}, st);
+            // h = a1^T Y_(0) for all restarts of a replica at once:
+            // H^T (Q^2 x S R) = Y_(0)^T [a1_s...]
+            if (gpipe)
+                gemm_f64_pipe<true>(P, (int)q2, S * R, Q, Y0tP{dY, q3, Q}, FacP{F.p, S, Q, R, 0},
+                                    HtStore{Hh.p, S, R, q2}, st);
+            else
+                gemm_f64<false, false>(NP, R, (int)q2, Q, A1tA{F.p, Q, R}, Y0Bp{dY, q3, Q, S}, HStore{Hh.p, R, q2},
+                                       st);
             const size_t smem_h = (size_t)(3 * R * R + 2 * (R + 2) + (R + 8)) * sizeof(double) + 16;
             OCTEN_CUDA(cudaFuncSetAttribute(gevd_hsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_h));
             gevd_hsolve_kernel<<<NP, 256, smem_h, st>>>(d); OCTEN_LAUNCHED(1);

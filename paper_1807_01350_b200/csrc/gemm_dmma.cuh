@@ -189,7 +189,7 @@ namespace pipe {
 constexpr int BM = 128, BN = 64, BK = 16, ST = 3, PAD = 4;
 constexpr int A_M_FAST_ELEMS = BK * (BM + PAD);  // [k][m]
 constexpr int A_K_FAST_ELEMS = BM * (BK + PAD);  // [m][k]
-constexpr int B_ELEMS = BN * (BK + PAD);         // [n][k]
+constexpr int B_ELEMS = BN * (BK + PAD);         // [n][k] (K-fast B) or [k][n] with BK * (BN + PAD) <= B_ELEMS
 template <bool A_KFAST>
 constexpr int a_elems() {
     return A_KFAST ? A_K_FAST_ELEMS : A_M_FAST_ELEMS;
@@ -210,7 +210,7 @@ __device__ __forceinline__ void wait() {
 }
 }  // namespace pipe
 
-template <bool A_KFAST, class AF, class BF, class CF>
+template <bool A_KFAST, class AF, class BF, class CF, bool B_KFAST = true>
 __global__ void __launch_bounds__(256)
     gemm_dmma_pipe_kernel(int M, int N, int K, int ksplit, int kchunk, AF af, BF bf, CF cf, double* partial) {
     using namespace pipe;
@@ -251,10 +251,17 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const int c = tid + r * 256;  // 512 chunks
-            const int nn = c >> 3, kk = (c & 7) * 2;
-            const int gn = n0 + nn, gk = k0 + kk;
-            const bool v = gn < N && gk < kend;
-            cp16(bs + nn * (BK + PAD) + kk, v ? bf(batch, gk, gn) : dummy, v);
+            if (B_KFAST) {
+                const int nn = c >> 3, kk = (c & 7) * 2;
+                const int gn = n0 + nn, gk = k0 + kk;
+                const bool v = gn < N && gk < kend;
+                cp16(bs + nn * (BK + PAD) + kk, v ? bf(batch, gk, gn) : dummy, v);
+            } else {  // pairs (n, n+1): [k][n] layout
+                const int kk = c >> 5, nn = (c & 31) * 2;
+                const int gn = n0 + nn, gk = k0 + kk;
+                const bool v = gn < N && gk < kend;
+                cp16(bs + kk * (BN + PAD) + nn, v ? bf(batch, gk, gn) : dummy, v);
+            }
         }
     };
 
@@ -285,7 +292,8 @@ __global__ void __launch_bounds__(256)
                 fa[i] = A_KFAST ? as[m * (BK + PAD) + kk + t4] : as[(kk + t4) * (BM + PAD) + m];
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) fb[j] = bs[(wn + j * 8 + g) * (BK + PAD) + kk + t4];
+            for (int j = 0; j < 4; ++j)
+                fb[j] = B_KFAST ? bs[(wn + j * 8 + g) * (BK + PAD) + kk + t4] : bs[(kk + t4) * (BN + PAD) + wn + j * 8 + g];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(256)
             }
 }
 
-template <bool A_KFAST, class AF, class BF, class CF>
+template <bool A_KFAST, class AF, class BF, class CF, bool B_KFAST = true>
 void gemm_f64_pipe(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaStream_t st, int ksplit = 1,
                    double* workspace = nullptr) {
     if (batches <= 0 || M <= 0 || N <= 0) return;
@@ -320,12 +328,13 @@ void gemm_f64_pipe(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaSt
     const size_t smem = pipe::smem_bytes<A_KFAST>();
     static bool attr = false;
     if (!attr) {
-        OCTEN_CUDA(cudaFuncSetAttribute(gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF>,
+        OCTEN_CUDA(cudaFuncSetAttribute(gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF, B_KFAST>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     dim3 grid((N + pipe::BN - 1) / pipe::BN, (M + pipe::BM - 1) / pipe::BM, batches * ksplit);
-    gemm_dmma_pipe_kernel<A_KFAST><<<grid, 256, smem, st>>>(M, N, K, ksplit, kchunk, af, bf, cf, workspace);
+    gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF, B_KFAST><<<grid, 256, smem, st>>>(M, N, K, ksplit, kchunk, af, bf, cf,
+                                                                                 workspace);
     OCTEN_LAUNCHED(1);
     if (ksplit > 1) {
         const size_t total = (size_t)batches * M * N;
