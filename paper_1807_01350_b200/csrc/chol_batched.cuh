@@ -486,6 +486,118 @@ __global__ void __launch_bounds__(256) chol_bwd_step_kernel(const double* L, int
     if (jq == 0 && i < k0) y[i] -= acc;
 }
 
+// Whole solve L L^T x = b in ONE CTA per (right-hand side, matrix): the
+// vector lives in shared memory and the 2 * nblk block steps are separated
+// by barriers instead of kernel launches.  Forward step k: x_k <- Linv_k x_k,
+// then every later row i: x_i -= L(i, k-block) x_k (threads along rows,
+// coalesced column reads).  Backward step k: x_k <- Linv_k^T x_k, then every
+// earlier row i: x_i -= L(k-block, i) . x_k (one warp per row, lanes along
+// the contiguous block row, shuffle reduction).  All right-hand sides and
+// matrices run concurrently, one SM each, each streaming its factor once per
+// direction.
+constexpr int kSolveThreads = 1024;
+
+__global__ void __launch_bounds__(kSolveThreads) chol_solve_cta_kernel(const double* L, int n, int ldl, long long sL,
+                                                                    const double* linv, int nblk, double* X, int ldx,
+                                                                    long long sX) {
+    extern __shared__ double xs[];  // n (+ 64 padding) + 16 * 64 partials
+    double* part = xs + n + kCholNB;
+    const int b = blockIdx.y, r = blockIdx.x;
+    const double* Lb = L + (size_t)b * sL;
+    const double* ivb = linv + (size_t)b * nblk * kCholNB * kCholNB;
+    double* x = X + (size_t)b * sX + (size_t)r * ldx;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < n + kCholNB; i += kSolveThreads) xs[i] = i < n ? x[i] : 0.0;
+    __syncthreads();
+    // 64 x 64 (transposed) block mat-vec in place on xs[k0 .. k0+64):
+    // thread (row t, group q of 4 columns); 16 partials per row
+    auto block_matvec = [&](const double* iv, int k0, int nb, bool transposed) {
+        const int t = tid & 63, q = tid >> 6;  // q in 0..15
+        double acc = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int j = 4 * q + jj;
+            const double m = transposed ? iv[j + kCholNB * t] : iv[t + kCholNB * j];
+            acc += m * xs[k0 + j];
+        }
+        part[q * kCholNB + t] = acc;
+        __syncthreads();
+        if (tid < kCholNB) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int qq = 0; qq < 16; ++qq) sacc += part[qq * kCholNB + tid];
+            if (tid < nb) xs[k0 + tid] = sacc;
+        }
+        __syncthreads();
+    };
+    for (int kb = 0; kb < nblk; ++kb) {
+        const int k0 = kb * kCholNB, nb = min(kCholNB, n - k0);
+        block_matvec(ivb + (size_t)kb * kCholNB * kCholNB, k0, nb, false);
+        for (int i = k0 + nb + tid; i < n; i += kSolveThreads) {
+            // 16 independent loads in flight per batch (memory-level
+            // parallelism is what bounds a single-SM stream)
+            const double* col = Lb + i + (size_t)ldl * k0;
+            double sacc = 0.0;
+            for (int j0 = 0; j0 < nb; j0 += 16) {
+                double v[16];
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) v[jj] = (j0 + jj < nb) ? __ldg(col + (size_t)ldl * (j0 + jj)) : 0.0;
+                double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                for (int jj = 0; jj < 16; jj += 2) {
+                    s0 += v[jj] * xs[k0 + j0 + jj];
+                    s1 += v[jj + 1] * xs[k0 + j0 + jj + 1];
+                }
+                sacc += s0 + s1;
+            }
+            xs[i] -= sacc;
+        }
+        __syncthreads();
+    }
+    for (int kb = nblk - 1; kb >= 0; --kb) {
+        const int k0 = kb * kCholNB, nb = min(kCholNB, n - k0);
+        block_matvec(ivb + (size_t)kb * kCholNB * kCholNB, k0, nb, true);
+        const double x0 = xs[k0 + lane], x1 = xs[k0 + 32 + lane];  // zero past nb (Linv padding)
+        // 8 rows per warp pass: 16 independent loads per lane in flight
+        constexpr int RW = 8;
+        for (int i0 = warp * RW; i0 < k0; i0 += (kSolveThreads / 32) * RW) {
+            double acc[RW];
+#pragma unroll
+            for (int rr = 0; rr < RW; ++rr) {
+                const int i = i0 + rr;
+                const double* row = Lb + k0 + (size_t)ldl * i;  // L(k0 + j, i), j contiguous
+                const double a0 = (i < k0 && lane < nb) ? __ldg(row + lane) : 0.0;
+                const double a1 = (i < k0 && lane + 32 < nb) ? __ldg(row + lane + 32) : 0.0;
+                acc[rr] = a0 * x0 + a1 * x1;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int rr = 0; rr < RW; ++rr) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], o);
+            if (lane < RW && i0 + lane < k0) {
+                double v = acc[0];
+#pragma unroll
+                for (int rr = 1; rr < RW; ++rr)
+                    if (lane == rr) v = acc[rr];
+                xs[i0 + lane] -= v;
+            }
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < n; i += kSolveThreads) x[i] = xs[i];
+}
+
+inline void chol_solve_cta(const double* L, int n, int ldl, long long sL, const DevBuf<double>& linv, double* X,
+                           int ldx, long long sX, int nrhs, int batch, cudaStream_t st) {
+    if (n <= 0 || nrhs <= 0 || batch <= 0) return;
+    const int nblk = (n + kCholNB - 1) / kCholNB;
+    const size_t smem = (size_t)(n + kCholNB + 16 * kCholNB) * sizeof(double);
+    if (smem > 48 * 1024)
+        OCTEN_CUDA(cudaFuncSetAttribute(chol_solve_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    chol_solve_cta_kernel<<<dim3(nrhs, batch), kSolveThreads, smem, st>>>(L, n, ldl, sL, linv.p, nblk, X, ldx, sX);
+    OCTEN_LAUNCHED(1);
+}
+
 // Solve L L^T x = b in place (X) using the diagonal-block inverses from
 // chol_batched; Y is scratch of the same layout.
 inline void chol_solve_blocked(const double* L, int n, int ldl, long long sL, const DevBuf<double>& linv, double* X,

@@ -980,8 +980,8 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
                 OCTEN_CUDA(cudaMemcpyAsync(Y1.p + (size_t)p * d * R, g1.p, sizeof(double) * d * R,
                                            cudaMemcpyDeviceToDevice, st));
             OCTEN_CUDA(cudaMemcpyAsync(Y2.p, g2.p, sizeof(double) * P * d * R, cudaMemcpyDeviceToDevice, st));
-            chol_solve_blocked(Gj.p, (int)d, (int)d, d * d, linvj, Y1.p, (int)d, d * R, R, P, st);
-            chol_solve_blocked(Gj.p, (int)d, (int)d, d * d, linvj, Y2.p, (int)d, d * R, R, P, st);
+            chol_solve_cta(Gj.p, (int)d, (int)d, d * d, linvj, Y1.p, (int)d, d * R, R, P, st);
+            chol_solve_cta(Gj.p, (int)d, (int)d, d * d, linvj, Y2.p, (int)d, d * R, R, P, st);
             if (P > 1) {
                 pair_rms_kernel<<<P - 1, 256, 0, st>>>(P, Q, sh, R, d, n, g1.p, Y1.p, g2.p, Y2.p, RF.p, SC.p, rmsb.p);
                 OCTEN_LAUNCHED(1);
@@ -1023,7 +1023,7 @@ void MergeEngine::solve_nontemporal(int n, const double* dStack, double* dOut, c
                            std::to_string(sum_rank[n]) + " of " + std::to_string(d) + ")");
     gemm_f64_splitk<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{dStack, PQ, 0},
                                            StoreCM{dOut, d, 0}, st, kws);
-    chol_solve_blocked(Lsum[n].p, (int)d, (int)d, 0, Lsum_inv[n], dOut, (int)d, 0, R, 1, st);
+    chol_solve_cta(Lsum[n].p, (int)d, (int)d, 0, Lsum_inv[n], dOut, (int)d, 0, R, 1, st);
 }
 
 void MergeEngine::temporal_stack(const double* dY, int p0, int pl, const double* dA, const double* dB, double* dOut,
@@ -1081,7 +1081,7 @@ void MergeEngine::temporal_append(const double* dTstack, const double* dW, std::
     hv.reserve((size_t)t * R);
     OCTEN_CUDA(cudaMemcpyAsync(hv.p, BZ.p + (size_t)t * R, sizeof(double) * t * R, cudaMemcpyDeviceToDevice, st));
     append_dots_kernel<<<R, 256, 0, st>>>(PQ, dTstack, dHist, dots.p); OCTEN_LAUNCHED(1);
-    chol_solve_blocked(Gc.p, (int)t, (int)t, 0, linvc, BZ.p, (int)t, 0, 2 * R, 1, st);
+    chol_solve_cta(Gc.p, (int)t, (int)t, 0, linvc, BZ.p, (int)t, 0, 2 * R, 1, st);
     const int rank_c = rk.to_host(1, st)[0];
     append_decide_kernel<<<R, 256, 0, st>>>(R, t, rank_c, dots.p, hv.p, BZ.p, md.p, dRows, coef.p, err.p,
                                             2 /* temporal mode */); OCTEN_LAUNCHED(1);
@@ -1181,7 +1181,7 @@ void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, dou
                                            ")");
             }
             // each column r against its own factor
-            chol_solve_blocked(Gw.p, (int)d, (int)d, d * d, Gw_inv, sw2.p, (int)d, d, 1, nb, st);
+            chol_solve_cta(Gw.p, (int)d, (int)d, d * d, Gw_inv, sw2.p, (int)d, d, 1, nb, st);
             for (int mi = 0; mi < nmodes; ++mi) {
                 const int n = fused ? mi : gi;
                 OCTEN_CUDA(cudaMemcpyAsync(solved[n].p, sw2.p + (size_t)mi * R * d, sizeof(double) * d * R,
