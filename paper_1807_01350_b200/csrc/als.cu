@@ -1160,7 +1160,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         if (v_in_smem) smem_eig += q2 * sizeof(double);
         // subspace iteration for the top-R block when the matrix is large
         // enough for it to pay and its scratch fits the V region
-        const int mblk = std::min(Q, R + 8);
+        const int mblk = std::min(Q, R + 4);
         const int use_sub = (Q >= 2 * mblk && (size_t)2 * Q * mblk + 2 * mblk * mblk + mblk <= q2) ? mblk : 0;
         OCTEN_CUDA(cudaFuncSetAttribute(gevd_eig_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eig));
         gevd_eig_sym_kernel<<<P * 2, 256, smem_eig, st>>>(d, v_in_smem, use_sub); OCTEN_LAUNCHED(1);

@@ -19,6 +19,9 @@
 #pragma once
 
 #include "octen_common.cuh"
+#if defined(__CUDACC__)
+#include "gemm_dmma.cuh"  // block_dmma_small (device paths of the team routines)
+#endif
 
 namespace octen {
 
@@ -1813,6 +1816,13 @@ OCTEN_HD double top_singular_pair(const Team& team, int m, int n, const double* 
 template <class Team>
 OCTEN_HD void team_symm_block(const Team& team, int n, const double* a, int m, const double* u,
                               double* w) {
+#if defined(__CUDA_ARCH__)
+    if (team.size() >= 64) {  // a whole block: FP64 tensor cores
+        block_dmma_small(n, m, n, a, 1, n, u, 1, n, w, 1, n);
+        team.sync();
+        return;
+    }
+#endif
     for (int e = team.tid(); e < n * m; e += team.size()) {
         const int i = e % n, j = e / n;
         const double* uj = u + (size_t)n * j;
@@ -1890,12 +1900,24 @@ OCTEN_HD int subspace_eig_top(const Team& team, int n, const double* a, int k, i
         u[e] = (double)(splitmix(0x5eedULL + (uint64_t)e) >> 11) * 0x1.0p-52 - 1.0;
     team.sync();
     if (!team_cgs2(team, n, m, u, cf, red)) return 0;
-    int products = 0, target = 3;
+    // first Rayleigh-Ritz after 6 products: with a gap of ~1e-4 at k (the
+    // compressed low-rank Gram) that is already converged, so one RR suffices
+    int products = 0, target = 6;
     for (;;) {
         team_symm_block(team, n, a, m, u, w);  // W = A U
         ++products;
         if (products >= target) {
             // Rayleigh-Ritz: H = U^T W (symmetrised), H = Hv diag(theta) Hv^T
+#if defined(__CUDA_ARCH__)
+            if (team.size() >= 64) {
+                block_dmma_small(m, m, n, u, n, 1, w, 1, n, hv, 1, m);  // hv: scratch here
+                team.sync();
+                for (int e = team.tid(); e < m * m; e += team.size()) {
+                    const int i = e % m, j = e / m;
+                    h[e] = 0.5 * (hv[i + (size_t)m * j] + hv[j + (size_t)m * i]);
+                }
+            } else
+#endif
             for (int e = team.tid(); e < m * m; e += team.size()) {
                 const int i = e % m, j = e / m;
                 if (i > j) continue;

@@ -352,3 +352,78 @@ def test_history_telescopes(ob):
     _, hs = st.summaries()
     for r in range(4):
         assert np.max(np.abs(shadow.replicas[r].temporal.T @ c_raw - hs[r])) < 1e-8
+
+
+# ------------------------------------------------- full-size property checks
+
+def _truth_stream(ob, dims, R, K0, t, nb, Q, P, sh, seed, iters=30, noise=0.0, dtype="f32"):
+    """Rank-R U(0,1) truth (+ noise) streamed as device batches (fp32: the
+    BASELINE fp32 configs; fp64: exact inputs)."""
+    import torch
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    I, J = dims
+    K = K0 + nb * t
+    A = torch.rand((I, R), generator=g, device="cuda", dtype=torch.float64)
+    B = torch.rand((J, R), generator=g, device="cuda", dtype=torch.float64)
+    C = torch.rand((K, R), generator=g, device="cuda", dtype=torch.float64)
+    x = torch.einsum("kr,jr,ir->kji", C, B, A)
+    if noise:
+        x += noise * x.pow(2).mean().sqrt() * torch.randn(x.shape, generator=g, device="cuda", dtype=torch.float64)
+    xd = (x.to(torch.float32) if dtype == "f32" else x).permute(2, 1, 0)  # (I, J, K) first-index-fastest view
+    cfg = ob.StreamConfig(rank=R, p=P, q=Q, shared=sh, seed=seed,
+                          als=ob.AlsConfig(rank=R, max_iters=iters, rel_tol=1e-8, n_restarts=3))
+    st = ob.init_stream(xd[:, :, :K0], cfg)
+    for b in range(nb):
+        ob.ingest_batch(st, xd[:, :, K0 + b * t:K0 + (b + 1) * t])
+    return st, (A.cpu().numpy(), B.cpu().numpy(), C.cpu().numpy()), x
+
+
+def _fit_gpu(x, m):
+    """fitness (eval.cpp:10-20) of a model against the device tensor (K, J, I)."""
+    import torch
+    f = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in m.factors]
+    lam = torch.from_numpy(np.asarray(m.lambda_)).cuda()
+    xh = torch.einsum("kr,jr,ir->kji", f[2] * lam[None, :], f[1], f[0])
+    return 100.0 * (1.0 - float((x - xh).norm() / x.norm()))
+
+
+def test_c3_scale_noiseless_stream_recovers_truth(ob):
+    # BASELINE c3 shapes (I=J=1000, Q=100, P=16, R=20, batches of 100 after
+    # K0=1000; shared=10, DESIGN.md §4), exact (fp64) inputs, two batches: the
+    # model recovers the ground truth (size-independent property)
+    st, (A, B, C), x = _truth_stream(ob, (1000, 1000), 20, 1000, 100, 2, 100, 16, 10, 3, dtype="f64")
+    m = st.model
+    assert st.slices_seen == 1200
+    truth = O.KruskalModel([A, B, C], np.ones(20))
+    assert min(O.congruence(truth, O.KruskalModel(m.factors, m.lambda_))) > 0.999
+    for rec in st.log:
+        assert rec.temporal_residual < 1e-6
+
+
+def test_c3_scale_fp32_compression_within_tolerance(ob):
+    # the north-star tolerance at the full c3 batch shape: the fp32 batch
+    # through the split-TF32 tcgen05 path stays within 1e-4 relative Frobenius
+    # error of the exact (fp64) compression of the same values, every replica
+    I = J = 1000
+    t, Q, P, sh = 100, 100, 16, 10
+    rs = O.gen_replicas([I, J], Q, P, sh, 55)
+    O.extend_temporal(rs, t)
+    u = [r.nontemporal[0] for r in rs.replicas]
+    v = [r.nontemporal[1] for r in rs.replicas]
+    w = [r.temporal for r in rs.replicas]
+    x = rng.Substream(9).uniform01_array(I * J * t).reshape((I, J, t), order="F").astype(np.float32)
+    z32 = ob.compress(x, u, v, w, sh)
+    z64 = ob.compress(x.astype(np.float64), u, v, w, sh)
+    for a, b in zip(z32, z64):
+        assert rel(a, b) < 1e-4
+
+
+def test_c5_shapes_noiseless_stream_recovers_truth(ob):
+    # BASELINE c5 per-GPU shapes (I=J=2000, Q=128, P=32, R=32; shared=32 <= 67
+    # per the replica bound, SURVEY §8d), exact inputs, a short stream
+    st, (A, B, C), x = _truth_stream(ob, (2000, 2000), 32, 200, 200, 1, 128, 32, 32, 5, iters=30, dtype="f64")
+    m = st.model
+    assert all(np.isfinite(f).all() for f in m.factors) and np.isfinite(m.lambda_).all()
+    truth = O.KruskalModel([A, B, C], np.ones(32))
+    assert min(O.congruence(truth, O.KruskalModel(m.factors, m.lambda_))) > 0.999
