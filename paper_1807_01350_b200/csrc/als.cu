@@ -436,11 +436,13 @@ __global__ void als_init_state_kernel(AlsDev d) {
 
 // ---------------- sweeps ----------------
 
-// MTTKRP of mode 0 (a,r) = sum_b T(a,b,r) B(b,r) and of mode 1
-// (b,r) = sum_a T(a,b,r) A(a,r), from T = Y x3 C.  One block per
-// (problem, r); the 8 warps split the b range, lanes run along the contiguous
-// a index of T; mode 0 partials are combined across warps in fixed order.
-__global__ void __launch_bounds__(256) als_mttkrp_T_kernel(AlsDev d, int mode) {
+// MTTKRP from a partial contraction T(u, v, r) (row u + Q v of the
+// per-replica T, column s R + r): contract_first == 0 gives
+// M(u, r) = sum_v T(u,v,r) F_fsrc(v,r), contract_first == 1 gives
+// M(v, r) = sum_u T(u,v,r) F_fsrc(u,r).  One block per (problem, r); the 8
+// warps split the v range, lanes run along the contiguous u index of T; the
+// contract-v partials are combined across warps in fixed order.
+__global__ void __launch_bounds__(256) als_mttkrp_T_kernel(AlsDev d, int contract_first, int fsrc) {
     const int R = d.R, Q = d.Q;
     const int prob = blockIdx.x / R, r = blockIdx.x % R;
     if (!d.state[prob].active) return;
@@ -450,8 +452,8 @@ __global__ void __launch_bounds__(256) als_mttkrp_T_kernel(AlsDev d, int mode) {
     double* M = d.Mb + (size_t)prob * Q * R + (size_t)Q * r;
     constexpr int MAXA = 8;  // Q <= 256
     __shared__ double part[8][257];
-    if (mode == 0) {
-        const double* B = d.f(prob, 1) + (size_t)Q * r;
+    if (!contract_first) {
+        const double* B = d.f(prob, fsrc) + (size_t)Q * r;
         double acc[MAXA];
 #pragma unroll
         for (int i = 0; i < MAXA; ++i) acc[i] = 0.0;
@@ -477,7 +479,7 @@ __global__ void __launch_bounds__(256) als_mttkrp_T_kernel(AlsDev d, int mode) {
             M[a] = sum;
         }
     } else {
-        const double* A = d.f(prob, 0) + (size_t)Q * r;
+        const double* A = d.f(prob, fsrc) + (size_t)Q * r;
         double av[MAXA];
 #pragma unroll
         for (int i = 0; i < MAXA; ++i) {
@@ -495,35 +497,6 @@ __global__ void __launch_bounds__(256) als_mttkrp_T_kernel(AlsDev d, int mode) {
             }
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if (lane == 0) M[b] = acc;
-        }
-    }
-}
-
-// KR[p][(a + Q b), s R + r] = A(a,r) B(b,r)
-__global__ void __launch_bounds__(256) als_kr_kernel(AlsDev d) {
-    // one block per (r, problem): the Q^2 column of KR, coalesced writes
-    const int r = blockIdx.x, prob = blockIdx.y;
-    const int Q = d.Q, R = d.R;
-    if (!d.state[prob].active) return;
-    __shared__ double av[256], bv[256];
-    for (int i = threadIdx.x; i < Q; i += blockDim.x) {
-        av[i] = d.f(prob, 0)[i + (size_t)Q * r];
-        bv[i] = d.f(prob, 1)[i + (size_t)Q * r];
-    }
-    __syncthreads();
-    const int p = prob / d.S, s = prob % d.S;
-    double* K = d.KR + (size_t)p * d.q2() * d.S * R + d.q2() * (size_t)(s * R + r);
-    const int q2 = Q * Q;
-    // e = a + Q b, walked as (b, a) to avoid a division per element
-    int b = threadIdx.x / Q, a = threadIdx.x % Q;
-    const int db = blockDim.x / Q, da = blockDim.x % Q;
-    for (int e = threadIdx.x; e < q2; e += blockDim.x) {
-        K[e] = av[a] * bv[b];
-        a += da;
-        b += db;
-        if (a >= Q) {
-            a -= Q;
-            ++b;
         }
     }
 }
@@ -758,6 +731,21 @@ struct YmatA {  // A(p, m, k) = Y[p][m + Q^2 k]   (Y as Q^2 x Q)
         return Y[(size_t)p * q3 + m + q2 * k];
     }
 };
+struct YmidA {  // A(p, m, k) = Y[p][i + Q k + Q^2 c], m = i + Q c   (rows of Y x2)
+    const double* Y;
+    size_t q3;
+    int Q;
+    __device__ double operator()(int p, int m, int k) const {
+        const int c = m / Q, i = m - c * Q;
+        return Y[(size_t)p * q3 + i + (size_t)Q * (k + (size_t)Q * c)];
+    }
+};
+struct Y0tA {  // A(p, m, k) = Y[p][k + Q m]   (rows of Y x1: m = b + Q c)
+    const double* Y;
+    size_t q3;
+    int Q;
+    __device__ double operator()(int p, int m, int k) const { return Y[(size_t)p * q3 + k + (size_t)Q * m]; }
+};
 struct FacB {  // B(p, k, n) = F[(p S + n / R)][mode][k + Q (n % R)]
     const double* F;
     int S, Q, R, mode;
@@ -787,34 +775,13 @@ struct FacP {  // &F[(p S + n / R)][mode][k + Q (n % R)]   (K-fast)
         return F + ((size_t)prob * 3 + mode) * Q * R + k + (size_t)Q * (n % R);
     }
 };
-struct YtP {  // &Y[p][k + Q^2 c]   (K-fast)
+struct YmidP {  // &Y[p][i + Q k + Q^2 c], m = i + Q c   (Y x2: rows (i, c), M-fast in runs of Q)
     const double* Y;
-    size_t q3, q2;
-    __device__ const double* operator()(int p, int c, int k) const { return Y + (size_t)p * q3 + k + q2 * c; }
-};
-struct KRP {  // &KR[p][k + Q^2 n]   (K-fast)
-    const double* K;
-    size_t q2;
-    int SR;
-    __device__ const double* operator()(int p, int k, int n) const { return K + (size_t)p * q2 * SR + k + q2 * n; }
-};
-struct YtA {  // A(p, c, k) = Y[p][k + Q^2 c]   (Y_(2)^T rows)
-    const double* Y;
-    size_t q3, q2;
-    __device__ double operator()(int p, int c, int k) const { return Y[(size_t)p * q3 + k + q2 * c]; }
-};
-struct KRB {  // B(p, k, n) = KR[p][k + Q^2 n]  (materialized Khatri-Rao product)
-    const double* K;
-    size_t q2;
-    int SR;
-    __device__ double operator()(int p, int k, int n) const { return K[(size_t)p * q2 * SR + k + q2 * n]; }
-};
-struct M2Store {  // -> Mb[p S + n/R][c + Q (n%R)]
-    double* M;
-    int S, Q, R;
-    __device__ void operator()(int p, int c, int n, double v) const {
-        const int prob = p * S + n / R;
-        M[(size_t)prob * Q * R + c + (size_t)Q * (n % R)] = v;
+    size_t q3;
+    unsigned Q, qinv;  // qinv = ceil(2^32 / Q): m / Q = umulhi(m, qinv) for m Q < 2^32
+    __device__ const double* operator()(int p, int m, int k) const {
+        const unsigned c = __umulhi((unsigned)m, qinv), i = (unsigned)m - c * Q;
+        return Y + (size_t)p * q3 + i + (size_t)Q * (k + (size_t)Q * c);
     }
 };
 // GEVD Grams
@@ -1254,8 +1221,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
 
     // ---- sweeps
     const int SR = S * R;
-    const int ks_m2 = pick_ksplit(P, Q, SR, (int)q2);
-    ws.reserve(std::max<size_t>(ws.n, (size_t)P * ks_m2 * Q * SR));
+    const unsigned qinv = (unsigned)((0x100000000ull + (unsigned)Q - 1) / (unsigned)Q);
     const int upd_threads = 256;
     const size_t smem_upd = (size_t)(4 * R * R + 2 * Q * R + R + 2 * (R + 2) + upd_threads) * sizeof(double) + (R + 8) * sizeof(int) + 16;
     OCTEN_CUDA(cudaFuncSetAttribute(als_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_upd));
@@ -1284,7 +1250,6 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     ls[0] = st;
     for (int l = 1; l < L; ++l) ls[l] = lane_st[l];
     active_count.reserve(kMaxLanes);
-    ws2.reserve(ws.n * (L - 1) + 1);
     AlsDev dl[kMaxLanes];
     for (int l = 0; l < L; ++l) {
         const int pb = lp0[l], pn = lp1[l] - lp0[l], qb = pb * S;
@@ -1314,35 +1279,82 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     }
     int* hcount = nullptr;  // [parity][lane]
     OCTEN_CUDA(cudaMallocHost(&hcount, 2 * kMaxLanes * sizeof(int)));
+    // OCTEN_ALS_PROFILE: CUDA events between the kernels of lane 0's sweeps
+    static const bool want_prof = std::getenv("OCTEN_ALS_PROFILE") != nullptr;
+    constexpr int kProfPh = 6;
+    std::vector<cudaEvent_t> pev;
+    if (want_prof) {
+        pev.resize((size_t)max_iters * (kProfPh + 1));
+        for (cudaEvent_t& e : pev) OCTEN_CUDA(cudaEventCreate(&e));
+    }
+    auto mark = [&](int l, int sw, int ph, cudaStream_t ss) {
+        if (want_prof && l == 0) OCTEN_CUDA(cudaEventRecord(pev[(size_t)sw * (kProfPh + 1) + ph], ss));
+    };
     auto launch_sweep = [&](int l, int sw, bool offset_wait) {
         const AlsDev& x = dl[l];
         cudaStream_t ss = ls[l];
         const int pn = x.P, npn = x.NP;
-        double* wsl = l == 0 ? ws.p : ws2.p + (size_t)(l - 1) * ws.n;
         OCTEN_CUDA(cudaMemsetAsync(x.active_count, 0, sizeof(int), ss));
         // lane l starts its first sweep after lane l-1's first T-GEMM
         if (offset_wait) OCTEN_CUDA(cudaStreamWaitEvent(ss, lane_ev[1 + l - 1], 0));
-        // T = Y x3 C  (Q^2 x SR per replica)
-        if (pipe_ok)
-            gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmatP{x.Y, q3, q2}, FacP{x.F, S, Q, R, 2}, TStore{x.T, q2, SR},
-                                 ss);
-        else
-            gemm_f64<false, true>(pn, (int)q2, SR, Q, YmatA{x.Y, q3, q2, S, false}, FacB{x.F, S, Q, R, 2},
-                                  TStore{x.T, q2, SR}, ss);
-        if (sw == 0 && l + 1 < L) OCTEN_CUDA(cudaEventRecord(lane_ev[1 + l], ss));
-        als_mttkrp_T_kernel<<<npn * R, 256, 0, ss>>>(x, 0); OCTEN_LAUNCHED(1);
-        als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, 0, sw); OCTEN_LAUNCHED(1);
-        als_mttkrp_T_kernel<<<npn * R, 256, 0, ss>>>(x, 1); OCTEN_LAUNCHED(1);
-        als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, 1, sw); OCTEN_LAUNCHED(1);
-        als_kr_kernel<<<dim3(R, npn), 256, 0, ss>>>(x);
-        OCTEN_LAUNCHED(1);
-        if (pipe_ok)
-            gemm_f64_pipe<true>(pn, Q, SR, (int)q2, YtP{x.Y, q3, q2}, KRP{x.KR, q2, SR}, M2Store{x.Mb, S, Q, R}, ss,
-                                ks_m2, wsl);
-        else
-            gemm_f64<true, true>(pn, Q, SR, (int)q2, YtA{x.Y, q3, q2}, KRB{x.KR, q2, SR}, M2Store{x.Mb, S, Q, R}, ss,
-                                 ks_m2, wsl);
-        als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, 2, sw); OCTEN_LAUNCHED(1);
+        // Dimension tree over sweep pairs: consecutive mode updates that leave
+        // one factor untouched share the partial contraction with it.
+        //   even sweep: T = Y x3 C -> modes 0 (contract v with B), 1 (contract
+        //               u with A); T = Y x2 B -> mode 2 (contract u with A)
+        //   odd sweep:  the same T -> mode 0 (contract v with C); T = Y x1 A ->
+        //               modes 1 (contract v with C), 2 (contract u with B)
+        // 1.5 Q^3 S R GEMMs per sweep instead of 2 (or 3 without a tree).
+        auto tgemm = [&](int contracted) {
+            if (contracted == 2) {  // rows (i, j)
+                if (pipe_ok)
+                    gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmatP{x.Y, q3, q2}, FacP{x.F, S, Q, R, 2},
+                                         TStore{x.T, q2, SR}, ss);
+                else
+                    gemm_f64<false, true>(pn, (int)q2, SR, Q, YmatA{x.Y, q3, q2, S, false}, FacB{x.F, S, Q, R, 2},
+                                          TStore{x.T, q2, SR}, ss);
+            } else if (contracted == 1) {  // rows (i, k)
+                if (pipe_ok)
+                    gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmidP{x.Y, q3, (unsigned)Q, qinv}, FacP{x.F, S, Q, R, 1},
+                                         TStore{x.T, q2, SR}, ss);
+                else
+                    gemm_f64<false, true>(pn, (int)q2, SR, Q, YmidA{x.Y, q3, Q}, FacB{x.F, S, Q, R, 1},
+                                          TStore{x.T, q2, SR}, ss);
+            } else {  // rows (j, k)
+                if (pipe_ok)
+                    gemm_f64_pipe<true>(pn, (int)q2, SR, Q, Y0tP{x.Y, q3, Q}, FacP{x.F, S, Q, R, 0},
+                                        TStore{x.T, q2, SR}, ss);
+                else
+                    gemm_f64<true, true>(pn, (int)q2, SR, Q, Y0tA{x.Y, q3, Q}, FacB{x.F, S, Q, R, 0},
+                                         TStore{x.T, q2, SR}, ss);
+            }
+        };
+        auto mode_step = [&](int contract_first, int fsrc, int mode) {
+            als_mttkrp_T_kernel<<<npn * R, 256, 0, ss>>>(x, contract_first, fsrc); OCTEN_LAUNCHED(1);
+            als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, mode, sw); OCTEN_LAUNCHED(1);
+        };
+        mark(l, sw, 0, ss);
+        if ((sw & 1) == 0) {
+            tgemm(2);
+            if (sw == 0 && l + 1 < L) OCTEN_CUDA(cudaEventRecord(lane_ev[1 + l], ss));
+            mark(l, sw, 1, ss);
+            mode_step(0, 1, 0);
+            mark(l, sw, 2, ss);
+            mode_step(1, 0, 1);
+            mark(l, sw, 3, ss);
+            tgemm(1);
+            mark(l, sw, 4, ss);
+            mode_step(1, 0, 2);
+        } else {
+            mark(l, sw, 1, ss);
+            mode_step(0, 2, 0);
+            mark(l, sw, 2, ss);
+            tgemm(0);
+            mark(l, sw, 3, ss);
+            mode_step(0, 2, 1);
+            mark(l, sw, 4, ss);
+            mode_step(1, 1, 2);
+        }
+        mark(l, sw, 5, ss);
         OCTEN_CUDA(cudaGetLastError());
         OCTEN_CUDA(cudaMemcpyAsync(hcount + kMaxLanes * (sw & 1) + l, x.active_count, sizeof(int),
                                    cudaMemcpyDeviceToHost, ss));
@@ -1371,6 +1383,31 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     }
     OCTEN_CUDA(cudaStreamSynchronize(st));
     last_sweeps = sweep;
+    if (want_prof) {
+        static const char* names[kProfPh] = {"even:gemm|odd:-", "mode0", "even:mode1|odd:gemm", "even:gemm|odd:mode1",
+                                             "mode2", "gap"};
+        double acc[2][kProfPh] = {};
+        int cnt[2] = {0, 0};
+        for (int s2 = 0; s2 < sweep; ++s2) {
+            ++cnt[s2 & 1];
+            for (int ph = 0; ph < kProfPh; ++ph) {
+                float ms = 0.f;
+                const size_t b = (size_t)s2 * (kProfPh + 1);
+                if (ph + 1 < kProfPh)
+                    OCTEN_CUDA(cudaEventElapsedTime(&ms, pev[b + ph], pev[b + ph + 1]));
+                else if (s2 + 1 < sweep)
+                    OCTEN_CUDA(cudaEventElapsedTime(&ms, pev[b + kProfPh - 1], pev[b + kProfPh + 1]));
+                acc[s2 & 1][ph] += ms;
+            }
+        }
+        for (int e = 0; e < 2; ++e) {
+            std::fprintf(stderr, "octen als lane0 (L=%d, %d sweeps) %s sweeps us:", L, sweep, e ? "odd" : "even");
+            for (int ph = 0; ph < kProfPh; ++ph)
+                std::fprintf(stderr, " %s %.1f", names[ph], cnt[e] ? acc[e][ph] * 1e3 / cnt[e] : 0.0);
+            std::fprintf(stderr, "\n");
+        }
+        for (cudaEvent_t e : pev) cudaEventDestroy(e);
+    }
     if (d.tsc) {
         std::vector<double> raw = tscbuf.to_host(64, st);
         const long long* t = reinterpret_cast<const long long*>(raw.data());

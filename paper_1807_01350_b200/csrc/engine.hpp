@@ -64,7 +64,7 @@ public:
 private:
     void alloc(int P, int S, int Q, int R, int max_iters);
     int P_ = 0, S_ = 0, Q_ = 0, R_ = 0, I_ = 0;
-    DevBuf<double> normx2, F, G, lam, T, KR, Mb, fit_hist, res_hist, ws, ws2, tscbuf;
+    DevBuf<double> normx2, F, G, lam, T, KR, Mb, fit_hist, res_hist, ws, tscbuf;
     static constexpr int kMaxLanes = 4;
     cudaStream_t lane_st[kMaxLanes] = {};   // sweep lanes 1..L-1 (lane 0 runs on the caller's stream)
     cudaEvent_t lane_ev[3 * kMaxLanes] = {};
