@@ -33,6 +33,7 @@ namespace {
 
 constexpr double kDegenerateNorm = 1e-14;  // cp_als.cpp:17
 constexpr double kEps = 2.220446049250313e-16;
+constexpr int kAlsMaxLanes = 4;  // AlsEngine::kMaxLanes
 
 struct AlsDev {
     int P, S, Q, R, NP, max_iters;
@@ -45,13 +46,14 @@ struct AlsDev {
     double* T;
     double* KR;
     double* Mb;
+    double* Vinv;  // per problem R x R: inverse (or pseudo-inverse) of the mode's Hadamard Gram
     double* fit_hist;
     double* res_hist;
     AlsState* state;
     DevStatus* err;
     Mt64* rngs;
     const std::uint64_t* rescue_seed;
-    int* active_count;
+    int* hact;  // host-mapped [sweep][kMaxLanes] "a problem of this lane is still active" flags
     // GEVD
     double* Gev;
     double* EV;
@@ -436,101 +438,22 @@ __global__ void als_init_state_kernel(AlsDev d) {
 
 // ---------------- sweeps ----------------
 
-// MTTKRP from a partial contraction T(u, v, r) (row u + Q v of the
-// per-replica T, column s R + r): contract_first == 0 gives
-// M(u, r) = sum_v T(u,v,r) F_fsrc(v,r), contract_first == 1 gives
-// M(v, r) = sum_u T(u,v,r) F_fsrc(u,r).  One block per (problem, r); the 8
-// warps split the v range, lanes run along the contiguous u index of T; the
-// contract-v partials are combined across warps in fixed order.
-__global__ void __launch_bounds__(256) als_mttkrp_T_kernel(AlsDev d, int contract_first, int fsrc) {
-    const int R = d.R, Q = d.Q;
-    const int prob = blockIdx.x / R, r = blockIdx.x % R;
-    if (!d.state[prob].active) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int p = prob / d.S, s = prob % d.S;
-    const double* tcol = d.T + (size_t)p * d.q2() * d.S * R + (size_t)d.q2() * (s * R + r);
-    double* M = d.Mb + (size_t)prob * Q * R + (size_t)Q * r;
-    constexpr int MAXA = 8;  // Q <= 256
-    __shared__ double part[8][257];
-    if (!contract_first) {
-        const double* B = d.f(prob, fsrc) + (size_t)Q * r;
-        double acc[MAXA];
-#pragma unroll
-        for (int i = 0; i < MAXA; ++i) acc[i] = 0.0;
-#pragma unroll 2
-        for (int b = warp; b < Q; b += nw) {
-            const double w = __ldg(B + b);
-            const double* row = tcol + (size_t)Q * b;
-#pragma unroll
-            for (int i = 0; i < MAXA; ++i) {
-                const int a = lane + 32 * i;
-                if (a < Q) acc[i] += __ldg(row + a) * w;
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < MAXA; ++i) {
-            const int a = lane + 32 * i;
-            if (a < Q) part[warp][a] = acc[i];
-        }
-        __syncthreads();
-        for (int a = threadIdx.x; a < Q; a += blockDim.x) {
-            double sum = 0.0;
-            for (int w = 0; w < nw; ++w) sum += part[w][a];
-            M[a] = sum;
-        }
-    } else {
-        const double* A = d.f(prob, fsrc) + (size_t)Q * r;
-        double av[MAXA];
-#pragma unroll
-        for (int i = 0; i < MAXA; ++i) {
-            const int a = lane + 32 * i;
-            av[i] = a < Q ? __ldg(A + a) : 0.0;
-        }
-#pragma unroll 2
-        for (int b = warp; b < Q; b += nw) {
-            const double* row = tcol + (size_t)Q * b;
-            double acc = 0.0;
-#pragma unroll
-            for (int i = 0; i < MAXA; ++i) {
-                const int a = lane + 32 * i;
-                if (a < Q) acc += __ldg(row + a) * av[i];
-            }
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) M[b] = acc;
-        }
-    }
-}
-
-// One mode update per problem: raw = M V^-1 (COD of the Hadamard Gram;
-// cp_als.cpp:298-323), non-finite check, normalize into lambda with the
-// seeded rescue, new Gram; after mode 2 the fit and the convergence test
-// (cp_als.cpp:325-345).  V^-1 is formed from the Cholesky factor (or the
-// eigen pseudo-inverse when V is numerically singular, matching COD's
-// minimum-norm solve), then raw = M V^-1 is a parallel (Q x R)(R x R) product.
-__global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
-    const int prob = blockIdx.x;
-    AlsState* st = d.state + prob;
-    if (!st->active) return;
-    const int Q = d.Q, R = d.R;
-    extern __shared__ double sm[];
-    double* V = sm;                 // R*R
-    double* Lf = V + R * R;         // R*R
-    double* Ev = Lf + R * R;        // R*R  (eigenvectors / L^-1)
-    double* Vi = Ev + R * R;        // R*R  (V^-1 or V^+)
-    double* raw = Vi + R * R;       // Q*R
-    double* Ms = raw + Q * R;       // Q*R  (staged MTTKRP)
-    double* nrm = Ms + Q * R;       // R
-    double* cs = nrm + R;           // 2(R+2)
-    double* red = cs + 2 * (R + 2); // blockDim
+// V = Hadamard product of the other two modes' Grams, then Vi = V^-1 from
+// the Cholesky factor, or the eigen pseudo-inverse when V is numerically
+// singular (matching COD's minimum-norm solve; cp_als.cpp:298-323).  It needs
+// only the other modes' Grams, so it runs in extra blocks of the MTTKRP launch
+// of the same mode, off the update's critical path.  256 threads; sm holds
+// 4 R^2 + 2 (R + 2) + 256 doubles and R + 8 ints.
+__device__ void als_vinv_block(const AlsDev& d, int prob, int mode, double* sm) {
+    const int R = d.R;
+    double* V = sm;                  // R*R
+    double* Lf = V + R * R;          // R*R
+    double* Ev = Lf + R * R;         // R*R  (eigenvectors / L^-1)
+    double* Vi = Ev + R * R;         // R*R
+    double* cs = Vi + R * R;         // 2(R+2)
+    double* red = cs + 2 * (R + 2);  // blockDim
     int* iw = (int*)(red + blockDim.x);  // R + 8
-    __shared__ int rank, bad;
-    const double* M = Ms;
-#define OCTEN_TSC(i) \
-    if (d.tsc && threadIdx.x == 0 && blockIdx.x == 0) d.tsc[(i)] = clock64();
-    OCTEN_TSC(0)
-    {
-        g2s_copy(Ms, d.Mb + (size_t)prob * Q * R, Q * R);
-    }
+    __shared__ int rank;
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
         double v = 1.0;
         for (int k = 0; k < 3; ++k)
@@ -538,9 +461,7 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
         V[e] = v;
         Lf[e] = v;
     }
-    if (threadIdx.x == 0) bad = 0;
     __syncthreads();
-    OCTEN_TSC(1)
     {
         // Lf = chol(V), Ev = Lf^-1, block-cooperative (R <= 64).  (A fully
         // unrolled one-warp register version measured 3.5x slower: its
@@ -552,7 +473,7 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
         if (threadIdx.x == 0) rank = rk;
     }
     __syncthreads();
-    OCTEN_TSC(2)
+    double* out = d.Vinv + (size_t)prob * R * R;
     if (rank == R) {
         // Vi = L^-T L^-1 on the FP64 tensor cores: Vi(i, j) = sum_k Ev(k, i) Ev(k, j)
         block_dmma_small(R, R, R, Ev, R, 1, Ev, 1, R, Vi, 1, R);
@@ -574,7 +495,140 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
         }
     }
     __syncthreads();
-    OCTEN_TSC(3)
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) out[e] = Vi[e];
+}
+
+// MTTKRP from a partial contraction T(u, v, r) (row u + Q v of the
+// per-replica T, column s R + r): contract_first == 0 gives
+// M(u, r) = sum_v T(u,v,r) F_fsrc(v,r), contract_first == 1 gives
+// M(v, r) = sum_u T(u,v,r) F_fsrc(u,r).  One block per (problem, r); the 8
+// warps split the v range, lanes run along the contiguous u index of T; the
+// contract-v partials are combined across warps in fixed order.
+// One T column (Q x Q, u fastest) against the weight vector w: warps take
+// rows v (U rows per round, all loads issued first), lanes run along u.
+template <int NA>
+__device__ __forceinline__ void mttkrp_column(const double* __restrict__ tcol, const double* __restrict__ w,
+                                              double* __restrict__ M, int Q, int contract_first) {
+    constexpr int U = 4;
+    __shared__ double part[8][257];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (!contract_first) {  // M(u) = sum_v T(u, v) w(v)
+        double acc[NA];
+#pragma unroll
+        for (int i = 0; i < NA; ++i) acc[i] = 0.0;
+        for (int b0 = warp; b0 < Q; b0 += U * nw) {
+            double x[U][NA], wv[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int b = b0 + j * nw;
+                const bool vb = b < Q;
+                wv[j] = vb ? __ldg(w + b) : 0.0;
+                const double* row = tcol + (size_t)Q * b;
+#pragma unroll
+                for (int i = 0; i < NA; ++i) {
+                    const int a = lane + 32 * i;
+                    x[j][i] = (vb && a < Q) ? __ldg(row + a) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j)
+#pragma unroll
+                for (int i = 0; i < NA; ++i) acc[i] += x[j][i] * wv[j];
+        }
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            const int a = lane + 32 * i;
+            if (a < Q) part[warp][a] = acc[i];
+        }
+        __syncthreads();
+        for (int a = threadIdx.x; a < Q; a += blockDim.x) {
+            double sum = 0.0;
+            for (int v = 0; v < nw; ++v) sum += part[v][a];
+            M[a] = sum;
+        }
+    } else {  // M(v) = sum_u T(u, v) w(u)
+        double av[NA];
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            const int a = lane + 32 * i;
+            av[i] = a < Q ? __ldg(w + a) : 0.0;
+        }
+        for (int b0 = warp; b0 < Q; b0 += U * nw) {
+            double acc[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int b = b0 + j * nw;
+                const bool vb = b < Q;
+                const double* row = tcol + (size_t)Q * b;
+                double x[NA];
+#pragma unroll
+                for (int i = 0; i < NA; ++i) {
+                    const int a = lane + 32 * i;
+                    x[i] = (vb && a < Q) ? __ldg(row + a) : 0.0;
+                }
+                acc[j] = 0.0;
+#pragma unroll
+                for (int i = 0; i < NA; ++i) acc[j] += x[i] * av[i];
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                double v = acc[j];
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                const int b = b0 + j * nw;
+                if (lane == 0 && b < Q) M[b] = v;
+            }
+        }
+    }
+}
+
+// The first NP blocks instead form Vi of `mode` (als_vinv_block).
+template <int NA>
+__global__ void __launch_bounds__(256, 3) als_mttkrp_T_kernel(AlsDev d, int contract_first, int fsrc, int mode) {
+    extern __shared__ double vsm[];
+    if ((int)blockIdx.x < d.NP) {
+        if (d.state[blockIdx.x].active) als_vinv_block(d, blockIdx.x, mode, vsm);
+        return;
+    }
+    const int R = d.R, Q = d.Q;
+    const int bid = blockIdx.x - d.NP;
+    const int prob = bid / R, r = bid % R;
+    if (!d.state[prob].active) return;
+    const int p = prob / d.S, s = prob % d.S;
+    const double* tcol = d.T + (size_t)p * d.q2() * d.S * R + (size_t)d.q2() * (s * R + r);
+    double* M = d.Mb + (size_t)prob * Q * R + (size_t)Q * r;
+    const double* w = d.f(prob, fsrc) + (size_t)Q * r;
+    mttkrp_column<NA>(tcol, w, M, Q, contract_first);
+}
+
+// One mode update per problem: raw = M V^-1 (COD of the Hadamard Gram;
+// cp_als.cpp:298-323), non-finite check, normalize into lambda with the
+// seeded rescue, new Gram; after mode 2 the fit and the convergence test
+// (cp_als.cpp:325-345).  V^-1 (als_vinv_block, formed during the MTTKRP)
+// makes raw = M V^-1 a parallel (Q x R)(R x R) product.
+__global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
+    const int prob = blockIdx.x;
+    AlsState* st = d.state + prob;
+    if (!st->active) return;
+    const int Q = d.Q, R = d.R;
+    extern __shared__ double sm[];
+    double* Vi = sm;                // R*R  (V^-1 or V^+, from als_vinv_block)
+    double* raw = Vi + R * R;       // Q*R
+    double* Ms = raw + Q * R;       // Q*R  (staged MTTKRP)
+    double* nrm = Ms + Q * R;       // R
+    double* cs = nrm + R;           // 2(R+2)
+    double* red = cs + 2 * (R + 2); // blockDim
+    __shared__ int bad;
+    const double* M = Ms;
+#define OCTEN_TSC(i) \
+    if (d.tsc && threadIdx.x == 0 && blockIdx.x == 0) d.tsc[(i)] = clock64();
+    OCTEN_TSC(0)
+    {
+        g2s_copy(Ms, d.Mb + (size_t)prob * Q * R, Q * R);
+    }
+    g2s_copy(Vi, d.Vinv + (size_t)prob * R * R, R * R);
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    OCTEN_TSC(1)
     // raw = M Vi on the FP64 tensor cores (Q x R x R)
     block_dmma_small(Q, R, R, M, 1, Q, Vi, 1, R, raw, 1, Q);
     __syncthreads();
@@ -689,7 +743,7 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
             st->iterations = sweep + 1;
             st->active = 0;
         } else {
-            atomicAdd(d.active_count, 1);
+            d.hact[(size_t)sweep * kAlsMaxLanes] = 1;  // host-mapped; visible once the sweep's event completes
         }
     }
 #undef OCTEN_TSC
@@ -965,13 +1019,13 @@ void AlsEngine::alloc(int P, int S, int Q, int R, int max_iters) {
     T.reserve((size_t)P * q2 * S * R);
     KR.reserve((size_t)P * q2 * S * R);
     Mb.reserve(NP * Q * R);
+    Vinv.reserve(NP * R * R);
     fit_hist.reserve(NP * max_iters);
     res_hist.reserve(NP * max_iters);
     state.reserve(NP);
     err.reserve(NP);
     rngs.reserve(NP);
     rescue_seed.reserve(NP);
-    active_count.reserve(1);
     Gev.reserve((size_t)P * 2 * q2);
     EV.reserve((size_t)P * 2 * q2);
     Ur.reserve((size_t)P * 2 * Q * R);
@@ -1003,6 +1057,7 @@ AlsEngine::~AlsEngine() {
             cudaStreamSynchronize(ls);
             cudaStreamDestroy(ls);
         }
+    if (hact) cudaFreeHost(hact);
     for (cudaEvent_t e : lane_ev)
         if (e) cudaEventDestroy(e);
 }
@@ -1038,13 +1093,13 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     d.T = T.p;
     d.KR = KR.p;
     d.Mb = Mb.p;
+    d.Vinv = Vinv.p;
     d.fit_hist = fit_hist.p;
     d.res_hist = res_hist.p;
     d.state = state.p;
     d.err = err.p;
     d.rngs = rngs.p;
     d.rescue_seed = rescue_seed.p;
-    d.active_count = active_count.p;
     d.Gev = Gev.p;
     d.EV = EV.p;
     d.Ur = Ur.p;
@@ -1223,8 +1278,11 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     const int SR = S * R;
     const unsigned qinv = (unsigned)((0x100000000ull + (unsigned)Q - 1) / (unsigned)Q);
     const int upd_threads = 256;
-    const size_t smem_upd = (size_t)(4 * R * R + 2 * Q * R + R + 2 * (R + 2) + upd_threads) * sizeof(double) + (R + 8) * sizeof(int) + 16;
+    const size_t smem_upd = (size_t)(R * R + 2 * Q * R + R + 2 * (R + 2) + upd_threads) * sizeof(double) + 16;
     OCTEN_CUDA(cudaFuncSetAttribute(als_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_upd));
+    const size_t smem_vinv = (size_t)(4 * R * R + 2 * (R + 2) + 256) * sizeof(double) + (R + 8) * sizeof(int) + 16;
+    auto mttkrp_kernel = Q <= 128 ? als_mttkrp_T_kernel<4> : als_mttkrp_T_kernel<8>;
+    OCTEN_CUDA(cudaFuncSetAttribute(mttkrp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_vinv));
     // 16-byte pairs along every fast index need an even Q (and aligned bases)
     const bool pipe_ok = (Q % 2 == 0) && ((uintptr_t)dY % 16 == 0) && ((uintptr_t)F.p % 16 == 0) &&
                          ((uintptr_t)KR.p % 16 == 0);
@@ -1249,7 +1307,15 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     cudaStream_t ls[kMaxLanes];
     ls[0] = st;
     for (int l = 1; l < L; ++l) ls[l] = lane_st[l];
-    active_count.reserve(kMaxLanes);
+    if (hact_n < (size_t)max_iters * kMaxLanes) {
+        if (hact) cudaFreeHost(hact);
+        hact = nullptr;
+        hact_n = (size_t)max_iters * kMaxLanes;
+        OCTEN_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hact), hact_n * sizeof(int), cudaHostAllocMapped));
+    }
+    std::memset(hact, 0, (size_t)max_iters * kMaxLanes * sizeof(int));
+    int* hact_dev = nullptr;
+    OCTEN_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hact_dev), hact, 0));
     AlsDev dl[kMaxLanes];
     for (int l = 0; l < L; ++l) {
         const int pb = lp0[l], pn = lp1[l] - lp0[l], qb = pb * S;
@@ -1265,36 +1331,40 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         x.T = T.p + (size_t)pb * q2 * SR;
         x.KR = KR.p + (size_t)pb * q2 * SR;
         x.Mb = Mb.p + (size_t)qb * Q * R;
+        x.Vinv = Vinv.p + (size_t)qb * R * R;
         x.fit_hist = fit_hist.p + (size_t)qb * max_iters;
         x.res_hist = res_hist.p + (size_t)qb * max_iters;
         x.state = state.p + qb;
         x.err = err.p + qb;
         x.rngs = rngs.p + qb;
         x.rescue_seed = rescue_seed.p + qb;
-        x.active_count = active_count.p + l;
+        x.hact = hact_dev + l;
     }
     if (L > 1) {
         OCTEN_CUDA(cudaEventRecord(lane_ev[0], st));
         for (int l = 1; l < L; ++l) OCTEN_CUDA(cudaStreamWaitEvent(ls[l], lane_ev[0], 0));
     }
-    int* hcount = nullptr;  // [parity][lane]
-    OCTEN_CUDA(cudaMallocHost(&hcount, 2 * kMaxLanes * sizeof(int)));
-    // OCTEN_ALS_PROFILE: CUDA events between the kernels of lane 0's sweeps
+    // OCTEN_ALS_PROFILE: CUDA events between the kernels of lane 0's sweeps,
+    // averaged per sweep parity and label (diagnostics)
     static const bool want_prof = std::getenv("OCTEN_ALS_PROFILE") != nullptr;
-    constexpr int kProfPh = 6;
-    std::vector<cudaEvent_t> pev;
-    if (want_prof) {
-        pev.resize((size_t)max_iters * (kProfPh + 1));
-        for (cudaEvent_t& e : pev) OCTEN_CUDA(cudaEventCreate(&e));
-    }
-    auto mark = [&](int l, int sw, int ph, cudaStream_t ss) {
-        if (want_prof && l == 0) OCTEN_CUDA(cudaEventRecord(pev[(size_t)sw * (kProfPh + 1) + ph], ss));
+    struct ProfMark {
+        int sweep;
+        const char* label;
+        cudaEvent_t ev;
+    };
+    std::vector<ProfMark> pmarks;
+    if (want_prof) pmarks.reserve((size_t)max_iters * 16);
+    auto mark = [&](int l, int sw, const char* label, cudaStream_t ss) {
+        if (!want_prof || l != 0) return;
+        ProfMark m{sw, label, nullptr};
+        OCTEN_CUDA(cudaEventCreate(&m.ev));
+        OCTEN_CUDA(cudaEventRecord(m.ev, ss));
+        pmarks.push_back(m);
     };
     auto launch_sweep = [&](int l, int sw, bool offset_wait) {
         const AlsDev& x = dl[l];
         cudaStream_t ss = ls[l];
         const int pn = x.P, npn = x.NP;
-        OCTEN_CUDA(cudaMemsetAsync(x.active_count, 0, sizeof(int), ss));
         // lane l starts its first sweep after lane l-1's first T-GEMM
         if (offset_wait) OCTEN_CUDA(cudaStreamWaitEvent(ss, lane_ev[1 + l - 1], 0));
         // Dimension tree over sweep pairs: consecutive mode updates that leave
@@ -1329,35 +1399,30 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             }
         };
         auto mode_step = [&](int contract_first, int fsrc, int mode) {
-            als_mttkrp_T_kernel<<<npn * R, 256, 0, ss>>>(x, contract_first, fsrc); OCTEN_LAUNCHED(1);
+            mttkrp_kernel<<<npn * (R + 1), 256, smem_vinv, ss>>>(x, contract_first, fsrc, mode);
+            OCTEN_LAUNCHED(1);
+            mark(l, sw, mode == 0 ? "mttkrp0" : mode == 1 ? "mttkrp1" : "mttkrp2", ss);
             als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, mode, sw); OCTEN_LAUNCHED(1);
+            mark(l, sw, mode == 0 ? "update0" : mode == 1 ? "update1" : "update2", ss);
         };
-        mark(l, sw, 0, ss);
+        mark(l, sw, "start", ss);
         if ((sw & 1) == 0) {
             tgemm(2);
             if (sw == 0 && l + 1 < L) OCTEN_CUDA(cudaEventRecord(lane_ev[1 + l], ss));
-            mark(l, sw, 1, ss);
+            mark(l, sw, "gemm Yx3C", ss);
             mode_step(0, 1, 0);
-            mark(l, sw, 2, ss);
             mode_step(1, 0, 1);
-            mark(l, sw, 3, ss);
             tgemm(1);
-            mark(l, sw, 4, ss);
+            mark(l, sw, "gemm Yx2B", ss);
             mode_step(1, 0, 2);
         } else {
-            mark(l, sw, 1, ss);
             mode_step(0, 2, 0);
-            mark(l, sw, 2, ss);
             tgemm(0);
-            mark(l, sw, 3, ss);
+            mark(l, sw, "gemm Yx1A", ss);
             mode_step(0, 2, 1);
-            mark(l, sw, 4, ss);
             mode_step(1, 1, 2);
         }
-        mark(l, sw, 5, ss);
         OCTEN_CUDA(cudaGetLastError());
-        OCTEN_CUDA(cudaMemcpyAsync(hcount + kMaxLanes * (sw & 1) + l, x.active_count, sizeof(int),
-                                   cudaMemcpyDeviceToHost, ss));
         OCTEN_CUDA(cudaEventRecord(lane_ev[kMaxLanes + kMaxLanes * (sw & 1) + l], ss));
     };
     int sweep = 0;
@@ -1368,7 +1433,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             int left = 0;
             for (int l = 0; l < L; ++l) {
                 OCTEN_CUDA(cudaEventSynchronize(lane_ev[kMaxLanes + kMaxLanes * ((sweep - 1) & 1) + l]));
-                left += hcount[kMaxLanes * ((sweep - 1) & 1) + l];
+                left += reinterpret_cast<volatile int*>(hact)[(size_t)(sweep - 1) * kMaxLanes + l];
             }
             ++host_syncs;
             if (left == 0) {
@@ -1384,42 +1449,47 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     OCTEN_CUDA(cudaStreamSynchronize(st));
     last_sweeps = sweep;
     if (want_prof) {
-        static const char* names[kProfPh] = {"even:gemm|odd:-", "mode0", "even:mode1|odd:gemm", "even:gemm|odd:mode1",
-                                             "mode2", "gap"};
-        double acc[2][kProfPh] = {};
+        // duration of each label = time since the previous mark (any sweep)
+        std::vector<std::string> lab[2];
+        std::vector<double> acc[2];
         int cnt[2] = {0, 0};
-        for (int s2 = 0; s2 < sweep; ++s2) {
-            ++cnt[s2 & 1];
-            for (int ph = 0; ph < kProfPh; ++ph) {
-                float ms = 0.f;
-                const size_t b = (size_t)s2 * (kProfPh + 1);
-                if (ph + 1 < kProfPh)
-                    OCTEN_CUDA(cudaEventElapsedTime(&ms, pev[b + ph], pev[b + ph + 1]));
-                else if (s2 + 1 < sweep)
-                    OCTEN_CUDA(cudaEventElapsedTime(&ms, pev[b + kProfPh - 1], pev[b + kProfPh + 1]));
-                acc[s2 & 1][ph] += ms;
+        int last_sw = -1;
+        for (size_t i = 1; i < pmarks.size(); ++i) {
+            const int e = pmarks[i].sweep & 1;
+            if (pmarks[i].sweep != last_sw && std::string(pmarks[i].label) == "start") ++cnt[pmarks[i].sweep & 1];
+            last_sw = pmarks[i].sweep;
+            float ms = 0.f;
+            OCTEN_CUDA(cudaEventElapsedTime(&ms, pmarks[i - 1].ev, pmarks[i].ev));
+            const std::string key = std::string(pmarks[i].label) == "start" ? "gap" : pmarks[i].label;
+            size_t k = 0;
+            while (k < lab[e].size() && lab[e][k] != key) ++k;
+            if (k == lab[e].size()) {
+                lab[e].push_back(key);
+                acc[e].push_back(0.0);
             }
+            acc[e][k] += ms;
         }
+        cnt[0] += 1;  // sweep 0's start mark is the first mark
         for (int e = 0; e < 2; ++e) {
-            std::fprintf(stderr, "octen als lane0 (L=%d, %d sweeps) %s sweeps us:", L, sweep, e ? "odd" : "even");
-            for (int ph = 0; ph < kProfPh; ++ph)
-                std::fprintf(stderr, " %s %.1f", names[ph], cnt[e] ? acc[e][ph] * 1e3 / cnt[e] : 0.0);
+            std::fprintf(stderr, "octen als lane0 (L=%d, %d sweeps) %s sweeps, us:", L, sweep, e ? "odd" : "even");
+            for (size_t k = 0; k < lab[e].size(); ++k)
+                std::fprintf(stderr, " %s %.1f", lab[e][k].c_str(), cnt[e] ? acc[e][k] * 1e3 / cnt[e] : 0.0);
             std::fprintf(stderr, "\n");
         }
-        for (cudaEvent_t e : pev) cudaEventDestroy(e);
+        for (ProfMark& m : pmarks) cudaEventDestroy(m.ev);
     }
     if (d.tsc) {
         std::vector<double> raw = tscbuf.to_host(64, st);
         const long long* t = reinterpret_cast<const long long*>(raw.data());
         std::fprintf(stderr, "octen als update phases (cycles from start):");
-        for (int i = 1; i < 32 && t[i]; ++i) std::fprintf(stderr, " %lld", t[i] - t[0]);
+        for (int i = 1; i < 32; ++i)
+            if (t[i]) std::fprintf(stderr, " [%d] %lld", i, t[i] - t[0]);
         std::fprintf(stderr, "\n");
     }
     if (std::getenv("OCTEN_DEBUG_ALS")) {
         const std::vector<int> ed = eigdbg.to_host(1, st);
         std::fprintf(stderr, "octen als: %d problems, %d sweeps, %d GEVD eigen fallbacks\n", NP, sweep, ed[0]);
     }
-    cudaFreeHost(hcount);
 
     // ---- errors (lowest replica, then restart, wins)
     std::vector<DevStatus> he = err.to_host(NP, st);

@@ -283,8 +283,10 @@ __global__ void __launch_bounds__(256)
         commit();
         const double* as = As + (kt % ST) * AE;
         const double* bs = Bs + (kt % ST) * B_ELEMS;
+        const int kvalid = kend - (kbeg + kt * BK);  // < BK only on a ragged last tile (uniform)
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
+            if (kk >= kvalid) break;
             double fa[4], fb[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
