@@ -584,6 +584,8 @@ __device__ __forceinline__ void mttkrp_column(const double* __restrict__ tcol, c
 // The first NP blocks instead form Vi of `mode` (als_vinv_block).
 template <int NA>
 __global__ void __launch_bounds__(256, 3) als_mttkrp_T_kernel(AlsDev d, int contract_first, int fsrc, int mode) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ double vsm[];
     if ((int)blockIdx.x < d.NP) {
         if (d.state[blockIdx.x].active) als_vinv_block(d, blockIdx.x, mode, vsm);
@@ -606,6 +608,8 @@ __global__ void __launch_bounds__(256, 3) als_mttkrp_T_kernel(AlsDev d, int cont
 // (cp_als.cpp:325-345).  V^-1 (als_vinv_block, formed during the MTTKRP)
 // makes raw = M V^-1 a parallel (Q x R)(R x R) product.
 __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
+    pdl_trigger();
+    pdl_wait();
     const int prob = blockIdx.x;
     AlsState* st = d.state + prob;
     if (!st->active) return;
@@ -1057,6 +1061,15 @@ AlsEngine::~AlsEngine() {
             cudaStreamSynchronize(ls);
             cudaStreamDestroy(ls);
         }
+    for (cudaStream_t ls : lane_hp)
+        if (ls) {
+            cudaStreamSynchronize(ls);
+            cudaStreamDestroy(ls);
+        }
+    if (gemm_st) {
+        cudaStreamSynchronize(gemm_st);
+        cudaStreamDestroy(gemm_st);
+    }
     if (hact) cudaFreeHost(hact);
     for (cudaEvent_t e : lane_ev)
         if (e) cudaEventDestroy(e);
@@ -1276,6 +1289,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
 
     // ---- sweeps
     const int SR = S * R;
+    static const bool use_pdl = std::getenv("OCTEN_NO_PDL") == nullptr;
     const unsigned qinv = (unsigned)((0x100000000ull + (unsigned)Q - 1) / (unsigned)Q);
     const int upd_threads = 256;
     const size_t smem_upd = (size_t)(R * R + 2 * Q * R + R + 2 * (R + 2) + upd_threads) * sizeof(double) + 16;
@@ -1300,13 +1314,32 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         lp0[l] = (int)((long long)P * l / L);
         lp1[l] = (int)((long long)P * (l + 1) / L);
     }
-    for (int l = 1; l < L; ++l)
-        if (!lane_st[l]) OCTEN_CUDA(cudaStreamCreateWithFlags(&lane_st[l], cudaStreamNonBlocking));
+    // With several lanes, the T-GEMMs of all lanes go through one
+    // low-priority stream (so they run one at a time, in enqueue order) while
+    // the latency-bound MTTKRP / update kernels stay on high-priority lane
+    // streams: lane l's mode updates overlap the other lanes' GEMMs.
+    // (Measured slower at c3: a lane's 4-replica GEMM alone is ~1.07 waves.
+    // Off unless OCTEN_ALS_GEMM_STREAM=1.)
+    static const bool gsplit_env = [] {
+        const char* e = std::getenv("OCTEN_ALS_GEMM_STREAM");
+        return e && e[0] == '1';
+    }();
+    const bool gsplit = gsplit_env && L > 1;
+    if (!lane_st[1]) {
+        for (int l = 0; l < kMaxLanes; ++l) OCTEN_CUDA(cudaStreamCreateWithFlags(&lane_st[l], cudaStreamNonBlocking));
+    }
+    if (gsplit && !gemm_st) {
+        int least = 0, greatest = 0;
+        OCTEN_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        OCTEN_CUDA(cudaStreamCreateWithPriority(&gemm_st, cudaStreamNonBlocking, least));
+        for (int l = 0; l < kMaxLanes; ++l)
+            OCTEN_CUDA(cudaStreamCreateWithPriority(&lane_hp[l], cudaStreamNonBlocking, greatest));
+    }
     for (cudaEvent_t& e : lane_ev)
         if (!e) OCTEN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     cudaStream_t ls[kMaxLanes];
-    ls[0] = st;
-    for (int l = 1; l < L; ++l) ls[l] = lane_st[l];
+    ls[0] = gsplit ? lane_hp[0] : st;
+    for (int l = 1; l < L; ++l) ls[l] = gsplit ? lane_hp[l] : lane_st[l];
     if (hact_n < (size_t)max_iters * kMaxLanes) {
         if (hact) cudaFreeHost(hact);
         hact = nullptr;
@@ -1342,7 +1375,9 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     }
     if (L > 1) {
         OCTEN_CUDA(cudaEventRecord(lane_ev[0], st));
-        for (int l = 1; l < L; ++l) OCTEN_CUDA(cudaStreamWaitEvent(ls[l], lane_ev[0], 0));
+        for (int l = 0; l < L; ++l)
+            if (ls[l] != st) OCTEN_CUDA(cudaStreamWaitEvent(ls[l], lane_ev[0], 0));
+        if (gsplit) OCTEN_CUDA(cudaStreamWaitEvent(gemm_st, lane_ev[0], 0));
     }
     // OCTEN_ALS_PROFILE: CUDA events between the kernels of lane 0's sweeps,
     // averaged per sweep parity and label (diagnostics)
@@ -1361,78 +1396,103 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         OCTEN_CUDA(cudaEventRecord(m.ev, ss));
         pmarks.push_back(m);
     };
-    auto launch_sweep = [&](int l, int sw, bool offset_wait) {
+    // Dimension tree over sweep pairs: consecutive mode updates that leave
+    // one factor untouched share the partial contraction with it.
+    //   even sweep: T = Y x3 C -> modes 0 (contract v with B), 1 (contract
+    //               u with A); T = Y x2 B -> mode 2 (contract u with A)
+    //   odd sweep:  the same T -> mode 0 (contract v with C); T = Y x1 A ->
+    //               modes 1 (contract v with C), 2 (contract u with B)
+    // 1.5 Q^3 S R GEMMs per sweep instead of 2 (or 3 without a tree).  Each
+    // sweep is enqueued as two segments, each segment for every lane in turn,
+    // so the GEMM stream alternates between lanes.
+    auto launch_seg = [&](int l, int sw, int seg) {
         const AlsDev& x = dl[l];
         cudaStream_t ss = ls[l];
         const int pn = x.P, npn = x.NP;
-        // lane l starts its first sweep after lane l-1's first T-GEMM
-        if (offset_wait) OCTEN_CUDA(cudaStreamWaitEvent(ss, lane_ev[1 + l - 1], 0));
-        // Dimension tree over sweep pairs: consecutive mode updates that leave
-        // one factor untouched share the partial contraction with it.
-        //   even sweep: T = Y x3 C -> modes 0 (contract v with B), 1 (contract
-        //               u with A); T = Y x2 B -> mode 2 (contract u with A)
-        //   odd sweep:  the same T -> mode 0 (contract v with C); T = Y x1 A ->
-        //               modes 1 (contract v with C), 2 (contract u with B)
-        // 1.5 Q^3 S R GEMMs per sweep instead of 2 (or 3 without a tree).
         auto tgemm = [&](int contracted) {
+            cudaStream_t gs = ss;
+            bool pd = use_pdl;
+            if (gsplit) {
+                OCTEN_CUDA(cudaEventRecord(lane_ev[kGin + l], ss));
+                OCTEN_CUDA(cudaStreamWaitEvent(gemm_st, lane_ev[kGin + l], 0));
+                gs = gemm_st;
+                pd = false;
+            }
             if (contracted == 2) {  // rows (i, j)
                 if (pipe_ok)
                     gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmatP{x.Y, q3, q2}, FacP{x.F, S, Q, R, 2},
-                                         TStore{x.T, q2, SR}, ss);
+                                         TStore{x.T, q2, SR}, gs, 1, nullptr, pd);
                 else
                     gemm_f64<false, true>(pn, (int)q2, SR, Q, YmatA{x.Y, q3, q2, S, false}, FacB{x.F, S, Q, R, 2},
-                                          TStore{x.T, q2, SR}, ss);
+                                          TStore{x.T, q2, SR}, gs);
             } else if (contracted == 1) {  // rows (i, k)
                 if (pipe_ok)
                     gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmidP{x.Y, q3, (unsigned)Q, qinv}, FacP{x.F, S, Q, R, 1},
-                                         TStore{x.T, q2, SR}, ss);
+                                         TStore{x.T, q2, SR}, gs, 1, nullptr, pd);
                 else
                     gemm_f64<false, true>(pn, (int)q2, SR, Q, YmidA{x.Y, q3, Q}, FacB{x.F, S, Q, R, 1},
-                                          TStore{x.T, q2, SR}, ss);
+                                          TStore{x.T, q2, SR}, gs);
             } else {  // rows (j, k)
                 if (pipe_ok)
                     gemm_f64_pipe<true>(pn, (int)q2, SR, Q, Y0tP{x.Y, q3, Q}, FacP{x.F, S, Q, R, 0},
-                                        TStore{x.T, q2, SR}, ss);
+                                        TStore{x.T, q2, SR}, gs, 1, nullptr, pd);
                 else
                     gemm_f64<true, true>(pn, (int)q2, SR, Q, Y0tA{x.Y, q3, Q}, FacB{x.F, S, Q, R, 0},
-                                         TStore{x.T, q2, SR}, ss);
+                                         TStore{x.T, q2, SR}, gs);
             }
+            if (gsplit) {
+                OCTEN_CUDA(cudaEventRecord(lane_ev[kGout + l], gemm_st));
+                OCTEN_CUDA(cudaStreamWaitEvent(ss, lane_ev[kGout + l], 0));
+            }
+            mark(l, sw, contracted == 2 ? "gemm Yx3C" : contracted == 1 ? "gemm Yx2B" : "gemm Yx1A", ss);
         };
         auto mode_step = [&](int contract_first, int fsrc, int mode) {
-            mttkrp_kernel<<<npn * (R + 1), 256, smem_vinv, ss>>>(x, contract_first, fsrc, mode);
-            OCTEN_LAUNCHED(1);
+            if (use_pdl) {
+                launch_pdl(mttkrp_kernel, dim3(npn * (R + 1)), dim3(256), smem_vinv, ss, x, contract_first, fsrc, mode);
+            } else {
+                mttkrp_kernel<<<npn * (R + 1), 256, smem_vinv, ss>>>(x, contract_first, fsrc, mode);
+                OCTEN_LAUNCHED(1);
+            }
             mark(l, sw, mode == 0 ? "mttkrp0" : mode == 1 ? "mttkrp1" : "mttkrp2", ss);
-            als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, mode, sw); OCTEN_LAUNCHED(1);
+            if (use_pdl) {
+                launch_pdl(als_update_kernel, dim3(npn), dim3(upd_threads), smem_upd, ss, x, mode, sw);
+            } else {
+                als_update_kernel<<<npn, upd_threads, smem_upd, ss>>>(x, mode, sw);
+                OCTEN_LAUNCHED(1);
+            }
             mark(l, sw, mode == 0 ? "update0" : mode == 1 ? "update1" : "update2", ss);
         };
-        mark(l, sw, "start", ss);
+        if (seg == 0) mark(l, sw, "start", ss);
         if ((sw & 1) == 0) {
-            tgemm(2);
-            if (sw == 0 && l + 1 < L) OCTEN_CUDA(cudaEventRecord(lane_ev[1 + l], ss));
-            mark(l, sw, "gemm Yx3C", ss);
-            mode_step(0, 1, 0);
-            mode_step(1, 0, 1);
-            tgemm(1);
-            mark(l, sw, "gemm Yx2B", ss);
-            mode_step(1, 0, 2);
+            if (seg == 0) {
+                tgemm(2);
+                mode_step(0, 1, 0);
+                mode_step(1, 0, 1);
+            } else {
+                tgemm(1);
+                mode_step(1, 0, 2);
+            }
         } else {
-            mode_step(0, 2, 0);
-            tgemm(0);
-            mark(l, sw, "gemm Yx1A", ss);
-            mode_step(0, 2, 1);
-            mode_step(1, 1, 2);
+            if (seg == 0) {
+                mode_step(0, 2, 0);
+            } else {
+                tgemm(0);
+                mode_step(0, 2, 1);
+                mode_step(1, 1, 2);
+            }
         }
         OCTEN_CUDA(cudaGetLastError());
-        OCTEN_CUDA(cudaEventRecord(lane_ev[kMaxLanes + kMaxLanes * (sw & 1) + l], ss));
+        if (seg == 1) OCTEN_CUDA(cudaEventRecord(lane_ev[kSweepEv + kMaxLanes * (sw & 1) + l], ss));
     };
     int sweep = 0;
     for (; sweep < max_iters; ++sweep) {
-        for (int l = 0; l < L; ++l) launch_sweep(l, sweep, l >= 1 && sweep == 0);
+        for (int seg = 0; seg < 2; ++seg)
+            for (int l = 0; l < L; ++l) launch_seg(l, sweep, seg);
         if (sweep >= 1) {
             // problems still active after the previous sweep
             int left = 0;
             for (int l = 0; l < L; ++l) {
-                OCTEN_CUDA(cudaEventSynchronize(lane_ev[kMaxLanes + kMaxLanes * ((sweep - 1) & 1) + l]));
+                OCTEN_CUDA(cudaEventSynchronize(lane_ev[kSweepEv + kMaxLanes * ((sweep - 1) & 1) + l]));
                 left += reinterpret_cast<volatile int*>(hact)[(size_t)(sweep - 1) * kMaxLanes + l];
             }
             ++host_syncs;
@@ -1442,10 +1502,11 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             }
         }
     }
-    for (int l = 1; l < L; ++l) {
-        OCTEN_CUDA(cudaEventRecord(lane_ev[0], ls[l]));
-        OCTEN_CUDA(cudaStreamWaitEvent(st, lane_ev[0], 0));
-    }
+    for (int l = 0; l < L; ++l)
+        if (ls[l] != st) {
+            OCTEN_CUDA(cudaEventRecord(lane_ev[0], ls[l]));
+            OCTEN_CUDA(cudaStreamWaitEvent(st, lane_ev[0], 0));
+        }
     OCTEN_CUDA(cudaStreamSynchronize(st));
     last_sweeps = sweep;
     if (want_prof) {

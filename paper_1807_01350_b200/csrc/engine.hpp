@@ -69,7 +69,12 @@ private:
     int* hact = nullptr;  // host-mapped per-sweep activity flags
     size_t hact_n = 0;
     cudaStream_t lane_st[kMaxLanes] = {};   // sweep lanes 1..L-1 (lane 0 runs on the caller's stream)
-    cudaEvent_t lane_ev[3 * kMaxLanes] = {};
+    cudaStream_t lane_hp[kMaxLanes] = {};   // OCTEN_ALS_GEMM_STREAM=1: high-priority lanes
+    cudaStream_t gemm_st = nullptr;         //   and the lanes' T-GEMMs (low priority)
+    // lane_ev: [0] fork/join, [kGin + l] lane -> GEMM stream, [kGout + l]
+    // GEMM stream -> lane, [kSweepEv + 4 (sweep & 1) + l] end of a sweep
+    static constexpr int kGin = 1, kGout = 1 + kMaxLanes, kSweepEv = 1 + 2 * kMaxLanes;
+    cudaEvent_t lane_ev[1 + 4 * kMaxLanes] = {};
     DevBuf<double> Gev, EV, Ur, Wmix, Smix, Tmp6, Pm, Hh, gscr;
     DevBuf<int> usable, att_start, att_used, todo, peel_fail, eigdbg;
     DevBuf<AlsState> state;

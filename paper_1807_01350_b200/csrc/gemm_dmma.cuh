@@ -16,6 +16,24 @@
 
 namespace octen {
 
+// Launch `k` as a programmatic dependent of the previous work on `st` (the
+// kernel must call pdl_wait() before reading its predecessor's output).
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    OCTEN_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+    OCTEN_LAUNCHED(1);
+}
+
 __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
     asm volatile(
         "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
@@ -214,6 +232,8 @@ template <bool A_KFAST, class AF, class BF, class CF, bool B_KFAST = true>
 __global__ void __launch_bounds__(256)
     gemm_dmma_pipe_kernel(int M, int N, int K, int ksplit, int kchunk, AF af, BF bf, CF cf, double* partial) {
     using namespace pipe;
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ double pipe_smem[];
     constexpr int AE = a_elems<A_KFAST>();
     double* As = pipe_smem;                 // ST x AE
@@ -321,7 +341,7 @@ __global__ void __launch_bounds__(256)
 
 template <bool A_KFAST, class AF, class BF, class CF, bool B_KFAST = true>
 void gemm_f64_pipe(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaStream_t st, int ksplit = 1,
-                   double* workspace = nullptr) {
+                   double* workspace = nullptr, bool pdl = false) {
     if (batches <= 0 || M <= 0 || N <= 0) return;
     if (K <= 0) ksplit = 1;
     if (ksplit < 1) ksplit = 1;
@@ -335,9 +355,14 @@ void gemm_f64_pipe(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaSt
         attr = true;
     }
     dim3 grid((N + pipe::BN - 1) / pipe::BN, (M + pipe::BM - 1) / pipe::BM, batches * ksplit);
-    gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF, B_KFAST><<<grid, 256, smem, st>>>(M, N, K, ksplit, kchunk, af, bf, cf,
-                                                                                 workspace);
-    OCTEN_LAUNCHED(1);
+    if (pdl) {
+        launch_pdl(gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF, B_KFAST>, grid, dim3(256), smem, st, M, N, K, ksplit,
+                   kchunk, af, bf, cf, workspace);
+    } else {
+        gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF, B_KFAST><<<grid, 256, smem, st>>>(M, N, K, ksplit, kchunk, af, bf,
+                                                                                     cf, workspace);
+        OCTEN_LAUNCHED(1);
+    }
     if (ksplit > 1) {
         const size_t total = (size_t)batches * M * N;
         int blocks = (int)((total + 255) / 256);

@@ -79,6 +79,15 @@ struct DevStatus {
 OCTEN_HD inline double dsq(double x) { return x * x; }
 
 #if defined(__CUDACC__)
+// Programmatic dependent launch.  A kernel launched with launch_pdl may start
+// while its predecessor on the stream is still running: it must call
+// pdl_wait() before touching anything the predecessor writes (the wait returns
+// once the predecessor has completed and its writes are visible; it is a no-op
+// in a kernel launched normally).  pdl_trigger() lets the successor launch
+// once every block of this grid has issued it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // Block-wide global -> shared copy with four independent loads in flight per
 // thread.  (A plain `dst[e] = src[e]` loop through generic pointers makes
 // every load wait for the previous shared store, since the compiler cannot
