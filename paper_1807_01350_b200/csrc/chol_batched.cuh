@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "devbuf.hpp"
+#include "evprof.hpp"
 #include "gemm_dmma.cuh"
 #include "octen_common.cuh"
 #include "small_linalg.cuh"
@@ -57,6 +58,9 @@ constexpr int kDiagThreads = 128;
 constexpr int kHalf = kCholNB / 2;
 constexpr int kDLD = kCholNB + 1;  // shared leading dimension
 constexpr size_t kDiagSmem = (size_t)(2 * kCholNB * kDLD + kHalf * (kHalf + 1) + 160) * sizeof(double);
+__device__ long long g_diag_tsc[16];  // OCTEN_PROFILE: phase clocks of block 0 at k0 == 0
+#define DIAG_TSC(i) \
+    if (blockIdx.x == 0 && k0 == 0 && threadIdx.x == 0) g_diag_tsc[(i)] = clock64();
 
 __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int n, int lda, long long sA, int k0,
                                                                  double tol, const double* maxdiag, int* rank,
@@ -69,6 +73,7 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
     double* a = A + (size_t)blockIdx.x * sA;
     const int nb = min(kCholNB, n - k0);
     const int tid = threadIdx.x;
+    DIAG_TSC(0)
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
         double v[8];
@@ -89,8 +94,10 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
     const double md = maxdiag[blockIdx.x];
     const double thr = (md > 0.0) ? tol * md : INFINITY;
     __syncthreads();
+    DIAG_TSC(1)
     const int n1 = min(kHalf, nb);
     const int rk1 = block_chol_inv_t<5, kDiagThreads>(S, kDLD, n1, thr, S, kDLD, X, kDLD, scr);
+    DIAG_TSC(2)
     int dead = n1 - rk1;
     const int n2 = nb - n1;
     if (n2 > 0) {
@@ -128,7 +135,9 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
             A22[i + kDLD * j] -= s0 + s1;
         }
         __syncthreads();
+        DIAG_TSC(3)
         const int rk2 = block_chol_inv_t<5, kDiagThreads>(A22, kDLD, n2, thr, A22, kDLD, X22, kDLD, scr);
+        DIAG_TSC(4)
         dead += n2 - rk2;
         // X21 = -X22 (L21 X11): T = L21 X11, then X21 = -X22 T
         for (int e = tid; e < kHalf * kHalf; e += kDiagThreads) {
@@ -156,6 +165,7 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
         }
         __syncthreads();
     }
+    DIAG_TSC(5)
     if (tid == 0 && dead) atomicSub(&rank[blockIdx.x], dead);
     // write back: L (lower of the nb x nb block, upper zeroed) and L^-1
     double* inv = Linv + ((size_t)blockIdx.x * nblk + k0 / kCholNB) * kCholNB * kCholNB;
@@ -165,6 +175,7 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
         inv[e] = (in && i >= j) ? X[i + kDLD * j] : 0.0;
         if (in) a[(k0 + i) + (size_t)lda * (k0 + j)] = (i >= j) ? S[i + kDLD * j] : 0.0;
     }
+    DIAG_TSC(6)
 }
 
 // Rows below the diagonal block: L21 = A21 * L11^-T as an in-place GEMM
@@ -350,17 +361,22 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
     OCTEN_CUDA(cudaEventRecord(ev_start, st));
     OCTEN_CUDA(cudaStreamWaitEvent(crit, ev_start, 0));
     int pending_rest = -1;  // step whose part 2 is in flight on `st`
+    static thread_local EvProf cp;
+    const bool prof = EvProf::enabled() && n >= 512;
+    if (prof) cp.mark("begin", crit);
     for (int kb = 0; kb < nblk; ++kb) {
         const int k0 = kb * kCholNB;
         chol_diag_kernel<<<batch, kDiagThreads, kDiagSmem, crit>>>(A, n, lda, sA, k0, tol, maxdiag, rank, linv.p,
                                                                     nblk);
         OCTEN_LAUNCHED(1);
+        if (prof) cp.mark("diag", crit);
         const int nb = min(kCholNB, n - k0);
         const int rows = n - k0 - nb;
         if (rows <= 0) break;
         const int r0 = k0 + nb;
         gemm_f64<false, true>(batch, rows, nb, nb, PanelA{A, lda, sA, r0, k0}, PanelB{linv.p, nblk, k0 / kCholNB},
                                                PanelC{A, lda, sA, r0, k0}, crit);
+        if (prof) cp.mark("panel", crit);
         const int tiles = (rows + kCholNB - 1) / kCholNB;
         if (tiles > 1) {
             OCTEN_CUDA(cudaEventRecord(ev_panel[kb], crit));
@@ -370,8 +386,10 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
             OCTEN_CUDA(cudaStreamWaitEvent(crit, ev_rest[pending_rest], 0));
             pending_rest = -1;
         }
+        if (prof) cp.mark("wait", crit);
         chol_trail_kernel<<<dim3(tiles, 1, batch), 256, kTrailSmem, crit>>>(A, n, lda, sA, r0, k0, nb, 1);
         OCTEN_LAUNCHED(1);
+        if (prof) cp.mark("part1", crit);
         if (tiles > 1) {
             chol_trail_kernel<<<dim3((tiles - 1) * tiles / 2, 1, batch), 256, kTrailSmem, st>>>(A, n, lda, sA, r0, k0,
                                                                                                  nb, 2);
@@ -383,6 +401,16 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
     // join: everything on `st` after this waits for the critical chain
     OCTEN_CUDA(cudaEventRecord(ev_end, crit));
     OCTEN_CUDA(cudaStreamWaitEvent(st, ev_end, 0));
+    if (prof) {
+        cp.mark("join", st);
+        cp.report("chol_batched crit chain");
+        long long t[16];
+        OCTEN_CUDA(cudaMemcpyFromSymbol(t, g_diag_tsc, sizeof t));
+        std::fprintf(stderr, "octen chol_diag phases (cycles, block 0, k0 = 0):");
+        for (int i = 1; i < 12; ++i)
+            if (t[i]) std::fprintf(stderr, " [%d] %lld", i, t[i] - t[0]);
+        std::fprintf(stderr, "\n");
+    }
 }
 
 // Blocked solves with the stored diagonal-block inverses.  Step k of the

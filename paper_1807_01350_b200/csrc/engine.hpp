@@ -178,6 +178,7 @@ public:
     DevBuf<double> Gp[2];    // P x d x d
     DevBuf<double> Lsum[2];  // d x d (Cholesky of sum_p G_p)
     DevBuf<double> Lsum_inv[2], Gw_inv;  // diagonal-block inverses of the factors
+    DevBuf<double> Ginv[2];  // (sum_p G_p)^-1, full d x d
     int sum_rank[2] = {0, 0};
     DevBuf<double> Lw[2];    // shared x shared whitener (non-temporal modes)
     int white_ok[2] = {0, 0};

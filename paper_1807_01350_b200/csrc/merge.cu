@@ -24,6 +24,7 @@
 
 #include "chol_batched.cuh"
 #include "engine.hpp"
+#include "evprof.hpp"
 #include "gemm_dmma.cuh"
 #include "small_linalg.cuh"
 
@@ -96,6 +97,11 @@ void gemm_f64_splitk(int batches, int M, int N, int K, AF af, BF bf, CF cf, cuda
     const int ks = pick_ksplit(batches, M, N, K, 296, 64);
     if (ks > 1) ws.reserve((size_t)batches * ks * M * N);
     gemm_f64<A_KFAST, B_KFAST>(batches, M, N, K, af, bf, cf, st, ks, ks > 1 ? ws.p : nullptr);
+}
+
+__global__ void identity_kernel(double* A, long long d) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)d * d; e += (size_t)gridDim.x * blockDim.x)
+        A[e] = (e % d == e / d) ? 1.0 : 0.0;
 }
 
 }  // namespace
@@ -867,6 +873,14 @@ void MergeEngine::set_projections(int P_, int Q_, int sh, int R_, std::int64_t I
         ranks.reserve(128);
         chol_batched(Lsum[n].p, (int)d, (int)d, 0, 1, kGramRankTol, maxdiag.p, ranks.p, Lsum_inv[n], st);
         sum_rank[n] = ranks.to_host(1, st)[0];
+        // (sum_p U_p U_p^T)^-1, formed once per stream: every batch's
+        // unweighted non-temporal solve is then one GEMM
+        if (sum_rank[n] == d) {
+            Ginv[n].reserve((size_t)d * d);
+            identity_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>(Ginv[n].p, d);
+            OCTEN_LAUNCHED(1);
+            chol_solve_cta(Lsum[n].p, (int)d, (int)d, 0, Lsum_inv[n], Ginv[n].p, (int)d, 0, (int)d, 1, st);
+        }
         // whitener of the shared block (reference replica; the block is shared)
         DevBuf<int> okb;
         okb.reserve(1);
@@ -942,6 +956,7 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
     a.maxoff = maxoff_d;
     a.ambig = ambig.p;
     a.err = err.p;
+    OCTEN_PROF("begin", st);
     align_prep_kernel<<<P, 128, 0, st>>>(a); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     check_errs(err, 1, st);
@@ -994,9 +1009,12 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
         a.rms = nullptr;
     }
     const size_t smem = (size_t)(R * R + 2 * R) * sizeof(double);
+    OCTEN_PROF("prep+pair", st);
     align_match_kernel<<<P, 128, smem, st>>>(a); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     check_errs(err, P + 1, st);
+    OCTEN_PROF("match", st);
+    EvProf::get().report("align");
     if (out) {
         out->perms = perms.to_host((size_t)P * R, st);
         out->scales = red.to_host((size_t)P * 3 * R, st);
@@ -1021,9 +1039,11 @@ void MergeEngine::solve_nontemporal(int n, const double* dStack, double* dOut, c
     if (sum_rank[n] < d)
         throw NumericError("recover: rank-deficient projection on mode " + std::to_string(n + 1) + " (rank " +
                            std::to_string(sum_rank[n]) + " of " + std::to_string(d) + ")");
+    tmp.reserve((size_t)d * R);
     gemm_f64_splitk<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{dStack, PQ, 0},
+                                           StoreCM{tmp.p, d, 0}, st, kws);
+    gemm_f64_splitk<false, true>(1, (int)d, R, (int)d, UcatA{Ginv[n].p, d, 0}, ColB{tmp.p, d, 0},
                                            StoreCM{dOut, d, 0}, st, kws);
-    chol_solve_cta(Lsum[n].p, (int)d, (int)d, 0, Lsum_inv[n], dOut, (int)d, 0, R, 1, st);
 }
 
 void MergeEngine::temporal_stack(const double* dY, int p0, int pl, const double* dA, const double* dB, double* dOut,
@@ -1117,10 +1137,12 @@ void MergeEngine::recover(const double* dY, const double* dW, std::int64_t t, do
 void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, double* dAfin, double* dBfin,
                              cudaStream_t st) {
     const long long PQ = (long long)P * Q;
+    OCTEN_PROF("begin", st);
     for (int n = 0; n < 2; ++n) {
         solved[n].reserve((size_t)dims[n] * R);
         solve_nontemporal(n, stacks.p + (size_t)n * PQ * R, solved[n].p, st);
     }
+    OCTEN_PROF("solve_nontemporal", st);
     // two refinement passes (streaming.cpp:107-120)
     DevBuf<double> w;
     w.reserve((size_t)P * R);
@@ -1142,6 +1164,7 @@ void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, dou
                                             lp_ok[1].p, w.p); OCTEN_LAUNCHED(1);
         weight_mass_kernel<<<1, 64, 0, st>>>(P, Q, R, std::max(dims[0], dims[1]), w.p); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
+        OCTEN_PROF("refine", st);
         for (int n = 0; n < 2; ++n) {
             const long long d = dims[n];
             if (PQ < d)
@@ -1170,7 +1193,9 @@ void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, dou
                 gemm_f64_splitk<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{sw.p, PQ, 0},
                                       StoreCM{sw2.p + (size_t)mi * R * d, d, 0}, st, kws);
             }
+            OCTEN_PROF("wgram+rhs", st);
             chol_batched(Gw.p, (int)d, (int)d, d * d, nb, kGramRankTol, maxdiag.p, ranks.p, Gw_inv, st);
+            OCTEN_PROF("chol", st);
             std::vector<int> rk = ranks.to_host(nb, st);
             for (int mi = 0; mi < nmodes; ++mi) {
                 const int n = fused ? mi : gi;
@@ -1181,7 +1206,9 @@ void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, dou
                                            ")");
             }
             // each column r against its own factor
+            OCTEN_PROF("rank-check", st);
             chol_solve_cta(Gw.p, (int)d, (int)d, d * d, Gw_inv, sw2.p, (int)d, d, 1, nb, st);
+            OCTEN_PROF("chol_solve", st);
             for (int mi = 0; mi < nmodes; ++mi) {
                 const int n = fused ? mi : gi;
                 OCTEN_CUDA(cudaMemcpyAsync(solved[n].p, sw2.p + (size_t)mi * R * d, sizeof(double) * d * R,
@@ -1219,6 +1246,8 @@ void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, dou
     }
     OCTEN_CUDA(cudaGetLastError());
     check_errs(err, 2, st);
+    OCTEN_PROF("gauge", st);
+    EvProf::get().report("recover_ab");
 }
 
 }  // namespace octen

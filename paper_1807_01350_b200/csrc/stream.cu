@@ -18,6 +18,7 @@
 #include "errors.hpp"
 #include "rng_host.hpp"
 #include "stream.hpp"
+#include "evprof.hpp"
 
 namespace octen {
 
@@ -386,6 +387,8 @@ void Stream::merge_phase(const double* models_all, double* rows_out) {
     if (!pending) throw ConfigError("octen: merge without a begun batch");
     try {
         t_recover = Clock::now();
+        static thread_local EvProf sp;
+        sp.mark("begin", st);
         const int P = cfg.p, Q = cfg.q, R = cfg.rank;
         const size_t qr = (size_t)Q * R, mc = models_count();
         // CP-ALS failures of any rank (lowest replica first)
@@ -409,13 +412,18 @@ void Stream::merge_phase(const double* models_all, double* rows_out) {
                                        sizeof(double) * gl * R, cudaMemcpyDeviceToDevice, st));
         }
         AlignResultHost ar;
+        sp.mark("hdr+gather", st);
         merge.align(MfAll.p, MlamAll.p, tgram, st, &ar);
+        sp.mark("align", st);
         prec.min_match_similarity = ar.min_match;
         prec.max_offdiag_similarity = ar.max_offdiag;
         Anew.reserve((size_t)I * R);
         Bnew.reserve((size_t)J * R);
         merge.recover_ab(pending_first ? nullptr : A.p, pending_first ? nullptr : B.p, Anew.p, Bnew.p, st);
+        sp.mark("recover_ab", st);
         if (pl > 0) merge.temporal_stack(Y.p, p0, pl, Anew.p, Bnew.p, rows_out, true, st);
+        sp.mark("temporal_stack", st);
+        sp.report("merge_phase");
         OCTEN_CUDA(cudaStreamSynchronize(st));
     } catch (...) {
         fail_pending();
@@ -449,7 +457,11 @@ void Stream::finish(const double* rows_all) {
         OCTEN_LAUNCHED(1);
         rows.reserve((size_t)t_new * R);
         double residual = 0.0;
+        static thread_local EvProf fp;
+        fp.mark("begin", st);
         merge.temporal_append(tstackAll.p, dW.p, t_new, hist.p, rows.p, &residual, st);
+        fp.mark("temporal_append", st);
+        fp.report("finish");
         prec.temporal_residual = residual;
         prec.warned = residual > cfg.residual_warning ? 1 : 0;
         if (prec.warned && cfg.strict) {
