@@ -393,20 +393,7 @@ __device__ inline int block_greedy_match(int r, const double* sim, int ld, doubl
 // and x (ld ldx, lower; upper zeroed) are written.  Returns the rank (all
 // threads).
 // ---------------------------------------------------------------------------
-// 1/sqrt(d) for a positive normal d: the hardware approximation refined by
-// two Newton steps (relative error ~1 ulp; no special-value slow path).
-__device__ __forceinline__ double rsqrt_nr(double d) {
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-    const double hd = 0.5 * d;
-    y = y * fma(-hd * y, y, 1.5);
-    y = y * fma(-hd * y, y, 1.5);
-    return y;
-}
-
-// kWarp: one warp runs it alone (kThreads == 32, lanes as the team, warp
-// barriers; scratch private to the warp).
-template <int kPer, int kThreads, bool kWarp = false>
+template <int kPer, int kThreads>
 __device__ inline int block_chol_inv_t(const double* a, int lda, int n, double thr, double* l, int ldl, double* x,
                                        int ldx, double* scratch) {
     // kThreads == blockDim.x (compile time: the owner arithmetic below divides by it)
@@ -415,18 +402,12 @@ __device__ inline int block_chol_inv_t(const double* a, int lda, int n, double t
     double* colk = scratch;        // 65
     double* rowk = scratch + 65;   // 65
     double* shv = scratch + 130;   // [0..1] reciprocal pivots (double-buffered), [2] dead count
-    const int tid = kWarp ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
-    auto sync = [] {
-        if (kWarp)
-            __syncwarp();
-        else
-            __syncthreads();
-    };
+    const int tid = threadIdx.x;
     double av[kPer], bv[kPer];
     int iv[kPer], jv[kPer];
-    for (int e = tid; e <= 64; e += kThreads) {
-        colk[e] = 0.0;
-        rowk[e] = 0.0;
+    if (tid <= 64) {
+        colk[tid] = 0.0;
+        rowk[tid] = 0.0;
     }
     if (tid == 0) shv[2] = 0.0;
 #pragma unroll
@@ -442,45 +423,41 @@ __device__ inline int block_chol_inv_t(const double* a, int lda, int n, double t
         av[s] = ok ? a[i + (size_t)lda * j] : 0.0;
         bv[s] = (ok && i == j) ? 1.0 : 0.0;
     }
-    // Branch-free: every lane evaluates the pivot (only the owner's result is
-    // kept) and the reciprocal square root is the approximate MUFU value plus
-    // two Newton steps (no slow-path call), so the column loop has no
-    // divergent branches.
     auto pivot = [&](int k) {
         const int ed = k * (k + 3) / 2;
-        const bool own = tid == ed % kThreads;
-        const int sd = ed / kThreads;
-        double d = 0.0;
+        if (tid == ed % kThreads) {
+            const int sd = ed / kThreads;
 #pragma unroll
-        for (int s = 0; s < kPer; ++s) d = (s == sd) ? av[s] : d;
-        const bool dead = !(d > thr);
-        const double rp = dead ? 0.0 : rsqrt_nr(d);
-#pragma unroll
-        for (int s = 0; s < kPer; ++s) av[s] = (own && s == sd) ? d * rp : av[s];
-        if (own) {
-            shv[k & 1] = rp;
-            if (dead) shv[2] += 1.0;
+            for (int s = 0; s < kPer; ++s)
+                if (s == sd) {
+                    const double d = av[s];
+                    const bool dead = !(d > thr);
+                    const double rp = dead ? 0.0 : rsqrt(d);
+                    av[s] = dead ? 0.0 : d * rp;
+                    shv[k & 1] = rp;
+                    if (dead) shv[2] += 1.0;
+                }
         }
     };
-    sync();
+    __syncthreads();
     if (n > 0) pivot(0);
-    sync();
+    __syncthreads();
     for (int k = 0; k < n; ++k) {
         const double rp = shv[k & 1];
 #pragma unroll
         for (int s = 0; s < kPer; ++s) {
             const int i = iv[s], j = jv[s];
-            const bool c = (j == k) && (i > k);
-            const double va = av[s] * rp;
-            av[s] = c ? va : av[s];
-            if (c) colk[i] = va;
-            const bool r = (i == k);
-            const double vb = bv[s] * rp;
-            bv[s] = r ? vb : bv[s];
-            if (r) rowk[j] = vb;
+            if (j == k && i > k) {
+                av[s] *= rp;
+                colk[i] = av[s];
+            }
+            if (i == k) {
+                bv[s] *= rp;
+                rowk[j] = bv[s];
+            }
         }
         if (tid == 0) colk[k] = 0.0;
-        sync();
+        __syncthreads();
 #pragma unroll
         for (int s = 0; s < kPer; ++s) {
             const double ci = colk[iv[s]];
@@ -488,7 +465,7 @@ __device__ inline int block_chol_inv_t(const double* a, int lda, int n, double t
             bv[s] -= ci * rowk[jv[s]];
         }
         if (k + 1 < n) pivot(k + 1);
-        sync();
+        __syncthreads();
     }
     for (int e = tid; e < n * n; e += kThreads) {
         const int i = e % n, j = e / n;
@@ -503,102 +480,8 @@ __device__ inline int block_chol_inv_t(const double* a, int lda, int n, double t
             l[iv[s] + (size_t)ldl * jv[s]] = av[s];
             x[iv[s] + (size_t)ldx * jv[s]] = bv[s];
         }
-    sync();
+    __syncthreads();
     return n - (int)shv[2];
-}
-
-// Same contract as block_chol_inv_t with one barrier per column.  Column k
-// of A and row k of B (I -> L^-1) are published unscaled, together with the
-// pivot d_k, by the owners of those elements at the end of step k-1
-// (parity-double-buffered); every thread then forms rp = d_k^-1/2 itself and
-// applies the rank-1 updates with the factor rp^2:
-//   a_ij -= a_ik a_jk / d_k  (j > k),   b_ij -= a_ik b_kj / d_k  (i > k),
-// finalising l_ik = a_ik rp and x_kj = b_kj rp as step k passes them.
-// scratch: 2 x (65 + 65 + 1) + 1 doubles.
-template <int kPer, int kThreads, bool kWarp = false>
-__device__ inline int block_chol_inv_1b(const double* a, int lda, int n, double thr, double* l, int ldl, double* x,
-                                        int ldx, double* scratch) {
-    double* colk = scratch;        // [2][65] unscaled column k of A (rows i > k meaningful)
-    double* rowk = scratch + 130;  // [2][65] unscaled row k of B (cols j <= k)
-    double* dk = scratch + 260;    // [2] pivots
-    double* deadc = scratch + 262;
-    const int tid = kWarp ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
-    auto sync = [] {
-        if (kWarp)
-            __syncwarp();
-        else
-            __syncthreads();
-    };
-    double av[kPer], bv[kPer];
-    int iv[kPer], jv[kPer];
-    for (int e = tid; e < 130; e += kThreads) rowk[e] = 0.0;
-    if (tid == 0) *deadc = 0.0;
-#pragma unroll
-    for (int s = 0; s < kPer; ++s) {
-        const int e = tid + kThreads * s;
-        int i = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-        while ((i + 1) * (i + 2) / 2 <= e) ++i;
-        while (i * (i + 1) / 2 > e) --i;
-        const int j = e - i * (i + 1) / 2;
-        const bool ok = i < n;
-        iv[s] = ok ? i : 64;
-        jv[s] = ok ? j : 64;
-        av[s] = ok ? a[i + (size_t)lda * j] : 0.0;
-        bv[s] = (ok && i == j) ? 1.0 : 0.0;
-    }
-    sync();
-    // publish column 0 of A and row 0 of B
-#pragma unroll
-    for (int s = 0; s < kPer; ++s) {
-        if (jv[s] == 0 && iv[s] < 64) colk[iv[s]] = av[s];
-        if (iv[s] == 0 && jv[s] == 0) {
-            dk[0] = av[s];
-            rowk[0] = bv[s];
-        }
-    }
-    sync();
-    for (int k = 0; k < n; ++k) {
-        const int p = k & 1;
-        const double* ck = colk + 65 * p;
-        const double* rk = rowk + 65 * p;
-        const double d = dk[p];
-        const bool dead = !(d > thr);
-        const double rp = dead ? 0.0 : rsqrt_nr(d);
-        const double f = rp * rp;
-        double* cn = colk + 65 * (p ^ 1);
-        double* rn = rowk + 65 * (p ^ 1);
-#pragma unroll
-        for (int s = 0; s < kPer; ++s) {
-            const int i = iv[s], j = jv[s];
-            const double ci = ck[i], cj = ck[j], bj = rk[j];
-            // A: column k finalises, columns j > k update
-            const double fa = (j == k) ? av[s] * rp : av[s] - (j > k ? ci * cj * f : 0.0);
-            // B: row k finalises, rows i > k update
-            const double fb = (i == k) ? bv[s] * rp : bv[s] - (i > k ? ci * bj * f : 0.0);
-            av[s] = fa;
-            bv[s] = fb;
-            if (j == k + 1 && i < 64) cn[i] = fa;
-            if (i == k + 1) rn[j] = fb;
-            if (i == k + 1 && j == k + 1) dk[p ^ 1] = fa;
-        }
-        if (tid == 0 && dead) *deadc += 1.0;
-        sync();
-    }
-    for (int e = tid; e < n * n; e += kThreads) {
-        const int i = e % n, j = e / n;
-        if (i < j) {
-            l[i + (size_t)ldl * j] = 0.0;
-            x[i + (size_t)ldx * j] = 0.0;
-        }
-    }
-#pragma unroll
-    for (int s = 0; s < kPer; ++s)
-        if (iv[s] < 64) {
-            l[iv[s] + (size_t)ldl * jv[s]] = av[s];
-            x[iv[s] + (size_t)ldx * jv[s]] = bv[s];
-        }
-    sync();
-    return n - (int)*deadc;
 }
 
 // Block-cooperative semi-definite Cholesky with the inverse of the factor,
