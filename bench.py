@@ -61,6 +61,7 @@ class ClockSampler:
         self.gpu = gpu
         self.proc = None
         self.lines = []
+        self.n0 = 0
 
     def start(self):
         try:
@@ -76,6 +77,12 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def mark(self):
+        """Start of the timed region: only samples from here on count (the
+        sampler is started earlier, so nvidia-smi's own start-up -- process
+        spawn, NVML init -- stays out of the timed region)."""
+        self.n0 = len(self.lines)
+
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -86,7 +93,7 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[self.n0:]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -289,12 +296,13 @@ def main():
     del first
     batches = [syn.batch(K0 + i * t, t) for i in range(args.warmup + args.steps)]
     torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
     for i in range(args.warmup):
         ingest(batches[i])
     times0 = (ctypes_stage_times(ob, st))
     l0 = ob._capi.LIB.octen_launch_count()
-    clk = ClockSampler(local)
-    clk.start()
+    clk.mark()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)

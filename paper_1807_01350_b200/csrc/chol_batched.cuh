@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "devbuf.hpp"
@@ -216,14 +217,17 @@ struct PanelC {
 // column-coalesced.
 constexpr int kTrailLD = kCholNB + 4;
 
-__global__ void __launch_bounds__(256, 2) chol_trail_kernel(double* A, int n, int lda, long long sA, int r0, int k0,
-                                                         int nb, int part) {
+__global__ void __launch_bounds__(256, 3) chol_trail_kernel(double* A, int n, int lda, long long sA, int r0, int k0,
+                                                         int nb, int part, int ntiles, int ntasks) {
     extern __shared__ double trail_smem[];
     double* Pi = trail_smem;                       // [64 k][kTrailLD m]
     double* Pj = trail_smem + kCholNB * kTrailLD;  // [64 k][kTrailLD m]
     // part 0: every lower tile; 1: tile column tj = 0 only (the next panel
-    // column, on the critical path); 2: tile columns tj >= 1 (lookahead)
-    const int t = blockIdx.x;
+    // column, on the critical path); 2: tile columns tj >= 1 (lookahead).
+    // Tasks (tile, matrix) are strided over the grid, so a capped grid
+    // leaves room on the SMs for the critical chain's kernels.
+    for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
+    const int t = task % ntiles, mat = task / ntiles;
     int ti, tj;
     if (part == 1) {
         ti = t;
@@ -238,19 +242,9 @@ __global__ void __launch_bounds__(256, 2) chol_trail_kernel(double* A, int n, in
             ++tj;
         }
     }
-    double* a = A + (size_t)blockIdx.z * sA;
+    double* a = A + (size_t)mat * sA;
     const int i0 = r0 + kCholNB * ti, j0 = r0 + kCholNB * tj;
     const int tid = threadIdx.x;
-    // C tile prefetch (lower part) into registers: its latency overlaps the
-    // panel staging and the DMMAs
-    double cv[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        const int e = tid + 256 * r;
-        const int m = e & (kCholNB - 1), nn = e >> 6;
-        const int gi = i0 + m, gj = j0 + nn;
-        cv[r] = (gi < n && gj < n && gi >= gj) ? a[gi + (size_t)lda * gj] : 0.0;
-    }
     // panels: batches of loads into registers, then shared stores
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -305,12 +299,26 @@ __global__ void __launch_bounds__(256, 2) chol_trail_kernel(double* A, int n, in
                 Cs[m + (kCholNB + 1) * nn] = acc[i][j][v];
             }
     __syncthreads();
+    // read-modify-write of the C tile (lower part), 8 loads in flight per thread
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        const int e = tid + 256 * r;
-        const int m = e & (kCholNB - 1), nn = e >> 6;
-        const int gi = i0 + m, gj = j0 + nn;
-        if (gi < n && gj < n && gi >= gj) a[gi + (size_t)lda * gj] = cv[r] - Cs[m + (kCholNB + 1) * nn];
+    for (int h = 0; h < 2; ++h) {
+        double cv[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = tid + 256 * (8 * h + r);
+            const int m = e & (kCholNB - 1), nn = e >> 6;
+            const int gi = i0 + m, gj = j0 + nn;
+            cv[r] = (gi < n && gj < n && gi >= gj) ? a[gi + (size_t)lda * gj] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = tid + 256 * (8 * h + r);
+            const int m = e & (kCholNB - 1), nn = e >> 6;
+            const int gi = i0 + m, gj = j0 + nn;
+            if (gi < n && gj < n && gi >= gj) a[gi + (size_t)lda * gj] = cv[r] - Cs[m + (kCholNB + 1) * nn];
+        }
+    }
+    __syncthreads();  // Cs aliases the panel buffers of the next task
     }
 }
 
@@ -387,12 +395,21 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
             pending_rest = -1;
         }
         if (prof) cp.mark("wait", crit);
-        chol_trail_kernel<<<dim3(tiles, 1, batch), 256, kTrailSmem, crit>>>(A, n, lda, sA, r0, k0, nb, 1);
+        chol_trail_kernel<<<tiles * batch, 256, kTrailSmem, crit>>>(A, n, lda, sA, r0, k0, nb, 1, tiles,
+                                                                    tiles * batch);
         OCTEN_LAUNCHED(1);
         if (prof) cp.mark("part1", crit);
         if (tiles > 1) {
-            chol_trail_kernel<<<dim3((tiles - 1) * tiles / 2, 1, batch), 256, kTrailSmem, st>>>(A, n, lda, sA, r0, k0,
-                                                                                                 nb, 2);
+            // OCTEN_TRAIL_CAP: cap the grid (tasks are strided over it) to
+            // leave SM room for the critical chain (diagnostics)
+            const int t2 = (tiles - 1) * tiles / 2;
+            static const int cap_env = [] {
+                const char* e = std::getenv("OCTEN_TRAIL_CAP");
+                return e ? std::atoi(e) : 0;
+            }();
+            const int cap = cap_env > 0 ? cap_env : 1 << 30;
+            chol_trail_kernel<<<std::min(t2 * batch, cap), 256, kTrailSmem, st>>>(A, n, lda, sA, r0, k0, nb, 2, t2,
+                                                                                  t2 * batch);
             OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaEventRecord(ev_rest[kb], st));
             pending_rest = kb;
