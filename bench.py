@@ -312,6 +312,11 @@ def main():
     e1.record()
     barrier()
     clocks = clk.stop()
+    if os.environ.get("OCTEN_BENCH_STEPLOG") and not sharded:
+        for rec in st.log[-args.steps:]:
+            print("step %d: compress %.2f als %.2f recover %.2f total %.2f ms" % (
+                rec.batch_index, rec.compress_seconds * 1e3, rec.als_seconds * 1e3, rec.recover_seconds * 1e3,
+                rec.total_seconds * 1e3), file=sys.stderr)
     ms = e0.elapsed_time(e1) / args.steps
     launches = ob._capi.LIB.octen_launch_count() - l0
     times1 = ctypes_stage_times(ob, st)

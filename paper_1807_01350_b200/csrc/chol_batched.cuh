@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "devbuf.hpp"
@@ -544,12 +545,12 @@ constexpr int kSolveThreads = 1024;
 
 __global__ void __launch_bounds__(kSolveThreads) chol_solve_cta_kernel(const double* L, int n, int ldl, long long sL,
                                                                     const double* linv, int nblk, double* X, int ldx,
-                                                                    long long sX) {
+                                                                    long long sX, int backward_only, int nblk_f) {
     extern __shared__ double xs[];  // n (+ 64 padding) + 16 * 64 partials
     double* part = xs + n + kCholNB;
     const int b = blockIdx.y, r = blockIdx.x;
     const double* Lb = L + (size_t)b * sL;
-    const double* ivb = linv + (size_t)b * nblk * kCholNB * kCholNB;
+    const double* ivb = linv + (size_t)b * nblk_f * kCholNB * kCholNB;  // the factor's block count
     double* x = X + (size_t)b * sX + (size_t)r * ldx;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < n + kCholNB; i += kSolveThreads) xs[i] = i < n ? x[i] : 0.0;
@@ -575,7 +576,7 @@ __global__ void __launch_bounds__(kSolveThreads) chol_solve_cta_kernel(const dou
         }
         __syncthreads();
     };
-    for (int kb = 0; kb < nblk; ++kb) {
+    for (int kb = 0; kb < (backward_only ? 0 : nblk); ++kb) {
         const int k0 = kb * kCholNB, nb = min(kCholNB, n - k0);
         block_matvec(ivb + (size_t)kb * kCholNB * kCholNB, k0, nb, false);
         for (int i = k0 + nb + tid; i < n; i += kSolveThreads) {
@@ -632,20 +633,9 @@ __global__ void __launch_bounds__(kSolveThreads) chol_solve_cta_kernel(const dou
     for (int i = tid; i < n; i += kSolveThreads) x[i] = xs[i];
 }
 
-inline void chol_solve_cta(const double* L, int n, int ldl, long long sL, const DevBuf<double>& linv, double* X,
-                           int ldx, long long sX, int nrhs, int batch, cudaStream_t st) {
-    if (n <= 0 || nrhs <= 0 || batch <= 0) return;
-    const int nblk = (n + kCholNB - 1) / kCholNB;
-    const size_t smem = (size_t)(n + kCholNB + 16 * kCholNB) * sizeof(double);
-    if (smem > 48 * 1024)
-        OCTEN_CUDA(cudaFuncSetAttribute(chol_solve_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    chol_solve_cta_kernel<<<dim3(nrhs, batch), kSolveThreads, smem, st>>>(L, n, ldl, sL, linv.p, nblk, X, ldx, sX);
-    OCTEN_LAUNCHED(1);
-}
-
 // Solve L L^T x = b in place (X) using the diagonal-block inverses from
 // chol_batched; Y is scratch of the same layout.
-inline void chol_solve_blocked(const double* L, int n, int ldl, long long sL, const DevBuf<double>& linv, double* X,
+inline void chol_solve_blocked_impl(const double* L, int n, int ldl, long long sL, const DevBuf<double>& linv, double* X,
                                int ldx, long long sX, int nrhs, int batch, cudaStream_t st) {
     if (n <= 0 || nrhs <= 0 || batch <= 0) return;
     static thread_local DevBuf<double> Y;
@@ -666,6 +656,31 @@ inline void chol_solve_blocked(const double* L, int n, int ldl, long long sL, co
                                                                          kb);
         OCTEN_LAUNCHED(1);
     }
+}
+
+// backward_only: X already holds L^-1 b (e.g. the border row of an augmented
+// factorization); only L^-T is applied.  The factor may carry more rows than
+// n (ldl >= n): its diagonal-block inverses are indexed by ceil(ldl / 64)
+// blocks.
+inline void chol_solve_cta(const double* L, int n, int ldl, long long sL, const DevBuf<double>& linv, double* X,
+                           int ldx, long long sX, int nrhs, int batch, cudaStream_t st, bool backward_only = false) {
+    if (n <= 0 || nrhs <= 0 || batch <= 0) return;
+    const int nblk = (n + kCholNB - 1) / kCholNB;
+    static const bool blocked = [] {  // diagnostics: OCTEN_SOLVE_MODE=blocked (one launch per block step)
+        const char* e = std::getenv("OCTEN_SOLVE_MODE");
+        return e && std::string(e) == "blocked";
+    }();
+    if (blocked && !backward_only && ldl == n) {
+        chol_solve_blocked_impl(L, n, ldl, sL, linv, X, ldx, sX, nrhs, batch, st);
+        return;
+    }
+    const int nblk_f = (ldl + kCholNB - 1) / kCholNB;  // blocks of the stored factor (Linv indexing)
+    const size_t smem = (size_t)(n + kCholNB + 16 * kCholNB) * sizeof(double);
+    if (smem > 48 * 1024)
+        OCTEN_CUDA(cudaFuncSetAttribute(chol_solve_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    chol_solve_cta_kernel<<<dim3(nrhs, batch), kSolveThreads, smem, st>>>(L, n, ldl, sL, linv.p, nblk, X, ldx, sX,
+                                                                          backward_only ? 1 : 0, nblk_f);
+    OCTEN_LAUNCHED(1);
 }
 
 }  // namespace octen

@@ -37,15 +37,35 @@ struct BlockCache {
             m.erase(it);
             return p;
         }
+        // New blocks come from the device's stream-ordered pool on a private
+        // stream: unlike cudaMalloc this does not synchronize the device, so
+        // a buffer that grows mid-stream (C, per-batch scratch) does not
+        // stall the kernels in flight.  Freed pool memory is kept (release
+        // threshold max) and the pool is reused.
         void* p = nullptr;
-        cudaError_t e = cudaMalloc(&p, bytes);
+        cudaStream_t s = alloc_stream(dev);
+        cudaError_t e = cudaMallocAsync(&p, bytes, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) {
             (void)cudaGetLastError();
             trim(dev);
-            OCTEN_CUDA(cudaMalloc(&p, bytes));
+            OCTEN_CUDA(cudaMallocAsync(&p, bytes, s));
+            OCTEN_CUDA(cudaStreamSynchronize(s));
         }
         got = bytes;
         return p;
+    }
+    static cudaStream_t alloc_stream(int dev) {
+        static thread_local cudaStream_t s[16] = {};
+        if (!s[dev & 15]) {
+            OCTEN_CUDA(cudaStreamCreateWithFlags(&s[dev & 15], cudaStreamNonBlocking));
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                unsigned long long thr = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        }
+        return s[dev & 15];
     }
     void give(void* p, size_t bytes) {
         int dev = 0;
@@ -54,8 +74,12 @@ struct BlockCache {
     }
     void trim(int dev) {
         OCTEN_CUDA(cudaDeviceSynchronize());
-        for (auto& kv : free_blocks[dev & 15]) cudaFree(kv.second);
+        cudaStream_t s = alloc_stream(dev);
+        for (auto& kv : free_blocks[dev & 15]) cudaFreeAsync(kv.second, s);
         free_blocks[dev & 15].clear();
+        OCTEN_CUDA(cudaStreamSynchronize(s));
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
     }
 };
 

@@ -68,6 +68,12 @@ struct StoreCM {  // C(b, i, j) -> X[b*bs + i + ld j]
     long long bs;
     __device__ void operator()(int b, int i, int j, double v) const { X[(size_t)b * bs + i + (size_t)ld * j] = v; }
 };
+struct BorderStore {  // C(b, i, j) -> X[ld i + ms j]  (row `d` of augmented matrix j; X points at that row)
+    double* X;
+    long long ld;
+    long long ms;
+    __device__ void operator()(int, int i, int j, double v) const { X[(size_t)ld * i + (size_t)ms * j] = v; }
+};
 struct AccumCM {
     double* X;
     long long ld;
@@ -461,7 +467,10 @@ __global__ void weight_mass_kernel(int P, int Q, int R, long long max_dim, doubl
 
 // Gw[r](i,j) = sum_p w_pr^2 G_p(i,j), lower triangle.
 __global__ void __launch_bounds__(256) weighted_gram_kernel(int P, int R, long long d, const double* Gp,
-                                                            const double* w, double* Gw) {
+                                                            const double* w, double* Gw, long long ldg) {
+    // output: matrix r at Gw + r ldg^2, leading dimension ldg (>= d); with
+    // ldg = d + 1 the last row is the border of the augmented system
+    // [G b; b^T -1] (filled by the right-hand-side GEMM; -1 keeps its pivot dead)
     // Gw[r] = sum_p w_pr^2 G_p on the lower triangle; 16 columns r per pass
     // with the squared weights in shared memory (registers hold the partial
     // sums, G_p is streamed once per pass)
@@ -485,8 +494,20 @@ __global__ void __launch_bounds__(256) weighted_gram_kernel(int P, int R, long l
             }
 #pragma unroll
             for (int c = 0; c < 16; ++c)
-                if (r0 + c < R) Gw[(size_t)(r0 + c) * total + e] = acc[c];
+                if (r0 + c < R) Gw[(size_t)(r0 + c) * ldg * ldg + i + (size_t)ldg * j] = acc[c];
         }
+    }
+    if (ldg > d && blockIdx.x == 0)
+        for (int r = threadIdx.x; r < R; r += blockDim.x) Gw[(size_t)r * ldg * ldg + d + (size_t)ldg * d] = -1.0;
+}
+
+// y_r = border row of augmented matrix r (the forward solve L^-1 b_r after
+// the factorization) -> Y[r d + i]
+__global__ void border_row_kernel(int nb, long long d, const double* G, long long ldg, double* Y) {
+    const size_t total = (size_t)nb * d;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const size_t i = e % d, r = e / d;
+        Y[e] = G[r * ldg * ldg + d + ldg * i];
     }
 }
 
@@ -1180,21 +1201,24 @@ void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, dou
             const long long d = dims[fused ? 0 : gi];
             const int nmodes = fused ? 2 : 1;
             const int nb = nmodes * R;
-            Gw.reserve((size_t)nb * d * d);
+            // augmented systems [G_r b_r; b_r^T -1] (ld d + 1): the
+            // factorization leaves the forward solve L^-1 b_r in its last row
+            const long long ldg = d + 1, ms = ldg * ldg;
+            Gw.reserve((size_t)nb * ms);
             sw2.reserve((size_t)d * nb);
             for (int mi = 0; mi < nmodes; ++mi) {
                 const int n = fused ? mi : gi;
-                weighted_gram_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>(P, R, d, Gp[n].p, w.p,
-                                                                              Gw.p + (size_t)mi * R * d * d);
+                double* Gm = Gw.p + (size_t)mi * R * ms;
+                weighted_gram_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>(P, R, d, Gp[n].p, w.p, Gm, ldg);
                 OCTEN_LAUNCHED(1);
                 scale_stack_kernel<<<grid_for((size_t)PQ * R), 256, 0, st>>>(P, Q, R, stacks.p + (size_t)n * PQ * R,
                                                                             w.p, sw.p);
                 OCTEN_LAUNCHED(1);
                 gemm_f64_splitk<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{sw.p, PQ, 0},
-                                      StoreCM{sw2.p + (size_t)mi * R * d, d, 0}, st, kws);
+                                      BorderStore{Gm + d, ldg, ms}, st, kws);
             }
             OCTEN_PROF("wgram+rhs", st);
-            chol_batched(Gw.p, (int)d, (int)d, d * d, nb, kGramRankTol, maxdiag.p, ranks.p, Gw_inv, st);
+            chol_batched(Gw.p, (int)ldg, (int)ldg, ms, nb, kGramRankTol, maxdiag.p, ranks.p, Gw_inv, st);
             OCTEN_PROF("chol", st);
             std::vector<int> rk = ranks.to_host(nb, st);
             for (int mi = 0; mi < nmodes; ++mi) {
@@ -1207,7 +1231,9 @@ void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, dou
             }
             // each column r against its own factor
             OCTEN_PROF("rank-check", st);
-            chol_solve_cta(Gw.p, (int)d, (int)d, d * d, Gw_inv, sw2.p, (int)d, d, 1, nb, st);
+            border_row_kernel<<<grid_for((size_t)nb * d), 256, 0, st>>>(nb, d, Gw.p, ldg, sw2.p);
+            OCTEN_LAUNCHED(1);
+            chol_solve_cta(Gw.p, (int)d, (int)ldg, ms, Gw_inv, sw2.p, (int)d, d, 1, nb, st, /*backward_only=*/true);
             OCTEN_PROF("chol_solve", st);
             for (int mi = 0; mi < nmodes; ++mi) {
                 const int n = fused ? mi : gi;
