@@ -47,6 +47,7 @@ struct AlsDev {
     double* KR;
     double* Mb;
     double* Vinv;  // per problem R x R: inverse (or pseudo-inverse) of the mode's Hadamard Gram
+    int* mcount;   // per problem: finished blocks of the current fused MTTKRP + update launch
     double* fit_hist;
     double* res_hist;
     AlsState* state;
@@ -504,117 +505,15 @@ __device__ void als_vinv_block(const AlsDev& d, int prob, int mode, double* sm) 
 // M(v, r) = sum_u T(u,v,r) F_fsrc(u,r).  One block per (problem, r); the 8
 // warps split the v range, lanes run along the contiguous u index of T; the
 // contract-v partials are combined across warps in fixed order.
-// One T column (Q x Q, u fastest) against the weight vector w: warps take
-// rows v (U rows per round, all loads issued first), lanes run along u.
-template <int NA>
-__device__ __forceinline__ void mttkrp_column(const double* __restrict__ tcol, const double* __restrict__ w,
-                                              double* __restrict__ M, int Q, int contract_first) {
-    constexpr int U = 4;
-    __shared__ double part[8][257];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    if (!contract_first) {  // M(u) = sum_v T(u, v) w(v)
-        double acc[NA];
-#pragma unroll
-        for (int i = 0; i < NA; ++i) acc[i] = 0.0;
-        for (int b0 = warp; b0 < Q; b0 += U * nw) {
-            double x[U][NA], wv[U];
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                const int b = b0 + j * nw;
-                const bool vb = b < Q;
-                wv[j] = vb ? __ldg(w + b) : 0.0;
-                const double* row = tcol + (size_t)Q * b;
-#pragma unroll
-                for (int i = 0; i < NA; ++i) {
-                    const int a = lane + 32 * i;
-                    x[j][i] = (vb && a < Q) ? __ldg(row + a) : 0.0;
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < U; ++j)
-#pragma unroll
-                for (int i = 0; i < NA; ++i) acc[i] += x[j][i] * wv[j];
-        }
-#pragma unroll
-        for (int i = 0; i < NA; ++i) {
-            const int a = lane + 32 * i;
-            if (a < Q) part[warp][a] = acc[i];
-        }
-        __syncthreads();
-        for (int a = threadIdx.x; a < Q; a += blockDim.x) {
-            double sum = 0.0;
-            for (int v = 0; v < nw; ++v) sum += part[v][a];
-            M[a] = sum;
-        }
-    } else {  // M(v) = sum_u T(u, v) w(u)
-        double av[NA];
-#pragma unroll
-        for (int i = 0; i < NA; ++i) {
-            const int a = lane + 32 * i;
-            av[i] = a < Q ? __ldg(w + a) : 0.0;
-        }
-        for (int b0 = warp; b0 < Q; b0 += U * nw) {
-            double acc[U];
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                const int b = b0 + j * nw;
-                const bool vb = b < Q;
-                const double* row = tcol + (size_t)Q * b;
-                double x[NA];
-#pragma unroll
-                for (int i = 0; i < NA; ++i) {
-                    const int a = lane + 32 * i;
-                    x[i] = (vb && a < Q) ? __ldg(row + a) : 0.0;
-                }
-                acc[j] = 0.0;
-#pragma unroll
-                for (int i = 0; i < NA; ++i) acc[j] += x[i] * av[i];
-            }
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                double v = acc[j];
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                const int b = b0 + j * nw;
-                if (lane == 0 && b < Q) M[b] = v;
-            }
-        }
-    }
-}
-
-// The first NP blocks instead form Vi of `mode` (als_vinv_block).
-template <int NA>
-__global__ void __launch_bounds__(256, 3) als_mttkrp_T_kernel(AlsDev d, int contract_first, int fsrc, int mode) {
-    pdl_trigger();
-    pdl_wait();
-    extern __shared__ double vsm[];
-    if ((int)blockIdx.x < d.NP) {
-        if (d.state[blockIdx.x].active) als_vinv_block(d, blockIdx.x, mode, vsm);
-        return;
-    }
-    const int R = d.R, Q = d.Q;
-    const int bid = blockIdx.x - d.NP;
-    const int prob = bid / R, r = bid % R;
-    if (!d.state[prob].active) return;
-    const int p = prob / d.S, s = prob % d.S;
-    const double* tcol = d.T + (size_t)p * d.q2() * d.S * R + (size_t)d.q2() * (s * R + r);
-    double* M = d.Mb + (size_t)prob * Q * R + (size_t)Q * r;
-    const double* w = d.f(prob, fsrc) + (size_t)Q * r;
-    mttkrp_column<NA>(tcol, w, M, Q, contract_first);
-}
-
 // One mode update per problem: raw = M V^-1 (COD of the Hadamard Gram;
 // cp_als.cpp:298-323), non-finite check, normalize into lambda with the
 // seeded rescue, new Gram; after mode 2 the fit and the convergence test
 // (cp_als.cpp:325-345).  V^-1 (als_vinv_block, formed during the MTTKRP)
 // makes raw = M V^-1 a parallel (Q x R)(R x R) product.
-__global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
-    pdl_trigger();
-    pdl_wait();
-    const int prob = blockIdx.x;
+__device__ void als_update_block(const AlsDev& d, int prob, int mode, int sweep, double* sm) {
     AlsState* st = d.state + prob;
     if (!st->active) return;
     const int Q = d.Q, R = d.R;
-    extern __shared__ double sm[];
     double* Vi = sm;                // R*R  (V^-1 or V^+, from als_vinv_block)
     double* raw = Vi + R * R;       // Q*R
     double* Ms = raw + Q * R;       // Q*R  (staged MTTKRP)
@@ -624,7 +523,7 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     __shared__ int bad;
     const double* M = Ms;
 #define OCTEN_TSC(i) \
-    if (d.tsc && threadIdx.x == 0 && blockIdx.x == 0) d.tsc[(i)] = clock64();
+    if (d.tsc && threadIdx.x == 0 && prob == 0) d.tsc[(i)] = clock64();
     OCTEN_TSC(0)
     {
         g2s_copy(Ms, d.Mb + (size_t)prob * Q * R, Q * R);
@@ -752,6 +651,132 @@ __global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
     }
 #undef OCTEN_TSC
 }
+
+__global__ void als_update_kernel(AlsDev d, int mode, int sweep) {
+    pdl_trigger();
+    pdl_wait();
+    extern __shared__ double sm[];
+    als_update_block(d, blockIdx.x, mode, sweep, sm);
+}
+
+// One T column (Q x Q, u fastest) against the weight vector w: warps take
+// rows v (U rows per round, all loads issued first), lanes run along u.
+template <int NA>
+__device__ __forceinline__ void mttkrp_column(const double* __restrict__ tcol, const double* __restrict__ w,
+                                              double* __restrict__ M, int Q, int contract_first) {
+    constexpr int U = 4;
+    __shared__ double part[8][257];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (!contract_first) {  // M(u) = sum_v T(u, v) w(v)
+        double acc[NA];
+#pragma unroll
+        for (int i = 0; i < NA; ++i) acc[i] = 0.0;
+        for (int b0 = warp; b0 < Q; b0 += U * nw) {
+            double x[U][NA], wv[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int b = b0 + j * nw;
+                const bool vb = b < Q;
+                wv[j] = vb ? __ldg(w + b) : 0.0;
+                const double* row = tcol + (size_t)Q * b;
+#pragma unroll
+                for (int i = 0; i < NA; ++i) {
+                    const int a = lane + 32 * i;
+                    x[j][i] = (vb && a < Q) ? __ldg(row + a) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j)
+#pragma unroll
+                for (int i = 0; i < NA; ++i) acc[i] += x[j][i] * wv[j];
+        }
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            const int a = lane + 32 * i;
+            if (a < Q) part[warp][a] = acc[i];
+        }
+        __syncthreads();
+        for (int a = threadIdx.x; a < Q; a += blockDim.x) {
+            double sum = 0.0;
+            for (int v = 0; v < nw; ++v) sum += part[v][a];
+            M[a] = sum;
+        }
+    } else {  // M(v) = sum_u T(u, v) w(u)
+        double av[NA];
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            const int a = lane + 32 * i;
+            av[i] = a < Q ? __ldg(w + a) : 0.0;
+        }
+        for (int b0 = warp; b0 < Q; b0 += U * nw) {
+            double acc[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int b = b0 + j * nw;
+                const bool vb = b < Q;
+                const double* row = tcol + (size_t)Q * b;
+                double x[NA];
+#pragma unroll
+                for (int i = 0; i < NA; ++i) {
+                    const int a = lane + 32 * i;
+                    x[i] = (vb && a < Q) ? __ldg(row + a) : 0.0;
+                }
+                acc[j] = 0.0;
+#pragma unroll
+                for (int i = 0; i < NA; ++i) acc[j] += x[i] * av[i];
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                double v = acc[j];
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                const int b = b0 + j * nw;
+                if (lane == 0 && b < Q) M[b] = v;
+            }
+        }
+    }
+}
+
+// The first NP blocks instead form Vi of `mode` (als_vinv_block).  With
+// `fused`, the last of a problem's R + 1 blocks to finish (fence + counter)
+// runs the mode update for it (als_update_block), so the update needs no
+// launch of its own and overlaps the other problems' contractions.
+template <int NA>
+__global__ void __launch_bounds__(256, 3) als_mttkrp_T_kernel(AlsDev d, int contract_first, int fsrc, int mode,
+                                                              int sweep, int fused) {
+    pdl_trigger();
+    pdl_wait();
+    extern __shared__ double vsm[];
+    const int R = d.R, Q = d.Q;
+    int prob;
+    if ((int)blockIdx.x < d.NP) {
+        prob = blockIdx.x;
+        if (!d.state[prob].active) return;
+        als_vinv_block(d, prob, mode, vsm);
+    } else {
+        const int bid = blockIdx.x - d.NP;
+        prob = bid / R;
+        const int r = bid % R;
+        if (!d.state[prob].active) return;
+        const int p = prob / d.S, s = prob % d.S;
+        const double* tcol = d.T + (size_t)p * d.q2() * d.S * R + (size_t)d.q2() * (s * R + r);
+        double* M = d.Mb + (size_t)prob * Q * R + (size_t)Q * r;
+        const double* w = d.f(prob, fsrc) + (size_t)Q * r;
+        mttkrp_column<NA>(tcol, w, M, Q, contract_first);
+    }
+    if (!fused) return;
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(d.mcount + prob, 1) == R;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x == 0) d.mcount[prob] = 0;
+    als_update_block(d, prob, mode, sweep, vsm);
+}
+
 
 // Best restart per replica (strictly greater final fit wins; cp_als.cpp:347-356).
 __global__ void als_select_kernel(AlsDev d, double* Mf, double* Mlam, int* best_out) {
@@ -1107,6 +1132,8 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     d.KR = KR.p;
     d.Mb = Mb.p;
     d.Vinv = Vinv.p;
+    mcount.reserve(NP);
+    d.mcount = mcount.p;
     d.fit_hist = fit_hist.p;
     d.res_hist = res_hist.p;
     d.state = state.p;
@@ -1296,7 +1323,12 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     OCTEN_CUDA(cudaFuncSetAttribute(als_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_upd));
     const size_t smem_vinv = (size_t)(4 * R * R + 2 * (R + 2) + 256) * sizeof(double) + (R + 8) * sizeof(int) + 16;
     auto mttkrp_kernel = Q <= 128 ? als_mttkrp_T_kernel<4> : als_mttkrp_T_kernel<8>;
-    OCTEN_CUDA(cudaFuncSetAttribute(mttkrp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_vinv));
+    // MTTKRP + update fused in one launch unless OCTEN_ALS_NOFUSE (diagnostics)
+    static const bool fuse_update = std::getenv("OCTEN_ALS_NOFUSE") == nullptr;
+    const size_t smem_mk = fuse_update ? std::max(smem_vinv, smem_upd) : smem_vinv;
+    OCTEN_CUDA(cudaFuncSetAttribute(mttkrp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mk));
+    mcount.reserve(NP);
+    mcount.zero(NP, st);
     // 16-byte pairs along every fast index need an even Q (and aligned bases)
     const bool pipe_ok = (Q % 2 == 0) && ((uintptr_t)dY % 16 == 0) && ((uintptr_t)F.p % 16 == 0) &&
                          ((uintptr_t)KR.p % 16 == 0);
@@ -1365,6 +1397,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         x.KR = KR.p + (size_t)pb * q2 * SR;
         x.Mb = Mb.p + (size_t)qb * Q * R;
         x.Vinv = Vinv.p + (size_t)qb * R * R;
+        x.mcount = mcount.p + qb;
         x.fit_hist = fit_hist.p + (size_t)qb * max_iters;
         x.res_hist = res_hist.p + (size_t)qb * max_iters;
         x.state = state.p + qb;
@@ -1447,13 +1480,16 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             mark(l, sw, contracted == 2 ? "gemm Yx3C" : contracted == 1 ? "gemm Yx2B" : "gemm Yx1A", ss);
         };
         auto mode_step = [&](int contract_first, int fsrc, int mode) {
+            const int fz = fuse_update ? 1 : 0;
             if (use_pdl) {
-                launch_pdl(mttkrp_kernel, dim3(npn * (R + 1)), dim3(256), smem_vinv, ss, x, contract_first, fsrc, mode);
+                launch_pdl(mttkrp_kernel, dim3(npn * (R + 1)), dim3(256), smem_mk, ss, x, contract_first, fsrc, mode,
+                           sw, fz);
             } else {
-                mttkrp_kernel<<<npn * (R + 1), 256, smem_vinv, ss>>>(x, contract_first, fsrc, mode);
+                mttkrp_kernel<<<npn * (R + 1), 256, smem_mk, ss>>>(x, contract_first, fsrc, mode, sw, fz);
                 OCTEN_LAUNCHED(1);
             }
             mark(l, sw, mode == 0 ? "mttkrp0" : mode == 1 ? "mttkrp1" : "mttkrp2", ss);
+            if (fuse_update) return;
             if (use_pdl) {
                 launch_pdl(als_update_kernel, dim3(npn), dim3(upd_threads), smem_upd, ss, x, mode, sw);
             } else {

@@ -76,7 +76,7 @@ private:
     static constexpr int kGin = 1, kGout = 1 + kMaxLanes, kSweepEv = 1 + 2 * kMaxLanes;
     cudaEvent_t lane_ev[1 + 4 * kMaxLanes] = {};
     DevBuf<double> Gev, EV, Ur, Wmix, Smix, Tmp6, Pm, Hh, gscr;
-    DevBuf<int> usable, att_start, att_used, todo, peel_fail, eigdbg;
+    DevBuf<int> usable, att_start, att_used, todo, peel_fail, eigdbg, mcount;
     DevBuf<AlsState> state;
     DevBuf<DevStatus> err;
     DevBuf<Mt64> rngs;
