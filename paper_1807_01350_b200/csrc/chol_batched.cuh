@@ -56,8 +56,9 @@ __global__ void chol_maxdiag_kernel(const double* A, int n, int lda, long long s
 // only 528 elements (one or two per thread), so the 64 sequential steps are
 // cheap; the coupling products are fully parallel.  A pivot <= tol * maxdiag
 // is dead: its column of L and row of L^-1 become zero and the rank drops.
-constexpr int kDiagThreads = 128;
+constexpr int kDiagThreads = 256;
 constexpr int kHalf = kCholNB / 2;
+constexpr int kDiagPer = (kHalf * (kHalf + 1) / 2 + kDiagThreads - 1) / kDiagThreads;  // packed elements per thread
 constexpr int kDLD = kCholNB + 1;  // shared leading dimension
 constexpr size_t kDiagSmem = (size_t)(2 * kCholNB * kDLD + kHalf * (kHalf + 1) + 160) * sizeof(double);
 __device__ long long g_diag_tsc[16];  // OCTEN_PROFILE: phase clocks of block 0 at k0 == 0
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
     const int tid = threadIdx.x;
     DIAG_TSC(0)
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
+    for (int h = 0; h < kCholNB * kCholNB / (8 * kDiagThreads); ++h) {
         double v[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
     __syncthreads();
     DIAG_TSC(1)
     const int n1 = min(kHalf, nb);
-    const int rk1 = block_chol_inv_t<5, kDiagThreads>(S, kDLD, n1, thr, S, kDLD, X, kDLD, scr);
+    const int rk1 = block_chol_inv_t<kDiagPer, kDiagThreads>(S, kDLD, n1, thr, S, kDLD, X, kDLD, scr);
     DIAG_TSC(2)
     int dead = n1 - rk1;
     const int n2 = nb - n1;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(kDiagThreads) chol_diag_kernel(double* A, int 
         }
         __syncthreads();
         DIAG_TSC(3)
-        const int rk2 = block_chol_inv_t<5, kDiagThreads>(A22, kDLD, n2, thr, A22, kDLD, X22, kDLD, scr);
+        const int rk2 = block_chol_inv_t<kDiagPer, kDiagThreads>(A22, kDLD, n2, thr, A22, kDLD, X22, kDLD, scr);
         DIAG_TSC(4)
         dead += n2 - rk2;
         // X21 = -X22 (L21 X11): T = L21 X11, then X21 = -X22 T
