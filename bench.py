@@ -39,6 +39,10 @@ CONFIGS = {
     "c2": dict(I=500, J=500, K0=500, t=50, Q=50, P=8, R=10, shared=12, iters=30, restarts=3),
     "small": dict(I=200, J=200, K0=100, t=20, Q=20, P=16, R=5, shared=5, iters=30, restarts=3),
 }
+# c4: sparse COO 1e5 x 1e5 x 2e4 (~1e8 nnz), batches of 1000 slices (~5e6 nnz),
+# Zipf(1.2) rows/columns, uniform slices, U(0,1) values; compression + CP-ALS
+# (the reference's merge throws NumericError at this shape)
+C4 = dict(I=100000, J=100000, t=1000, Q=64, P=16, R=16, nnz=5_000_000, zipf=1.2, iters=30, restarts=3)
 
 
 def peaks():
@@ -233,6 +237,155 @@ def run_reference(args, cfg, rank, world):
 
 
 # ---------------------------------------------------------------------------
+# c4: sparse COO batches
+# ---------------------------------------------------------------------------
+
+class CooSynth:
+    """c4 batches generated on the device: i, j ~ truncated Zipf(1.2) on the
+    extents (inverse CDF), k uniform in the batch, values U(0,1); duplicate
+    (i, j, k) are dropped (the reference rejects them, tensor.cpp:99-100) and
+    the survivors shuffled into arbitrary input order."""
+
+    def __init__(self, torch, dev, c, seed):
+        self.torch, self.dev, self.c = torch, dev, c
+        self.g = torch.Generator(device=dev)
+        self.g.manual_seed(seed)
+        w = torch.arange(1, c["I"] + 1, device=dev, dtype=torch.float64).pow(-c["zipf"])
+        self.cdf = torch.cumsum(w, 0) / w.sum()
+
+    def batch(self):
+        torch, c, g = self.torch, self.c, self.g
+        n = int(c["nnz"] * 1.7)  # Zipf(1.2) pairs collide: ~1/3 of the draws are duplicates
+        I, J, t = c["I"], c["J"], c["t"]
+        i = torch.searchsorted(self.cdf, torch.rand(n, generator=g, device=self.dev, dtype=torch.float64))
+        j = torch.searchsorted(self.cdf, torch.rand(n, generator=g, device=self.dev, dtype=torch.float64))
+        i.clamp_(max=I - 1)
+        j.clamp_(max=J - 1)
+        k = torch.randint(0, t, (n,), generator=g, device=self.dev)
+        key = torch.unique((k * I + i) * J + j)
+        key = key[torch.randperm(key.numel(), generator=g, device=self.dev)][: c["nnz"]]
+        jj = (key % J).to(torch.int32)
+        ii = ((key // J) % I).to(torch.int32)
+        kk = (key // (I * J)).to(torch.int32)
+        v = torch.rand(key.numel(), generator=g, device=self.dev, dtype=torch.float32)
+        return ii.contiguous(), jj.contiguous(), kk.contiguous(), v
+
+
+def run_sparse(args, torch, dev, ob, steps, warmup, with_cpu):
+    """c4 step = compress one ~5e6-nnz COO batch into the P=16 summaries +
+    CP-ALS on every replica.  Each call of the C-ABI is synchronous (the
+    batch is validated before the summaries change), so a step is timed by
+    the host clock between device synchronizations; the L2 is flushed
+    between steps outside the timed region."""
+    c = C4
+    I, J, t, Q, P, R = (c[k] for k in ("I", "J", "t", "Q", "P", "R"))
+    r = np.random.default_rng(11)
+    u = [r.random((I, Q)) for _ in range(P)]
+    v = [r.random((J, Q)) for _ in range(P)]
+    t0 = time.perf_counter()
+    hs = ob.CooSummaries(u, v, device=dev.index or 0)
+    t_setup = time.perf_counter() - t0
+    syn = CooSynth(torch, dev, c, 99)
+    nb = warmup + steps
+    batches = [syn.batch() for _ in range(nb)]
+    ws = [torch.rand((P, Q, t), generator=syn.g, device=dev, dtype=torch.float64) for _ in range(nb)]
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    cfg = ob.AlsConfig(max_iters=c["iters"], rel_tol=1e-8, n_restarts=c["restarts"])
+    cfg.rank = R
+    seeds = list(range(100, 100 + P))
+    torch.cuda.synchronize()
+    tot = tc = 0.0
+    nnz_timed = 0
+    launches = 0
+    st0 = None
+    for s in range(nb):
+        ii, jj, kk, vv = batches[s]
+        flush.fill_(float(s))
+        torch.cuda.synchronize()
+        if s == warmup:
+            st0 = hs.stage_times()
+            l0 = ob._capi.LIB.octen_launch_count()
+        a = time.perf_counter()
+        hs.compress_device(t, ws[s], ii, jj, kk, vv)
+        b = time.perf_counter()
+        hs.cp_als(cfg, seeds, fetch=False)
+        e = time.perf_counter()
+        if s >= warmup:
+            tot += e - a
+            tc += b - a
+            nnz_timed += vv.numel()
+    launches = ob._capi.LIB.octen_launch_count() - l0
+    st1 = hs.stage_times()
+    d = {k: st1[k] - st0[k] for k in st1}
+    nb_t = max(d["batches"], 1)
+    nnz_step = nnz_timed / steps
+    groups = d["groups"] / nb_t
+    slice_ms = d["slice_ms"] / nb_t
+    flops = 2.0 * P * (nnz_step * Q + groups * Q * Q)  # useful flops of the slice kernel per launch
+    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+    out = {"metric": "nnz streamed/sec per batch update", "value": nnz_timed / tot, "unit": "nnz/s",
+           "ms_per_step": tot * 1e3 / steps, "steps": steps, "warmup": warmup,
+           "compress_nnz_per_s": nnz_timed / tc,
+           "config": {"workload": "c4", **c, "nnz_per_batch": nnz_step, "groups_per_batch": groups,
+                      "l2": "flushed between steps (256 MB write)", "projections": "U(0,1) fp64, fp32 on device"},
+           "stages_ms": {"validate_sort": d["prep_ms"] / nb_t, "slice_kernel": slice_ms,
+                         "mode3_accumulate": d["accum_ms"] / nb_t, "cp_als": d["als_ms"] / max(d["als_runs"], 1),
+                         "compress_host_clock": tc * 1e3 / steps},
+           "roofline": {"kernel": "coo_slice_kernel (gather-accumulate + per-(k,i) rank-1 updates)",
+                        "bound": "fp32 FFMA", "achieved": flops / (slice_ms * 1e-3) / 1e12 if slice_ms else 0.0,
+                        "peak": fp32_peak, "unit": "TFLOP/s",
+                        "frac": flops / (slice_ms * 1e-3) / 1e12 / fp32_peak if slice_ms else 0.0,
+                        "peak_source": "nominal FP32 FFMA: 148 SMs x 128 lanes x 2 x 1.965 GHz (not measured)",
+                        "flops_per_launch": flops, "traffic": None},
+           "gpu_launches": int(launches), "setup_s": t_setup}
+    # e2e: host COO arrays + host temporal rows through the public API, model read back
+    if args.e2e_steps > 0:
+        hb = []
+        for s in range(args.e2e_steps + 1):
+            ii, jj, kk, vv = syn.batch()
+            idx = np.stack([ii.cpu().numpy(), jj.cpu().numpy(), kk.cpu().numpy()], 1)
+            hb.append((ob.SparseTensor((I, J, t), idx, vv.cpu().numpy()), [r.random((t, Q)) for _ in range(P)]))
+        hs.compress(*hb[0])
+        hs.cp_als(cfg, seeds)
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        nn = 0
+        for sp, w in hb[1:]:
+            hs.compress(sp, w)
+            hs.cp_als(cfg, seeds)
+            nn += sp.nnz
+        e2e_s = time.perf_counter() - a
+        out["e2e"] = {"value": nn / e2e_s, "unit": "nnz/s",
+                      "h2d_bytes_per_step": int(nn / args.e2e_steps * 16 + P * t * Q * 8),
+                      "d2h_bytes_per_step": P * (3 * Q * R + R) * 8}
+    if with_cpu:
+        out["cpu_baseline"] = cpu_sample_sparse(batches[0], ws[0], u, v, P, R, c)
+    return out
+
+
+def cpu_sample_sparse(batch, w, u, v, P, R, c, sample=50_000):
+    """Oracle port on the host: the entry-wise compress (compress_coo_direct,
+    = compress(to_dense(batch))) of `sample` entries for one replica, scaled
+    to the batch's nnz and P replicas, + CP-ALS (cp_als.cpp) on one Q^3
+    replica summary scaled by P."""
+    from oracle import octen_oracle as O
+    ii, jj, kk, vv = (x.cpu().numpy() for x in batch)
+    wh = w[0].cpu().numpy().T  # t x Q
+    n = min(sample, ii.size)
+    a = time.perf_counter()
+    z = O.compress_coo_direct(ii[:n], jj[:n], kk[:n], vv[:n].astype(np.float64), u[0], v[0], wh)
+    tcomp = (time.perf_counter() - a) * (ii.size / n) * P
+    a = time.perf_counter()
+    O.cp_als(z, O.AlsConfig(R, c["iters"], 1e-8, c["restarts"], 5))
+    tals = (time.perf_counter() - a) * P
+    sec = tcomp + tals
+    return {"value": ii.size / sec, "unit": "nnz/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": "oracle port: entry-wise compress of %d of %d nnz for 1 of %d replicas + CP-ALS on 1 replica, "
+                      "scaled" % (n, ii.size, P),
+            "stages_s": {"compress_s": tcomp, "als_s": tals}}
+
+
+# ---------------------------------------------------------------------------
 # own arm
 # ---------------------------------------------------------------------------
 
@@ -242,7 +395,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="octen", choices=["octen", "reference"])
-    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + ["c4"])
+    ap.add_argument("--no-sparse", action="store_true", help="skip the c4 sparse leg of the default line")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
@@ -250,7 +404,7 @@ def main():
                     help="N>1: one replica-sharded stream over all ranks (NCCL all-gathers, strong scaling) "
                          "or N independent streams (weak scaling)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = CONFIGS.get(args.config, C4)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -272,6 +426,14 @@ def main():
         torch.cuda.synchronize()
 
     import paper_1807_01350_b200 as ob
+    if args.config == "c4":
+        sp = run_sparse(args, torch, dev, ob, args.steps, args.warmup,
+                        rank == 0 and world == 1 and not args.no_cpu_baseline)
+        if rank == 0:
+            sp.update({"n_gpus": world, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                       "dtype": "f32 slice products + f64 mode-3 accumulate / CP-ALS", "data": "synthetic"})
+            print(json.dumps(sp), flush=True)
+        return
     I, J, K0, t, Q, P, R, sh = (cfg[k] for k in ("I", "J", "K0", "t", "Q", "P", "R", "shared"))
     nb = args.warmup + args.steps + args.e2e_steps + 1
     sharded = world > 1 and args.multi == "sharded"
@@ -389,6 +551,14 @@ def main():
             cpu = {"value": None, "unit": "entries/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": "failed: %r" % (exc,)}
 
+    sparse = None
+    if rank == 0 and world == 1 and not args.no_sparse and args.config == "c3":
+        del batches
+        try:
+            sparse = run_sparse(args, torch, dev, ob, 3, 3, not args.no_cpu_baseline)
+        except Exception as exc:  # pragma: no cover
+            sparse = {"error": repr(exc)}
+
     if rank == 0:
         line = {"metric": "tensor entries streamed/sec per batch update", "value": value, "unit": "entries/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -400,6 +570,8 @@ def main():
                                                             else "single"))},
                 "stages": stage, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks}
+        if sparse is not None:
+            line["sparse_c4"] = sparse
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -186,6 +186,56 @@ int octen_temporal_stack_from_summaries(int p, int q, int rank, int64_t I, int64
 int octen_recover_temporal_append(int p, int q, int rank, int64_t t, const double* temporal_stack,
                                   const double* w, double* history, double* new_rows, double* residual);
 
+/* ---- sparse (COO) temporal batches ----
+ * The reference ingests coordinate data as SparseTensor
+ * (proj/include/cpstream/tensor.hpp:66-90; read_tensor_coo, src/io.cpp:49-84),
+ * whose constructor validates it (src/tensor.cpp:87-102), and densifies it
+ * before compress/update_summaries (read_tensor_any, src/io.cpp:124-132;
+ * src/compression.cpp:108-153).  These entry points compress the COO batch
+ * directly, with the same result (to fp32 accumulation of the slice products)
+ * and the same errors, checked before the summaries change:
+ *   index out of bounds -> OCTEN_ERR_CONFIG "SparseTensor: index out of bounds"
+ *   non-finite value    -> OCTEN_ERR_NUMERIC "SparseTensor: non-finite value"
+ *   duplicate index     -> OCTEN_ERR_CONFIG "SparseTensor: duplicate index"
+ * (the first offending entry in input order wins, as in the reference).
+ * Entries are SoA: i[nnz], j[nnz], k[nnz] (0-based int32, k is the slice
+ * within this batch, 0 <= k < t) and values[nnz] (fp32).  Q <= 128. */
+typedef struct octen_coo_summaries octen_coo_summaries;
+
+/* Device-resident SummaryState for a COO stream (compression.hpp:56-60,
+ * init_summaries compression.cpp:132-139) over replicas u: p x I x Q,
+ * v: p x J x Q (host, col-major per replica). */
+int octen_coo_create(int p, int q, int64_t I, int64_t J, const double* u, const double* v, int device,
+                     octen_coo_summaries** out);
+/* update_summaries(S, compress(to_dense(batch))) for every replica.
+ * w: p x t x Q temporal rows of this batch (col-major per replica).  With
+ * location OCTEN_DEVICE, w/i/j/k/values are device pointers. */
+int octen_coo_compress(octen_coo_summaries* h, int64_t t, const double* w, int64_t nnz, const int32_t* i,
+                       const int32_t* j, const int32_t* k, const float* values, int location);
+/* y: p x Q^3 (host). */
+int octen_coo_get_summaries(const octen_coo_summaries* h, double* y);
+/* Zero the summaries. */
+int octen_coo_reset(octen_coo_summaries* h);
+/* cp_als (cp_als.hpp:48) on every resident summary, seeds[p]; outputs as
+ * octen_cp_als_batched (any output pointer may be NULL). */
+int octen_coo_cp_als(octen_coo_summaries* h, const octen_als_config* cfg, const uint64_t* seeds, double* factors,
+                     double* lambda, double* fit, int32_t* iterations);
+/* Cumulative device times (CUDA events on the handle's stream):
+ * out[0] validate + sort ms, out[1] slice-kernel ms, out[2] mode-3
+ * accumulate ms, out[3] distinct (k, i) groups, out[4] nnz, out[5] batches,
+ * out[6] CP-ALS ms, out[7] CP-ALS runs. */
+int octen_coo_stage_times(const octen_coo_summaries* h, double* out);
+/* Raw CUDA stream of the handle (cudaStream_t), for callers that order
+ * their own device work against it. */
+void* octen_coo_cuda_stream(const octen_coo_summaries* h);
+void octen_coo_destroy(octen_coo_summaries* h);
+
+/* One-shot compress of a COO batch (host arrays): z = p x Q^3 (host,
+ * overwritten) = compress(to_dense(batch)) per replica. */
+int octen_compress_coo(int p, int q, int64_t I, int64_t J, int64_t t, const double* u, const double* v,
+                       const double* w, int64_t nnz, const int32_t* i, const int32_t* j, const int32_t* k,
+                       const float* values, double* z);
+
 #ifdef __cplusplus
 }
 #endif

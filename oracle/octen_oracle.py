@@ -249,6 +249,55 @@ def compress(t: np.ndarray, rs: ReplicaSet, replica: int, row_begin: int, row_en
     return out
 
 
+def sparse_to_dense(shape, indices, values) -> np.ndarray:
+    """SparseTensor validation (tensor.cpp:87-102) then to_dense
+    (tensor.cpp:118-122).  indices: nnz x order (0-based), values: nnz.
+    Entries are checked in input order; per entry arity, then bounds, then
+    finiteness, then duplicates, as the constructor does."""
+    shape = tuple(int(d) for d in shape)
+    if any(d < 1 for d in shape):
+        raise ConfigError("Shape: dimensions must be positive")
+    idx = np.asarray(indices, dtype=np.int64).reshape(-1, len(shape)) if len(indices) else np.zeros((0, len(shape)), np.int64)
+    vals = np.asarray(values, dtype=np.float64)
+    seen = set()
+    for e in range(idx.shape[0]):
+        ix = tuple(int(x) for x in idx[e])
+        for m in range(len(shape)):
+            if ix[m] < 0 or ix[m] >= shape[m]:
+                raise ConfigError("SparseTensor: index out of bounds")
+        if not math.isfinite(vals[e]):
+            raise NumericError("SparseTensor: non-finite value")
+        if ix in seen:
+            raise ConfigError("SparseTensor: duplicate index")
+        seen.add(ix)
+    out = np.zeros(shape, order="F")
+    if idx.shape[0]:
+        out[tuple(idx.T)] = vals
+    return out
+
+
+def compress_coo_direct(i, j, k, vals, u: np.ndarray, v: np.ndarray, w: np.ndarray, chunk: int = 1 << 14) -> np.ndarray:
+    """compress(to_dense(batch)) (compression.cpp:108-130 on tensor.cpp:118-122)
+    for one replica, evaluated entry-wise without densifying:
+    Z(a,b,c) = sum_e v_e U(i_e,a) V(j_e,b) W(k_e,c).  Equal to the dense
+    compress by linearity of the mode products (checked against it in
+    tests/test_oracle_kat.py)."""
+    q = u.shape[1]
+    z = np.zeros((q, q * q))
+    for s in range(0, len(vals), chunk):
+        e = slice(s, s + chunk)
+        a = u[i[e]] * np.asarray(vals[e], dtype=np.float64)[:, None]
+        kr = (v[j[e]][:, :, None] * w[k[e]][:, None, :]).reshape(-1, q * q)  # column b + Q c
+        z += a.T @ kr
+    return z.reshape(q, q, q)  # [a, b, c]
+
+
+def coo_probe(i, j, k, vals, u, v, w, a, b, c) -> float:
+    """<compress(to_dense(batch)), a (x) b (x) c> = sum_e v_e (U a)_i (V b)_j (W c)_k,
+    exact in O(nnz): the size-independent check of a full-scale compression."""
+    return float(np.sum(np.asarray(vals, np.float64) * (u @ a)[i] * (v @ b)[j] * (w @ c)[k]))
+
+
 @dataclass
 class SummaryState:
     """compression.hpp:56-60."""

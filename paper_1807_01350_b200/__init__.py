@@ -24,7 +24,7 @@ from . import sharding as _sharding
 __all__ = ["ConfigError", "NumericError", "IoError", "CudaError", "AlsConfig", "StreamConfig", "BatchRecord",
            "KruskalModel", "StreamState", "init_stream", "ingest_batch", "compress", "cp_als_batched",
            "align_replicas", "recover_nontemporal", "temporal_stack_from_summaries", "recover_temporal_append",
-           "version"]
+           "SparseTensor", "CooSummaries", "compress_coo", "version"]
 
 
 class Error(RuntimeError):
@@ -440,3 +440,143 @@ def recover_temporal_append(temporal_stack: np.ndarray, w: List[np.ndarray], his
     for i in range(p):
         history[i] = H[i * q * rank:(i + 1) * q * rank].reshape((q, rank), order="F").copy()
     return rows, res.value
+
+
+# ---------------------------------------------------------------------------
+# Sparse (COO) temporal batches
+# ---------------------------------------------------------------------------
+
+class SparseTensor:
+    """tensor.hpp:66-90 -- a COO temporal batch of shape (I, J, t): indices
+    (nnz x 3, 0-based; the third is the slice within the batch) and values.
+    Stored SoA (int32 i, j, k; float32 values) for the device.  Validation
+    (tensor.cpp:87-102) happens on the device when the batch is compressed,
+    with the reference's exceptions and messages."""
+
+    def __init__(self, shape, indices, values):
+        if len(shape) != 3:
+            raise ConfigError("octen: sparse batches are order-3 (I, J, t)")
+        self.shape = tuple(int(d) for d in shape)
+        idx = np.asarray(indices)
+        if idx.size == 0:
+            idx = np.zeros((0, 3), dtype=np.int64)
+        if idx.ndim != 2 or idx.shape[1] != 3:
+            raise ConfigError("SparseTensor: index arity mismatch")
+        if np.any(idx > np.iinfo(np.int32).max) or np.any(idx < np.iinfo(np.int32).min):
+            raise ConfigError("SparseTensor: index out of bounds")
+        self.i = np.ascontiguousarray(idx[:, 0], dtype=np.int32)
+        self.j = np.ascontiguousarray(idx[:, 1], dtype=np.int32)
+        self.k = np.ascontiguousarray(idx[:, 2], dtype=np.int32)
+        self.values = np.ascontiguousarray(values, dtype=np.float32)
+        if self.values.shape != (idx.shape[0],):
+            raise ConfigError("SparseTensor: values do not match indices")
+
+    @property
+    def nnz(self) -> int:
+        return int(self.values.shape[0])
+
+    @staticmethod
+    def from_dense(t) -> "SparseTensor":
+        """tensor.cpp:104-116 (nonzeros in first-index-fastest order)."""
+        a = np.asarray(t)
+        flat = a.ravel(order="F")
+        nz = np.nonzero(flat)[0]
+        idx = np.stack(np.unravel_index(nz, a.shape, order="F"), axis=1)
+        return SparseTensor(a.shape, idx, flat[nz])
+
+
+def _stack_cols(mats, rows, q):
+    return np.concatenate([_f64(m).reshape(rows, q, order="F").ravel(order="F") for m in mats])
+
+
+class CooSummaries:
+    """Device-resident SummaryState (compression.hpp:56-60) fed by COO
+    batches: compress() is update_summaries(compress(to_dense(batch)))
+    (compression.cpp:108-153, io.cpp:124-132) without densifying."""
+
+    def __init__(self, u: List[np.ndarray], v: List[np.ndarray], device: int = 0):
+        self.p = len(u)
+        self.I, self.q = np.asarray(u[0]).shape
+        self.J = np.asarray(v[0]).shape[0]
+        U = _stack_cols(u, self.I, self.q)
+        V = _stack_cols(v, self.J, self.q)
+        h = ctypes.c_void_p()
+        _check(C.LIB.octen_coo_create(self.p, self.q, self.I, self.J, _dptr(U), _dptr(V), device, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            C.LIB.octen_coo_destroy(h)
+            self._h = None
+
+    def compress(self, batch: SparseTensor, w) -> None:
+        """w: per-replica temporal rows of this batch (t x Q each) or a
+        stacked (p, t, Q) array."""
+        t = batch.shape[2]
+        if (batch.shape[0], batch.shape[1]) != (self.I, self.J):
+            raise ConfigError("compress: extent mismatch on mode 1")
+        W = _stack_cols(list(w), t, self.q)
+        _check(C.LIB.octen_coo_compress(self._h, t, W.ctypes.data, batch.nnz, batch.i.ctypes.data,
+                                        batch.j.ctypes.data, batch.k.ctypes.data, batch.values.ctypes.data,
+                                        C.OCTEN_HOST))
+
+    def compress_device(self, t: int, w, i, j, k, values) -> None:
+        """Device-resident inputs (torch CUDA tensors): w float64 (p, Q, t)
+        contiguous = per replica t x Q column-major; i, j, k int32; values
+        float32."""
+        _check(C.LIB.octen_coo_compress(self._h, int(t), w.data_ptr(), int(values.numel()), i.data_ptr(),
+                                        j.data_ptr(), k.data_ptr(), values.data_ptr(), C.OCTEN_DEVICE))
+
+    def summaries(self) -> List[np.ndarray]:
+        q3 = self.q ** 3
+        y = np.zeros(self.p * q3)
+        _check(C.LIB.octen_coo_get_summaries(self._h, _dptr(y)))
+        return [y[r * q3:(r + 1) * q3].reshape((self.q,) * 3, order="F") for r in range(self.p)]
+
+    def reset(self) -> None:
+        _check(C.LIB.octen_coo_reset(self._h))
+
+    def cp_als(self, cfg: AlsConfig, seeds: List[int], fetch: bool = True):
+        """cp_als (cp_als.cpp:240-359) on every resident summary."""
+        p, q, r = self.p, self.q, cfg.rank
+        f = np.zeros(p * 3 * q * r)
+        lam = np.zeros(p * r)
+        fit = np.zeros(p)
+        it = np.zeros(p, dtype=np.int32)
+        sd = (C.c_u64 * p)(*seeds)
+        c = cfg._c()
+        _check(C.LIB.octen_coo_cp_als(self._h, ctypes.byref(c), sd, _dptr(f) if fetch else None,
+                                      _dptr(lam) if fetch else None, _dptr(fit), it.ctypes.data_as(C.P_i32)))
+        models = []
+        for i in range(p):
+            fs = [f[(i * 3 + n) * q * r:(i * 3 + n + 1) * q * r].reshape((q, r), order="F").copy() for n in range(3)]
+            models.append(KruskalModel(fs, lam[i * r:(i + 1) * r].copy()))
+        return models, fit, it
+
+    def stage_times(self) -> dict:
+        out = np.zeros(8)
+        _check(C.LIB.octen_coo_stage_times(self._h, _dptr(out)))
+        keys = ["prep_ms", "slice_ms", "accum_ms", "groups", "nnz", "batches", "als_ms", "als_runs"]
+        return dict(zip(keys, out.tolist()))
+
+    def cuda_stream(self) -> int:
+        return int(C.LIB.octen_coo_cuda_stream(self._h) or 0)
+
+
+def compress_coo(batch: SparseTensor, u: List[np.ndarray], v: List[np.ndarray], w: List[np.ndarray]) -> List[np.ndarray]:
+    """compress (compression.cpp:108-130) of to_dense(batch) for every
+    replica, computed from the COO entries on the device."""
+    p = len(u)
+    I, q = np.asarray(u[0]).shape
+    J = np.asarray(v[0]).shape[0]
+    t = batch.shape[2]
+    if (batch.shape[0], batch.shape[1]) != (I, J):
+        raise ConfigError("compress: extent mismatch on mode 1")
+    U = _stack_cols(u, I, q)
+    V = _stack_cols(v, J, q)
+    W = _stack_cols(w, t, q)
+    z = np.zeros(p * q ** 3)
+    _check(C.LIB.octen_compress_coo(p, q, I, J, t, _dptr(U), _dptr(V), _dptr(W), batch.nnz, batch.i.ctypes.data,
+                                    batch.j.ctypes.data, batch.k.ctypes.data, batch.values.ctypes.data, _dptr(z)))
+    return [z[r * q ** 3:(r + 1) * q ** 3].reshape((q, q, q), order="F") for r in range(p)]

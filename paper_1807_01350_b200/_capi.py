@@ -86,6 +86,19 @@ SIGNATURES = {
                                                            P_dbl, P_dbl, P_dbl, P_dbl, P_dbl, P_dbl]),
     "octen_recover_temporal_append": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i64, P_dbl, P_dbl,
                                                      P_dbl, P_dbl, P_dbl]),
+    "octen_coo_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_i64, c_i64, P_dbl, P_dbl, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_void_p)]),
+    "octen_coo_compress": (ctypes.c_int, [ctypes.c_void_p, c_i64, ctypes.c_void_p, c_i64, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "octen_coo_get_summaries": (ctypes.c_int, [ctypes.c_void_p, P_dbl]),
+    "octen_coo_reset": (ctypes.c_int, [ctypes.c_void_p]),
+    "octen_coo_cp_als": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(AlsConfigC), P_u64, P_dbl, P_dbl, P_dbl,
+                                        P_i32]),
+    "octen_coo_stage_times": (ctypes.c_int, [ctypes.c_void_p, P_dbl]),
+    "octen_coo_cuda_stream": (ctypes.c_void_p, [ctypes.c_void_p]),
+    "octen_coo_destroy": (None, [ctypes.c_void_p]),
+    "octen_compress_coo": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_i64, c_i64, c_i64, P_dbl, P_dbl, P_dbl, c_i64,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, P_dbl]),
 }
 
 

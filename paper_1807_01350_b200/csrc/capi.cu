@@ -16,6 +16,25 @@ struct octen_stream {
     std::unique_ptr<octen::Stream> s;
 };
 
+struct octen_coo_summaries {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[2] = {};
+    octen::CooEngine eng;
+    octen::AlsEngine als;
+    octen::DevBuf<double> Y, W;
+    octen::DevBuf<int> hi, hj, hk;
+    octen::DevBuf<float> hv;
+    double als_ms = 0;
+    long long als_runs = 0;
+    ~octen_coo_summaries() {
+        if (st) cudaStreamSynchronize(st);
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
 namespace {
 
 thread_local std::string g_err;
@@ -389,6 +408,125 @@ int octen_recover_temporal_append(int p, int q, int rank, int64_t t, const doubl
         std::vector<double> h2 = dH.to_host(stk.size(), ss.st);
         hist_to_blocks(h2, p, q, rank, history);
     });
+}
+
+
+int octen_coo_create(int p, int q, int64_t I, int64_t J, const double* u, const double* v, int device,
+                     octen_coo_summaries** out) {
+    return guard([&] {
+        *out = nullptr;
+        if (p < 1 || q < 1 || I < 1 || J < 1) throw octen::ConfigError("octen_coo_create: bad shape");
+        OCTEN_CUDA(cudaSetDevice(device));
+        auto h = std::make_unique<octen_coo_summaries>();
+        h->device = device;
+        OCTEN_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+        for (auto& e : h->ev) OCTEN_CUDA(cudaEventCreate(&e));
+        h->eng.set_projections(p, q, I, J, u, v, h->st);
+        const size_t n = (size_t)p * q * q * q;
+        h->Y.reserve(n);
+        h->Y.zero(n, h->st);
+        OCTEN_CUDA(cudaStreamSynchronize(h->st));
+        *out = h.release();
+    });
+}
+
+int octen_coo_compress(octen_coo_summaries* h, int64_t t, const double* w, int64_t nnz, const int32_t* i,
+                       const int32_t* j, const int32_t* k, const float* values, int location) {
+    return guard([&] {
+        check_dtype(OCTEN_F32, location);
+        OCTEN_CUDA(cudaSetDevice(h->device));
+        auto& e = h->eng;
+        if (t < 1) throw octen::ConfigError("compress: temporal extent must be >= 1");
+        const double* dW = w;
+        const int *di = i, *dj = j, *dk = k;
+        const float* dv = values;
+        if (location == OCTEN_HOST) {
+            h->W.upload(w, (size_t)e.P * t * e.Q, h->st);
+            dW = h->W.p;
+            if (nnz > 0) {
+                h->hi.upload(i, (size_t)nnz, h->st);
+                h->hj.upload(j, (size_t)nnz, h->st);
+                h->hk.upload(k, (size_t)nnz, h->st);
+                h->hv.upload(values, (size_t)nnz, h->st);
+                di = h->hi.p, dj = h->hj.p, dk = h->hk.p, dv = h->hv.p;
+            }
+        }
+        e.compress(t, nnz, di, dj, dk, dv, dW, h->Y.p, h->st);
+        e.collect(h->st);
+    });
+}
+
+int octen_coo_get_summaries(const octen_coo_summaries* h, double* y) {
+    return guard([&] {
+        OCTEN_CUDA(cudaSetDevice(h->device));
+        const auto& e = h->eng;
+        h->Y.download(y, (size_t)e.P * e.Q * e.Q * e.Q, h->st);
+        OCTEN_CUDA(cudaStreamSynchronize(h->st));
+    });
+}
+
+int octen_coo_reset(octen_coo_summaries* h) {
+    return guard([&] {
+        OCTEN_CUDA(cudaSetDevice(h->device));
+        const auto& e = h->eng;
+        h->Y.zero((size_t)e.P * e.Q * e.Q * e.Q, h->st);
+        OCTEN_CUDA(cudaStreamSynchronize(h->st));
+    });
+}
+
+int octen_coo_cp_als(octen_coo_summaries* h, const octen_als_config* cfg, const uint64_t* seeds, double* factors,
+                     double* lambda, double* fit, int32_t* iterations) {
+    return guard([&] {
+        OCTEN_CUDA(cudaSetDevice(h->device));
+        const int p = h->eng.P, q = h->eng.Q;
+        std::vector<std::uint64_t> sd(seeds, seeds + p);
+        OCTEN_CUDA(cudaEventRecord(h->ev[0], h->st));
+        h->als.run(p, cfg->n_restarts, q, cfg->rank, cfg->max_iters, cfg->rel_tol, h->Y.p, sd, h->st);
+        OCTEN_CUDA(cudaEventRecord(h->ev[1], h->st));
+        if (factors) h->als.Mf.download(factors, (size_t)p * 3 * q * cfg->rank, h->st);
+        if (lambda) h->als.Mlam.download(lambda, (size_t)p * cfg->rank, h->st);
+        OCTEN_CUDA(cudaStreamSynchronize(h->st));
+        float ms = 0.f;
+        OCTEN_CUDA(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+        h->als_ms += ms;
+        ++h->als_runs;
+        for (int r = 0; r < p; ++r) {
+            if (fit) fit[r] = h->als.results[r].fit;
+            if (iterations) iterations[r] = h->als.results[r].iterations;
+        }
+    });
+}
+
+int octen_coo_stage_times(const octen_coo_summaries* h, double* out) {
+    return guard([&] {
+        const auto& e = h->eng;
+        out[0] = e.ms_prep;
+        out[1] = e.ms_slice;
+        out[2] = e.ms_accum;
+        out[3] = e.groups_total;
+        out[4] = e.nnz_total;
+        out[5] = (double)e.batches;
+        out[6] = h->als_ms;
+        out[7] = (double)h->als_runs;
+    });
+}
+
+void* octen_coo_cuda_stream(const octen_coo_summaries* h) { return h ? (void*)h->st : nullptr; }
+
+void octen_coo_destroy(octen_coo_summaries* h) { delete h; }
+
+int octen_compress_coo(int p, int q, int64_t I, int64_t J, int64_t t, const double* u, const double* v,
+                       const double* w, int64_t nnz, const int32_t* i, const int32_t* j, const int32_t* k,
+                       const float* values, double* z) {
+    octen_coo_summaries* h = nullptr;
+    int rc = octen_coo_create(p, q, I, J, u, v, 0, &h);
+    if (rc != OCTEN_OK) return rc;
+    rc = octen_coo_compress(h, t, w, nnz, i, j, k, values, OCTEN_HOST);
+    if (rc == OCTEN_OK) rc = octen_coo_get_summaries(h, z);
+    std::string msg = g_err;
+    octen_coo_destroy(h);
+    g_err = msg;
+    return rc;
 }
 
 }  // extern "C"

@@ -177,6 +177,11 @@ void run_accumulate(CompressEngine& e, std::int64_t t, const T* Z2, const double
 
 }  // namespace
 
+void accumulate_z2_f32(int P, int Q, std::int64_t t, const float* Z2, const double* dW, double* dY, cudaStream_t st) {
+    gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<float>{Z2, (int)t, Q}, G3B{dW, t, 0, Q}, G3C{dY, Q}, st);
+    OCTEN_CUDA(cudaGetLastError());
+}
+
 cudaEvent_t CompressEngine::event(int i) {
     while ((int)g1_events.size() <= i) {
         cudaEvent_t ev;

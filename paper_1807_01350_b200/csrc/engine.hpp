@@ -131,6 +131,51 @@ public:
     ~CompressEngine();
 };
 
+// Y_p += Z2_p (Q^2 x t) W_p (t x Q) for every replica (fp64 DMMA), Z2 fp32
+// P x Q^2 x t (the mode-1/2 output layout of the dense path).
+void accumulate_z2_f32(int P, int Q, std::int64_t t, const float* Z2, const double* dW, double* dY, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Stage 1, sparse input: compression of one COO temporal batch
+// (SparseTensor, tensor.hpp:66-90, validated as tensor.cpp:87-102) into the
+// P summaries without densifying it (coo.cu).
+// ---------------------------------------------------------------------------
+struct CooStatus {
+    int bounds, nonfinite, dup, pad;  // first offending entry (input order), INT_MAX if none
+    unsigned long long groups;        // distinct (k, i) pairs of the batch
+};
+
+class CooEngine {
+public:
+    CooEngine();
+    ~CooEngine();
+    // Projections (host, column-major per replica: U_p I x Q, V_p J x Q).
+    void set_projections(int P, int Q, std::int64_t I, std::int64_t J, const double* hU, const double* hV,
+                         cudaStream_t st);
+    // Validate a COO batch (device arrays i, j, k int32 with k < t, values
+    // fp32) and accumulate its compression with temporal rows W (P x t x Q,
+    // device) into Y (P x Q^3, device).  Throws the reference's SparseTensor
+    // errors before Y changes.
+    void compress(std::int64_t t, std::int64_t nnz, const int* di, const int* dj, const int* dk, const float* dv,
+                  const double* dW, double* dY, cudaStream_t st);
+    // Fold the last compress's event times into the counters (synchronizes).
+    void collect(cudaStream_t st);
+
+    int P = 0, Q = 0, QP = 0, ldp = 0;
+    std::int64_t I = 0, J = 0;
+    DevBuf<float> U32, V32;  // I x (P QP), J x (P QP) row-major, zero-padded
+    DevBuf<unsigned long long> keys, keys2;
+    DevBuf<int> idx, idx2, off;
+    DevBuf<int4> ent;
+    DevBuf<char> sort_tmp;
+    DevBuf<CooStatus> err;
+    DevBuf<float> Z2;
+    cudaEvent_t evs[4] = {};
+    bool pending = false;
+    double ms_prep = 0, ms_slice = 0, ms_accum = 0, groups_total = 0, nnz_total = 0;
+    long long batches = 0;
+};
+
 // ---------------------------------------------------------------------------
 // Stage 3: alignment and merge (recovery.cpp / streaming.cpp:89-177).
 // ---------------------------------------------------------------------------
