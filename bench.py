@@ -36,6 +36,7 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     # name: I, J, K0, t, Q, P, R, shared, als_iters
     "c3": dict(I=1000, J=1000, K0=1000, t=100, Q=100, P=16, R=20, shared=10, iters=30, restarts=3),
+    "c5": dict(I=2000, J=2000, K0=200, t=200, Q=128, P=32, R=32, shared=32, iters=30, restarts=3),
     "c2": dict(I=500, J=500, K0=500, t=50, Q=50, P=8, R=10, shared=12, iters=30, restarts=3),
     "small": dict(I=200, J=200, K0=100, t=20, Q=20, P=16, R=5, shared=5, iters=30, restarts=3),
 }
@@ -122,7 +123,7 @@ class Synth:
     RMS (BASELINE.json c3), generated on the device in fp64 and rounded to
     fp32; batches are Fortran-ordered (I, J, t) views of (t, J, I) storage."""
 
-    def __init__(self, torch, dev, I, J, K, R, seed):
+    def __init__(self, torch, dev, I, J, K, R, seed, noise=0.01):
         self.torch = torch
         self.dev = dev
         g = torch.Generator(device=dev)
@@ -132,7 +133,7 @@ class Synth:
         self.B = torch.rand((J, R), generator=g, device=dev, dtype=torch.float64)
         self.C = torch.rand((K, R), generator=g, device=dev, dtype=torch.float64)
         clean = torch.einsum("kr,jr,ir->kji", self.C[:10], self.B, self.A)
-        self.sigma = 0.01 * float(clean.pow(2).mean().sqrt())
+        self.sigma = noise * float(clean.pow(2).mean().sqrt())
         del clean
 
     def batch(self, k0, t, out=None):
@@ -336,7 +337,8 @@ def run_sparse(args, torch, dev, ob, steps, warmup, with_cpu):
                         "peak": fp32_peak, "unit": "TFLOP/s",
                         "frac": flops / (slice_ms * 1e-3) / 1e12 / fp32_peak if slice_ms else 0.0,
                         "peak_source": "nominal FP32 FFMA: 148 SMs x 128 lanes x 2 x 1.965 GHz (not measured)",
-                        "flops_per_launch": flops, "traffic": None},
+                        "flops_per_launch": flops, "traffic": c4_traffic(),
+                        "traffic_unit": "bytes/launch (ncu dram__bytes_read+write, profiles/r1_c4_roofline.json)"},
            "gpu_launches": int(launches), "setup_s": t_setup}
     # e2e: host COO arrays + host temporal rows through the public API, model read back
     if args.e2e_steps > 0:
@@ -361,6 +363,14 @@ def run_sparse(args, torch, dev, ob, steps, warmup, with_cpu):
     if with_cpu:
         out["cpu_baseline"] = cpu_sample_sparse(batches[0], ws[0], u, v, P, R, c)
     return out
+
+
+def c4_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_c4_roofline.json")) as f:
+            return json.load(f)["traffic_bytes_per_launch"]
+    except Exception:
+        return None
 
 
 def cpu_sample_sparse(batch, w, u, v, P, R, c, sample=50_000):
@@ -396,6 +406,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="octen", choices=["octen", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + ["c4"])
+    ap.add_argument("--noise", type=float, default=0.01, help="Gaussian noise sigma relative to the clean RMS")
     ap.add_argument("--no-sparse", action="store_true", help="skip the c4 sparse leg of the default line")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -440,7 +451,7 @@ def main():
     # sharded: every rank sees the same batches and seeds (one stream);
     # replicas: independent streams with per-rank data
     dseed = 1234 if sharded else 1234 + rank
-    syn = Synth(torch, dev, I, J, K0 + nb * t, R, seed=dseed)
+    syn = Synth(torch, dev, I, J, K0 + nb * t, R, seed=dseed, noise=args.noise)
     first = syn.batch(0, K0)
     scfg = ob.StreamConfig(rank=R, p=P, q=Q, shared=sh, seed=7 * dseed + 3,
                            als=ob.AlsConfig(max_iters=cfg["iters"], rel_tol=1e-8, n_restarts=cfg["restarts"]),
@@ -564,7 +575,7 @@ def main():
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
                 "dtype": "f32 compress (split-TF32/FP32) + f64 CP-ALS/merge", "data": "synthetic",
-                "config": {"workload": args.config, **cfg, "l2": "inputs larger than L2 (400 MB fp32 batch)",
+                "config": {"workload": args.config, **cfg, "noise": args.noise, "l2": "inputs larger than L2 (%d MB fp32 batch)" % (I * J * t * 4 // 10**6),
                            "parallelism": ("replica-sharded x%d (NCCL all-gather of replica models)" % world
                                            if sharded else ("independent streams x%d" % world if world > 1
                                                             else "single"))},
