@@ -312,21 +312,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // or columns past the tensors are TMA zero-filled; A columns past slice k
 // meet zero B rows (j >= J), so they contribute nothing.
 // ---------------------------------------------------------------------------
-constexpr int M2_BN = 112;
+// N tile (columns b of V_p): 112 covers Q <= 112 (c3: Q = 100), 128 covers
+// Q <= 128 (c5); the stage size follows it
+constexpr int M2_BN_MAX = 128;
 constexpr int M2_STAGES = 3;
 constexpr int M2_A_BYTES = BM * BKB;                      // 16 KB
-constexpr int M2_B_BYTES = M2_BN * BKB;                   // 14 KB
-constexpr int M2_STAGE_BYTES = 2 * M2_A_BYTES + 2 * M2_B_BYTES;
+template <int BN2>
+constexpr int m2_b_bytes() { return BN2 * BKB; }          // 14 / 16 KB
+template <int BN2>
+constexpr int m2_stage_bytes() { return 2 * M2_A_BYTES + 2 * m2_b_bytes<BN2>(); }
 constexpr uint32_t M2_TMEM_COLS = 128;
 
+template <int BN2>
 constexpr uint32_t make_idesc_m2() {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(M2_BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN2 >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
+template <int BN2>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_mode2_tf32x3_kernel(const __grid_constant__ CUtensorMap map_z1, const __grid_constant__ CUtensorMap map_vhi,
                            const __grid_constant__ CUtensorMap map_vlo, float* __restrict__ Z2, int Q, int J, int tc,
                            long long zstride) {
+    constexpr int M2_BN = BN2;
+    constexpr int M2_B_BYTES = m2_b_bytes<BN2>();
+    constexpr int M2_STAGE_BYTES = m2_stage_bytes<BN2>();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full_bar = (uint64_t*)(smem + M2_STAGES * M2_STAGE_BYTES);
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc_m2();
+            constexpr uint32_t idesc = make_idesc_m2<BN2>();
             for (int kb = 0; kb < num_kb; ++kb) {
                 const int s = kb % M2_STAGES;
                 const uint32_t ph = (kb / M2_STAGES) & 1;
@@ -545,21 +554,28 @@ bool tc_mode2_tf32x3(const float* Z1, long long N1, int J, int tc, const float* 
     if (!tc_gemm_available()) return false;
     // the A box of slice k starts at column k J: TMA needs that inner
     // coordinate on a 16-byte boundary, hence J % 4 == 0
-    if (Q > M2_BN || Q < 1 || (J % 4) != 0 || (N1 % 4) != 0 || (ldv % 4) != 0 || ((uintptr_t)Z1 % 16) != 0 ||
+    if (Q > M2_BN_MAX || Q < 1 || (J % 4) != 0 || (N1 % 4) != 0 || (ldv % 4) != 0 || ((uintptr_t)Z1 % 16) != 0 ||
         ((uintptr_t)Vhi % 16) != 0 || ((uintptr_t)Vlo % 16) != 0 || (long long)P * tc > 2147483647LL)
         return false;
+    const int bn2 = Q <= 112 ? 112 : 128;
     CUtensorMap mz, mh, ml;
     if (!make_map(&mz, Z1, (uint64_t)N1, (uint64_t)P * Q, (uint64_t)N1 * 4, BK, BM)) return false;
     // inner extent ldv (zero-padded past J, a whole number of 16-byte units)
-    if (!make_map(&mh, Vhi, (uint64_t)ldv, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, M2_BN)) return false;
-    if (!make_map(&ml, Vlo, (uint64_t)ldv, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, M2_BN)) return false;
-    const size_t smem = M2_STAGES * M2_STAGE_BYTES + 1024 + 256;
-    static bool attr = false;
-    if (!attr) {
-        OCTEN_CUDA(cudaFuncSetAttribute(tc_mode2_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
-    tc_mode2_tf32x3_kernel<<<P * tc, NUM_THREADS, smem, st>>>(mz, mh, ml, Z2, Q, J, tc, zstride);
+    if (!make_map(&mh, Vhi, (uint64_t)ldv, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, bn2)) return false;
+    if (!make_map(&ml, Vlo, (uint64_t)ldv, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, bn2)) return false;
+    auto launch = [&](auto kern, size_t stage_bytes, bool& attr) {
+        const size_t smem = M2_STAGES * stage_bytes + 1024 + 256;
+        if (!attr) {
+            OCTEN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        kern<<<P * tc, NUM_THREADS, smem, st>>>(mz, mh, ml, Z2, Q, J, tc, zstride);
+    };
+    static bool attr112 = false, attr128 = false;
+    if (bn2 == 112)
+        launch(tc_mode2_tf32x3_kernel<112>, (size_t)m2_stage_bytes<112>(), attr112);
+    else
+        launch(tc_mode2_tf32x3_kernel<128>, (size_t)m2_stage_bytes<128>(), attr128);
     OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     return true;

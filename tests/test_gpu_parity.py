@@ -73,7 +73,8 @@ def test_compress_f32_within_tolerance(ob):
         assert rel(got[r], want) < 1e-5  # fp32 inputs: BASELINE tolerance is 1e-4
 
 
-@pytest.mark.parametrize("shape", [(200, 300, 12, 40, 5, 4), (1000, 64, 9, 100, 4, 10), (96, 50, 7, 30, 9, 6)])
+@pytest.mark.parametrize("shape", [(200, 300, 12, 40, 5, 4), (1000, 64, 9, 100, 4, 10), (96, 50, 7, 30, 9, 6),
+                                   (300, 200, 6, 128, 3, 32), (160, 128, 5, 120, 2, 8)])
 def test_compress_f32_tcgen05_vs_simt_and_oracle(ob, shape, monkeypatch):
     # the tcgen05 split-TF32 mode-1 kernel (M/N/K tails: several tiles, K not a
     # multiple of 32) against the fp64 oracle and the SIMT fp32 path
