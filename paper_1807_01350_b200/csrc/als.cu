@@ -23,6 +23,7 @@
 #include <stdexcept>
 
 #include "engine.hpp"
+#include "evprof.hpp"
 #include "gemm_dmma.cuh"
 #include "rng_host.hpp"
 #include "small_linalg.cuh"
@@ -1166,6 +1167,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     host_syncs = 0;
 
     // ---- norms, zero-tensor check (cp_als.cpp:255-256)
+    OCTEN_PROF("begin", st);
     ws.reserve((size_t)P * 64);
     als_norm_kernel<<<dim3(64, P), 256, 0, st>>>(d, ws.p); OCTEN_LAUNCHED(1);
     als_norm_finish_kernel<<<(P + 127) / 128, 128, 0, st>>>(d, ws.p, 64); OCTEN_LAUNCHED(1);
@@ -1225,8 +1227,10 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         const int mblk = std::min(Q, R + 4);
         const int use_sub = (Q >= 2 * mblk && (size_t)2 * Q * mblk + 2 * mblk * mblk + mblk <= q2) ? mblk : 0;
         OCTEN_CUDA(cudaFuncSetAttribute(gevd_eig_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eig));
+        OCTEN_PROF("grams", st);
         gevd_eig_sym_kernel<<<P * 2, 256, smem_eig, st>>>(d, v_in_smem, use_sub); OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
+        OCTEN_PROF("eig", st);
         // mixtures -> p1/p2 for all attempts
         if (S <= 4) {
             const size_t smem_mix = (size_t)S * 6 * Q * sizeof(double);
@@ -1255,8 +1259,10 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             todo.upload(td.data(), NP, st);
             peel_fail.zero(NP, st);
             const size_t smem_pen = (size_t)(5 * R * R + 7 * R + 72) * sizeof(double);
+            OCTEN_PROF("mix", st);
             gevd_pencil_kernel<<<NP, 128, smem_pen, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
+            OCTEN_PROF("pencil", st);
             // h = a1^T Y_(0) for all restarts of a replica at once:
             // H^T (Q^2 x S R) = Y_(0)^T [a1_s...]
             if (gpipe)
@@ -1274,8 +1280,10 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             const int peel_threads = 128;
             const size_t smem_peel = (q2 + 2 * Q + peel_threads + 2 + Q) * sizeof(double);
             OCTEN_CUDA(cudaFuncSetAttribute(gevd_peel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_peel));
+            OCTEN_PROF("hsolve", st);
             gevd_peel_kernel<<<NP * R, peel_threads, smem_peel, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
+            OCTEN_PROF("peel", st);
             std::vector<int> au = att_used.to_host(NP, st);
             std::vector<int> pf = peel_fail.to_host(NP, st);
             ++host_syncs;
@@ -1313,6 +1321,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     }
     als_init_state_kernel<<<NP, 128, 0, st>>>(d); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
+    OCTEN_PROF("init", st);
 
     // ---- sweeps
     const int SR = S * R;
@@ -1603,9 +1612,12 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             throw NumericError(als_failure_message(3, e.a, 0));
         }
     }
+    OCTEN_PROF("sweeps", st);
     DevBuf<int> best;
     best.reserve(P);
     als_select_kernel<<<P, 256, 0, st>>>(d, Mf.p, Mlam.p, best.p); OCTEN_LAUNCHED(1);
+    OCTEN_PROF("select", st);
+    EvProf::get().report("als");
     OCTEN_CUDA(cudaGetLastError());
     std::vector<int> hb = best.to_host(P, st);
     std::vector<double> fh = fit_hist.to_host((size_t)NP * max_iters, st);

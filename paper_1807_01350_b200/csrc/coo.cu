@@ -99,7 +99,8 @@ __global__ void coo_scan_kernel(const unsigned long long* __restrict__ keys, con
 // entries are consumed in rounds of <= kChunkE entries / kChunkG groups:
 //   phase A' Us[g][c] = U(i_g, c)            (cp.async, overlapping phase A)
 //   phase A  Rs[g][c] = sum_{e in g} v_e V(j_e, c)   (float4 gathers; NS thread
-//            sets each take a contiguous share of the round's entries)
+//            sets each take the whole groups of a contiguous share of the
+//            round's entries: one writer per group, fixed summation order)
 //   phase B  acc += Us[g][rows]^T Rs[g][cols] over the round's groups
 // A group split across two rounds is simply two groups (the sum is linear).
 template <int QP, int TM>
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(256) coo_slice_kernel(const int4* __restrict__
     extern __shared__ __align__(16) float sm[];
     float* Rs = sm;                     // [kChunkG][NC]
     float* Us = sm + kChunkG * NC;      // [kChunkG][NC]
-    __shared__ int s_j[kChunkE], s_g[kChunkE], s_gi[kChunkG];
+    __shared__ int s_j[kChunkE], s_g[kChunkE], s_gi[kChunkG], s_gs[kChunkG];
     __shared__ float s_v[kChunkE];
     __shared__ int s_wsum[8], s_nused;
 
@@ -141,8 +142,6 @@ __global__ void __launch_bounds__(256) coo_slice_kernel(const int4* __restrict__
         const int n = (int)(end - pos < kChunkE ? end - pos : kChunkE);
         int head = 0, ei = 0;
         if (tid == 0) s_nused = n;
-        for (int x = tid; x < kChunkG * NQ; x += 256)
-            reinterpret_cast<float4*>(Rs)[x] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (tid < n) {
             const int4 en = ent[pos + tid];
             ei = en.x;
@@ -164,7 +163,10 @@ __global__ void __launch_bounds__(256) coo_slice_kernel(const int4* __restrict__
         const int gid = base + incl - 1;
         if (tid < n) {
             s_g[tid] = gid;
-            if (head && gid < kChunkG) s_gi[gid] = ei;
+            if (head && gid < kChunkG) {
+                s_gi[gid] = ei;
+                s_gs[gid] = tid;
+            }
             if (head && gid == kChunkG) s_nused = tid;
         }
         __syncthreads();
@@ -182,27 +184,26 @@ __global__ void __launch_bounds__(256) coo_slice_kernel(const int4* __restrict__
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         // phase A: thread set s accumulates the V rows (float4 column quad cq)
-        // of entries [nused s / NS, nused (s+1) / NS); a group's partial sum
-        // goes to Rs by shared atomic add (groups at range ends are shared)
+        // of the whole groups that start in [nused s / NS, nused (s+1) / NS)
+        // (range ends snapped to group heads): every group has one owner, so
+        // the sums are plain stores in a fixed order (run-to-run
+        // deterministic)
         if (4 * cq < cols_valid) {
+            auto snap = [&](int x) {  // first group head >= x, else nused
+                int lo = 0, hi = ng;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_gs[mid] < x) lo = mid + 1; else hi = mid;
+                }
+                return lo < ng ? s_gs[lo] : nused;
+            };
             const float* vc = V + colbase + 4 * cq;
-            const int e_lo = nused * sset / NS, e_hi = nused * (sset + 1) / NS;
+            const int e_lo = sset == 0 ? 0 : snap(nused * sset / NS);
+            const int e_hi = sset == NS - 1 ? nused : snap(nused * (sset + 1) / NS);
             float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
             int gc = e_lo < e_hi ? s_g[e_lo] : 0;
-            // only the groups at the ends of the range can be shared with a
-            // neighbouring set: those are added atomically, the rest stored
-            const int g_first = (e_lo > 0 && e_lo < e_hi && s_g[e_lo - 1] == gc) ? gc : -1;
-            const int g_last = (e_hi < nused && e_lo < e_hi && s_g[e_hi] == s_g[e_hi - 1]) ? s_g[e_hi - 1] : -1;
             auto flush = [&](int g) {
-                float* r = Rs + gc * NC + 4 * cq;
-                if (gc == g_first || gc == g_last) {
-                    atomicAdd(r, a.x);
-                    atomicAdd(r + 1, a.y);
-                    atomicAdd(r + 2, a.z);
-                    atomicAdd(r + 3, a.w);
-                } else {
-                    *reinterpret_cast<float4*>(r) = a;
-                }
+                *reinterpret_cast<float4*>(Rs + gc * NC + 4 * cq) = a;
                 a = make_float4(0.f, 0.f, 0.f, 0.f);
                 gc = g;
             };

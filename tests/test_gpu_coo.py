@@ -98,6 +98,9 @@ def test_coo_heavy_slice_and_rows_span_many_rounds(ob):
     z = ob.compress_coo(ob.SparseTensor(shape, idx, vals), u, v, w)
     for a, b in zip(z, oracle_z(shape, idx, vals, u, v, w)):
         assert rel(a, b) < TOL
+    # run-to-run determinism (no unordered atomics)
+    z2 = ob.compress_coo(ob.SparseTensor(shape, idx, vals), u, v, w)
+    assert all(np.array_equal(a, b) for a, b in zip(z, z2))
 
 
 def test_coo_empty_batch_and_empty_slices(ob):
