@@ -95,6 +95,16 @@ int octen_stream_init(const octen_stream_config* cfg, const void* data, int dtyp
 int octen_stream_ingest(octen_stream* s, const void* data, int dtype, int location, int order,
                         const int64_t* dims);
 
+/* Start the host->device copy of a LATER batch (host memory; pinned for
+ * the copy to overlap) on a copy stream of the handle, so it runs while the
+ * device works on the batches before it.  The next octen_stream_ingest /
+ * octen_stream_begin whose data pointer, dtype and dims match the oldest
+ * pending prefetch consumes the copy instead of transferring the batch again.
+ * At most two prefetches may be pending; the host buffer must stay unchanged
+ * until its batch is ingested.  (An extension: the reference's ingest_batch
+ * is synchronous and has no prefetch, streaming.hpp:70.) */
+int octen_stream_prefetch(octen_stream* s, const void* data, int dtype, int order, const int64_t* dims);
+
 void octen_stream_destroy(octen_stream* s);
 
 /* Stream state accessors (StreamState, streaming.hpp:48-59).

@@ -230,6 +230,20 @@ class StreamState:
         hs = [h[i * q * rank:(i + 1) * q * rank].reshape((q, rank), order="F") for i in range(p)]
         return ys, hs
 
+    def prefetch(self, batch) -> None:
+        """Start the host->device copy of a later batch (host array; pin it,
+        e.g. a pinned torch CPU tensor, for the copy to overlap the device work
+        of the batches before it).  The next ingest of the same array consumes
+        the copy.  At most two may be pending; the array must not change until
+        it is ingested (octen_stream_prefetch)."""
+        keep, ptr, dt, loc, dims = _batch_args(batch)
+        if loc != C.OCTEN_HOST:
+            raise ConfigError("octen: prefetch takes a host batch")
+        d = (C.c_i64 * len(dims))(*dims)
+        _check(C.LIB.octen_stream_prefetch(self._h, ptr, dt, len(dims), d))
+        ka = getattr(self, "_pf_keep", [])
+        self._pf_keep = (ka + [keep])[-3:]  # the copies read these buffers until ingested
+
     def replica_models(self) -> List[KruskalModel]:
         info = self._info()
         rank, p, q = info[4], info[5], info[6]

@@ -60,6 +60,7 @@ SIGNATURES = {
     "octen_stream_ingest": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, P_i64]),
     "octen_stream_destroy": (None, [ctypes.c_void_p]),
+    "octen_stream_prefetch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, P_i64]),
     "octen_stream_create": (ctypes.c_int, [ctypes.POINTER(StreamConfigC), ctypes.c_int, ctypes.c_int,
                                            ctypes.POINTER(ctypes.c_void_p)]),
     "octen_stream_exchange_sizes": (ctypes.c_int, [ctypes.c_void_p, P_i64]),

@@ -159,6 +159,15 @@ int octen_stream_ingest(octen_stream* s, const void* data, int dtype, int locati
     });
 }
 
+int octen_stream_prefetch(octen_stream* s, const void* data, int dtype, int order, const int64_t* dims) {
+    return guard([&] {
+        if (!s || !data || !dims) throw octen::ConfigError("octen_stream_prefetch: null argument");
+        check_dtype(dtype, OCTEN_HOST);
+        OCTEN_CUDA(cudaSetDevice(s->s->cfg.device));
+        s->s->prefetch(data, dtype, order, dims);
+    });
+}
+
 void octen_stream_destroy(octen_stream* s) { delete s; }
 
 int octen_stream_create(const octen_stream_config* cfg, int shard_rank, int shard_world, octen_stream** out) {

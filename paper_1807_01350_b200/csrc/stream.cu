@@ -8,6 +8,8 @@
 // device.
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include <chrono>
 #include <cmath>
 #include <memory>
@@ -115,6 +117,16 @@ Stream::~Stream() {
         cudaStreamDestroy(cp);
     }
     for (cudaEvent_t e : copy_ev) cudaEventDestroy(e);
+    if (pcp) {
+        cudaStreamSynchronize(pcp);
+        cudaStreamDestroy(pcp);
+    }
+    for (auto& v : pf_ev)
+        for (cudaEvent_t e : v) cudaEventDestroy(e);
+    for (cudaEvent_t e : slot_free)
+        if (e) cudaEventDestroy(e);
+    if (pin_ev) cudaEventDestroy(pin_ev);
+    if (pin_buf) cudaFreeHost(pin_buf);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     for (auto& e : evs)
@@ -185,8 +197,41 @@ void Stream::extend_temporal(std::int64_t t_new) {
             s2.fill_uniform(w + (size_t)t_new * sh, t_new, Q - sh, t_new);
         }
     }
-    dW.upload(hW.data(), hW.size(), st);
+    upload_mapped(dW, hW.data(), hW.size());
     ++batches_drawn;
+}
+
+namespace {
+__global__ void pull_f64_kernel(double* __restrict__ dst, const double* __restrict__ src, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+}  // namespace
+
+// Host -> device copy of a small per-batch array through a pinned, mapped
+// staging buffer read by a kernel: it bypasses the copy engines, so it is
+// not queued behind a prefetch of the next batch (octen_stream_prefetch).
+void Stream::upload_mapped(DevBuf<double>& dst, const double* h, size_t n) {
+    if (n > pin_cap) {
+        if (pin_buf) {
+            OCTEN_CUDA(cudaStreamSynchronize(st));
+            OCTEN_CUDA(cudaFreeHost(pin_buf));
+        }
+        OCTEN_CUDA(cudaHostAlloc((void**)&pin_buf, n * sizeof(double), cudaHostAllocMapped));
+        pin_cap = n;
+        if (!pin_ev) OCTEN_CUDA(cudaEventCreateWithFlags(&pin_ev, cudaEventDisableTiming));
+    } else if (pin_ev) {
+        OCTEN_CUDA(cudaEventSynchronize(pin_ev));  // the previous pull has read the staging buffer
+    }
+    std::memcpy(pin_buf, h, n * sizeof(double));
+    double* src = nullptr;
+    OCTEN_CUDA(cudaHostGetDevicePointer((void**)&src, pin_buf, 0));
+    dst.reserve(n);
+    const int blocks = (int)std::min<size_t>(148, (n + 255) / 256);
+    pull_f64_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(dst.p, src, n);
+    OCTEN_LAUNCHED(1);
+    OCTEN_CUDA(cudaGetLastError());
+    OCTEN_CUDA(cudaEventRecord(pin_ev, st));
 }
 
 const void* Stream::stage_input(const void* data, int dtype, int location, size_t n) {
@@ -271,6 +316,90 @@ void Stream::prepare(int order, const std::int64_t* dims) {
 }
 
 // ---- phase 1: stage, compress and decompose the owned replicas ----
+namespace {
+__global__ void __launch_bounds__(256) h2d_pull_kernel(int4* __restrict__ dst, const int4* __restrict__ src,
+                                                       long long n16) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (; i + 7 * stride < n16; i += 8 * stride) {
+        int4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = src[i + u * stride];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dst[i + u * stride] = v[u];
+    }
+    for (; i < n16; i += stride) dst[i] = src[i];
+}
+}  // namespace
+
+void Stream::prefetch(const void* data, int dtype, int order, const std::int64_t* dims) {
+    if (order != 3 || dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+        throw ConfigError("octen: prefetch needs an order-3 batch with positive extents");
+    if (initialized && (dims[0] != I || dims[1] != J))
+        throw ConfigError("ingest_batch: extent mismatch on mode 1 at batch " + std::to_string(batches_seen));
+    if (pf.size() >= 2) throw ConfigError("octen: two prefetched batches are already pending");
+    if (!pcp) {
+        int lo = 0, hi = 0;
+        OCTEN_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        OCTEN_CUDA(cudaStreamCreateWithPriority(&pcp, cudaStreamNonBlocking, lo));  // lowest priority
+        for (auto& e : slot_free) {
+            OCTEN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            OCTEN_CUDA(cudaEventRecord(e, st));
+        }
+    }
+    Prefetch f;
+    f.host = data;
+    f.dtype = dtype;
+    for (int i = 0; i < 3; ++i) f.dims[i] = dims[i];
+    f.slot = pf.empty() ? 0 : 1 - pf.front().slot;
+    const std::int64_t t = dims[2];
+    const size_t plane = (size_t)dims[0] * dims[1], n = plane * t;
+    const size_t esz = dtype == 1 ? sizeof(float) : sizeof(double);
+    // chunking as in begin(): about five chunks, bounded by the Z1 chunk of
+    // the compression once the stream knows its shapes
+    const std::int64_t cs = initialized ? comp.chunk_slices : t;
+    f.sub = std::max<std::int64_t>(1, std::min<std::int64_t>(cs, std::min<std::int64_t>(t, (t + 4) / 5)));
+    f.nch = (t + f.sub - 1) / f.sub;
+    void* dst = dtype == 1 ? (void*)PX32[f.slot].reserve(n) : (void*)PX64[f.slot].reserve(n);
+    auto& evv = pf_ev[f.slot];
+    while ((std::int64_t)evv.size() < f.nch) {
+        cudaEvent_t e;
+        OCTEN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evv.push_back(e);
+    }
+    // the slot's previous batch must have been read by the compression
+    OCTEN_CUDA(cudaStreamWaitEvent(pcp, slot_free[f.slot], 0));
+    // Pinned (device-mapped) host memory is pulled by a small kernel (8 CTAs,
+    // 8 x 16 B loads in flight per thread: far more than PCIe needs) on the
+    // low-priority copy stream.  The copy engines stay free, so the small H2D
+    // transfers of the batch being processed (ALS/merge parameters) are not
+    // queued behind this batch.  Pageable memory goes through the copy engine.
+    // The pull kernel is for BACKGROUND copies only (another prefetch is
+    // pending, so this batch is not the next one consumed and its copy will
+    // overlap device work); a copy that the next ingest waits for anyway
+    // takes the faster copy engine.
+    cudaPointerAttributes at{};
+    const void* mapped = nullptr;
+    if (!pf.empty() && cudaPointerGetAttributes(&at, data) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+        at.devicePointer)
+        mapped = at.devicePointer;
+    (void)cudaGetLastError();
+    for (std::int64_t c = 0; c < f.nch; ++c) {
+        const std::int64_t k0 = c * f.sub, kc = std::min(f.sub, t - k0);
+        const size_t off = plane * k0 * esz, bytes = plane * kc * esz;
+        if (mapped && (((uintptr_t)mapped + off) % 16) == 0 && (((uintptr_t)dst + off) % 16) == 0 && bytes % 16 == 0) {
+            h2d_pull_kernel<<<8, 256, 0, pcp>>>((int4*)((char*)dst + off), (const int4*)((const char*)mapped + off),
+                                                 (long long)(bytes / 16));
+            OCTEN_LAUNCHED(1);
+        } else {
+            OCTEN_CUDA(cudaMemcpyAsync((char*)dst + off, (const char*)data + off, bytes, cudaMemcpyHostToDevice, pcp));
+        }
+        OCTEN_CUDA(cudaEventRecord(evv[c], pcp));
+    }
+    OCTEN_CUDA(cudaGetLastError());
+    pf.push_back(f);
+}
+
 void Stream::begin(const void* data, int dtype, int location, int order, const std::int64_t* dims,
                    double* models_out) {
     if (pending) throw ConfigError("octen: the previous batch has not finished (begin/merge/finish)");
@@ -308,7 +437,17 @@ void Stream::begin(const void* data, int dtype, int location, int order, const s
             // chunk is scanned for non-finite values before Y is touched
             flag.reserve(1);
             flag.zero(1, st);
-            if (location == 0) {
+            const bool use_pf = location == 0 && !pf.empty() && pf.front().host == data &&
+                                pf.front().dtype == dtype && order == 3 && pf.front().dims[0] == dims[0] &&
+                                pf.front().dims[1] == dims[1] && pf.front().dims[2] == dims[2];
+            if (location == 0 && !use_pf) pf.clear();  // stale prefetches (the caller changed course)
+            if (use_pf) {
+                const Prefetch f = pf.front();
+                pf.erase(pf.begin());
+                const void* dst = dtype == 1 ? (const void*)PX32[f.slot].p : (const void*)PX64[f.slot].p;
+                comp.project(dst, dtype, t, st, pf_ev[f.slot].data(), f.sub, flag.p);
+                OCTEN_CUDA(cudaEventRecord(slot_free[f.slot], st));
+            } else if (location == 0) {
                 const std::int64_t sub = std::max<std::int64_t>(
                     1, std::min<std::int64_t>(comp.chunk_slices, std::min<std::int64_t>(t, (t + 4) / 5)));
                 const std::int64_t nch = (t + sub - 1) / sub;

@@ -55,6 +55,12 @@ public:
     void init(const void* data, int dtype, int location, int order, const std::int64_t* dims);
     void ingest(const void* data, int dtype, int location, int order, const std::int64_t* dims);
     void get_factor(int mode, double* out);
+    // Start the host->device copy of a later batch (host, pinned for overlap)
+    // on a copy stream, so it overlaps the device work of the batches before
+    // it.  A later begin/ingest whose data pointer, dtype and extents match
+    // the oldest pending prefetch consumes it.  At most two prefetches are
+    // pending; the host buffer must not change until the batch is ingested.
+    void prefetch(const void* data, int dtype, int order, const std::int64_t* dims);
 
     void begin(const void* data, int dtype, int location, int order, const std::int64_t* dims, double* models_out);
     void merge_phase(const double* models_all, double* rows_out);
@@ -80,6 +86,21 @@ public:
     DevBuf<double> xmodels, xrows, MfAll, MlamAll, tstackAll;
     DevBuf<float> X32;
     DevBuf<int> flag;
+    struct Prefetch {
+        const void* host = nullptr;
+        int dtype = 0, slot = 0;
+        std::int64_t dims[3] = {0, 0, 0};
+        std::int64_t sub = 1, nch = 0;
+    };
+    std::vector<Prefetch> pf;            // pending, oldest first (<= 2)
+    DevBuf<float> PX32[2];
+    DevBuf<double> PX64[2];
+    std::vector<cudaEvent_t> pf_ev[2];   // per copied chunk
+    cudaEvent_t slot_free[2] = {};       // recorded on st once a slot's batch is read
+    cudaStream_t pcp = nullptr;          // prefetch copy stream
+    double* pin_buf = nullptr;           // pinned, mapped staging of small per-batch uploads
+    size_t pin_cap = 0;
+    cudaEvent_t pin_ev = nullptr;
     std::vector<BatchRecordC> log;
     // cumulative device milliseconds: compress, als, recover, gemm1 (mode-1 contraction)
     double dev_ms[4] = {0, 0, 0, 0};
@@ -99,6 +120,7 @@ private:
     void prepare(int order, const std::int64_t* dims);
     void gen_replicas();
     void extend_temporal(std::int64_t t_new);
+    void upload_mapped(DevBuf<double>& dst, const double* h, size_t n);
     const void* stage_input(const void* data, int dtype, int location, size_t n);
     void check_finite(const void* dX, int dtype, size_t n);
     void ensure_c_capacity(std::int64_t rows);
