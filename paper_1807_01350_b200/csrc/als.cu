@@ -149,8 +149,30 @@ __global__ void __launch_bounds__(256) gevd_eig_sym_kernel(AlsDev d, int v_in_sm
                 atomicAnd(&d.usable[p], (th[0] > 0.0 && th[R - 1] > kEps * Q * th[0]) ? 1 : 0);
             return;
         }
-        // no usable gap at R: full Jacobi below (A is untouched)
+        // no usable gap at R: dense top-R solve below (A is untouched)
         if (threadIdx.x == 0) atomicAdd(&d.eigdbg[0], 1);
+    }
+    {
+        // Householder + bisection + inverse iteration for the top R (the
+        // cyclic Jacobi solver needed ~40x more barriers: 2.5 ms at Q = 64);
+        // V holds [u (Q R) | theta (R) | work (3 Q + 5 Q kb)]
+        const int kb = (int)(((long long)Q * Q - (long long)Q * R - R - 3LL * Q) / (5LL * Q));
+        if (kb >= 1) {
+            double* u = V;
+            double* th = u + (size_t)Q * R;
+            double* work = th + R;
+            const int ok = sym_eig_top_tridiag(team, Q, A, R, u, th, work, kb, cs, cs + (Q + 2));
+            if (ok) {
+                for (int e = threadIdx.x; e < Q * R; e += blockDim.x) ur[e] = u[e];
+                if (threadIdx.x == 0)
+                    atomicAnd(&d.usable[p], (th[0] > 0.0 && th[R - 1] > kEps * Q * th[0]) ? 1 : 0);
+                return;
+            }
+            // (not expected) a vanished vector: restore A and use Jacobi
+            __syncthreads();
+            g2s_copy(A, src, Q * Q);
+            __syncthreads();
+        }
     }
     jacobi_eig_sym(team, Q, A, V, cs, iw);
     __syncthreads();
@@ -1225,7 +1247,13 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         // subspace iteration for the top-R block when the matrix is large
         // enough for it to pay and its scratch fits the V region
         const int mblk = std::min(Q, R + 4);
-        const int use_sub = (Q >= 2 * mblk && (size_t)2 * Q * mblk + 2 * mblk * mblk + mblk <= q2) ? mblk : 0;
+        // Q <= 64: the dense top-R solve (sym_eig_top_tridiag, 0.9 ms at Q = 64)
+        // beats a subspace attempt that may have to give up on a gapless
+        // spectrum first (c4: 1.3 ms); at larger Q subspace iteration wins
+        // when there is a gap (c3 0.59 vs 1.45 ms, c5 1.28 vs 3.3 ms)
+        static const bool force_dense = std::getenv("OCTEN_EIG_DENSE") != nullptr;  // diagnostics
+        const int use_sub =
+            (!force_dense && Q > 64 && Q >= 2 * mblk && (size_t)2 * Q * mblk + 2 * mblk * mblk + mblk <= q2) ? mblk : 0;
         OCTEN_CUDA(cudaFuncSetAttribute(gevd_eig_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eig));
         OCTEN_PROF("grams", st);
         gevd_eig_sym_kernel<<<P * 2, 256, smem_eig, st>>>(d, v_in_smem, use_sub); OCTEN_LAUNCHED(1);

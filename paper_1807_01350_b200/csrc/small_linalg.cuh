@@ -1990,4 +1990,210 @@ OCTEN_HD int subspace_eig_top(const Team& team, int n, const double* a, int k, i
     return 1;
 }
 
+// ---------------------------------------------------------------------------
+// Top-k eigenpairs of a symmetric n x n matrix (column-major, destroyed) by
+// Householder tridiagonalisation, Sturm bisection of the k largest
+// eigenvalues, inverse iteration on the tridiagonal matrix, CGS2 and the
+// back-transformation -- the dense fallback of subspace_eig_top when the
+// spectrum has no gap at k (e.g. summaries of unstructured sparse data),
+// where the cyclic Jacobi solver took ~40x more barriers.  Same role as the
+// BDCSVD thin-U of the unfoldings (cp_als.cpp:96-100): the first k columns of
+// the Gram eigenbasis in descending eigenvalue order.
+//   u      n x k output (eigenvectors), theta k output (descending)
+//   work   3 n + 4 n kb doubles (d, e, Householder norms, inverse-iteration
+//          LU and vectors for batches of kb eigenvectors), kb >= 1
+//   cf, red  CGS2 / reduction scratch (k and team.size() + 2 doubles)
+// Returns 0 if a vector vanishes (not expected for symmetric input).
+// ---------------------------------------------------------------------------
+OCTEN_HD inline int tridiag_count_below(int n, const double* d, const double* e, double x) {
+    // number of eigenvalues of T strictly below x (Sturm count, LDL^T pivots)
+    int cnt = 0;
+    double q = d[0] - x;
+    if (q < 0.0) ++cnt;
+    for (int i = 1; i < n; ++i) {
+        const double qq = (q == 0.0) ? 1e-300 : q;
+        q = d[i] - x - e[i - 1] * e[i - 1] / qq;
+        if (q < 0.0) ++cnt;
+    }
+    return cnt;
+}
+
+template <class Team>
+OCTEN_HD int sym_eig_top_tridiag(const Team& team, int n, double* a, int k, double* u, double* theta,
+                                 double* work, int kb, double* cf, double* red) {
+    double* d = work;
+    double* e = work + n;
+    double* vn = work + 2 * n;
+    double* scr = work + 3 * n;  // 4 n kb
+    const int tid = team.tid(), nt = team.size();
+    // ---- 1. Householder tridiagonalisation (lower): A <- H A H, v stored in
+    //      column kk below the subdiagonal, |v|^2 in vn[kk]
+    for (int kk = 0; kk + 2 < n; ++kk) {
+        double* x = a + (size_t)n * kk + kk + 1;  // length L
+        const int L = n - kk - 1;
+        double loc = 0.0;
+        for (int i = tid; i < L; i += nt) loc += x[i] * x[i];
+        const double xn2 = team_reduce_sum(team, loc, red);
+        const double alpha = x[0];
+        const double tail = xn2 - alpha * alpha;
+        if (!(tail > 1e-300 * (xn2 + 1e-300))) {  // already reduced
+            team.sync();
+            if (tid == 0) {
+                e[kk] = alpha;
+                vn[kk] = 0.0;
+            }
+            team.sync();
+            continue;
+        }
+        const double beta = alpha > 0.0 ? -sqrt(xn2) : sqrt(xn2);
+        const double v0 = alpha - beta;
+        const double vv = tail + v0 * v0, c = 2.0 / vv;
+        double* B = a + (size_t)n * (kk + 1) + kk + 1;  // L x L, ld n
+        double* p = scr;                                 // L
+        // p = c B v  (v = x with v[0] = v0)
+        for (int i = tid; i < L; i += nt) {
+            double sacc = B[i] * v0;
+            for (int j = 1; j < L; ++j) sacc += B[i + (size_t)n * j] * x[j];
+            p[i] = c * sacc;
+        }
+        team.sync();
+        double loc2 = 0.0;
+        for (int i = tid; i < L; i += nt) loc2 += (i == 0 ? v0 : x[i]) * p[i];
+        const double vp = team_reduce_sum(team, loc2, red);
+        const double K = 0.5 * c * vp;
+        // B -= v w^T + w v^T,  w = p - K v
+        for (int idx = tid; idx < L * L; idx += nt) {
+            const int i = idx % L, j = idx / L;
+            const double vi = i == 0 ? v0 : x[i], vj = j == 0 ? v0 : x[j];
+            const double wi = p[i] - K * vi, wj = p[j] - K * vj;
+            B[i + (size_t)n * j] -= vi * wj + wi * vj;
+        }
+        team.sync();
+        if (tid == 0) {
+            e[kk] = beta;
+            vn[kk] = vv;
+            x[0] = v0;  // column kk below the diagonal now holds v
+        }
+        team.sync();
+    }
+    if (tid == 0) {
+        for (int i = 0; i < n; ++i) d[i] = a[i + (size_t)n * i];
+        if (n >= 2) {
+            e[n - 2] = a[(n - 1) + (size_t)n * (n - 2)];
+            vn[n - 2] = 0.0;
+        }
+        vn[n - 1] = 0.0;
+    }
+    team.sync();
+    // ---- 2. the k largest eigenvalues by bisection, one per thread
+    double gl = 0.0, gu = 0.0, tnorm = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+        const double lo = d[i] - r, hi = d[i] + r;
+        if (i == 0 || lo < gl) gl = lo;
+        if (i == 0 || hi > gu) gu = hi;
+    }
+    tnorm = fmax(fabs(gl), fabs(gu));
+    for (int r = tid; r < k; r += nt) {
+        const int m = n - 1 - r;  // ascending index of the (r+1)-th largest
+        double lo = gl - 1e-300 - 2.2e-16 * tnorm, hi = gu + 2.2e-16 * tnorm + 1e-300;
+        for (int it = 0; it < 200; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            if (hi - lo <= 4.4e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300 || mid == lo || mid == hi) break;
+            if (tridiag_count_below(n, d, e, mid) > m)
+                hi = mid;
+            else
+                lo = mid;
+        }
+        theta[r] = 0.5 * (lo + hi);
+    }
+    team.sync();
+    // ---- 3. eigenvectors of T by inverse iteration: Gaussian elimination with
+    //      partial pivoting of T - theta I (U has two superdiagonals), three
+    //      solves from a fixed pseudo-random start; one thread per vector,
+    //      kb vectors at a time (5 n doubles of scratch each)
+    for (int r0 = 0; r0 < k; r0 += kb) {
+        const int nb = (k - r0) < kb ? (k - r0) : kb;
+        for (int rr = tid; rr < nb; rr += nt) {
+            const int r = r0 + rr;
+            double* ml = scr + (size_t)5 * n * rr;  // multipliers
+            double* u0 = ml + n;                     // U diagonal
+            double* u1 = u0 + n;                     // U superdiagonal
+            double* u2 = u1 + n;                     // U second superdiagonal (pivoting fill)
+            double* sw = u2 + n;                     // 1.0 where rows i, i+1 were swapped
+            double* y = u + (size_t)n * r;
+            const double tiny = 2.2e-16 * tnorm + 1e-300;
+            const double sh = theta[r];
+            double ci = d[0] - sh, bi = n > 1 ? e[0] : 0.0;
+            for (int i = 0; i + 1 < n; ++i) {
+                const double sub = e[i], cn = d[i + 1] - sh, bn = (i + 2 < n) ? e[i + 1] : 0.0;
+                if (fabs(ci) >= fabs(sub)) {
+                    const double piv = (ci == 0.0) ? tiny : ci;
+                    const double mlt = sub / piv;
+                    u0[i] = piv;
+                    u1[i] = bi;
+                    u2[i] = 0.0;
+                    ml[i] = mlt;
+                    sw[i] = 0.0;
+                    ci = cn - mlt * bi;
+                    bi = bn;
+                } else {
+                    const double mlt = ci / sub;
+                    u0[i] = sub;
+                    u1[i] = cn;
+                    u2[i] = bn;
+                    ml[i] = mlt;
+                    sw[i] = 1.0;
+                    ci = bi - mlt * cn;
+                    bi = -mlt * bn;
+                }
+            }
+            u0[n - 1] = (fabs(ci) < tiny) ? (ci < 0.0 ? -tiny : tiny) : ci;
+            for (int i = 0; i < n; ++i)
+                if (fabs(u0[i]) < tiny) u0[i] = u0[i] < 0.0 ? -tiny : tiny;
+            for (int i = 0; i < n; ++i)
+                y[i] = (double)(splitmix(0x7e1dULL + (uint64_t)i * 131 + (uint64_t)r) >> 11) * 0x1.0p-53 + 0.25;
+            for (int it = 0; it < 3; ++it) {
+                for (int i = 0; i + 1 < n; ++i) {  // b <- L^-1 P b
+                    if (sw[i] != 0.0) {
+                        const double t0 = y[i];
+                        y[i] = y[i + 1];
+                        y[i + 1] = t0;
+                    }
+                    y[i + 1] -= ml[i] * y[i];
+                }
+                double nrm = 0.0;
+                for (int i = n - 1; i >= 0; --i) {  // U y = b
+                    double v = y[i];
+                    if (i + 1 < n) v -= u1[i] * y[i + 1];
+                    if (i + 2 < n) v -= u2[i] * y[i + 2];
+                    v /= u0[i];
+                    y[i] = v;
+                    nrm = fmax(nrm, fabs(v));
+                }
+                const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;
+                for (int i = 0; i < n; ++i) y[i] *= inv;
+            }
+        }
+        team.sync();
+    }
+    // ---- 4. orthonormalise (clusters of close eigenvalues), descending order
+    if (!team_cgs2(team, n, k, u, cf, red)) return 0;
+    // ---- 5. back-transformation u <- H_0 ... H_{n-3} u (one thread per vector)
+    for (int r = tid; r < k; r += nt) {
+        double* y = u + (size_t)n * r;
+        for (int kk = n - 3; kk >= 0; --kk) {
+            if (!(vn[kk] > 0.0)) continue;
+            const double* v = a + (size_t)n * kk + kk + 1;
+            const int L = n - kk - 1;
+            double sacc = 0.0;
+            for (int i = 0; i < L; ++i) sacc += v[i] * y[kk + 1 + i];
+            sacc *= 2.0 / vn[kk];
+            for (int i = 0; i < L; ++i) y[kk + 1 + i] -= sacc * v[i];
+        }
+    }
+    team.sync();
+    return 1;
+}
+
 }  // namespace octen

@@ -83,3 +83,9 @@ extern "C" int h_lu_inverse_team(int n, const double* a, double* inv) {
     return lu_fullpiv_inverse_team(team, n, m.data(), n, inv, n, rp.data(), cp.data(), piv.data(), scr.data()) ? 1
                                                                                                              : 0;
 }
+
+extern "C" int h_sym_eig_top_tridiag(int n, const double* a, int k, double* u, double* theta, int kb) {
+    std::vector<double> am(a, a + (size_t)n * n), work((size_t)3 * n + (size_t)5 * n * kb), cf(k + 8), red(8);
+    TeamHost team;
+    return sym_eig_top_tridiag(team, n, am.data(), k, u, theta, work.data(), kb, cf.data(), red.data());
+}

@@ -228,3 +228,39 @@ def test_eig_real_team_matches_the_serial_routine(lib):
         assert np.allclose(wr0, wr1, rtol=1e-10, atol=1e-10) and np.allclose(wi0, wi1, rtol=1e-10, atol=1e-10)
         # eigenvectors of a non-normal matrix move with ulp-level changes;
         # the residual test above (vs LAPACK) pins both versions
+
+
+@pytest.mark.parametrize("n,k,kb,kind", [(64, 16, 15, "gapless"), (100, 20, 25, "gapless"), (128, 32, 32, "lowrank"),
+                                         (40, 40, 7, "gapless"), (30, 5, 5, "cluster")])
+def test_sym_eig_top_tridiag(lib, n, k, kb, kind):
+    # the dense fallback of the GEVD eigenbasis: Householder + bisection +
+    # inverse iteration, against LAPACK (numpy.linalg.eigh)
+    r = np.random.default_rng(n + k)
+    if kind == "gapless":
+        x = r.random((n, 3 * n))
+        a = x @ x.T
+    elif kind == "lowrank":
+        x = r.random((n, k)) @ r.random((k, 4 * n)) + 1e-4 * r.standard_normal((n, 4 * n))
+        a = x @ x.T
+    else:  # clustered: eigenvalues 1 +- 1e-9 in the top block
+        qm, _ = np.linalg.qr(r.standard_normal((n, n)))
+        ev = np.concatenate([1.0 + 1e-9 * np.arange(8), np.linspace(0.1, 0.5, n - 8)])
+        a = (qm * ev) @ qm.T
+        a = 0.5 * (a + a.T)
+    a = np.asfortranarray(a)
+    u = np.zeros((n, k), order="F")
+    th = np.zeros(k)
+    lib.h_sym_eig_top_tridiag.restype = ctypes.c_int
+    assert lib.h_sym_eig_top_tridiag(n, P(a), k, P(u), P(th), kb) == 1
+    w, v = np.linalg.eigh(a)
+    w, v = w[::-1], v[:, ::-1]
+    scale = abs(w[0])
+    assert np.max(np.abs(th - w[:k])) <= 1e-12 * scale
+    assert np.max(np.abs(u.T @ u - np.eye(k))) < 1e-12
+    # residuals |A u - theta u| at rounding level
+    res = np.linalg.norm(a @ u - u * th, axis=0)
+    assert np.max(res) <= 1e-11 * scale
+    if kind != "cluster":
+        # the same subspace as LAPACK's top-k eigenvectors
+        s = np.linalg.svd(v[:, :k].T @ u, compute_uv=False)
+        assert s.min() > 1 - 1e-9
