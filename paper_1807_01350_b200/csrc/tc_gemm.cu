@@ -15,6 +15,7 @@
 //   warps 4..7  epilogue: tcgen05.ld 32x32b.x32 -> fp32 stores
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <cstdint>
 #include <cstring>
@@ -303,6 +304,215 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Persistent GEMM1: one CTA per SM loops over the output tiles (m-tiles
+// fastest, tile L = blockIdx.x + i * gridDim.x, so the CTAs running at the
+// same time share X slabs in L2).  The accumulator is double-buffered in
+// TMEM (2 x 256 of the 512 columns): four dedicated epilogue warps (8..11)
+// drain tile i while the MMA warp accumulates tile i+1, and the stage ring
+// (TMA -> converters -> MMA) runs on across tile boundaries.  The per-tile
+// prologue (TMEM alloc, barrier init, pipeline fill) and the epilogue's
+// 128 KB of stores no longer sit between mainloops.
+//   warp 0: TMA producer    warp 1: TMEM alloc + MMA issuer
+//   warps 2..7: X lo split   warps 8..11: epilogue (TMEM lanes 32 (w % 4) ..)
+// ---------------------------------------------------------------------------
+constexpr int G1P_THREADS = 384;
+constexpr int G1P_EPI_WARP0 = 8;
+constexpr uint32_t G1P_TMEM_COLS = 512;
+constexpr size_t G1P_EPI_BYTES = 4 * 32 * 33 * sizeof(float);
+
+__global__ void __launch_bounds__(G1P_THREADS, 1)
+    tc_gemm_tf32x3_persistent_kernel(const __grid_constant__ CUtensorMap map_ahi,
+                                     const __grid_constant__ CUtensorMap map_alo,
+                                     const __grid_constant__ CUtensorMap map_x, float* __restrict__ Z, int M,
+                                     long long N, int K, long long ldz, int scP, int scQ, int scSh, int mt,
+                                     long long ntiles) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full_bar = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+    uint64_t* conv_bar = full_bar + STAGES;
+    uint64_t* empty_bar = conv_bar + STAGES;
+    uint64_t* tfull_bar = empty_bar + STAGES;  // [2] MMA -> epilogue
+    uint64_t* tempty_bar = tfull_bar + 2;      // [2] epilogue -> MMA
+    uint32_t* tmem_slot = (uint32_t*)(tempty_bar + 2);
+    float* epi = (float*)(smem + STAGES * STAGE_BYTES + 256);  // 4 warps x 32 x 33 epilogue staging
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int num_kb = (K + G1_BK - 1) / G1_BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&conv_bar[s], CONVERT_WARPS * 32);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull_bar[b], 1);
+            mbar_init(&tempty_bar[b], 4 * 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(G1P_TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---- TMA producer ----
+            uint32_t it = 0;
+            for (long long L = blockIdx.x; L < ntiles; L += gridDim.x) {
+                const int m0 = (int)(L % mt) * BM;
+                const long long n0 = (L / mt) * BN;
+                for (int kb = 0; kb < num_kb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    if (it >= STAGES) mbar_wait(&empty_bar[s], ph ^ 1);
+                    uint8_t* st = smem + s * STAGE_BYTES;
+                    mbar_arrive_expect_tx(&full_bar[s], 2 * A_BYTES + B_BYTES);
+                    tma_load_2d(st, &map_ahi, &full_bar[s], kb * G1_BK, m0);
+                    tma_load_2d(st + A_BYTES, &map_alo, &full_bar[s], kb * G1_BK, m0);
+                    tma_load_2d(st + 2 * A_BYTES, &map_x, &full_bar[s], kb * G1_BK, (int)n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---- MMA issuer ----
+            constexpr uint32_t idesc = make_idesc();
+            uint32_t it = 0, ti = 0;
+            for (long long L = blockIdx.x; L < ntiles; L += gridDim.x, ++ti) {
+                const uint32_t acc = ti & 1, use = ti >> 1;
+                if (ti >= 2) mbar_wait(&tempty_bar[acc], (use - 1) & 1);  // tile ti-2 drained
+                tc_fence_after();
+                const uint32_t dt = tmem_base + acc * 256;
+                for (int kb = 0; kb < num_kb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(&conv_bar[s], ph);
+                    tc_fence_after();
+                    uint8_t* st = smem + s * STAGE_BYTES;
+                    const uint32_t a_hi = smem_u32(st), a_lo = smem_u32(st + A_BYTES);
+                    const uint32_t b_hi = smem_u32(st + 2 * A_BYTES), b_lo = smem_u32(st + 2 * A_BYTES + B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < G1_BK / 8; ++k) {
+                        const uint32_t off = k * 32;
+                        const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+                        mma_tf32(dt, make_desc_sw64(a_hi + off), make_desc_sw64(b_hi + off), idesc, acc0);
+                        mma_tf32(dt, make_desc_sw64(a_hi + off), make_desc_sw64(b_lo + off), idesc, 1u);
+                        mma_tf32(dt, make_desc_sw64(a_lo + off), make_desc_sw64(b_hi + off), idesc, 1u);
+                    }
+                    mma_commit(&empty_bar[s]);
+                }
+                mma_commit(&tfull_bar[acc]);
+            }
+        }
+    } else if (warp < G1P_EPI_WARP0) {
+        // ---- X hi/lo split (warps 2..7) ----
+        const int ct = threadIdx.x - CONVERT_WARP0 * 32;
+        uint32_t it = 0;
+        for (long long L = blockIdx.x; L < ntiles; L += gridDim.x) {
+            for (int kb = 0; kb < num_kb; ++kb, ++it) {
+                const int s = it % STAGES;
+                const uint32_t ph = (it / STAGES) & 1;
+                mbar_wait(&full_bar[s], ph);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                float4* bx = (float4*)(st + 2 * A_BYTES);
+                float4* bl = (float4*)(st + 2 * A_BYTES + B_BYTES);
+                for (int i = ct; i < B_BYTES / 16; i += CONVERT_WARPS * 32) {
+                    const float4 v = bx[i];
+                    float4 l;
+                    l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                    bl[i] = l;
+                }
+                fence_proxy_async();
+                mbar_arrive(&conv_bar[s]);
+            }
+        }
+    } else {
+        // ---- epilogue (warps 8..11) ----
+        const int q = warp & 3;
+        uint32_t ti = 0;
+        for (long long L = blockIdx.x; L < ntiles; L += gridDim.x, ++ti) {
+            const uint32_t acc = ti & 1, use = ti >> 1;
+            const int m0 = (int)(L % mt) * BM;
+            const long long n0 = (L / mt) * BN;
+            mbar_wait(&tfull_bar[acc], use & 1);
+            tc_fence_after();
+            // staged through shared memory so every store instruction writes
+            // whole 128 B lines (8 lanes per row): lane-per-row stores left
+            // half-written sectors in L2 that were evicted early under the
+            // concurrent mainloop (ECC read-modify-write, 1.7x DRAM traffic)
+            float* tile = epi + q * 32 * 33;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) tile[lane * 33 + j] = __uint_as_float(r[j]);
+                __syncwarp();
+                const int cc = (lane & 7) * 4;
+                const long long col = n0 + c0 + cc;
+#pragma unroll 1
+                for (int it2 = 0; it2 < 8; ++it2) {
+                    const int rr = it2 * 4 + (lane >> 3);
+                    const int row = m0 + q * 32 + rr;
+                    if (row >= M) continue;
+                    const float v0 = tile[rr * 33 + cc], v1 = tile[rr * 33 + cc + 1], v2 = tile[rr * 33 + cc + 2],
+                                v3 = tile[rr * 33 + cc + 3];
+                    auto put = [&](float* zrow) {
+                        if (col + 4 <= N && (ldz % 4) == 0) {
+                            *(float4*)(zrow + col) = make_float4(v0, v1, v2, v3);
+                        } else {
+                            if (col < N) zrow[col] = v0;
+                            if (col + 1 < N) zrow[col + 1] = v1;
+                            if (col + 2 < N) zrow[col + 2] = v2;
+                            if (col + 3 < N) zrow[col + 3] = v3;
+                        }
+                    };
+                    if (scP <= 0) {
+                        put(Z + (size_t)row * ldz);
+                    } else if (row < scSh) {
+                        for (int p = 0; p < scP; ++p) put(Z + ((size_t)p * scQ + row) * ldz);
+                    } else {
+                        const int pr = scQ - scSh;
+                        const int p = (row - scSh) / pr, a = scSh + (row - scSh) % pr;
+                        put(Z + ((size_t)p * scQ + a) * ldz);
+                    }
+                }
+                __syncwarp();
+            }
+            // every thread's TMEM reads of this buffer are complete
+            tc_fence_before();
+            mbar_arrive(&tempty_bar[acc]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(G1P_TMEM_COLS));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Mode-2 contraction of the compression, batched over (replica p, slice k):
 //   Z2[p][a + Q b + Q^2 k] = sum_j Z1[p Q + a][k J + j] * V_p[j, b]
 // One CTA per (p, k): M = 128 rows of Z1 (a < Q used), N = 112 columns
@@ -535,6 +745,29 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
     if (!make_map(&mx, X, (uint64_t)K, (uint64_t)N, (uint64_t)K * 4, G1_BK, BN, CU_TENSOR_MAP_SWIZZLE_64B))
         return false;
     const size_t smem = STAGES * STAGE_BYTES + 1024 + 256;
+    static const bool classic = std::getenv("OCTEN_G1_CLASSIC") != nullptr;  // diagnostics: one CTA per tile
+    if (!classic) {
+        static bool pattr = false;
+        if (!pattr) {
+            OCTEN_CUDA(cudaFuncSetAttribute(tc_gemm_tf32x3_persistent_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + G1P_EPI_BYTES)));
+            pattr = true;
+        }
+        static int nsm = 0;
+        if (!nsm) {
+            int dev = 0;
+            OCTEN_CUDA(cudaGetDevice(&dev));
+            OCTEN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        }
+        const int mt = (M + BM - 1) / BM;
+        const long long ntiles = (long long)mt * ((N + BN - 1) / BN);
+        const int grid = (int)std::min<long long>(ntiles, nsm);
+        tc_gemm_tf32x3_persistent_kernel<<<grid, G1P_THREADS, smem + G1P_EPI_BYTES, st>>>(mhi, mlo, mx, Z, M, N, K, N, scatter_p,
+                                                                          scatter_q, scatter_sh, mt, ntiles);
+        OCTEN_LAUNCHED(1);
+        OCTEN_CUDA(cudaGetLastError());
+        return true;
+    }
     static bool attr = false;
     if (!attr) {
         OCTEN_CUDA(cudaFuncSetAttribute(tc_gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
