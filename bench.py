@@ -411,9 +411,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
-    ap.add_argument("--multi", default="sharded", choices=["sharded", "replicas"],
-                    help="N>1: one replica-sharded stream over all ranks (NCCL all-gathers, strong scaling) "
-                         "or N independent streams (weak scaling)")
+    ap.add_argument("--multi", default="sharded", choices=["sharded", "temporal", "replicas"],
+                    help="N>1: one replica-sharded stream over all ranks (NCCL all-gathers, strong scaling); "
+                         "'temporal': the same with the compression sharded over the batch's slices "
+                         "(NCCL reduce-scatter of the partial summaries); or N independent streams (weak scaling)")
     args = ap.parse_args()
     cfg = CONFIGS.get(args.config, C4)
     rank = int(os.environ.get("RANK", "0"))
@@ -447,7 +448,8 @@ def main():
         return
     I, J, K0, t, Q, P, R, sh = (cfg[k] for k in ("I", "J", "K0", "t", "Q", "P", "R", "shared"))
     nb = args.warmup + args.steps + args.e2e_steps + 2
-    sharded = world > 1 and args.multi == "sharded"
+    sharded = world > 1 and args.multi in ("sharded", "temporal")
+    temporal = world > 1 and args.multi == "temporal"
     # sharded: every rank sees the same batches and seeds (one stream);
     # replicas: independent streams with per-rank data
     dseed = 1234 if sharded else 1234 + rank
@@ -460,8 +462,16 @@ def main():
     t_init = time.perf_counter()
     if sharded:
         st = ob.ShardedStream(scfg, rank, world, lambda snd, rcv: dist.all_gather_into_tensor(rcv, snd))
-        st.ingest(first)
-        ingest = st.ingest
+        if temporal:
+            def ingest(b):
+                tb = b.shape[2]
+                lo, hi = tb * rank // world, tb * (rank + 1) // world
+                st.ingest_temporal(b[:, :, lo:hi], lo, tb,
+                                   lambda snd, rcv: dist.reduce_scatter_tensor(rcv, snd, op=dist.ReduceOp.SUM))
+            ingest(first)
+        else:
+            st.ingest(first)
+            ingest = st.ingest
     else:
         st = ob.init_stream(first, scfg)
         ingest = lambda b: ob.ingest_batch(st, b)  # noqa: E731
@@ -514,8 +524,10 @@ def main():
             h.copy_(d.permute(2, 1, 0))
             hb.append(h.permute(2, 1, 0))
         torch.cuda.synchronize()
-        st.prefetch(hb[0])  # warm-up: copy streams, both prefetch slots, staging buffers
-        st.prefetch(hb[1])
+        use_pf = not temporal  # a temporal shard reads only its slices: no whole-batch prefetch
+        if use_pf:
+            st.prefetch(hb[0])  # warm-up: copy streams, both prefetch slots, staging buffers
+            st.prefetch(hb[1])
         ingest(hb[0])
         ingest(hb[1])
         _ = st.model
@@ -526,10 +538,11 @@ def main():
         # the next batch's H2D copy is started (prefetch) before the current
         # batch is ingested, so it overlaps this batch's device work; every
         # step's copy is inside the timed region
-        st.prefetch(hb[0])
+        if use_pf:
+            st.prefetch(hb[0])
         e2e_marks = []
         for i, h in enumerate(hb):
-            if i + 1 < len(hb):
+            if use_pf and i + 1 < len(hb):
                 st.prefetch(hb[i + 1])
             ingest(h)
             m = st.model  # D2H of the updated model (factors + lambda)
@@ -591,9 +604,12 @@ def main():
                 "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
                 "dtype": "f32 compress (split-TF32/FP32) + f64 CP-ALS/merge", "data": "synthetic",
                 "config": {"workload": args.config, **cfg, "noise": args.noise, "l2": "inputs larger than L2 (%d MB fp32 batch)" % (I * J * t * 4 // 10**6),
-                           "parallelism": ("replica-sharded x%d (NCCL all-gather of replica models)" % world
-                                           if sharded else ("independent streams x%d" % world if world > 1
-                                                            else "single"))},
+                           "parallelism": (("temporal-sharded compression x%d (NCCL reduce-scatter of partial "
+                                            "summaries) + replica-sharded CP-ALS (NCCL all-gather)" % world)
+                                           if temporal else
+                                           ("replica-sharded x%d (NCCL all-gather of replica models)" % world
+                                            if sharded else ("independent streams x%d" % world if world > 1
+                                                             else "single")))},
                 "stages": stage, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks}
         if sparse is not None:

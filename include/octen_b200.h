@@ -155,6 +155,25 @@ int octen_stream_begin(octen_stream* s, const void* data, int dtype, int locatio
 int octen_stream_merge(octen_stream* s, const double* models_all, double* rows_out);
 int octen_stream_finish(octen_stream* s, const double* rows_all);
 
+/* ---- temporal sharding of the compression (the largest tensors) ----
+ * Instead of octen_stream_begin, rank g compresses only its share of the
+ * batch's slices, [k_off, k_off + dims_local[2]) of t_total, into partial
+ * summaries of EVERY replica (the compression is additive over slices,
+ * compression.cpp:141-153), and the caller reduce-scatters them by owner:
+ *   octen_stream_begin_temporal -> partial_out : shard_world * B doubles (device)
+ *                                   block g = replicas of rank g (chunk x Q^3)
+ *                                   + 1 status double (non-finite flag)
+ *   reduce-scatter (sum)         -> owned      : B doubles (this rank's block)
+ *   octen_stream_begin_reduced   -> models_out (as octen_stream_begin)
+ * then the all-gathers / merge / finish as in the replica-sharded protocol.
+ * B = octen_stream_partial_block_size().  A non-finite value on any rank
+ * makes every rank raise the same NumericError in begin_reduced.  Results
+ * equal the unsharded stream up to the summation order of the partials. */
+int octen_stream_partial_block_size(const octen_stream* s, int64_t* n);
+int octen_stream_begin_temporal(octen_stream* s, const void* data, int dtype, int location, int order,
+                                const int64_t* dims_local, int64_t k_off, int64_t t_total, double* partial_out);
+int octen_stream_begin_reduced(octen_stream* s, const double* owned_block, double* models_out);
+
 /* ---- stage-level entry points (the reference's L2 API, batched over replicas) ---- */
 
 /* compress (proj/include/cpstream/compression.hpp:82-83; src/compression.cpp:108-130)

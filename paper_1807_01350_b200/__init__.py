@@ -333,10 +333,50 @@ class ShardedStream(StreamState):
     def finish(self, rows_all):
         _check(C.LIB.octen_stream_finish(self._h, ctypes.c_void_p(rows_all.data_ptr())))
 
+    # temporal sharding of the compression (octen_stream_begin_temporal /
+    # octen_stream_begin_reduced): this rank's slices of the batch
+    def begin_temporal(self, local_slices, k_off: int, t_total: int):
+        """Partial summaries of every replica from this rank's slices
+        [k_off, k_off + local t) of a batch of t_total slices; returns the
+        world x B partial buffer for the caller's reduce-scatter (sum)."""
+        import torch
+        if not hasattr(self, "_pp"):
+            n = C.c_i64()
+            _check(C.LIB.octen_stream_partial_block_size(self._h, ctypes.byref(n)))
+            dev = torch.device("cuda", self.config.device)
+            self.partial_count = n.value
+            self._pp = torch.zeros(n.value * self.shard_world, dtype=torch.float64, device=dev)
+            self._po = torch.zeros(n.value, dtype=torch.float64, device=dev)
+        keep, ptr, dt, loc, dims = _batch_args(local_slices)
+        d = (C.c_i64 * len(dims))(*dims)
+        _check(C.LIB.octen_stream_begin_temporal(self._h, ptr, dt, loc, len(dims), d, int(k_off), int(t_total),
+                                                 ctypes.c_void_p(self._pp.data_ptr())))
+        del keep
+        return self._pp
+
+    def begin_reduced(self, owned):
+        _check(C.LIB.octen_stream_begin_reduced(self._h, ctypes.c_void_p(owned.data_ptr()),
+                                                ctypes.c_void_p(self._mo.data_ptr())))
+        return self._mo
+
+    def ingest_temporal(self, local_slices, k_off: int, t_total: int, reduce_scatter) -> None:
+        """One batch with the compression sharded over the temporal mode:
+        `reduce_scatter(send, recv)` sums the world x B partials into this
+        rank's B (e.g. torch.distributed.reduce_scatter_tensor over NCCL)."""
+        import torch
+        self.begin_temporal(local_slices, k_off, t_total)
+        reduce_scatter(self._pp, self._po)
+        torch.cuda.synchronize()
+        self.begin_reduced(self._po)
+        self._exchange()
+
     def ingest(self, batch) -> None:
         """init_stream on the first call, ingest_batch afterwards."""
-        import torch
         self.begin(batch)
+        self._exchange()
+
+    def _exchange(self) -> None:
+        import torch
         self._allgather(self._mo, self._ma)
         torch.cuda.synchronize()
         self.merge(self._ma)

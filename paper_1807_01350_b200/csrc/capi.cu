@@ -159,6 +159,32 @@ int octen_stream_ingest(octen_stream* s, const void* data, int dtype, int locati
     });
 }
 
+int octen_stream_partial_block_size(const octen_stream* s, int64_t* n) {
+    return guard([&] {
+        if (!s || !n) throw octen::ConfigError("octen_stream_partial_block_size: null argument");
+        *n = (int64_t)s->s->partial_block_count();
+    });
+}
+
+int octen_stream_begin_temporal(octen_stream* s, const void* data, int dtype, int location, int order,
+                                const int64_t* dims_local, int64_t k_off, int64_t t_total, double* partial_out) {
+    return guard([&] {
+        if (!s || !dims_local || !partial_out || (!data && dims_local[2] > 0))
+            throw octen::ConfigError("octen_stream_begin_temporal: null argument");
+        check_dtype(dtype, location);
+        OCTEN_CUDA(cudaSetDevice(s->s->cfg.device));
+        s->s->begin_temporal(data, dtype, location, order, dims_local, k_off, t_total, partial_out);
+    });
+}
+
+int octen_stream_begin_reduced(octen_stream* s, const double* owned_block, double* models_out) {
+    return guard([&] {
+        if (!s || !owned_block || !models_out) throw octen::ConfigError("octen_stream_begin_reduced: null argument");
+        OCTEN_CUDA(cudaSetDevice(s->s->cfg.device));
+        s->s->begin_reduced(owned_block, models_out);
+    });
+}
+
 int octen_stream_prefetch(octen_stream* s, const void* data, int dtype, int order, const int64_t* dims) {
     return guard([&] {
         if (!s || !data || !dims) throw octen::ConfigError("octen_stream_prefetch: null argument");

@@ -301,6 +301,17 @@ void CompressEngine::accumulate(int dtype, std::int64_t t, const double* dW, dou
         run_accumulate<double>(*this, t, Z2d.p, dW, dY, st);
 }
 
+void CompressEngine::accumulate_rows(int dtype, std::int64_t t, const double* dW, std::int64_t t_total,
+                                     std::int64_t k0, double* dY, cudaStream_t st) {
+    if (dtype == 1)
+        gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<float>{Z2f.p, (int)t, Q}, G3B{dW, t_total, k0, Q}, G3C{dY, Q},
+                              st);
+    else
+        gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<double>{Z2d.p, (int)t, Q}, G3B{dW, t_total, k0, Q}, G3C{dY, Q},
+                              st);
+    OCTEN_CUDA(cudaGetLastError());
+}
+
 void CompressEngine::compress_f32(const float* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st) {
     project(dX, 1, t, st, nullptr, 0, nullptr);
     accumulate(1, t, dW, dY, st);

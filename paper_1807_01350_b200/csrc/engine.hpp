@@ -104,6 +104,10 @@ public:
     void project(const void* dX, int dtype, std::int64_t t, cudaStream_t st, const cudaEvent_t* ready,
                  std::int64_t ready_slices, int* flag);
     void accumulate(int dtype, std::int64_t t, const double* dW, double* dY, cudaStream_t st);
+    // The same for t slices whose temporal rows are rows [k0, k0 + t) of a
+    // W with t_total rows per replica (temporal sharding).
+    void accumulate_rows(int dtype, std::int64_t t, const double* dW, std::int64_t t_total, std::int64_t k0,
+                         double* dY, cudaStream_t st);
 
     int P = 0, Q = 0, shared = 0;
     std::int64_t I = 0, J = 0, Meff = 0;

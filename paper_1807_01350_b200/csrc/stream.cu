@@ -426,7 +426,7 @@ void Stream::begin(const void* data, int dtype, int location, int order, const s
     prec = BatchRecordC{};
     prec.batch_index = first ? 0 : batches_seen;
     prec.t_new = t;
-    const int Q = cfg.q, R = cfg.rank;
+    const int Q = cfg.q;
     try {
         auto tc = Clock::now();
         const size_t n = (size_t)I * J * t;
@@ -488,34 +488,151 @@ void Stream::begin(const void* data, int dtype, int location, int order, const s
         OCTEN_CUDA(cudaEventRecord(evs[1], st));
         OCTEN_CUDA(cudaStreamSynchronize(st));
         prec.compress_seconds = std::chrono::duration<double>(Clock::now() - tc).count();
-        auto ta = Clock::now();
-        OCTEN_CUDA(cudaEventRecord(evs[2], st));
-        double hdr[4] = {0, 0, 0, 0};
-        const size_t qr = (size_t)Q * R;
-        if (pl > 0) {
-            std::vector<std::uint64_t> seeds(pl);
-            for (int r = 0; r < pl; ++r)
-                seeds[r] = rng::derive(cfg.seed, {rng::kStreamAls, (std::uint64_t)(p0 + r), (std::uint64_t)prec.batch_index});
-            try {
-                als.run(pl, cfg.als_n_restarts, Q, R, cfg.als_max_iters, cfg.als_rel_tol, Y.p, seeds, st);
-            } catch (const NumericError&) {
-                // a replica's CP-ALS failed: every rank raises it after the exchange
-                if (als.failure.kind == 0) throw;
-                hdr[0] = als.failure.kind;
-                hdr[1] = als.failure.a;
-                hdr[2] = als.failure.b;
-            }
-            if (hdr[0] == 0.0) {
-                OCTEN_CUDA(cudaMemcpyAsync(models_out + 4, als.Mf.p, sizeof(double) * pl * 3 * qr,
-                                           cudaMemcpyDeviceToDevice, st));
-                OCTEN_CUDA(cudaMemcpyAsync(models_out + 4 + (size_t)chunk * 3 * qr, als.Mlam.p, sizeof(double) * pl * R,
-                                           cudaMemcpyDeviceToDevice, st));
-            }
+        als_phase(models_out);
+    } catch (...) {
+        fail_pending();
+    }
+}
+
+// CP-ALS of the owned replicas on the updated summaries, packed into this
+// rank's models block (status header + factors + lambdas).
+void Stream::als_phase(double* models_out) {
+    const int Q = cfg.q, R = cfg.rank;
+    auto ta = Clock::now();
+    OCTEN_CUDA(cudaEventRecord(evs[2], st));
+    double hdr[4] = {0, 0, 0, 0};
+    const size_t qr = (size_t)Q * R;
+    if (pl > 0) {
+        std::vector<std::uint64_t> seeds(pl);
+        for (int r = 0; r < pl; ++r)
+            seeds[r] = rng::derive(cfg.seed, {rng::kStreamAls, (std::uint64_t)(p0 + r), (std::uint64_t)prec.batch_index});
+        try {
+            als.run(pl, cfg.als_n_restarts, Q, R, cfg.als_max_iters, cfg.als_rel_tol, Y.p, seeds, st);
+        } catch (const NumericError&) {
+            // a replica's CP-ALS failed: every rank raises it after the exchange
+            if (als.failure.kind == 0) throw;
+            hdr[0] = als.failure.kind;
+            hdr[1] = als.failure.a;
+            hdr[2] = als.failure.b;
         }
-        OCTEN_CUDA(cudaMemcpyAsync(models_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
-        OCTEN_CUDA(cudaEventRecord(evs[3], st));
+        if (hdr[0] == 0.0) {
+            OCTEN_CUDA(cudaMemcpyAsync(models_out + 4, als.Mf.p, sizeof(double) * pl * 3 * qr,
+                                       cudaMemcpyDeviceToDevice, st));
+            OCTEN_CUDA(cudaMemcpyAsync(models_out + 4 + (size_t)chunk * 3 * qr, als.Mlam.p, sizeof(double) * pl * R,
+                                       cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    OCTEN_CUDA(cudaMemcpyAsync(models_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
+    OCTEN_CUDA(cudaEventRecord(evs[3], st));
+    OCTEN_CUDA(cudaStreamSynchronize(st));
+    prec.als_seconds = std::chrono::duration<double>(Clock::now() - ta).count();
+}
+
+namespace {
+__global__ void add_f64_kernel(double* __restrict__ y, const double* __restrict__ x, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        y[i] += x[i];
+}
+__global__ void set_status_kernel(double* out, int G, size_t blk, const int* flag) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < G) out[(size_t)g * blk + blk - 1] = *flag ? 1.0 : 0.0;
+}
+}  // namespace
+
+// ---- temporal sharding, phase 1a: this rank's slices [k_off, k_off + t_local)
+// of a batch of t_total slices, compressed into partial summaries of EVERY
+// replica, laid out as shard_world blocks (block g: replicas of rank g,
+// chunk x Q^3, then one status double = this rank's non-finite flag) for a
+// reduce-scatter (sum) by the caller.  The temporal rows of the whole batch
+// are drawn here (identically on every rank).
+void Stream::begin_temporal(const void* data, int dtype, int location, int order, const std::int64_t* dims_local,
+                            std::int64_t k_off, std::int64_t t_total, double* partial_out) {
+    if (pending) throw ConfigError("octen: the previous batch has not finished (begin/merge/finish)");
+    if (order != 3) throw ConfigError("ingest_batch: batch order mismatch at batch " + std::to_string(batches_seen));
+    const std::int64_t t_local = dims_local[2];
+    if (t_total < 1 || k_off < 0 || t_local < 0 || k_off + t_local > t_total)
+        throw ConfigError("octen: temporal shard outside the batch");
+    const bool first = !initialized;
+    if (first) {
+        const std::int64_t full[3] = {dims_local[0], dims_local[1], t_total};
+        prepare(order, full);
+    } else {
+        if (dims_local[0] != I)
+            throw ConfigError("ingest_batch: extent mismatch on mode 1 at batch " + std::to_string(batches_seen));
+        if (dims_local[1] != J)
+            throw ConfigError("ingest_batch: extent mismatch on mode 2 at batch " + std::to_string(batches_seen));
+    }
+    if (!comp_all_ready) {
+        comp_all.set_projections(cfg.p, cfg.q, cfg.shared, I, J, hU.data(), hV.data(), st);
+        comp_all_ready = true;
+    }
+    context = first ? std::string() : "batch " + std::to_string(batches_seen) + ": ";
+    if (!first && cfg.strict) snapshot(backup);
+    pending = true;
+    pending_first = first;
+    pending_t = t_total;
+    t_start = Clock::now();
+    prec = BatchRecordC{};
+    prec.batch_index = first ? 0 : batches_seen;
+    prec.t_new = t_total;
+    tshard_drawn = batches_drawn;
+    tshard_tgram = tgram;
+    const int P = cfg.p, Q = cfg.q;
+    const size_t q3 = (size_t)Q * Q * Q, blk = (size_t)chunk * q3 + 1;
+    try {
+        auto tc = Clock::now();
+        OCTEN_CUDA(cudaEventRecord(evs[0], st));
+        extend_temporal(t_total);
+        flag.reserve(1);
+        flag.zero(1, st);
+        Zpart.reserve((size_t)shard_world * chunk * q3);
+        Zpart.zero((size_t)shard_world * chunk * q3, st);
+        if (t_local > 0) {
+            const void* dX = stage_input(data, dtype, location, (size_t)I * J * t_local);
+            comp_all.project(dX, dtype, t_local, st, nullptr, 0, flag.p);
+            comp_all.accumulate_rows(dtype, t_local, dW.p, t_total, k_off, Zpart.p, st);
+        }
+        // replica-contiguous partials -> per-owner blocks with a status slot
+        OCTEN_CUDA(cudaMemcpy2DAsync(partial_out, blk * sizeof(double), Zpart.p, (size_t)chunk * q3 * sizeof(double),
+                                     (size_t)chunk * q3 * sizeof(double), shard_world, cudaMemcpyDeviceToDevice, st));
+        set_status_kernel<<<1, 32 * ((shard_world + 31) / 32), 0, st>>>(partial_out, shard_world, blk, flag.p);
+        OCTEN_LAUNCHED(1);
+        OCTEN_CUDA(cudaGetLastError());
+        OCTEN_CUDA(cudaEventRecord(evs[1], st));
         OCTEN_CUDA(cudaStreamSynchronize(st));
-        prec.als_seconds = std::chrono::duration<double>(Clock::now() - ta).count();
+        prec.compress_seconds = std::chrono::duration<double>(Clock::now() - tc).count();
+        (void)P;
+    } catch (...) {
+        batches_drawn = tshard_drawn;
+        tgram = tshard_tgram;
+        fail_pending();
+    }
+}
+
+// ---- temporal sharding, phase 1b: the reduced block of this rank's replicas
+// (sum over ranks of their partials; last slot = number of ranks that saw a
+// non-finite value) is added to the owned summaries, then CP-ALS as begin().
+void Stream::begin_reduced(const double* owned_block, double* models_out) {
+    if (!pending) throw ConfigError("octen: begin_reduced without begin_temporal");
+    const int Q = cfg.q;
+    const size_t q3 = (size_t)Q * Q * Q, blk = (size_t)chunk * q3 + 1;
+    try {
+        double status = 0.0;
+        OCTEN_CUDA(cudaMemcpyAsync(&status, owned_block + blk - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+        if (status != 0.0) {
+            batches_drawn = tshard_drawn;
+            tgram = tshard_tgram;
+            throw NumericError("DenseTensor: non-finite value");
+        }
+        if (pl > 0) {
+            const size_t n = (size_t)pl * q3;
+            add_f64_kernel<<<(int)std::min<size_t>(148 * 8, (n + 255) / 256), 256, 0, st>>>(Y.p, owned_block, n);
+            OCTEN_LAUNCHED(1);
+            OCTEN_CUDA(cudaGetLastError());
+        }
+        ++batches_seen;
+        als_phase(models_out);
     } catch (...) {
         fail_pending();
     }

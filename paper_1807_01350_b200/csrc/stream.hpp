@@ -64,6 +64,13 @@ public:
 
     void begin(const void* data, int dtype, int location, int order, const std::int64_t* dims, double* models_out);
     void merge_phase(const double* models_all, double* rows_out);
+    // temporal sharding of the compression (octen_stream_begin_temporal /
+    // octen_stream_begin_reduced): partial summaries of every replica from
+    // this rank's slices, reduce-scattered by the caller, then CP-ALS.
+    void begin_temporal(const void* data, int dtype, int location, int order, const std::int64_t* dims_local,
+                        std::int64_t k_off, std::int64_t t_total, double* partial_out);
+    void begin_reduced(const double* owned_block, double* models_out);
+    size_t partial_block_count() const { return (size_t)chunk * cfg.q * cfg.q * cfg.q + 1; }
     void finish(const double* rows_all);
     size_t models_count() const { return 4 + (size_t)chunk * (3 * (size_t)cfg.q * cfg.rank + cfg.rank); }
     size_t rows_count() const { return (size_t)chunk * cfg.q * cfg.rank; }
@@ -79,6 +86,8 @@ public:
     bool initialized = false;
     std::vector<double> hU, hV, hW, tgram;
     CompressEngine comp;
+    CompressEngine comp_all;  // every replica (temporal sharding)
+    bool comp_all_ready = false;
     AlsEngine als;
     MergeEngine merge;
     // Y: pl x Q^3 (owned replicas); hist: P*Q x R (all replicas, kept redundantly)
@@ -86,6 +95,9 @@ public:
     DevBuf<double> xmodels, xrows, MfAll, MlamAll, tstackAll;
     DevBuf<float> X32;
     DevBuf<int> flag;
+    DevBuf<double> Zpart;                 // temporal sharding: partial summaries, world x chunk x Q^3
+    std::int64_t tshard_drawn = 0;        // temporal state before begin_temporal (rollback)
+    std::vector<double> tshard_tgram;
     struct Prefetch {
         const void* host = nullptr;
         int dtype = 0, slot = 0;
@@ -125,6 +137,7 @@ private:
     void check_finite(const void* dX, int dtype, size_t n);
     void ensure_c_capacity(std::int64_t rows);
     void accumulate_stage_times();
+    void als_phase(double* models_out);
     void snapshot(Snapshot& s);
     void restore(Snapshot& s);
     [[noreturn]] void fail_pending();

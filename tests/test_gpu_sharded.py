@@ -114,3 +114,76 @@ def test_sharded_world1_ingest_path_matches_stream(ob):
     sh.ingest(batch)
     for f, g in zip(sh.model.factors, ref.model.factors):
         assert np.array_equal(f, g)
+
+
+def _drive_temporal(ranks, batch, world):
+    """Temporal sharding: rank g compresses its contiguous slice range of the
+    batch into partials of every replica; the reduce-scatter is a host-side
+    sum over ranks of each owner's block."""
+    import torch
+    t = batch.shape[2]
+    bounds = [t * g // world for g in range(world + 1)]
+    parts = []
+    for g, r in enumerate(ranks):
+        loc = np.asfortranarray(batch[:, :, bounds[g]:bounds[g + 1]])
+        parts.append(r.begin_temporal(loc, bounds[g], t).clone())
+    blk = ranks[0].partial_count
+    owned = [sum(p[g * blk:(g + 1) * blk] for p in parts) for g in range(world)]
+    mo = [r.begin_reduced(owned[g].contiguous()).clone() for g, r in enumerate(ranks)]
+    ma = torch.cat(mo)
+    ro = [r.merge(ma).clone() for r in ranks]
+    ra = torch.cat(ro)
+    for r in ranks:
+        r.finish(ra)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_temporal_sharding_matches_unsharded(ob, world):
+    # compression sharded over slices + reduce-scatter of the partials: the
+    # summaries equal the unsharded ones up to the summation order, the
+    # models to the ALS's sensitivity to that (noisy, well-posed data)
+    # noiseless low-rank data: ALS converges to the truth from either order
+    # of summation (on noisy data 30 sweeps amplify 1e-16 summary differences)
+    x, _ = O.generate_synthetic([60, 60, 70], 3, 3, 0.0, 0.0)
+    cfg = _cfg(ob, 3, 8, 12, 3, 38, iters=100, tol=1e-12)
+    ref = ob.init_stream(O.slice_mode(x, 2, 0, 40), cfg)
+    ranks = [ob.ShardedStream(cfg, g, world, None) for g in range(world)]
+    _drive_temporal(ranks, O.slice_mode(x, 2, 0, 40), world)
+    for b in range(3):
+        batch = O.slice_mode(x, 2, 40 + 10 * b, 10)
+        ob.ingest_batch(ref, batch)
+        _drive_temporal(ranks, batch, world)
+    ys_ref, _ = ref.summaries()
+    for g, r in enumerate(ranks):
+        ys, _ = r.summaries()
+        for i, y in enumerate(ys):
+            yr = ys_ref[r.p0 + i]
+            assert np.linalg.norm(y - yr) <= 1e-12 * np.linalg.norm(yr)
+    want = ref.model
+    for r in ranks:
+        got = r.model
+        cong = min(O.congruence(O.KruskalModel(want.factors, want.lambda_), O.KruskalModel(got.factors, got.lambda_)))
+        assert cong > 1 - 1e-6
+        assert r.slices_seen == ref.slices_seen
+
+
+def test_temporal_sharding_nonfinite_raises_on_every_rank(ob):
+    x = _data()
+    cfg = _cfg(ob, 3, 8, 12, 3, 38)
+    world = 2
+    ranks = [ob.ShardedStream(cfg, g, world, None) for g in range(world)]
+    _drive_temporal(ranks, O.slice_mode(x, 2, 0, 40), world)
+    bad = np.array(O.slice_mode(x, 2, 40, 10))
+    bad[3, 4, 8] = np.nan  # in rank 1's half only
+    seen = [r.slices_seen for r in ranks]
+    t = bad.shape[2]
+    parts = [r.begin_temporal(np.asfortranarray(bad[:, :, 5 * g:5 * (g + 1)]), 5 * g, t).clone()
+             for g, r in enumerate(ranks)]
+    blk = ranks[0].partial_count
+    owned = [sum(p[g * blk:(g + 1) * blk] for p in parts) for g in range(world)]
+    for g, r in enumerate(ranks):
+        with pytest.raises(ob.NumericError, match="non-finite"):
+            r.begin_reduced(owned[g].contiguous())
+    # the state is unchanged: the next good batch goes through on both ranks
+    _drive_temporal(ranks, O.slice_mode(x, 2, 40, 10), world)
+    assert [r.slices_seen for r in ranks] == [s_ + 10 for s_ in seen]

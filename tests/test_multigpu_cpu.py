@@ -140,3 +140,63 @@ def test_gloo_two_rank_sharded_stream_matches_unsharded(tmp_path):
     for k, f in zip("abc", ref.model.factors):
         assert np.allclose(r0[k], f, rtol=0, atol=1e-12 * np.abs(f).max())
     assert np.allclose(r0["lam"], ref.model.lambda_, rtol=1e-12)
+
+
+def _temporal_rank(rank, world, port, out_dir):
+    """Temporal sharding on CPU: each rank compresses its slice range into
+    partials of EVERY replica (oracle compress with the batch's temporal rows
+    at its offset), the partials are reduce-scattered by owner over gloo, and
+    the owners' summaries must equal the unsharded oracle's."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x = _data()
+        p0, pl = S.shard_range(P, world, rank)
+        chunk = -(-P // world)
+        rs = O.gen_replicas([x.shape[0], x.shape[1]], Q, P, SH, SEED)
+        y = [np.zeros((Q, Q, Q)) for _ in range(P)]
+        k = 0
+        for b in range(NB + 1):
+            t0, t = (0, K0) if b == 0 else (K0 + (b - 1) * T, T)
+            O.extend_temporal(rs, t)  # every rank draws the whole batch's rows
+            lo, hi = t * rank // world, t * (rank + 1) // world
+            part = np.zeros(world * (chunk * Q ** 3 + 1))
+            if hi > lo:
+                loc = O.slice_mode(x, 2, t0 + lo, hi - lo)
+                for r in range(P):
+                    z = O.compress(loc, rs, r, k + lo, k + hi)
+                    g, i = r // chunk, r % chunk
+                    off = g * (chunk * Q ** 3 + 1) + i * Q ** 3
+                    part[off:off + Q ** 3] = z.ravel(order="F")
+            send = torch.from_numpy(part)
+            recv = torch.zeros(chunk * Q ** 3 + 1, dtype=torch.float64)
+            dist.reduce_scatter(recv, list(send.chunk(world)))
+            got = recv.numpy()
+            for i in range(pl):
+                y[p0 + i] = y[p0 + i] + got[i * Q ** 3:(i + 1) * Q ** 3].reshape((Q, Q, Q), order="F")
+            k += t
+        np.save(os.path.join(out_dir, "y%d.npy" % rank), np.stack([y[p0 + i] for i in range(pl)]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_temporal_sharding_reduce_scatter_two_ranks(tmp_path):
+    world = 2
+    port = _free_port()
+    mp.spawn(_temporal_rank, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    x = _data()
+    rs = O.gen_replicas([x.shape[0], x.shape[1]], Q, P, SH, SEED)
+    summ = O.init_summaries(rs)
+    k = 0
+    for b in range(NB + 1):
+        t0, t = (0, K0) if b == 0 else (K0 + (b - 1) * T, T)
+        O.extend_temporal(rs, t)
+        O.update_summaries(summ, [O.compress(O.slice_mode(x, 2, t0, t), rs, r, k, k + t) for r in range(P)])
+        k += t
+    for g in range(world):
+        p0, pl = S.shard_range(P, world, g)
+        ys = np.load(os.path.join(str(tmp_path), "y%d.npy" % g))
+        for i in range(pl):
+            ref = summ.y[p0 + i]
+            assert np.linalg.norm(ys[i] - ref) <= 1e-12 * np.linalg.norm(ref)
