@@ -345,8 +345,11 @@ def run_sparse(args, torch, dev, ob, steps, warmup, with_cpu):
         hb = []
         for s in range(args.e2e_steps + 1):
             ii, jj, kk, vv = syn.batch()
-            idx = np.stack([ii.cpu().numpy(), jj.cpu().numpy(), kk.cpu().numpy()], 1)
-            hb.append((ob.SparseTensor((I, J, t), idx, vv.cpu().numpy()), [r.random((t, Q)) for _ in range(P)]))
+            # pinned host arrays (the COO entries as a loader would hand them over)
+            pin = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True).copy_(x) for x in (ii, jj, kk, vv)]
+            sp = ob.SparseTensor.from_arrays((I, J, t), *[x.numpy() for x in pin])
+            sp._keep = pin
+            hb.append((sp, [r.random((t, Q)) for _ in range(P)]))
         hs.compress(*hb[0])
         hs.cp_als(cfg, seeds)
         torch.cuda.synchronize()

@@ -525,6 +525,19 @@ class SparseTensor:
         if self.values.shape != (idx.shape[0],):
             raise ConfigError("SparseTensor: values do not match indices")
 
+    @staticmethod
+    def from_arrays(shape, i: np.ndarray, j: np.ndarray, k: np.ndarray, values: np.ndarray) -> "SparseTensor":
+        """Wrap existing SoA arrays without copying (contiguous int32 i, j, k
+        and float32 values; e.g. numpy views of pinned torch CPU tensors, so
+        the device copy runs at full PCIe speed)."""
+        sp = SparseTensor.__new__(SparseTensor)
+        sp.shape = tuple(int(d) for d in shape)
+        for a, dt in ((i, np.int32), (j, np.int32), (k, np.int32), (values, np.float32)):
+            if a.dtype != dt or a.ndim != 1 or not a.flags.c_contiguous or a.shape[0] != values.shape[0]:
+                raise ConfigError("SparseTensor.from_arrays: contiguous int32 i, j, k and float32 values of one length")
+        sp.i, sp.j, sp.k, sp.values = i, j, k, values
+        return sp
+
     @property
     def nnz(self) -> int:
         return int(self.values.shape[0])
