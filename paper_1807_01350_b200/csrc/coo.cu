@@ -99,8 +99,9 @@ __global__ void coo_scan_kernel(const unsigned long long* __restrict__ keys, con
 // entries are consumed in rounds of <= kChunkE entries / kChunkG groups:
 //   phase A' Us[g][c] = U(i_g, c)            (cp.async, overlapping phase A)
 //   phase A  Rs[g][c] = sum_{e in g} v_e V(j_e, c)   (float4 gathers; NS thread
-//            sets each take the whole groups of a contiguous share of the
-//            round's entries: one writer per group, fixed summation order)
+//            sets each take an equal contiguous share of the round's entries;
+//            partial sums of groups split across sets are added afterwards in
+//            set order: fixed summation order)
 //   phase B  acc += Us[g][rows]^T Rs[g][cols] over the round's groups
 // A group split across two rounds is simply two groups (the sum is linear).
 template <int QP, int TM>
@@ -121,7 +122,8 @@ __global__ void __launch_bounds__(256) coo_slice_kernel(const int4* __restrict__
     float* Us = sm + kChunkG * NC;      // [kChunkG][NC]
     __shared__ int s_j[kChunkE], s_g[kChunkE], s_gi[kChunkG], s_gs[kChunkG];
     __shared__ float s_v[kChunkE];
-    __shared__ int s_wsum[8], s_nused;
+    __shared__ int s_wsum[8], s_nused, s_cg[8];
+    __shared__ float4 s_carry[256];  // NS x NQ continuation partial sums
 
     const int k = blockIdx.x, p0 = blockIdx.y * RB;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -184,26 +186,25 @@ __global__ void __launch_bounds__(256) coo_slice_kernel(const int4* __restrict__
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         // phase A: thread set s accumulates the V rows (float4 column quad cq)
-        // of the whole groups that start in [nused s / NS, nused (s+1) / NS)
-        // (range ends snapped to group heads): every group has one owner, so
-        // the sums are plain stores in a fixed order (run-to-run
-        // deterministic)
+        // of entries [nused s / NS, nused (s+1) / NS).  A group is stored by
+        // the set in which it starts; a set whose range begins inside a group
+        // (a continuation) leaves that partial sum in carry[s], and the
+        // carries are added in set order after the barrier -- equal work per
+        // set and a fixed summation order (run-to-run deterministic)
+        const int e_lo = nused * sset / NS, e_hi = nused * (sset + 1) / NS;
+        const bool cont = e_lo > 0 && e_lo < e_hi && s_g[e_lo - 1] == s_g[e_lo];
+        if (cq == 0) s_cg[sset] = cont ? s_g[e_lo] : -1;
         if (4 * cq < cols_valid) {
-            auto snap = [&](int x) {  // first group head >= x, else nused
-                int lo = 0, hi = ng;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (s_gs[mid] < x) lo = mid + 1; else hi = mid;
-                }
-                return lo < ng ? s_gs[lo] : nused;
-            };
             const float* vc = V + colbase + 4 * cq;
-            const int e_lo = sset == 0 ? 0 : snap(nused * sset / NS);
-            const int e_hi = sset == NS - 1 ? nused : snap(nused * (sset + 1) / NS);
             float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
             int gc = e_lo < e_hi ? s_g[e_lo] : 0;
+            bool carry = cont;
             auto flush = [&](int g) {
-                *reinterpret_cast<float4*>(Rs + gc * NC + 4 * cq) = a;
+                if (carry)
+                    s_carry[sset * NQ + cq] = a;
+                else
+                    *reinterpret_cast<float4*>(Rs + gc * NC + 4 * cq) = a;
+                carry = false;
                 a = make_float4(0.f, 0.f, 0.f, 0.f);
                 gc = g;
             };
@@ -236,6 +237,23 @@ __global__ void __launch_bounds__(256) coo_slice_kernel(const int4* __restrict__
             if (e_lo < e_hi) flush(gc);
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        // carries, in set order (the owner's store came first)
+        if (sset == 0 && 4 * cq < cols_valid) {
+#pragma unroll
+            for (int s2 = 1; s2 < NS; ++s2) {
+                const int g = s_cg[s2];
+                if (g < 0) continue;
+                float4* r = reinterpret_cast<float4*>(Rs + g * NC + 4 * cq);
+                const float4 c = s_carry[s2 * NQ + cq];
+                float4 v = *r;
+                v.x += c.x;
+                v.y += c.y;
+                v.z += c.z;
+                v.w += c.w;
+                *r = v;
+            }
+        }
         __syncthreads();
 
         // phase B: rank-1 updates of the replica's Q x Q slice matrix.  Thread
