@@ -42,7 +42,7 @@ namespace octen {
 namespace {
 
 constexpr int kChunkE = 256;  // entries staged per round of a slice CTA
-constexpr int kChunkG = 32;   // distinct rows i (groups) per round
+constexpr int kChunkG = 48;   // distinct rows i (groups) per round
 
 __global__ void coo_keys_kernel(const int* __restrict__ ci, const int* __restrict__ cj, const int* __restrict__ ck,
                                 const float* __restrict__ cv, long long nnz, int I, int J, int t,
