@@ -410,6 +410,7 @@ def main():
     ap.add_argument("--impl", default="octen", choices=["octen", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + ["c4"])
     ap.add_argument("--noise", type=float, default=0.01, help="Gaussian noise sigma relative to the clean RMS")
+    ap.add_argument("--als-iters", type=int, default=0, help="override the config's CP-ALS max_iters")
     ap.add_argument("--no-sparse", action="store_true", help="skip the c4 sparse leg of the default line")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -419,7 +420,9 @@ def main():
                          "'temporal': the same with the compression sharded over the batch's slices "
                          "(NCCL reduce-scatter of the partial summaries); or N independent streams (weak scaling)")
     args = ap.parse_args()
-    cfg = CONFIGS.get(args.config, C4)
+    cfg = dict(CONFIGS.get(args.config, C4))
+    if args.als_iters > 0:
+        cfg["iters"] = args.als_iters
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
