@@ -571,18 +571,23 @@ def main():
     g1_flops = dt[4] / max(dt[5], 1)
     achieved = g1_flops / (g1_ms * 1e-3) / 1e12 if g1_ms > 0 else 0.0
     traffic = None
+    pipe_pct = None
     try:  # dram read+write bytes per GEMM1 launch from the committed ncu --set full capture (c3)
         with open(os.path.join(ROOT, "profiles", "r1_roofline.json")) as f:
             rj = json.load(f)
         if args.config == "c3":
             traffic = rj["traffic_bytes_per_launch"]
+            pipe_pct = rj.get("tensor_pipe_active_pct")
     except Exception:
         traffic = None
     roofline = {"kernel": "compression mode-1 contraction (GEMM1)", "bound": "tensor", "achieved": achieved,
                 "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak, "traffic": traffic,
                 "traffic_unit": "bytes/launch (ncu dram__bytes_read+write, profiles/r1_roofline.json)",
                 "peak_source": "%s bf16 %.1f TF/s / 2 (dense TF32)" % (peak_kind, bf16),
-                "flops_per_launch": g1_flops, "ms_per_launch": g1_ms}
+                "flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
+                "issued_tflops": 3.0 * achieved, "issued_frac": 3.0 * achieved / tf32_peak,
+                "issued_note": "split-TF32: 3 tcgen05 MMAs (hi*hi, hi*lo, lo*hi) per useful product",
+                "tensor_pipe_active_pct_ncu": pipe_pct}
     stage = {"compress_ms": dt[0] / args.steps, "als_ms": dt[1] / args.steps, "merge_ms": dt[2] / args.steps,
              "gemm1_ms": dt[3] / args.steps, "init_s": t_init}
 
