@@ -16,6 +16,7 @@
 // it onto Eigen::Map without copies.
 #pragma once
 
+#include <climits>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -245,5 +246,79 @@ inline void ingest_batch_f32(StreamState& st, const std::vector<std::int64_t>& d
     check(octen_stream_ingest(st.handle.get(), data, OCTEN_F32, OCTEN_HOST, (int)dims.size(), dims.data()));
     detail::refresh(st);
 }
+
+// ---- sparse (COO) batches: proj/include/cpstream/tensor.hpp:66-90 ----
+// The reference validates entries in the SparseTensor constructor and
+// densifies before compress; here the entries go to the device as they are
+// (octen_coo_*), validated there with the same errors and messages.
+struct SparseTensor {
+    struct Entry {
+        std::vector<std::int64_t> index;
+        double value = 0.0;
+    };
+    std::vector<std::int64_t> dims;
+    std::vector<Entry> entries;
+    SparseTensor() = default;
+    SparseTensor(std::vector<std::int64_t> d, std::vector<Entry> e) : dims(std::move(d)), entries(std::move(e)) {}
+    std::int64_t nnz() const { return (std::int64_t)entries.size(); }
+};
+
+// Device-resident SummaryState fed by COO batches (compression.hpp:56-60):
+// compress() is update_summaries(compress(batch.to_dense())) for every replica.
+class CooSummaries {
+public:
+    // u[r]: I x Q, v[r]: J x Q (column-major) per replica
+    CooSummaries(const std::vector<Matrix>& u, const std::vector<Matrix>& v, int device = 0)
+        : p_((int)u.size()), q_(u.empty() ? 0 : (int)u[0].cols()) {
+        if (u.empty() || u.size() != v.size()) throw ConfigError("CooSummaries: replica count mismatch");
+        i_ = u[0].rows();
+        j_ = v[0].rows();
+        std::vector<double> U, V;
+        for (const Matrix& m : u) U.insert(U.end(), m.v.begin(), m.v.end());
+        for (const Matrix& m : v) V.insert(V.end(), m.v.begin(), m.v.end());
+        octen_coo_summaries* raw = nullptr;
+        check(octen_coo_create(p_, q_, i_, j_, U.data(), V.data(), device, &raw));
+        h_ = std::shared_ptr<octen_coo_summaries>(raw, octen_coo_destroy);
+    }
+    // w[r]: t x Q temporal rows of this batch per replica
+    void compress(const SparseTensor& batch, const std::vector<Matrix>& w) {
+        if (batch.dims.size() != 3) throw ConfigError("compress: tensor order mismatch");
+        if (batch.dims[0] != i_ || batch.dims[1] != j_) throw ConfigError("compress: extent mismatch on mode 1");
+        const std::int64_t t = batch.dims[2], n = batch.nnz();
+        std::vector<std::int32_t> ii((size_t)n), jj((size_t)n), kk((size_t)n);
+        std::vector<float> vals((size_t)n);
+        for (std::int64_t e = 0; e < n; ++e) {
+            const auto& en = batch.entries[(size_t)e];
+            if (en.index.size() != 3) throw ConfigError("SparseTensor: index arity mismatch");
+            auto narrow = [](std::int64_t x) {  // out-of-range values stay out of range
+                return (std::int32_t)(x < INT32_MIN ? INT32_MIN : x > INT32_MAX ? INT32_MAX : x);
+            };
+            ii[(size_t)e] = narrow(en.index[0]);
+            jj[(size_t)e] = narrow(en.index[1]);
+            kk[(size_t)e] = narrow(en.index[2]);
+            vals[(size_t)e] = (float)en.value;
+        }
+        std::vector<double> W;
+        for (const Matrix& m : w) W.insert(W.end(), m.v.begin(), m.v.end());
+        if ((std::int64_t)W.size() != (std::int64_t)p_ * t * q_) throw ConfigError("compress: temporal rows mismatch");
+        check(octen_coo_compress(h_.get(), t, W.data(), n, ii.data(), jj.data(), kk.data(), vals.data(), OCTEN_HOST));
+    }
+    // summaries: p tensors Q x Q x Q
+    std::vector<DenseTensor> summaries() const {
+        const size_t q3 = (size_t)q_ * q_ * q_;
+        std::vector<double> y((size_t)p_ * q3);
+        check(octen_coo_get_summaries(h_.get(), y.data()));
+        std::vector<DenseTensor> out;
+        for (int r = 0; r < p_; ++r)
+            out.emplace_back(std::vector<std::int64_t>{q_, q_, q_},
+                             std::vector<double>(y.begin() + (std::ptrdiff_t)(r * q3), y.begin() + (std::ptrdiff_t)((r + 1) * q3)));
+        return out;
+    }
+
+private:
+    int p_ = 0, q_ = 0;
+    std::int64_t i_ = 0, j_ = 0;
+    std::shared_ptr<octen_coo_summaries> h_;
+};
 
 }  // namespace cpstream_b200

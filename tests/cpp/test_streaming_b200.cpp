@@ -205,6 +205,65 @@ int main() {
         ingest_batch(st, slice_last(full, 4, 4));
         CHECK(st.slices_seen == 8);
     }
+    // sparse batches (tensor.hpp:66-90, tensor.cpp:87-122): the device COO
+    // compression equals compress(to_dense(batch)) done with the dense path,
+    // and the SparseTensor errors keep their reference text
+    {
+        const std::int64_t I = 14, J = 11, t = 5, Q = 4;
+        std::vector<Matrix> u, v, w;
+        std::uint64_t s = 99;
+        auto uni = [&s] {
+            s = s * 6364136223846793005ULL + 1442695040888963407ULL;
+            return (double)(s >> 11) * 0x1.0p-53;
+        };
+        for (int r = 0; r < 2; ++r) {
+            Matrix a(I, Q), b(J, Q), c(t, Q);
+            for (double& x : a.v) x = uni();
+            for (double& x : b.v) x = uni();
+            for (double& x : c.v) x = uni();
+            u.push_back(a);
+            v.push_back(b);
+            w.push_back(c);
+        }
+        SparseTensor sp({I, J, t}, {});
+        DenseTensor dense = DenseTensor::zeros({I, J, t});
+        for (std::int64_t k = 0; k < t; ++k)
+            for (std::int64_t i = 0; i < I; i += 3)
+                for (std::int64_t j = (i + k) % 2; j < J; j += 2) {
+                    const float val = (float)uni();
+                    sp.entries.push_back({{i, j, k}, (double)val});
+                    dense.data[(size_t)(i + I * j + I * J * k)] = (double)val;
+                }
+        CooSummaries cs(u, v);
+        cs.compress(sp, w);
+        const std::vector<DenseTensor> ys = cs.summaries();
+        // the same contraction by triple loops (compression.cpp:108-130 on to_dense)
+        double err = 0.0, nrm = 0.0;
+        for (int r = 0; r < 2; ++r)
+            for (std::int64_t a = 0; a < Q; ++a)
+                for (std::int64_t b = 0; b < Q; ++b)
+                    for (std::int64_t c = 0; c < Q; ++c) {
+                        double z = 0.0;
+                        for (std::int64_t k = 0; k < t; ++k)
+                            for (std::int64_t j = 0; j < J; ++j)
+                                for (std::int64_t i = 0; i < I; ++i)
+                                    z += dense.data[(size_t)(i + I * j + I * J * k)] * u[r](i, a) * v[r](j, b) *
+                                         w[r](k, c);
+                        const double y = ys[(size_t)r].data[(size_t)(a + Q * b + Q * Q * c)];
+                        err += (y - z) * (y - z);
+                        nrm += z * z;
+                    }
+        CHECK(std::sqrt(err / nrm) < 1e-5);
+        SparseTensor oob({I, J, t}, {{{0, 0, 0}, 1.0}, {{I, 0, 0}, 1.0}});
+        CHECK(throws_as<ConfigError>([&] { cs.compress(oob, w); }, "SparseTensor: index out of bounds"));
+        SparseTensor dup({I, J, t}, {{{1, 2, 3}, 1.0}, {{1, 2, 3}, 2.0}});
+        CHECK(throws_as<ConfigError>([&] { cs.compress(dup, w); }, "SparseTensor: duplicate index"));
+        SparseTensor nan({I, J, t}, {{{1, 2, 3}, std::nan("")}});
+        CHECK(throws_as<NumericError>([&] { cs.compress(nan, w); }, "SparseTensor: non-finite value"));
+        // a rejected batch leaves the summaries as they were
+        const std::vector<DenseTensor> again = cs.summaries();
+        CHECK(again[0].data == ys[0].data && again[1].data == ys[1].data);
+    }
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
