@@ -156,6 +156,11 @@ def _batch_args(batch):
         else:
             raise ConfigError("octen: batch dtype must be float32 or float64")
         loc = C.OCTEN_DEVICE if batch.is_cuda else C.OCTEN_HOST
+        if batch.is_cuda:
+            # the library works on its own CUDA streams: work queued on
+            # torch's current stream (e.g. the kernels producing this batch)
+            # must be complete before the batch is read
+            torch.cuda.current_stream(batch.device).synchronize()
         return batch, ctypes.c_void_p(batch.data_ptr()), dt, loc, dims
     a = np.asarray(batch)
     if a.dtype == np.float32:
@@ -592,6 +597,8 @@ class CooSummaries:
         """Device-resident inputs (torch CUDA tensors): w float64 (p, Q, t)
         contiguous = per replica t x Q column-major; i, j, k int32; values
         float32."""
+        import torch
+        torch.cuda.current_stream(values.device).synchronize()  # producers on torch's stream
         _check(C.LIB.octen_coo_compress(self._h, int(t), w.data_ptr(), int(values.numel()), i.data_ptr(),
                                         j.data_ptr(), k.data_ptr(), values.data_ptr(), C.OCTEN_DEVICE))
 
