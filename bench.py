@@ -412,7 +412,7 @@ def main():
     ap.add_argument("--noise", type=float, default=0.01, help="Gaussian noise sigma relative to the clean RMS")
     ap.add_argument("--als-iters", type=int, default=0, help="override the config's CP-ALS max_iters")
     ap.add_argument("--no-sparse", action="store_true", help="skip the c4 sparse leg of the default line")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--multi", default="sharded", choices=["sharded", "temporal", "replicas"],
@@ -522,8 +522,8 @@ def main():
     e2e = None
     if args.e2e_steps > 0:
         hb = []
-        # pinned host batches: at most ~4 GB of them
-        e2e_steps = max(2, min(args.e2e_steps, int(4e9 // (entries * 4)) - 2))
+        # pinned host batches: at most ~8 GB of them
+        e2e_steps = max(2, min(args.e2e_steps, int(8e9 // (entries * 4)) - 2))
         for i in range(e2e_steps + 2):  # +2: untimed warm-up of the host-input path
             d = syn.batch(K0 + (args.warmup + args.steps + i) * t, t)
             h = torch.empty((t, J, I), dtype=torch.float32, pin_memory=True)
