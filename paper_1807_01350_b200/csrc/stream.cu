@@ -8,6 +8,7 @@
 // device.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include <chrono>
@@ -317,6 +318,15 @@ void Stream::prepare(int order, const std::int64_t* dims) {
 
 // ---- phase 1: stage, compress and decompose the owned replicas ----
 namespace {
+// CTAs of the background pull (OCTEN_PULL_CTAS, diagnostics; default 8)
+int pull_ctas() {
+    static const int n = [] {
+        const char* e = std::getenv("OCTEN_PULL_CTAS");
+        return e ? std::max(1, std::atoi(e)) : 8;
+    }();
+    return n;
+}
+
 __global__ void __launch_bounds__(256) h2d_pull_kernel(int4* __restrict__ dst, const int4* __restrict__ src,
                                                        long long n16) {
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -388,7 +398,7 @@ void Stream::prefetch(const void* data, int dtype, int order, const std::int64_t
         const std::int64_t k0 = c * f.sub, kc = std::min(f.sub, t - k0);
         const size_t off = plane * k0 * esz, bytes = plane * kc * esz;
         if (mapped && (((uintptr_t)mapped + off) % 16) == 0 && (((uintptr_t)dst + off) % 16) == 0 && bytes % 16 == 0) {
-            h2d_pull_kernel<<<8, 256, 0, pcp>>>((int4*)((char*)dst + off), (const int4*)((const char*)mapped + off),
+            h2d_pull_kernel<<<pull_ctas(), 256, 0, pcp>>>((int4*)((char*)dst + off), (const int4*)((const char*)mapped + off),
                                                  (long long)(bytes / 16));
             OCTEN_LAUNCHED(1);
         } else {
