@@ -105,6 +105,13 @@ int octen_stream_ingest(octen_stream* s, const void* data, int dtype, int locati
  * is synchronous and has no prefetch, streaming.hpp:70.) */
 int octen_stream_prefetch(octen_stream* s, const void* data, int dtype, int order, const int64_t* dims);
 
+/* Fitness (proj/src/eval.cpp:10-20, 100 (1 - |X - Xhat| / |X|)) of the
+ * stream's current model on slices [k0, k0 + t) of the stream, given as a
+ * batch I x J x t (dtype/location as octen_stream_ingest); computed on the
+ * device without materialising the reconstruction. */
+int octen_stream_batch_fitness(octen_stream* s, const void* data, int dtype, int location, int order,
+                               const int64_t* dims, int64_t k0, double* fitness);
+
 void octen_stream_destroy(octen_stream* s);
 
 /* Stream state accessors (StreamState, streaming.hpp:48-59).

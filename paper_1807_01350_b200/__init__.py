@@ -249,6 +249,16 @@ class StreamState:
         ka = getattr(self, "_pf_keep", [])
         self._pf_keep = (ka + [keep])[-3:]  # the copies read these buffers until ingested
 
+    def batch_fitness(self, batch, k0: int) -> float:
+        """eval.cpp:10-20 fitness of the current model on slices [k0, k0 + t)
+        of the stream, given as a batch (computed on the device)."""
+        keep, ptr, dt, loc, dims = _batch_args(batch)
+        d = (C.c_i64 * len(dims))(*dims)
+        out = ctypes.c_double()
+        _check(C.LIB.octen_stream_batch_fitness(self._h, ptr, dt, loc, len(dims), d, int(k0), ctypes.byref(out)))
+        del keep
+        return out.value
+
     def replica_models(self) -> List[KruskalModel]:
         info = self._info()
         rank, p, q = info[4], info[5], info[6]

@@ -159,6 +159,16 @@ int octen_stream_ingest(octen_stream* s, const void* data, int dtype, int locati
     });
 }
 
+int octen_stream_batch_fitness(octen_stream* s, const void* data, int dtype, int location, int order,
+                               const int64_t* dims, int64_t k0, double* fitness) {
+    return guard([&] {
+        if (!s || !data || !dims || !fitness) throw octen::ConfigError("octen_stream_batch_fitness: null argument");
+        check_dtype(dtype, location);
+        OCTEN_CUDA(cudaSetDevice(s->s->cfg.device));
+        *fitness = s->s->batch_fitness(data, dtype, location, order, dims, k0);
+    });
+}
+
 int octen_stream_partial_block_size(const octen_stream* s, int64_t* n) {
     return guard([&] {
         if (!s || !n) throw octen::ConfigError("octen_stream_partial_block_size: null argument");

@@ -858,6 +858,110 @@ void Stream::accumulate_stage_times() {
     gemm1_launches = comp.gemm1_launches;
 }
 
+namespace {
+// fitness support (eval.cpp:10-20 without materialising the reconstruction)
+template <typename T>
+struct FitXA {  // A(0, i, n) = X[i + I n]   (X_(1), n = j + J k)
+    const T* X;
+    long long I;
+    __device__ double operator()(int, int i, int n) const { return (double)X[(size_t)i + (size_t)I * n]; }
+};
+struct FitKrB {  // B(0, n, r) = B(j, r) C(k0 + k, r),  n = j + J k
+    const double* B;
+    const double* C;
+    long long J, ldc, k0;
+    __device__ double operator()(int, int n, int r) const {
+        const long long k = n / J, j = n - k * J;
+        return B[j + J * r] * C[(k0 + k) + ldc * r];
+    }
+};
+struct FitWC {  // W(i, r)
+    double* W;
+    long long I;
+    __device__ void operator()(int, int i, int r, double v) const { W[(size_t)i + (size_t)I * r] = v; }
+};
+template <typename T>
+__global__ void sumsq_kernel(const T* __restrict__ x, size_t n, double* out) {
+    double acc = 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const double v = (double)x[i];
+        acc += v * v;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sacc = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sacc += part[w];
+        out[blockIdx.x] = sacc;  // per-block partials, summed in block order on the host
+    }
+}
+}  // namespace
+
+// Fitness of the current model on t slices X (I x J x t, first index fastest)
+// that are the model's temporal rows [k0, k0 + t): eval.cpp:10-20,
+//   100 (1 - |X - Xhat| / |X|),  |X - Xhat|^2 = |X|^2 - 2 <X, Xhat> + |Xhat|^2,
+// with <X, Xhat> = sum_r lambda_r a_r^T X_(1) (c_r (x) b_r) as one GEMM
+// (X_(1) against the Khatri-Rao rows, formed on the fly) and |Xhat|^2 from
+// the R x R Grams.  The reconstruction is never materialised.
+double Stream::batch_fitness(const void* data, int dtype, int location, int order, const std::int64_t* dims,
+                             std::int64_t k0) {
+    if (!initialized) throw ConfigError("octen: stream is not initialised");
+    if (order != 3 || dims[0] != I || dims[1] != J) throw ConfigError("fitness: extent mismatch");
+    const std::int64_t t = dims[2];
+    if (t < 1 || k0 < 0 || k0 + t > K) throw ConfigError("fitness: slice range outside the model");
+    const int R = cfg.rank;
+    const size_t n = (size_t)I * J * t;
+    const void* dX = stage_input(data, dtype, location, n);
+    const int nb = (int)std::min<size_t>(148 * 4, (n + 255) / 256);
+    DevBuf<double> part, W;
+    part.reserve((size_t)nb);
+    W.reserve((size_t)I * R);
+    const long long Jt = (long long)J * t;
+    const int ks = pick_ksplit(1, (int)I, R, (int)std::min<long long>(Jt, 1 << 30));
+    DevBuf<double> wsp;
+    if (ks > 1) wsp.reserve((size_t)ks * I * R);
+    if (dtype == 1) {
+        sumsq_kernel<float><<<nb, 256, 0, st>>>((const float*)dX, n, part.p);
+        gemm_f64<false, false>(1, (int)I, R, (int)Jt, FitXA<float>{(const float*)dX, I},
+                               FitKrB{B.p, C.p, J, capC, k0}, FitWC{W.p, I}, st, ks, ks > 1 ? wsp.p : nullptr);
+    } else {
+        sumsq_kernel<double><<<nb, 256, 0, st>>>((const double*)dX, n, part.p);
+        gemm_f64<false, false>(1, (int)I, R, (int)Jt, FitXA<double>{(const double*)dX, I},
+                               FitKrB{B.p, C.p, J, capC, k0}, FitWC{W.p, I}, st, ks, ks > 1 ? wsp.p : nullptr);
+    }
+    OCTEN_LAUNCHED(1);
+    OCTEN_CUDA(cudaGetLastError());
+    std::vector<double> hp = part.to_host((size_t)nb, st);
+    std::vector<double> hW = W.to_host((size_t)I * R, st);
+    std::vector<double> hA = A.to_host((size_t)I * R, st), hB = B.to_host((size_t)J * R, st);
+    std::vector<double> hC((size_t)t * R), hl = lam.to_host((size_t)R, st);
+    OCTEN_CUDA(cudaMemcpy2DAsync(hC.data(), t * sizeof(double), C.p + k0, capC * sizeof(double), t * sizeof(double), R,
+                                 cudaMemcpyDeviceToHost, st));
+    OCTEN_CUDA(cudaStreamSynchronize(st));
+    double nx2 = 0.0;
+    for (double v : hp) nx2 += v;
+    double inner = 0.0;
+    for (int r = 0; r < R; ++r) {
+        double sacc = 0.0;
+        for (std::int64_t i = 0; i < I; ++i) sacc += hA[(size_t)i + (size_t)I * r] * hW[(size_t)i + (size_t)I * r];
+        inner += hl[(size_t)r] * sacc;
+    }
+    auto gram = [&](const std::vector<double>& f, std::int64_t rows, int a, int b) {
+        double g = 0.0;
+        for (std::int64_t i = 0; i < rows; ++i) g += f[(size_t)i + (size_t)rows * a] * f[(size_t)i + (size_t)rows * b];
+        return g;
+    };
+    double nh2 = 0.0;
+    for (int a = 0; a < R; ++a)
+        for (int b = 0; b < R; ++b)
+            nh2 += hl[(size_t)a] * hl[(size_t)b] * gram(hA, I, a, b) * gram(hB, J, a, b) * gram(hC, t, a, b);
+    const double res2 = std::max(0.0, nx2 - 2.0 * inner + nh2);
+    if (!(nx2 > 0.0)) return res2 == 0.0 ? 100.0 : -INFINITY;
+    return 100.0 * (1.0 - std::sqrt(res2) / std::sqrt(nx2));
+}
+
 void Stream::get_factor(int mode, double* out) {
     const int R = cfg.rank;
     if (mode == 0)

@@ -55,6 +55,9 @@ public:
     void init(const void* data, int dtype, int location, int order, const std::int64_t* dims);
     void ingest(const void* data, int dtype, int location, int order, const std::int64_t* dims);
     void get_factor(int mode, double* out);
+    // eval.cpp:10-20 fitness of the model on slices [k0, k0 + t) given as a batch
+    double batch_fitness(const void* data, int dtype, int location, int order, const std::int64_t* dims,
+                         std::int64_t k0);
     // Start the host->device copy of a later batch (host, pinned for overlap)
     // on a copy stream, so it overlaps the device work of the batches before
     // it.  A later begin/ingest whose data pointer, dtype and extents match
