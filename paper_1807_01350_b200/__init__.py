@@ -202,13 +202,10 @@ class StreamState:
     def model(self) -> KruskalModel:
         info = self._info()
         dims, rank = info[1:4], info[4]
-        factors = []
-        for m in range(3):
-            f = np.zeros((dims[m], rank), order="F")
-            _check(C.LIB.octen_stream_get_factor(self._h, m, _dptr(f)))
-            factors.append(f)
+        factors = [np.zeros((dims[m], rank), order="F") for m in range(3)]
         lam = np.zeros(rank)
-        _check(C.LIB.octen_stream_get_lambda(self._h, _dptr(lam)))
+        _check(C.LIB.octen_stream_get_model(self._h, _dptr(factors[0]), _dptr(factors[1]), _dptr(factors[2]),
+                                            _dptr(lam)))
         return KruskalModel(factors, lam)
 
     @property

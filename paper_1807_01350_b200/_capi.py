@@ -77,6 +77,7 @@ SIGNATURES = {
     "octen_stream_info": (ctypes.c_int, [ctypes.c_void_p, P_i64]),
     "octen_stream_get_factor": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, P_dbl]),
     "octen_stream_get_lambda": (ctypes.c_int, [ctypes.c_void_p, P_dbl]),
+    "octen_stream_get_model": (ctypes.c_int, [ctypes.c_void_p, P_dbl, P_dbl, P_dbl, P_dbl]),
     "octen_stream_get_record": (ctypes.c_int, [ctypes.c_void_p, c_i64, ctypes.POINTER(BatchRecordC)]),
     "octen_stream_get_summaries": (ctypes.c_int, [ctypes.c_void_p, P_dbl]),
     "octen_stream_get_history": (ctypes.c_int, [ctypes.c_void_p, P_dbl]),

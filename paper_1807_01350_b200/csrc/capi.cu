@@ -269,6 +269,19 @@ int octen_stream_get_factor(const octen_stream* s, int mode, double* out) {
     return guard([&] { s->s->get_factor(mode, out); });
 }
 
+int octen_stream_get_model(const octen_stream* s, double* a, double* b, double* c, double* lambda) {
+    return guard([&] {
+        auto& x = *s->s;
+        const int R = x.cfg.rank;
+        OCTEN_CUDA(cudaMemcpyAsync(a, x.A.p, sizeof(double) * x.I * R, cudaMemcpyDeviceToHost, x.st));
+        OCTEN_CUDA(cudaMemcpyAsync(b, x.B.p, sizeof(double) * x.J * R, cudaMemcpyDeviceToHost, x.st));
+        OCTEN_CUDA(cudaMemcpy2DAsync(c, x.K * sizeof(double), x.C.p, x.capC * sizeof(double), x.K * sizeof(double), R,
+                                     cudaMemcpyDeviceToHost, x.st));
+        x.lam.download(lambda, R, x.st);
+        OCTEN_CUDA(cudaStreamSynchronize(x.st));
+    });
+}
+
 int octen_stream_get_lambda(const octen_stream* s, double* out) {
     return guard([&] {
         auto& x = *s->s;
