@@ -109,6 +109,12 @@ int octen_stream_prefetch(octen_stream* s, const void* data, int dtype, int orde
  * stream's current model on slices [k0, k0 + t) of the stream, given as a
  * batch I x J x t (dtype/location as octen_stream_ingest); computed on the
  * device without materialising the reconstruction. */
+/* congruence (proj/src/eval.cpp:22-46): per-component factor match score
+ * (product over modes of |cos|) after exhaustive (rank <= 6) or greedy
+ * matching.  ground/est: factors of every mode stacked, dims[n] x rank
+ * col-major each; scores: rank.  Host computation. */
+int octen_congruence(int order, int rank, const int64_t* dims, const double* ground, const double* est,
+                     double* scores);
 int octen_stream_batch_fitness(octen_stream* s, const void* data, int dtype, int location, int order,
                                const int64_t* dims, int64_t k0, double* fitness);
 

@@ -24,7 +24,7 @@ from . import sharding as _sharding
 __all__ = ["ConfigError", "NumericError", "IoError", "CudaError", "AlsConfig", "StreamConfig", "BatchRecord",
            "KruskalModel", "StreamState", "init_stream", "ingest_batch", "compress", "cp_als_batched",
            "align_replicas", "recover_nontemporal", "temporal_stack_from_summaries", "recover_temporal_append",
-           "SparseTensor", "CooSummaries", "compress_coo", "version"]
+           "SparseTensor", "CooSummaries", "compress_coo", "congruence", "version"]
 
 
 class Error(RuntimeError):
@@ -661,3 +661,20 @@ def compress_coo(batch: SparseTensor, u: List[np.ndarray], v: List[np.ndarray], 
     _check(C.LIB.octen_compress_coo(p, q, I, J, t, _dptr(U), _dptr(V), _dptr(W), batch.nnz, batch.i.ctypes.data,
                                     batch.j.ctypes.data, batch.k.ctypes.data, batch.values.ctypes.data, _dptr(z)))
     return [z[r * q ** 3:(r + 1) * q ** 3].reshape((q, q, q), order="F") for r in range(p)]
+
+
+def congruence(ground: KruskalModel, est: KruskalModel) -> List[float]:
+    """eval.cpp:22-46 per-component congruence (factor match score) after
+    exhaustive (rank <= 6) or greedy matching (octen_congruence)."""
+    r = len(np.asarray(ground.lambda_))
+    if len(np.asarray(est.lambda_)) != r or len(ground.factors) != len(est.factors):
+        raise ConfigError("congruence: rank mismatch")
+    dims = [np.asarray(f).shape[0] for f in ground.factors]
+    if [np.asarray(f).shape[0] for f in est.factors] != dims:
+        raise ConfigError("congruence: factor shape mismatch")
+    g = np.concatenate([_f64(f).ravel(order="F") for f in ground.factors])
+    e = np.concatenate([_f64(f).ravel(order="F") for f in est.factors])
+    out = np.zeros(r)
+    d = (C.c_i64 * len(dims))(*dims)
+    _check(C.LIB.octen_congruence(len(dims), r, d, _dptr(g), _dptr(e), _dptr(out)))
+    return out.tolist()

@@ -60,6 +60,7 @@ SIGNATURES = {
     "octen_stream_ingest": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, P_i64]),
     "octen_stream_destroy": (None, [ctypes.c_void_p]),
+    "octen_congruence": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P_i64, P_dbl, P_dbl, P_dbl]),
     "octen_stream_batch_fitness": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                   ctypes.c_int, P_i64, c_i64, P_dbl]),
     "octen_stream_partial_block_size": (ctypes.c_int, [ctypes.c_void_p, P_i64]),

@@ -2,6 +2,8 @@
 // message carrying the reference's error text.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -156,6 +158,61 @@ int octen_stream_ingest(octen_stream* s, const void* data, int dtype, int locati
         if (!s || !data || !dims) throw octen::ConfigError("octen_stream_ingest: null argument");
         check_dtype(dtype, location);
         s->s->ingest(data, dtype, location, order, dims);
+    });
+}
+
+int octen_congruence(int order, int rank, const int64_t* dims, const double* ground, const double* est,
+                     double* scores) {
+    // eval.cpp:22-46: per-component product over modes of |cos| between the
+    // normalised columns, matched exhaustively (rank <= 6) or greedily
+    // (recovery.cpp:42-104).  Host-side evaluation (no device work).
+    return guard([&] {
+        if (order < 1 || rank < 1 || !dims || !ground || !est || !scores)
+            throw octen::ConfigError("congruence: bad arguments");
+        const int r = rank;
+        std::vector<double> sim((size_t)r * r, 1.0);
+        size_t off = 0;
+        for (int n = 0; n < order; ++n) {
+            const int64_t d = dims[n];
+            const double* g = ground + off;
+            const double* e = est + off;
+            off += (size_t)d * r;
+            std::vector<double> gn(r, 0.0), en(r, 0.0);
+            for (int c = 0; c < r; ++c) {
+                for (int64_t i = 0; i < d; ++i) {
+                    gn[c] += g[i + d * c] * g[i + d * c];
+                    en[c] += e[i + d * c] * e[i + d * c];
+                }
+                gn[c] = std::sqrt(gn[c]);
+                en[c] = std::sqrt(en[c]);
+            }
+            for (int a = 0; a < r; ++a)
+                for (int b = 0; b < r; ++b) {
+                    double sacc = 0.0;
+                    for (int64_t i = 0; i < d; ++i)
+                        sacc += (gn[a] > 0.0 ? g[i + d * a] / gn[a] : g[i + d * a]) *
+                                (en[b] > 0.0 ? e[i + d * b] / en[b] : e[i + d * b]);
+                    sim[(size_t)a + (size_t)r * b] *= std::fabs(sacc);
+                }
+        }
+        std::vector<int> perm(r);
+        if (r <= 6) {
+            std::vector<int> cand(r);
+            for (int i = 0; i < r; ++i) cand[i] = i;
+            double best = -INFINITY;
+            do {
+                double tot = 0.0;
+                for (int i = 0; i < r; ++i) tot += sim[(size_t)i + (size_t)r * cand[i]];
+                if (tot > best) {
+                    best = tot;
+                    perm = cand;
+                }
+            } while (std::next_permutation(cand.begin(), cand.end()));
+        } else {
+            std::vector<unsigned char> ua(r), ub(r);
+            octen::greedy_match(r, sim.data(), r, 1e-9, perm.data(), ua.data(), ub.data());
+        }
+        for (int i = 0; i < r; ++i) scores[i] = sim[(size_t)i + (size_t)r * perm[i]];
     });
 }
 

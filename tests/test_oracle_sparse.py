@@ -67,3 +67,18 @@ def test_python_sparse_tensor_host_checks():
         ob.SparseTensor((2, 2, 2), [[0, 0, 0]], [1.0, 2.0])
     sp = ob.SparseTensor((2, 2, 2), [], [])
     assert sp.nnz == 0 and sp.i.dtype == np.int32
+
+
+@pytest.mark.parametrize("rank", [3, 6, 9])
+def test_congruence_host_abi_matches_oracle(rank):
+    # eval.cpp:22-46 through the C-ABI's host evaluation (no GPU needed)
+    import paper_1807_01350_b200 as ob
+    r = np.random.default_rng(rank)
+    dims = (20, 15, 12)
+    g = O.KruskalModel([r.random((d, rank)) for d in dims], np.ones(rank))
+    perm = r.permutation(rank)
+    e = O.KruskalModel([f[:, perm] * (1 + 0.05 * r.standard_normal(f[:, perm].shape)) for f in g.factors],
+                       np.ones(rank))
+    got = ob.congruence(g, e)
+    want = O.congruence(g, e)
+    assert np.allclose(got, want, rtol=0, atol=1e-12)
