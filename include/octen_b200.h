@@ -84,6 +84,13 @@ const char* octen_last_error(void);
 const char* octen_version(void);
 /* Number of kernels this library has launched in this process. */
 int64_t octen_launch_count(void);
+/* Kernel path counters of this process (no reference counterpart; the
+ * evidence that the tensor-core path ran):
+ * out[0] all launches (= octen_launch_count), out[1] tcgen05 launches of
+ * the fp32 dense compression (GEMM1 + mode-2), out[2] fp32 compression
+ * chunks that ran on the SIMT GEMM because their shape is outside the
+ * tcgen05 kernels' limits, out[3] DMMA launches of the fp64 compression. */
+void octen_kernel_counts(int64_t* out);
 
 /* init_stream (proj/include/cpstream/streaming.hpp:64; src/streaming.cpp:181-256).
  * data: I x J x t0 batch, first index fastest, dtype OCTEN_F64/F32 at
@@ -123,6 +130,11 @@ void octen_stream_destroy(octen_stream* s);
 /* Stream state accessors (StreamState, streaming.hpp:48-59).
  * info[0..7] = order, I, J, K(slices_seen), rank, p, q, batches_seen. */
 int octen_stream_info(const octen_stream* s, int64_t* info);
+/* measure_footprint (proj/include/cpstream/eval.hpp; src/eval.cpp:48-60) of
+ * the stream's device-resident state: out[0] replica bytes, out[1] summary
+ * bytes (owned replicas), out[2] factor bytes, out[3] accumulator bytes. */
+int octen_stream_footprint(const octen_stream* s, int64_t* out);
+
 /* KruskalModel factor `mode` (dim x rank, col-major) and lambda (rank). */
 int octen_stream_get_factor(const octen_stream* s, int mode, double* out);
 int octen_stream_get_lambda(const octen_stream* s, double* out);

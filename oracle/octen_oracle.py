@@ -1393,6 +1393,38 @@ def congruence(ground: KruskalModel, est: KruskalModel):
     return [float(sim[i, perm[i]]) for i in range(rank)]
 
 
+def memory_account(cfg, nontemporal_dims, t_old: int, t_new: int) -> dict:
+    """eval.cpp:62-86 -- element counts of the streaming state against the
+    paper's space formula."""
+    if cfg.q < 1 or cfg.p < 1 or cfg.rank < 1:
+        raise ConfigError("memory_account: invalid configuration")
+    order = len(nontemporal_dims) + 1
+    t_sum = int(sum(nontemporal_dims))
+    q_pow = cfg.q ** order
+    sm = {
+        "predicted_replica_elements": cfg.p * cfg.q * t_sum,
+        "predicted_summary_elements": cfg.p * q_pow,
+        "predicted_factor_elements": (t_sum + t_old + t_new) * cfg.rank + cfg.rank,
+        "predicted_accumulator_elements": cfg.p * cfg.q * cfg.rank,
+    }
+    sm["predicted_elements"] = sum(sm.values())
+    sm["formula_elements"] = cfg.p * cfg.q * (cfg.p * t_sum + t_new + cfg.rank) + (t_sum + t_old) * cfg.rank + q_pow
+    sm["ratio"] = sm["predicted_elements"] / sm["formula_elements"]
+    return sm
+
+
+def measure_footprint(st) -> dict:
+    """eval.cpp:48-60 -- bytes of the state as stored (8 per double); the
+    temporal window is empty between batches (drop_temporal_history)."""
+    fp = {"replica_bytes": 0, "summary_bytes": 0, "factor_bytes": 0, "accumulator_bytes": 0}
+    for rep in st.replicas.replicas:
+        fp["replica_bytes"] += sum(8 * m.size for m in rep.nontemporal) + 8 * rep.temporal.size
+    fp["summary_bytes"] = sum(8 * y.size for y in st.summaries.y)
+    fp["factor_bytes"] = sum(8 * f.size for f in st.model.factors) + 8 * len(st.model.lambda_)
+    fp["accumulator_bytes"] = sum(8 * h.size for h in st.summaries.history)
+    return fp
+
+
 def generate_synthetic(dims, rank: int, seed: int, noise_mu: float = 0.0, noise_sigma: float = 0.0,
                        exact_noise: bool = True):
     """commands.cpp:110-134 -- U(0,1) factors from {9,n}, lambda = 1,

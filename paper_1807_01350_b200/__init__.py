@@ -66,6 +66,16 @@ def version() -> str:
     return C.LIB.octen_version().decode()
 
 
+def kernel_counts() -> dict:
+    """Process-wide kernel path counters (octen_kernel_counts): every launch,
+    tcgen05 launches of the fp32 dense compression, fp32 chunks that fell
+    back to the SIMT GEMM (shape outside the tcgen05 kernels' limits), DMMA
+    launches of the fp64 compression."""
+    out = (C.c_i64 * 4)()
+    C.LIB.octen_kernel_counts(out)
+    return {"launches": out[0], "tcgen05": out[1], "simt_fallbacks": out[2], "dmma_compress": out[3]}
+
+
 @dataclass
 class AlsConfig:
     """cp_als.hpp:25-31."""
@@ -246,6 +256,15 @@ class StreamState:
         ka = getattr(self, "_pf_keep", [])
         self._pf_keep = (ka + [keep])[-3:]  # the copies read these buffers until ingested
 
+    def footprint(self) -> dict:
+        """measure_footprint (eval.cpp:48-60) of the device-resident state."""
+        out = (C.c_i64 * 4)()
+        _check(C.LIB.octen_stream_footprint(self._h, out))
+        fp = {"replica_bytes": out[0], "summary_bytes": out[1], "factor_bytes": out[2],
+              "accumulator_bytes": out[3]}
+        fp["total"] = sum(fp.values())
+        return fp
+
     def batch_fitness(self, batch, k0: int) -> float:
         """eval.cpp:10-20 fitness of the current model on slices [k0, k0 + t)
         of the stream, given as a batch (computed on the device)."""
@@ -322,6 +341,18 @@ class ShardedStream(StreamState):
         self._ro = torch.zeros(self.rows_count, dtype=torch.float64, device=dev)
         self._ra = torch.zeros(self.rows_count * shard_world, dtype=torch.float64, device=dev)
         self._allgather = allgather
+        # the zero fills run on torch's stream; the library writes these
+        # buffers on its own stream
+        torch.cuda.current_stream(dev).synchronize()
+
+    @staticmethod
+    def _torch_ready(t) -> None:
+        """A torch CUDA tensor handed to the library (e.g. a fresh NCCL
+        all_gather / reduce_scatter output) was produced on torch's current
+        stream: wait for it before the library's own stream reads it."""
+        import torch
+        if getattr(t, "is_cuda", False):
+            torch.cuda.current_stream(t.device).synchronize()
 
     def summaries(self):
         """The owned replicas' summaries (p_local Q^3 tensors) and the full
@@ -338,11 +369,13 @@ class ShardedStream(StreamState):
         return self._mo
 
     def merge(self, models_all):
+        self._torch_ready(models_all)
         _check(C.LIB.octen_stream_merge(self._h, ctypes.c_void_p(models_all.data_ptr()),
                                         ctypes.c_void_p(self._ro.data_ptr())))
         return self._ro
 
     def finish(self, rows_all):
+        self._torch_ready(rows_all)
         _check(C.LIB.octen_stream_finish(self._h, ctypes.c_void_p(rows_all.data_ptr())))
 
     # temporal sharding of the compression (octen_stream_begin_temporal /
@@ -359,6 +392,7 @@ class ShardedStream(StreamState):
             self.partial_count = n.value
             self._pp = torch.zeros(n.value * self.shard_world, dtype=torch.float64, device=dev)
             self._po = torch.zeros(n.value, dtype=torch.float64, device=dev)
+            torch.cuda.current_stream(dev).synchronize()
         keep, ptr, dt, loc, dims = _batch_args(local_slices)
         d = (C.c_i64 * len(dims))(*dims)
         _check(C.LIB.octen_stream_begin_temporal(self._h, ptr, dt, loc, len(dims), d, int(k_off), int(t_total),
@@ -367,6 +401,7 @@ class ShardedStream(StreamState):
         return self._pp
 
     def begin_reduced(self, owned):
+        self._torch_ready(owned)
         _check(C.LIB.octen_stream_begin_reduced(self._h, ctypes.c_void_p(owned.data_ptr()),
                                                 ctypes.c_void_p(self._mo.data_ptr())))
         return self._mo
@@ -665,15 +700,24 @@ def compress_coo(batch: SparseTensor, u: List[np.ndarray], v: List[np.ndarray], 
 
 def congruence(ground: KruskalModel, est: KruskalModel) -> List[float]:
     """eval.cpp:22-46 per-component congruence (factor match score) after
-    exhaustive (rank <= 6) or greedy matching (octen_congruence)."""
-    r = len(np.asarray(ground.lambda_))
-    if len(np.asarray(est.lambda_)) != r or len(ground.factors) != len(est.factors):
+    exhaustive (rank <= 6) or greedy matching (octen_congruence).  Checks
+    and messages in the reference's order: rank, order, per-mode rows."""
+    gf = [_f64(f) for f in ground.factors]
+    ef = [_f64(f) for f in est.factors]
+    r = len(np.asarray(ground.lambda_))  # KruskalModel::rank() (cp_als.hpp:17)
+    if len(np.asarray(est.lambda_)) != r:
         raise ConfigError("congruence: rank mismatch")
-    dims = [np.asarray(f).shape[0] for f in ground.factors]
-    if [np.asarray(f).shape[0] for f in est.factors] != dims:
-        raise ConfigError("congruence: factor shape mismatch")
-    g = np.concatenate([_f64(f).ravel(order="F") for f in ground.factors])
-    e = np.concatenate([_f64(f).ravel(order="F") for f in est.factors])
+    if len(gf) != len(ef):
+        raise ConfigError("congruence: order mismatch")
+    for n, (g, e) in enumerate(zip(gf, ef)):
+        if g.shape[0] != e.shape[0]:
+            raise ConfigError("congruence: factor shape mismatch on mode %d" % (n + 1))
+    for n, f in enumerate(gf + ef):  # the C call reads d_n * r values per factor
+        if f.ndim != 2 or f.shape[1] != r:
+            raise ConfigError("congruence: factor shape mismatch on mode %d" % (n % max(len(gf), 1) + 1))
+    dims = [g.shape[0] for g in gf]
+    g = np.concatenate([f.ravel(order="F") for f in gf])
+    e = np.concatenate([f.ravel(order="F") for f in ef])
     out = np.zeros(r)
     d = (C.c_i64 * len(dims))(*dims)
     _check(C.LIB.octen_congruence(len(dims), r, d, _dptr(g), _dptr(e), _dptr(out)))

@@ -54,6 +54,8 @@ SIGNATURES = {
     "octen_last_error": (ctypes.c_char_p, []),
     "octen_version": (ctypes.c_char_p, []),
     "octen_launch_count": (ctypes.c_int64, []),
+    "octen_kernel_counts": (None, [P_i64]),
+    "octen_stream_footprint": (ctypes.c_int, [ctypes.c_void_p, P_i64]),
     "octen_stream_get_stage_times": (ctypes.c_int, [ctypes.c_void_p, P_dbl]),
     "octen_stream_init": (ctypes.c_int, [ctypes.POINTER(StreamConfigC), ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, P_i64, ctypes.POINTER(ctypes.c_void_p)]),

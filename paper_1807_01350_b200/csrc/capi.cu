@@ -68,6 +68,32 @@ int guard(F&& f) {
     }
 }
 
+// Every stream entry point runs on the handle's device and restores the
+// caller's current device afterwards.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        int cur = 0;
+        OCTEN_CUDA(cudaGetDevice(&cur));
+        if (cur != dev) {
+            OCTEN_CUDA(cudaSetDevice(dev));
+            prev = cur;
+        }
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <class F>
+int sguard(const octen_stream* s, F&& f) {
+    return guard([&] {
+        if (!s || !s->s) throw octen::ConfigError("octen: null stream handle");
+        DeviceGuard dg(s->s->cfg.device);
+        f();
+    });
+}
+
 octen::StreamCfg to_cfg(const octen_stream_config* c) {
     octen::StreamCfg s;
     s.rank = c->rank;
@@ -131,8 +157,13 @@ const char* octen_version(void) { return "octen_b200 0.1 (sm_100a)"; }
 
 int64_t octen_launch_count(void) { return (int64_t)octen::launch_counter().load(); }
 
+void octen_kernel_counts(int64_t* out) {
+    out[0] = (int64_t)octen::launch_counter().load();
+    for (int i = 0; i < octen::kNumPathCounters; ++i) out[1 + i] = (int64_t)octen::path_counter(i).load();
+}
+
 int octen_stream_get_stage_times(const octen_stream* s, double* out) {
-    return guard([&] {
+    return sguard(s, [&] {
         const auto& x = *s->s;
         for (int i = 0; i < 4; ++i) out[i] = x.dev_ms[i];
         out[4] = x.gemm1_flops;
@@ -145,6 +176,7 @@ int octen_stream_init(const octen_stream_config* cfg, const void* data, int dtyp
     return guard([&] {
         if (!cfg || !data || !dims || !out) throw octen::ConfigError("octen_stream_init: null argument");
         check_dtype(dtype, location);
+        DeviceGuard dg(cfg->device);
         auto h = std::make_unique<octen_stream>();
         h->s = std::make_unique<octen::Stream>(to_cfg(cfg));
         h->s->init(data, dtype, location, order, dims);
@@ -154,7 +186,7 @@ int octen_stream_init(const octen_stream_config* cfg, const void* data, int dtyp
 
 int octen_stream_ingest(octen_stream* s, const void* data, int dtype, int location, int order,
                         const int64_t* dims) {
-    return guard([&] {
+    return sguard(s, [&] {
         if (!s || !data || !dims) throw octen::ConfigError("octen_stream_ingest: null argument");
         check_dtype(dtype, location);
         s->s->ingest(data, dtype, location, order, dims);
@@ -196,6 +228,7 @@ int octen_congruence(int order, int rank, const int64_t* dims, const double* gro
                 }
         }
         std::vector<int> perm(r);
+        for (int i = 0; i < r; ++i) perm[i] = i;  // exhaustive_match starts from the identity
         if (r <= 6) {
             std::vector<int> cand(r);
             for (int i = 0; i < r; ++i) cand[i] = i;
@@ -218,16 +251,15 @@ int octen_congruence(int order, int rank, const int64_t* dims, const double* gro
 
 int octen_stream_batch_fitness(octen_stream* s, const void* data, int dtype, int location, int order,
                                const int64_t* dims, int64_t k0, double* fitness) {
-    return guard([&] {
+    return sguard(s, [&] {
         if (!s || !data || !dims || !fitness) throw octen::ConfigError("octen_stream_batch_fitness: null argument");
         check_dtype(dtype, location);
-        OCTEN_CUDA(cudaSetDevice(s->s->cfg.device));
         *fitness = s->s->batch_fitness(data, dtype, location, order, dims, k0);
     });
 }
 
 int octen_stream_partial_block_size(const octen_stream* s, int64_t* n) {
-    return guard([&] {
+    return sguard(s, [&] {
         if (!s || !n) throw octen::ConfigError("octen_stream_partial_block_size: null argument");
         *n = (int64_t)s->s->partial_block_count();
     });
@@ -235,37 +267,42 @@ int octen_stream_partial_block_size(const octen_stream* s, int64_t* n) {
 
 int octen_stream_begin_temporal(octen_stream* s, const void* data, int dtype, int location, int order,
                                 const int64_t* dims_local, int64_t k_off, int64_t t_total, double* partial_out) {
-    return guard([&] {
+    return sguard(s, [&] {
         if (!s || !dims_local || !partial_out || (!data && dims_local[2] > 0))
             throw octen::ConfigError("octen_stream_begin_temporal: null argument");
         check_dtype(dtype, location);
-        OCTEN_CUDA(cudaSetDevice(s->s->cfg.device));
         s->s->begin_temporal(data, dtype, location, order, dims_local, k_off, t_total, partial_out);
     });
 }
 
 int octen_stream_begin_reduced(octen_stream* s, const double* owned_block, double* models_out) {
-    return guard([&] {
+    return sguard(s, [&] {
         if (!s || !owned_block || !models_out) throw octen::ConfigError("octen_stream_begin_reduced: null argument");
-        OCTEN_CUDA(cudaSetDevice(s->s->cfg.device));
         s->s->begin_reduced(owned_block, models_out);
     });
 }
 
 int octen_stream_prefetch(octen_stream* s, const void* data, int dtype, int order, const int64_t* dims) {
-    return guard([&] {
+    return sguard(s, [&] {
         if (!s || !data || !dims) throw octen::ConfigError("octen_stream_prefetch: null argument");
         check_dtype(dtype, OCTEN_HOST);
-        OCTEN_CUDA(cudaSetDevice(s->s->cfg.device));
         s->s->prefetch(data, dtype, order, dims);
     });
 }
 
-void octen_stream_destroy(octen_stream* s) { delete s; }
+void octen_stream_destroy(octen_stream* s) {
+    if (!s) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (s->s) cudaSetDevice(s->s->cfg.device);
+    delete s;
+    cudaSetDevice(cur);
+}
 
 int octen_stream_create(const octen_stream_config* cfg, int shard_rank, int shard_world, octen_stream** out) {
     return guard([&] {
         if (!cfg || !out) throw octen::ConfigError("octen_stream_create: null argument");
+        DeviceGuard dg(cfg->device);
         auto h = std::make_unique<octen_stream>();
         h->s = std::make_unique<octen::Stream>(to_cfg(cfg), shard_rank, shard_world);
         *out = h.release();
@@ -273,7 +310,7 @@ int octen_stream_create(const octen_stream_config* cfg, int shard_rank, int shar
 }
 
 int octen_stream_exchange_sizes(const octen_stream* s, int64_t* sizes) {
-    return guard([&] {
+    return sguard(s, [&] {
         if (!s || !sizes) throw octen::ConfigError("octen_stream_exchange_sizes: null argument");
         const auto& x = *s->s;
         sizes[0] = (int64_t)x.models_count();
@@ -287,7 +324,7 @@ int octen_stream_exchange_sizes(const octen_stream* s, int64_t* sizes) {
 
 int octen_stream_begin(octen_stream* s, const void* data, int dtype, int location, int order, const int64_t* dims,
                        double* models_out) {
-    return guard([&] {
+    return sguard(s, [&] {
         if (!s || !data || !dims || !models_out) throw octen::ConfigError("octen_stream_begin: null argument");
         check_dtype(dtype, location);
         s->s->begin(data, dtype, location, order, dims, models_out);
@@ -295,21 +332,21 @@ int octen_stream_begin(octen_stream* s, const void* data, int dtype, int locatio
 }
 
 int octen_stream_merge(octen_stream* s, const double* models_all, double* rows_out) {
-    return guard([&] {
+    return sguard(s, [&] {
         if (!s || !models_all || !rows_out) throw octen::ConfigError("octen_stream_merge: null argument");
         s->s->merge_phase(models_all, rows_out);
     });
 }
 
 int octen_stream_finish(octen_stream* s, const double* rows_all) {
-    return guard([&] {
+    return sguard(s, [&] {
         if (!s || !rows_all) throw octen::ConfigError("octen_stream_finish: null argument");
         s->s->finish(rows_all);
     });
 }
 
 int octen_stream_info(const octen_stream* s, int64_t* info) {
-    return guard([&] {
+    return sguard(s, [&] {
         const auto& x = *s->s;
         info[0] = 3;
         info[1] = x.I;
@@ -322,12 +359,27 @@ int octen_stream_info(const octen_stream* s, int64_t* info) {
     });
 }
 
+int octen_stream_footprint(const octen_stream* s, int64_t* out) {
+    // measure_footprint (eval.cpp:48-60) of the device-resident state: 8 bytes
+    // per double held for the stream's logical state (U_p/V_p projections,
+    // owned summaries, model, history accumulators); the temporal window is
+    // empty between batches, as in the reference.
+    return sguard(s, [&] {
+        const auto& x = *s->s;
+        const int64_t P = x.cfg.p, Q = x.cfg.q, R = x.cfg.rank;
+        out[0] = 8 * P * Q * (x.I + x.J);
+        out[1] = 8 * (int64_t)x.pl * Q * Q * Q;
+        out[2] = 8 * ((x.I + x.J + x.K) * R + R);
+        out[3] = 8 * P * Q * R;
+    });
+}
+
 int octen_stream_get_factor(const octen_stream* s, int mode, double* out) {
-    return guard([&] { s->s->get_factor(mode, out); });
+    return sguard(s, [&] { s->s->get_factor(mode, out); });
 }
 
 int octen_stream_get_model(const octen_stream* s, double* a, double* b, double* c, double* lambda) {
-    return guard([&] {
+    return sguard(s, [&] {
         auto& x = *s->s;
         const int R = x.cfg.rank;
         OCTEN_CUDA(cudaMemcpyAsync(a, x.A.p, sizeof(double) * x.I * R, cudaMemcpyDeviceToHost, x.st));
@@ -340,7 +392,7 @@ int octen_stream_get_model(const octen_stream* s, double* a, double* b, double* 
 }
 
 int octen_stream_get_lambda(const octen_stream* s, double* out) {
-    return guard([&] {
+    return sguard(s, [&] {
         auto& x = *s->s;
         x.lam.download(out, x.cfg.rank, x.st);
         OCTEN_CUDA(cudaStreamSynchronize(x.st));
@@ -348,7 +400,7 @@ int octen_stream_get_lambda(const octen_stream* s, double* out) {
 }
 
 int octen_stream_get_record(const octen_stream* s, int64_t index, octen_batch_record* out) {
-    return guard([&] {
+    return sguard(s, [&] {
         const auto& x = *s->s;
         if (index < 0 || index >= (int64_t)x.log.size()) throw octen::ConfigError("octen_stream_get_record: index");
         const auto& r = x.log[(size_t)index];
@@ -366,7 +418,7 @@ int octen_stream_get_record(const octen_stream* s, int64_t index, octen_batch_re
 }
 
 int octen_stream_get_summaries(const octen_stream* s, double* y) {
-    return guard([&] {
+    return sguard(s, [&] {
         auto& x = *s->s;
         const size_t n = (size_t)x.pl * x.cfg.q * x.cfg.q * x.cfg.q;
         x.Y.download(y, n, x.st);
@@ -375,7 +427,7 @@ int octen_stream_get_summaries(const octen_stream* s, double* y) {
 }
 
 int octen_stream_get_history(const octen_stream* s, double* h) {
-    return guard([&] {
+    return sguard(s, [&] {
         auto& x = *s->s;
         const int P = x.cfg.p, Q = x.cfg.q, R = x.cfg.rank;
         std::vector<double> stk = x.hist.to_host((size_t)P * Q * R, x.st);
@@ -384,7 +436,7 @@ int octen_stream_get_history(const octen_stream* s, double* h) {
 }
 
 int octen_stream_get_replica_models(const octen_stream* s, double* factors, double* lambda) {
-    return guard([&] {
+    return sguard(s, [&] {
         auto& x = *s->s;
         const int P = x.cfg.p, Q = x.cfg.q, R = x.cfg.rank;
         x.MfAll.download(factors, (size_t)P * 3 * Q * R, x.st);

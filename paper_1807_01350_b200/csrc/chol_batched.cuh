@@ -333,14 +333,13 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
                          int* rank, DevBuf<double>& linv, cudaStream_t st) {
     if (batch <= 0 || n <= 0) return;
     constexpr size_t kTrailSmem = 2 * kCholNB * kTrailLD * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    attr.once([&] {
         OCTEN_CUDA(cudaFuncSetAttribute(chol_trail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kTrailSmem));
         OCTEN_CUDA(cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kDiagSmem));
-        attr = true;
-    }
+    });
     const int nblk = (n + kCholNB - 1) / kCholNB;
     linv.reserve((size_t)batch * nblk * kCholNB * kCholNB);
     chol_maxdiag_kernel<<<batch, 256, 0, st>>>(A, n, lda, sA, maxdiag, rank); OCTEN_LAUNCHED(1);

@@ -10,8 +10,12 @@
 //   GEMM3  Y_p += Z2_p (Q^2 x t) W_p          fp64 accumulate (update_summaries)
 //
 // The batch is processed in chunks of temporal slices so Z1 stays bounded.
-// fp32 input: GEMM1 runs on the tensor cores (tcgen05, split-TF32) when the
-// sm_100a kernel is available, else this SIMT path; fp64 input: SIMT fp64.
+// fp32 input: GEMM1 and GEMM2 run on the tensor cores (tcgen05, split-TF32).
+// A shape outside those kernels' limits (K or J not a multiple of 4, Q > 128)
+// runs that chunk on the SIMT GEMM and is counted (octen_kernel_counts); the
+// tcgen05 path being unavailable on the device is an error unless
+// OCTEN_DISABLE_TCGEN05 / OCTEN_ALLOW_SIMT opts in (diagnostics).
+// fp64 input: GEMM1 and GEMM2 on the FP64 tensor cores (DMMA).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -20,6 +24,7 @@
 #include <vector>
 
 #include "engine.hpp"
+#include "errors.hpp"
 #include "gemm_dmma.cuh"
 #include "tc_gemm.hpp"
 
@@ -114,6 +119,10 @@ __global__ void nonfinite_chunk_kernel(const float* x32, const double* x64, size
 // copies of later chunks overlap the contractions of earlier ones; with
 // `flag` every chunk is also scanned for non-finite values (the batch must
 // be rejected before the summaries change).
+bool simt_opt_in() {
+    return std::getenv("OCTEN_DISABLE_TCGEN05") != nullptr || std::getenv("OCTEN_ALLOW_SIMT") != nullptr;
+}
+
 template <typename T>
 void run_project(CompressEngine& e, const T* dX, std::int64_t t, T* Z1, T* Z2, const T* A, const T* V,
                  std::int64_t tc_max, cudaStream_t st, bool use_tc, const cudaEvent_t* ready, int* flag) {
@@ -139,14 +148,32 @@ void run_project(CompressEngine& e, const T* dX, std::int64_t t, T* Z1, T* Z2, c
         if constexpr (std::is_same<T, float>::value) {
             // tensor-core path: GEMM1 scatters its rows replica-contiguously
             // (P*Q x N1) for the batched tcgen05 mode-2 contraction
-            if (use_tc)
-                done = tc_gemm_tf32x3(e.Ahi.p, e.Alo.p, e.lda_tc, Xc, Z1, (int)e.Meff, (long long)N1, (int)e.I, st, P,
-                                      Q, e.shared);
+            if (use_tc) {
+                if (!tc_gemm_available()) {
+                    if (!simt_opt_in())
+                        throw CudaError("octen: the tcgen05 compression kernels are unavailable on this device "
+                                        "(sm_100a required; set OCTEN_ALLOW_SIMT=1 to run the SIMT GEMMs)");
+                } else {
+                    done = tc_gemm_tf32x3(e.Ahi.p, e.Alo.p, e.lda_tc, Xc, Z1, (int)e.Meff, (long long)N1, (int)e.I,
+                                          st, P, Q, e.shared);
+                    if (done)
+                        path_counter(kTcgen05Launches).fetch_add(1);
+                    else
+                        path_counter(kSimtFallbacks).fetch_add(1);
+                }
+            }
             e.used_tc = done;
         }
-        if (!done)
-            gemm_simt<T, T, true, true>(1, (int)e.Meff, (int)N1, (int)e.I, G1A<T>{A, e.I}, G1B<T>{Xc, e.I},
-                                        G1C<T>{Z1, N1}, st);
+        if (!done) {
+            if constexpr (std::is_same<T, double>::value) {
+                gemm_f64<true, true>(1, (int)e.Meff, (int)N1, (int)e.I, G1A<T>{A, e.I}, G1B<T>{Xc, e.I},
+                                     G1C<T>{Z1, N1}, st);
+                path_counter(kDmmaCompress).fetch_add(1);
+            } else {
+                gemm_simt<T, T, true, true>(1, (int)e.Meff, (int)N1, (int)e.I, G1A<T>{A, e.I}, G1B<T>{Xc, e.I},
+                                            G1C<T>{Z1, N1}, st);
+            }
+        }
         OCTEN_CUDA(cudaEventRecord(e.event(2 * e.g1_used + 1), st));
         ++e.g1_used;
         ++e.gemm1_launches;
@@ -155,13 +182,22 @@ void run_project(CompressEngine& e, const T* dX, std::int64_t t, T* Z1, T* Z2, c
         bool done2 = false;
         if constexpr (std::is_same<T, float>::value) {
             static const bool no_m2 = std::getenv("OCTEN_DISABLE_TC_MODE2") != nullptr;
-            if (done && !no_m2)
+            if (done && !no_m2) {
                 done2 = tc_mode2_tf32x3(Z1, N1, (int)e.J, tc, e.Vhi.p, e.Vlo.p, e.ldv_tc, P, Q, Z2c, zs, st);
+                path_counter(done2 ? kTcgen05Launches : kSimtFallbacks).fetch_add(1);
+            }
         }
-        if (!done2)
-            gemm_simt<T, T, true, false>(P * tc, Q, Q, (int)e.J,
-                                         G2A<T>{Z1, done ? e.rowmap_id.p : e.rowmap.p, N1, e.J, tc, Q},
-                                         G2B<T>{V, e.J, tc, Q}, G2C<T>{Z2c, zs, tc, Q}, st);
+        if (!done2) {
+            if constexpr (std::is_same<T, double>::value) {
+                gemm_f64<true, true>(P * tc, Q, Q, (int)e.J, G2A<T>{Z1, e.rowmap.p, N1, e.J, tc, Q},
+                                     G2B<T>{V, e.J, tc, Q}, G2C<T>{Z2c, zs, tc, Q}, st);
+                path_counter(kDmmaCompress).fetch_add(1);
+            } else {
+                gemm_simt<T, T, true, false>(P * tc, Q, Q, (int)e.J,
+                                             G2A<T>{Z1, done ? e.rowmap_id.p : e.rowmap.p, N1, e.J, tc, Q},
+                                             G2B<T>{V, e.J, tc, Q}, G2C<T>{Z2c, zs, tc, Q}, st);
+            }
+        }
     }
     OCTEN_CUDA(cudaGetLastError());
 }

@@ -301,12 +301,11 @@ void launch_slices(const CooEngine& e, std::int64_t t, float* Z2, cudaStream_t s
     constexpr int RB = 256 / TPR;
     constexpr int NC = RB * QP;
     const size_t smem = (size_t)2 * kChunkG * NC * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    attr.once([&] {
         OCTEN_CUDA(cudaFuncSetAttribute(coo_slice_kernel<QP, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
-        attr = true;
-    }
+    });
     dim3 grid((unsigned)t, (unsigned)((e.P + RB - 1) / RB));
     coo_slice_kernel<QP, TM><<<grid, 256, smem, st>>>(e.ent.p, e.off.p, e.U32.p, e.V32.p, e.ldp, e.P, e.Q,
                                                       (long long)e.Q * e.Q * t, Z2);

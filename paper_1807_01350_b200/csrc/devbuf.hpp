@@ -13,6 +13,7 @@
 
 #include <cstddef>
 #include <map>
+#include <utility>
 #include <vector>
 
 #include "errors.hpp"
@@ -67,11 +68,9 @@ struct BlockCache {
         }
         return s[dev & 15];
     }
-    void give(void* p, size_t bytes) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        free_blocks[dev & 15].emplace(bytes, p);
-    }
+    // A block goes back to the list of the device it was allocated on (which
+    // need not be the current one when the owner is released).
+    void give(void* p, size_t bytes, int dev) { free_blocks[dev & 15].emplace(bytes, p); }
     void trim(int dev) {
         OCTEN_CUDA(cudaDeviceSynchronize());
         cudaStream_t s = alloc_stream(dev);
@@ -87,14 +86,20 @@ template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    int dev = 0;  // device ordinal the block belongs to
 
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
 
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+        std::swap(dev, o.dev);
+    }
     void release() {
-        if (p) BlockCache::get().give(p, n * sizeof(T));
+        if (p) BlockCache::get().give(p, n * sizeof(T), dev);
         p = nullptr;
         n = 0;
     }
@@ -104,6 +109,7 @@ struct DevBuf {
         release();
         if (count == 0) count = 1;
         size_t got = 0;
+        OCTEN_CUDA(cudaGetDevice(&dev));
         p = static_cast<T*>(BlockCache::get().take(count * sizeof(T), got));
         n = got / sizeof(T);
         return p;
@@ -112,11 +118,14 @@ struct DevBuf {
     T* grow(size_t count, size_t keep, cudaStream_t st) {
         if (count <= n && p) return p;
         size_t got = 0;
+        int qdev = 0;
+        OCTEN_CUDA(cudaGetDevice(&qdev));
         T* q = static_cast<T*>(BlockCache::get().take(count * sizeof(T), got));
         if (p && keep) OCTEN_CUDA(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
         OCTEN_CUDA(cudaStreamSynchronize(st));
         release();
         p = q;
+        dev = qdev;
         n = got / sizeof(T);
         return p;
     }

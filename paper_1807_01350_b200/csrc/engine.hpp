@@ -229,6 +229,8 @@ public:
     DevBuf<double> Lsum_inv[2], Gw_inv;  // diagonal-block inverses of the factors
     DevBuf<double> Ginv[2];  // (sum_p G_p)^-1, full d x d
     int sum_rank[2] = {0, 0};
+    bool sum_qr[2] = {false, false};  // full rank only by the QR rule: solve by QR each batch
+    int qr_rank_check(int n, const double* w, int r, const double* rhs, double* x, cudaStream_t st);
     DevBuf<double> Lw[2];    // shared x shared whitener (non-temporal modes)
     int white_ok[2] = {0, 0};
     DevBuf<double> Lp[2];    // P x Q x Q chol(U_p^T U_p)

@@ -348,12 +348,11 @@ void gemm_f64_pipe(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaSt
     int kchunk = (K + ksplit - 1) / ksplit;
     kchunk = ((kchunk + pipe::BK - 1) / pipe::BK) * pipe::BK;
     const size_t smem = pipe::smem_bytes<A_KFAST>();
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    attr.once([&] {
         OCTEN_CUDA(cudaFuncSetAttribute(gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF, B_KFAST>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    });
     dim3 grid((N + pipe::BN - 1) / pipe::BN, (M + pipe::BM - 1) / pipe::BM, batches * ksplit);
     if (pdl) {
         launch_pdl(gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF, B_KFAST>, grid, dim3(256), smem, st, M, N, K, ksplit,

@@ -23,6 +23,7 @@
 #include <string>
 
 #include "chol_batched.cuh"
+#include "colpiv_qr.cuh"
 #include "engine.hpp"
 #include "evprof.hpp"
 #include "gemm_dmma.cuh"
@@ -512,6 +513,23 @@ __global__ void border_row_kernel(int nb, long long d, const double* G, long lon
 }
 
 // SW(k, r) = w_{k/Q, r}^2 * stack(k, r)
+// The stacked projection of a non-temporal mode (stack_projections,
+// recovery.cpp:293-313): row p Q + a, column i = U_p(i, a), rows scaled by
+// the replica weight w[p + P r] when w is given (recover_nontemporal_weighted,
+// recovery.cpp:328-331); also the matching weighted right-hand side.
+__global__ void stack_proj_kernel(int P, int Q, long long d, const double* U, const double* w, int R, int r,
+                                  const double* rhs, double* out, double* rhs_out) {
+    const long long PQ = (long long)P * Q;
+    const size_t total = (size_t)PQ * d;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const long long row = (long long)(e % PQ), i = (long long)(e / PQ);
+        const int p = (int)(row / Q), a = (int)(row % Q);
+        const double wv = w ? w[p + (size_t)P * r] : 1.0;
+        out[e] = wv * U[(size_t)p * d * Q + i + (size_t)d * a];
+        if (i == 0 && rhs) rhs_out[row] = wv * rhs[row];
+    }
+}
+
 __global__ void scale_stack_kernel(int P, int Q, int R, const double* stack, const double* w, double* sw) {
     const size_t PQ = (size_t)P * Q, total = PQ * R;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
@@ -894,9 +912,16 @@ void MergeEngine::set_projections(int P_, int Q_, int sh, int R_, std::int64_t I
         ranks.reserve(128);
         chol_batched(Lsum[n].p, (int)d, (int)d, 0, 1, kGramRankTol, maxdiag.p, ranks.p, Lsum_inv[n], st);
         sum_rank[n] = ranks.to_host(1, st)[0];
+        sum_qr[n] = false;
+        if (sum_rank[n] < d && PQ >= d) {
+            // the Gram test cannot resolve |r_ii| / |r_00| below ~3e-6: decide
+            // with the reference's own rule on the stacked projection
+            sum_rank[n] = qr_rank_check(n, nullptr, 0, nullptr, nullptr, st);
+            sum_qr[n] = sum_rank[n] == d;
+        }
         // (sum_p U_p U_p^T)^-1, formed once per stream: every batch's
         // unweighted non-temporal solve is then one GEMM
-        if (sum_rank[n] == d) {
+        if (sum_rank[n] == d && !sum_qr[n]) {
             Ginv[n].reserve((size_t)d * d);
             identity_kernel<<<grid_for((size_t)d * d), 256, 0, st>>>(Ginv[n].p, d);
             OCTEN_LAUNCHED(1);
@@ -1052,6 +1077,31 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
     }
 }
 
+// Rank (and, with rhs / x given, the least-squares solution) of the stacked
+// projection of mode n, rows weighted by column r of w when w is given, by
+// column-pivoted QR at the reference's threshold (recovery.cpp:26-38): the
+// fallback for systems whose Gram pivots fall under kGramRankTol.  rhs: PQ
+// x 1 (weighted, one column r) or PQ x R (unweighted, every column).
+int MergeEngine::qr_rank_check(int n, const double* w, int r, const double* rhs, double* x, cudaStream_t st) {
+    const long long d = dims[n], PQ = (long long)P * Q;
+    const int nrhs = rhs ? (w ? 1 : R) : 0;
+    DevBuf<double> Am, Bm, nrm;
+    DevBuf<int> pv, rk;
+    Am.reserve((size_t)PQ * d);
+    Bm.reserve((size_t)PQ * std::max(nrhs, 1));
+    nrm.reserve((size_t)d);
+    pv.reserve((size_t)d);
+    rk.reserve(1);
+    stack_proj_kernel<<<grid_for((size_t)PQ * d), 256, 0, st>>>(P, Q, d, Ud[n].p, w, R, r, w ? rhs : nullptr, Am.p,
+                                                                 Bm.p);
+    OCTEN_LAUNCHED(1);
+    if (rhs && !w)
+        OCTEN_CUDA(cudaMemcpyAsync(Bm.p, rhs, sizeof(double) * PQ * R, cudaMemcpyDeviceToDevice, st));
+    colpiv_qr_solve((int)PQ, (int)d, Am.p, PQ, 0, Bm.p, PQ, 0, nrhs, kRankTol, x ? x : Bm.p, d, 0, rk.p, nrm.p, pv.p,
+                    1, st);
+    return rk.to_host(1, st)[0];
+}
+
 void MergeEngine::solve_nontemporal(int n, const double* dStack, double* dOut, cudaStream_t st) {
     const long long d = dims[n], PQ = (long long)P * Q;
     if (PQ < d)
@@ -1060,6 +1110,10 @@ void MergeEngine::solve_nontemporal(int n, const double* dStack, double* dOut, c
     if (sum_rank[n] < d)
         throw NumericError("recover: rank-deficient projection on mode " + std::to_string(n + 1) + " (rank " +
                            std::to_string(sum_rank[n]) + " of " + std::to_string(d) + ")");
+    if (sum_qr[n]) {  // full rank by the reference's QR rule only: solve on the stacked projection
+        qr_rank_check(n, nullptr, 0, dStack, dOut, st);
+        return;
+    }
     tmp.reserve((size_t)d * R);
     gemm_f64_splitk<false, true>(1, (int)d, R, (int)PQ, UcatA{Ud[n].p, d, 0}, ColB{dStack, PQ, 0},
                                            StoreCM{tmp.p, d, 0}, st, kws);
@@ -1221,20 +1275,28 @@ void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, dou
             chol_batched(Gw.p, (int)ldg, (int)ldg, ms, nb, kGramRankTol, maxdiag.p, ranks.p, Gw_inv, st);
             OCTEN_PROF("chol", st);
             std::vector<int> rk = ranks.to_host(nb, st);
-            for (int mi = 0; mi < nmodes; ++mi) {
-                const int n = fused ? mi : gi;
+            // A Gram pivot under kGramRankTol only bounds |r_ii| / |r_00| by
+            // 3e-6; the reference's threshold is 1e-10 on the weighted stacked
+            // projection itself.  Those columns are decided (and, when full
+            // rank, solved) by column-pivoted QR after the Cholesky solves.
+            std::vector<std::pair<int, int>> qr_cols;  // (mi, r)
+            for (int mi = 0; mi < nmodes; ++mi)
                 for (int r = 0; r < R; ++r)
-                    if (rk[mi * R + r] < d)
-                        throw NumericError("recover: rank-deficient projection on mode " + std::to_string(n + 1) +
-                                           " (rank " + std::to_string(rk[mi * R + r]) + " of " + std::to_string(d) +
-                                           ")");
-            }
+                    if (rk[mi * R + r] < d) qr_cols.emplace_back(mi, r);
             // each column r against its own factor
             OCTEN_PROF("rank-check", st);
             border_row_kernel<<<grid_for((size_t)nb * d), 256, 0, st>>>(nb, d, Gw.p, ldg, sw2.p);
             OCTEN_LAUNCHED(1);
             chol_solve_cta(Gw.p, (int)d, (int)ldg, ms, Gw_inv, sw2.p, (int)d, d, 1, nb, st, /*backward_only=*/true);
             OCTEN_PROF("chol_solve", st);
+            for (const auto& c : qr_cols) {
+                const int n = fused ? c.first : gi;
+                const int qrank = qr_rank_check(n, w.p, c.second, stacks.p + (size_t)n * PQ * R + (size_t)PQ * c.second,
+                                                sw2.p + ((size_t)c.first * R + c.second) * d, st);
+                if (qrank < d)
+                    throw NumericError("recover: rank-deficient projection on mode " + std::to_string(n + 1) +
+                                       " (rank " + std::to_string(qrank) + " of " + std::to_string(d) + ")");
+            }
             for (int mi = 0; mi < nmodes; ++mi) {
                 const int n = fused ? mi : gi;
                 OCTEN_CUDA(cudaMemcpyAsync(solved[n].p, sw2.p + (size_t)mi * R * d, sizeof(double) * d * R,

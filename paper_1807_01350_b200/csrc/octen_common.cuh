@@ -20,6 +20,10 @@
 
 #define OCTEN_LAUNCHED(n) ::octen::launch_counter().fetch_add((n), std::memory_order_relaxed)
 
+#if defined(__CUDACC__)
+#include <cuda_runtime.h>
+#endif
+
 namespace octen {
 
 // Number of kernels this library has launched (reported by bench.py as
@@ -28,6 +32,33 @@ inline std::atomic<long long>& launch_counter() {
     static std::atomic<long long> c{0};
     return c;
 }
+// Path counters (octen_kernel_counts): tcgen05 launches of the fp32 dense
+// compression (GEMM1 + mode-2), chunks of it that ran on the SIMT GEMM
+// instead (a shape outside the tcgen05 kernels' limits), and DMMA launches
+// of the fp64-input compression.
+enum PathCounter { kTcgen05Launches = 0, kSimtFallbacks = 1, kDmmaCompress = 2, kNumPathCounters = 3 };
+inline std::atomic<long long>& path_counter(int i) {
+    static std::atomic<long long> c[kNumPathCounters];
+    return c[i];
+}
+
+#if defined(__CUDACC__)
+// Kernel attributes (cudaFuncSetAttribute) are per device: a process that
+// drives handles on several GPUs must set them once per device ordinal, not
+// once per process.  `PerDevice` remembers the devices already done.
+struct PerDevice {
+    std::atomic<unsigned long long> done{0};
+    template <class F>
+    void once(F&& f) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const unsigned long long bit = 1ull << (dev & 63);
+        if (done.load(std::memory_order_acquire) & bit) return;
+        f();
+        done.fetch_or(bit, std::memory_order_release);
+    }
+};
+#endif
 
 // A "team" is the set of threads cooperating on one small problem: a CUDA
 // thread block on the device, a single thread on the host.  Team-parallel

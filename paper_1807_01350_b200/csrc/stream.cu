@@ -269,8 +269,7 @@ void Stream::ensure_c_capacity(std::int64_t rows) {
         OCTEN_CUDA(cudaMemcpy2DAsync(nc.p, cap * sizeof(double), C.p, capC * sizeof(double), K * sizeof(double),
                                      cfg.rank, cudaMemcpyDeviceToDevice, st));
     OCTEN_CUDA(cudaStreamSynchronize(st));
-    std::swap(C.p, nc.p);
-    std::swap(C.n, nc.n);
+    C.swap(nc);
     capC = cap;
 }
 
@@ -744,10 +743,8 @@ void Stream::finish(const double* rows_all) {
         }
         append_rows_kernel<<<grid1d((size_t)t_new * R), 256, 0, st>>>(C.p, K, capC, R, rows.p, t_new);
         OCTEN_LAUNCHED(1);
-        std::swap(A.p, Anew.p);
-        std::swap(A.n, Anew.n);
-        std::swap(B.p, Bnew.p);
-        std::swap(B.n, Bnew.n);
+        A.swap(Anew);
+        B.swap(Bnew);
         normalize_model_kernel<<<R, 256, 0, st>>>(A.p, I, B.p, J, C.p, K + t_new, capC, lam.p);
         OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
@@ -808,18 +805,12 @@ void Stream::snapshot(Snapshot& s) {
 }
 
 void Stream::restore(Snapshot& s) {
-    std::swap(Y.p, s.Y.p);
-    std::swap(Y.n, s.Y.n);
-    std::swap(hist.p, s.hist.p);
-    std::swap(hist.n, s.hist.n);
-    std::swap(A.p, s.A.p);
-    std::swap(A.n, s.A.n);
-    std::swap(B.p, s.B.p);
-    std::swap(B.n, s.B.n);
-    std::swap(C.p, s.C.p);
-    std::swap(C.n, s.C.n);
-    std::swap(lam.p, s.lam.p);
-    std::swap(lam.n, s.lam.n);
+    Y.swap(s.Y);
+    hist.swap(s.hist);
+    A.swap(s.A);
+    B.swap(s.B);
+    C.swap(s.C);
+    lam.swap(s.lam);
     capC = s.capC;
     K = s.K;
     batches_seen = s.batches_seen;
@@ -914,6 +905,7 @@ double Stream::batch_fitness(const void* data, int dtype, int location, int orde
     const int R = cfg.rank;
     const size_t n = (size_t)I * J * t;
     const void* dX = stage_input(data, dtype, location, n);
+    check_finite(dX, dtype, n);  // the reference builds a DenseTensor from the batch first
     const int nb = (int)std::min<size_t>(148 * 4, (n + 255) / 256);
     DevBuf<double> part, W;
     part.reserve((size_t)nb);
@@ -957,8 +949,8 @@ double Stream::batch_fitness(const void* data, int dtype, int location, int orde
     for (int a = 0; a < R; ++a)
         for (int b = 0; b < R; ++b)
             nh2 += hl[(size_t)a] * hl[(size_t)b] * gram(hA, I, a, b) * gram(hB, J, a, b) * gram(hC, t, a, b);
+    if (!(nx2 > 0.0)) throw NumericError("fitness: zero-norm reference tensor");  // eval.cpp:13
     const double res2 = std::max(0.0, nx2 - 2.0 * inner + nh2);
-    if (!(nx2 > 0.0)) return res2 == 0.0 ? 100.0 : -INFINITY;
     return 100.0 * (1.0 - std::sqrt(res2) / std::sqrt(nx2));
 }
 

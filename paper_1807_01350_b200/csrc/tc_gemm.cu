@@ -747,18 +747,14 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
     const size_t smem = STAGES * STAGE_BYTES + 1024 + 256;
     static const bool classic = std::getenv("OCTEN_G1_CLASSIC") != nullptr;  // diagnostics: one CTA per tile
     if (!classic) {
-        static bool pattr = false;
-        if (!pattr) {
+        static PerDevice pattr;
+        pattr.once([&] {
             OCTEN_CUDA(cudaFuncSetAttribute(tc_gemm_tf32x3_persistent_kernel,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + G1P_EPI_BYTES)));
-            pattr = true;
-        }
-        static int nsm = 0;
-        if (!nsm) {
-            int dev = 0;
-            OCTEN_CUDA(cudaGetDevice(&dev));
-            OCTEN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        }
+        });
+        int nsm = 0, dev = 0;
+        OCTEN_CUDA(cudaGetDevice(&dev));
+        OCTEN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         const int mt = (M + BM - 1) / BM;
         const long long ntiles = (long long)mt * ((N + BN - 1) / BN);
         const int grid = (int)std::min<long long>(ntiles, nsm);
@@ -768,11 +764,10 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
         OCTEN_CUDA(cudaGetLastError());
         return true;
     }
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    attr.once([&] {
         OCTEN_CUDA(cudaFuncSetAttribute(tc_gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    });
     if ((N + BN - 1) / BN > 65535) return false;
     dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
     tc_gemm_tf32x3_kernel<<<grid, NUM_THREADS, smem, st>>>(mhi, mlo, mx, Z, M, N, K, N, scatter_p, scatter_q,
@@ -796,15 +791,14 @@ bool tc_mode2_tf32x3(const float* Z1, long long N1, int J, int tc, const float* 
     // inner extent ldv (zero-padded past J, a whole number of 16-byte units)
     if (!make_map(&mh, Vhi, (uint64_t)ldv, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, bn2)) return false;
     if (!make_map(&ml, Vlo, (uint64_t)ldv, (uint64_t)P * Q, (uint64_t)ldv * 4, BK, bn2)) return false;
-    auto launch = [&](auto kern, size_t stage_bytes, bool& attr) {
+    auto launch = [&](auto kern, size_t stage_bytes, PerDevice& attr) {
         const size_t smem = M2_STAGES * stage_bytes + 1024 + 256;
-        if (!attr) {
+        attr.once([&] {
             OCTEN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-        }
+        });
         kern<<<P * tc, NUM_THREADS, smem, st>>>(mz, mh, ml, Z2, Q, J, tc, zstride);
     };
-    static bool attr112 = false, attr128 = false;
+    static PerDevice attr112, attr128;
     if (bn2 == 112)
         launch(tc_mode2_tf32x3_kernel<112>, (size_t)m2_stage_bytes<112>(), attr112);
     else

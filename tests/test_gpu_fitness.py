@@ -41,3 +41,40 @@ def test_batch_fitness_matches_numpy(ob, noise, dtype):
         assert st.batch_fitness(np.asfortranarray(x[:, :, 60:70]), 60) > 99.9
     with pytest.raises(ob.ConfigError):
         st.batch_fitness(np.asfortranarray(x[:, :, 60:70]), 65)  # past the slices seen
+
+
+def test_batch_fitness_reference_errors(ob):
+    # eval.cpp:13 zero-norm reference tensor; tensor.cpp DenseTensor rejects
+    # non-finite values before fitness runs
+    x, _ = O.generate_synthetic([30, 28, 20], 2, 9, 0.0, 0.0)
+    x = np.asfortranarray(x)
+    cfg = ob.StreamConfig(rank=2, p=6, q=8, shared=2, seed=3, als=ob.AlsConfig(rank=2, max_iters=50))
+    st = ob.init_stream(x[:, :, :12], cfg)
+    with pytest.raises(ob.NumericError, match="fitness: zero-norm reference tensor"):
+        st.batch_fitness(np.zeros((30, 28, 4), order="F"), 0)
+    bad = np.array(x[:, :, :4], order="F")
+    bad[3, 2, 1] = np.nan
+    with pytest.raises(ob.NumericError, match="DenseTensor: non-finite value"):
+        st.batch_fitness(bad, 0)
+
+
+def test_measured_footprint_matches_accounting(ob):
+    # test_eval.cpp:104-126 on the device-resident state
+    from oracle import rng
+    s = rng.Substream(31)
+    truth = O.KruskalModel([s.fill_uniform(d, 2) for d in (10, 9, 12)], np.ones(2))
+    full = O.reconstruct_fast(truth)
+    cfg = ob.StreamConfig(rank=2, p=4, q=6, shared=2, seed=7, als=ob.AlsConfig(rank=2, max_iters=120))
+    st = ob.init_stream(O.slice_mode(full, 2, 0, 6), cfg)
+    ob.ingest_batch(st, O.slice_mode(full, 2, 6, 6))
+    fp = st.footprint()
+    assert fp["summary_bytes"] == 8 * 4 * 6 * 6 * 6
+    assert fp["replica_bytes"] == 8 * 4 * 6 * (10 + 9)
+    assert fp["accumulator_bytes"] == 8 * 4 * 6 * 2
+    assert fp["factor_bytes"] == 8 * (2 * (10 + 9 + 12) + 2)
+    ref = O.init_stream(O.slice_mode(full, 2, 0, 6), O.StreamConfig(rank=2, p=4, q=6, shared=2, seed=7,
+                                                                     als=O.AlsConfig(2, 120, 1e-8, 3, 0)))
+    O.ingest_batch(ref, O.slice_mode(full, 2, 6, 6))
+    want = O.measure_footprint(ref)
+    for k in want:
+        assert fp[k] == want[k]

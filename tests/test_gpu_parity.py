@@ -57,7 +57,10 @@ def test_compress_f64_matches_oracle(ob, shape):
     I, J, t, Q, P, sh = shape
     rs, u, v, w = _small_replicas(I, J, t, Q, P, sh)
     x = (rng.Substream(9).uniform01_array(I * J * t) * 2 - 1).reshape((I, J, t), order="F")
+    c0 = ob.kernel_counts()
     got = ob.compress(x, u, v, w, sh)
+    c1 = ob.kernel_counts()
+    assert c1["dmma_compress"] - c0["dmma_compress"] == 2  # GEMM1 and mode-2 on the FP64 tensor cores
     for r in range(P):
         want = O.compress(x, rs, r, 0, t)
         assert rel(got[r], want) < 1e-12  # fp64 path
@@ -81,7 +84,15 @@ def test_compress_f32_tcgen05_vs_simt_and_oracle(ob, shape, monkeypatch):
     I, J, t, Q, P, sh = shape
     rs, u, v, w = _small_replicas(I, J, t, Q, P, sh, seed=I + J)
     x = rng.Substream(I * J).uniform01_array(I * J * t).reshape((I, J, t), order="F").astype(np.float32)
+    c0 = ob.kernel_counts()
     got_tc = ob.compress(x, u, v, w, sh)
+    c1 = ob.kernel_counts()
+    # the tensor-core path ran: GEMM1 on tcgen05, and mode-2 too unless J is
+    # not a multiple of 4 (a TMA box alignment limit: that chunk's mode-2 is
+    # the counted SIMT fallback)
+    mode2_tc = J % 4 == 0
+    assert c1["tcgen05"] - c0["tcgen05"] == (2 if mode2_tc else 1)
+    assert c1["simt_fallbacks"] - c0["simt_fallbacks"] == (0 if mode2_tc else 1)
     monkeypatch.setenv("OCTEN_DISABLE_TCGEN05", "1")
     got_simt = ob.compress(x, u, v, w, sh)
     monkeypatch.delenv("OCTEN_DISABLE_TCGEN05")
@@ -192,6 +203,46 @@ def test_recover_nontemporal_matches_oracle(ob):
     got = ob.recover_nontemporal(stack, blocks, 0)
     want = O.recover_nontemporal(stack, proj, 0)
     assert rel(got, want) < 1e-9
+
+
+def _near_dependent_blocks(eps, d=40, q=15, p=4, seed=41):
+    """Projection blocks whose stacked projection has one column within
+    `eps` (relative) of the span of two others: |r_nn| / |r_00| ~ eps."""
+    rs = O.gen_replicas([d, 10], q, p, 3, seed)
+    blocks = [r.nontemporal[0].copy() for r in rs.replicas]
+    noise = rng.Substream(seed + 1)
+    for b in blocks:
+        b[d - 1, :] = 0.5 * (b[0, :] + b[1, :]) + eps * (noise.fill_uniform(1, q)[0] - 0.5)
+    proj = np.vstack([b.T for b in blocks])
+    return blocks, proj
+
+
+@pytest.mark.parametrize("eps", [1e-7, 1e-8])
+def test_recover_nontemporal_qr_band(ob, eps):
+    # |r_nn| / |r_00| between the reference's QR threshold (1e-10,
+    # recovery.cpp:26-38) and what a Gram pivot can resolve (~3e-6): the
+    # reference solves, so must the device (column-pivoted QR fallback)
+    blocks, proj = _near_dependent_blocks(eps)
+    assert O.colpiv_qr_rank(proj, O.K_RANK_TOL) == proj.shape[1]
+    truth = rng.Substream(7).fill_uniform(proj.shape[1], 3)
+    stack = proj @ truth + 1e-9 * rng.Substream(8).fill_uniform(proj.shape[0], 3)
+    got = ob.recover_nontemporal(stack, blocks, 0)
+    want = O.recover_nontemporal(stack, proj, 0)
+    # conditioning ~1/eps: the two least-squares solutions agree to ~eps^-1 ulp
+    assert rel(got, want) < 1e-16 / eps * 1e3
+
+
+def test_recover_nontemporal_qr_band_rank_deficient(ob):
+    # below the reference's threshold both raise the same rank message
+    blocks, proj = _near_dependent_blocks(1e-13)
+    rk = O.colpiv_qr_rank(proj, O.K_RANK_TOL)
+    assert rk == proj.shape[1] - 1
+    stack = np.ones((proj.shape[0], 2))
+    with pytest.raises(O.NumericError):
+        O.recover_nontemporal(stack, proj, 0)
+    with pytest.raises(ob.NumericError, match=r"recover: rank-deficient projection on mode 1 \(rank %d of %d\)"
+                       % (rk, proj.shape[1])):
+        ob.recover_nontemporal(stack, blocks, 0)
 
 
 def test_recover_nontemporal_error_messages(ob):

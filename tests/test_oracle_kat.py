@@ -356,6 +356,33 @@ def test_kruskal_check_and_replica_bound():  # test_recovery.cpp:255-268; accept
         O.replica_bound(10, 10, 10, 5, 5)
 
 
+def test_memory_account_known_answer():  # test_eval.cpp:88-102
+    cfg = O.StreamConfig(rank=5, p=20, q=30)
+    # T = 100 split over two non-temporal modes, t_old = t_new = 5:
+    # 600*(2000 + 5 + 5) + 105*5 + 27000 = 1,233,525
+    sm = O.memory_account(cfg, [50, 50], 5, 5)
+    assert sm["formula_elements"] == 1233525
+    assert sm["predicted_summary_elements"] == 20 * 27000
+    assert sm["predicted_elements"] == (sm["predicted_replica_elements"] + sm["predicted_summary_elements"] +
+                                        sm["predicted_factor_elements"] + sm["predicted_accumulator_elements"])
+    assert sm["ratio"] == pytest.approx(sm["predicted_elements"] / 1233525.0)
+    with pytest.raises(O.ConfigError):
+        O.memory_account(O.StreamConfig(rank=0, p=20, q=30), [50, 50], 5, 5)
+
+
+def test_measured_footprint_matches_accounting():  # test_eval.cpp:104-126
+    truth = random_truth([10, 9, 12], 2, 31)
+    full = O.reconstruct_fast(truth)
+    cfg = O.StreamConfig(rank=2, p=4, q=6, shared=2, seed=7, als=O.AlsConfig(2, 120, 1e-8, 3, 0))
+    st = O.init_stream(O.slice_mode(full, 2, 0, 6), cfg)
+    O.ingest_batch(st, O.slice_mode(full, 2, 6, 6))
+    fp = O.measure_footprint(st)
+    assert fp["summary_bytes"] == 8 * 4 * 6 * 6 * 6
+    assert fp["replica_bytes"] == 8 * 4 * 6 * (10 + 9)
+    assert fp["accumulator_bytes"] == 8 * 4 * 6 * 2
+    assert fp["factor_bytes"] == 8 * (2 * (10 + 9 + 12) + 2)
+
+
 def test_match_columns_known_gauge():  # test_recovery.cpp:304-337
     s = rng.Substream(66)
     stored = []
