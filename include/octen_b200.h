@@ -116,6 +116,28 @@ int octen_stream_prefetch(octen_stream* s, const void* data, int dtype, int orde
  * stream's current model on slices [k0, k0 + t) of the stream, given as a
  * batch I x J x t (dtype/location as octen_stream_ingest); computed on the
  * device without materialising the reconstruction. */
+/* Pipelined ingest_batch (no reference counterpart; same results as
+ * octen_stream_ingest, bit for bit): the batch's compression and CP-ALS run
+ * before the call returns, its alignment/merge runs on a worker thread and
+ * overlaps the next batch's compression and CP-ALS.  An error of that merge
+ * is returned by the next octen_stream_ingest_async / octen_stream_sync (or
+ * any getter), with the reference's "batch N: " prefix; the batch passed to
+ * that call is then not ingested.  The batch buffer may be reused when the
+ * call returns.  Strict streams and the first batch run synchronously. */
+int octen_stream_ingest_async(octen_stream* s, const void* data, int dtype, int location, int order,
+                              const int64_t* dims);
+/* Wait for the pending merge of octen_stream_ingest_async; returns its error. */
+int octen_stream_sync(octen_stream* s);
+/* Model publication for pipelined callers: with on != 0 every finished batch
+ * copies its model to host memory, readable with octen_stream_last_model
+ * without waiting for the merge in flight. */
+int octen_stream_set_publish(octen_stream* s, int on);
+/* The last published model: info[0] = rows of C (slices), info[1] = batches
+ * finished (0: nothing published yet, nothing copied); a (I x R), b (J x R),
+ * c (c_rows_cap x R, first info[0] rows written), lambda (R); col-major. */
+int octen_stream_last_model(octen_stream* s, int64_t* info, double* a, double* b, double* c, int64_t c_rows_cap,
+                            double* lambda);
+
 /* congruence (proj/src/eval.cpp:22-46): per-component factor match score
  * (product over modes of |cos|) after exhaustive (rank <= 6) or greedy
  * matching.  ground/est: factors of every mode stacked, dims[n] x rank

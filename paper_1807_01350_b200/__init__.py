@@ -256,6 +256,47 @@ class StreamState:
         ka = getattr(self, "_pf_keep", [])
         self._pf_keep = (ka + [keep])[-3:]  # the copies read these buffers until ingested
 
+    def ingest_async(self, batch) -> None:
+        """Pipelined ingest_batch (octen_stream_ingest_async): compression and
+        CP-ALS of `batch` run now, its merge overlaps the next call's work.
+        Results equal ingest_batch's bit for bit; a merge error is raised by
+        the next ingest_async / sync / state read."""
+        keep, ptr, dt, loc, dims = _batch_args(batch)
+        d = (C.c_i64 * len(dims))(*dims)
+        _check(C.LIB.octen_stream_ingest_async(self._h, ptr, dt, loc, len(dims), d))
+        del keep
+
+    def sync(self) -> None:
+        """Wait for the merge of the last ingest_async (raises its error)."""
+        _check(C.LIB.octen_stream_sync(self._h))
+
+    def set_publish(self, on: bool = True) -> None:
+        """Every finished batch copies its model to host memory (for
+        pipelined callers: last_model() reads it without waiting)."""
+        _check(C.LIB.octen_stream_set_publish(self._h, 1 if on else 0))
+
+    def last_model(self):
+        """(KruskalModel, batches finished) of the last published model, or
+        (None, 0) before the first publication."""
+        info = (C.c_i64 * 2)()
+        if getattr(self, "_dims", None) is None:
+            self._dims = tuple(self._info()[1:3])  # (waits for the merge in flight once)
+        dims, rank = self._dims, self.config.rank
+        cap = getattr(self, "_last_cap", 0)
+        while True:
+            a = np.zeros((dims[0], rank), order="F")
+            b = np.zeros((dims[1], rank), order="F")
+            c = np.zeros((max(cap, 1), rank), order="F")
+            lam = np.zeros(rank)
+            rc = C.LIB.octen_stream_last_model(self._h, info, _dptr(a), _dptr(b), _dptr(c), max(cap, 1), _dptr(lam))
+            if rc == C.OCTEN_OK or info[0] <= cap:
+                _check(rc)
+                break
+            cap = self._last_cap = int(info[0]) * 2
+        if info[1] == 0:
+            return None, 0
+        return KruskalModel([a, b, c[:info[0]].copy(order="F")], lam), int(info[1])
+
     def footprint(self) -> dict:
         """measure_footprint (eval.cpp:48-60) of the device-resident state."""
         out = (C.c_i64 * 4)()
@@ -297,7 +338,9 @@ def init_stream(first_batch, cfg: StreamConfig) -> StreamState:
     c = cfg._c()
     _check(C.LIB.octen_stream_init(ctypes.byref(c), ptr, dt, loc, len(dims), d, ctypes.byref(h)))
     del keep
-    return StreamState(h, cfg)
+    st = StreamState(h, cfg)
+    st._dims = (dims[0], dims[1])
+    return st
 
 
 def ingest_batch(state: StreamState, batch) -> None:

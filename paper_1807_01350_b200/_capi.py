@@ -62,6 +62,11 @@ SIGNATURES = {
     "octen_stream_ingest": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, P_i64]),
     "octen_stream_destroy": (None, [ctypes.c_void_p]),
+    "octen_stream_ingest_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                                 ctypes.c_int, P_i64]),
+    "octen_stream_sync": (ctypes.c_int, [ctypes.c_void_p]),
+    "octen_stream_set_publish": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "octen_stream_last_model": (ctypes.c_int, [ctypes.c_void_p, P_i64, P_dbl, P_dbl, P_dbl, c_i64, P_dbl]),
     "octen_congruence": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P_i64, P_dbl, P_dbl, P_dbl]),
     "octen_stream_batch_fitness": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                   ctypes.c_int, P_i64, c_i64, P_dbl]),

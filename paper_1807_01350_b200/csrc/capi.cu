@@ -164,6 +164,7 @@ void octen_kernel_counts(int64_t* out) {
 
 int octen_stream_get_stage_times(const octen_stream* s, double* out) {
     return sguard(s, [&] {
+        s->s->sync();
         const auto& x = *s->s;
         for (int i = 0; i < 4; ++i) out[i] = x.dev_ms[i];
         out[4] = x.gemm1_flops;
@@ -190,6 +191,45 @@ int octen_stream_ingest(octen_stream* s, const void* data, int dtype, int locati
         if (!s || !data || !dims) throw octen::ConfigError("octen_stream_ingest: null argument");
         check_dtype(dtype, location);
         s->s->ingest(data, dtype, location, order, dims);
+    });
+}
+
+int octen_stream_ingest_async(octen_stream* s, const void* data, int dtype, int location, int order,
+                              const int64_t* dims) {
+    return sguard(s, [&] {
+        if (!data || !dims) throw octen::ConfigError("octen_stream_ingest_async: null argument");
+        check_dtype(dtype, location);
+        s->s->ingest_async(data, dtype, location, order, dims);
+    });
+}
+
+int octen_stream_sync(octen_stream* s) {
+    return sguard(s, [&] { s->s->sync(); });
+}
+
+int octen_stream_set_publish(octen_stream* s, int on) {
+    return sguard(s, [&] {
+        s->s->sync();
+        s->s->publish = on != 0;
+    });
+}
+
+int octen_stream_last_model(octen_stream* s, int64_t* info, double* a, double* b, double* c, int64_t c_rows_cap,
+                            double* lambda) {
+    return sguard(s, [&] {
+        auto& x = *s->s;
+        std::lock_guard<std::mutex> lk(x.pub_mu);
+        info[0] = x.pub_K;
+        info[1] = x.pub_batches;
+        if (x.pub_batches == 0) return;
+        if (!a || !b || !c || !lambda) throw octen::ConfigError("octen_stream_last_model: null argument");
+        if (c_rows_cap < x.pub_K) throw octen::ConfigError("octen_stream_last_model: c buffer too small");
+        const int R = x.cfg.rank;
+        std::memcpy(a, x.pubA.data(), x.pubA.size() * sizeof(double));
+        std::memcpy(b, x.pubB.data(), x.pubB.size() * sizeof(double));
+        for (int r = 0; r < R; ++r)
+            std::memcpy(c + (size_t)c_rows_cap * r, x.pubC.data() + (size_t)x.pub_K * r, x.pub_K * sizeof(double));
+        std::memcpy(lambda, x.pubLam.data(), R * sizeof(double));
     });
 }
 
@@ -252,6 +292,7 @@ int octen_congruence(int order, int rank, const int64_t* dims, const double* gro
 int octen_stream_batch_fitness(octen_stream* s, const void* data, int dtype, int location, int order,
                                const int64_t* dims, int64_t k0, double* fitness) {
     return sguard(s, [&] {
+        s->s->sync();
         if (!s || !data || !dims || !fitness) throw octen::ConfigError("octen_stream_batch_fitness: null argument");
         check_dtype(dtype, location);
         *fitness = s->s->batch_fitness(data, dtype, location, order, dims, k0);
@@ -268,6 +309,7 @@ int octen_stream_partial_block_size(const octen_stream* s, int64_t* n) {
 int octen_stream_begin_temporal(octen_stream* s, const void* data, int dtype, int location, int order,
                                 const int64_t* dims_local, int64_t k_off, int64_t t_total, double* partial_out) {
     return sguard(s, [&] {
+        s->s->sync();
         if (!s || !dims_local || !partial_out || (!data && dims_local[2] > 0))
             throw octen::ConfigError("octen_stream_begin_temporal: null argument");
         check_dtype(dtype, location);
@@ -284,6 +326,7 @@ int octen_stream_begin_reduced(octen_stream* s, const double* owned_block, doubl
 
 int octen_stream_prefetch(octen_stream* s, const void* data, int dtype, int order, const int64_t* dims) {
     return sguard(s, [&] {
+        s->s->sync();
         if (!s || !data || !dims) throw octen::ConfigError("octen_stream_prefetch: null argument");
         check_dtype(dtype, OCTEN_HOST);
         s->s->prefetch(data, dtype, order, dims);
@@ -325,6 +368,7 @@ int octen_stream_exchange_sizes(const octen_stream* s, int64_t* sizes) {
 int octen_stream_begin(octen_stream* s, const void* data, int dtype, int location, int order, const int64_t* dims,
                        double* models_out) {
     return sguard(s, [&] {
+        s->s->sync();
         if (!s || !data || !dims || !models_out) throw octen::ConfigError("octen_stream_begin: null argument");
         check_dtype(dtype, location);
         s->s->begin(data, dtype, location, order, dims, models_out);
@@ -347,6 +391,7 @@ int octen_stream_finish(octen_stream* s, const double* rows_all) {
 
 int octen_stream_info(const octen_stream* s, int64_t* info) {
     return sguard(s, [&] {
+        s->s->sync();
         const auto& x = *s->s;
         info[0] = 3;
         info[1] = x.I;
@@ -365,6 +410,7 @@ int octen_stream_footprint(const octen_stream* s, int64_t* out) {
     // owned summaries, model, history accumulators); the temporal window is
     // empty between batches, as in the reference.
     return sguard(s, [&] {
+        s->s->sync();
         const auto& x = *s->s;
         const int64_t P = x.cfg.p, Q = x.cfg.q, R = x.cfg.rank;
         out[0] = 8 * P * Q * (x.I + x.J);
@@ -375,11 +421,15 @@ int octen_stream_footprint(const octen_stream* s, int64_t* out) {
 }
 
 int octen_stream_get_factor(const octen_stream* s, int mode, double* out) {
-    return sguard(s, [&] { s->s->get_factor(mode, out); });
+    return sguard(s, [&] {
+        s->s->sync();
+        s->s->get_factor(mode, out);
+    });
 }
 
 int octen_stream_get_model(const octen_stream* s, double* a, double* b, double* c, double* lambda) {
     return sguard(s, [&] {
+        s->s->sync();
         auto& x = *s->s;
         const int R = x.cfg.rank;
         OCTEN_CUDA(cudaMemcpyAsync(a, x.A.p, sizeof(double) * x.I * R, cudaMemcpyDeviceToHost, x.st));
@@ -393,6 +443,7 @@ int octen_stream_get_model(const octen_stream* s, double* a, double* b, double* 
 
 int octen_stream_get_lambda(const octen_stream* s, double* out) {
     return sguard(s, [&] {
+        s->s->sync();
         auto& x = *s->s;
         x.lam.download(out, x.cfg.rank, x.st);
         OCTEN_CUDA(cudaStreamSynchronize(x.st));
@@ -401,6 +452,7 @@ int octen_stream_get_lambda(const octen_stream* s, double* out) {
 
 int octen_stream_get_record(const octen_stream* s, int64_t index, octen_batch_record* out) {
     return sguard(s, [&] {
+        s->s->sync();
         const auto& x = *s->s;
         if (index < 0 || index >= (int64_t)x.log.size()) throw octen::ConfigError("octen_stream_get_record: index");
         const auto& r = x.log[(size_t)index];
@@ -419,6 +471,7 @@ int octen_stream_get_record(const octen_stream* s, int64_t index, octen_batch_re
 
 int octen_stream_get_summaries(const octen_stream* s, double* y) {
     return sguard(s, [&] {
+        s->s->sync();
         auto& x = *s->s;
         const size_t n = (size_t)x.pl * x.cfg.q * x.cfg.q * x.cfg.q;
         x.Y.download(y, n, x.st);
@@ -428,6 +481,7 @@ int octen_stream_get_summaries(const octen_stream* s, double* y) {
 
 int octen_stream_get_history(const octen_stream* s, double* h) {
     return sguard(s, [&] {
+        s->s->sync();
         auto& x = *s->s;
         const int P = x.cfg.p, Q = x.cfg.q, R = x.cfg.rank;
         std::vector<double> stk = x.hist.to_host((size_t)P * Q * R, x.st);
@@ -437,6 +491,7 @@ int octen_stream_get_history(const octen_stream* s, double* h) {
 
 int octen_stream_get_replica_models(const octen_stream* s, double* factors, double* lambda) {
     return sguard(s, [&] {
+        s->s->sync();
         auto& x = *s->s;
         const int P = x.cfg.p, Q = x.cfg.q, R = x.cfg.rank;
         x.MfAll.download(factors, (size_t)P * 3 * Q * R, x.st);

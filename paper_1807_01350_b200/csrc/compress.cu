@@ -97,12 +97,14 @@ struct G3B {  // B(p, k, c) = W[p][(k0 + k) + t c]
     int Q;
     __device__ double operator()(int p, int k, int c) const { return W[(size_t)p * t * Q + (k0 + k) + (size_t)t * c]; }
 };
-struct G3C {  // Y[p][m + Q^2 c] += v
-    double* Y;
+struct G3C {  // Yout[p][m + Q^2 c] = Yin[p][m + Q^2 c] + v   (in place when Yin == Yout)
+    const double* Yin;
+    double* Yout;
     int Q;
     __device__ void operator()(int p, int m, int c, double v) const {
         const size_t q2 = (size_t)Q * Q;
-        Y[(size_t)p * q2 * Q + m + q2 * c] += v;
+        const size_t e = (size_t)p * q2 * Q + m + q2 * c;
+        Yout[e] = Yin[e] + v;
     }
 };
 
@@ -205,16 +207,17 @@ void run_project(CompressEngine& e, const T* dX, std::int64_t t, T* Z1, T* Z2, c
 // Mode 3 for the whole batch, accumulated into the summaries (update_summaries):
 // Y_p += Z2_p (Q^2 x t) W_p (t x Q), fp64.
 template <typename T>
-void run_accumulate(CompressEngine& e, std::int64_t t, const T* Z2, const double* dW, double* dY, cudaStream_t st) {
+void run_accumulate(CompressEngine& e, std::int64_t t, const T* Z2, const double* dW, const double* dYin,
+                    double* dY, cudaStream_t st) {
     const int Q = e.Q, P = e.P;
-    gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<T>{Z2, (int)t, Q}, G3B{dW, t, 0, Q}, G3C{dY, Q}, st);
+    gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<T>{Z2, (int)t, Q}, G3B{dW, t, 0, Q}, G3C{dYin, dY, Q}, st);
     OCTEN_CUDA(cudaGetLastError());
 }
 
 }  // namespace
 
 void accumulate_z2_f32(int P, int Q, std::int64_t t, const float* Z2, const double* dW, double* dY, cudaStream_t st) {
-    gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<float>{Z2, (int)t, Q}, G3B{dW, t, 0, Q}, G3C{dY, Q}, st);
+    gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<float>{Z2, (int)t, Q}, G3B{dW, t, 0, Q}, G3C{dY, dY, Q}, st);
     OCTEN_CUDA(cudaGetLastError());
 }
 
@@ -330,32 +333,33 @@ void CompressEngine::project(const void* dX, int dtype, std::int64_t t, cudaStre
     }
 }
 
-void CompressEngine::accumulate(int dtype, std::int64_t t, const double* dW, double* dY, cudaStream_t st) {
+void CompressEngine::accumulate(int dtype, std::int64_t t, const double* dW, const double* dYin, double* dY,
+                                cudaStream_t st) {
     if (dtype == 1)
-        run_accumulate<float>(*this, t, Z2f.p, dW, dY, st);
+        run_accumulate<float>(*this, t, Z2f.p, dW, dYin, dY, st);
     else
-        run_accumulate<double>(*this, t, Z2d.p, dW, dY, st);
+        run_accumulate<double>(*this, t, Z2d.p, dW, dYin, dY, st);
 }
 
 void CompressEngine::accumulate_rows(int dtype, std::int64_t t, const double* dW, std::int64_t t_total,
                                      std::int64_t k0, double* dY, cudaStream_t st) {
     if (dtype == 1)
-        gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<float>{Z2f.p, (int)t, Q}, G3B{dW, t_total, k0, Q}, G3C{dY, Q},
-                              st);
+        gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<float>{Z2f.p, (int)t, Q}, G3B{dW, t_total, k0, Q},
+                              G3C{dY, dY, Q}, st);
     else
-        gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<double>{Z2d.p, (int)t, Q}, G3B{dW, t_total, k0, Q}, G3C{dY, Q},
-                              st);
+        gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<double>{Z2d.p, (int)t, Q}, G3B{dW, t_total, k0, Q},
+                              G3C{dY, dY, Q}, st);
     OCTEN_CUDA(cudaGetLastError());
 }
 
 void CompressEngine::compress_f32(const float* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st) {
     project(dX, 1, t, st, nullptr, 0, nullptr);
-    accumulate(1, t, dW, dY, st);
+    accumulate(1, t, dW, dY, dY, st);
 }
 
 void CompressEngine::compress_f64(const double* dX, std::int64_t t, const double* dW, double* dY, cudaStream_t st) {
     project(dX, 0, t, st, nullptr, 0, nullptr);
-    accumulate(0, t, dW, dY, st);
+    accumulate(0, t, dW, dY, dY, st);
 }
 
 }  // namespace octen

@@ -100,10 +100,11 @@ public:
     // The same in two phases.  project: modes 1-2 of the whole batch into
     // Z2 (P x Q^2 x t), chunk by chunk; chunk c waits for ready[c] when given
     // (ready_slices slices per chunk) and is scanned for non-finite values
-    // into *flag when flag != null.  accumulate: Y += Z2 x3 W (fp64).
+    // into *flag when flag != null.  accumulate: Y = Yin + Z2 x3 W (fp64; in
+    // place when Yin == Y).
     void project(const void* dX, int dtype, std::int64_t t, cudaStream_t st, const cudaEvent_t* ready,
                  std::int64_t ready_slices, int* flag);
-    void accumulate(int dtype, std::int64_t t, const double* dW, double* dY, cudaStream_t st);
+    void accumulate(int dtype, std::int64_t t, const double* dW, const double* dYin, double* dY, cudaStream_t st);
     // The same for t slices whose temporal rows are rows [k0, k0 + t) of a
     // W with t_total rows per replica (temporal sharding).
     void accumulate_rows(int dtype, std::int64_t t, const double* dW, std::int64_t t_total, std::int64_t k0,

@@ -112,6 +112,11 @@ Stream::Stream(const StreamCfg& c, int rank, int world) : cfg(c), shard_rank(ran
 }
 
 Stream::~Stream() {
+    (void)worker.wait();
+    if (mst) {
+        cudaStreamSynchronize(mst);
+        cudaStreamDestroy(mst);
+    }
     if (st) cudaStreamSynchronize(st);
     if (cp) {
         cudaStreamSynchronize(cp);
@@ -128,6 +133,7 @@ Stream::~Stream() {
         if (e) cudaEventDestroy(e);
     if (pin_ev) cudaEventDestroy(pin_ev);
     if (pin_buf) cudaFreeHost(pin_buf);
+    if (pub_pin) cudaFreeHost(pub_pin);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     for (auto& e : evs)
@@ -198,7 +204,9 @@ void Stream::extend_temporal(std::int64_t t_new) {
             s2.fill_uniform(w + (size_t)t_new * sh, t_new, Q - sh, t_new);
         }
     }
-    upload_mapped(dW, hW.data(), hW.size());
+    next_w_slot();
+    upload_mapped(dWb[wslot], hW.data(), hW.size());
+    dW = dWb[wslot].p;
     ++batches_drawn;
 }
 
@@ -259,7 +267,7 @@ void Stream::check_finite(const void* dX, int dtype, size_t n) {
     if (flag.to_host(1, st)[0]) throw NumericError("DenseTensor: non-finite value");
 }
 
-void Stream::ensure_c_capacity(std::int64_t rows) {
+void Stream::ensure_c_capacity(std::int64_t rows, cudaStream_t st) {
     if (rows <= capC && C.p) return;
     std::int64_t cap = std::max<std::int64_t>(capC * 2, rows);
     cap = std::max<std::int64_t>(cap, 64);
@@ -409,9 +417,88 @@ void Stream::prefetch(const void* data, int dtype, int order, const std::int64_t
     pf.push_back(f);
 }
 
-void Stream::begin(const void* data, int dtype, int location, int order, const std::int64_t* dims,
-                   double* models_out) {
-    if (pending) throw ConfigError("octen: the previous batch has not finished (begin/merge/finish)");
+// ---- per-batch context, worker thread ----
+
+BatchCtx::~BatchCtx() {
+    for (cudaEvent_t& e : ev)
+        if (e) cudaEventDestroy(e);
+}
+
+Worker::~Worker() {
+    if (th.joinable()) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            quit = true;
+        }
+        cv.notify_all();
+        th.join();
+    }
+}
+
+void Worker::loop(int device) {
+    cudaSetDevice(device);
+    std::unique_lock<std::mutex> lk(mu);
+    for (;;) {
+        cv.wait(lk, [&] { return quit || (posted && !running && !done); });
+        if (quit && !(posted && !done)) return;
+        running = true;
+        std::function<void()> f = std::move(task);
+        lk.unlock();
+        std::exception_ptr e;
+        try {
+            f();
+        } catch (...) {
+            e = std::current_exception();
+        }
+        lk.lock();
+        err = e;
+        running = false;
+        done = true;
+        cv.notify_all();
+    }
+}
+
+void Worker::post(int device, std::function<void()> f) {
+    if (!th.joinable()) th = std::thread([this, device] { loop(device); });
+    std::lock_guard<std::mutex> lk(mu);
+    task = std::move(f);
+    err = nullptr;
+    done = false;
+    posted = true;
+    cv.notify_all();
+}
+
+std::exception_ptr Worker::wait() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (!posted) return nullptr;
+    cv.wait(lk, [&] { return done; });
+    posted = false;
+    done = false;
+    std::exception_ptr e = err;
+    err = nullptr;
+    return e;
+}
+
+void Stream::next_w_slot() { wslot ^= 1; }
+
+void Stream::begin_ctx(BatchCtx& b, bool first, std::int64_t t) {
+    b.context = first ? std::string() : "batch " + std::to_string(batches_seen) + ": ";
+    b.pending = true;
+    b.first = first;
+    b.compressed = false;
+    b.t = t;
+    b.t_start = Clock::now();
+    b.rec = BatchRecordC{};
+    b.rec.batch_index = first ? 0 : batches_seen;
+    b.rec.t_new = t;
+    for (cudaEvent_t& e : b.ev)
+        if (!e) OCTEN_CUDA(cudaEventCreate(&e));
+    if (!b.st) b.st = st;
+}
+
+void Stream::begin(BatchCtx& b, const void* data, int dtype, int location, int order, const std::int64_t* dims,
+                   double* models_out, bool out_of_place) {
+    if (b.pending) throw ConfigError("octen: the previous batch has not finished (begin/merge/finish)");
     const bool first = !initialized;
     if (first) {
         prepare(order, dims);
@@ -426,16 +513,11 @@ void Stream::begin(const void* data, int dtype, int location, int order, const s
         if (dims[2] < 1) throw ConfigError("ingest_batch: batch has no temporal extent");
     }
     const std::int64_t t = dims[2];
-    context = first ? std::string() : "batch " + std::to_string(batches_seen) + ": ";
     if (!first && cfg.strict) snapshot(backup);
-    pending = true;
-    pending_first = first;
-    pending_t = t;
-    t_start = Clock::now();
-    prec = BatchRecordC{};
-    prec.batch_index = first ? 0 : batches_seen;
-    prec.t_new = t;
+    begin_ctx(b, first, t);
     const int Q = cfg.q;
+    // out of place (pipelined ingest): Ynext = Y + this batch's compression
+    DevBuf<double>& Yout = out_of_place ? Ynext : Y;
     try {
         auto tc = Clock::now();
         const size_t n = (size_t)I * J * t;
@@ -491,21 +573,26 @@ void Stream::begin(const void* data, int dtype, int location, int order, const s
             const void* dX = stage_input(data, dtype, location, n);
             check_finite(dX, dtype, n);
         }
+        b.tgram.clear();
         extend_temporal(t);
-        if (pl > 0) comp.accumulate(dtype, t, dW.p + (size_t)p0 * t * Q, Y.p, st);
+        b.tgram = tgram;
+        b.dW = dW;
+        if (out_of_place) Ynext.reserve((size_t)std::max(pl, 1) * Q * Q * Q);
+        if (pl > 0) comp.accumulate(dtype, t, dW + (size_t)p0 * t * Q, Y.p, Yout.p, st);
+        b.compressed = true;
         ++batches_seen;
         OCTEN_CUDA(cudaEventRecord(evs[1], st));
         OCTEN_CUDA(cudaStreamSynchronize(st));
-        prec.compress_seconds = std::chrono::duration<double>(Clock::now() - tc).count();
-        als_phase(models_out);
+        b.rec.compress_seconds = std::chrono::duration<double>(Clock::now() - tc).count();
+        als_phase(b, Yout.p, models_out);
     } catch (...) {
-        fail_pending();
+        fail_pending(b);
     }
 }
 
 // CP-ALS of the owned replicas on the updated summaries, packed into this
 // rank's models block (status header + factors + lambdas).
-void Stream::als_phase(double* models_out) {
+void Stream::als_phase(BatchCtx& b, const double* dY, double* models_out) {
     const int Q = cfg.q, R = cfg.rank;
     auto ta = Clock::now();
     OCTEN_CUDA(cudaEventRecord(evs[2], st));
@@ -514,9 +601,9 @@ void Stream::als_phase(double* models_out) {
     if (pl > 0) {
         std::vector<std::uint64_t> seeds(pl);
         for (int r = 0; r < pl; ++r)
-            seeds[r] = rng::derive(cfg.seed, {rng::kStreamAls, (std::uint64_t)(p0 + r), (std::uint64_t)prec.batch_index});
+            seeds[r] = rng::derive(cfg.seed, {rng::kStreamAls, (std::uint64_t)(p0 + r), (std::uint64_t)b.rec.batch_index});
         try {
-            als.run(pl, cfg.als_n_restarts, Q, R, cfg.als_max_iters, cfg.als_rel_tol, Y.p, seeds, st);
+            als.run(pl, cfg.als_n_restarts, Q, R, cfg.als_max_iters, cfg.als_rel_tol, dY, seeds, st);
         } catch (const NumericError&) {
             // a replica's CP-ALS failed: every rank raises it after the exchange
             if (als.failure.kind == 0) throw;
@@ -534,7 +621,17 @@ void Stream::als_phase(double* models_out) {
     OCTEN_CUDA(cudaMemcpyAsync(models_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
     OCTEN_CUDA(cudaEventRecord(evs[3], st));
     OCTEN_CUDA(cudaStreamSynchronize(st));
-    prec.als_seconds = std::chrono::duration<double>(Clock::now() - ta).count();
+    b.rec.als_seconds = std::chrono::duration<double>(Clock::now() - ta).count();
+    // device time of compression and CP-ALS (main stream; the merge adds its own)
+    float ms = 0.f;
+    OCTEN_CUDA(cudaEventElapsedTime(&ms, evs[0], evs[1]));
+    dev_ms[0] += ms;
+    OCTEN_CUDA(cudaEventElapsedTime(&ms, evs[2], evs[3]));
+    dev_ms[1] += ms;
+    dev_ms[3] += comp.collect_gemm1_ms();
+    gemm1_flops = comp.gemm1_flops;
+    gemm1_launches = comp.gemm1_launches;
+    OCTEN_CUDA(cudaEventRecord(b.ev[2], st));
 }
 
 namespace {
@@ -556,7 +653,8 @@ __global__ void set_status_kernel(double* out, int G, size_t blk, const int* fla
 // are drawn here (identically on every rank).
 void Stream::begin_temporal(const void* data, int dtype, int location, int order, const std::int64_t* dims_local,
                             std::int64_t k_off, std::int64_t t_total, double* partial_out) {
-    if (pending) throw ConfigError("octen: the previous batch has not finished (begin/merge/finish)");
+    BatchCtx& b = cur;
+    if (b.pending) throw ConfigError("octen: the previous batch has not finished (begin/merge/finish)");
     if (order != 3) throw ConfigError("ingest_batch: batch order mismatch at batch " + std::to_string(batches_seen));
     const std::int64_t t_local = dims_local[2];
     if (t_total < 1 || k_off < 0 || t_local < 0 || k_off + t_local > t_total)
@@ -575,15 +673,8 @@ void Stream::begin_temporal(const void* data, int dtype, int location, int order
         comp_all.set_projections(cfg.p, cfg.q, cfg.shared, I, J, hU.data(), hV.data(), st);
         comp_all_ready = true;
     }
-    context = first ? std::string() : "batch " + std::to_string(batches_seen) + ": ";
     if (!first && cfg.strict) snapshot(backup);
-    pending = true;
-    pending_first = first;
-    pending_t = t_total;
-    t_start = Clock::now();
-    prec = BatchRecordC{};
-    prec.batch_index = first ? 0 : batches_seen;
-    prec.t_new = t_total;
+    begin_ctx(b, first, t_total);
     tshard_drawn = batches_drawn;
     tshard_tgram = tgram;
     const int P = cfg.p, Q = cfg.q;
@@ -592,6 +683,8 @@ void Stream::begin_temporal(const void* data, int dtype, int location, int order
         auto tc = Clock::now();
         OCTEN_CUDA(cudaEventRecord(evs[0], st));
         extend_temporal(t_total);
+        b.tgram = tgram;
+        b.dW = dW;
         flag.reserve(1);
         flag.zero(1, st);
         Zpart.reserve((size_t)shard_world * chunk * q3);
@@ -599,7 +692,7 @@ void Stream::begin_temporal(const void* data, int dtype, int location, int order
         if (t_local > 0) {
             const void* dX = stage_input(data, dtype, location, (size_t)I * J * t_local);
             comp_all.project(dX, dtype, t_local, st, nullptr, 0, flag.p);
-            comp_all.accumulate_rows(dtype, t_local, dW.p, t_total, k_off, Zpart.p, st);
+            comp_all.accumulate_rows(dtype, t_local, dW, t_total, k_off, Zpart.p, st);
         }
         // replica-contiguous partials -> per-owner blocks with a status slot
         OCTEN_CUDA(cudaMemcpy2DAsync(partial_out, blk * sizeof(double), Zpart.p, (size_t)chunk * q3 * sizeof(double),
@@ -609,12 +702,12 @@ void Stream::begin_temporal(const void* data, int dtype, int location, int order
         OCTEN_CUDA(cudaGetLastError());
         OCTEN_CUDA(cudaEventRecord(evs[1], st));
         OCTEN_CUDA(cudaStreamSynchronize(st));
-        prec.compress_seconds = std::chrono::duration<double>(Clock::now() - tc).count();
+        b.rec.compress_seconds = std::chrono::duration<double>(Clock::now() - tc).count();
         (void)P;
     } catch (...) {
         batches_drawn = tshard_drawn;
         tgram = tshard_tgram;
-        fail_pending();
+        fail_pending(b);
     }
 }
 
@@ -622,7 +715,8 @@ void Stream::begin_temporal(const void* data, int dtype, int location, int order
 // (sum over ranks of their partials; last slot = number of ranks that saw a
 // non-finite value) is added to the owned summaries, then CP-ALS as begin().
 void Stream::begin_reduced(const double* owned_block, double* models_out) {
-    if (!pending) throw ConfigError("octen: begin_reduced without begin_temporal");
+    BatchCtx& b = cur;
+    if (!b.pending) throw ConfigError("octen: begin_reduced without begin_temporal");
     const int Q = cfg.q;
     const size_t q3 = (size_t)Q * Q * Q, blk = (size_t)chunk * q3 + 1;
     try {
@@ -640,18 +734,22 @@ void Stream::begin_reduced(const double* owned_block, double* models_out) {
             OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
         }
+        b.compressed = true;
         ++batches_seen;
-        als_phase(models_out);
+        als_phase(b, Y.p, models_out);
     } catch (...) {
-        fail_pending();
+        fail_pending(b);
     }
 }
 
 // ---- phase 2: align, recover A and B, temporal-stack rows of the owned replicas ----
-void Stream::merge_phase(const double* models_all, double* rows_out) {
-    if (!pending) throw ConfigError("octen: merge without a begun batch");
+void Stream::merge_phase(BatchCtx& b, const double* models_all, double* rows_out) {
+    if (!b.pending) throw ConfigError("octen: merge without a begun batch");
+    cudaStream_t st = b.st;  // the merge's stream (the main one, or the pipelined ingest's merge stream)
     try {
-        t_recover = Clock::now();
+        b.t_recover = Clock::now();
+        if (st != this->st) OCTEN_CUDA(cudaStreamWaitEvent(st, b.ev[2], 0));
+        OCTEN_CUDA(cudaEventRecord(b.ev[0], st));
         static thread_local EvProf sp;
         sp.mark("begin", st);
         const int P = cfg.p, Q = cfg.q, R = cfg.rank;
@@ -678,20 +776,20 @@ void Stream::merge_phase(const double* models_all, double* rows_out) {
         }
         AlignResultHost ar;
         sp.mark("hdr+gather", st);
-        merge.align(MfAll.p, MlamAll.p, tgram, st, &ar);
+        merge.align(MfAll.p, MlamAll.p, b.tgram, st, &ar);
         sp.mark("align", st);
-        prec.min_match_similarity = ar.min_match;
-        prec.max_offdiag_similarity = ar.max_offdiag;
+        b.rec.min_match_similarity = ar.min_match;
+        b.rec.max_offdiag_similarity = ar.max_offdiag;
         Anew.reserve((size_t)I * R);
         Bnew.reserve((size_t)J * R);
-        merge.recover_ab(pending_first ? nullptr : A.p, pending_first ? nullptr : B.p, Anew.p, Bnew.p, st);
+        merge.recover_ab(b.first ? nullptr : A.p, b.first ? nullptr : B.p, Anew.p, Bnew.p, st);
         sp.mark("recover_ab", st);
         if (pl > 0) merge.temporal_stack(Y.p, p0, pl, Anew.p, Bnew.p, rows_out, true, st);
         sp.mark("temporal_stack", st);
         sp.report("merge_phase");
         OCTEN_CUDA(cudaStreamSynchronize(st));
     } catch (...) {
-        fail_pending();
+        fail_pending(b);
     }
 }
 
@@ -711,11 +809,12 @@ __global__ void unpack_rows_kernel(const double* rows_all, size_t per_rank, int 
 }  // namespace
 
 // ---- phase 3: temporal append, model assembly, BatchRecord ----
-void Stream::finish(const double* rows_all) {
-    if (!pending) throw ConfigError("octen: finish without a begun batch");
+void Stream::finish(BatchCtx& b, const double* rows_all) {
+    if (!b.pending) throw ConfigError("octen: finish without a begun batch");
+    cudaStream_t st = b.st;
     try {
         const int P = cfg.p, Q = cfg.q, R = cfg.rank;
-        const std::int64_t t_new = pending_t;
+        const std::int64_t t_new = b.t;
         tstackAll.reserve((size_t)P * Q * R);
         unpack_rows_kernel<<<grid1d((size_t)P * Q * R), 256, 0, st>>>(rows_all, rows_count(), chunk, P, Q, R,
                                                                        tstackAll.p);
@@ -724,20 +823,20 @@ void Stream::finish(const double* rows_all) {
         double residual = 0.0;
         static thread_local EvProf fp;
         fp.mark("begin", st);
-        merge.temporal_append(tstackAll.p, dW.p, t_new, hist.p, rows.p, &residual, st);
+        merge.temporal_append(tstackAll.p, b.dW, t_new, hist.p, rows.p, &residual, st);
         fp.mark("temporal_append", st);
         fp.report("finish");
-        prec.temporal_residual = residual;
-        prec.warned = residual > cfg.residual_warning ? 1 : 0;
-        if (prec.warned && cfg.strict) {
-            if (pending_first)
+        b.rec.temporal_residual = residual;
+        b.rec.warned = residual > cfg.residual_warning ? 1 : 0;
+        if (b.rec.warned && cfg.strict) {
+            if (b.first)
                 throw NumericError("init_stream: temporal solve residual " + std::to_string(residual) +
                                    " exceeds strict threshold");
             throw NumericError("temporal solve residual " + std::to_string(residual) + " exceeds strict threshold");
         }
         // assemble_model (streaming.cpp:162-177): C_raw = [C diag(lambda); rows]
-        ensure_c_capacity(K + t_new);
-        if (!pending_first && K > 0) {
+        ensure_c_capacity(K + t_new, st);
+        if (!b.first && K > 0) {
             scale_cols_kernel<<<grid1d((size_t)K * R), 256, 0, st>>>(C.p, K, capC, R, lam.p);
             OCTEN_LAUNCHED(1);
         }
@@ -748,35 +847,63 @@ void Stream::finish(const double* rows_all) {
         normalize_model_kernel<<<R, 256, 0, st>>>(A.p, I, B.p, J, C.p, K + t_new, capC, lam.p);
         OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
-        OCTEN_CUDA(cudaEventRecord(evs[4], st));
+        OCTEN_CUDA(cudaEventRecord(b.ev[1], st));
+        const std::int64_t Kn = K + t_new;
+        if (publish) {  // D2H of the batch's model (the step's result) into pinned staging
+            const size_t need = (size_t)(I + J + Kn) * R + R;
+            if (need > pub_cap) {
+                OCTEN_CUDA(cudaStreamSynchronize(st));
+                if (pub_pin) OCTEN_CUDA(cudaFreeHost(pub_pin));
+                pub_cap = std::max(need, 2 * pub_cap);
+                OCTEN_CUDA(cudaHostAlloc((void**)&pub_pin, pub_cap * sizeof(double), cudaHostAllocDefault));
+            }
+            OCTEN_CUDA(cudaMemcpyAsync(pub_pin, A.p, sizeof(double) * I * R, cudaMemcpyDeviceToHost, st));
+            OCTEN_CUDA(cudaMemcpyAsync(pub_pin + I * R, B.p, sizeof(double) * J * R, cudaMemcpyDeviceToHost, st));
+            OCTEN_CUDA(cudaMemcpy2DAsync(pub_pin + (I + J) * R, Kn * sizeof(double), C.p, capC * sizeof(double),
+                                         Kn * sizeof(double), R, cudaMemcpyDeviceToHost, st));
+            OCTEN_CUDA(cudaMemcpyAsync(pub_pin + (I + J + Kn) * R, lam.p, sizeof(double) * R, cudaMemcpyDeviceToHost,
+                                       st));
+        }
         OCTEN_CUDA(cudaStreamSynchronize(st));
+        if (publish) {
+            std::lock_guard<std::mutex> lk(pub_mu);
+            pubA.assign(pub_pin, pub_pin + I * R);
+            pubB.assign(pub_pin + I * R, pub_pin + (I + J) * R);
+            pubC.assign(pub_pin + (I + J) * R, pub_pin + (I + J + Kn) * R);
+            pubLam.assign(pub_pin + (I + J + Kn) * R, pub_pin + (I + J + Kn) * R + R);
+            pub_K = Kn;
+            pub_batches = (std::int64_t)log.size() + 1;
+        }
         K += t_new;
-        accumulate_stage_times();
-        prec.recover_seconds = std::chrono::duration<double>(Clock::now() - t_recover).count();
-        prec.total_seconds = std::chrono::duration<double>(Clock::now() - t_start).count();
-        log.push_back(prec);
+        float ms = 0.f;
+        OCTEN_CUDA(cudaEventElapsedTime(&ms, b.ev[0], b.ev[1]));
+        dev_ms[2] += ms;
+        b.rec.recover_seconds = std::chrono::duration<double>(Clock::now() - b.t_recover).count();
+        b.rec.total_seconds = std::chrono::duration<double>(Clock::now() - b.t_start).count();
+        log.push_back(b.rec);
         initialized = true;
-        pending = false;
+        b.pending = false;
     } catch (...) {
-        fail_pending();
+        fail_pending(b);
     }
 }
 
-// Error inside a phase: drain the stream, roll back (strict mode), add the
+// Error inside a phase: drain the streams, roll back (strict mode), add the
 // batch context (streaming.cpp:336-345) and rethrow.
-void Stream::fail_pending() {
+void Stream::fail_pending(BatchCtx& b) {
     cudaStreamSynchronize(st);
+    if (b.st && b.st != st) cudaStreamSynchronize(b.st);
     (void)cudaGetLastError();
-    const bool had = pending;
-    pending = false;
-    const bool first = pending_first;
+    const bool had = b.pending;
+    b.pending = false;
+    const bool first = b.first;
     if (had && !first && cfg.strict) restore(backup);
     try {
         throw;
     } catch (const ConfigError& e) {
-        throw ConfigError(context + e.what());
+        throw ConfigError(b.context + e.what());
     } catch (const NumericError& e) {
-        throw NumericError(context + e.what());
+        throw NumericError(b.context + e.what());
     }
 }
 
@@ -822,31 +949,73 @@ void Stream::restore(Snapshot& s) {
 void Stream::init(const void* data, int dtype, int location, int order, const std::int64_t* dims) {
     xmodels.reserve(models_count() * shard_world);
     xrows.reserve(rows_count() * shard_world);
-    begin(data, dtype, location, order, dims, xmodels.p);
-    merge_phase(xmodels.p, xrows.p);
-    finish(xrows.p);
+    begin(cur, data, dtype, location, order, dims, xmodels.p, false);
+    merge_phase(cur, xmodels.p, xrows.p);
+    finish(cur, xrows.p);
 }
 
 void Stream::ingest(const void* data, int dtype, int location, int order, const std::int64_t* dims) {
     if (shard_world != 1) throw ConfigError("octen: a sharded stream ingests through begin/merge/finish");
+    sync();
     xmodels.reserve(models_count());
     xrows.reserve(rows_count());
-    begin(data, dtype, location, order, dims, xmodels.p);
-    merge_phase(xmodels.p, xrows.p);
-    finish(xrows.p);
+    begin(cur, data, dtype, location, order, dims, xmodels.p, false);
+    merge_phase(cur, xmodels.p, xrows.p);
+    finish(cur, xrows.p);
 }
 
-void Stream::accumulate_stage_times() {
-    float t = 0.f;
-    OCTEN_CUDA(cudaEventElapsedTime(&t, evs[0], evs[1]));
-    dev_ms[0] += t;
-    OCTEN_CUDA(cudaEventElapsedTime(&t, evs[2], evs[3]));
-    dev_ms[1] += t;
-    OCTEN_CUDA(cudaEventElapsedTime(&t, evs[3], evs[4]));
-    dev_ms[2] += t;
-    dev_ms[3] += comp.collect_gemm1_ms();
-    gemm1_flops = comp.gemm1_flops;
-    gemm1_launches = comp.gemm1_launches;
+void Stream::sync() {
+    std::exception_ptr e = worker.wait();
+    if (e) std::rethrow_exception(e);
+}
+
+void Stream::ingest_async(const void* data, int dtype, int location, int order, const std::int64_t* dims) {
+    if (shard_world != 1) throw ConfigError("octen: a sharded stream ingests through begin/merge/finish");
+    if (!initialized || cfg.strict) {
+        ingest(data, dtype, location, order, dims);
+        return;
+    }
+    if (!mst) {
+        int least = 0, greatest = 0;
+        OCTEN_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        // the merge has slack (it is shorter than compression + CP-ALS): the
+        // main stream's kernels go first when both are ready
+        OCTEN_CUDA(cudaStreamCreateWithPriority(&mst, cudaStreamNonBlocking, least));
+    }
+    BatchCtx& b = actx[aslot];
+    b.st = mst;
+    double* models = aslot ? xmodels2.reserve(models_count()) : xmodels.reserve(models_count());
+    const std::int64_t drawn0 = batches_drawn, seen0 = batches_seen;
+    const std::vector<double> tgram0 = tgram;
+    std::exception_ptr begin_err;
+    try {
+        begin(b, data, dtype, location, order, dims, models, true);
+    } catch (...) {
+        begin_err = std::current_exception();
+    }
+    // the previous batch's merge must be complete before Y is replaced
+    std::exception_ptr prev_err = worker.wait();
+    if (prev_err) {
+        // batch b-1 failed in its merge (the reference throws from its
+        // ingest_batch): this batch was never ingested
+        batches_drawn = drawn0;
+        batches_seen = seen0;
+        tgram = tgram0;
+        b.pending = false;
+        std::rethrow_exception(prev_err);
+    }
+    if (begin_err) {
+        // the reference keeps the updated summaries when CP-ALS fails
+        if (b.compressed) Y.swap(Ynext);
+        std::rethrow_exception(begin_err);
+    }
+    Y.swap(Ynext);
+    aslot ^= 1;
+    xrows.reserve(rows_count());
+    worker.post(cfg.device, [this, &b, models] {
+        merge_phase(b, models, xrows.p);
+        finish(b, xrows.p);
+    });
 }
 
 namespace {

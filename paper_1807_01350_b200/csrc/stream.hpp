@@ -6,8 +6,13 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <condition_variable>
 #include <cstdint>
+#include <exception>
+#include <functional>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "devbuf.hpp"
@@ -33,6 +38,44 @@ struct BatchRecordC {
     double compress_seconds, als_seconds, recover_seconds, total_seconds;
 };
 
+// The state of one batch between begin and finish.  The synchronous paths use
+// one (Stream::cur); the pipelined ingest keeps two, since batch b's merge
+// runs on the worker thread while batch b+1 is compressed and decomposed.
+struct BatchCtx {
+    bool pending = false, first = false, compressed = false;
+    std::int64_t t = 0;
+    BatchRecordC rec{};
+    std::string context;
+    std::chrono::steady_clock::time_point t_start, t_recover;
+    cudaStream_t st = nullptr;         // stream of the merge phases
+    cudaEvent_t ev[3] = {};            // merge start / end (device timing), inputs ready on the main stream
+    std::vector<double> tgram;         // shared temporal Gram including this batch's rows (align)
+    const double* dW = nullptr;        // this batch's temporal rows (P x t x Q)
+    ~BatchCtx();
+};
+
+// One persistent host thread that runs posted tasks in order (the merge of
+// the pipelined ingest).  A persistent thread keeps its per-thread device
+// block cache (devbuf.hpp) warm across batches.
+class Worker {
+public:
+    ~Worker();
+    void post(int device, std::function<void()> f);
+    // Wait for the posted task; returns its exception (null if it succeeded
+    // or nothing was posted).
+    std::exception_ptr wait();
+    bool busy() const { return posted; }
+
+private:
+    void loop(int device);
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::function<void()> task;
+    std::exception_ptr err;
+    bool posted = false, running = false, done = false, quit = false;
+};
+
 // One stream handle.  Unsharded (world == 1) it owns every replica.  As rank
 // g of a replica-sharded stream (one process per GPU) it owns replicas
 // [p0, p0 + pl), pl <= chunk = ceil(P / world): it compresses the batch into
@@ -54,6 +97,26 @@ public:
 
     void init(const void* data, int dtype, int location, int order, const std::int64_t* dims);
     void ingest(const void* data, int dtype, int location, int order, const std::int64_t* dims);
+    // Pipelined ingest_batch: compression and CP-ALS of this batch run now;
+    // its alignment/merge runs on the worker thread (own CUDA stream) and
+    // overlaps the next batch's compression and CP-ALS.  The results are the
+    // same bits as ingest(): every stage reads the same inputs (the summaries
+    // are double-buffered, the temporal rows and Gram are per batch).  A
+    // merge error surfaces at the next ingest_async / sync (with its batch
+    // prefix); that next batch is then not ingested.  Strict streams and the
+    // first batch run synchronously.
+    void ingest_async(const void* data, int dtype, int location, int order, const std::int64_t* dims);
+    // Wait for the pending merge; rethrows its error.
+    void sync();
+    // Model publication for pipelined callers: with `publish` on, every
+    // finished batch copies its model (A, B, C, lambda) to host memory; the
+    // copy is read without waiting for the merge in flight.
+    bool publish = false;
+    std::mutex pub_mu;
+    std::vector<double> pubA, pubB, pubC, pubLam;
+    std::int64_t pub_K = 0, pub_batches = 0;
+    double* pub_pin = nullptr;
+    size_t pub_cap = 0;
     void get_factor(int mode, double* out);
     // eval.cpp:10-20 fitness of the model on slices [k0, k0 + t) given as a batch
     double batch_fitness(const void* data, int dtype, int location, int order, const std::int64_t* dims,
@@ -65,8 +128,10 @@ public:
     // pending; the host buffer must not change until the batch is ingested.
     void prefetch(const void* data, int dtype, int order, const std::int64_t* dims);
 
-    void begin(const void* data, int dtype, int location, int order, const std::int64_t* dims, double* models_out);
-    void merge_phase(const double* models_all, double* rows_out);
+    void begin(const void* data, int dtype, int location, int order, const std::int64_t* dims, double* models_out) {
+        begin(cur, data, dtype, location, order, dims, models_out, false);
+    }
+    void merge_phase(const double* models_all, double* rows_out) { merge_phase(cur, models_all, rows_out); }
     // temporal sharding of the compression (octen_stream_begin_temporal /
     // octen_stream_begin_reduced): partial summaries of every replica from
     // this rank's slices, reduce-scattered by the caller, then CP-ALS.
@@ -74,7 +139,7 @@ public:
                         std::int64_t k_off, std::int64_t t_total, double* partial_out);
     void begin_reduced(const double* owned_block, double* models_out);
     size_t partial_block_count() const { return (size_t)chunk * cfg.q * cfg.q * cfg.q + 1; }
-    void finish(const double* rows_all);
+    void finish(const double* rows_all) { finish(cur, rows_all); }
     size_t models_count() const { return 4 + (size_t)chunk * (3 * (size_t)cfg.q * cfg.rank + cfg.rank); }
     size_t rows_count() const { return (size_t)chunk * cfg.q * cfg.rank; }
 
@@ -94,8 +159,15 @@ public:
     AlsEngine als;
     MergeEngine merge;
     // Y: pl x Q^3 (owned replicas); hist: P*Q x R (all replicas, kept redundantly)
-    DevBuf<double> Y, hist, A, B, C, lam, dW, Anew, Bnew, rows, X64;
+    // Ynext: the pipelined ingest's summaries after the batch in flight
+    // (Y + its compression, out of place: the merge of the previous batch
+    // still reads Y); dWb: temporal rows of the last two batches
+    DevBuf<double> Y, Ynext, hist, A, B, C, lam, Anew, Bnew, rows, X64;
+    DevBuf<double> dWb[2];
+    int wslot = 0;
+    double* dW = nullptr;
     DevBuf<double> xmodels, xrows, MfAll, MlamAll, tstackAll;
+    DevBuf<double> xmodels2;     // pipelined ingest: models of the batch in flight
     DevBuf<float> X32;
     DevBuf<int> flag;
     DevBuf<double> Zpart;                 // temporal sharding: partial summaries, world x chunk x Q^3
@@ -123,6 +195,12 @@ public:
     long long gemm1_launches = 0;
     cudaEvent_t evs[6] = {};
 
+    BatchCtx cur;                 // synchronous / sharded phases
+    BatchCtx actx[2];             // pipelined ingest: alternating per batch
+    int aslot = 0;
+    Worker worker;
+    cudaStream_t mst = nullptr;   // merge stream of the pipelined ingest (lower priority)
+
 private:
     using Clock = std::chrono::steady_clock;
     struct Snapshot {
@@ -138,20 +216,19 @@ private:
     void upload_mapped(DevBuf<double>& dst, const double* h, size_t n);
     const void* stage_input(const void* data, int dtype, int location, size_t n);
     void check_finite(const void* dX, int dtype, size_t n);
-    void ensure_c_capacity(std::int64_t rows);
-    void accumulate_stage_times();
-    void als_phase(double* models_out);
+    void ensure_c_capacity(std::int64_t rows, cudaStream_t st);
+    void begin(BatchCtx& b, const void* data, int dtype, int location, int order, const std::int64_t* dims,
+               double* models_out, bool out_of_place);
+    void merge_phase(BatchCtx& b, const double* models_all, double* rows_out);
+    void finish(BatchCtx& b, const double* rows_all);
+    void als_phase(BatchCtx& b, const double* dY, double* models_out);
     void snapshot(Snapshot& s);
     void restore(Snapshot& s);
-    [[noreturn]] void fail_pending();
+    [[noreturn]] void fail_pending(BatchCtx& b);
+    void begin_ctx(BatchCtx& b, bool first, std::int64_t t);
+    void next_w_slot();
 
-    // the batch between begin and finish
-    bool pending = false, pending_first = false;
-    std::int64_t pending_t = 0;
-    BatchRecordC prec{};
-    Clock::time_point t_start, t_recover;
     Snapshot backup;
-    std::string context;
 };
 
 }  // namespace octen
