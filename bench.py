@@ -212,29 +212,95 @@ def cpu_sample(cfg, seed=7, slices=5, replicas=1, cols=2):
     return total, {"compress_s": tc, "als_s": ta, "merge_s": tm}, detail
 
 
+class HostSynth:
+    """The c3/c5 workload on the host for the reference arm: the same recipe as
+    Synth (rank-R U(0,1) factors, lambda = 1, N(0, sigma) noise with sigma =
+    `noise` x the clean RMS of the first slices), generated with numpy, fp32
+    rounded like the device arm's input and handed to the port as fp64."""
+
+    def __init__(self, I, J, K, R, seed, noise):
+        self.g = np.random.default_rng(seed)
+        self.A = self.g.random((I, R))
+        self.B = self.g.random((J, R))
+        self.C = self.g.random((K, R))
+        self.sigma = noise * float(np.sqrt(np.mean(self._clean(0, min(10, K)) ** 2)))
+
+    def _clean(self, k0, t):
+        # X_(0) = A KR(C, B)^T (tensor.cpp unfolding identity), then fold
+        kr = (self.C[k0:k0 + t, None, :] * self.B[None, :, :]).reshape(t * self.B.shape[0], -1)
+        x = self.A @ kr.T  # I x (J t), column j + J k
+        return x.reshape((self.A.shape[0], self.B.shape[0], t), order="F")
+
+    def batch(self, k0, t):
+        x = self._clean(k0, t)
+        x += self.sigma * self.g.standard_normal(x.shape)
+        return np.asfortranarray(x.astype(np.float32).astype(np.float64))
+
+
 def run_reference(args, cfg, rank, world):
+    """The reference arm: the oracle port of the reference (oracle/, a numpy /
+    LAPACK restatement of proj/src; the reference itself cannot be built
+    here) run as the reference runs: full ingest_batch steps
+    (streaming.cpp:258-346) on the same workload, the compression and CP-ALS
+    fanned out over min(cores, P) worker threads (parallel_replicas,
+    streaming.cpp:36-69; BLAS single-threaded inside each worker), the merge
+    with BLAS on every host core.  init_stream on the K0 block is untimed.
+    Rank 0 only; the step time is the mean of the timed ingest_batch calls,
+    with the reference's own BatchRecord stage timers beside it."""
     if rank != 0:
         return
-    import os as _os
-    entries = cfg["I"] * cfg["J"] * cfg["t"]
-    cores = _os.cpu_count()
-    for _ in range(args.warmup):
-        cpu_sample(cfg, slices=2, cols=1)
-    times = []
-    det = None
-    for _ in range(args.steps):
-        tot, parts, det = cpu_sample(cfg, slices=2, cols=1)
-        times.append(tot)
+    from oracle import octen_oracle as O
+    cores = os.cpu_count()
+    I, J, K0, t, Q, P, R, sh = (cfg[k] for k in ("I", "J", "K0", "t", "Q", "P", "R", "shared"))
+    nb = args.warmup + args.steps
+    dseed = 1234
+    syn = HostSynth(I, J, K0 + nb * t, R, dseed, args.noise)
+    scfg = O.StreamConfig(rank=R, p=P, q=Q, shared=sh, seed=7 * dseed + 3,
+                          als=O.AlsConfig(R, cfg["iters"], 1e-8, cfg["restarts"], 0), workers=0)
+    t0 = time.perf_counter()
+    st = O.init_stream(syn.batch(0, K0), scfg)
+    t_init = time.perf_counter() - t0
+    times, recs = [], []
+    for i in range(nb):
+        b = syn.batch(K0 + i * t, t)
+        a = time.perf_counter()
+        O.ingest_batch(st, b)
+        e = time.perf_counter() - a
+        if i >= args.warmup:
+            times.append(e)
+            recs.append(st.log[-1])
     sec = float(np.mean(times))
-    v = entries / sec
+    v = I * J * t / sec
+    workers = O.resolve_workers(scfg)
+    stages = {"compress_s": float(np.mean([r.compress_seconds for r in recs])),
+              "als_s": float(np.mean([r.als_seconds for r in recs])),
+              "recover_s": float(np.mean([r.recover_seconds for r in recs])), "init_s": t_init}
+    sample = ("full ingest_batch steps of the oracle port (numpy/LAPACK restatement of the reference) on the "
+              "%s workload: %d timed + %d warm-up batches of %dx%dx%d after an untimed init_stream on %d slices; "
+              "compress + CP-ALS over %d replica threads, merge with %d-thread BLAS" %
+              (args.config, args.steps, args.warmup, I, J, t, K0, workers, cores))
     line = {"metric": "tensor entries streamed/sec per batch update", "value": v, "unit": "entries/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.config, **cfg},
-            "cpu_baseline": {"value": v, "unit": "entries/s", "cores": cores, "kind": "port", "sample": det},
+            "config": bench_config(args, cfg, int(os.environ.get("WORLD_SIZE", "1"))),
+            "stages_s": stages, "step_s": [round(x, 3) for x in times],
+            "cpu_baseline": {"value": v, "unit": "entries/s", "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def bench_config(args, cfg, world):
+    """The `config` of a bench line (both arms print the same one)."""
+    I, J, t = cfg["I"], cfg["J"], cfg["t"]
+    sharded = world > 1 and args.multi in ("sharded", "temporal")
+    temporal = world > 1 and args.multi == "temporal"
+    par = (("temporal-sharded compression x%d (NCCL reduce-scatter of partial summaries) + replica-sharded "
+            "CP-ALS (NCCL all-gather)" % world) if temporal else
+           ("replica-sharded x%d (NCCL all-gather of replica models)" % world if sharded else
+            ("independent streams x%d" % world if world > 1 else "single")))
+    return {"workload": args.config, **cfg, "noise": args.noise,
+            "l2": "inputs larger than L2 (%d MB fp32 batch)" % (I * J * t * 4 // 10**6), "parallelism": par}
 
 
 # ---------------------------------------------------------------------------
@@ -638,13 +704,7 @@ def main():
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
                 "dtype": "f32 compress (split-TF32/FP32) + f64 CP-ALS/merge", "data": "synthetic",
-                "config": {"workload": args.config, **cfg, "noise": args.noise, "l2": "inputs larger than L2 (%d MB fp32 batch)" % (I * J * t * 4 // 10**6),
-                           "parallelism": (("temporal-sharded compression x%d (NCCL reduce-scatter of partial "
-                                            "summaries) + replica-sharded CP-ALS (NCCL all-gather)" % world)
-                                           if temporal else
-                                           ("replica-sharded x%d (NCCL all-gather of replica models)" % world
-                                            if sharded else ("independent streams x%d" % world if world > 1
-                                                             else "single")))},
+                "config": bench_config(args, cfg, world),
                 "stages": stage, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks}
         if sparse is not None:

@@ -163,6 +163,9 @@ int octen_stream_get_lambda(const octen_stream* s, double* out);
 /* The whole model in one call (one synchronisation): a I x R, b J x R,
  * c K x R (col-major), lambda R. */
 int octen_stream_get_model(const octen_stream* s, double* a, double* b, double* c, double* lambda);
+/* Number of BatchRecords in the stream's log (streaming.hpp:57: one per
+ * successful init/ingest; a failed batch still counts in batches_seen). */
+int octen_stream_log_size(const octen_stream* s, int64_t* n);
 /* BatchRecord of log entry `index` (0 = init). */
 int octen_stream_get_record(const octen_stream* s, int64_t index, octen_batch_record* out);
 /* SummaryState: y (p x Q^3; a sharded handle returns its p_local owned

@@ -1266,14 +1266,57 @@ def _nontemporal_dims_of(t, tmode):
     return [t.shape[n] for n in range(t.ndim) if n != tmode]
 
 
+def resolve_workers(cfg) -> int:
+    """streaming.cpp:36-41: workers = cfg.workers, or min(hardware
+    concurrency, p) when 0."""
+    import os
+    w = cfg.workers if cfg.workers > 0 else min(os.cpu_count() or 1, cfg.p)
+    return max(1, min(w, cfg.p))
+
+
+def parallel_replicas(n: int, workers: int, fn):
+    """streaming.cpp:45-69: fn(i) for i in [0, n) on `workers` threads; slot
+    i is written only by iteration i (deterministic for any worker count);
+    the first exception (lowest index) is rethrown after the join.  BLAS runs
+    single-threaded inside each worker (the reference's Eigen is)."""
+    if workers <= 1 or n <= 1:
+        return [fn(i) for i in range(n)]
+    from concurrent.futures import ThreadPoolExecutor
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    out = [None] * n
+    errs = [None] * n
+
+    def run(i):
+        try:
+            out[i] = fn(i)
+        except Exception as e:  # noqa: BLE001
+            errs[i] = e
+
+    if threadpool_limits is not None:
+        with threadpool_limits(limits=1):
+            with ThreadPoolExecutor(max_workers=workers) as ex:
+                list(ex.map(run, range(n)))
+    else:
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            list(ex.map(run, range(n)))
+    for e in errs:
+        if e is not None:
+            raise e
+    return out
+
+
 def _run_replica_als(st: StreamState, batch_index: int):
     cfg = st.config
-    models = []
-    for r in range(cfg.p):
+
+    def one(r):
         als = AlsConfig(cfg.rank, cfg.als.max_iters, cfg.als.rel_tol, cfg.als.n_restarts,
                         rng.derive(cfg.seed, [rng.K_STREAM_ALS, r, batch_index]))
-        models.append(cp_als(st.summaries.y[r], als).model)
-    return models
+        return cp_als(st.summaries.y[r], als).model
+
+    return parallel_replicas(cfg.p, resolve_workers(cfg), one)
 
 
 def init_stream(first_batch: np.ndarray, cfg_in: StreamConfig) -> StreamState:
@@ -1300,11 +1343,17 @@ def init_stream(first_batch: np.ndarray, cfg_in: StreamConfig) -> StreamState:
     rs = gen_replicas(nt, cfg.q, cfg.p, cfg.shared, cfg.seed, tmode)
     st = StreamState(cfg, rs, init_summaries(rs))
     rec = BatchRecord(0, t0)
+    import time as _time
+    t_begin = _time.perf_counter()
     extend_temporal(st.replicas, t0)
-    z = [compress(first_batch, st.replicas, r, 0, t0) for r in range(cfg.p)]
+    z = parallel_replicas(cfg.p, resolve_workers(cfg), lambda r: compress(first_batch, st.replicas, r, 0, t0))
     update_summaries(st.summaries, z)
+    t_c = _time.perf_counter()
+    rec.compress_seconds = t_c - t_begin
     models = _run_replica_als(st, 0)
     st.replica_models = models
+    t_a = _time.perf_counter()
+    rec.als_seconds = t_a - t_c
     aligned = align_replicas(models, st.replicas)
     rec.min_match_similarity = aligned.min_match_similarity
     rec.max_offdiag_similarity = aligned.max_offdiag_similarity
@@ -1317,6 +1366,8 @@ def init_stream(first_batch: np.ndarray, cfg_in: StreamConfig) -> StreamState:
     st.model = _assemble_model(final, temporal.new_rows, tmode)
     drop_temporal_history(st.replicas)
     st.slices_seen = t0
+    rec.recover_seconds = _time.perf_counter() - t_a
+    rec.total_seconds = _time.perf_counter() - t_begin
     st.log.append(rec)
     return st
 
@@ -1338,13 +1389,20 @@ def ingest_batch(st: StreamState, batch: np.ndarray) -> None:
     backup = copy.deepcopy(st) if st.config.strict else None
     context = "batch %d: " % st.summaries.batches_seen
     try:
+        import time as _time
+        t_begin = _time.perf_counter()
         rec = BatchRecord(st.summaries.batches_seen, t_new)
         k_old = st.slices_seen
         extend_temporal(st.replicas, t_new)
-        z = [compress(batch, st.replicas, r, k_old, k_old + t_new) for r in range(st.config.p)]
+        z = parallel_replicas(st.config.p, resolve_workers(st.config),
+                              lambda r: compress(batch, st.replicas, r, k_old, k_old + t_new))
         update_summaries(st.summaries, z)
+        t_c = _time.perf_counter()
+        rec.compress_seconds = t_c - t_begin
         models = _run_replica_als(st, rec.batch_index)
         st.replica_models = models
+        t_a = _time.perf_counter()
+        rec.als_seconds = t_a - t_c
         aligned = align_replicas(models, st.replicas)
         rec.min_match_similarity = aligned.min_match_similarity
         rec.max_offdiag_similarity = aligned.max_offdiag_similarity
@@ -1359,6 +1417,8 @@ def ingest_batch(st: StreamState, batch: np.ndarray) -> None:
         st.model = _assemble_model(final, temporal_raw, tmode)
         drop_temporal_history(st.replicas)
         st.slices_seen += t_new
+        rec.recover_seconds = _time.perf_counter() - t_a
+        rec.total_seconds = _time.perf_counter() - t_begin
         st.log.append(rec)
     except ConfigError as e:
         if backup is not None:

@@ -191,8 +191,9 @@ class StreamState:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            C.LIB.octen_stream_destroy(h)
+        lib = getattr(C, "LIB", None) if C is not None else None  # None at interpreter shutdown
+        if h and lib is not None:
+            lib.octen_stream_destroy(h)
             self._h = None
 
     def _info(self):
@@ -221,8 +222,9 @@ class StreamState:
     @property
     def log(self) -> List[BatchRecord]:
         out = []
-        n = self._info()[7]
-        for i in range(n):
+        nn = C.c_i64()
+        _check(C.LIB.octen_stream_log_size(self._h, ctypes.byref(nn)))
+        for i in range(nn.value):
             r = C.BatchRecordC()
             _check(C.LIB.octen_stream_get_record(self._h, i, ctypes.byref(r)))
             out.append(BatchRecord(r.batch_index, r.t_new, r.temporal_residual, r.min_match_similarity,
@@ -663,8 +665,9 @@ class CooSummaries:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            C.LIB.octen_coo_destroy(h)
+        lib = getattr(C, "LIB", None) if C is not None else None
+        if h is not None and h.value and lib is not None:
+            lib.octen_coo_destroy(h)
             self._h = None
 
     def compress(self, batch: SparseTensor, w) -> None:

@@ -65,6 +65,7 @@ SIGNATURES = {
     "octen_stream_ingest_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                  ctypes.c_int, P_i64]),
     "octen_stream_sync": (ctypes.c_int, [ctypes.c_void_p]),
+    "octen_stream_log_size": (ctypes.c_int, [ctypes.c_void_p, P_i64]),
     "octen_stream_set_publish": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "octen_stream_last_model": (ctypes.c_int, [ctypes.c_void_p, P_i64, P_dbl, P_dbl, P_dbl, c_i64, P_dbl]),
     "octen_congruence": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P_i64, P_dbl, P_dbl, P_dbl]),

@@ -25,6 +25,7 @@
 #include "engine.hpp"
 #include "evprof.hpp"
 #include "gemm_dmma.cuh"
+#include "h2d_param.cuh"
 #include "rng_host.hpp"
 #include "small_linalg.cuh"
 
@@ -1118,6 +1119,11 @@ AlsEngine::~AlsEngine() {
         cudaStreamSynchronize(gemm_st);
         cudaStreamDestroy(gemm_st);
     }
+    for (cudaStream_t ls : lane_gemm)
+        if (ls) {
+            cudaStreamSynchronize(ls);
+            cudaStreamDestroy(ls);
+        }
     if (hact) cudaFreeHost(hact);
     for (cudaEvent_t e : lane_ev)
         if (e) cudaEventDestroy(e);
@@ -1218,15 +1224,18 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
                 for (int i = 0; i < Q; ++i) w2[i] = ws.uniform01() * 2 - 1;
             }
         }
-    Wmix.upload(hw.data(), hw.size(), st);
-    rescue_seed.upload(hres.data(), NP, st);
+    Wmix.reserve(hw.size());
+    h2d_param(Wmix.p, hw.data(), hw.size() * sizeof(double), st);
+    rescue_seed.reserve(NP);
+    h2d_param(rescue_seed.p, hres.data(), NP * sizeof(std::uint64_t), st);
 
     // ---- GEVD init (usable when Q >= R and Q >= 2; cp_als.cpp:64)
     std::vector<int> used(NP, -1);
     const bool shape_ok = (Q >= R) && (Q >= 2);
     if (shape_ok) {
         std::vector<int> ones(P, 1);
-        usable.upload(ones.data(), P, st);
+        usable.reserve(P);
+        h2d_param(usable.p, ones.data(), P * sizeof(int), st);
         const int ks = pick_ksplit(P, Q, Q, (int)q2);
         ws.reserve((size_t)P * ks * q2);
         const bool gpipe = (Q % 2 == 0) && ((uintptr_t)dY % 16 == 0);
@@ -1283,8 +1292,10 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             bool any = false;
             for (int prob = 0; prob < NP; ++prob) any |= td[prob] != 0;
             if (!any) break;
-            att_start.upload(start.data(), NP, st);
-            todo.upload(td.data(), NP, st);
+            att_start.reserve(NP);
+            h2d_param(att_start.p, start.data(), NP * sizeof(int), st);
+            todo.reserve(NP);
+            h2d_param(todo.p, td.data(), NP * sizeof(int), st);
             peel_fail.zero(NP, st);
             const size_t smem_pen = (size_t)(5 * R * R + 7 * R + 72) * sizeof(double);
             OCTEN_PROF("mix", st);
@@ -1369,6 +1380,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     // 16-byte pairs along every fast index need an even Q (and aligned bases)
     const bool pipe_ok = (Q % 2 == 0) && ((uintptr_t)dY % 16 == 0) && ((uintptr_t)F.p % 16 == 0) &&
                          ((uintptr_t)KR.p % 16 == 0);
+
     // Up to four lanes (replica slices, each on its own stream): the
     // latency-bound per-problem kernels of one lane overlap the DMMA GEMMs of
     // the other.  Lane 1 starts half a phase late (after lane 0's first
@@ -1378,6 +1390,19 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     int L = 4;  // measured: 1 lane 14.1 ms, 2 lanes 13.5, 4 lanes 13.4 (c3 CP-ALS stage)
     if (const char* ev = std::getenv("OCTEN_ALS_LANES")) L = std::max(1, std::min(kMaxLanes, std::atoi(ev)));
     L = std::min(L, P);
+    int nsm = 148;
+    {
+        int dev = 0;
+        OCTEN_CUDA(cudaGetDevice(&dev));
+        OCTEN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    // OCTEN_ALS_LANE_CTAS > 0 caps each lane's T-GEMM grid (a persistent
+    // tile loop on a share of the SMs).  Measured at c3 with the pipelined
+    // merge: one CTA per tile (0, the default) 13.9 ms per step, 296 CTAs
+    // 14.0, 148 14.5, 74 16.7: the lanes' GEMMs already overlap each other.
+    int lane_ctas = 0;
+    if (const char* ev = std::getenv("OCTEN_ALS_LANE_CTAS")) lane_ctas = std::max(0, std::atoi(ev));
+    (void)nsm;
     int lp0[kMaxLanes], lp1[kMaxLanes];
     for (int l = 0; l < L; ++l) {
         lp0[l] = (int)((long long)P * l / L);
@@ -1389,11 +1414,15 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     // streams: lane l's mode updates overlap the other lanes' GEMMs.
     // (Measured slower at c3: a lane's 4-replica GEMM alone is ~1.07 waves.
     // Off unless OCTEN_ALS_GEMM_STREAM=1.)
-    static const bool gsplit_env = [] {
+    // OCTEN_ALS_GEMM_STREAM=2: the same split with one low-priority GEMM
+    // stream per lane, so the lanes' GEMMs still run side by side while the
+    // update kernels take the SMs first when both are ready.
+    static const int gsplit_env = [] {
         const char* e = std::getenv("OCTEN_ALS_GEMM_STREAM");
-        return e && e[0] == '1';
+        return e ? std::atoi(e) : 0;
     }();
-    const bool gsplit = gsplit_env && L > 1;
+    const bool gsplit = gsplit_env >= 1 && L > 1;
+    const bool gper = gsplit_env == 2;
     if (!lane_st[1]) {
         for (int l = 0; l < kMaxLanes; ++l) OCTEN_CUDA(cudaStreamCreateWithFlags(&lane_st[l], cudaStreamNonBlocking));
     }
@@ -1401,8 +1430,10 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         int least = 0, greatest = 0;
         OCTEN_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         OCTEN_CUDA(cudaStreamCreateWithPriority(&gemm_st, cudaStreamNonBlocking, least));
-        for (int l = 0; l < kMaxLanes; ++l)
+        for (int l = 0; l < kMaxLanes; ++l) {
             OCTEN_CUDA(cudaStreamCreateWithPriority(&lane_hp[l], cudaStreamNonBlocking, greatest));
+            OCTEN_CUDA(cudaStreamCreateWithPriority(&lane_gemm[l], cudaStreamNonBlocking, least));
+        }
     }
     for (cudaEvent_t& e : lane_ev)
         if (!e) OCTEN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1448,6 +1479,8 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         for (int l = 0; l < L; ++l)
             if (ls[l] != st) OCTEN_CUDA(cudaStreamWaitEvent(ls[l], lane_ev[0], 0));
         if (gsplit) OCTEN_CUDA(cudaStreamWaitEvent(gemm_st, lane_ev[0], 0));
+        if (gsplit && gper)
+            for (int l = 0; l < L; ++l) OCTEN_CUDA(cudaStreamWaitEvent(lane_gemm[l], lane_ev[0], 0));
     }
     // OCTEN_ALS_PROFILE: CUDA events between the kernels of lane 0's sweeps,
     // averaged per sweep parity and label (diagnostics)
@@ -1483,35 +1516,35 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             cudaStream_t gs = ss;
             bool pd = use_pdl;
             if (gsplit) {
+                gs = gper ? lane_gemm[l] : gemm_st;
                 OCTEN_CUDA(cudaEventRecord(lane_ev[kGin + l], ss));
-                OCTEN_CUDA(cudaStreamWaitEvent(gemm_st, lane_ev[kGin + l], 0));
-                gs = gemm_st;
+                OCTEN_CUDA(cudaStreamWaitEvent(gs, lane_ev[kGin + l], 0));
                 pd = false;
             }
             if (contracted == 2) {  // rows (i, j)
                 if (pipe_ok)
                     gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmatP{x.Y, q3, q2}, FacP{x.F, S, Q, R, 2},
-                                         TStore{x.T, q2, SR}, gs, 1, nullptr, pd);
+                                         TStore{x.T, q2, SR}, gs, 1, nullptr, pd, lane_ctas);
                 else
                     gemm_f64<false, true>(pn, (int)q2, SR, Q, YmatA{x.Y, q3, q2, S, false}, FacB{x.F, S, Q, R, 2},
                                           TStore{x.T, q2, SR}, gs);
             } else if (contracted == 1) {  // rows (i, k)
                 if (pipe_ok)
                     gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmidP{x.Y, q3, (unsigned)Q, qinv}, FacP{x.F, S, Q, R, 1},
-                                         TStore{x.T, q2, SR}, gs, 1, nullptr, pd);
+                                         TStore{x.T, q2, SR}, gs, 1, nullptr, pd, lane_ctas);
                 else
                     gemm_f64<false, true>(pn, (int)q2, SR, Q, YmidA{x.Y, q3, Q}, FacB{x.F, S, Q, R, 1},
                                           TStore{x.T, q2, SR}, gs);
             } else {  // rows (j, k)
                 if (pipe_ok)
                     gemm_f64_pipe<true>(pn, (int)q2, SR, Q, Y0tP{x.Y, q3, Q}, FacP{x.F, S, Q, R, 0},
-                                        TStore{x.T, q2, SR}, gs, 1, nullptr, pd);
+                                        TStore{x.T, q2, SR}, gs, 1, nullptr, pd, lane_ctas);
                 else
                     gemm_f64<true, true>(pn, (int)q2, SR, Q, Y0tA{x.Y, q3, Q}, FacB{x.F, S, Q, R, 0},
                                          TStore{x.T, q2, SR}, gs);
             }
             if (gsplit) {
-                OCTEN_CUDA(cudaEventRecord(lane_ev[kGout + l], gemm_st));
+                OCTEN_CUDA(cudaEventRecord(lane_ev[kGout + l], gs));
                 OCTEN_CUDA(cudaStreamWaitEvent(ss, lane_ev[kGout + l], 0));
             }
             mark(l, sw, contracted == 2 ? "gemm Yx3C" : contracted == 1 ? "gemm Yx2B" : "gemm Yx1A", ss);

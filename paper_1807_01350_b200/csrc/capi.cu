@@ -326,7 +326,7 @@ int octen_stream_begin_reduced(octen_stream* s, const double* owned_block, doubl
 
 int octen_stream_prefetch(octen_stream* s, const void* data, int dtype, int order, const int64_t* dims) {
     return sguard(s, [&] {
-        s->s->sync();
+        // no sync: the prefetch touches only the main thread's staging state
         if (!s || !data || !dims) throw octen::ConfigError("octen_stream_prefetch: null argument");
         check_dtype(dtype, OCTEN_HOST);
         s->s->prefetch(data, dtype, order, dims);
@@ -447,6 +447,13 @@ int octen_stream_get_lambda(const octen_stream* s, double* out) {
         auto& x = *s->s;
         x.lam.download(out, x.cfg.rank, x.st);
         OCTEN_CUDA(cudaStreamSynchronize(x.st));
+    });
+}
+
+int octen_stream_log_size(const octen_stream* s, int64_t* n) {
+    return sguard(s, [&] {
+        s->s->sync();
+        *n = (int64_t)s->s->log.size();
     });
 }
 

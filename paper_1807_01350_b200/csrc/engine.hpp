@@ -71,6 +71,7 @@ private:
     cudaStream_t lane_st[kMaxLanes] = {};   // sweep lanes 1..L-1 (lane 0 runs on the caller's stream)
     cudaStream_t lane_hp[kMaxLanes] = {};   // OCTEN_ALS_GEMM_STREAM=1: high-priority lanes
     cudaStream_t gemm_st = nullptr;         //   and the lanes' T-GEMMs (low priority)
+    cudaStream_t lane_gemm[kMaxLanes] = {}; // OCTEN_ALS_GEMM_STREAM=2: one low-priority GEMM stream per lane
     // lane_ev: [0] fork/join, [kGin + l] lane -> GEMM stream, [kGout + l]
     // GEMM stream -> lane, [kSweepEv + 4 (sweep & 1) + l] end of a sweep
     static constexpr int kGin = 1, kGout = 1 + kMaxLanes, kSweepEv = 1 + 2 * kMaxLanes;

@@ -24,6 +24,7 @@
 
 #include "chol_batched.cuh"
 #include "colpiv_qr.cuh"
+#include "h2d_param.cuh"
 #include "engine.hpp"
 #include "evprof.hpp"
 #include "gemm_dmma.cuh"
@@ -968,11 +969,11 @@ void MergeEngine::align(const double* dMf, const double* dMlam, const std::vecto
     Lwt.reserve((size_t)std::max(1, sh * sh));
     iscr.zero(8, st);
     if (sh > 0 && (int)tgram.size() == sh * sh) {
-        OCTEN_CUDA(cudaMemcpyAsync(Lwt.p, tgram.data(), sizeof(double) * sh * sh, cudaMemcpyHostToDevice, st));
+        h2d_param(Lwt.p, tgram.data(), sizeof(double) * sh * sh, st);
         chol_small_from_host_kernel<<<1, 32, 0, st>>>(Lwt.p, sh, iscr.p + 2); OCTEN_LAUNCHED(1);
     }
     std::vector<int> wok = {white_ok[0], white_ok[1], 0};
-    OCTEN_CUDA(cudaMemcpyAsync(iscr.p, wok.data(), 2 * sizeof(int), cudaMemcpyHostToDevice, st));
+    h2d_param(iscr.p, wok.data(), 2 * sizeof(int), st);
     double* scales_d = red.p;
     double* minsim_d = red.p + (size_t)P * 3 * R;
     double* maxoff_d = minsim_d + P;
@@ -1327,7 +1328,7 @@ void MergeEngine::recover_ab(const double* dStoredA, const double* dStoredB, dou
     } else {
         std::vector<int> id(R);
         for (int i = 0; i < R; ++i) id[i] = i;
-        perm.upload(id.data(), R, st);
+        h2d_param(perm.p, id.data(), R * sizeof(int), st);
         finalize_kernel<<<R, 256, 0, st>>>(R, dims[0], solved[0].p, perm.p, nullptr, dAfin, err.p, 0); OCTEN_LAUNCHED(1);
         finalize_kernel<<<R, 256, 0, st>>>(R, dims[1], solved[1].p, perm.p, nullptr, dBfin, err.p + 1, 1); OCTEN_LAUNCHED(1);
         last_perm = id;

@@ -22,6 +22,7 @@
 #include "rng_host.hpp"
 #include "stream.hpp"
 #include "evprof.hpp"
+#include "h2d_param.cuh"
 
 namespace octen {
 
@@ -397,8 +398,12 @@ void Stream::prefetch(const void* data, int dtype, int order, const std::int64_t
     // takes the faster copy engine.
     cudaPointerAttributes at{};
     const void* mapped = nullptr;
-    if (!pf.empty() && cudaPointerGetAttributes(&at, data) == cudaSuccess && at.type == cudaMemoryTypeHost &&
-        at.devicePointer)
+    static const bool use_ce = [] {  // OCTEN_PREFETCH_CE=1: background copies on the copy engine too
+        const char* e = std::getenv("OCTEN_PREFETCH_CE");
+        return e && e[0] == '1';
+    }();
+    if (!use_ce && !pf.empty() && cudaPointerGetAttributes(&at, data) == cudaSuccess &&
+        at.type == cudaMemoryTypeHost && at.devicePointer)
         mapped = at.devicePointer;
     (void)cudaGetLastError();
     for (std::int64_t c = 0; c < f.nch; ++c) {
@@ -618,7 +623,7 @@ void Stream::als_phase(BatchCtx& b, const double* dY, double* models_out) {
                                        cudaMemcpyDeviceToDevice, st));
         }
     }
-    OCTEN_CUDA(cudaMemcpyAsync(models_out, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
+    h2d_param(models_out, hdr, sizeof(hdr), st);
     OCTEN_CUDA(cudaEventRecord(evs[3], st));
     OCTEN_CUDA(cudaStreamSynchronize(st));
     b.rec.als_seconds = std::chrono::duration<double>(Clock::now() - ta).count();
