@@ -344,6 +344,26 @@ def ls_solve(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return np.linalg.lstsq(a, b, rcond=None)[0]
 
 
+def colpiv_qr_solve(a: np.ndarray, b: np.ndarray, threshold: float):
+    """One ColPivHouseholderQR (Eigen) with setThreshold(threshold): returns
+    (rank, x) with rank = #|r_ii| > threshold * max|r_jj| and, when the rank
+    is full, x = P R^-1 (Q^T b) (else x = None) -- the rank test and the
+    solve of recovery.cpp:26-38 / 396-401 from the same factorization."""
+    if a.size == 0:
+        return 0, None
+    qm, rm, piv = sla.qr(a, mode="economic", pivoting=True)
+    d = np.abs(np.diag(rm))
+    if d.size == 0 or d.max() == 0.0:
+        return 0, None
+    rank = int(np.sum(d > threshold * d.max()))
+    if rank < a.shape[1]:
+        return rank, None
+    z = sla.solve_triangular(rm, qm.T @ b, lower=False)
+    x = np.empty_like(z)
+    x[piv] = z
+    return rank, x
+
+
 def cod_solve(a: np.ndarray, b: np.ndarray, threshold: Optional[float] = None) -> np.ndarray:
     """Eigen CompleteOrthogonalDecomposition(a).solve(b): minimum-norm LS with
     a rank-revealing pivoted QR (LAPACK gelsy).  Default threshold is Eigen's
@@ -697,11 +717,11 @@ def checked_solve(proj: np.ndarray, rhs: np.ndarray, mode: int) -> np.ndarray:
     if proj.shape[0] < proj.shape[1]:
         raise NumericError("recover: mode %d projection is %dx%d; p*Q must reach the mode extent "
                            "(raise p per the replica bound)" % (mode + 1, proj.shape[0], proj.shape[1]))
-    rank = colpiv_qr_rank(proj, K_RANK_TOL)
+    rank, x = colpiv_qr_solve(proj, rhs, K_RANK_TOL)
     if rank < proj.shape[1]:
         raise NumericError("recover: rank-deficient projection on mode %d (rank %d of %d)"
                            % (mode + 1, rank, proj.shape[1]))
-    return ls_solve(proj, rhs)
+    return x
 
 
 def greedy_match(sim: np.ndarray, tie_tol: float = 1e-9, log=None):
@@ -923,11 +943,18 @@ def recover_nontemporal_weighted(stacked_factor, stacked_projection, mode: int, 
     if stacked_factor.shape[0] != stacked_projection.shape[0]:
         raise ConfigError("recover_nontemporal: stack and projection row counts differ")
     rank = stacked_factor.shape[1]
-    p = col_weights.shape[0]
     out = np.zeros((stacked_projection.shape[1], rank))
-    for r in range(rank):
+
+    def one(r):
         w = np.repeat(col_weights[:, r], q)
-        out[:, r] = checked_solve(stacked_projection * w[:, None], stacked_factor[:, r] * w, mode)
+        return checked_solve(stacked_projection * w[:, None], stacked_factor[:, r] * w, mode)
+
+    # the R column solves are independent (the reference runs them in a
+    # loop); the port spreads them over the host cores, lowest column's
+    # error first
+    import os
+    for r, x in enumerate(parallel_replicas(rank, os.cpu_count() or 1, one)):
+        out[:, r] = x
     return out
 
 
@@ -960,7 +987,8 @@ def recover_temporal_append(temporal_stack, rs: ReplicaSet, summaries: SummarySt
         raise NumericError("recover_temporal_append: p*Q too small for the batch extent")
     new_rows = np.zeros((t_new, rank))
     res_sq = rhs_sq = 0.0
-    for r in range(rank):
+
+    def one(r):
         rhs = temporal_stack[:, r].copy()
         hist_col = history[:, r].copy()
         wproj = proj.copy()
@@ -974,9 +1002,9 @@ def recover_temporal_append(temporal_stack, rs: ReplicaSet, summaries: SummarySt
             fitted = rhs - wproj @ solved
         else:
             system = np.hstack([wproj, hist_col[:, None]])
-            if colpiv_qr_rank(system, K_RANK_TOL) < system.shape[1]:
+            qrank, sol = colpiv_qr_solve(system, rhs, K_RANK_TOL)
+            if qrank < system.shape[1]:
                 raise NumericError("recover_temporal_append: rank-deficient joint system")
-            sol = ls_solve(system, rhs)
             gauge = float(sol[t_new])
             if not math.isfinite(gauge):
                 raise NumericError("recover_temporal_append: non-finite history gauge")
@@ -986,9 +1014,15 @@ def recover_temporal_append(temporal_stack, rs: ReplicaSet, summaries: SummarySt
             else:
                 solved = sol[:t_new] / gauge
             fitted = rhs - gauge * (hist_col + wproj @ solved)
+        return solved, float(fitted @ fitted), float(rhs @ rhs)
+
+    # independent per-column solves (a loop in the reference), spread over
+    # the host cores; sums in column order
+    import os
+    for r, (solved, f2, r2) in enumerate(parallel_replicas(rank, os.cpu_count() or 1, one)):
         new_rows[:, r] = solved
-        res_sq += float(fitted @ fitted)
-        rhs_sq += float(rhs @ rhs)
+        res_sq += f2
+        rhs_sq += r2
     rel = math.sqrt(res_sq / rhs_sq) if rhs_sq > 0.0 else 0.0
     for rep in range(p):
         w_new = rs.replicas[rep].temporal_rows(k_old, k_old + t_new)

@@ -387,20 +387,20 @@ void Stream::prefetch(const void* data, int dtype, int order, const std::int64_t
     }
     // the slot's previous batch must have been read by the compression
     OCTEN_CUDA(cudaStreamWaitEvent(pcp, slot_free[f.slot], 0));
-    // Pinned (device-mapped) host memory is pulled by a small kernel (8 CTAs,
-    // 8 x 16 B loads in flight per thread: far more than PCIe needs) on the
-    // low-priority copy stream.  The copy engines stay free, so the small H2D
-    // transfers of the batch being processed (ALS/merge parameters) are not
-    // queued behind this batch.  Pageable memory goes through the copy engine.
-    // The pull kernel is for BACKGROUND copies only (another prefetch is
-    // pending, so this batch is not the next one consumed and its copy will
-    // overlap device work); a copy that the next ingest waits for anyway
-    // takes the faster copy engine.
+    // The copy runs on the low-priority copy stream through the copy engine.
+    // The small per-batch H2D parameter uploads of the batch being processed
+    // are read by kernels from mapped host memory (h2d_param.cuh), so they do
+    // not queue behind this DMA.  With OCTEN_PREFETCH_PULL=1 a BACKGROUND copy
+    // (another prefetch is pending) of pinned memory is pulled by an 8-CTA
+    // kernel instead (the round-1 scheme, before the parameter bypass).
     cudaPointerAttributes at{};
     const void* mapped = nullptr;
-    static const bool use_ce = [] {  // OCTEN_PREFETCH_CE=1: background copies on the copy engine too
-        const char* e = std::getenv("OCTEN_PREFETCH_CE");
-        return e && e[0] == '1';
+    // Background copies go through the copy engine (55 GB/s measured; the
+    // per-batch parameter uploads bypass it, h2d_param.cuh).  OCTEN_PREFETCH_PULL=1
+    // pulls them with an 8-CTA kernel instead (c3 e2e 15.2 vs 14.7 ms/step).
+    static const bool use_ce = [] {
+        const char* e = std::getenv("OCTEN_PREFETCH_PULL");
+        return !(e && e[0] == '1');
     }();
     if (!use_ce && !pf.empty() && cudaPointerGetAttributes(&at, data) == cudaSuccess &&
         at.type == cudaMemoryTypeHost && at.devicePointer)
@@ -541,7 +541,22 @@ void Stream::begin(BatchCtx& b, const void* data, int dtype, int location, int o
                 const Prefetch f = pf.front();
                 pf.erase(pf.begin());
                 const void* dst = dtype == 1 ? (const void*)PX32[f.slot].p : (const void*)PX64[f.slot].p;
-                comp.project(dst, dtype, t, st, pf_ev[f.slot].data(), f.sub, flag.p);
+                // a copy that has already landed is contracted in one chunk
+                // (the chunks only exist to overlap a copy still in flight)
+                bool landed = true;
+                for (std::int64_t c = 0; c < f.nch && landed; ++c) {
+                    const cudaError_t q = cudaEventQuery(pf_ev[f.slot][c]);
+                    if (q == cudaErrorNotReady) {
+                        landed = false;
+                        (void)cudaGetLastError();
+                    } else {
+                        OCTEN_CUDA(q);
+                    }
+                }
+                if (landed)
+                    comp.project(dst, dtype, t, st, nullptr, 0, flag.p);
+                else
+                    comp.project(dst, dtype, t, st, pf_ev[f.slot].data(), f.sub, flag.p);
                 OCTEN_CUDA(cudaEventRecord(slot_free[f.slot], st));
             } else if (location == 0) {
                 const std::int64_t sub = std::max<std::int64_t>(
