@@ -55,6 +55,46 @@ def peaks():
         return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
+def pipe_peaks():
+    """Measured arithmetic peaks of the pipes the path uses
+    (scripts/micro/peaks.cu on this pool's B200, profiles/peaks_b200.json):
+    tcgen05 kind::tf32, DMMA fp64, FFMA fp32."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks_b200.json")) as f:
+            d = json.load(f)
+        return {"tf32": float(d["tcgen05_tf32_tflops"]), "dmma": float(d["dmma_f64_tflops"]),
+                "ffma": float(d["ffma_f32_tflops"]), "source": "measured (profiles/peaks_b200.json)"}
+    except Exception:
+        return {"tf32": 1100.0, "dmma": 37.0, "ffma": 72.0, "source": "nominal (peaks file missing)"}
+
+
+def cpu_baseline_step(cfg, noise):
+    """cpu_baseline of the own arm: the oracle port timed on ONE full
+    ingest_batch of a workload batch (compression of t slices into P
+    replicas, CP-ALS on every replica, the whole merge) after an untimed
+    init_stream on t slices (the per-batch work does not depend on K0)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import octen_oracle as O
+    I, J, t, Q, P, R, sh = (cfg[k] for k in ("I", "J", "t", "Q", "P", "R", "shared"))
+    with threadpool_limits(limits=1):
+        syn = HostSynth(I, J, 2 * t, R, 1234, noise)
+        scfg = O.StreamConfig(rank=R, p=P, q=Q, shared=sh, seed=7 * 1234 + 3,
+                              als=O.AlsConfig(R, cfg["iters"], 1e-8, cfg["restarts"], 0), workers=0)
+        st = O.init_stream(syn.batch(0, t), scfg)
+        b = syn.batch(t, t)
+        a = time.perf_counter()
+        O.ingest_batch(st, b)
+        sec = time.perf_counter() - a
+        rec = st.log[-1]
+        workers = O.resolve_workers(scfg)
+    return {"value": I * J * t / sec, "unit": "entries/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": "one full ingest_batch of a %dx%dx%d batch (oracle port: compress + CP-ALS over %d replica "
+                      "threads, merge column solves over %d threads, single-threaded BLAS) after an untimed "
+                      "init_stream on %d slices" % (I, J, t, workers, os.cpu_count(), t),
+            "stages_s": {"compress_s": rec.compress_seconds, "als_s": rec.als_seconds,
+                         "recover_s": rec.recover_seconds, "total_s": sec}}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -243,13 +283,22 @@ def run_reference(args, cfg, rank, world):
     here) run as the reference runs: full ingest_batch steps
     (streaming.cpp:258-346) on the same workload, the compression and CP-ALS
     fanned out over min(cores, P) worker threads (parallel_replicas,
-    streaming.cpp:36-69; BLAS single-threaded inside each worker), the merge
-    with BLAS on every host core.  init_stream on the K0 block is untimed.
+    streaming.cpp:36-69), single-threaded BLAS as the reference's Eigen; the
+    port also spreads the merge's independent per-column QR solves over the
+    cores (the reference runs them in a loop), so it is a faster CPU
+    baseline than the reference itself.  init_stream on the K0 block is
+    untimed.
     Rank 0 only; the step time is the mean of the timed ingest_batch calls,
     with the reference's own BatchRecord stage timers beside it."""
     if rank != 0:
         return
     from oracle import octen_oracle as O
+    # BLAS single-threaded throughout, as the reference's Eigen: the port's
+    # parallelism is its explicit fan-out over replicas / independent
+    # column solves (threaded LAPACK measured slower on the pivoted QRs:
+    # 1.2 s vs 0.37 s for 1600 x 1000 on 8 cores)
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(limits=1)
     cores = os.cpu_count()
     I, J, K0, t, Q, P, R, sh = (cfg[k] for k in ("I", "J", "K0", "t", "Q", "P", "R", "shared"))
     nb = args.warmup + args.steps
@@ -277,7 +326,8 @@ def run_reference(args, cfg, rank, world):
               "recover_s": float(np.mean([r.recover_seconds for r in recs])), "init_s": t_init}
     sample = ("full ingest_batch steps of the oracle port (numpy/LAPACK restatement of the reference) on the "
               "%s workload: %d timed + %d warm-up batches of %dx%dx%d after an untimed init_stream on %d slices; "
-              "compress + CP-ALS over %d replica threads, merge with %d-thread BLAS" %
+              "compress + CP-ALS over %d replica threads, independent merge column solves over %d threads, "
+              "single-threaded BLAS" %
               (args.config, args.steps, args.warmup, I, J, t, K0, workers, cores))
     line = {"metric": "tensor entries streamed/sec per batch update", "value": v, "unit": "entries/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
@@ -561,6 +611,7 @@ def main():
     if pipelined:
         st.sync()
     times0 = (ctypes_stage_times(ob, st))
+    ks0 = st.kernel_stats() if hasattr(st, "kernel_stats") else None
     l0 = ob._capi.LIB.octen_launch_count()
     clk.mark()
     barrier()
@@ -574,6 +625,17 @@ def main():
     e1.record()
     barrier()
     clocks = clk.stop()
+    # model quality (outside the timed region): eval.cpp fitness of the
+    # streamed model on the last timed batch, computed on the device
+    quality = None
+    try:
+        kl = K0 + (args.warmup + args.steps - 1) * t
+        quality = {"batch_fitness_pct": st.batch_fitness(batches[args.warmup + args.steps - 1], kl),
+                   "slices": [kl, kl + t],
+                   "note": "fitness (eval.cpp:10-20) of the model after the last timed batch on that batch; "
+                           "rank-%d U(0,1) truth + %.2g%% noise" % (R, 100 * args.noise)}
+    except Exception as exc:  # pragma: no cover
+        quality = {"error": repr(exc)}
     if os.environ.get("OCTEN_BENCH_STEPLOG") and not sharded:
         for rec in st.log[-args.steps:]:
             print("step %d: compress %.2f als %.2f recover %.2f total %.2f ms" % (
@@ -656,7 +718,8 @@ def main():
                "step_ms": [round((b - a) * 1e3, 2) for a, b in zip([tw] + e2e_marks[:-1], e2e_marks)]}
 
     hbm, bf16, peak_kind = peaks()
-    tf32_peak = bf16 / 2.0
+    pk = pipe_peaks()
+    tf32_peak = pk["tf32"]
     g1_ms = dt[3] / max(dt[5], 1)  # per launch
     g1_flops = dt[4] / max(dt[5], 1)
     achieved = g1_flops / (g1_ms * 1e-3) / 1e12 if g1_ms > 0 else 0.0
@@ -670,23 +733,72 @@ def main():
             pipe_pct = rj.get("tensor_pipe_active_pct")
     except Exception:
         traffic = None
-    roofline = {"kernel": "compression mode-1 contraction (GEMM1)", "bound": "tensor", "achieved": achieved,
-                "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak, "traffic": traffic,
-                "traffic_unit": "bytes/launch (ncu dram__bytes_read+write, profiles/r1_roofline.json)",
-                "peak_source": "%s bf16 %.1f TF/s / 2 (dense TF32)" % (peak_kind, bf16),
-                "flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
-                "issued_tflops": 3.0 * achieved, "issued_frac": 3.0 * achieved / tf32_peak,
-                "issued_note": "split-TF32: 3 tcgen05 MMAs (hi*hi, hi*lo, lo*hi) per useful product",
-                "tensor_pipe_active_pct_ncu": pipe_pct}
+    ks1 = st.kernel_stats() if hasattr(st, "kernel_stats") else None
+    kd = {k: ks1[k] - ks0[k] for k in ks1} if (ks1 and ks0) else None
+    rooflines = {
+        "gemm1": {"kernel": "tc_gemm_tf32x3_persistent_kernel (compression mode-1 contraction, GEMM1)",
+                  "bound": "tensor (tcgen05 kind::tf32)", "achieved": achieved, "peak": tf32_peak,
+                  "unit": "TFLOP/s", "frac": achieved / tf32_peak, "traffic": traffic,
+                  "traffic_unit": "bytes/launch (ncu dram__bytes_read+write, profiles/r1_roofline.json)",
+                  "peak_source": pk["source"], "flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
+                  "issued_tflops": 3.0 * achieved, "issued_frac": 3.0 * achieved / tf32_peak,
+                  "issued_note": "split-TF32: 3 tcgen05 MMAs (hi*hi, hi*lo, lo*hi) per useful product",
+                  "tensor_pipe_active_pct_ncu": pipe_pct}}
+    if kd and kd["gemm_launches"] > 0:
+        gms = kd["gemm_ms"] / kd["gemm_launches"]
+        gfl = kd["gemm_flops"] / kd["gemm_launches"]
+        rooflines["als_tgemm"] = {
+            "kernel": "gemm_dmma_pipe_kernel (CP-ALS partial contractions T = Y x_n F, all restarts of a lane's "
+                      "replicas)", "bound": "FP64 tensor (DMMA)", "achieved": gfl / (gms * 1e-3) / 1e12,
+            "peak": pk["dmma"], "unit": "TFLOP/s", "frac": gfl / (gms * 1e-3) / 1e12 / pk["dmma"],
+            "flops_per_launch": gfl, "ms_per_launch": gms, "launches_per_step": kd["gemm_launches"] / args.steps,
+            "peak_source": pk["source"],
+            "note": "duration from CUDA events on the lane stream while the other lanes and the pipelined merge "
+                    "share the GPU"}
+    if kd and kd["mttkrp_launches"] > 0:
+        mms = kd["mttkrp_ms"] / kd["mttkrp_launches"]
+        mby = kd["mttkrp_bytes"] / kd["mttkrp_launches"]
+        rooflines["als_mttkrp"] = {
+            "kernel": "als_mttkrp_T_kernel (contraction of T with a factor + the fused mode update)",
+            "bound": "hbm", "achieved": mby / (mms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": mby / (mms * 1e-3) / 1e9 / hbm, "bytes_per_launch": mby, "ms_per_launch": mms,
+            "launches_per_step": kd["mttkrp_launches"] / args.steps, "peak_source": "%s HBM copy" % peak_kind,
+            "note": "the launch includes the serial R x R update of the last column block per problem"}
+    if kd and kd["sweeps"] > 0:
+        als_flops = kd["gemm_flops"] / args.steps
+        rooflines["als_stage"] = {"bound": "FP64 tensor (DMMA)", "achieved": als_flops / (dt[1] / args.steps * 1e-3) / 1e12,
+                                  "peak": pk["dmma"], "unit": "TFLOP/s",
+                                  "frac": als_flops / (dt[1] / args.steps * 1e-3) / 1e12 / pk["dmma"],
+                                  "flops_per_step": als_flops, "sweeps_per_step": kd["sweeps"] / args.steps,
+                                  "note": "T-GEMM flops (1.5 per sweep, 2 Q^3 S R each, per replica) over the "
+                                          "device-timed CP-ALS stage"}
+    # merge: Gram-formulation flops of one batch (2 passes x 2 modes x R
+    # bordered Cholesky factorizations of order d+1 + the weighted Grams)
+    d = I
+    merge_flops = 2 * 2 * (R * (d + 1) ** 3 / 3.0 + 2.0 * R * P * d * d)
+    mms_step = dt[2] / args.steps
+    rooflines["merge_stage"] = {"bound": "FP64 tensor (DMMA)", "achieved": merge_flops / (mms_step * 1e-3) / 1e12,
+                                "peak": pk["dmma"], "unit": "TFLOP/s",
+                                "frac": merge_flops / (mms_step * 1e-3) / 1e12 / pk["dmma"],
+                                "flops_per_step": merge_flops,
+                                "note": "runs on the merge stream concurrently with the next batch's compression "
+                                        "and CP-ALS (pipelined ingest); its time includes that sharing"}
+    # the headline roofline: the kernel with the largest device-time share
+    shares = {"gemm1": dt[3]}
+    if kd:
+        shares["als_tgemm"] = kd["gemm_ms"]
+        shares["als_mttkrp"] = kd["mttkrp_ms"]
+    top = max(shares, key=shares.get)
+    roofline = dict(rooflines[top])
+    roofline["why"] = "largest summed device time of the step's kernels (%s)" % ", ".join(
+        "%s %.2f ms" % (k, v / args.steps) for k, v in shares.items())
     stage = {"compress_ms": dt[0] / args.steps, "als_ms": dt[1] / args.steps, "merge_ms": dt[2] / args.steps,
              "gemm1_ms": dt[3] / args.steps, "init_s": t_init}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            sec, parts, det = cpu_sample(cfg)
-            cpu = {"value": entries / sec, "unit": "entries/s", "cores": os.cpu_count(), "kind": "port",
-                   "sample": det, "stages_s": parts}
+            cpu = cpu_baseline_step(cfg, args.noise)
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "entries/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": "failed: %r" % (exc,)}
@@ -705,7 +817,8 @@ def main():
                 "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
                 "dtype": "f32 compress (split-TF32/FP32) + f64 CP-ALS/merge", "data": "synthetic",
                 "config": bench_config(args, cfg, world),
-                "stages": stage, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "stages": stage, "roofline": roofline, "rooflines": rooflines, "cpu_baseline": cpu, "e2e": e2e,
+                "model_quality": quality,
                 "gpu_launches": int(launches), "clocks": clocks}
         if sparse is not None:
             line["sparse_c4"] = sparse

@@ -138,6 +138,22 @@ int octen_stream_set_publish(octen_stream* s, int on);
 int octen_stream_last_model(octen_stream* s, int64_t* info, double* a, double* b, double* c, int64_t c_rows_cap,
                             double* lambda);
 
+/* On-device generate_synthetic (proj/src/commands.cpp:110-134; SynthSpec,
+ * proj/include/cpstream/commands.hpp): U(0,1) factors from derive(seed,
+ * {9, n}), X = reconstruct(model) + N(mu, sigma) in flat order from one
+ * mt19937_64 stream derive(seed, {10}) with the reference's Box-Muller.
+ * octen_synth_next writes the next t slices along the last mode (I x J x t,
+ * first index fastest) to device memory as fp64 or fp32; batches come in
+ * stream order.  Values equal the reference's up to the last ulp of
+ * log/sin/cos.  Order-3 tensors. */
+typedef struct octen_synth octen_synth;
+int octen_synth_create(int order, const int64_t* dims, int rank, uint64_t seed, double noise_mu,
+                       double noise_sigma, int device, octen_synth** out);
+int octen_synth_next(octen_synth* h, int64_t t, void* out_device, int dtype);
+/* The normalized truth model (model.normalize()): factors[n] dims[n] x rank. */
+int octen_synth_truth(const octen_synth* h, double* const* factors, double* lambda);
+void octen_synth_destroy(octen_synth* h);
+
 /* congruence (proj/src/eval.cpp:22-46): per-component factor match score
  * (product over modes of |cos|) after exhaustive (rank <= 6) or greedy
  * matching.  ground/est: factors of every mode stacked, dims[n] x rank
@@ -163,6 +179,12 @@ int octen_stream_get_lambda(const octen_stream* s, double* out);
 /* The whole model in one call (one synchronisation): a I x R, b J x R,
  * c K x R (col-major), lambda R. */
 int octen_stream_get_model(const octen_stream* s, double* a, double* b, double* c, double* lambda);
+/* Live kernel timing of the CP-ALS stage, cumulative over the stream (CUDA
+ * events on the launching streams; no reference counterpart): out[0] T-GEMM
+ * milliseconds, out[1] T-GEMM launches, out[2] their algorithmic flops,
+ * out[3] MTTKRP (+ fused update) milliseconds, out[4] launches, out[5] bytes
+ * of the partial contractions they read, out[6] sweeps, out[7] reserved. */
+int octen_stream_get_kernel_stats(const octen_stream* s, double* out);
 /* Number of BatchRecords in the stream's log (streaming.hpp:57: one per
  * successful init/ingest; a failed batch still counts in batches_seen). */
 int octen_stream_log_size(const octen_stream* s, int64_t* n);

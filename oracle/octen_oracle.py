@@ -351,14 +351,14 @@ def colpiv_qr_solve(a: np.ndarray, b: np.ndarray, threshold: float):
     solve of recovery.cpp:26-38 / 396-401 from the same factorization."""
     if a.size == 0:
         return 0, None
-    qm, rm, piv = sla.qr(a, mode="economic", pivoting=True)
+    qm, rm, piv = sla.qr(a, mode="economic", pivoting=True, check_finite=False)
     d = np.abs(np.diag(rm))
     if d.size == 0 or d.max() == 0.0:
         return 0, None
     rank = int(np.sum(d > threshold * d.max()))
     if rank < a.shape[1]:
         return rank, None
-    z = sla.solve_triangular(rm, qm.T @ b, lower=False)
+    z = sla.solve_triangular(rm, qm.T @ b, lower=False, check_finite=False)
     x = np.empty_like(z)
     x[piv] = z
     return rank, x

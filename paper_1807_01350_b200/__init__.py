@@ -299,6 +299,13 @@ class StreamState:
             return None, 0
         return KruskalModel([a, b, c[:info[0]].copy(order="F")], lam), int(info[1])
 
+    def kernel_stats(self) -> dict:
+        """Live CP-ALS kernel timing (octen_stream_get_kernel_stats)."""
+        out = (ctypes.c_double * 8)()
+        _check(C.LIB.octen_stream_get_kernel_stats(self._h, out))
+        keys = ["gemm_ms", "gemm_launches", "gemm_flops", "mttkrp_ms", "mttkrp_launches", "mttkrp_bytes", "sweeps"]
+        return dict(zip(keys, list(out)[:7]))
+
     def footprint(self) -> dict:
         """measure_footprint (eval.cpp:48-60) of the device-resident state."""
         out = (C.c_i64 * 4)()
@@ -475,6 +482,48 @@ class ShardedStream(StreamState):
         self._allgather(self._ro, self._ra)
         torch.cuda.synchronize()
         self.finish(self._ra)
+
+
+class SynthStream:
+    """On-device generate_synthetic (commands.cpp:110-134; octen_synth_*):
+    U(0,1) factors from derive(seed, {9, n}), X = reconstruct + N(mu, sigma)
+    noise in flat order from derive(seed, {10}).  next(t) returns the next t
+    slices as a CUDA tensor viewed (I, J, t) first-index-fastest."""
+
+    def __init__(self, dims, rank: int, seed: int, noise_mu: float = 0.0, noise_sigma: float = 0.0,
+                 device: int = 0):
+        self.dims = [int(d) for d in dims]
+        self.rank = int(rank)
+        self.device = device
+        h = ctypes.c_void_p()
+        d = (C.c_i64 * len(self.dims))(*self.dims)
+        _check(C.LIB.octen_synth_create(len(self.dims), d, self.rank, int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                        float(noise_mu), float(noise_sigma), device, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        lib = getattr(C, "LIB", None) if C is not None else None
+        if h is not None and h.value and lib is not None:
+            lib.octen_synth_destroy(h)
+            self._h = None
+
+    def next(self, t: int, dtype: str = "f32", out=None):
+        import torch
+        I, J = self.dims[0], self.dims[1]
+        tdt = torch.float32 if dtype == "f32" else torch.float64
+        if out is None:
+            out = torch.empty((t, J, I), dtype=tdt, device=torch.device("cuda", self.device)).permute(2, 1, 0)
+        _check(C.LIB.octen_synth_next(self._h, int(t), ctypes.c_void_p(out.data_ptr()),
+                                      C.OCTEN_F32 if tdt == torch.float32 else C.OCTEN_F64))
+        return out
+
+    def truth(self) -> KruskalModel:
+        fs = [np.zeros((d, self.rank), order="F") for d in self.dims]
+        arr = (C.P_dbl * len(fs))(*[_dptr(f) for f in fs])
+        lam = np.zeros(self.rank)
+        _check(C.LIB.octen_synth_truth(self._h, arr, _dptr(lam)))
+        return KruskalModel(fs, lam)
 
 
 def compress(batch, u: List[np.ndarray], v: List[np.ndarray], w: List[np.ndarray], shared: int) -> List[np.ndarray]:

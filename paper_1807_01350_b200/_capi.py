@@ -62,10 +62,16 @@ SIGNATURES = {
     "octen_stream_ingest": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, P_i64]),
     "octen_stream_destroy": (None, [ctypes.c_void_p]),
+    "octen_synth_create": (ctypes.c_int, [ctypes.c_int, P_i64, ctypes.c_int, c_u64, c_dbl, c_dbl, ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_void_p)]),
+    "octen_synth_next": (ctypes.c_int, [ctypes.c_void_p, c_i64, ctypes.c_void_p, ctypes.c_int]),
+    "octen_synth_truth": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(P_dbl), P_dbl]),
+    "octen_synth_destroy": (None, [ctypes.c_void_p]),
     "octen_stream_ingest_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                  ctypes.c_int, P_i64]),
     "octen_stream_sync": (ctypes.c_int, [ctypes.c_void_p]),
     "octen_stream_log_size": (ctypes.c_int, [ctypes.c_void_p, P_i64]),
+    "octen_stream_get_kernel_stats": (ctypes.c_int, [ctypes.c_void_p, P_dbl]),
     "octen_stream_set_publish": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "octen_stream_last_model": (ctypes.c_int, [ctypes.c_void_p, P_i64, P_dbl, P_dbl, P_dbl, c_i64, P_dbl]),
     "octen_congruence": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P_i64, P_dbl, P_dbl, P_dbl]),

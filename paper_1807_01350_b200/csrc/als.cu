@@ -760,6 +760,83 @@ __device__ __forceinline__ void mttkrp_column(const double* __restrict__ tcol, c
     }
 }
 
+// The same contraction with 16-byte loads, eight of them in flight per thread
+// before their first use (Q even, Q <= 128, 256 threads).  contract_first ==
+// 0: thread (pair pu, group vg) sums rows v = vg, vg + 4, ... of pairs
+// (2 pu, 2 pu + 1); the four group partials are added in group order.
+// contract_first == 1: warp w takes rows v = w, w + 8, ...; its lanes hold
+// pairs pu = lane, lane + 32 of each row and the row sum is a fixed shuffle
+// tree.
+__device__ __forceinline__ void mttkrp_column_v2(const double* __restrict__ tcol, const double* __restrict__ w,
+                                                 double* __restrict__ M, int Q, int contract_first) {
+    constexpr int B = 8;  // rows of a thread in flight per batch (registers: 80 at 3 CTAs per SM)
+    __shared__ double2 part2[4][64];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int QP = Q >> 1;  // pairs per row
+    if (!contract_first) {  // M(u) = sum_v T(u, v) w(v)
+        const int pu = tid & 63, vg = tid >> 6;
+        double2 acc = make_double2(0.0, 0.0);
+        if (pu < QP) {
+#pragma unroll 1
+            for (int v0 = vg; v0 < Q; v0 += 4 * B) {
+                double2 x[B];
+                double wv[B];
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    const int v = v0 + 4 * j;
+                    x[j] = make_double2(0.0, 0.0);
+                    wv[j] = 0.0;
+                    if (v < Q) {
+                        x[j] = __ldg(reinterpret_cast<const double2*>(tcol + (size_t)Q * v) + pu);
+                        wv[j] = __ldg(w + v);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    acc.x += x[j].x * wv[j];
+                    acc.y += x[j].y * wv[j];
+                }
+            }
+        }
+        part2[vg][pu] = acc;
+        __syncthreads();
+        for (int e = tid; e < QP; e += blockDim.x) {
+            double2 sacc = part2[0][e];
+            for (int g = 1; g < 4; ++g) {
+                sacc.x += part2[g][e].x;
+                sacc.y += part2[g][e].y;
+            }
+            M[2 * e] = sacc.x;
+            M[2 * e + 1] = sacc.y;
+        }
+    } else {  // M(v) = sum_u T(u, v) w(u)
+        double2 wa = make_double2(0.0, 0.0), wb = make_double2(0.0, 0.0);
+        if (lane < QP) wa = __ldg(reinterpret_cast<const double2*>(w) + lane);
+        if (lane + 32 < QP) wb = __ldg(reinterpret_cast<const double2*>(w) + lane + 32);
+#pragma unroll 1
+        for (int v0 = warp; v0 < Q; v0 += 8 * (B / 2)) {
+            double2 xa[B / 2], xb[B / 2];
+#pragma unroll
+            for (int j = 0; j < B / 2; ++j) {
+                const int v = v0 + 8 * j;
+                xa[j] = xb[j] = make_double2(0.0, 0.0);
+                if (v < Q) {
+                    const double2* row = reinterpret_cast<const double2*>(tcol + (size_t)Q * v);
+                    if (lane < QP) xa[j] = __ldg(row + lane);
+                    if (lane + 32 < QP) xb[j] = __ldg(row + lane + 32);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < B / 2; ++j) {
+                const int v = v0 + 8 * j;
+                double sacc = (xa[j].x * wa.x + xa[j].y * wa.y) + (xb[j].x * wb.x + xb[j].y * wb.y);
+                for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+                if (lane == 0 && v < Q) M[v] = sacc;
+            }
+        }
+    }
+}
+
 // The first NP blocks instead form Vi of `mode` (als_vinv_block).  With
 // `fused`, the last of a problem's R + 1 blocks to finish (fence + counter)
 // runs the mode update for it (als_update_block), so the update needs no
@@ -785,7 +862,10 @@ __global__ void __launch_bounds__(256, 3) als_mttkrp_T_kernel(AlsDev d, int cont
         const double* tcol = d.T + (size_t)p * d.q2() * d.S * R + (size_t)d.q2() * (s * R + r);
         double* M = d.Mb + (size_t)prob * Q * R + (size_t)Q * r;
         const double* w = d.f(prob, fsrc) + (size_t)Q * r;
-        mttkrp_column<NA>(tcol, w, M, Q, contract_first);
+        if (NA == 0)
+            mttkrp_column_v2(tcol, w, M, Q, contract_first);
+        else
+            mttkrp_column<NA == 0 ? 4 : NA>(tcol, w, M, Q, contract_first);
     }
     if (!fused) return;
     __shared__ int last;
@@ -1125,6 +1205,8 @@ AlsEngine::~AlsEngine() {
             cudaStreamDestroy(ls);
         }
     if (hact) cudaFreeHost(hact);
+    for (cudaEvent_t e : kev)
+        if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : lane_ev)
         if (e) cudaEventDestroy(e);
 }
@@ -1370,7 +1452,10 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     const size_t smem_upd = (size_t)(R * R + 2 * Q * R + R + 2 * (R + 2) + upd_threads) * sizeof(double) + 16;
     OCTEN_CUDA(cudaFuncSetAttribute(als_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_upd));
     const size_t smem_vinv = (size_t)(4 * R * R + 2 * (R + 2) + 256) * sizeof(double) + (R + 8) * sizeof(int) + 16;
-    auto mttkrp_kernel = Q <= 128 ? als_mttkrp_T_kernel<4> : als_mttkrp_T_kernel<8>;
+    // 16-byte, one-round-trip contraction when Q is even and <= 128
+    static const bool mk_v1 = std::getenv("OCTEN_ALS_MTTKRP_V1") != nullptr;  // diagnostics: the round-1 kernel
+    const bool v2_ok = !mk_v1 && Q % 2 == 0 && Q <= 128 && ((uintptr_t)T.p % 16 == 0) && ((uintptr_t)F.p % 16 == 0);
+    auto mttkrp_kernel = v2_ok ? als_mttkrp_T_kernel<0> : (Q <= 128 ? als_mttkrp_T_kernel<4> : als_mttkrp_T_kernel<8>);
     // MTTKRP + update fused in one launch unless OCTEN_ALS_NOFUSE (diagnostics)
     static const bool fuse_update = std::getenv("OCTEN_ALS_NOFUSE") == nullptr;
     const size_t smem_mk = fuse_update ? std::max(smem_vinv, smem_upd) : smem_vinv;
@@ -1390,19 +1475,6 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     int L = 4;  // measured: 1 lane 14.1 ms, 2 lanes 13.5, 4 lanes 13.4 (c3 CP-ALS stage)
     if (const char* ev = std::getenv("OCTEN_ALS_LANES")) L = std::max(1, std::min(kMaxLanes, std::atoi(ev)));
     L = std::min(L, P);
-    int nsm = 148;
-    {
-        int dev = 0;
-        OCTEN_CUDA(cudaGetDevice(&dev));
-        OCTEN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    }
-    // OCTEN_ALS_LANE_CTAS > 0 caps each lane's T-GEMM grid (a persistent
-    // tile loop on a share of the SMs).  Measured at c3 with the pipelined
-    // merge: one CTA per tile (0, the default) 13.9 ms per step, 296 CTAs
-    // 14.0, 148 14.5, 74 16.7: the lanes' GEMMs already overlap each other.
-    int lane_ctas = 0;
-    if (const char* ev = std::getenv("OCTEN_ALS_LANE_CTAS")) lane_ctas = std::max(0, std::atoi(ev));
-    (void)nsm;
     int lp0[kMaxLanes], lp1[kMaxLanes];
     for (int l = 0; l < L; ++l) {
         lp0[l] = (int)((long long)P * l / L);
@@ -1442,6 +1514,8 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     for (int l = 1; l < L; ++l) ls[l] = gsplit ? lane_hp[l] : lane_st[l];
     if (hact_n < (size_t)max_iters * kMaxLanes) {
         if (hact) cudaFreeHost(hact);
+    for (cudaEvent_t e : kev)
+        if (e) cudaEventDestroy(e);
         hact = nullptr;
         hact_n = (size_t)max_iters * kMaxLanes;
         OCTEN_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hact), hact_n * sizeof(int), cudaHostAllocMapped));
@@ -1508,6 +1582,21 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     // 1.5 Q^3 S R GEMMs per sweep instead of 2 (or 3 without a tree).  Each
     // sweep is enqueued as two segments, each segment for every lane in turn,
     // so the GEMM stream alternates between lanes.
+    krec.clear();
+    auto ktime_begin = [&](cudaStream_t ss) {
+        const int i = (int)krec.size() * 2;
+        while ((int)kev.size() < i + 2) {
+            cudaEvent_t e;
+            OCTEN_CUDA(cudaEventCreate(&e));
+            kev.push_back(e);
+        }
+        OCTEN_CUDA(cudaEventRecord(kev[i], ss));
+        return i;
+    };
+    auto ktime_end = [&](int i, cudaStream_t ss, bool gemm, double work) {
+        OCTEN_CUDA(cudaEventRecord(kev[i + 1], ss));
+        krec.push_back(KevRec{i, gemm, work});
+    };
     auto launch_seg = [&](int l, int sw, int seg) {
         const AlsDev& x = dl[l];
         cudaStream_t ss = ls[l];
@@ -1521,28 +1610,30 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
                 OCTEN_CUDA(cudaStreamWaitEvent(gs, lane_ev[kGin + l], 0));
                 pd = false;
             }
+            const int kt0 = ktime_begin(gs);
             if (contracted == 2) {  // rows (i, j)
                 if (pipe_ok)
                     gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmatP{x.Y, q3, q2}, FacP{x.F, S, Q, R, 2},
-                                         TStore{x.T, q2, SR}, gs, 1, nullptr, pd, lane_ctas);
+                                         TStore{x.T, q2, SR}, gs, 1, nullptr, pd);
                 else
                     gemm_f64<false, true>(pn, (int)q2, SR, Q, YmatA{x.Y, q3, q2, S, false}, FacB{x.F, S, Q, R, 2},
                                           TStore{x.T, q2, SR}, gs);
             } else if (contracted == 1) {  // rows (i, k)
                 if (pipe_ok)
                     gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmidP{x.Y, q3, (unsigned)Q, qinv}, FacP{x.F, S, Q, R, 1},
-                                         TStore{x.T, q2, SR}, gs, 1, nullptr, pd, lane_ctas);
+                                         TStore{x.T, q2, SR}, gs, 1, nullptr, pd);
                 else
                     gemm_f64<false, true>(pn, (int)q2, SR, Q, YmidA{x.Y, q3, Q}, FacB{x.F, S, Q, R, 1},
                                           TStore{x.T, q2, SR}, gs);
             } else {  // rows (j, k)
                 if (pipe_ok)
                     gemm_f64_pipe<true>(pn, (int)q2, SR, Q, Y0tP{x.Y, q3, Q}, FacP{x.F, S, Q, R, 0},
-                                        TStore{x.T, q2, SR}, gs, 1, nullptr, pd, lane_ctas);
+                                        TStore{x.T, q2, SR}, gs, 1, nullptr, pd);
                 else
                     gemm_f64<true, true>(pn, (int)q2, SR, Q, Y0tA{x.Y, q3, Q}, FacB{x.F, S, Q, R, 0},
                                          TStore{x.T, q2, SR}, gs);
             }
+            ktime_end(kt0, gs, true, 2.0 * (double)pn * (double)q2 * SR * Q);
             if (gsplit) {
                 OCTEN_CUDA(cudaEventRecord(lane_ev[kGout + l], gs));
                 OCTEN_CUDA(cudaStreamWaitEvent(ss, lane_ev[kGout + l], 0));
@@ -1551,6 +1642,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         };
         auto mode_step = [&](int contract_first, int fsrc, int mode) {
             const int fz = fuse_update ? 1 : 0;
+            const int kt1 = ktime_begin(ss);
             if (use_pdl) {
                 launch_pdl(mttkrp_kernel, dim3(npn * (R + 1)), dim3(256), smem_mk, ss, x, contract_first, fsrc, mode,
                            sw, fz);
@@ -1558,6 +1650,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
                 mttkrp_kernel<<<npn * (R + 1), 256, smem_mk, ss>>>(x, contract_first, fsrc, mode, sw, fz);
                 OCTEN_LAUNCHED(1);
             }
+            ktime_end(kt1, ss, false, (double)npn * R * q2 * sizeof(double));  // T columns read (active problems at most)
             mark(l, sw, mode == 0 ? "mttkrp0" : mode == 1 ? "mttkrp1" : "mttkrp2", ss);
             if (fuse_update) return;
             if (use_pdl) {
@@ -1615,6 +1708,20 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         }
     OCTEN_CUDA(cudaStreamSynchronize(st));
     last_sweeps = sweep;
+    for (const KevRec& k : krec) {
+        float ms = 0.f;
+        OCTEN_CUDA(cudaEventElapsedTime(&ms, kev[k.ev], kev[k.ev + 1]));
+        if (k.gemm) {
+            kstats.gemm_ms += ms;
+            kstats.gemm_flops += k.work;
+            ++kstats.gemm_launches;
+        } else {
+            kstats.mttkrp_ms += ms;
+            kstats.mttkrp_bytes += k.work;
+            ++kstats.mttkrp_launches;
+        }
+    }
+    kstats.sweeps += sweep;
     if (want_prof) {
         // duration of each label = time since the previous mark (any sweep)
         std::vector<std::string> lab[2];

@@ -13,9 +13,14 @@
 #include "engine.hpp"
 #include "errors.hpp"
 #include "stream.hpp"
+#include "synth.hpp"
 
 struct octen_stream {
     std::unique_ptr<octen::Stream> s;
+};
+
+struct octen_synth {
+    std::unique_ptr<octen::SynthStream> g;
 };
 
 struct octen_coo_summaries {
@@ -233,6 +238,43 @@ int octen_stream_last_model(octen_stream* s, int64_t* info, double* a, double* b
     });
 }
 
+int octen_synth_create(int order, const int64_t* dims, int rank, uint64_t seed, double noise_mu,
+                       double noise_sigma, int device, octen_synth** out) {
+    return guard([&] {
+        if (!dims || !out || order < 0) throw octen::ConfigError("octen_synth_create: null argument");
+        DeviceGuard dg(device);
+        auto h = std::make_unique<octen_synth>();
+        h->g = std::make_unique<octen::SynthStream>(std::vector<std::int64_t>(dims, dims + order), rank, seed,
+                                                    noise_mu, noise_sigma, device);
+        *out = h.release();
+    });
+}
+
+int octen_synth_next(octen_synth* h, int64_t t, void* out_device, int dtype) {
+    return guard([&] {
+        if (!h || !out_device) throw octen::ConfigError("octen_synth_next: null argument");
+        if (dtype != OCTEN_F64 && dtype != OCTEN_F32) throw octen::ConfigError("octen: unknown dtype");
+        DeviceGuard dg(h->g->device);
+        h->g->next(t, out_device, dtype);
+    });
+}
+
+int octen_synth_truth(const octen_synth* h, double* const* factors, double* lambda) {
+    return guard([&] {
+        if (!h || !factors || !lambda) throw octen::ConfigError("octen_synth_truth: null argument");
+        h->g->truth(factors, lambda);
+    });
+}
+
+void octen_synth_destroy(octen_synth* h) {
+    if (!h) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (h->g) cudaSetDevice(h->g->device);
+    delete h;
+    cudaSetDevice(cur);
+}
+
 int octen_congruence(int order, int rank, const int64_t* dims, const double* ground, const double* est,
                      double* scores) {
     // eval.cpp:22-46: per-component product over modes of |cos| between the
@@ -447,6 +489,21 @@ int octen_stream_get_lambda(const octen_stream* s, double* out) {
         auto& x = *s->s;
         x.lam.download(out, x.cfg.rank, x.st);
         OCTEN_CUDA(cudaStreamSynchronize(x.st));
+    });
+}
+
+int octen_stream_get_kernel_stats(const octen_stream* s, double* out) {
+    return sguard(s, [&] {
+        s->s->sync();
+        const auto& k = s->s->als.kstats;
+        out[0] = k.gemm_ms;
+        out[1] = (double)k.gemm_launches;
+        out[2] = k.gemm_flops;
+        out[3] = k.mttkrp_ms;
+        out[4] = (double)k.mttkrp_launches;
+        out[5] = k.mttkrp_bytes;
+        out[6] = (double)k.sweeps;
+        out[7] = 0.0;
     });
 }
 

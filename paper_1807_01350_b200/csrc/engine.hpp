@@ -59,6 +59,13 @@ public:
     int last_sweeps = 0;
     int host_syncs = 0;
     AlsFailure failure;  // set when run() throws a NumericError
+    // Live kernel timing (CUDA events on the launching lane stream, summed
+    // after each run): the T-GEMMs and the MTTKRP (+ fused update) launches,
+    // with their algorithmic flops / bytes.
+    struct KernelStats {
+        double gemm_ms = 0, gemm_flops = 0, mttkrp_ms = 0, mttkrp_bytes = 0;
+        long long gemm_launches = 0, mttkrp_launches = 0, sweeps = 0;
+    } kstats;
     ~AlsEngine();
 
 private:
@@ -76,6 +83,13 @@ private:
     // GEMM stream -> lane, [kSweepEv + 4 (sweep & 1) + l] end of a sweep
     static constexpr int kGin = 1, kGout = 1 + kMaxLanes, kSweepEv = 1 + 2 * kMaxLanes;
     cudaEvent_t lane_ev[1 + 4 * kMaxLanes] = {};
+    std::vector<cudaEvent_t> kev;   // timing event pool: pairs (start, end)
+    struct KevRec {
+        int ev;        // index of the start event (end = ev + 1)
+        bool gemm;     // T-GEMM (else MTTKRP)
+        double work;   // flops (GEMM) or bytes (MTTKRP)
+    };
+    std::vector<KevRec> krec;
     DevBuf<double> Gev, EV, Ur, Wmix, Smix, Tmp6, Pm, Hh, gscr;
     DevBuf<int> usable, att_start, att_used, todo, peel_fail, eigdbg, mcount;
     DevBuf<AlsState> state;

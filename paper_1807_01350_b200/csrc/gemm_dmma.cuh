@@ -11,8 +11,6 @@
 
 #include <cuda_runtime.h>
 
-#include <algorithm>
-
 #include "gemm_simt.cuh"
 #include "octen_common.cuh"
 
@@ -232,8 +230,7 @@ __device__ __forceinline__ void wait() {
 
 template <bool A_KFAST, class AF, class BF, class CF, bool B_KFAST = true>
 __global__ void __launch_bounds__(256)
-    gemm_dmma_pipe_kernel(int M, int N, int K, int ksplit, int kchunk, AF af, BF bf, CF cf, double* partial,
-                          int gx, int gy, long long ntiles) {
+    gemm_dmma_pipe_kernel(int M, int N, int K, int ksplit, int kchunk, AF af, BF bf, CF cf, double* partial) {
     using namespace pipe;
     pdl_trigger();
     pdl_wait();
@@ -244,16 +241,12 @@ __global__ void __launch_bounds__(256)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t4 = lane & 3;
     const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
-    // Tiles are visited grid-stride (n-tile fastest, then m-tile, then
-    // batch x k-split): a grid smaller than the tile count (a CP-ALS lane's
-    // share of the SMs) loops, so no partial last wave is left behind.
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int bxi = (int)(tile % gx), byi = (int)((tile / gx) % gy), zb = (int)(tile / ((long long)gx * gy));
+    const int zb = blockIdx.z;
     const int batch = zb / ksplit, ks = zb % ksplit;
-    const int m0 = byi * BM, n0 = bxi * BN;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int kbeg = ks * kchunk;
     const int kend = min(K, kbeg + kchunk);
-    const int ntk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+    const int ntiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
     const double* dummy = af(batch, 0, 0);
 
     auto load = [&](int kt, int stg) {
@@ -300,13 +293,13 @@ __global__ void __launch_bounds__(256)
 
 #pragma unroll
     for (int s = 0; s < ST - 1; ++s) {
-        if (s < ntk) load(s, s);
+        if (s < ntiles) load(s, s);
         commit();
     }
-    for (int kt = 0; kt < ntk; ++kt) {
+    for (int kt = 0; kt < ntiles; ++kt) {
         wait<ST - 2>();
         __syncthreads();
-        if (kt + ST - 1 < ntk) load(kt + ST - 1, (kt + ST - 1) % ST);
+        if (kt + ST - 1 < ntiles) load(kt + ST - 1, (kt + ST - 1) % ST);
         commit();
         const double* as = As + (kt % ST) * AE;
         const double* bs = Bs + (kt % ST) * B_ELEMS;
@@ -330,7 +323,6 @@ __global__ void __launch_bounds__(256)
         }
     }
     wait<0>();
-    __syncthreads();  // the next tile's prologue refills the stages
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -345,12 +337,11 @@ __global__ void __launch_bounds__(256)
                         partial[(((size_t)batch * ksplit + ks) * M + gm) * N + gn] = acc[i][j][v];
                 }
             }
-    }
 }
 
 template <bool A_KFAST, class AF, class BF, class CF, bool B_KFAST = true>
 void gemm_f64_pipe(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaStream_t st, int ksplit = 1,
-                   double* workspace = nullptr, bool pdl = false, int max_ctas = 0) {
+                   double* workspace = nullptr, bool pdl = false) {
     if (batches <= 0 || M <= 0 || N <= 0) return;
     if (K <= 0) ksplit = 1;
     if (ksplit < 1) ksplit = 1;
@@ -362,16 +353,13 @@ void gemm_f64_pipe(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaSt
         OCTEN_CUDA(cudaFuncSetAttribute(gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF, B_KFAST>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     });
-    const int gx = (N + pipe::BN - 1) / pipe::BN, gy = (M + pipe::BM - 1) / pipe::BM;
-    const long long ntiles = (long long)gx * gy * batches * ksplit;
-    // max_ctas > 0: a persistent grid of at most that many CTAs loops over the tiles
-    const int grid = (int)(max_ctas > 0 ? std::min<long long>(ntiles, max_ctas) : ntiles);
+    dim3 grid((N + pipe::BN - 1) / pipe::BN, (M + pipe::BM - 1) / pipe::BM, batches * ksplit);
     if (pdl) {
-        launch_pdl(gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF, B_KFAST>, dim3(grid), dim3(256), smem, st, M, N, K,
-                   ksplit, kchunk, af, bf, cf, workspace, gx, gy, ntiles);
+        launch_pdl(gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF, B_KFAST>, grid, dim3(256), smem, st, M, N, K, ksplit,
+                   kchunk, af, bf, cf, workspace);
     } else {
         gemm_dmma_pipe_kernel<A_KFAST, AF, BF, CF, B_KFAST><<<grid, 256, smem, st>>>(M, N, K, ksplit, kchunk, af, bf,
-                                                                                     cf, workspace, gx, gy, ntiles);
+                                                                                     cf, workspace);
         OCTEN_LAUNCHED(1);
     }
     if (ksplit > 1) {
@@ -405,7 +393,5 @@ void gemm_f64(int batches, int M, int N, int K, AF af, BF bf, CF cf, cudaStream_
         OCTEN_LAUNCHED(1);
     }
 }
-
-
 
 }  // namespace octen
