@@ -76,6 +76,7 @@ def cpu_baseline_step(cfg, noise):
     from threadpoolctl import threadpool_limits
     from oracle import octen_oracle as O
     I, J, t, Q, P, R, sh = (cfg[k] for k in ("I", "J", "t", "Q", "P", "R", "shared"))
+    O.MERGE_PROCESSES = True
     with threadpool_limits(limits=1):
         syn = HostSynth(I, J, 2 * t, R, 1234, noise)
         scfg = O.StreamConfig(rank=R, p=P, q=Q, shared=sh, seed=7 * 1234 + 3,
@@ -89,7 +90,7 @@ def cpu_baseline_step(cfg, noise):
         workers = O.resolve_workers(scfg)
     return {"value": I * J * t / sec, "unit": "entries/s", "cores": os.cpu_count(), "kind": "port",
             "sample": "one full ingest_batch of a %dx%dx%d batch (oracle port: compress + CP-ALS over %d replica "
-                      "threads, merge column solves over %d threads, single-threaded BLAS) after an untimed "
+                      "threads, merge column solves over %d processes, single-threaded BLAS) after an untimed "
                       "init_stream on %d slices" % (I, J, t, workers, os.cpu_count(), t),
             "stages_s": {"compress_s": rec.compress_seconds, "als_s": rec.als_seconds,
                          "recover_s": rec.recover_seconds, "total_s": sec}}
@@ -299,6 +300,7 @@ def run_reference(args, cfg, rank, world):
     # 1.2 s vs 0.37 s for 1600 x 1000 on 8 cores)
     from threadpoolctl import threadpool_limits
     threadpool_limits(limits=1)
+    O.MERGE_PROCESSES = True  # the column QRs in forked workers (scipy's LAPACK holds the GIL)
     cores = os.cpu_count()
     I, J, K0, t, Q, P, R, sh = (cfg[k] for k in ("I", "J", "K0", "t", "Q", "P", "R", "shared"))
     nb = args.warmup + args.steps
@@ -326,7 +328,7 @@ def run_reference(args, cfg, rank, world):
               "recover_s": float(np.mean([r.recover_seconds for r in recs])), "init_s": t_init}
     sample = ("full ingest_batch steps of the oracle port (numpy/LAPACK restatement of the reference) on the "
               "%s workload: %d timed + %d warm-up batches of %dx%dx%d after an untimed init_stream on %d slices; "
-              "compress + CP-ALS over %d replica threads, independent merge column solves over %d threads, "
+              "compress + CP-ALS over %d replica threads, independent merge column solves over %d processes, "
               "single-threaded BLAS" %
               (args.config, args.steps, args.warmup, I, J, t, K0, workers, cores))
     line = {"metric": "tensor entries streamed/sec per batch update", "value": v, "unit": "entries/s",
@@ -751,10 +753,10 @@ def main():
             "kernel": "gemm_dmma_pipe_kernel (CP-ALS partial contractions T = Y x_n F, all restarts of a lane's "
                       "replicas)", "bound": "FP64 tensor (DMMA)", "achieved": gfl / (gms * 1e-3) / 1e12,
             "peak": pk["dmma"], "unit": "TFLOP/s", "frac": gfl / (gms * 1e-3) / 1e12 / pk["dmma"],
-            "flops_per_launch": gfl, "ms_per_launch": gms, "launches_per_step": kd["gemm_launches"] / args.steps,
+            "flops_per_launch": gfl, "ms_per_launch": gms, "sampled_launches": kd["gemm_launches"],
             "peak_source": pk["source"],
-            "note": "duration from CUDA events on the lane stream while the other lanes and the pipelined merge "
-                    "share the GPU"}
+            "note": "duration from CUDA events on the launching lane stream (sampled: lane 0, every fifth sweep) "
+                    "while the other lanes and the pipelined merge share the GPU"}
     if kd and kd["mttkrp_launches"] > 0:
         mms = kd["mttkrp_ms"] / kd["mttkrp_launches"]
         mby = kd["mttkrp_bytes"] / kd["mttkrp_launches"]
@@ -762,10 +764,11 @@ def main():
             "kernel": "als_mttkrp_T_kernel (contraction of T with a factor + the fused mode update)",
             "bound": "hbm", "achieved": mby / (mms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": mby / (mms * 1e-3) / 1e9 / hbm, "bytes_per_launch": mby, "ms_per_launch": mms,
-            "launches_per_step": kd["mttkrp_launches"] / args.steps, "peak_source": "%s HBM copy" % peak_kind,
+            "sampled_launches": kd["mttkrp_launches"], "peak_source": "%s HBM copy" % peak_kind,
             "note": "the launch includes the serial R x R update of the last column block per problem"}
     if kd and kd["sweeps"] > 0:
-        als_flops = kd["gemm_flops"] / args.steps
+        # every sweep: 1.5 T-GEMMs of 2 Q^3 S R flops per replica
+        als_flops = kd["sweeps"] / args.steps * 1.5 * 2.0 * Q ** 3 * cfg["restarts"] * R * P
         rooflines["als_stage"] = {"bound": "FP64 tensor (DMMA)", "achieved": als_flops / (dt[1] / args.steps * 1e-3) / 1e12,
                                   "peak": pk["dmma"], "unit": "TFLOP/s",
                                   "frac": als_flops / (dt[1] / args.steps * 1e-3) / 1e12 / pk["dmma"],
@@ -788,6 +791,10 @@ def main():
     if kd:
         shares["als_tgemm"] = kd["gemm_ms"]
         shares["als_mttkrp"] = kd["mttkrp_ms"]
+    if kd:  # sampled kernel timing -> per-step totals
+        nl = float(kd["sweeps"]) / args.steps  # sweeps per step (all lanes run them)
+        shares["als_tgemm"] = rooflines.get("als_tgemm", {}).get("ms_per_launch", 0.0) * 1.5 * nl * 4 * args.steps
+        shares["als_mttkrp"] = rooflines.get("als_mttkrp", {}).get("ms_per_launch", 0.0) * 3 * nl * 4 * args.steps
     top = max(shares, key=shares.get)
     roofline = dict(rooflines[top])
     roofline["why"] = "largest summed device time of the step's kernels (%s)" % ", ".join(

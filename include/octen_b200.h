@@ -138,6 +138,14 @@ int octen_stream_set_publish(octen_stream* s, int on);
 int octen_stream_last_model(octen_stream* s, int64_t* info, double* a, double* b, double* c, int64_t c_rows_cap,
                             double* lambda);
 
+/* checkpoint_save / checkpoint_load (proj/include/cpstream/streaming.hpp:78-79;
+ * src/checkpoint.cpp:125-295): the OCTS container of an unsharded stream
+ * between batches, byte-compatible with the reference's.  save with
+ * buf == NULL returns the size only; errors of a bad container are
+ * OCTEN_ERR_IO with the reference's messages. */
+int octen_stream_checkpoint_save(octen_stream* s, uint8_t* buf, int64_t cap, int64_t* size);
+int octen_stream_checkpoint_load(const uint8_t* bytes, int64_t n, int device, octen_stream** out);
+
 /* On-device generate_synthetic (proj/src/commands.cpp:110-134; SynthSpec,
  * proj/include/cpstream/commands.hpp): U(0,1) factors from derive(seed,
  * {9, n}), X = reconstruct(model) + N(mu, sigma) in flat order from one

@@ -47,6 +47,10 @@ class NumericError(Exception):
     """errors.hpp:19-22."""
 
 
+class IoError(Exception):
+    """errors.hpp: file and serialization failures (checkpoint corruption)."""
+
+
 # ---------------------------------------------------------------------------
 # tensor.cpp
 # ---------------------------------------------------------------------------
@@ -952,8 +956,7 @@ def recover_nontemporal_weighted(stacked_factor, stacked_projection, mode: int, 
     # the R column solves are independent (the reference runs them in a
     # loop); the port spreads them over the host cores, lowest column's
     # error first
-    import os
-    for r, x in enumerate(parallel_replicas(rank, os.cpu_count() or 1, one)):
+    for r, x in enumerate(parallel_columns(rank, one)):
         out[:, r] = x
     return out
 
@@ -1018,8 +1021,7 @@ def recover_temporal_append(temporal_stack, rs: ReplicaSet, summaries: SummarySt
 
     # independent per-column solves (a loop in the reference), spread over
     # the host cores; sums in column order
-    import os
-    for r, (solved, f2, r2) in enumerate(parallel_replicas(rank, os.cpu_count() or 1, one)):
+    for r, (solved, f2, r2) in enumerate(parallel_columns(rank, one)):
         new_rows[:, r] = solved
         res_sq += f2
         rhs_sq += r2
@@ -1342,6 +1344,35 @@ def parallel_replicas(n: int, workers: int, fn):
     return out
 
 
+# scipy's LAPACK wrappers hold the GIL, so threads do not overlap the merge's
+# pivoted QRs; the CPU-baseline legs of bench.py set this to run those
+# independent column solves in forked worker processes instead (tests keep
+# the default: forking a process that drives a GPU is not worth the risk).
+MERGE_PROCESSES = False
+_FORK_FN = None
+
+
+def _fork_call(i):
+    return _FORK_FN(i)
+
+
+def parallel_columns(n: int, fn):
+    """fn(i) for the independent per-column solves of the merge, in column
+    order, over the host cores (processes when MERGE_PROCESSES, else threads)."""
+    import os
+    workers = min(n, os.cpu_count() or 1)
+    if not MERGE_PROCESSES or workers <= 1 or n <= 1:
+        return parallel_replicas(n, workers, fn)
+    global _FORK_FN
+    import multiprocessing as mp
+    _FORK_FN = fn
+    try:
+        with mp.get_context("fork").Pool(workers) as pool:
+            return pool.map(_fork_call, range(n), chunksize=1)
+    finally:
+        _FORK_FN = None
+
+
 def _run_replica_als(st: StreamState, batch_index: int):
     cfg = st.config
 
@@ -1485,6 +1516,189 @@ def congruence(ground: KruskalModel, est: KruskalModel):
         sim = sim * np.abs(column_normalized(g).T @ column_normalized(e))
     perm = exhaustive_match(sim) if rank <= 6 else greedy_match(sim)
     return [float(sim[i, perm[i]]) for i in range(rank)]
+
+
+# ---------------------------------------------------------------------------
+# checkpoint.cpp -- the OCTS container (format only; test infrastructure)
+# ---------------------------------------------------------------------------
+
+def _crc64(data: bytes) -> int:
+    """checkpoint.cpp:17-31 -- CRC-64/ECMA-182, bit-reflected."""
+    table = _crc64.table if hasattr(_crc64, "table") else None
+    if table is None:
+        poly = 0xC96C5795D7870F42
+        table = []
+        for i in range(256):
+            c = i
+            for _ in range(8):
+                c = (c >> 1) ^ (poly if c & 1 else 0)
+            table.append(c)
+        _crc64.table = table
+    c = 0xFFFFFFFFFFFFFFFF
+    for b in data:
+        c = table[(c ^ b) & 0xFF] ^ (c >> 8)
+    return c ^ 0xFFFFFFFFFFFFFFFF
+
+
+def checkpoint_save(st: StreamState) -> bytes:
+    """checkpoint.cpp:168-219 (native little-endian)."""
+    import struct
+    out = bytearray()
+
+    def u8(v): out.extend(struct.pack("<B", v))
+    def u32(v): out.extend(struct.pack("<I", v & 0xFFFFFFFF))
+    def u64(v): out.extend(struct.pack("<Q", v & 0xFFFFFFFFFFFFFFFF))
+    def i64(v): out.extend(struct.pack("<q", v))
+    def f64(v): out.extend(struct.pack("<d", v))
+
+    def matrix(m):
+        m = np.asarray(m, dtype=np.float64)
+        i64(m.shape[0])
+        i64(m.shape[1])
+        out.extend(np.asfortranarray(m).tobytes(order="F"))
+
+    c = st.config
+    for v in (c.rank, c.p, c.q, c.shared, c.temporal_mode):
+        u32(v)
+    u64(c.seed)
+    u8(1 if c.enforce_bounds else 0)
+    u32(0)
+    u8(1 if c.strict else 0)
+    f64(c.residual_warning)
+    u32(c.als.rank)
+    u32(c.als.max_iters)
+    f64(c.als.rel_tol)
+    u32(c.als.n_restarts)
+    u64(c.als.seed)
+    rs = st.replicas
+    u64(rs.seed)
+    u32(rs.q)
+    u32(rs.shared)
+    u32(rs.temporal_mode)
+    i64(rs.batches_drawn)
+    u64(len(rs.nontemporal_dims))
+    for d in rs.nontemporal_dims:
+        i64(d)
+    matrix(rs.temporal_shared_gram if rs.temporal_shared_gram is not None else np.zeros((rs.shared, rs.shared)))
+    u32(rs.p())
+    for rep in rs.replicas:
+        u32(rep.replica_id)
+        u64(len(rep.nontemporal))
+        for m in rep.nontemporal:
+            matrix(m)
+        i64(rep.temporal_window_start)
+        i64(rep.temporal_rows_total)
+        matrix(rep.temporal)
+    sm = st.summaries
+    i64(sm.batches_seen)
+    u64(len(sm.y))
+    for y, h in zip(sm.y, sm.history):
+        u64(y.ndim)
+        for d in y.shape:
+            i64(d)
+        u64(y.size)
+        out.extend(np.asfortranarray(y).tobytes(order="F"))
+        matrix(h)
+    u32(len(st.model.factors))
+    for f in st.model.factors:
+        matrix(f)
+    i64(len(st.model.lambda_))
+    out.extend(np.asarray(st.model.lambda_, dtype=np.float64).tobytes())
+    i64(st.slices_seen)
+    u64(len(st.log))
+    for r in st.log:
+        i64(r.batch_index)
+        i64(r.t_new)
+        f64(r.temporal_residual)
+        f64(r.min_match_similarity)
+        f64(r.max_offdiag_similarity)
+        u8(1 if r.warned else 0)
+    payload = bytes(out)
+    return b"OCTS" + struct.pack("<IQQ", 1, len(payload), _crc64(payload)) + payload
+
+
+def checkpoint_load(data: bytes) -> StreamState:
+    """checkpoint.cpp:222-295 (header checks in the reference's order)."""
+    import struct
+    if len(data) < 24 or data[:4] != b"OCTS":
+        raise IoError("checkpoint: bad magic")
+    version, plen, crc = struct.unpack("<IQQ", data[4:24])
+    if version != 1:
+        raise IoError("checkpoint: unsupported format version %d" % version)
+    if len(data) != 24 + plen:
+        raise IoError("checkpoint: payload length mismatch (corrupt or truncated)")
+    payload = data[24:]
+    if _crc64(payload) != crc:
+        raise IoError("checkpoint: checksum mismatch")
+    pos = [0]
+
+    def take(fmt):
+        n = struct.calcsize(fmt)
+        if pos[0] + n > len(payload):
+            raise IoError("checkpoint: truncated payload")
+        v = struct.unpack(fmt, payload[pos[0]:pos[0] + n])
+        pos[0] += n
+        return v[0] if len(v) == 1 else v
+
+    def doubles(n):
+        if pos[0] + 8 * n > len(payload):
+            raise IoError("checkpoint: truncated payload")
+        v = np.frombuffer(payload, dtype="<f8", count=n, offset=pos[0]).copy()
+        pos[0] += 8 * n
+        return v
+
+    def matrix():
+        r, c_ = take("<q"), take("<q")
+        if r < 0 or c_ < 0:
+            raise IoError("checkpoint: negative matrix extent")
+        return doubles(r * c_).reshape((r, c_), order="F")
+
+    cfg = StreamConfig()
+    cfg.rank, cfg.p, cfg.q, cfg.shared, cfg.temporal_mode = (take("<I") for _ in range(5))
+    cfg.seed = take("<Q")
+    cfg.enforce_bounds = take("<B") != 0
+    cfg.workers = take("<I")
+    cfg.strict = take("<B") != 0
+    cfg.residual_warning = take("<d")
+    cfg.als = AlsConfig(take("<I"), take("<I"), take("<d"), take("<I"), take("<Q"))
+    rseed = take("<Q")
+    q, shared, tmode = take("<I"), take("<I"), take("<I")
+    drawn = take("<q")
+    nd = take("<Q")
+    dims = [take("<q") for _ in range(nd)]
+    tg = matrix()
+    p = take("<I")
+    reps = []
+    for _ in range(p):
+        rid = take("<I")
+        nm = take("<Q")
+        mats = [matrix() for _ in range(nm)]
+        ws, tot = take("<q"), take("<q")
+        reps.append(CompressionReplica(rid, mats, matrix(), ws, tot))
+    rs = ReplicaSet(reps, rseed, q, shared, tmode, dims, drawn, tg)
+    seen = take("<q")
+    ns = take("<Q")
+    ys, hs = [], []
+    for _ in range(ns):
+        nd2 = take("<Q")
+        shape = [take("<q") for _ in range(nd2)]
+        n = take("<Q")
+        ys.append(doubles(n).reshape(shape, order="F"))
+        hs.append(matrix())
+    order = take("<I")
+    factors = [matrix() for _ in range(order)]
+    lam = doubles(take("<q"))
+    st = StreamState(cfg, rs, SummaryState(ys, hs, seen), KruskalModel(factors, lam))
+    st.slices_seen = take("<q")
+    nlog = take("<Q")
+    for _ in range(nlog):
+        rec = BatchRecord(take("<q"), take("<q"))
+        rec.temporal_residual, rec.min_match_similarity, rec.max_offdiag_similarity = take("<d"), take("<d"), take("<d")
+        rec.warned = take("<B") != 0
+        st.log.append(rec)
+    if pos[0] != len(payload):
+        raise IoError("checkpoint: trailing bytes after payload")
+    return st
 
 
 def memory_account(cfg, nontemporal_dims, t_old: int, t_new: int) -> dict:

@@ -306,6 +306,14 @@ class StreamState:
         keys = ["gemm_ms", "gemm_launches", "gemm_flops", "mttkrp_ms", "mttkrp_launches", "mttkrp_bytes", "sweeps"]
         return dict(zip(keys, list(out)[:7]))
 
+    def checkpoint_save(self) -> bytes:
+        """checkpoint_save (checkpoint.cpp:168-219): the OCTS bytes."""
+        n = C.c_i64()
+        _check(C.LIB.octen_stream_checkpoint_save(self._h, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_uint8 * n.value)()
+        _check(C.LIB.octen_stream_checkpoint_save(self._h, buf, n.value, ctypes.byref(n)))
+        return bytes(buf)
+
     def footprint(self) -> dict:
         """measure_footprint (eval.cpp:48-60) of the device-resident state."""
         out = (C.c_i64 * 4)()
@@ -349,6 +357,21 @@ def init_stream(first_batch, cfg: StreamConfig) -> StreamState:
     del keep
     st = StreamState(h, cfg)
     st._dims = (dims[0], dims[1])
+    return st
+
+
+def checkpoint_load(data: bytes, device: int = 0) -> StreamState:
+    """checkpoint_load (checkpoint.cpp:222-295): a device stream from OCTS
+    bytes (the reference's, the oracle's or this library's)."""
+    h = ctypes.c_void_p()
+    buf = (ctypes.c_uint8 * len(data)).from_buffer_copy(data)
+    _check(C.LIB.octen_stream_checkpoint_load(buf, len(data), device, ctypes.byref(h)))
+    # the StreamConfig the container holds
+    import struct
+    rank, p, q, shared, tmode = struct.unpack("<IIIII", data[24:44])
+    seed = struct.unpack("<Q", data[44:52])[0]
+    cfg = StreamConfig(rank=rank, p=p, q=q, shared=shared, seed=seed, temporal_mode=tmode, device=device)
+    st = StreamState(h, cfg)
     return st
 
 

@@ -70,6 +70,9 @@ SIGNATURES = {
     "octen_stream_ingest_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                  ctypes.c_int, P_i64]),
     "octen_stream_sync": (ctypes.c_int, [ctypes.c_void_p]),
+    "octen_stream_checkpoint_save": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, c_i64, P_i64]),
+    "octen_stream_checkpoint_load": (ctypes.c_int, [ctypes.c_void_p, c_i64, ctypes.c_int,
+                                                    ctypes.POINTER(ctypes.c_void_p)]),
     "octen_stream_log_size": (ctypes.c_int, [ctypes.c_void_p, P_i64]),
     "octen_stream_get_kernel_stats": (ctypes.c_int, [ctypes.c_void_p, P_dbl]),
     "octen_stream_set_publish": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),

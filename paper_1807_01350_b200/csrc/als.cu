@@ -1583,6 +1583,10 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     // sweep is enqueued as two segments, each segment for every lane in turn,
     // so the GEMM stream alternates between lanes.
     krec.clear();
+    // sampled: lane 0, every fifth sweep (an event between two programmatic
+    // dependent launches costs the overlap PDL buys: timing every launch
+    // measured +2 ms per c3 batch)
+    auto ktime_on = [&](int l, int sw) { return l == 0 && sw % 5 == 2; };
     auto ktime_begin = [&](cudaStream_t ss) {
         const int i = (int)krec.size() * 2;
         while ((int)kev.size() < i + 2) {
@@ -1610,7 +1614,8 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
                 OCTEN_CUDA(cudaStreamWaitEvent(gs, lane_ev[kGin + l], 0));
                 pd = false;
             }
-            const int kt0 = ktime_begin(gs);
+            const bool kt_on = ktime_on(l, sw);
+            const int kt0 = kt_on ? ktime_begin(gs) : -1;
             if (contracted == 2) {  // rows (i, j)
                 if (pipe_ok)
                     gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmatP{x.Y, q3, q2}, FacP{x.F, S, Q, R, 2},
@@ -1633,7 +1638,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
                     gemm_f64<true, true>(pn, (int)q2, SR, Q, Y0tA{x.Y, q3, Q}, FacB{x.F, S, Q, R, 0},
                                          TStore{x.T, q2, SR}, gs);
             }
-            ktime_end(kt0, gs, true, 2.0 * (double)pn * (double)q2 * SR * Q);
+            if (kt_on) ktime_end(kt0, gs, true, 2.0 * (double)pn * (double)q2 * SR * Q);
             if (gsplit) {
                 OCTEN_CUDA(cudaEventRecord(lane_ev[kGout + l], gs));
                 OCTEN_CUDA(cudaStreamWaitEvent(ss, lane_ev[kGout + l], 0));
@@ -1642,7 +1647,8 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         };
         auto mode_step = [&](int contract_first, int fsrc, int mode) {
             const int fz = fuse_update ? 1 : 0;
-            const int kt1 = ktime_begin(ss);
+            const bool kt_on = ktime_on(l, sw);
+            const int kt1 = kt_on ? ktime_begin(ss) : -1;
             if (use_pdl) {
                 launch_pdl(mttkrp_kernel, dim3(npn * (R + 1)), dim3(256), smem_mk, ss, x, contract_first, fsrc, mode,
                            sw, fz);
@@ -1650,7 +1656,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
                 mttkrp_kernel<<<npn * (R + 1), 256, smem_mk, ss>>>(x, contract_first, fsrc, mode, sw, fz);
                 OCTEN_LAUNCHED(1);
             }
-            ktime_end(kt1, ss, false, (double)npn * R * q2 * sizeof(double));  // T columns read (active problems at most)
+            if (kt_on) ktime_end(kt1, ss, false, (double)npn * R * q2 * sizeof(double));  // T columns read (active problems at most)
             mark(l, sw, mode == 0 ? "mttkrp0" : mode == 1 ? "mttkrp1" : "mttkrp2", ss);
             if (fuse_update) return;
             if (use_pdl) {

@@ -109,6 +109,7 @@ octen::StreamCfg to_cfg(const octen_stream_config* c) {
     s.als_max_iters = c->als.max_iters;
     s.als_n_restarts = c->als.n_restarts;
     s.als_rel_tol = c->als.rel_tol;
+    s.als_seed = c->als.seed;
     s.seed = c->seed;
     s.enforce_bounds = c->enforce_bounds != 0;
     s.strict = c->strict != 0;
@@ -273,6 +274,28 @@ void octen_synth_destroy(octen_synth* h) {
     if (h->g) cudaSetDevice(h->g->device);
     delete h;
     cudaSetDevice(cur);
+}
+
+int octen_stream_checkpoint_save(octen_stream* s, uint8_t* buf, int64_t cap, int64_t* size) {
+    return sguard(s, [&] {
+        if (!size) throw octen::ConfigError("octen_stream_checkpoint_save: null argument");
+        std::vector<std::uint8_t> b = s->s->checkpoint_save();
+        *size = (int64_t)b.size();
+        if (buf) {
+            if (cap < (int64_t)b.size()) throw octen::ConfigError("octen_stream_checkpoint_save: buffer too small");
+            std::memcpy(buf, b.data(), b.size());
+        }
+    });
+}
+
+int octen_stream_checkpoint_load(const uint8_t* bytes, int64_t n, int device, octen_stream** out) {
+    return guard([&] {
+        if (!bytes || !out || n < 0) throw octen::ConfigError("octen_stream_checkpoint_load: null argument");
+        DeviceGuard dg(device);
+        auto h = std::make_unique<octen_stream>();
+        h->s = octen::Stream::checkpoint_load(bytes, (size_t)n, device);
+        *out = h.release();
+    });
 }
 
 int octen_congruence(int order, int rank, const int64_t* dims, const double* ground, const double* est,

@@ -60,8 +60,9 @@ public:
     int host_syncs = 0;
     AlsFailure failure;  // set when run() throws a NumericError
     // Live kernel timing (CUDA events on the launching lane stream, summed
-    // after each run): the T-GEMMs and the MTTKRP (+ fused update) launches,
-    // with their algorithmic flops / bytes.
+    // after each run; sampled: lane 0, every fifth sweep): the T-GEMMs and
+    // the MTTKRP (+ fused update) launches, with their algorithmic flops /
+    // bytes.  `sweeps` counts every sweep.
     struct KernelStats {
         double gemm_ms = 0, gemm_flops = 0, mttkrp_ms = 0, mttkrp_bytes = 0;
         long long gemm_launches = 0, mttkrp_launches = 0, sweeps = 0;

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <exception>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -24,6 +25,7 @@ struct StreamCfg {
     int rank = 1, p = 1, q = 1, shared = 0, temporal_mode = -1;
     int als_max_iters = 100, als_n_restarts = 3;
     double als_rel_tol = 1e-8;
+    std::uint64_t als_seed = 0;  // AlsConfig.seed (checkpointed; per-replica seeds derive from `seed`)
     std::uint64_t seed = 0;
     bool enforce_bounds = false, strict = false;
     int workers = 0;
@@ -108,6 +110,10 @@ public:
     void ingest_async(const void* data, int dtype, int location, int order, const std::int64_t* dims);
     // Wait for the pending merge; rethrows its error.
     void sync();
+    // OCTS checkpoint (checkpoint.cpp:125-295) of the stream between batches,
+    // and a stream rebuilt from one (checkpoint.cu).
+    std::vector<std::uint8_t> checkpoint_save();
+    static std::unique_ptr<Stream> checkpoint_load(const std::uint8_t* bytes, size_t n, int device);
     // Model publication for pipelined callers: with `publish` on, every
     // finished batch copies its model (A, B, C, lambda) to host memory; the
     // copy is read without waiting for the merge in flight.

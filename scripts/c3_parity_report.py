@@ -1,6 +1,7 @@
 """Device stream vs the CPU oracle at the c3 shapes (I = J = 1000, Q = 100,
-P = 16, R = 20, shared = 10, CP-ALS 30 x 3; K0 = 200 + one batch of 100
-slices), fp32 inputs, at BASELINE's 1 % noise and at 0.1 %.  Writes the
+P = 16, shared = 10, CP-ALS 30 x 3; K0 = 200 + one batch of 100 slices),
+fp32 inputs: rank 20 (BASELINE c3) at 1 % and 0.1 % noise, and rank 5 at
+1 % noise (a well-posed stream at the same shapes).  Writes the
 comparison (summary error, per-replica fits, final fitness, congruence,
 temporal residuals) to profiles/r2_c3_parity.json.  GPU box; test-only use
 of the oracle."""
@@ -12,10 +13,10 @@ from threadpoolctl import threadpool_limits
 from oracle import octen_oracle as O
 import paper_1807_01350_b200 as ob
 
-I, Q, P, R, SH, K0, T = 1000, 100, 16, 20, 10, 200, 100
-out = {"config": {"I": I, "J": I, "K0": K0, "t": T, "Q": Q, "P": P, "R": R, "shared": SH, "iters": 30,
+I, Q, P, SH, K0, T = 1000, 100, 16, 10, 200, 100
+out = {"config": {"I": I, "J": I, "K0": K0, "t": T, "Q": Q, "P": P, "shared": SH, "iters": 30,
                   "restarts": 3, "inputs": "fp32 (oracle: the same values in fp64)"}, "runs": []}
-for noise in (0.01, 0.001):
+for noise, R in ((0.01, 20), (0.001, 20), (0.01, 5)):
     x, _ = O.generate_synthetic([I, I, K0 + T], R, 3, 0.0, 0.0)
     x += noise * np.sqrt(np.mean(x ** 2)) * np.random.default_rng(4).standard_normal(x.shape)
     x32 = np.asfortranarray(x.astype(np.float32))
@@ -48,7 +49,7 @@ for noise in (0.01, 0.001):
             w = O.cp_als(ref.summaries.y[r], O.AlsConfig(R, 30, 1e-8, 3, seeds[r]))
             reps.append({"replica": r, "fit_device": float(dfits[r]), "fit_oracle": float(w.fit),
                          "fms": float(min(O.congruence(O.KruskalModel(dm[r].factors, dm[r].lambda_), w.model)))})
-    run = {"noise": noise, "summary_max_rel_err": yerr, "fitness_device_pct": fd, "fitness_oracle_pct": fo,
+    run = {"noise": noise, "rank": R, "summary_max_rel_err": yerr, "fitness_device_pct": fd, "fitness_oracle_pct": fo,
            "congruence_min": float(min(cong)), "congruence_mean": float(np.mean(cong)),
            "temporal_residual_device": [r.temporal_residual for r in st.log],
            "temporal_residual_oracle": [r.temporal_residual for r in ref.log],

@@ -32,10 +32,10 @@ def test_synth_matches_reference_generator(ob, dims, rank, sigma, batches):
         ref = want[:, :, k:k + t]
         assert np.max(np.abs(got - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref)))
         k += t
-    m = g.truth()
+    m = g.truth()  # normalize() of the bit-identical factors (norms summed in another order)
     for f, h in zip(m.factors, truth.factors):
-        assert np.array_equal(f, h)
-    assert np.allclose(m.lambda_, truth.lambda_, rtol=0, atol=0)
+        assert np.allclose(f, h, rtol=1e-14, atol=0)
+    assert np.allclose(m.lambda_, truth.lambda_, rtol=1e-14, atol=0)
     with pytest.raises(ob.ConfigError, match="gen: slice range outside the tensor"):
         g.next(1)
 
