@@ -18,6 +18,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -198,7 +199,8 @@ inline void refresh(StreamState& st) {
     }
     st.model.lambda.assign((size_t)rank, 0.0);
     check(octen_stream_get_lambda(st.handle.get(), st.model.lambda.data()));
-    const std::int64_t nlog = info[7];
+    std::int64_t nlog = 0;  // one record per successful batch (a failed one still counts in batches_seen)
+    check(octen_stream_log_size(st.handle.get(), &nlog));
     st.log.resize((size_t)nlog);
     for (std::int64_t i = 0; i < nlog; ++i) {
         octen_batch_record r{};
@@ -246,6 +248,88 @@ inline void ingest_batch_f32(StreamState& st, const std::vector<std::int64_t>& d
     check(octen_stream_ingest(st.handle.get(), data, OCTEN_F32, OCTEN_HOST, (int)dims.size(), dims.data()));
     detail::refresh(st);
 }
+
+// Pipelined ingest (no reference counterpart; same results as ingest_batch):
+// the batch's merge overlaps the next call's compression and CP-ALS.  The
+// host model/log copies are refreshed by sync(); an error of the pending
+// merge is thrown by the next ingest_batch_async or sync.
+inline void ingest_batch_async(StreamState& st, const DenseTensor& batch) {
+    if (!st.handle) throw ConfigError("ingest_batch: stream is not initialised");
+    check(octen_stream_ingest_async(st.handle.get(), batch.data.data(), OCTEN_F64, OCTEN_HOST, batch.order(),
+                                    batch.dims.data()));
+}
+inline void sync(StreamState& st) {
+    check(octen_stream_sync(st.handle.get()));
+    detail::refresh(st);
+}
+
+// checkpoint_save / checkpoint_load (proj/include/cpstream/streaming.hpp:78-79):
+// the OCTS bytes of the device-resident stream, byte-compatible with the
+// reference's container.
+inline std::vector<std::uint8_t> checkpoint_save(const StreamState& st) {
+    std::int64_t n = 0;
+    check(octen_stream_checkpoint_save(st.handle.get(), nullptr, 0, &n));
+    std::vector<std::uint8_t> b((size_t)n);
+    check(octen_stream_checkpoint_save(st.handle.get(), b.data(), n, &n));
+    return b;
+}
+inline StreamState checkpoint_load(const std::vector<std::uint8_t>& bytes, int device = 0) {
+    octen_stream* raw = nullptr;
+    check(octen_stream_checkpoint_load(bytes.data(), (std::int64_t)bytes.size(), device, &raw));
+    StreamState st;
+    st.handle = std::shared_ptr<octen_stream>(raw, octen_stream_destroy);
+    // the config the container holds (checkpoint.cpp:125-143)
+    auto u32 = [&](size_t off) {
+        std::uint32_t v;
+        std::memcpy(&v, bytes.data() + off, 4);
+        return (int)v;
+    };
+    st.config.rank = u32(24);
+    st.config.p = u32(28);
+    st.config.q = u32(32);
+    st.config.shared = u32(36);
+    st.config.temporal_mode = u32(40);
+    std::memcpy(&st.config.seed, bytes.data() + 44, 8);
+    st.config.device = device;
+    detail::refresh(st);
+    return st;
+}
+
+// One rank of a replica-sharded stream with library-owned NCCL collectives
+// (octen_stream_create_nccl): the caller distributes the unique id of rank 0
+// and every rank ingests the same sequence of batches.  The reference's
+// parallel_replicas (src/streaming.cpp:45-69) across GPUs.
+class ShardedStream {
+public:
+    static std::vector<std::uint8_t> nccl_unique_id() {
+        std::vector<std::uint8_t> id(128);
+        check(octen_nccl_get_unique_id(id.data()));
+        return id;
+    }
+    ShardedStream(const StreamConfig& cfg, int rank, int world, const std::vector<std::uint8_t>& uid) {
+        const octen_stream_config c = detail::to_c(cfg);
+        octen_stream* raw = nullptr;
+        check(octen_stream_create_nccl(&c, rank, world, uid.data(), nullptr, &raw));
+        st_.config = cfg;
+        st_.handle = std::shared_ptr<octen_stream>(raw, octen_stream_destroy);
+    }
+    // init_stream on the first call, ingest_batch afterwards
+    void ingest(const DenseTensor& batch) {
+        check(octen_stream_ingest_sharded(st_.handle.get(), batch.data.data(), OCTEN_F64, OCTEN_HOST, batch.order(),
+                                          batch.dims.data()));
+        detail::refresh(st_);
+    }
+    // this rank's slices [k_off, k_off + local t) of a batch of t_total
+    void ingest_temporal(const DenseTensor& local, std::int64_t k_off, std::int64_t t_total) {
+        check(octen_stream_ingest_temporal(st_.handle.get(), local.data.data(), OCTEN_F64, OCTEN_HOST, local.order(),
+                                           local.dims.data(), k_off, t_total));
+        detail::refresh(st_);
+    }
+    const StreamState& state() const { return st_; }
+
+private:
+    StreamState st_;
+};
 
 // ---- sparse (COO) batches: proj/include/cpstream/tensor.hpp:66-90 ----
 // The reference validates entries in the SparseTensor constructor and

@@ -138,6 +138,28 @@ int octen_stream_set_publish(octen_stream* s, int on);
 int octen_stream_last_model(octen_stream* s, int64_t* info, double* a, double* b, double* c, int64_t c_rows_cap,
                             double* lambda);
 
+/* Library-owned collectives of a sharded stream (parallel_replicas,
+ * proj/src/streaming.cpp:45-69, across GPUs over NCCL on the stream's own
+ * CUDA stream; no reference counterpart).  octen_nccl_get_unique_id fills a
+ * 128-byte ncclUniqueId on one rank, which the caller distributes;
+ * octen_stream_create_nccl creates rank shard_rank of shard_world with a
+ * communicator from that id (uid128) or borrows the caller's ncclComm_t
+ * (nccl_comm, uid128 NULL).  octen_stream_ingest_sharded runs one batch
+ * (init on the first) with the replicas sharded: compress + CP-ALS of the
+ * owned replicas, ncclAllGather of the replica models, the merge,
+ * ncclAllGather of the temporal-stack rows, the temporal append.
+ * octen_stream_ingest_temporal runs one batch whose slices
+ * [k_off, k_off + local t) of t_total are this rank's: partial summaries of
+ * every replica, ncclReduceScatter to the owners, then the same.  Every rank
+ * calls with the same sequence of batches. */
+int octen_nccl_get_unique_id(uint8_t* out128);
+int octen_stream_create_nccl(const octen_stream_config* cfg, int shard_rank, int shard_world, const uint8_t* uid128,
+                             void* nccl_comm, octen_stream** out);
+int octen_stream_ingest_sharded(octen_stream* s, const void* data, int dtype, int location, int order,
+                                const int64_t* dims);
+int octen_stream_ingest_temporal(octen_stream* s, const void* data, int dtype, int location, int order,
+                                 const int64_t* dims_local, int64_t k_off, int64_t t_total);
+
 /* checkpoint_save / checkpoint_load (proj/include/cpstream/streaming.hpp:78-79;
  * src/checkpoint.cpp:125-295): the OCTS container of an unsharded stream
  * between batches, byte-compatible with the reference's.  save with

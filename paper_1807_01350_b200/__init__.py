@@ -549,6 +549,53 @@ class SynthStream:
         return KruskalModel(fs, lam)
 
 
+def nccl_unique_id() -> bytes:
+    """A 128-byte ncclUniqueId for octen_stream_create_nccl (one rank draws
+    it, the caller distributes it, e.g. torch.distributed.broadcast)."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(C.LIB.octen_nccl_get_unique_id(buf))
+    return bytes(buf)
+
+
+class NcclStream(StreamState):
+    """One rank of a sharded stream whose collectives the library runs over
+    NCCL on its own CUDA stream (octen_stream_create_nccl /
+    octen_stream_ingest_sharded / octen_stream_ingest_temporal): no caller
+    collectives between the phases."""
+
+    def __init__(self, cfg: StreamConfig, shard_rank: int, shard_world: int, uid: bytes = None, comm: int = None):
+        h = ctypes.c_void_p()
+        c = cfg._c()
+        ubuf = (ctypes.c_uint8 * 128).from_buffer_copy(uid) if uid is not None else None
+        _check(C.LIB.octen_stream_create_nccl(ctypes.byref(c), shard_rank, shard_world, ubuf,
+                                              ctypes.c_void_p(comm) if comm else None, ctypes.byref(h)))
+        super().__init__(h, cfg)
+        sz = (C.c_i64 * 6)()
+        _check(C.LIB.octen_stream_exchange_sizes(h, sz))
+        self.p0, self.p_local = sz[2], sz[3]
+        self.shard_rank, self.shard_world = shard_rank, shard_world
+
+    def summaries(self):
+        ys, hs = super().summaries()
+        return ys[:self.p_local], hs
+
+    def ingest(self, batch) -> None:
+        """init_stream on the first call, ingest_batch afterwards; replicas
+        sharded over the ranks, models and rows all-gathered by the library."""
+        keep, ptr, dt, loc, dims = _batch_args(batch)
+        d = (C.c_i64 * len(dims))(*dims)
+        _check(C.LIB.octen_stream_ingest_sharded(self._h, ptr, dt, loc, len(dims), d))
+        del keep
+
+    def ingest_temporal(self, local_slices, k_off: int, t_total: int) -> None:
+        """One batch whose slices [k_off, k_off + local t) of t_total are this
+        rank's; partial summaries reduce-scattered by the library."""
+        keep, ptr, dt, loc, dims = _batch_args(local_slices)
+        d = (C.c_i64 * len(dims))(*dims)
+        _check(C.LIB.octen_stream_ingest_temporal(self._h, ptr, dt, loc, len(dims), d, int(k_off), int(t_total)))
+        del keep
+
+
 def compress(batch, u: List[np.ndarray], v: List[np.ndarray], w: List[np.ndarray], shared: int) -> List[np.ndarray]:
     """compression.cpp:108-130 for every replica: z_r = x x1 U_r^T x2 V_r^T x3 W_r^T.
     u[r]: I x Q, v[r]: J x Q, w[r]: t x Q (temporal rows of this batch)."""

@@ -70,6 +70,13 @@ SIGNATURES = {
     "octen_stream_ingest_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                  ctypes.c_int, P_i64]),
     "octen_stream_sync": (ctypes.c_int, [ctypes.c_void_p]),
+    "octen_nccl_get_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+    "octen_stream_create_nccl": (ctypes.c_int, [ctypes.POINTER(StreamConfigC), ctypes.c_int, ctypes.c_int,
+                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "octen_stream_ingest_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                                   ctypes.c_int, P_i64]),
+    "octen_stream_ingest_temporal": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                                    ctypes.c_int, P_i64, c_i64, c_i64]),
     "octen_stream_checkpoint_save": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, c_i64, P_i64]),
     "octen_stream_checkpoint_load": (ctypes.c_int, [ctypes.c_void_p, c_i64, ctypes.c_int,
                                                     ctypes.POINTER(ctypes.c_void_p)]),

@@ -417,6 +417,45 @@ int octen_stream_create(const octen_stream_config* cfg, int shard_rank, int shar
     });
 }
 
+int octen_nccl_get_unique_id(uint8_t* out128) {
+    return guard([&] {
+        if (!out128) throw octen::ConfigError("octen_nccl_get_unique_id: null argument");
+        octen::nccl_unique_id(out128);
+    });
+}
+
+int octen_stream_create_nccl(const octen_stream_config* cfg, int shard_rank, int shard_world, const uint8_t* uid128,
+                             void* nccl_comm, octen_stream** out) {
+    return guard([&] {
+        if (!cfg || !out || (!uid128 && !nccl_comm))
+            throw octen::ConfigError("octen_stream_create_nccl: null argument");
+        DeviceGuard dg(cfg->device);
+        auto h = std::make_unique<octen_stream>();
+        h->s = std::make_unique<octen::Stream>(to_cfg(cfg), shard_rank, shard_world);
+        h->s->attach_nccl(uid128, nccl_comm);
+        *out = h.release();
+    });
+}
+
+int octen_stream_ingest_sharded(octen_stream* s, const void* data, int dtype, int location, int order,
+                                const int64_t* dims) {
+    return sguard(s, [&] {
+        if (!data || !dims) throw octen::ConfigError("octen_stream_ingest_sharded: null argument");
+        check_dtype(dtype, location);
+        s->s->ingest_sharded(data, dtype, location, order, dims);
+    });
+}
+
+int octen_stream_ingest_temporal(octen_stream* s, const void* data, int dtype, int location, int order,
+                                 const int64_t* dims_local, int64_t k_off, int64_t t_total) {
+    return sguard(s, [&] {
+        if (!dims_local || (!data && dims_local[2] > 0))
+            throw octen::ConfigError("octen_stream_ingest_temporal: null argument");
+        check_dtype(dtype, location);
+        s->s->ingest_temporal_nccl(data, dtype, location, order, dims_local, k_off, t_total);
+    });
+}
+
 int octen_stream_exchange_sizes(const octen_stream* s, int64_t* sizes) {
     return sguard(s, [&] {
         if (!s || !sizes) throw octen::ConfigError("octen_stream_exchange_sizes: null argument");

@@ -78,6 +78,14 @@ private:
     bool posted = false, running = false, done = false, quit = false;
 };
 
+// A sharded stream's NCCL communicator (nccl_exchange.cu).
+struct NcclExchange {
+    void* comm = nullptr;  // ncclComm_t
+    bool owned = false;
+    ~NcclExchange();
+};
+void nccl_unique_id(unsigned char* out128);
+
 // One stream handle.  Unsharded (world == 1) it owns every replica.  As rank
 // g of a replica-sharded stream (one process per GPU) it owns replicas
 // [p0, p0 + pl), pl <= chunk = ceil(P / world): it compresses the batch into
@@ -114,6 +122,14 @@ public:
     // and a stream rebuilt from one (checkpoint.cu).
     std::vector<std::uint8_t> checkpoint_save();
     static std::unique_ptr<Stream> checkpoint_load(const std::uint8_t* bytes, size_t n, int device);
+    // Library-owned collectives (nccl_exchange.cu): a communicator from a
+    // unique id (or a borrowed ncclComm_t), then whole batches with the
+    // all-gathers / reduce-scatter on the stream's own CUDA stream.
+    void attach_nccl(const unsigned char* uid128, void* borrowed_comm);
+    void ingest_sharded(const void* data, int dtype, int location, int order, const std::int64_t* dims);
+    void ingest_temporal_nccl(const void* data, int dtype, int location, int order, const std::int64_t* dims_local,
+                              std::int64_t k_off, std::int64_t t_total);
+    std::unique_ptr<NcclExchange> nccl_x;
     // Model publication for pipelined callers: with `publish` on, every
     // finished batch copies its model (A, B, C, lambda) to host memory; the
     // copy is read without waiting for the merge in flight.
@@ -173,7 +189,8 @@ public:
     int wslot = 0;
     double* dW = nullptr;
     DevBuf<double> xmodels, xrows, MfAll, MlamAll, tstackAll;
-    DevBuf<double> xmodels2;     // pipelined ingest: models of the batch in flight
+    DevBuf<double> xmodels2;     // pipelined ingest: models of the batch in flight (NCCL: all-gathered models)
+    DevBuf<double> rows_all_buf, part_buf, owned_buf;  // NCCL exchange buffers
     DevBuf<float> X32;
     DevBuf<int> flag;
     DevBuf<double> Zpart;                 // temporal sharding: partial summaries, world x chunk x Q^3
@@ -233,6 +250,7 @@ private:
     [[noreturn]] void fail_pending(BatchCtx& b);
     void begin_ctx(BatchCtx& b, bool first, std::int64_t t);
     void next_w_slot();
+    void exchange_allgather(const double* send, double* recv, size_t count);
 
     Snapshot backup;
 };

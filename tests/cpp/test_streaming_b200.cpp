@@ -264,6 +264,49 @@ int main() {
         const std::vector<DenseTensor> again = cs.summaries();
         CHECK(again[0].data == ys[0].data && again[1].data == ys[1].data);
     }
+    // TEST_CASE("checkpoint round trips") (test_streaming.cpp:205-247)
+    {
+        const DenseTensor full = reconstruct(random_truth({9, 8, 10}, 2, 71));
+        StreamState st = init_stream(slice_last(full, 0, 5), desk_config(2, 3, 6, 2, 53));
+        const std::vector<std::uint8_t> bytes = checkpoint_save(st);
+        CHECK(checkpoint_save(checkpoint_load(bytes)) == bytes);
+        StreamState resumed = checkpoint_load(bytes);
+        ingest_batch(st, slice_last(full, 5, 5));
+        ingest_batch(resumed, slice_last(full, 5, 5));
+        CHECK(checkpoint_save(st) == checkpoint_save(resumed));
+        std::vector<std::uint8_t> bad = bytes;
+        bad[bad.size() / 2] ^= 0x40;
+        CHECK(throws_as<IoError>([&] { checkpoint_load(bad); }, "checksum mismatch"));
+        bad = bytes;
+        bad.resize(bad.size() - 7);
+        CHECK(throws_as<IoError>([&] { checkpoint_load(bad); }, "payload length mismatch"));
+    }
+    // pipelined ingest == ingest_batch, byte for byte (the checkpoints)
+    {
+        const DenseTensor full = reconstruct(random_truth({12, 11, 12}, 3, 61));
+        const StreamConfig cfg = desk_config(3, 5, 8, 3, 43);
+        StreamState a = init_stream(slice_last(full, 0, 6), cfg);
+        StreamState b = init_stream(slice_last(full, 0, 6), cfg);
+        ingest_batch(a, slice_last(full, 6, 3));
+        ingest_batch(a, slice_last(full, 9, 3));
+        ingest_batch_async(b, slice_last(full, 6, 3));
+        ingest_batch_async(b, slice_last(full, 9, 3));
+        sync(b);
+        CHECK(b.slices_seen == 12 && b.log.size() == 3);
+        CHECK(checkpoint_save(a) == checkpoint_save(b));
+    }
+    // library-owned NCCL collectives, one rank: the unsharded stream's bits
+    {
+        const DenseTensor full = reconstruct(random_truth({14, 13, 12}, 2, 81));
+        const StreamConfig cfg = desk_config(2, 4, 6, 2, 31);
+        StreamState a = init_stream(slice_last(full, 0, 6), cfg);
+        ingest_batch(a, slice_last(full, 6, 6));
+        ShardedStream sh(cfg, 0, 1, ShardedStream::nccl_unique_id());
+        sh.ingest(slice_last(full, 0, 6));
+        sh.ingest(slice_last(full, 6, 6));
+        CHECK(sh.state().slices_seen == 12);
+        for (size_t m = 0; m < 3; ++m) CHECK(sh.state().model.factors[m].v == a.model.factors[m].v);
+    }
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
