@@ -533,6 +533,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--collectives", default="library", choices=["library", "torch"],
+                    help="N>1 sharded modes: the library's own NCCL communicator (default) or the caller's "
+                         "torch.distributed collectives between the library's phases")
     ap.add_argument("--multi", default="sharded", choices=["sharded", "temporal", "replicas"],
                     help="N>1: one replica-sharded stream over all ranks (NCCL all-gathers, strong scaling); "
                          "'temporal': the same with the compression sharded over the batch's slices "
@@ -584,7 +587,21 @@ def main():
                            device=local)
     torch.cuda.synchronize()
     t_init = time.perf_counter()
-    if sharded:
+    if sharded and args.collectives == "library":
+        # the library's own NCCL communicator (octen_stream_create_nccl): rank
+        # 0's unique id travels over the torch process group once
+        uid = torch.tensor(list(ob.nccl_unique_id() if rank == 0 else bytes(128)), dtype=torch.uint8, device=dev)
+        dist.broadcast(uid, 0)
+        st = ob.NcclStream(scfg, rank, world, uid=bytes(uid.cpu().tolist()))
+        if temporal:
+            def ingest(b):
+                tb = b.shape[2]
+                lo, hi = tb * rank // world, tb * (rank + 1) // world
+                st.ingest_temporal(b[:, :, lo:hi], lo, tb)
+        else:
+            ingest = st.ingest
+        ingest(first)
+    elif sharded:
         st = ob.ShardedStream(scfg, rank, world, lambda snd, rcv: dist.all_gather_into_tensor(rcv, snd))
         if temporal:
             def ingest(b):
