@@ -132,9 +132,11 @@ int octen_stream_sync(octen_stream* s);
  * copies its model to host memory, readable with octen_stream_last_model
  * without waiting for the merge in flight. */
 int octen_stream_set_publish(octen_stream* s, int on);
-/* The last published model: info[0] = rows of C (slices), info[1] = batches
- * finished (0: nothing published yet, nothing copied); a (I x R), b (J x R),
- * c (c_rows_cap x R, first info[0] rows written), lambda (R); col-major. */
+/* The last published model: info[0] = rows of the temporal factor (slices),
+ * info[1] = batches finished (0: nothing published yet, nothing copied);
+ * a, b: the two non-temporal factors in mode order (I x R, J x R), c: the
+ * temporal factor (c_rows_cap x R, first info[0] rows written), lambda (R);
+ * col-major. */
 int octen_stream_last_model(octen_stream* s, int64_t* info, double* a, double* b, double* c, int64_t c_rows_cap,
                             double* lambda);
 
@@ -203,7 +205,9 @@ int octen_stream_info(const octen_stream* s, int64_t* info);
  * bytes (owned replicas), out[2] factor bytes, out[3] accumulator bytes. */
 int octen_stream_footprint(const octen_stream* s, int64_t* out);
 
-/* KruskalModel factor `mode` (dim x rank, col-major) and lambda (rank). */
+/* KruskalModel factor `mode` (dim x rank, col-major; the stream's mode
+ * order) and lambda (rank).  octen_stream_get_model: the factors of modes
+ * 0, 1, 2 into a, b, c. */
 int octen_stream_get_factor(const octen_stream* s, int mode, double* out);
 int octen_stream_get_lambda(const octen_stream* s, double* out);
 /* The whole model in one call (one synchronisation): a I x R, b J x R,

@@ -281,8 +281,9 @@ class StreamState:
         """(KruskalModel, batches finished) of the last published model, or
         (None, 0) before the first publication."""
         info = (C.c_i64 * 2)()
-        if getattr(self, "_dims", None) is None:
-            self._dims = tuple(self._info()[1:3])  # (waits for the merge in flight once)
+        tm = self.config.temporal_mode if self.config.temporal_mode >= 0 else 2
+        if getattr(self, "_dims", None) is None:  # (waits for the merge in flight once)
+            self._dims = tuple(d for n, d in enumerate(self._info()[1:4]) if n != tm)
         dims, rank = self._dims, self.config.rank
         cap = getattr(self, "_last_cap", 0)
         while True:
@@ -297,7 +298,9 @@ class StreamState:
             cap = self._last_cap = int(info[0]) * 2
         if info[1] == 0:
             return None, 0
-        return KruskalModel([a, b, c[:info[0]].copy(order="F")], lam), int(info[1])
+        fs = [a, b]  # the non-temporal factors in mode order, the temporal one at its mode
+        fs.insert(tm, c[:info[0]].copy(order="F"))
+        return KruskalModel(fs, lam), int(info[1])
 
     def kernel_stats(self) -> dict:
         """Live CP-ALS kernel timing (octen_stream_get_kernel_stats)."""
@@ -356,7 +359,8 @@ def init_stream(first_batch, cfg: StreamConfig) -> StreamState:
     _check(C.LIB.octen_stream_init(ctypes.byref(c), ptr, dt, loc, len(dims), d, ctypes.byref(h)))
     del keep
     st = StreamState(h, cfg)
-    st._dims = (dims[0], dims[1])
+    tm = cfg.temporal_mode if cfg.temporal_mode >= 0 else len(dims) - 1
+    st._dims = tuple(d for n, d in enumerate(dims) if n != tm)  # the non-temporal extents
     return st
 
 

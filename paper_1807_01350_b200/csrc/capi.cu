@@ -498,9 +498,9 @@ int octen_stream_info(const octen_stream* s, int64_t* info) {
         s->s->sync();
         const auto& x = *s->s;
         info[0] = 3;
-        info[1] = x.I;
-        info[2] = x.J;
-        info[3] = x.K;
+        // extents in the stream's mode order (the temporal mode holds K)
+        const int64_t ext[3] = {x.I, x.J, x.K};
+        for (int n = 0; n < 3; ++n) info[1 + n] = x.initialized ? ext[x.factor_slot(n)] : 0;
         info[4] = x.cfg.rank;
         info[5] = x.cfg.p;
         info[6] = x.cfg.q;
@@ -536,10 +536,14 @@ int octen_stream_get_model(const octen_stream* s, double* a, double* b, double* 
         s->s->sync();
         auto& x = *s->s;
         const int R = x.cfg.rank;
-        OCTEN_CUDA(cudaMemcpyAsync(a, x.A.p, sizeof(double) * x.I * R, cudaMemcpyDeviceToHost, x.st));
-        OCTEN_CUDA(cudaMemcpyAsync(b, x.B.p, sizeof(double) * x.J * R, cudaMemcpyDeviceToHost, x.st));
-        OCTEN_CUDA(cudaMemcpy2DAsync(c, x.K * sizeof(double), x.C.p, x.capC * sizeof(double), x.K * sizeof(double), R,
-                                     cudaMemcpyDeviceToHost, x.st));
+        // a, b, c: the factors of modes 0, 1, 2 (the stream's mode order)
+        double* out[3] = {a, b, c};
+        double* slot_out[3] = {nullptr, nullptr, nullptr};
+        for (int n = 0; n < 3; ++n) slot_out[x.factor_slot(n)] = out[n];
+        OCTEN_CUDA(cudaMemcpyAsync(slot_out[0], x.A.p, sizeof(double) * x.I * R, cudaMemcpyDeviceToHost, x.st));
+        OCTEN_CUDA(cudaMemcpyAsync(slot_out[1], x.B.p, sizeof(double) * x.J * R, cudaMemcpyDeviceToHost, x.st));
+        OCTEN_CUDA(cudaMemcpy2DAsync(slot_out[2], x.K * sizeof(double), x.C.p, x.capC * sizeof(double),
+                                     x.K * sizeof(double), R, cudaMemcpyDeviceToHost, x.st));
         x.lam.download(lambda, R, x.st);
         OCTEN_CUDA(cudaStreamSynchronize(x.st));
     });
@@ -620,9 +624,15 @@ int octen_stream_get_replica_models(const octen_stream* s, double* factors, doub
         s->s->sync();
         auto& x = *s->s;
         const int P = x.cfg.p, Q = x.cfg.q, R = x.cfg.rank;
-        x.MfAll.download(factors, (size_t)P * 3 * Q * R, x.st);
+        const size_t qr = (size_t)Q * R;
+        std::vector<double> f = x.MfAll.to_host((size_t)P * 3 * qr, x.st);
         x.MlamAll.download(lambda, (size_t)P * R, x.st);
         OCTEN_CUDA(cudaStreamSynchronize(x.st));
+        // the merge keeps them in slot order; return the stream's mode order
+        for (int p = 0; p < P; ++p)
+            for (int n = 0; n < 3; ++n)
+                std::memcpy(factors + ((size_t)p * 3 + n) * qr, f.data() + ((size_t)p * 3 + x.factor_slot(n)) * qr,
+                            qr * sizeof(double));
     });
 }
 

@@ -158,9 +158,14 @@ std::vector<std::uint8_t> Stream::checkpoint_save() {
     }
     // model, slices seen, log (checkpoint.cpp:195-211)
     w.u32(3);
-    w.matrix(I, R, a.data());
-    w.matrix(J, R, b.data());
-    w.matrix(K, R, c.data());
+    {  // factors in the stream's mode order
+        const std::vector<double>* fs[3] = {&a, &b, &c};
+        const std::int64_t rows[3] = {I, J, K};
+        for (int n = 0; n < 3; ++n) {
+            const int sl = factor_slot(n);
+            w.matrix(rows[sl], R, fs[sl]->data());
+        }
+    }
     w.i64(R);
     w.raw(l.data(), sizeof(double) * R);
     w.i64(K);
@@ -218,8 +223,9 @@ std::unique_ptr<Stream> Stream::checkpoint_load(const std::uint8_t* bytes, size_
     const int tmode = (int)r.get<std::uint32_t>();
     const std::int64_t drawn = r.get<std::int64_t>();
     const std::uint64_t ndims = r.get<std::uint64_t>();
-    expect(ndims == 2 && tmode == 2 && q == c.q && sh == c.shared && rseed == c.seed,
-           "the device path holds order-3 streams with the temporal mode last");
+    expect(ndims == 2 && tmode >= 0 && tmode <= 2 && tmode == c.temporal_mode && q == c.q && sh == c.shared &&
+               rseed == c.seed,
+           "the device path holds order-3 streams");
     const std::int64_t I = r.get<std::int64_t>(), J = r.get<std::int64_t>();
     std::int64_t rows, cols;
     std::vector<double> tg = r.matrix(rows, cols);
@@ -259,12 +265,18 @@ std::unique_ptr<Stream> Stream::checkpoint_load(const std::uint8_t* bytes, size_
                 for (int a2 = 0; a2 < Q; ++a2) hs[(size_t)p * Q + a2 + (size_t)P * Q * rr] = h[a2 + (size_t)Q * rr];
     }
     expect(r.get<std::uint32_t>() == 3, "model order");
-    std::vector<double> a = r.matrix(rows, cols);
-    expect(rows == I && cols == R, "factor shape");
-    std::vector<double> b = r.matrix(rows, cols);
-    expect(rows == J && cols == R, "factor shape");
-    std::vector<double> cm = r.matrix(rows, cols);
-    expect(rows == K && cols == R, "factor shape");
+    std::vector<double> fsl[3];  // by slot: A, B, C
+    {
+        const std::int64_t want[3] = {I, J, K};
+        for (int n = 0; n < 3; ++n) {
+            const int sl = n == tmode ? 2 : (n < tmode ? n : n - 1);
+            fsl[sl] = r.matrix(rows, cols);
+            expect(rows == want[sl] && cols == R, "factor shape");
+        }
+    }
+    std::vector<double>& a = fsl[0];
+    std::vector<double>& b = fsl[1];
+    std::vector<double>& cm = fsl[2];
     expect(r.get<std::int64_t>() == R, "lambda length");
     std::vector<double> l(R);
     r.raw(l.data(), sizeof(double) * R);
@@ -291,9 +303,12 @@ std::unique_ptr<Stream> Stream::checkpoint_load(const std::uint8_t* bytes, size_
     s->hV = std::move(hV);
     s->tgram = std::move(tg);
     s->batches_drawn = drawn;
-    if (s->pl > 0)
+    if (s->pl > 0) {
         s->comp.set_projections(s->pl, Q, sh, I, J, s->hU.data(), s->hV.data(), s->st);
+        s->comp.set_temporal_mode(tmode);
+    }
     s->merge.set_projections(c.p, Q, sh, R, I, J, s->hU.data(), s->hV.data(), s->st);
+    s->set_mode_strides();
     s->Y.upload(y.data(), y.size(), s->st);
     s->hist.upload(hs.data(), hs.size(), s->st);
     s->A.upload(a.data(), a.size(), s->st);

@@ -97,13 +97,18 @@ struct G3B {  // B(p, k, c) = W[p][(k0 + k) + t c]
     int Q;
     __device__ double operator()(int p, int k, int c) const { return W[(size_t)p * t * Q + (k0 + k) + (size_t)t * c]; }
 };
-struct G3C {  // Yout[p][m + Q^2 c] = Yin[p][m + Q^2 c] + v   (in place when Yin == Yout)
+struct G3C {  // Yout[p](a, b, c) = Yin[p](a, b, c) + v, m = a + Q b   (in place when Yin == Yout)
     const double* Yin;
     double* Yout;
     int Q;
+    // element strides of (non-temporal slot 0, slot 1, temporal) in the
+    // summaries, which keep the stream's original mode order
+    // (compression.cpp:117-127): (1, Q, Q^2) when the temporal mode is last
+    int s0, s1, st;
     __device__ void operator()(int p, int m, int c, double v) const {
-        const size_t q2 = (size_t)Q * Q;
-        const size_t e = (size_t)p * q2 * Q + m + q2 * c;
+        const size_t q3 = (size_t)Q * Q * Q;
+        const int a = m % Q, b = m / Q;
+        const size_t e = (size_t)p * q3 + (size_t)a * s0 + (size_t)b * s1 + (size_t)c * st;
         Yout[e] = Yin[e] + v;
     }
 };
@@ -210,14 +215,16 @@ template <typename T>
 void run_accumulate(CompressEngine& e, std::int64_t t, const T* Z2, const double* dW, const double* dYin,
                     double* dY, cudaStream_t st) {
     const int Q = e.Q, P = e.P;
-    gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<T>{Z2, (int)t, Q}, G3B{dW, t, 0, Q}, G3C{dYin, dY, Q}, st);
+    gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<T>{Z2, (int)t, Q}, G3B{dW, t, 0, Q},
+                          G3C{dYin, dY, Q, e.ys[0], e.ys[1], e.ys[2]}, st);
     OCTEN_CUDA(cudaGetLastError());
 }
 
 }  // namespace
 
 void accumulate_z2_f32(int P, int Q, std::int64_t t, const float* Z2, const double* dW, double* dY, cudaStream_t st) {
-    gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<float>{Z2, (int)t, Q}, G3B{dW, t, 0, Q}, G3C{dY, dY, Q}, st);
+    gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<float>{Z2, (int)t, Q}, G3B{dW, t, 0, Q}, G3C{dY, dY, Q, 1, Q, Q * Q},
+                          st);
     OCTEN_CUDA(cudaGetLastError());
 }
 
@@ -250,6 +257,7 @@ void CompressEngine::set_projections(int P_, int Q_, int shared_, std::int64_t I
     P = P_;
     Q = Q_;
     shared = shared_;
+    set_temporal_mode(2);  // the stream sets its own after this
     I = I_;
     J = J_;
     Meff = shared + (std::int64_t)P * (Q - shared);
@@ -345,10 +353,10 @@ void CompressEngine::accumulate_rows(int dtype, std::int64_t t, const double* dW
                                      std::int64_t k0, double* dY, cudaStream_t st) {
     if (dtype == 1)
         gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<float>{Z2f.p, (int)t, Q}, G3B{dW, t_total, k0, Q},
-                              G3C{dY, dY, Q}, st);
+                              G3C{dY, dY, Q, ys[0], ys[1], ys[2]}, st);
     else
         gemm_f64<false, true>(P, Q * Q, Q, (int)t, G3A<double>{Z2d.p, (int)t, Q}, G3B{dW, t_total, k0, Q},
-                              G3C{dY, dY, Q}, st);
+                              G3C{dY, dY, Q, ys[0], ys[1], ys[2]}, st);
     OCTEN_CUDA(cudaGetLastError());
 }
 

@@ -128,6 +128,15 @@ public:
 
     int P = 0, Q = 0, shared = 0;
     std::int64_t I = 0, J = 0, Meff = 0;
+    // element strides in Y_p of (non-temporal slot 0, slot 1, temporal): the
+    // summaries keep the stream's mode order (set_temporal_mode)
+    int ys[3] = {1, 0, 0};
+    void set_temporal_mode(int tm) {
+        const int q2 = Q * Q;
+        if (tm == 2) { ys[0] = 1; ys[1] = Q; ys[2] = q2; }
+        else if (tm == 1) { ys[0] = 1; ys[1] = q2; ys[2] = Q; }
+        else { ys[0] = Q; ys[1] = q2; ys[2] = 1; }
+    }
     DevBuf<float> A32;   // Meff x I row-major (deduplicated shared columns)
     DevBuf<float> Ahi, Alo;  // TF32 split of the fp64 projections (tcgen05 path)
     int lda_tc = 0;
@@ -246,6 +255,9 @@ public:
     DevBuf<double> Lsum_inv[2], Gw_inv;  // diagonal-block inverses of the factors
     DevBuf<double> Ginv[2];  // (sum_p G_p)^-1, full d x d
     int sum_rank[2] = {0, 0};
+    // strides of (slot 0, slot 1, temporal) in the summaries (temporal_stack)
+    int ys[3] = {1, 0, 0};
+    void set_ystrides(const int* s) { ys[0] = s[0]; ys[1] = s[1]; ys[2] = s[2]; }
     bool sum_qr[2] = {false, false};  // full rank only by the QR rule: solve by QR each batch
     int qr_rank_check(int n, const double* w, int r, const double* rhs, double* x, cudaStream_t st);
     DevBuf<double> Lw[2];    // shared x shared whitener (non-temporal modes)

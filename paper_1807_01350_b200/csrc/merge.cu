@@ -91,10 +91,14 @@ struct KrB {  // B(p, k = a + Q b, r) = Ut(a, r) * Vt(b, r), Ut/Vt: P x Q x R
         return Ut[(size_t)p * Q * R + a + (size_t)Q * r] * Vt[(size_t)p * Q * R + b + (size_t)Q * r];
     }
 };
-struct YtA2 {  // A(p, c, k) = Y[p][k + Q^2 c]
+struct YtA2 {  // A(p, c, k) = Y_p(a, b, c), k = a + Q b: the temporal unfolding (columns: slot 0 fastest)
     const double* Y;
     size_t q3, q2;
-    __device__ double operator()(int p, int c, int k) const { return Y[(size_t)p * q3 + k + q2 * c]; }
+    int Q, s0, s1, st;  // element strides of (slot 0, slot 1, temporal) in Y (the stream's mode order)
+    __device__ double operator()(int p, int c, int k) const {
+        const int a = k % Q, b = k / Q;
+        return Y[(size_t)p * q3 + (size_t)a * s0 + (size_t)b * s1 + (size_t)c * st];
+    }
 };
 
 // Small-output, long-K GEMMs of the merge (d x R right-hand sides with
@@ -897,6 +901,9 @@ void MergeEngine::set_projections(int P_, int Q_, int sh, int R_, std::int64_t I
     R = R_;
     dims[0] = I;
     dims[1] = J;
+    ys[0] = 1;  // temporal mode last unless the stream says otherwise (set_ystrides)
+    ys[1] = Q;
+    ys[2] = Q * Q;
     if (R > 64) throw ConfigError("octen: device merge supports rank <= 64");
     if (P > 64) throw ConfigError("octen: device merge supports p <= 64");
     const long long PQ = (long long)P * Q;
@@ -1138,7 +1145,7 @@ void MergeEngine::temporal_stack(const double* dY, int p0, int pl, const double*
     tmp.reserve((size_t)pl * Q * R);
     const int ks = pick_ksplit(pl, Q, R, (int)q2);
     tscr.reserve((size_t)pl * ks * Q * R);
-    gemm_f64<true, true>(pl, Q, R, (int)q2, YtA2{dY, q3, q2}, KrB{Ut, Vt, Q, R},
+    gemm_f64<true, true>(pl, Q, R, (int)q2, YtA2{dY, q3, q2, Q, ys[0], ys[1], ys[2]}, KrB{Ut, Vt, Q, R},
                                           StoreCM{tmp.p, Q, (long long)Q * R}, st, ks, tscr.p);
     const size_t smem = (size_t)(3 * R * R + 2 * (R + 2)) * sizeof(double) + (R + 8) * sizeof(int) + 16;
     const long long sp = replica_major ? (long long)Q * R : (long long)Q;

@@ -90,6 +90,31 @@ __global__ void normalize_model_kernel(double* A, long long I, double* B, long l
     if (threadIdx.x == 0) lam[r] = l;
 }
 
+// A batch with the temporal mode at position tm, as the I x J x t
+// temporal-last block the compression contracts: out(i, j, k) =
+// X(i, j, k) read with the strides of the batch's own mode order.
+template <typename T>
+__global__ void to_temporal_last_kernel(const T* __restrict__ X, T* __restrict__ out, long long I, long long J,
+                                        long long t, long long sI, long long sJ, long long sT) {
+    const long long n = I * J * t;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e % I, r = e / I, j = r % J, k = r / J;
+        out[e] = X[i * sI + j * sJ + k * sT];
+    }
+}
+// replica factors (P x 3 x Q x R, the stream's mode order) into slot order:
+// non-temporal slot 0, slot 1, then the temporal factor
+__global__ void factors_to_slots_kernel(const double* __restrict__ in, double* __restrict__ out, int P, long long qr,
+                                        int m0, int m1, int mt) {
+    const long long n = (long long)P * 3 * qr;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const long long x = e % qr, r = e / qr;
+        const int slot = (int)(r % 3), p = (int)(r / 3);
+        const int m = slot == 0 ? m0 : (slot == 1 ? m1 : mt);
+        out[e] = in[((long long)p * 3 + m) * qr + x];
+    }
+}
+
 int grid1d(size_t n) {
     size_t b = (n + 255) / 256;
     if (b > 148 * 8) b = 148 * 8;
@@ -151,8 +176,8 @@ void Stream::validate(int order) {
     if (cfg.shared < 0 || cfg.shared >= cfg.q) throw ConfigError("stream: shared must lie in [0, Q)");
     if (cfg.temporal_mode >= order) throw ConfigError("stream: temporal mode out of range");
     if (cfg.p >= 2 && cfg.shared < 1) throw ConfigError("stream: alignment across replicas needs shared >= 1");
-    if (order != 3 || cfg.temporal_mode != 2)
-        throw ConfigError("octen: the device path supports order-3 streams with the temporal mode last");
+    if (order != 3)
+        throw ConfigError("octen: the device path supports order-3 streams (any temporal mode)");
 }
 
 void Stream::gen_replicas() {
@@ -268,6 +293,73 @@ void Stream::check_finite(const void* dX, int dtype, size_t n) {
     if (flag.to_host(1, st)[0]) throw NumericError("DenseTensor: non-finite value");
 }
 
+// streaming.cpp:263-269: every non-temporal extent must match (messages
+// name the mode 1-based, in the stream's own mode order)
+void Stream::check_extents(const std::int64_t* dims) {
+    const int tm = cfg.temporal_mode;
+    const std::int64_t want[2] = {I, J};
+    int slot = 0;
+    for (int n = 0; n < 3; ++n) {
+        if (n == tm) continue;
+        if (dims[n] != want[slot])
+            throw ConfigError("ingest_batch: extent mismatch on mode " + std::to_string(n + 1) + " at batch " +
+                              std::to_string(batches_seen));
+        ++slot;
+    }
+    if (dims[tm] < 1) throw ConfigError("ingest_batch: batch has no temporal extent");
+}
+
+// The batch (the stream's mode order, first index fastest) as the I x J x t
+// temporal-last block on the device.
+const void* Stream::temporal_last(const void* data, int dtype, int location, const std::int64_t* dims) {
+    const int tm = cfg.temporal_mode;
+    const std::int64_t t = dims[tm];
+    const size_t n = (size_t)I * J * t, esz = dtype == 1 ? sizeof(float) : sizeof(double);
+    const void* src = data;
+    if (location == 0) {
+        void* d = dtype == 1 ? (void*)X32.reserve(n) : (void*)X64.reserve(n);
+        OCTEN_CUDA(cudaMemcpyAsync(d, data, n * esz, cudaMemcpyHostToDevice, st));
+        src = d;
+    }
+    long long stride[3] = {1, dims[0], dims[0] * dims[1]};
+    const long long sI = stride[tm == 0 ? 1 : 0], sJ = stride[tm == 2 ? 1 : 2], sT = stride[tm];
+    void* out;
+    if (dtype == 1) {
+        out = XT32.reserve(n);
+        to_temporal_last_kernel<float><<<grid1d(n), 256, 0, st>>>((const float*)src, (float*)out, I, J, t, sI, sJ, sT);
+    } else {
+        out = XT64.reserve(n);
+        to_temporal_last_kernel<double><<<grid1d(n), 256, 0, st>>>((const double*)src, (double*)out, I, J, t, sI, sJ,
+                                                                   sT);
+    }
+    OCTEN_LAUNCHED(1);
+    OCTEN_CUDA(cudaGetLastError());
+    return out;
+}
+
+// strides of (slot 0, slot 1, temporal) in the summaries for the merge's
+// temporal unfolding
+void Stream::set_mode_strides() {
+    const int Q = cfg.q, tm = cfg.temporal_mode, q2 = Q * Q;
+    int s3[3];
+    if (tm == 2) {
+        s3[0] = 1; s3[1] = Q; s3[2] = q2;
+    } else if (tm == 1) {
+        s3[0] = 1; s3[1] = q2; s3[2] = Q;
+    } else {
+        s3[0] = Q; s3[1] = q2; s3[2] = 1;
+    }
+    merge.set_ystrides(s3);
+}
+
+// the model's factor of mode n (the stream's mode order): A, B are the
+// non-temporal slots, C the temporal factor
+int Stream::factor_slot(int mode) const {
+    const int tm = cfg.temporal_mode;
+    if (mode == tm) return 2;
+    return mode < tm ? mode : mode - 1;
+}
+
 void Stream::ensure_c_capacity(std::int64_t rows, cudaStream_t st) {
     if (rows <= capC && C.p) return;
     std::int64_t cap = std::max<std::int64_t>(capC * 2, rows);
@@ -286,10 +378,12 @@ void Stream::ensure_c_capacity(std::int64_t rows, cudaStream_t st) {
 void Stream::prepare(int order, const std::int64_t* dims) {
     if (cfg.temporal_mode < 0) cfg.temporal_mode = order - 1;
     validate(order);
-    const std::int64_t t0 = dims[2];
+    const int tm = cfg.temporal_mode;
+    const std::int64_t t0 = dims[tm];
     if (t0 < 1) throw ConfigError("init_stream: first batch has no temporal extent");
-    I = dims[0];
-    J = dims[1];
+    // the non-temporal modes in ascending order are slots 0 and 1 (A, B)
+    I = dims[tm == 0 ? 1 : 0];
+    J = dims[tm == 2 ? 1 : 2];
     if (cfg.enforce_bounds) {
         // replica_bound_nmode (recovery.cpp:548-557) and kruskal_check (recovery.cpp:531-541)
         if (cfg.q <= cfg.shared) throw ConfigError("replica_bound: requires Q > shared");
@@ -308,10 +402,13 @@ void Stream::prepare(int order, const std::int64_t* dims) {
     gen_replicas();
     const int P = cfg.p, Q = cfg.q, R = cfg.rank;
     // compression and summaries for the owned replicas only
-    if (pl > 0)
+    if (pl > 0) {
         comp.set_projections(pl, Q, cfg.shared, I, J, hU.data() + (size_t)p0 * I * Q, hV.data() + (size_t)p0 * J * Q,
                              st);
+        comp.set_temporal_mode(tm);
+    }
     merge.set_projections(P, Q, cfg.shared, R, I, J, hU.data(), hV.data(), st);
+    set_mode_strides();
     const size_t q3 = (size_t)Q * Q * Q;
     Y.reserve((size_t)std::max(pl, 1) * q3);
     Y.zero((size_t)std::max(pl, 1) * q3, st);
@@ -353,6 +450,8 @@ __global__ void __launch_bounds__(256) h2d_pull_kernel(int4* __restrict__ dst, c
 void Stream::prefetch(const void* data, int dtype, int order, const std::int64_t* dims) {
     if (order != 3 || dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
         throw ConfigError("octen: prefetch needs an order-3 batch with positive extents");
+    if (cfg.temporal_mode >= 0 && cfg.temporal_mode != 2)
+        throw ConfigError("octen: prefetch needs the temporal mode last");
     if (initialized && (dims[0] != I || dims[1] != J))
         throw ConfigError("ingest_batch: extent mismatch on mode 1 at batch " + std::to_string(batches_seen));
     if (pf.size() >= 2) throw ConfigError("octen: two prefetched batches are already pending");
@@ -511,13 +610,16 @@ void Stream::begin(BatchCtx& b, const void* data, int dtype, int location, int o
         // streaming.cpp:258-346
         if (order != 3)
             throw ConfigError("ingest_batch: batch order mismatch at batch " + std::to_string(batches_seen));
-        if (dims[0] != I)
-            throw ConfigError("ingest_batch: extent mismatch on mode 1 at batch " + std::to_string(batches_seen));
-        if (dims[1] != J)
-            throw ConfigError("ingest_batch: extent mismatch on mode 2 at batch " + std::to_string(batches_seen));
-        if (dims[2] < 1) throw ConfigError("ingest_batch: batch has no temporal extent");
+        check_extents(dims);
     }
-    const std::int64_t t = dims[2];
+    const int tm = cfg.temporal_mode;
+    const std::int64_t t = dims[tm];
+    if (tm != 2) {
+        // the compression contracts temporal-last blocks: reorder the batch
+        // on the device once (one pass over it)
+        data = temporal_last(data, dtype, location, dims);
+        location = 1;
+    }
     if (!first && cfg.strict) snapshot(backup);
     begin_ctx(b, first, t);
     const int Q = cfg.q;
@@ -676,6 +778,8 @@ void Stream::begin_temporal(const void* data, int dtype, int location, int order
     BatchCtx& b = cur;
     if (b.pending) throw ConfigError("octen: the previous batch has not finished (begin/merge/finish)");
     if (order != 3) throw ConfigError("ingest_batch: batch order mismatch at batch " + std::to_string(batches_seen));
+    if (cfg.temporal_mode >= 0 && cfg.temporal_mode != 2)
+        throw ConfigError("octen: temporal sharding needs the temporal mode last");
     const std::int64_t t_local = dims_local[2];
     if (t_total < 1 || k_off < 0 || t_local < 0 || k_off + t_local > t_total)
         throw ConfigError("octen: temporal shard outside the batch");
@@ -793,6 +897,16 @@ void Stream::merge_phase(BatchCtx& b, const double* models_all, double* rows_out
                                        cudaMemcpyDeviceToDevice, st));
             OCTEN_CUDA(cudaMemcpyAsync(MlamAll.p + (size_t)g0 * R, blk + 4 + (size_t)chunk * 3 * qr,
                                        sizeof(double) * gl * R, cudaMemcpyDeviceToDevice, st));
+        }
+        if (cfg.temporal_mode != 2) {
+            // the replica models come in the stream's mode order; the merge
+            // works in slot order (non-temporal 0, 1, temporal)
+            const int tm = cfg.temporal_mode;
+            MfSlot.reserve((size_t)P * 3 * qr);
+            factors_to_slots_kernel<<<grid1d((size_t)P * 3 * qr), 256, 0, st>>>(
+                MfAll.p, MfSlot.p, P, (long long)qr, tm == 0 ? 1 : 0, tm == 2 ? 1 : 2, tm);
+            OCTEN_LAUNCHED(1);
+            MfAll.swap(MfSlot);
         }
         AlignResultHost ar;
         sp.mark("hdr+gather", st);
@@ -1088,12 +1202,14 @@ __global__ void sumsq_kernel(const T* __restrict__ x, size_t n, double* out) {
 double Stream::batch_fitness(const void* data, int dtype, int location, int order, const std::int64_t* dims,
                              std::int64_t k0) {
     if (!initialized) throw ConfigError("octen: stream is not initialised");
-    if (order != 3 || dims[0] != I || dims[1] != J) throw ConfigError("fitness: extent mismatch");
-    const std::int64_t t = dims[2];
+    const int tm = cfg.temporal_mode;
+    if (order != 3 || dims[tm == 0 ? 1 : 0] != I || dims[tm == 2 ? 1 : 2] != J)
+        throw ConfigError("fitness: extent mismatch");
+    const std::int64_t t = dims[tm];
     if (t < 1 || k0 < 0 || k0 + t > K) throw ConfigError("fitness: slice range outside the model");
     const int R = cfg.rank;
     const size_t n = (size_t)I * J * t;
-    const void* dX = stage_input(data, dtype, location, n);
+    const void* dX = tm == 2 ? stage_input(data, dtype, location, n) : temporal_last(data, dtype, location, dims);
     check_finite(dX, dtype, n);  // the reference builds a DenseTensor from the batch first
     const int nb = (int)std::min<size_t>(148 * 4, (n + 255) / 256);
     DevBuf<double> part, W;
@@ -1145,6 +1261,8 @@ double Stream::batch_fitness(const void* data, int dtype, int location, int orde
 
 void Stream::get_factor(int mode, double* out) {
     const int R = cfg.rank;
+    if (mode < 0 || mode > 2) throw ConfigError("octen_stream_get_factor: mode out of range");
+    mode = factor_slot(mode);
     if (mode == 0)
         OCTEN_CUDA(cudaMemcpyAsync(out, A.p, sizeof(double) * I * R, cudaMemcpyDeviceToHost, st));
     else if (mode == 1)

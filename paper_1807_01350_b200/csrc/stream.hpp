@@ -191,7 +191,8 @@ public:
     DevBuf<double> xmodels, xrows, MfAll, MlamAll, tstackAll;
     DevBuf<double> xmodels2;     // pipelined ingest: models of the batch in flight (NCCL: all-gathered models)
     DevBuf<double> rows_all_buf, part_buf, owned_buf;  // NCCL exchange buffers
-    DevBuf<float> X32;
+    DevBuf<float> X32, XT32;     // staged batch; its temporal-last reorder (temporal mode not last)
+    DevBuf<double> XT64, MfSlot;
     DevBuf<int> flag;
     DevBuf<double> Zpart;                 // temporal sharding: partial summaries, world x chunk x Q^3
     std::int64_t tshard_drawn = 0;        // temporal state before begin_temporal (rollback)
@@ -250,6 +251,14 @@ private:
     [[noreturn]] void fail_pending(BatchCtx& b);
     void begin_ctx(BatchCtx& b, bool first, std::int64_t t);
     void next_w_slot();
+    void check_extents(const std::int64_t* dims);
+    const void* temporal_last(const void* data, int dtype, int location, const std::int64_t* dims);
+    void set_mode_strides();
+
+public:
+    int factor_slot(int mode) const;
+
+private:
     void exchange_allgather(const double* send, double* recv, size_t count);
 
     Snapshot backup;
