@@ -170,6 +170,18 @@ int octen_stream_ingest_temporal(octen_stream* s, const void* data, int dtype, i
 int octen_stream_checkpoint_save(octen_stream* s, uint8_t* buf, int64_t cap, int64_t* size);
 int octen_stream_checkpoint_load(const uint8_t* bytes, int64_t n, int device, octen_stream** out);
 
+/* read_tensor_coo (proj/include/cpstream/io.hpp; src/io.cpp:49-84): the
+ * 1-based COO text format ("order d1 .. dN" header, one "i1 .. iN value" line
+ * per entry), parsed on the host with the reference's IoError messages and
+ * the SparseTensor constructor's per-entry checks (bounds, finiteness) in
+ * IoError("'path': ...") form; duplicates are reported by the device COO
+ * compression.  Entries come back 0-based, nnz x order row-major. */
+typedef struct octen_coo_file octen_coo_file;
+int octen_read_coo(const char* path, octen_coo_file** out);
+int octen_coo_file_info(const octen_coo_file* f, int64_t* order, int64_t* dims, int64_t* nnz);
+int octen_coo_file_entries(const octen_coo_file* f, int64_t* indices, double* values);
+void octen_coo_file_destroy(octen_coo_file* f);
+
 /* On-device generate_synthetic (proj/src/commands.cpp:110-134; SynthSpec,
  * proj/include/cpstream/commands.hpp): U(0,1) factors from derive(seed,
  * {9, n}), X = reconstruct(model) + N(mu, sigma) in flat order from one

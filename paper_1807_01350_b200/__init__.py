@@ -758,6 +758,27 @@ class SparseTensor:
         return int(self.values.shape[0])
 
     @staticmethod
+    def read(path: str) -> "SparseTensor":
+        """read_tensor_coo (io.cpp:49-84) of an order-3 file (octen_read_coo):
+        1-based text entries, the reference's IoError messages; duplicates
+        are reported when the batch is compressed."""
+        h = ctypes.c_void_p()
+        _check(C.LIB.octen_read_coo(str(path).encode(), ctypes.byref(h)))
+        try:
+            order, nnz = C.c_i64(), C.c_i64()
+            dims = (C.c_i64 * 16)()
+            _check(C.LIB.octen_coo_file_info(h, ctypes.byref(order), dims, ctypes.byref(nnz)))
+            if order.value != 3:
+                raise ConfigError("octen: sparse batches are order-3 (I, J, t)")
+            idx = np.zeros((nnz.value, 3), dtype=np.int64)
+            val = np.zeros(nnz.value)
+            if nnz.value:
+                _check(C.LIB.octen_coo_file_entries(h, idx.ctypes.data_as(C.P_i64), _dptr(val)))
+            return SparseTensor(tuple(dims[:3]), idx, val)
+        finally:
+            C.LIB.octen_coo_file_destroy(h)
+
+    @staticmethod
     def from_dense(t) -> "SparseTensor":
         """tensor.cpp:104-116 (nonzeros in first-index-fastest order)."""
         a = np.asarray(t)

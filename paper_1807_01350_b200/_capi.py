@@ -70,6 +70,10 @@ SIGNATURES = {
     "octen_stream_ingest_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                  ctypes.c_int, P_i64]),
     "octen_stream_sync": (ctypes.c_int, [ctypes.c_void_p]),
+    "octen_read_coo": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "octen_coo_file_info": (ctypes.c_int, [ctypes.c_void_p, P_i64, P_i64, P_i64]),
+    "octen_coo_file_entries": (ctypes.c_int, [ctypes.c_void_p, P_i64, P_dbl]),
+    "octen_coo_file_destroy": (None, [ctypes.c_void_p]),
     "octen_nccl_get_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "octen_stream_create_nccl": (ctypes.c_int, [ctypes.POINTER(StreamConfigC), ctypes.c_int, ctypes.c_int,
                                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),

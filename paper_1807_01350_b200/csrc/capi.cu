@@ -888,3 +888,87 @@ int octen_compress_coo(int p, int q, int64_t I, int64_t J, int64_t t, const doub
 }
 
 }  // extern "C"
+
+// ---- COO text files (read_tensor_coo, proj/src/io.cpp:49-84) ----
+// Parsed on the host (file I/O), validated per entry for arity, bounds and
+// finiteness with the reference's messages prefixed by the path (io.cpp:79-83
+// wraps the SparseTensor constructor's errors in IoError).  Duplicate
+// indices are left to the device COO compression (octen_coo_compress), which
+// raises the constructor's "SparseTensor: duplicate index".
+#include <cerrno>
+#include <cstdio>
+#include <fstream>
+#include <sstream>
+
+struct octen_coo_file {
+    std::vector<int64_t> dims;
+    std::vector<int64_t> idx;  // nnz x order, 0-based
+    std::vector<double> val;
+};
+
+extern "C" {
+
+int octen_read_coo(const char* path, octen_coo_file** out) {
+    return guard([&] {
+        if (!path || !out) throw octen::ConfigError("octen_read_coo: null argument");
+        const std::string p(path);
+        std::ifstream in(p);
+        if (!in) throw octen::IoError("cannot open '" + p + "' for reading");
+        std::string line;
+        if (!std::getline(in, line)) throw octen::IoError("'" + p + "': empty file");
+        std::istringstream header(line);
+        int order = 0;
+        if (!(header >> order) || order < 2) throw octen::IoError("'" + p + "': bad header");
+        auto f = std::make_unique<octen_coo_file>();
+        f->dims.resize((size_t)order);
+        for (int n = 0; n < order; ++n)
+            if (!(header >> f->dims[(size_t)n]))
+                throw octen::IoError("'" + p + "': header lists fewer extents than the order");
+        for (int64_t d : f->dims)
+            if (d < 1) throw octen::IoError("'" + p + "': Shape: dimensions must be positive");
+        size_t line_no = 1;
+        std::vector<int64_t> e((size_t)order);
+        while (std::getline(in, line)) {
+            ++line_no;
+            if (line.empty()) continue;
+            std::istringstream row(line);
+            for (int n = 0; n < order; ++n) {
+                if (!(row >> e[(size_t)n]))
+                    throw octen::IoError("'" + p + "': malformed entry at line " + std::to_string(line_no));
+                e[(size_t)n] -= 1;  // the file is 1-based
+            }
+            double v = 0.0;
+            if (!(row >> v)) throw octen::IoError("'" + p + "': missing value at line " + std::to_string(line_no));
+            // the SparseTensor constructor's checks, in its order (tensor.cpp:87-102)
+            for (int n = 0; n < order; ++n)
+                if (e[(size_t)n] < 0 || e[(size_t)n] >= f->dims[(size_t)n])
+                    throw octen::IoError("'" + p + "': SparseTensor: index out of bounds");
+            if (!std::isfinite(v)) throw octen::IoError("'" + p + "': SparseTensor: non-finite value");
+            f->idx.insert(f->idx.end(), e.begin(), e.end());
+            f->val.push_back(v);
+        }
+        *out = f.release();
+    });
+}
+
+int octen_coo_file_info(const octen_coo_file* f, int64_t* order, int64_t* dims, int64_t* nnz) {
+    return guard([&] {
+        if (!f || !order || !nnz) throw octen::ConfigError("octen_coo_file_info: null argument");
+        *order = (int64_t)f->dims.size();
+        if (dims)
+            for (size_t n = 0; n < f->dims.size(); ++n) dims[n] = f->dims[n];
+        *nnz = (int64_t)f->val.size();
+    });
+}
+
+int octen_coo_file_entries(const octen_coo_file* f, int64_t* indices, double* values) {
+    return guard([&] {
+        if (!f || !indices || !values) throw octen::ConfigError("octen_coo_file_entries: null argument");
+        std::memcpy(indices, f->idx.data(), f->idx.size() * sizeof(int64_t));
+        std::memcpy(values, f->val.data(), f->val.size() * sizeof(double));
+    });
+}
+
+void octen_coo_file_destroy(octen_coo_file* f) { delete f; }
+
+}  // extern "C"
