@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(G1P_THREADS, 1)
                                      const __grid_constant__ CUtensorMap map_alo,
                                      const __grid_constant__ CUtensorMap map_x, float* __restrict__ Z, int M,
                                      long long N, int K, long long ldz, int scP, int scQ, int scSh, int mt,
-                                     long long ntiles) {
+                                     long long ntiles, int two_mma) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full_bar = (uint64_t*)(smem + STAGES * STAGE_BYTES);
@@ -403,7 +403,8 @@ __global__ void __launch_bounds__(G1P_THREADS, 1)
                         const uint32_t off = k * 32;
                         const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
                         mma_tf32(dt, make_desc_sw64(a_hi + off), make_desc_sw64(b_hi + off), idesc, acc0);
-                        mma_tf32(dt, make_desc_sw64(a_hi + off), make_desc_sw64(b_lo + off), idesc, 1u);
+                        if (!two_mma)
+                            mma_tf32(dt, make_desc_sw64(a_hi + off), make_desc_sw64(b_lo + off), idesc, 1u);
                         mma_tf32(dt, make_desc_sw64(a_lo + off), make_desc_sw64(b_hi + off), idesc, 1u);
                     }
                     mma_commit(&empty_bar[s]);
@@ -423,14 +424,29 @@ __global__ void __launch_bounds__(G1P_THREADS, 1)
                 uint8_t* st = smem + s * STAGE_BYTES;
                 float4* bx = (float4*)(st + 2 * A_BYTES);
                 float4* bl = (float4*)(st + 2 * A_BYTES + B_BYTES);
-                for (int i = ct; i < B_BYTES / 16; i += CONVERT_WARPS * 32) {
-                    const float4 v = bx[i];
-                    float4 l;
-                    l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                    l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                    l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                    l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                    bl[i] = l;
+                if (two_mma) {
+                    // X rounded to the nearest TF32 in place (the MMAs then
+                    // read it exactly): round half away from zero on the
+                    // magnitude bits
+                    for (int i = ct; i < B_BYTES / 16; i += CONVERT_WARPS * 32) {
+                        const float4 v = bx[i];
+                        float4 h;
+                        h.x = __uint_as_float((__float_as_uint(v.x) + 0x1000u) & 0xFFFFE000u);
+                        h.y = __uint_as_float((__float_as_uint(v.y) + 0x1000u) & 0xFFFFE000u);
+                        h.z = __uint_as_float((__float_as_uint(v.z) + 0x1000u) & 0xFFFFE000u);
+                        h.w = __uint_as_float((__float_as_uint(v.w) + 0x1000u) & 0xFFFFE000u);
+                        bx[i] = h;
+                    }
+                } else {
+                    for (int i = ct; i < B_BYTES / 16; i += CONVERT_WARPS * 32) {
+                        const float4 v = bx[i];
+                        float4 l;
+                        l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                        l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                        l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                        l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                        bl[i] = l;
+                    }
                 }
                 fence_proxy_async();
                 mbar_arrive(&conv_bar[s]);
@@ -758,8 +774,12 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
         const int mt = (M + BM - 1) / BM;
         const long long ntiles = (long long)mt * ((N + BN - 1) / BN);
         const int grid = (int)std::min<long long>(ntiles, nsm);
-        tc_gemm_tf32x3_persistent_kernel<<<grid, G1P_THREADS, smem + G1P_EPI_BYTES, st>>>(mhi, mlo, mx, Z, M, N, K, N, scatter_p,
-                                                                          scatter_q, scatter_sh, mt, ntiles);
+        // two MMAs per k-step (A_hi X_rn + A_lo X_rn, X rounded to the
+        // nearest TF32) unless OCTEN_G1_3MMA asks for the A_hi X_hi +
+        // A_hi X_lo + A_lo X_hi split
+        static const int two_mma = std::getenv("OCTEN_G1_3MMA") ? 0 : 1;
+        tc_gemm_tf32x3_persistent_kernel<<<grid, G1P_THREADS, smem + G1P_EPI_BYTES, st>>>(
+            mhi, mlo, mx, Z, M, N, K, N, scatter_p, scatter_q, scatter_sh, mt, ntiles, two_mma);
         OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
         return true;
