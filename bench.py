@@ -752,6 +752,7 @@ def main():
             pipe_pct = rj.get("tensor_pipe_active_pct")
     except Exception:
         traffic = None
+    n_mma = 3.0 if os.environ.get("OCTEN_G1_3MMA") else 2.0  # the library's GEMM1 split (tc_gemm.cu)
     ks1 = st.kernel_stats() if hasattr(st, "kernel_stats") else None
     kd = {k: ks1[k] - ks0[k] for k in ks1} if (ks1 and ks0) else None
     rooflines = {
@@ -760,8 +761,10 @@ def main():
                   "unit": "TFLOP/s", "frac": achieved / tf32_peak, "traffic": traffic,
                   "traffic_unit": "bytes/launch (ncu dram__bytes_read+write, profiles/r1_roofline.json)",
                   "peak_source": pk["source"], "flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
-                  "issued_tflops": 3.0 * achieved, "issued_frac": 3.0 * achieved / tf32_peak,
-                  "issued_note": "split-TF32: 3 tcgen05 MMAs (hi*hi, hi*lo, lo*hi) per useful product",
+                  "issued_tflops": n_mma * achieved, "issued_frac": n_mma * achieved / tf32_peak,
+                  "issued_note": ("split-TF32: 2 tcgen05 MMAs per useful product (A_hi X_rn + A_lo X_rn, X rounded "
+                                  "to the nearest TF32)" if n_mma == 2 else
+                                  "split-TF32: 3 tcgen05 MMAs (hi*hi, hi*lo, lo*hi) per useful product"),
                   "tensor_pipe_active_pct_ncu": pipe_pct}}
     if kd and kd["gemm_launches"] > 0:
         gms = kd["gemm_ms"] / kd["gemm_launches"]

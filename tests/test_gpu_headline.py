@@ -155,16 +155,21 @@ def test_c5_proxy_reference_numeric_error():
 
 
 def test_c5_full_shape_numeric_error(ob):
-    # the BASELINE c5 stream itself (2000 x 2000, K0 = 200 slices, Q = 128,
-    # P = 32, R = 32, shared = 32, 1 % noise) from the on-device generator:
-    # the device raises the reference's error in init_stream, as the oracle
-    # does on the proxy above
+    # the BASELINE c5 stream itself (2000 x 2000, K0 = 200 then batches of
+    # 200 slices, Q = 128, P = 32, R = 32, shared = 32, 1 % noise; bench.py's
+    # c5 data): the device raises the reference's merge error within the
+    # first batches, as the oracle does on the proxy above
+    import os
+    import sys
     import torch
-    g = ob.SynthStream((2000, 2000, 200), 32, 5, 0.0, 0.0)
-    x = g.next(200, "f32")
-    sigma = 0.01 * float(x.double().pow(2).mean().sqrt())
-    x += sigma * torch.randn(x.shape, generator=torch.Generator(device="cuda").manual_seed(6), device="cuda")
-    cfg = ob.StreamConfig(rank=32, p=32, q=128, shared=32, seed=38,
-                          als=ob.AlsConfig(rank=32, max_iters=30, rel_tol=1e-8, n_restarts=3))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    c = bench.CONFIGS["c5"]
+    syn = bench.Synth(torch, torch.device("cuda", 0), c["I"], c["J"], c["K0"] + 6 * c["t"], c["R"], seed=1234,
+                      noise=0.01)
+    cfg = ob.StreamConfig(rank=c["R"], p=c["P"], q=c["Q"], shared=c["shared"], seed=7 * 1234 + 3,
+                          als=ob.AlsConfig(max_iters=30, rel_tol=1e-8, n_restarts=3))
     with pytest.raises(ob.NumericError, match=r"recover: rank-deficient projection on mode"):
-        ob.init_stream(x, cfg)
+        st = ob.init_stream(syn.batch(0, c["K0"]), cfg)
+        for b in range(6):
+            ob.ingest_batch(st, syn.batch(c["K0"] + b * c["t"], c["t"]))
