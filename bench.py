@@ -68,32 +68,80 @@ def pipe_peaks():
         return {"tf32": 1100.0, "dmma": 37.0, "ffma": 72.0, "source": "nominal (peaks file missing)"}
 
 
+def ref_backend():
+    """The CPU implementation the reference arm and cpu_baseline time: the
+    reference library compiled from its own sources (oracle/_ref, built by
+    oracle/Makefile against the Eigen stand-in; kind "reference") when the
+    snapshot carries it, else the oracle port (kind "port")."""
+    try:
+        from oracle import ref_lib
+        if ref_lib.available():
+            ref_lib.lib()
+            return "reference"
+    except Exception:  # pragma: no cover
+        pass
+    return "port"
+
+
+def ref_workers(cfg):
+    """min(cores, P) like the reference's resolve_workers (streaming.cpp:
+    36-43), capped so the per-worker copies of the batch the reference's
+    compress makes (compression.cpp:116, plus its matricize / product
+    temporaries, ~3 batch sizes) fit the host's free memory."""
+    I, J, t, P = (cfg[k] for k in ("I", "J", "t", "P"))
+    w = min(os.cpu_count() or 1, P)
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+        w = max(1, min(w, int(0.8 * avail // (3 * 8 * I * J * t))))
+    except Exception:  # pragma: no cover
+        pass
+    return w
+
+
 def cpu_baseline_step(cfg, noise):
-    """cpu_baseline of the own arm: the oracle port timed on ONE full
-    ingest_batch of a workload batch (compression of t slices into P
-    replicas, CP-ALS on every replica, the whole merge) after an untimed
-    init_stream on t slices (the per-batch work does not depend on K0)."""
+    """cpu_baseline of the own arm: the reference (oracle/_ref, else the
+    oracle port) timed on ONE full ingest_batch of a workload batch
+    (compression of t slices into P replicas, CP-ALS on every replica, the
+    whole merge) after an untimed init_stream on t slices (the per-batch work
+    does not depend on K0 beyond the temporal factor's row count)."""
     from threadpoolctl import threadpool_limits
     from oracle import octen_oracle as O
     I, J, t, Q, P, R, sh = (cfg[k] for k in ("I", "J", "t", "Q", "P", "R", "shared"))
-    O.MERGE_PROCESSES = True
+    kind = ref_backend()
+    workers = ref_workers(cfg) if kind == "reference" else 0
+    scfg = O.StreamConfig(rank=R, p=P, q=Q, shared=sh, seed=7 * 1234 + 3,
+                          als=O.AlsConfig(R, cfg["iters"], 1e-8, cfg["restarts"], 0), workers=workers)
+    syn = HostSynth(I, J, 2 * t, R, 1234, noise)
     with threadpool_limits(limits=1):
-        syn = HostSynth(I, J, 2 * t, R, 1234, noise)
-        scfg = O.StreamConfig(rank=R, p=P, q=Q, shared=sh, seed=7 * 1234 + 3,
-                              als=O.AlsConfig(R, cfg["iters"], 1e-8, cfg["restarts"], 0), workers=0)
-        st = O.init_stream(syn.batch(0, t), scfg)
-        b = syn.batch(t, t)
-        a = time.perf_counter()
-        O.ingest_batch(st, b)
-        sec = time.perf_counter() - a
-        rec = st.log[-1]
-        workers = O.resolve_workers(scfg)
-    return {"value": I * J * t / sec, "unit": "entries/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": "one full ingest_batch of a %dx%dx%d batch (oracle port: compress + CP-ALS over %d replica "
-                      "threads, merge column solves over %d processes, single-threaded BLAS) after an untimed "
-                      "init_stream on %d slices" % (I, J, t, workers, os.cpu_count(), t),
-            "stages_s": {"compress_s": rec.compress_seconds, "als_s": rec.als_seconds,
-                         "recover_s": rec.recover_seconds, "total_s": sec}}
+        if kind == "reference":
+            from oracle import ref_lib
+            st = ref_lib.RefStream(syn.batch(0, t), scfg)
+            b = syn.batch(t, t)
+            a = time.perf_counter()
+            st.ingest(b)
+            sec = time.perf_counter() - a
+            tm = st.timers()[-1]
+            stages = {"compress_s": float(tm[0]), "als_s": float(tm[1]), "recover_s": float(tm[2]), "total_s": sec}
+            what = ("the reference library compiled from its own sources (oracle/_ref: proj/src/*.cpp + the "
+                    "Eigen stand-in on single-threaded OpenBLAS), %d replica workers" % workers)
+        else:
+            O.MERGE_PROCESSES = True
+            st = O.init_stream(syn.batch(0, t), scfg)
+            b = syn.batch(t, t)
+            a = time.perf_counter()
+            O.ingest_batch(st, b)
+            sec = time.perf_counter() - a
+            rec = st.log[-1]
+            stages = {"compress_s": rec.compress_seconds, "als_s": rec.als_seconds,
+                      "recover_s": rec.recover_seconds, "total_s": sec}
+            workers = O.resolve_workers(scfg)
+            what = ("the oracle port (compress + CP-ALS over %d replica threads, merge column solves over %d "
+                    "processes, single-threaded BLAS)" % (workers, os.cpu_count()))
+    return {"value": I * J * t / sec, "unit": "entries/s", "cores": workers, "kind": kind,
+            "sample": "one full ingest_batch of a %dx%dx%d batch through %s, after an untimed init_stream on %d "
+                      "slices" % (I, J, t, what, t),
+            "stages_s": stages}
 
 
 class ClockSampler:
@@ -279,65 +327,81 @@ class HostSynth:
 
 
 def run_reference(args, cfg, rank, world):
-    """The reference arm: the oracle port of the reference (oracle/, a numpy /
-    LAPACK restatement of proj/src; the reference itself cannot be built
-    here) run as the reference runs: full ingest_batch steps
-    (streaming.cpp:258-346) on the same workload, the compression and CP-ALS
-    fanned out over min(cores, P) worker threads (parallel_replicas,
-    streaming.cpp:36-69), single-threaded BLAS as the reference's Eigen; the
-    port also spreads the merge's independent per-column QR solves over the
-    cores (the reference runs them in a loop), so it is a faster CPU
-    baseline than the reference itself.  init_stream on the K0 block is
-    untimed.
-    Rank 0 only; the step time is the mean of the timed ingest_batch calls,
-    with the reference's own BatchRecord stage timers beside it."""
+    """The reference arm: the reference library compiled from its own sources
+    (oracle/_ref: proj/src/*.cpp unmodified, Eigen replaced by the stand-in in
+    oracle/ref_shim on single-threaded OpenBLAS; tests/test_ref_pin.py runs the
+    reference's own unit tests on it) through its public API, full
+    ingest_batch steps (streaming.cpp:262-348) on the same workload, its own
+    std::thread fan-out over min(cores, P) replica workers
+    (parallel_replicas, streaming.cpp:45-69).  Falls back to the oracle port
+    (oracle/octen_oracle.py) when the snapshot has no oracle/_ref.  The
+    untimed init_stream runs on t slices (the reference copies the batch per
+    worker, compression.cpp:116; K0 = 1000 slices would need ~8 GB per
+    worker); the timed per-batch work does not depend on K0 beyond the
+    temporal factor's row count.  Rank 0 only; the step time is the mean of
+    the timed ingest_batch calls, the reference's BatchRecord stage timers
+    beside it."""
     if rank != 0:
         return
     from oracle import octen_oracle as O
-    # BLAS single-threaded throughout, as the reference's Eigen: the port's
-    # parallelism is its explicit fan-out over replicas / independent
-    # column solves (threaded LAPACK measured slower on the pivoted QRs:
-    # 1.2 s vs 0.37 s for 1600 x 1000 on 8 cores)
     from threadpoolctl import threadpool_limits
     threadpool_limits(limits=1)
-    O.MERGE_PROCESSES = True  # the column QRs in forked workers (scipy's LAPACK holds the GIL)
+    kind = ref_backend()
     cores = os.cpu_count()
     I, J, K0, t, Q, P, R, sh = (cfg[k] for k in ("I", "J", "K0", "t", "Q", "P", "R", "shared"))
     nb = args.warmup + args.steps
     dseed = 1234
-    syn = HostSynth(I, J, K0 + nb * t, R, dseed, args.noise)
+    workers = ref_workers(cfg) if kind == "reference" else 0
     scfg = O.StreamConfig(rank=R, p=P, q=Q, shared=sh, seed=7 * dseed + 3,
-                          als=O.AlsConfig(R, cfg["iters"], 1e-8, cfg["restarts"], 0), workers=0)
+                          als=O.AlsConfig(R, cfg["iters"], 1e-8, cfg["restarts"], 0), workers=workers)
+    k_init = t if kind == "reference" else K0
+    syn = HostSynth(I, J, k_init + nb * t, R, dseed, args.noise)
+    times, stage_rows = [], []
     t0 = time.perf_counter()
-    st = O.init_stream(syn.batch(0, K0), scfg)
-    t_init = time.perf_counter() - t0
-    times, recs = [], []
-    for i in range(nb):
-        b = syn.batch(K0 + i * t, t)
-        a = time.perf_counter()
-        O.ingest_batch(st, b)
-        e = time.perf_counter() - a
-        if i >= args.warmup:
-            times.append(e)
-            recs.append(st.log[-1])
+    if kind == "reference":
+        from oracle import ref_lib
+        st = ref_lib.RefStream(syn.batch(0, k_init), scfg)
+        t_init = time.perf_counter() - t0
+        for i in range(nb):
+            b = syn.batch(k_init + i * t, t)
+            a = time.perf_counter()
+            st.ingest(b)
+            e = time.perf_counter() - a
+            if i >= args.warmup:
+                times.append(e)
+                stage_rows.append(st.timers()[-1][:3])
+        impl = ("the reference library compiled from its own sources (oracle/_ref: proj/src/*.cpp with the Eigen "
+                "stand-in on single-threaded OpenBLAS)")
+    else:
+        O.MERGE_PROCESSES = True
+        st = O.init_stream(syn.batch(0, k_init), scfg)
+        t_init = time.perf_counter() - t0
+        for i in range(nb):
+            b = syn.batch(k_init + i * t, t)
+            a = time.perf_counter()
+            O.ingest_batch(st, b)
+            e = time.perf_counter() - a
+            if i >= args.warmup:
+                times.append(e)
+                r = st.log[-1]
+                stage_rows.append([r.compress_seconds, r.als_seconds, r.recover_seconds])
+        workers = O.resolve_workers(scfg)
+        impl = "the oracle port (numpy/LAPACK restatement of the reference; oracle/_ref was not built)"
     sec = float(np.mean(times))
     v = I * J * t / sec
-    workers = O.resolve_workers(scfg)
-    stages = {"compress_s": float(np.mean([r.compress_seconds for r in recs])),
-              "als_s": float(np.mean([r.als_seconds for r in recs])),
-              "recover_s": float(np.mean([r.recover_seconds for r in recs])), "init_s": t_init}
-    sample = ("full ingest_batch steps of the oracle port (numpy/LAPACK restatement of the reference) on the "
-              "%s workload: %d timed + %d warm-up batches of %dx%dx%d after an untimed init_stream on %d slices; "
-              "compress + CP-ALS over %d replica threads, independent merge column solves over %d processes, "
-              "single-threaded BLAS" %
-              (args.config, args.steps, args.warmup, I, J, t, K0, workers, cores))
+    sr = np.asarray(stage_rows, dtype=float)
+    stages = {"compress_s": float(sr[:, 0].mean()), "als_s": float(sr[:, 1].mean()),
+              "recover_s": float(sr[:, 2].mean()), "init_s": t_init}
+    sample = ("full ingest_batch steps of %s on the %s workload: %d timed + %d warm-up batches of %dx%dx%d after "
+              "an untimed init_stream on %d slices; %d replica workers" %
+              (impl, args.config, args.steps, args.warmup, I, J, t, k_init, workers))
     line = {"metric": "tensor entries streamed/sec per batch update", "value": v, "unit": "entries/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": bench_config(args, cfg, int(os.environ.get("WORLD_SIZE", "1"))),
             "stages_s": stages, "step_s": [round(x, 3) for x in times],
-            "cpu_baseline": {"value": v, "unit": "entries/s", "cores": cores, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "entries/s", "cores": workers, "kind": kind, "sample": sample},
             "e2e": {"value": v, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
