@@ -2,9 +2,9 @@
 
     python tests/golden/make_golden.py
 
-The reference (C++/Eigen) cannot be built in this container,
-so the fixtures are oracle outputs on small seeded inputs; the oracle itself
-is pinned to the reference's known-answer tests (tests/test_oracle_kat.py).
+The fixtures are oracle outputs on small seeded inputs; the reference
+compiled from its own sources (oracle/_ref) reproduces every
+one of them (tests/test_ref_pin.py::test_golden_fixtures_reproduced_by_reference).
 Every input is regenerated from its seed by the bit-exact host RNG
 (oracle/rng.py = proj/include/cpstream/rng.hpp), so the fixtures store only
 seeds, shapes and outputs.  Test infrastructure only.
