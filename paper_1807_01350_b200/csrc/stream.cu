@@ -6,7 +6,9 @@
 // compression.cpp:22-99) and the stage sequencing.  Summaries Y_p, history
 // accumulators M_p, the model factors and every contraction/solve live on the
 // device.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <cstdlib>
 #include <cstring>
@@ -1103,6 +1105,43 @@ void Stream::sync() {
     if (e) std::rethrow_exception(e);
 }
 
+namespace {
+// OCTEN_MERGE_SMS=k (experiment): the pipelined merge runs on a green-context
+// stream confined to k SMs, so its latency-bound factorizations cannot
+// occupy the SMs the next batch's compression and CP-ALS need.  Driver
+// entry points resolved at run time (libcuda is already loaded by the
+// runtime).  Returns null when unavailable.
+cudaStream_t green_merge_stream(int device, int sms, int priority) {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcuda.so.1", RTLD_NOW);
+    if (!h) return nullptr;
+    auto devget = reinterpret_cast<CUresult (*)(CUdevice*, int)>(dlsym(h, "cuDeviceGet"));
+    auto getres = reinterpret_cast<CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType)>(
+        dlsym(h, "cuDeviceGetDevResource"));
+    auto split = reinterpret_cast<CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*,
+                                               unsigned, unsigned)>(dlsym(h, "cuDevSmResourceSplitByCount"));
+    auto gen = reinterpret_cast<CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned)>(
+        dlsym(h, "cuDevResourceGenerateDesc"));
+    auto create = reinterpret_cast<CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned)>(
+        dlsym(h, "cuGreenCtxCreate"));
+    auto screate = reinterpret_cast<CUresult (*)(CUstream*, CUgreenCtx, unsigned, int)>(
+        dlsym(h, "cuGreenCtxStreamCreate"));
+    if (!devget || !getres || !split || !gen || !create || !screate) return nullptr;
+    CUdevice dev;
+    CUdevResource all, part, rest;
+    unsigned groups = 1;
+    CUdevResourceDesc desc;
+    CUgreenCtx g;
+    CUstream s;
+    if (devget(&dev, device) != CUDA_SUCCESS || getres(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+        split(&part, &groups, &all, &rest, 0, (unsigned)sms) != CUDA_SUCCESS || groups < 1 ||
+        gen(&desc, &part, 1) != CUDA_SUCCESS || create(&g, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+        screate(&s, g, CU_STREAM_NON_BLOCKING, priority) != CUDA_SUCCESS)
+        return nullptr;
+    return reinterpret_cast<cudaStream_t>(s);
+}
+}  // namespace
+
 void Stream::ingest_async(const void* data, int dtype, int location, int order, const std::int64_t* dims) {
     if (shard_world != 1) throw ConfigError("octen: a sharded stream ingests through begin/merge/finish");
     if (!initialized || cfg.strict) {
@@ -1114,7 +1153,12 @@ void Stream::ingest_async(const void* data, int dtype, int location, int order, 
         OCTEN_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         // the merge has slack (it is shorter than compression + CP-ALS): the
         // main stream's kernels go first when both are ready
-        OCTEN_CUDA(cudaStreamCreateWithPriority(&mst, cudaStreamNonBlocking, least));
+        static const int merge_sms = [] {
+            const char* e = std::getenv("OCTEN_MERGE_SMS");
+            return e ? std::atoi(e) : 0;
+        }();
+        if (merge_sms > 0) mst = green_merge_stream(cfg.device, merge_sms, least);
+        if (!mst) OCTEN_CUDA(cudaStreamCreateWithPriority(&mst, cudaStreamNonBlocking, least));
     }
     BatchCtx& b = actx[aslot];
     b.st = mst;
