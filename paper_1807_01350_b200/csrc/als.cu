@@ -1496,7 +1496,8 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     const bool gsplit = gsplit_env >= 1 && L > 1;
     const bool gper = gsplit_env == 2;
     if (!lane_st[1]) {
-        for (int l = 0; l < kMaxLanes; ++l) OCTEN_CUDA(cudaStreamCreateWithFlags(&lane_st[l], cudaStreamNonBlocking));
+        for (int l = 0; l < kMaxLanes; ++l)
+            OCTEN_CUDA(cudaStreamCreateWithPriority(&lane_st[l], cudaStreamNonBlocking, critical_stream_priority()));
     }
     if (gsplit && !gemm_st) {
         int least = 0, greatest = 0;

@@ -350,13 +350,14 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
     // factorization and panel of step k+1 (the scheduler hands freed SMs to
     // the high-priority CTAs first).  Part 1 of step k+1 waits for part 2 of
     // step k: both update block column k+2.
-    static thread_local cudaStream_t crit = nullptr;
+    // The chain's stream priority: chain_priority_over (octen_common.cuh).
+    static thread_local cudaStream_t crit_by_level[8] = {};
     static thread_local std::vector<cudaEvent_t> ev_panel, ev_rest;
     static thread_local cudaEvent_t ev_start = nullptr, ev_end = nullptr;
-    if (!crit) {
-        int lo = 0, hi = 0;
-        OCTEN_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        OCTEN_CUDA(cudaStreamCreateWithPriority(&crit, cudaStreamNonBlocking, hi));
+    const int cprio = chain_priority_over(st);
+    cudaStream_t& crit = crit_by_level[(cprio < 0 ? -cprio : cprio) & 7];
+    if (!crit) OCTEN_CUDA(cudaStreamCreateWithPriority(&crit, cudaStreamNonBlocking, cprio));
+    if (!ev_start) {
         OCTEN_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
         OCTEN_CUDA(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming));
     }

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <cstring>
 #include <map>
 #include <utility>
 #include <vector>
@@ -19,6 +20,34 @@
 #include "errors.hpp"
 
 namespace octen {
+
+// Device -> host reads of small results (status words, ranks, flags) through
+// a per-thread pinned staging buffer.  A pageable cudaMemcpyAsync D2H waits
+// for its stream inside the driver while holding a lock that other host
+// threads' CUDA calls need: the pipelined merge's worker reading a flag
+// behind a long factorization stalled the next batch's enqueue on the main
+// thread for ~1.5 ms per batch.  With a pinned destination the copy is truly
+// asynchronous and only the calling thread waits (cudaStreamSynchronize).
+inline void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    struct Stage {
+        void* p = nullptr;
+        size_t cap = 0;
+    };
+    static thread_local Stage* s = new Stage;  // never destroyed: may be in flight at thread exit
+    if (bytes == 0) {
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    if (bytes > s->cap) {
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+        if (s->p) OCTEN_CUDA(cudaFreeHost(s->p));
+        s->cap = bytes < (1u << 20) ? (1u << 20) : 2 * bytes;
+        OCTEN_CUDA(cudaHostAlloc(&s->p, s->cap, cudaHostAllocDefault));
+    }
+    OCTEN_CUDA(cudaMemcpyAsync(s->p, src, bytes, cudaMemcpyDeviceToHost, st));
+    OCTEN_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(dst, s->p, bytes);
+}
 
 struct BlockCache {
     std::multimap<size_t, void*> free_blocks[16];  // per device ordinal (bytes -> block)
@@ -141,8 +170,7 @@ struct DevBuf {
     }
     std::vector<T> to_host(size_t count, cudaStream_t st) const {
         std::vector<T> h(count);
-        download(h.data(), count, st);
-        OCTEN_CUDA(cudaStreamSynchronize(st));
+        d2h_sync(h.data(), p, count * sizeof(T), st);
         return h;
     }
 };

@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #if defined(__CUDACC__)
 #define OCTEN_HD __host__ __device__
@@ -43,6 +44,36 @@ inline std::atomic<long long>& path_counter(int i) {
 }
 
 #if defined(__CUDACC__)
+// Stream priorities (B200: least 0 .. greatest -5).  Measured at c3 with the
+// pipelined ingest (ms per step): the batch streams at the default (least)
+// priority with every merge factorization chain at the greatest, 13.1; the
+// batch streams one level below the greatest with the merge chain just above
+// the merge's least-priority bulk updates, 13.9 (CP-ALS 9.5 ms, but the
+// merge, now starved, 13.3 ms becomes the longer stage).  The first is the
+// default; OCTEN_PRIO_MODE=1 selects the second (diagnostics).
+inline int prio_mode() {
+    static const int m = [] {
+        const char* e = std::getenv("OCTEN_PRIO_MODE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return m;
+}
+// priority of the streams that carry a batch's compression and CP-ALS
+inline int critical_stream_priority() {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (prio_mode() == 1) return hi < lo ? hi + 1 : hi;
+    return lo;
+}
+// priority of a factorization chain whose bulk updates run on `st`
+inline int chain_priority_over(cudaStream_t st) {
+    int lo = 0, hi = 0, p = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (prio_mode() != 1) return hi;
+    if (cudaStreamGetPriority(st, &p) != cudaSuccess) p = lo;
+    return p > hi ? p - 1 : hi;
+}
+
 // Kernel attributes (cudaFuncSetAttribute) are per device: a process that
 // drives handles on several GPUs must set them once per device ordinal, not
 // once per process.  `PerDevice` remembers the devices already done.

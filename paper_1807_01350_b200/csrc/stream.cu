@@ -133,7 +133,7 @@ Stream::Stream(const StreamCfg& c, int rank, int world) : cfg(c), shard_rank(ran
     p0 = std::min(P, rank * chunk);
     pl = std::max(0, std::min(P, p0 + chunk) - p0);
     OCTEN_CUDA(cudaSetDevice(cfg.device));
-    OCTEN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    OCTEN_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, critical_stream_priority()));
     OCTEN_CUDA(cudaEventCreate(&ev0));
     OCTEN_CUDA(cudaEventCreate(&ev1));
     for (auto& e : evs) OCTEN_CUDA(cudaEventCreate(&e));
@@ -672,7 +672,7 @@ void Stream::begin(BatchCtx& b, const void* data, int dtype, int location, int o
                     dst = X32.reserve(n);
                 else
                     dst = X64.reserve(n);
-                if (!cp) OCTEN_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+                if (!cp) OCTEN_CUDA(cudaStreamCreateWithPriority(&cp, cudaStreamNonBlocking, critical_stream_priority()));
                 while ((std::int64_t)copy_ev.size() < nch) {
                     cudaEvent_t e;
                     OCTEN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -847,8 +847,7 @@ void Stream::begin_reduced(const double* owned_block, double* models_out) {
     const size_t q3 = (size_t)Q * Q * Q, blk = (size_t)chunk * q3 + 1;
     try {
         double status = 0.0;
-        OCTEN_CUDA(cudaMemcpyAsync(&status, owned_block + blk - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
-        OCTEN_CUDA(cudaStreamSynchronize(st));
+        d2h_sync(&status, owned_block + blk - 1, sizeof(double), st);
         if (status != 0.0) {
             batches_drawn = tshard_drawn;
             tgram = tshard_tgram;
@@ -883,9 +882,7 @@ void Stream::merge_phase(BatchCtx& b, const double* models_all, double* rows_out
         // CP-ALS failures of any rank (lowest replica first)
         std::vector<double> hdr((size_t)shard_world * 4);
         for (int g = 0; g < shard_world; ++g)
-            OCTEN_CUDA(cudaMemcpyAsync(hdr.data() + 4 * g, models_all + (size_t)g * mc, 4 * sizeof(double),
-                                       cudaMemcpyDeviceToHost, st));
-        OCTEN_CUDA(cudaStreamSynchronize(st));
+            d2h_sync(hdr.data() + 4 * g, models_all + (size_t)g * mc, 4 * sizeof(double), st);
         for (int g = 0; g < shard_world; ++g)
             if (hdr[4 * g] != 0.0)
                 throw NumericError(als_failure_message((int)hdr[4 * g], (int)hdr[4 * g + 1], (int)hdr[4 * g + 2]));
