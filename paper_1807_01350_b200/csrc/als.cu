@@ -1138,6 +1138,36 @@ struct HStore {  // H[prob][r][k]: row r of h contiguous (the peel reads H_r = h
 
 }  // namespace
 
+AlsHostDraws als_host_draws(const std::vector<std::uint64_t>& seeds, int S, int Q) {
+    const int P = (int)seeds.size(), NP = P * S;
+    AlsHostDraws d;
+    d.S = S;
+    d.Q = Q;
+    d.seeds = seeds;
+    d.restart_seed.resize(NP);
+    d.hres.resize(NP);
+    d.hw.resize((size_t)NP * 6 * Q);
+    for (int p = 0; p < P; ++p)
+        for (int s = 0; s < S; ++s) {
+            const int prob = p * S + s;
+            d.restart_seed[prob] = rng::derive(seeds[p], {rng::kAlsRestart, (std::uint64_t)s});
+            d.hres[prob] = rng::derive(d.restart_seed[prob], {rng::kAlsRescue});
+            for (int a = 0; a < 3; ++a) {
+                rng::Substream ws(rng::derive(d.restart_seed[prob], {rng::kAlsGevd, (std::uint64_t)a}));
+                double* w1 = d.hw.data() + ((size_t)prob * 6 + a * 2 + 0) * Q;
+                double* w2 = d.hw.data() + ((size_t)prob * 6 + a * 2 + 1) * Q;
+                for (int i = 0; i < Q; ++i) w1[i] = ws.uniform01() * 2 - 1;
+                for (int i = 0; i < Q; ++i) w2[i] = ws.uniform01() * 2 - 1;
+            }
+        }
+    return d;
+}
+
+void AlsEngine::prefetch_host_draws(const std::vector<std::uint64_t>& seeds, int S, int Q) {
+    if (next_draws.valid()) next_draws.wait();
+    next_draws = std::async(std::launch::async, als_host_draws, seeds, S, Q);
+}
+
 void AlsEngine::alloc(int P, int S, int Q, int R, int max_iters) {
     const size_t NP = (size_t)P * S, q2 = (size_t)Q * Q;
     P_ = P;
@@ -1276,36 +1306,27 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     d.peel_fail = peel_fail.p;
     host_syncs = 0;
 
-    // ---- norms, zero-tensor check (cp_als.cpp:255-256)
+    // ---- norms; the zero-tensor check (cp_als.cpp:255-256) reads them with
+    // the results at the end (no host round trip here: a zero summary only
+    // produces garbage in buffers this run owns, and its error takes
+    // precedence over any later one)
     OCTEN_PROF("begin", st);
     ws.reserve((size_t)P * 64);
     als_norm_kernel<<<dim3(64, P), 256, 0, st>>>(d, ws.p); OCTEN_LAUNCHED(1);
     als_norm_finish_kernel<<<(P + 127) / 128, 128, 0, st>>>(d, ws.p, 64); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
-    std::vector<double> hn = normx2.to_host(P, st);
-    ++host_syncs;
-    for (int p = 0; p < P; ++p)
-        if (hn[p] == 0.0) {
-            failure = {1, 0, 0};
-            throw NumericError(als_failure_message(1, 0, 0));
-        }
 
-    // ---- host RNG: restart seeds, GEVD mixtures, rescue seeds
-    std::vector<std::uint64_t> restart_seed(NP), hres(NP);
-    std::vector<double> hw((size_t)NP * 6 * Q);
-    for (int p = 0; p < P; ++p)
-        for (int s = 0; s < S; ++s) {
-            const int prob = p * S + s;
-            restart_seed[prob] = rng::derive(seeds[p], {rng::kAlsRestart, (std::uint64_t)s});
-            hres[prob] = rng::derive(restart_seed[prob], {rng::kAlsRescue});
-            for (int a = 0; a < 3; ++a) {
-                rng::Substream ws(rng::derive(restart_seed[prob], {rng::kAlsGevd, (std::uint64_t)a}));
-                double* w1 = hw.data() + ((size_t)prob * 6 + a * 2 + 0) * Q;
-                double* w2 = hw.data() + ((size_t)prob * 6 + a * 2 + 1) * Q;
-                for (int i = 0; i < Q; ++i) w1[i] = ws.uniform01() * 2 - 1;
-                for (int i = 0; i < Q; ++i) w2[i] = ws.uniform01() * 2 - 1;
-            }
-        }
+    // ---- host RNG: restart seeds, GEVD mixtures, rescue seeds (drawn ahead
+    // by prefetch_host_draws when the caller knew the seeds)
+    AlsHostDraws draws;
+    if (next_draws.valid()) {
+        AlsHostDraws nd = next_draws.get();
+        if (nd.seeds == seeds && nd.S == S && nd.Q == Q) draws = std::move(nd);
+    }
+    if (draws.seeds.empty()) draws = als_host_draws(seeds, S, Q);
+    const std::vector<std::uint64_t>& restart_seed = draws.restart_seed;
+    const std::vector<std::uint64_t>& hres = draws.hres;
+    const std::vector<double>& hw = draws.hw;
     Wmix.reserve(hw.size());
     h2d_param(Wmix.p, hw.data(), hw.size() * sizeof(double), st);
     rescue_seed.reserve(NP);
@@ -1772,7 +1793,17 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         std::fprintf(stderr, "octen als: %d problems, %d sweeps, %d GEVD eigen fallbacks\n", NP, sweep, ed[0]);
     }
 
-    // ---- errors (lowest replica, then restart, wins)
+    // ---- errors: a zero input first (cp_als.cpp:255-256), then the lowest
+    // replica, then restart
+    {
+        std::vector<double> hn = normx2.to_host(P, st);
+        ++host_syncs;
+        for (int p = 0; p < P; ++p)
+            if (hn[p] == 0.0) {
+                failure = {1, 0, 0};
+                throw NumericError(als_failure_message(1, 0, 0));
+            }
+    }
     std::vector<DevStatus> he = err.to_host(NP, st);
     std::vector<AlsState> hs = state.to_host(NP, st);
     for (int prob = 0; prob < NP; ++prob) {

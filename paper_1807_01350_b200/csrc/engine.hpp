@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <string>
+#include <future>
 #include <vector>
 
 #include "devbuf.hpp"
@@ -47,11 +48,24 @@ struct AlsFailure {
     int kind = 0, a = 0, b = 0;
 };
 
+// The host-RNG draws of one CP-ALS batch (restart seeds, GEVD slice
+// mixtures, rescue seeds; cp_als.cpp:265-283, 110-121), a pure function of
+// the per-replica seeds: prefetch_host_draws() computes the next batch's on a
+// helper thread so they are off its critical path.
+struct AlsHostDraws {
+    int S = 0, Q = 0;
+    std::vector<std::uint64_t> seeds, restart_seed, hres;
+    std::vector<double> hw;
+};
+AlsHostDraws als_host_draws(const std::vector<std::uint64_t>& seeds, int S, int Q);
+
 class AlsEngine {
 public:
     // Y: P x Q^3 device summaries.  seeds: per replica AlsConfig.seed.
     void run(int P, int S, int Q, int R, int max_iters, double rel_tol, const double* dY,
              const std::vector<std::uint64_t>& seeds, cudaStream_t st);
+    // Draw the host RNG of a later run() with these seeds now (helper thread).
+    void prefetch_host_draws(const std::vector<std::uint64_t>& seeds, int S, int Q);
 
     // Results: factors P x 3 x Q x R, lambda P x R (device).
     DevBuf<double> Mf, Mlam;
@@ -97,6 +111,7 @@ private:
     DevBuf<DevStatus> err;
     DevBuf<Mt64> rngs;
     DevBuf<std::uint64_t> rescue_seed;
+    std::future<AlsHostDraws> next_draws;
 };
 
 // ---------------------------------------------------------------------------

@@ -207,35 +207,58 @@ void Stream::gen_replicas() {
     batches_drawn = 0;
 }
 
-void Stream::extend_temporal(std::int64_t t_new) {
-    // compression.cpp:72-99
-    const int P = cfg.p, Q = cfg.q, sh = cfg.shared;
-    const std::uint64_t key = (std::uint64_t)batches_drawn;
+TemporalDraw draw_temporal(std::uint64_t seed, int P, int Q, int sh, std::uint64_t key, std::int64_t t_new) {
+    // compression.cpp:72-99: the shared leading columns once per batch, each
+    // replica's private columns from its own substream; the batch's
+    // contribution to the shared temporal Gram
+    TemporalDraw d;
+    d.key = key;
+    d.t = t_new;
     std::vector<double> shared_rows((size_t)t_new * sh);
     {
-        rng::Substream s(rng::derive(cfg.seed, {rng::kTemporalShared, key}));
+        rng::Substream s(rng::derive(seed, {rng::kTemporalShared, key}));
         s.fill_uniform(shared_rows.data(), t_new, sh, t_new);
     }
+    d.gram.assign((size_t)sh * sh, 0.0);
     for (int i = 0; i < sh; ++i)
         for (int j = 0; j < sh; ++j) {
             double acc = 0.0;
             for (std::int64_t k = 0; k < t_new; ++k)
                 acc += shared_rows[k + (size_t)t_new * i] * shared_rows[k + (size_t)t_new * j];
-            tgram[i + (size_t)sh * j] += acc;
+            d.gram[i + (size_t)sh * j] = acc;
         }
-    hW.assign((size_t)P * t_new * Q, 0.0);
+    d.w.assign((size_t)P * t_new * Q, 0.0);
     for (int r = 0; r < P; ++r) {
-        double* w = hW.data() + (size_t)r * t_new * Q;
+        double* w = d.w.data() + (size_t)r * t_new * Q;
         for (size_t i = 0; i < shared_rows.size(); ++i) w[i] = shared_rows[i];
         if (Q > sh) {
-            rng::Substream s2(rng::derive(cfg.seed, {rng::kTemporalPrivate, key, (std::uint64_t)r}));
+            rng::Substream s2(rng::derive(seed, {rng::kTemporalPrivate, key, (std::uint64_t)r}));
             s2.fill_uniform(w + (size_t)t_new * sh, t_new, Q - sh, t_new);
         }
     }
+    return d;
+}
+
+void Stream::extend_temporal(std::int64_t t_new) {
+    // compression.cpp:72-99.  The draws are a pure function of (seed, batch
+    // key, t_new): the next batch's rows are drawn ahead on a helper thread
+    // (assuming the same t_new) so the ~0.5 ms of host RNG at c3 is off the
+    // batch's critical path; a mismatched guess is discarded.
+    const int P = cfg.p, Q = cfg.q, sh = cfg.shared;
+    const std::uint64_t key = (std::uint64_t)batches_drawn;
+    TemporalDraw d;
+    if (next_draw.valid()) {
+        TemporalDraw nd = next_draw.get();
+        if (nd.key == key && nd.t == t_new) d = std::move(nd);
+    }
+    if (d.w.empty()) d = draw_temporal(cfg.seed, P, Q, sh, key, t_new);
+    for (size_t e = 0; e < d.gram.size(); ++e) tgram[e] += d.gram[e];
+    hW = std::move(d.w);
     next_w_slot();
     upload_mapped(dWb[wslot], hW.data(), hW.size());
     dW = dWb[wslot].p;
     ++batches_drawn;
+    next_draw = std::async(std::launch::async, draw_temporal, cfg.seed, P, Q, sh, key + 1, t_new);
 }
 
 namespace {
@@ -692,17 +715,27 @@ void Stream::begin(BatchCtx& b, const void* data, int dtype, int location, int o
             } else {
                 comp.project(data, dtype, t, st, nullptr, 0, flag.p);
             }
-            if (flag.to_host(1, st)[0]) throw NumericError("DenseTensor: non-finite value");
+            // in place, Y must not be touched by a batch with non-finite
+            // values; out of place (Ynext) the mode-3 accumulation is enqueued
+            // first and the scan is read once, after it
+            if (!out_of_place && flag.to_host(1, st)[0]) throw NumericError("DenseTensor: non-finite value");
         } else {
             const void* dX = stage_input(data, dtype, location, n);
             check_finite(dX, dtype, n);
         }
+        const std::int64_t drawn_before = batches_drawn;
+        const std::vector<double> tgram_before = tgram;
         b.tgram.clear();
         extend_temporal(t);
         b.tgram = tgram;
         b.dW = dW;
         if (out_of_place) Ynext.reserve((size_t)std::max(pl, 1) * Q * Q * Q);
         if (pl > 0) comp.accumulate(dtype, t, dW + (size_t)p0 * t * Q, Y.p, Yout.p, st);
+        if (pl > 0 && out_of_place && flag.to_host(1, st)[0]) {
+            batches_drawn = drawn_before;  // the draw of this batch never happened
+            tgram = tgram_before;
+            throw NumericError("DenseTensor: non-finite value");
+        }
         b.compressed = true;
         ++batches_seen;
         OCTEN_CUDA(cudaEventRecord(evs[1], st));
@@ -728,6 +761,11 @@ void Stream::als_phase(BatchCtx& b, const double* dY, double* models_out) {
             seeds[r] = rng::derive(cfg.seed, {rng::kStreamAls, (std::uint64_t)(p0 + r), (std::uint64_t)b.rec.batch_index});
         try {
             als.run(pl, cfg.als_n_restarts, Q, R, cfg.als_max_iters, cfg.als_rel_tol, dY, seeds, st);
+            // the next batch's host draws, off its critical path
+            for (int r = 0; r < pl; ++r)
+                seeds[r] = rng::derive(cfg.seed,
+                                       {rng::kStreamAls, (std::uint64_t)(p0 + r), (std::uint64_t)b.rec.batch_index + 1});
+            als.prefetch_host_draws(seeds, cfg.als_n_restarts, Q);
         } catch (const NumericError&) {
             // a replica's CP-ALS failed: every rank raises it after the exchange
             if (als.failure.kind == 0) throw;

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <exception>
 #include <functional>
+#include <future>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -77,6 +78,15 @@ private:
     std::exception_ptr err;
     bool posted = false, running = false, done = false, quit = false;
 };
+
+// One batch's temporal projection rows (all replicas, P x t x Q) and the
+// shared columns' Gram contribution, drawn on the host (extend_temporal).
+struct TemporalDraw {
+    std::uint64_t key = 0;
+    std::int64_t t = 0;
+    std::vector<double> w, gram;
+};
+TemporalDraw draw_temporal(std::uint64_t seed, int P, int Q, int sh, std::uint64_t key, std::int64_t t_new);
 
 // A sharded stream's NCCL communicator (nccl_exchange.cu).
 struct NcclExchange {
@@ -237,6 +247,7 @@ private:
     void prepare(int order, const std::int64_t* dims);
     void gen_replicas();
     void extend_temporal(std::int64_t t_new);
+    std::future<TemporalDraw> next_draw;  // the next batch's temporal rows, drawn ahead
     void upload_mapped(DevBuf<double>& dst, const double* h, size_t n);
     const void* stage_input(const void* data, int dtype, int location, size_t n);
     void check_finite(const void* dX, int dtype, size_t n);

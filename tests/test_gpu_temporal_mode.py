@@ -47,7 +47,9 @@ def test_temporal_mode_matches_oracle(ob, tm):
     assert min(O.congruence(md, ref.model)) > 1 - 1e-8
     # evaluation, checkpoint and replica models in the same order
     sl = O.slice_mode(full, tm, 16, 8)
-    assert abs(st.batch_fitness(sl, 16) - O.fitness(sl, O.slice_mode(O.reconstruct_fast(md), tm, 16, 8))) < 1e-6
+    # |X - Xhat|^2 = |X|^2 - 2<X, Xhat> + |Xhat|^2 cancels near a perfect fit:
+    # ~sqrt(eps) relative in the residual, ~1e-6 in the percentage
+    assert abs(st.batch_fitness(sl, 16) - O.fitness(sl, O.slice_mode(O.reconstruct_fast(md), tm, 16, 8))) < 1e-5
     b = st.checkpoint_save()
     assert O.checkpoint_save(O.checkpoint_load(b)) == b
     back = ob.checkpoint_load(b)
