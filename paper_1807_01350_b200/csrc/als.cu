@@ -1235,6 +1235,7 @@ AlsEngine::~AlsEngine() {
             cudaStreamDestroy(ls);
         }
     if (hact) cudaFreeHost(hact);
+    if (res_pin) cudaFreeHost(res_pin);
     for (cudaEvent_t e : kev)
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : lane_ev)
@@ -1734,7 +1735,30 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             OCTEN_CUDA(cudaEventRecord(lane_ev[0], ls[l]));
             OCTEN_CUDA(cudaStreamWaitEvent(st, lane_ev[0], 0));
         }
+    // best restart per replica and every result the host needs, in one
+    // read (the select kernel is harmless when a failure is raised below)
+    DevBuf<int> best;
+    best.reserve(P);
+    als_select_kernel<<<P, 256, 0, st>>>(d, Mf.p, Mlam.p, best.p); OCTEN_LAUNCHED(1);
+    OCTEN_CUDA(cudaGetLastError());
+    const size_t o_norm = 0, o_err = o_norm + P * sizeof(double), o_state = o_err + NP * sizeof(DevStatus),
+                 o_best = o_state + NP * sizeof(AlsState), o_fh = (o_best + P * sizeof(int) + 7) & ~size_t(7),
+                 o_rh = o_fh + (size_t)NP * max_iters * sizeof(double), o_end = o_rh + (size_t)NP * max_iters * sizeof(double);
+    if (o_end > res_cap) {
+        if (res_pin) OCTEN_CUDA(cudaFreeHost(res_pin));
+        res_cap = 2 * o_end;
+        OCTEN_CUDA(cudaHostAlloc((void**)&res_pin, res_cap, cudaHostAllocDefault));
+    }
+    OCTEN_CUDA(cudaMemcpyAsync(res_pin + o_norm, normx2.p, P * sizeof(double), cudaMemcpyDeviceToHost, st));
+    OCTEN_CUDA(cudaMemcpyAsync(res_pin + o_err, err.p, NP * sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+    OCTEN_CUDA(cudaMemcpyAsync(res_pin + o_state, state.p, NP * sizeof(AlsState), cudaMemcpyDeviceToHost, st));
+    OCTEN_CUDA(cudaMemcpyAsync(res_pin + o_best, best.p, P * sizeof(int), cudaMemcpyDeviceToHost, st));
+    OCTEN_CUDA(cudaMemcpyAsync(res_pin + o_fh, fit_hist.p, (size_t)NP * max_iters * sizeof(double),
+                               cudaMemcpyDeviceToHost, st));
+    OCTEN_CUDA(cudaMemcpyAsync(res_pin + o_rh, res_hist.p, (size_t)NP * max_iters * sizeof(double),
+                               cudaMemcpyDeviceToHost, st));
     OCTEN_CUDA(cudaStreamSynchronize(st));
+    ++host_syncs;
     last_sweeps = sweep;
     for (const KevRec& k : krec) {
         float ms = 0.f;
@@ -1796,16 +1820,15 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     // ---- errors: a zero input first (cp_als.cpp:255-256), then the lowest
     // replica, then restart
     {
-        std::vector<double> hn = normx2.to_host(P, st);
-        ++host_syncs;
+        const double* hn = reinterpret_cast<const double*>(res_pin + o_norm);
         for (int p = 0; p < P; ++p)
             if (hn[p] == 0.0) {
                 failure = {1, 0, 0};
                 throw NumericError(als_failure_message(1, 0, 0));
             }
     }
-    std::vector<DevStatus> he = err.to_host(NP, st);
-    std::vector<AlsState> hs = state.to_host(NP, st);
+    const DevStatus* he = reinterpret_cast<const DevStatus*>(res_pin + o_err);
+    const AlsState* hs = reinterpret_cast<const AlsState*>(res_pin + o_state);
     for (int prob = 0; prob < NP; ++prob) {
         if (!hs[prob].failed) continue;
         const DevStatus& e = he[prob];
@@ -1818,16 +1841,11 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             throw NumericError(als_failure_message(3, e.a, 0));
         }
     }
-    OCTEN_PROF("sweeps", st);
-    DevBuf<int> best;
-    best.reserve(P);
-    als_select_kernel<<<P, 256, 0, st>>>(d, Mf.p, Mlam.p, best.p); OCTEN_LAUNCHED(1);
-    OCTEN_PROF("select", st);
+    OCTEN_PROF("sweeps+select", st);
     EvProf::get().report("als");
-    OCTEN_CUDA(cudaGetLastError());
-    std::vector<int> hb = best.to_host(P, st);
-    std::vector<double> fh = fit_hist.to_host((size_t)NP * max_iters, st);
-    std::vector<double> rh = res_hist.to_host((size_t)NP * max_iters, st);
+    const int* hb = reinterpret_cast<const int*>(res_pin + o_best);
+    const double* fh = reinterpret_cast<const double*>(res_pin + o_fh);
+    const double* rh = reinterpret_cast<const double*>(res_pin + o_rh);
     results.assign(P, AlsReplicaResult{});
     for (int p = 0; p < P; ++p) {
         const int prob = p * S + hb[p];
@@ -1836,9 +1854,8 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         r.iterations = hs[prob].iterations;
         r.rescued = hs[prob].rescued != 0;
         r.gevd_attempt = used[prob];
-        r.fit_history.assign(fh.begin() + (size_t)prob * max_iters, fh.begin() + (size_t)prob * max_iters + r.iterations);
-        r.residual_history.assign(rh.begin() + (size_t)prob * max_iters,
-                                  rh.begin() + (size_t)prob * max_iters + r.iterations);
+        r.fit_history.assign(fh + (size_t)prob * max_iters, fh + (size_t)prob * max_iters + r.iterations);
+        r.residual_history.assign(rh + (size_t)prob * max_iters, rh + (size_t)prob * max_iters + r.iterations);
         r.fit = r.fit_history.empty() ? -INFINITY : r.fit_history.back();
     }
 }

@@ -112,6 +112,8 @@ private:
     DevBuf<Mt64> rngs;
     DevBuf<std::uint64_t> rescue_seed;
     std::future<AlsHostDraws> next_draws;
+    unsigned char* res_pin = nullptr;  // pinned landing area of run()'s results (one read)
+    size_t res_cap = 0;
 };
 
 // ---------------------------------------------------------------------------
