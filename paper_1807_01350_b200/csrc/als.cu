@@ -235,6 +235,15 @@ __global__ void __launch_bounds__(256) gevd_mix_kernel(AlsDev d) {
         }
 }
 
+// Round 0 of the GEVD attempts: every problem of a usable replica starts at
+// attempt 0.
+__global__ void gevd_round0_kernel(AlsDev d) {
+    const int prob = blockIdx.x * blockDim.x + threadIdx.x;
+    if (prob >= d.NP) return;
+    d.att_start[prob] = 0;
+    d.todo[prob] = d.usable[prob / d.S] ? 1 : 0;
+}
+
 // Per problem: pick the first GEVD attempt whose pencil is invertible, has a
 // real Schur form and gives non-degenerate a1 columns (cp_als.cpp:110-150).
 __global__ void gevd_pencil_kernel(AlsDev d) {
@@ -1388,18 +1397,21 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
                                                 Tmp6Store{Tmp6.p, Q, R}, st);
         gemm_f64<true, false>(NP * 6, R, R, Q, UrTA{Ur.p, Q, R, S}, Tmp6B{Tmp6.p, Q, R},
                                                PmStore{Pm.p, R}, st);
-        std::vector<int> hus = usable.to_host(P, st);
-        ++host_syncs;
+        // round 0 starts from the device's usability flags (no host round
+        // trip); the host learns them with the round's outcome
         std::vector<int> start(NP, 0), td(NP, 0);
-        for (int prob = 0; prob < NP; ++prob) td[prob] = hus[prob / S] ? 1 : 0;
+        att_start.reserve(NP);
+        todo.reserve(NP);
         for (int round = 0; round < 3; ++round) {
-            bool any = false;
-            for (int prob = 0; prob < NP; ++prob) any |= td[prob] != 0;
-            if (!any) break;
-            att_start.reserve(NP);
-            h2d_param(att_start.p, start.data(), NP * sizeof(int), st);
-            todo.reserve(NP);
-            h2d_param(todo.p, td.data(), NP * sizeof(int), st);
+            if (round == 0) {
+                gevd_round0_kernel<<<(NP + 127) / 128, 128, 0, st>>>(d); OCTEN_LAUNCHED(1);
+            } else {
+                bool any = false;
+                for (int prob = 0; prob < NP; ++prob) any |= td[prob] != 0;
+                if (!any) break;
+                h2d_param(att_start.p, start.data(), NP * sizeof(int), st);
+                h2d_param(todo.p, td.data(), NP * sizeof(int), st);
+            }
             peel_fail.zero(NP, st);
             const size_t smem_pen = (size_t)(5 * R * R + 7 * R + 72) * sizeof(double);
             OCTEN_PROF("mix", st);
@@ -1427,8 +1439,28 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             gevd_peel_kernel<<<NP * R, peel_threads, smem_peel, st>>>(d); OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaGetLastError());
             OCTEN_PROF("peel", st);
-            std::vector<int> au = att_used.to_host(NP, st);
-            std::vector<int> pf = peel_fail.to_host(NP, st);
+            std::vector<int> au(NP), pf(NP);
+            {
+                // one read: this round's attempts and peel flags (+ the
+                // usability flags after round 0)
+                const size_t nb = (size_t)NP * sizeof(int);
+                if (3 * nb + P * sizeof(int) > res_cap) {
+                    if (res_pin) OCTEN_CUDA(cudaFreeHost(res_pin));
+                    res_cap = 2 * (3 * nb + P * sizeof(int));
+                    OCTEN_CUDA(cudaHostAlloc((void**)&res_pin, res_cap, cudaHostAllocDefault));
+                }
+                OCTEN_CUDA(cudaMemcpyAsync(res_pin, att_used.p, nb, cudaMemcpyDeviceToHost, st));
+                OCTEN_CUDA(cudaMemcpyAsync(res_pin + nb, peel_fail.p, nb, cudaMemcpyDeviceToHost, st));
+                if (round == 0)
+                    OCTEN_CUDA(cudaMemcpyAsync(res_pin + 2 * nb, usable.p, P * sizeof(int), cudaMemcpyDeviceToHost, st));
+                OCTEN_CUDA(cudaStreamSynchronize(st));
+                std::memcpy(au.data(), res_pin, nb);
+                std::memcpy(pf.data(), res_pin + nb, nb);
+                if (round == 0) {
+                    const int* hus = reinterpret_cast<const int*>(res_pin + 2 * nb);
+                    for (int prob = 0; prob < NP; ++prob) td[prob] = hus[prob / S] ? 1 : 0;
+                }
+            }
             ++host_syncs;
             for (int prob = 0; prob < NP; ++prob) {
                 if (!td[prob]) continue;
