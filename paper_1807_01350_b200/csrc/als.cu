@@ -35,7 +35,7 @@ namespace {
 
 constexpr double kDegenerateNorm = 1e-14;  // cp_als.cpp:17
 constexpr double kEps = 2.220446049250313e-16;
-constexpr int kAlsMaxLanes = 4;  // AlsEngine::kMaxLanes
+constexpr int kAlsMaxLanes = 8;  // AlsEngine::kMaxLanes
 
 struct AlsDev {
     int P, S, Q, R, NP, max_iters;

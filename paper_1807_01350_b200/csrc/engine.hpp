@@ -87,7 +87,7 @@ private:
     void alloc(int P, int S, int Q, int R, int max_iters);
     int P_ = 0, S_ = 0, Q_ = 0, R_ = 0, I_ = 0;
     DevBuf<double> normx2, F, G, lam, T, KR, Mb, Vinv, fit_hist, res_hist, ws, tscbuf;
-    static constexpr int kMaxLanes = 4;
+    static constexpr int kMaxLanes = 8;
     int* hact = nullptr;  // host-mapped per-sweep activity flags
     size_t hact_n = 0;
     cudaStream_t lane_st[kMaxLanes] = {};   // sweep lanes 1..L-1 (lane 0 runs on the caller's stream)
