@@ -9,6 +9,6 @@ tail -3 gpurun_out/${TAG}_tests.log
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.log 2>&1; echo "bench rc=$?"
 tail -1 gpurun_out/${TAG}_bench.log | cut -c1-400
 if [ -n "$REF" ]; then
-  timeout 1800 python bench.py --impl reference --steps ${REF_STEPS:-3} --warmup 1 > gpurun_out/${TAG}_ref.log 2>&1; echo "ref rc=$?"
+  timeout 1800 python bench.py --impl reference --steps ${REF_STEPS:-3} --warmup ${REF_WARMUP:-1} > gpurun_out/${TAG}_ref.log 2>&1; echo "ref rc=$?"
   tail -1 gpurun_out/${TAG}_ref.log | cut -c1-600
 fi
