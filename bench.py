@@ -372,6 +372,19 @@ def run_reference(args, cfg, rank, world):
                 stage_rows.append(st.timers()[-1][:3])
         impl = ("the reference library compiled from its own sources (oracle/_ref: proj/src/*.cpp with the Eigen "
                 "stand-in on single-threaded OpenBLAS)")
+        # the reference model's fitness (eval.cpp:10-20) on its last batch,
+        # beside the device arm's model_quality
+        try:
+            m = st.model()
+            k_last = k_init + (nb - 1) * t
+            A, B, Cm = m.factors
+            xh = np.einsum("ir,jr,kr->ijk", A * m.lambda_, B, Cm[k_last:k_last + t], optimize=True)
+            nx = float(np.linalg.norm(b))
+            quality = {"batch_fitness_pct": 100.0 * (1.0 - float(np.linalg.norm(b - xh)) / nx),
+                       "slices": [k_last, k_last + t],
+                       "note": "fitness (eval.cpp:10-20) of the reference's model after its last batch on that batch"}
+        except Exception as exc:  # pragma: no cover
+            quality = {"error": repr(exc)}
     else:
         O.MERGE_PROCESSES = True
         st = O.init_stream(syn.batch(0, k_init), scfg)
@@ -387,6 +400,7 @@ def run_reference(args, cfg, rank, world):
                 stage_rows.append([r.compress_seconds, r.als_seconds, r.recover_seconds])
         workers = O.resolve_workers(scfg)
         impl = "the oracle port (numpy/LAPACK restatement of the reference; oracle/_ref was not built)"
+        quality = None
     sec = float(np.mean(times))
     v = I * J * t / sec
     sr = np.asarray(stage_rows, dtype=float)
@@ -400,7 +414,7 @@ def run_reference(args, cfg, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": bench_config(args, cfg, int(os.environ.get("WORLD_SIZE", "1"))),
-            "stages_s": stages, "step_s": [round(x, 3) for x in times],
+            "stages_s": stages, "step_s": [round(x, 3) for x in times], "model_quality": quality,
             "cpu_baseline": {"value": v, "unit": "entries/s", "cores": workers, "kind": kind, "sample": sample},
             "e2e": {"value": v, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -727,6 +741,7 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     launches = ob._capi.LIB.octen_launch_count() - l0
     times1 = ctypes_stage_times(ob, st)
+    ks1 = st.kernel_stats() if hasattr(st, "kernel_stats") else None  # the timed steps only
     dt = [b - a for a, b in zip(times0, times1)]
     if world > 1:
         tt = torch.tensor([ms], device=dev)
@@ -817,7 +832,6 @@ def main():
     except Exception:
         traffic = None
     n_mma = 3.0 if os.environ.get("OCTEN_G1_3MMA") else 2.0  # the library's GEMM1 split (tc_gemm.cu)
-    ks1 = st.kernel_stats() if hasattr(st, "kernel_stats") else None
     kd = {k: ks1[k] - ks0[k] for k in ks1} if (ks1 and ks0) else None
     rooflines = {
         "gemm1": {"kernel": "tc_gemm_tf32x3_persistent_kernel (compression mode-1 contraction, GEMM1)",

@@ -81,14 +81,19 @@ struct AlsDev {
 };
 
 __device__ double block_sum(double v, double* red) {
-    // deterministic block reduction (fixed tree)
-    red[threadIdx.x] = v;
+    // deterministic block reduction (fixed tree): butterfly within each warp,
+    // then the warp sums in warp order; two barriers (blockDim a multiple of 32)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
     __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-        if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-        __syncthreads();
+    if (warp == 0) {
+        double w = lane < nw ? red[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if (lane == 0) red[32] = w;
     }
-    const double out = red[0];
+    __syncthreads();
+    const double out = red[32];
     __syncthreads();
     return out;
 }

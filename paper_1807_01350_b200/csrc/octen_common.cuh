@@ -150,23 +150,32 @@ OCTEN_HD inline double dsq(double x) { return x * x; }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
-// Block-wide global -> shared copy with four independent loads in flight per
-// thread.  (A plain `dst[e] = src[e]` loop through generic pointers makes
-// every load wait for the previous shared store, since the compiler cannot
-// rule out aliasing: one global latency per element per thread.)  src must
-// be read-only for the kernel's lifetime.
+// Block-wide global -> shared copy with eight independent loads in flight per
+// thread (the ALS update's 2400-element M / V^-1 staging in one latency).
+// (A plain `dst[e] = src[e]` loop through generic pointers makes every load
+// wait for the previous shared store, since the compiler cannot rule out
+// aliasing: one global latency per element per thread.)  src must not have
+// been read by this SM earlier in the kernel while other blocks wrote it
+// (the non-coherent load path).
 __device__ __forceinline__ void g2s_copy(double* dst, const double* src, int n) {
+    constexpr int U = 8;
     const int st = blockDim.x;
     int e = threadIdx.x;
-    for (; e + 3 * st < n; e += 4 * st) {
-        const double v0 = __ldg(src + e), v1 = __ldg(src + e + st);
-        const double v2 = __ldg(src + e + 2 * st), v3 = __ldg(src + e + 3 * st);
-        dst[e] = v0;
-        dst[e + st] = v1;
-        dst[e + 2 * st] = v2;
-        dst[e + 3 * st] = v3;
+    for (; e + (U - 1) * st < n; e += U * st) {
+        double v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) v[j] = __ldg(src + e + j * st);
+#pragma unroll
+        for (int j = 0; j < U; ++j) dst[e + j * st] = v[j];
     }
-    for (; e < n; e += st) dst[e] = __ldg(src + e);
+    {
+        double v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) v[j] = (e + j * st < n) ? __ldg(src + e + j * st) : 0.0;
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+            if (e + j * st < n) dst[e + j * st] = v[j];
+    }
 }
 #endif
 
