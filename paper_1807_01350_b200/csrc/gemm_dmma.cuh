@@ -164,52 +164,30 @@ __global__ void __launch_bounds__(256)
 // FP64 tensor cores: C(m, n) = sum_k A(m, k) B(k, n) with element strides
 //   A(m, k) = A[m * sam + k * sak],  B(k, n) = B[k * sbk + n * sbn],
 //   C(m, n) = C[m * scm + n * scn].
-// The block's warps take 8 x 8 output tiles round-robin, up to four tiles
-// per warp at once with independent accumulators (the K loop's DMMA chains
-// interleave instead of running back to back), and step k by 4 (DMMA
-// m8n8k4); indices past M / N / K read as zero.  Every output accumulates
-// over k in ascending order, so the bits do not depend on the grouping.
-// For the R x R and Q x R products of the ALS update (Q <= 256, R <= 64).
-// No barrier inside: callers synchronize before reading C.
+// The block's warps take 8 x 8 output tiles round-robin and step k by 4
+// (DMMA m8n8k4); indices past M / N / K read as zero.  For the R x R and
+// Q x R products of the ALS update (Q <= 256, R <= 64).  No barrier inside:
+// callers synchronize before reading C.
 // ---------------------------------------------------------------------------
 __device__ inline void block_dmma_small(int M, int N, int K, const double* A, int sam, int sak, const double* B,
                                         int sbk, int sbn, double* C, int scm, int scn) {
-    constexpr int G = 4;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int g = lane >> 2, t4 = lane & 3;
-    const int tm = (M + 7) >> 3, tn = (N + 7) >> 3, nt = tm * tn;
-    for (int base = warp; base < nt; base += G * nw) {
-        double c0[G], c1[G];
-        int m0[G], n0[G];
-        bool on[G];
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-            const int tile = base + j * nw;
-            on[j] = tile < nt;  // warp-uniform
-            m0[j] = on[j] ? (tile % tm) * 8 : 0;
-            n0[j] = on[j] ? (tile / tm) * 8 : 0;
-            c0[j] = c1[j] = 0.0;
-        }
+    const int tm = (M + 7) >> 3, tn = (N + 7) >> 3;
+    for (int tile = warp; tile < tm * tn; tile += nw) {
+        const int m0 = (tile % tm) * 8, n0 = (tile / tm) * 8;
+        double c0 = 0.0, c1 = 0.0;
+        const int am = m0 + g, bn = n0 + g;
         for (int k0 = 0; k0 < K; k0 += 4) {
             const int k = k0 + t4;
-            const bool kin = k < K;
-#pragma unroll
-            for (int j = 0; j < G; ++j) {
-                if (!on[j]) continue;
-                const int am = m0[j] + g, bn = n0[j] + g;
-                const double a = (am < M && kin) ? A[am * sam + k * sak] : 0.0;
-                const double b = (bn < N && kin) ? B[k * sbk + bn * sbn] : 0.0;
-                dmma_m8n8k4(c0[j], c1[j], a, b);
-            }
+            const double a = (am < M && k < K) ? A[am * sam + k * sak] : 0.0;
+            const double b = (bn < N && k < K) ? B[k * sbk + bn * sbn] : 0.0;
+            dmma_m8n8k4(c0, c1, a, b);
         }
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-            if (!on[j]) continue;
-            const int cm = m0[j] + g, cn = n0[j] + 2 * t4;
-            if (cm < M) {
-                if (cn < N) C[cm * scm + cn * scn] = c0[j];
-                if (cn + 1 < N) C[cm * scm + (cn + 1) * scn] = c1[j];
-            }
+        const int cm = m0 + g, cn = n0 + 2 * t4;
+        if (cm < M) {
+            if (cn < N) C[cm * scm + cn * scn] = c0;
+            if (cn + 1 < N) C[cm * scm + (cn + 1) * scn] = c1;
         }
     }
 }

