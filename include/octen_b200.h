@@ -89,7 +89,9 @@ int64_t octen_launch_count(void);
  * out[0] all launches (= octen_launch_count), out[1] tcgen05 launches of
  * the fp32 dense compression (GEMM1 + mode-2), out[2] fp32 compression
  * chunks that ran on the SIMT GEMM because their shape is outside the
- * tcgen05 kernels' limits, out[3] DMMA launches of the fp64 compression. */
+ * tcgen05 kernels' limits, out[3] DMMA launches of the fp64 compression,
+ * out[4] tcgen05 (kind::i8 digit-split fp64) launches of the CP-ALS T-GEMM.
+ * out must hold 5 values. */
 void octen_kernel_counts(int64_t* out);
 
 /* init_stream (proj/include/cpstream/streaming.hpp:64; src/streaming.cpp:181-256).
@@ -309,6 +311,16 @@ int octen_compress(int p, int q, int shared, int64_t I, int64_t J, int64_t t, co
  * factors: p x 3 x Q x rank, lambda: p x rank, fit: p, iterations: p. */
 int octen_cp_als_batched(int p, int q, const double* y, const octen_als_config* cfg, const uint64_t* seeds,
                          double* factors, double* lambda, double* fit, int32_t* iterations);
+
+/* One partial MTTKRP contraction of the device CP-ALS (the fp64 GEMM of
+ * cp_als.cpp:296-303 as the dimension tree forms it): T = Y x_mode F for all
+ * s restarts.  y: p x Q^3 (first index fastest); factors: p x s x 3 x Q x r
+ * (restart-major, the mode's Q x r block column-major); t: p x Q^2 x (s r),
+ * t[p][m + Q^2 (s_ r + c)] with m the two remaining indices, first fastest.
+ * engine 1: int8 tcgen05 with exact digit splitting (the sweeps' path),
+ * engine 0: the FP64 DMMA GEMM. */
+int octen_als_tgemm(int p, int q, int s, int r, int mode, const double* y, const double* factors, double* t,
+                    int engine);
 
 /* align_replicas (proj/include/cpstream/recovery.hpp:43; src/recovery.cpp:106-291).
  * models: factors p x 3 x Q x R, lambda p x R; u/v: p x I x Q / p x J x Q;

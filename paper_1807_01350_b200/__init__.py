@@ -70,10 +70,12 @@ def kernel_counts() -> dict:
     """Process-wide kernel path counters (octen_kernel_counts): every launch,
     tcgen05 launches of the fp32 dense compression, fp32 chunks that fell
     back to the SIMT GEMM (shape outside the tcgen05 kernels' limits), DMMA
-    launches of the fp64 compression."""
-    out = (C.c_i64 * 4)()
+    launches of the fp64 compression, tcgen05 (kind::i8 digit-split fp64)
+    launches of the CP-ALS T-GEMM."""
+    out = (C.c_i64 * 5)()
     C.LIB.octen_kernel_counts(out)
-    return {"launches": out[0], "tcgen05": out[1], "simt_fallbacks": out[2], "dmma_compress": out[3]}
+    return {"launches": out[0], "tcgen05": out[1], "simt_fallbacks": out[2], "dmma_compress": out[3],
+            "tcgen05_als": out[4]}
 
 
 @dataclass
@@ -640,6 +642,22 @@ def cp_als_batched(tensors: List[np.ndarray], cfg: AlsConfig, seeds: List[int]):
         fs = [f[(i * 3 + n) * q * r:(i * 3 + n + 1) * q * r].reshape((q, r), order="F").copy() for n in range(3)]
         models.append(KruskalModel(fs, lam[i * r:(i + 1) * r].copy()))
     return models, fit, it
+
+
+def als_tgemm(y: np.ndarray, factors: np.ndarray, mode: int, engine: int = 1) -> np.ndarray:
+    """One partial MTTKRP contraction of the device CP-ALS (octen_als_tgemm):
+    T = Y x_mode F for every restart.  y: p x Q x Q x Q; factors:
+    p x s x 3 x Q x R (the mode's Q x R blocks).  Returns p x Q^2 x (s R)
+    with row m = the two remaining indices (first fastest).  engine 1: the
+    int8 tcgen05 digit-split GEMM the sweeps use, 0: the FP64 DMMA GEMM."""
+    p, q = y.shape[0], y.shape[1]
+    s, r = factors.shape[1], factors.shape[4]
+    yf = np.concatenate([_f64(y[i]).ravel(order="F") for i in range(p)])
+    ff = np.concatenate([_f64(factors[i, j, n]).ravel(order="F") for i in range(p) for j in range(s)
+                         for n in range(3)])
+    t = np.zeros(p * q * q * s * r)
+    _check(C.LIB.octen_als_tgemm(p, q, s, r, mode, _dptr(yf), _dptr(ff), _dptr(t), engine))
+    return t.reshape((p, s * r, q * q)).transpose(0, 2, 1).copy()
 
 
 def align_replicas(models: List[KruskalModel], u: List[np.ndarray], v: List[np.ndarray], tgram: np.ndarray,

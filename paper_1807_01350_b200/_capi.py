@@ -115,6 +115,8 @@ SIGNATURES = {
                                       P_dbl, ctypes.c_void_p, ctypes.c_int, P_dbl]),
     "octen_cp_als_batched": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P_dbl, ctypes.POINTER(AlsConfigC), P_u64,
                                             P_dbl, P_dbl, P_dbl, P_i32]),
+    "octen_als_tgemm": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P_dbl,
+                                       P_dbl, P_dbl, ctypes.c_int]),
     "octen_align_replicas": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i64, c_i64,
                                             P_dbl, P_dbl, P_dbl, P_dbl, P_dbl, P_dbl, P_i32, P_dbl, P_dbl]),
     "octen_recover_nontemporal": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_i64, ctypes.c_int, ctypes.c_int,

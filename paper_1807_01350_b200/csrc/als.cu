@@ -26,6 +26,8 @@
 #include "evprof.hpp"
 #include "gemm_dmma.cuh"
 #include "h2d_param.cuh"
+#include "ozaki.hpp"
+#include "ozaki_digits.cuh"
 #include "rng_host.hpp"
 #include "small_linalg.cuh"
 
@@ -74,6 +76,11 @@ struct AlsDev {
     int* att_used;
     int* todo;
     int* peel_fail;
+    // digits of every factor for the int8 tensor-core T-GEMM (ozaki_digits.cuh
+    // layout; null: the DMMA T-GEMM, no digits written)
+    std::uint8_t* Fd;
+    double* Fcs;
+    int oz_G;
     __device__ size_t q3() const { return (size_t)Q * Q * Q; }
     __device__ size_t q2() const { return (size_t)Q * Q; }
     __device__ double* f(int prob, int n) const { return F + ((size_t)prob * 3 + n) * Q * R; }
@@ -646,6 +653,11 @@ __device__ void als_update_block(const AlsDev& d, int prob, int mode, int sweep,
     double* g = d.g(prob, mode);
     // Gram of the new factor on the FP64 tensor cores: g(i, j) = sum_q raw(q, i) raw(q, j)
     block_dmma_small(R, R, Q, raw, Q, 1, raw, 1, Q, g, 1, R);
+    if (d.Fd) {  // the new factor's digits for the next T-GEMM that contracts this mode
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int r = warp; r < R; r += nw)
+            oz::factor_column_digits(d.Fd, d.Fcs, d.oz_G, d.S, R, Q, prob, mode, r, raw + (size_t)Q * r, lane);
+    }
     __syncthreads();
     OCTEN_TSC(8)
     if (mode != 2) return;
@@ -1296,6 +1308,9 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     d.err = err.p;
     d.rngs = rngs.p;
     d.rescue_seed = rescue_seed.p;
+    d.Fd = nullptr;
+    d.Fcs = nullptr;
+    d.oz_G = 0;
     d.Gev = Gev.p;
     d.EV = EV.p;
     d.Ur = Ur.p;
@@ -1608,6 +1623,35 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         x.rescue_seed = rescue_seed.p + qb;
         x.hact = hact_dev + l;
     }
+    // The T-GEMMs run on the int8 tensor cores with exact digit splitting
+    // (ozaki.cu): the summaries are sliced once here, in all three
+    // orientations, before the lanes fork (a normal launch, so every
+    // programmatic dependent launch after it sees the slices).
+    const bool use_oz = ozaki_selected(Q);
+    CUtensorMap ozmap[3][kMaxLanes], ozbmap[kMaxLanes];
+    if (use_oz) {
+        const size_t pitch = (size_t)ozaki_pitch(Q);
+        const int G = ozaki_groups(S, R);
+        oz_a.reserve((size_t)3 * P * kOzSlices * q2 * pitch);
+        oz_e.reserve((size_t)3 * P * q2);
+        oz_fd.reserve(ozaki_fd_bytes(P, S, R));
+        oz_fcs.reserve(ozaki_fcs_count(P, S, R));
+        oz_fd.zero(ozaki_fd_bytes(P, S, R), st);  // (padding columns stay zero)
+        ozaki_slice_y(dY, P, Q, oz_a.p, oz_e.p, st);
+        ozaki_slice_factors(F.p, P, S, Q, R, oz_fd.p, oz_fcs.p, st);
+        const size_t plane_bytes = ozaki_fd_bytes(1, 1, 1) / 3, plane_cols = ozaki_fcs_count(1, 1, 1) / 3;
+        for (int l = 0; l < L; ++l) {
+            for (int o = 0; o < 3; ++o)
+                if (!ozaki_make_map(&ozmap[o][l], oz_a.p, P, Q, o, lp0[l], lp1[l] - lp0[l]))
+                    throw CudaError("octen: tensor map of the CP-ALS digit slices could not be encoded");
+            if (!ozaki_make_fmap(&ozbmap[l], oz_fd.p, Q, G, lp0[l], lp1[l] - lp0[l]))
+                throw CudaError("octen: tensor map of the CP-ALS factor digits could not be encoded");
+            AlsDev& x = dl[l];
+            x.Fd = oz_fd.p + (size_t)lp0[l] * 3 * G * plane_bytes;
+            x.Fcs = oz_fcs.p + (size_t)lp0[l] * 3 * G * plane_cols;
+            x.oz_G = G;
+        }
+    }
     if (L > 1) {
         OCTEN_CUDA(cudaEventRecord(lane_ev[0], st));
         for (int l = 0; l < L; ++l)
@@ -1676,7 +1720,10 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
             }
             const bool kt_on = ktime_on(l, sw);
             const int kt0 = kt_on ? ktime_begin(gs) : -1;
-            if (contracted == 2) {  // rows (i, j)
+            if (use_oz) {
+                ozaki_tgemm(ozmap[contracted][l], ozbmap[l], oz_e.p + ((size_t)contracted * P + lp0[l]) * q2, x.Fcs,
+                            x.T, pn, Q, S, R, contracted, gs, pd);
+            } else if (contracted == 2) {  // rows (i, j)
                 if (pipe_ok)
                     gemm_f64_pipe<false>(pn, (int)q2, SR, Q, YmatP{x.Y, q3, q2}, FacP{x.F, S, Q, R, 2},
                                          TStore{x.T, q2, SR}, gs, 1, nullptr, pd);
@@ -1895,6 +1942,47 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         r.residual_history.assign(rh + (size_t)prob * max_iters, rh + (size_t)prob * max_iters + r.iterations);
         r.fit = r.fit_history.empty() ? -INFINITY : r.fit_history.back();
     }
+}
+
+
+// One T-GEMM of the dimension tree (the partial MTTKRP contraction
+// T = Y x_mode F of every restart), on the engine the sweeps use (engine 1:
+// int8 tcgen05 digit split, ozaki.cu) or the DMMA GEMM (engine 0), for the
+// kernel-level parity tests.  Device pointers: Y P x Q^3, F P x S x 3 x Q x R,
+// T P x Q^2 x S R (T[p][m + Q^2 n], n = s R + r).
+void als_tgemm(int P, int Q, int S, int R, int mode, const double* Y, const double* F, double* T, int engine,
+               cudaStream_t st) {
+    if (mode < 0 || mode > 2 || P < 1 || Q < 1 || S < 1 || R < 1) throw ConfigError("als_tgemm: bad shape");
+    const size_t q2 = (size_t)Q * Q, q3 = q2 * Q;
+    const int SR = S * R;
+    if (engine == 1) {
+        if (!ozaki_supported(Q)) throw ConfigError("als_tgemm: the tcgen05 digit-split GEMM needs Q <= 128 on sm_100");
+        DevBuf<std::uint8_t> a, fd;
+        DevBuf<int> e;
+        DevBuf<double> fcs;
+        a.reserve((size_t)3 * P * kOzSlices * q2 * ozaki_pitch(Q));
+        e.reserve((size_t)3 * P * q2);
+        fd.reserve(ozaki_fd_bytes(P, S, R));
+        fcs.reserve(ozaki_fcs_count(P, S, R));
+        fd.zero(ozaki_fd_bytes(P, S, R), st);
+        ozaki_slice_y(Y, P, Q, a.p, e.p, st);
+        ozaki_slice_factors(F, P, S, Q, R, fd.p, fcs.p, st);
+        CUtensorMap map, fmap;
+        if (!ozaki_make_map(&map, a.p, P, Q, mode, 0, P) || !ozaki_make_fmap(&fmap, fd.p, Q, ozaki_groups(S, R), 0, P))
+            throw CudaError("als_tgemm: tensor map");
+        ozaki_tgemm(map, fmap, e.p + (size_t)mode * P * q2, fcs.p, T, P, Q, S, R, mode, st, false);
+        OCTEN_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    const unsigned qinv = (unsigned)((0x100000000ull + Q - 1) / Q);
+    if (mode == 2)
+        gemm_f64<false, true>(P, (int)q2, SR, Q, YmatA{Y, q3, q2, S, false}, FacB{F, S, Q, R, 2}, TStore{T, q2, SR}, st);
+    else if (mode == 1)
+        gemm_f64_pipe<false>(P, (int)q2, SR, Q, YmidP{Y, q3, (unsigned)Q, qinv}, FacP{F, S, Q, R, 1},
+                             TStore{T, q2, SR}, st, 1, nullptr, false);
+    else
+        gemm_f64<true, true>(P, (int)q2, SR, Q, Y0tA{Y, q3, Q}, FacB{F, S, Q, R, 0}, TStore{T, q2, SR}, st);
+    OCTEN_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace octen

@@ -686,6 +686,21 @@ int octen_cp_als_batched(int p, int q, const double* y, const octen_als_config* 
     });
 }
 
+int octen_als_tgemm(int p, int q, int s, int r, int mode, const double* y, const double* factors, double* t,
+                    int engine) {
+    return guard([&] {
+        ScopedStream ss;
+        const size_t q2 = (size_t)q * q;
+        octen::DevBuf<double> dY, dF, dT;
+        dY.upload(y, (size_t)p * q2 * q, ss.st);
+        dF.upload(factors, (size_t)p * s * 3 * q * r, ss.st);
+        dT.reserve((size_t)p * q2 * s * r);
+        octen::als_tgemm(p, q, s, r, mode, dY.p, dF.p, dT.p, engine, ss.st);
+        dT.download(t, (size_t)p * q2 * s * r, ss.st);
+        OCTEN_CUDA(cudaStreamSynchronize(ss.st));
+    });
+}
+
 int octen_align_replicas(int p, int q, int shared, int rank, int64_t I, int64_t J, const double* u,
                          const double* v, const double* tgram, const double* factors, const double* lambda,
                          double* stacks, int32_t* perms, double* scales, double* sims) {

@@ -59,6 +59,11 @@ struct AlsHostDraws {
 };
 AlsHostDraws als_host_draws(const std::vector<std::uint64_t>& seeds, int S, int Q);
 
+// One dimension-tree T-GEMM, T = Y x_mode F (als.cu; engine 1: tcgen05
+// digit split, engine 0: DMMA), for kernel-level tests.
+void als_tgemm(int P, int Q, int S, int R, int mode, const double* Y, const double* F, double* T, int engine,
+               cudaStream_t st);
+
 class AlsEngine {
 public:
     // Y: P x Q^3 device summaries.  seeds: per replica AlsConfig.seed.
@@ -106,6 +111,10 @@ private:
     };
     std::vector<KevRec> krec;
     DevBuf<double> Gev, EV, Ur, Wmix, Smix, Tmp6, Pm, Hh, gscr;
+    DevBuf<std::uint8_t> oz_a;  // digit slices of the summaries, 3 orientations (ozaki.hpp)
+    DevBuf<int> oz_e;           // their row exponents
+    DevBuf<std::uint8_t> oz_fd; // digits of the factors (written by the mode updates)
+    DevBuf<double> oz_fcs;      // their column scales
     DevBuf<int> usable, att_start, att_used, todo, peel_fail, eigdbg, mcount;
     DevBuf<AlsState> state;
     DevBuf<DevStatus> err;

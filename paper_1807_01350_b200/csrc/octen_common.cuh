@@ -36,8 +36,9 @@ inline std::atomic<long long>& launch_counter() {
 // Path counters (octen_kernel_counts): tcgen05 launches of the fp32 dense
 // compression (GEMM1 + mode-2), chunks of it that ran on the SIMT GEMM
 // instead (a shape outside the tcgen05 kernels' limits), and DMMA launches
-// of the fp64-input compression.
-enum PathCounter { kTcgen05Launches = 0, kSimtFallbacks = 1, kDmmaCompress = 2, kNumPathCounters = 3 };
+// of the fp64-input compression, tcgen05 (kind::i8, digit-split fp64)
+// launches of the CP-ALS T-GEMM.
+enum PathCounter { kTcgen05Launches = 0, kSimtFallbacks = 1, kDmmaCompress = 2, kTcgen05Als = 3, kNumPathCounters = 4 };
 inline std::atomic<long long>& path_counter(int i) {
     static std::atomic<long long> c[kNumPathCounters];
     return c[i];

@@ -735,6 +735,8 @@ bool g_disabled = false;
 
 }  // namespace
 
+void* tc_tensor_map_encoder() { return (void*)get_encode(); }
+
 bool tc_gemm_available() {
     if (g_disabled) return false;
     if (std::getenv("OCTEN_DISABLE_TCGEN05")) return false;

@@ -11,6 +11,8 @@
 namespace octen {
 
 bool tc_gemm_available();
+// cuTensorMapEncodeTiled through the runtime's driver entry point (nullptr if absent).
+void* tc_tensor_map_encoder();
 // A_hi / A_lo: M x K row-major (leading dimension lda >= K, lda % 4 == 0);
 // X: K x N column-major (K contiguous); Z: M x N row-major (ld N).
 // scatter_p > 0: output row m of the deduplicated stack is written to the
