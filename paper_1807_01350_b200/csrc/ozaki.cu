@@ -167,14 +167,17 @@ __device__ __forceinline__ void oz_pack4(const unsigned long long (&g)[4], uint3
     w[0] = __byte_perm(e01, e23, 0x5410);  // byte 6: slice 1 (top)
 }
 
-// One thread per row m of every (orientation, replica): the row's exponent,
-// then its digits 16 bytes at a time into the 7 slice planes.
+// 32 rows m of one (orientation, replica) per 128-thread CTA: the rows are
+// staged in shared memory with coalesced loads (along k when the row is
+// contiguous, orientation 0; along m otherwise), then four threads per row
+// form its exponent (a shuffle max) and its digits, 16 bytes at a time.
+constexpr int SL_ROWS = 32;
 __global__ void __launch_bounds__(128) oz_slice_y_kernel(const double* __restrict__ Y, int P, int Q, int pitch,
                                                          uint8_t* __restrict__ As, int* __restrict__ Ea) {
+    extern __shared__ double tile[];  // SL_ROWS x (Q + 1)
     const int o = blockIdx.z, p = blockIdx.y;
-    const int q2 = Q * Q;
-    const int m = blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= q2) return;
+    const int q2 = Q * Q, ld = Q + 1;
+    const int m0 = blockIdx.x * SL_ROWS;
     size_t s0, s1, sk;
     if (o == 2) {
         s0 = 1, s1 = (size_t)Q, sk = (size_t)q2;
@@ -183,22 +186,47 @@ __global__ void __launch_bounds__(128) oz_slice_y_kernel(const double* __restric
     } else {
         s0 = (size_t)Q, s1 = (size_t)q2, sk = 1;
     }
-    const double* row = Y + (size_t)p * q2 * Q + (size_t)(m % Q) * s0 + (size_t)(m / Q) * s1;
+    const double* Yp = Y + (size_t)p * q2 * Q;
+    const int tid = threadIdx.x;
+    if (sk == 1) {  // row-contiguous: a warp per row, lanes along k
+        for (int r = tid >> 5; r < SL_ROWS; r += 4) {
+            const int m = m0 + r;
+            const double* row = Yp + (size_t)(m % Q) * s0 + (size_t)(m / Q) * s1;
+            for (int k = tid & 31; k < Q; k += 32) tile[r * ld + k] = m < q2 ? __ldg(row + k) : 0.0;
+        }
+    } else {  // m-contiguous: lanes along m
+        const int r = tid & 31;
+        const int m = m0 + r;
+        const double* row = Yp + (size_t)(m % Q) * s0 + (size_t)(m / Q) * s1;
+        for (int k = tid >> 5; k < Q; k += 4) tile[r * ld + k] = m < q2 ? __ldg(row + k * sk) : 0.0;
+    }
+    __syncthreads();
+    const int r = tid >> 2, part = tid & 3;  // four threads per row, 32 k each
+    const int m = m0 + r;
+    const double* trow = tile + r * ld;
     double mx = 0.0;
-    bool bad = false;
-    for (int k = 0; k < Q; ++k) {
-        const double v = __ldg(row + k * sk);
+    int bad = 0;
+    for (int k = part * 32; k < min(Q, part * 32 + 32); ++k) {
+        const double v = trow[k];
         bad |= !isfinite(v);
         mx = fmax(mx, fabs(v));
     }
-    const int e = oz_exponent(mx, bad);
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, 1);
+    bad |= __shfl_xor_sync(0xffffffffu, bad, 2);
+    const int e = oz_exponent(mx, bad != 0);
+    if (m >= q2) return;
     const size_t plane = (size_t)o * P + p;
-    Ea[plane * q2 + m] = e;
+    if (part == 0) Ea[plane * q2 + m] = e;
     double c1 = 0.0, c2 = 0.0;
     if (e != kBadExp) oz_scales(e, c1, c2);
     const size_t splane = (size_t)q2 * pitch;
     uint8_t* out = As + plane * NS * splane + (size_t)m * pitch;
-    for (int k0 = 0; k0 < pitch; k0 += 16) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int k0 = part * 32 + h * 16;
+        if (k0 >= pitch) break;
         uint32_t w[4][NS];
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
@@ -206,7 +234,7 @@ __global__ void __launch_bounds__(128) oz_slice_y_kernel(const double* __restric
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const int k = k0 + 4 * qd + t;
-                g[t] = (k < Q && e != kBadExp) ? oz_digits(__ldg(row + k * sk), c1, c2) : 0ull;
+                g[t] = (k < Q && e != kBadExp) ? oz_digits(trow[k], c1, c2) : 0ull;
             }
             oz_pack4(g, w[qd]);
         }
@@ -216,6 +244,15 @@ __global__ void __launch_bounds__(128) oz_slice_y_kernel(const double* __restric
     }
 }
 
+// Persistent over the m-tiles of one (replica, 64-column group): CTA c of
+// the group takes tiles c, c + cpg, ...  The group's 64 columns are two
+// halves of 32, each with its own TMEM buffer (8 diagonals x 32 columns), so
+// the epilogue of one half overlaps the MMAs of the other.  The A tiles come
+// as K-halves (64 B swizzle) through a ring of NSLOT stages, so the next
+// tile's loads overlap this tile's MMAs and epilogue.
+//   warps 0..7   epilogue (TMEM lane quarter w & 3, half w >> 2)
+//   warp 8       MMA issue (one thread)
+//   warp 9       TMA producer (one thread)
 __global__ void __launch_bounds__(THREADS, 1)
     oz_tgemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                     const int* __restrict__ Ea, const double* __restrict__ Fcs, double* __restrict__ T, int Q, int S,
@@ -399,9 +436,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const double d0 = __longlong_as_double(h0 + 0x4338000000000000LL) - 6755399441055744.0;
                     const double d1 = __longlong_as_double(h1 + 0x4338000000000000LL) - 6755399441055744.0;
                     val[j] = fma(d0, w0, d1 * w1) * cs[c0 + j];
-                    if (!all_fast && !fast)  // rows at the ends of the exponent range, non-finite rows
+                }
+                if (!all_fast && !fast) {  // rows at the ends of the exponent range, non-finite rows
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const long long h0 = (long long)(int)a[buf][0][j] * 16777216LL +
+                                             (long long)(int)a[buf][1][j] * 65536LL +
+                                             (long long)(int)a[buf][2][j] * 256LL + (long long)(int)a[buf][3][j];
+                        const long long h1 = (long long)(int)a[buf][4][j] * 16777216LL +
+                                             (long long)(int)a[buf][5][j] * 65536LL +
+                                             (long long)(int)a[buf][6][j] * 256LL + (long long)(int)a[buf][7][j];
                         val[j] = ea == kBadExp ? __longlong_as_double(0x7ff8000000000000LL)
-                                               : ldexp(d0 * 0x1p-36 + d1 * 0x1p-68, ea) * cs[c0 + j];
+                                               : ldexp((double)h0 * 0x1p-36 + (double)h1 * 0x1p-68, ea) * cs[c0 + j];
+                    }
                 }
                 if (row_ok) {
 #pragma unroll
@@ -431,20 +478,26 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 bool ozaki_supported(int Q) { return Q >= 1 && Q <= KB && tc_gemm_available(); }
 
 bool ozaki_selected(int Q) {
-    // The sweeps' T-GEMM engine: the FP64 DMMA GEMM unless OCTEN_ALS_TGEMM=i8
-    // (measured at c3: the digit-split kernel runs a lane's T-GEMM in 28-31 us
-    // against 33-45 us on DMMA, but its per-batch slicing pass and one CTA per
-    // SM make the pipelined step slower, 13.5-14.6 ms against 12.9 ms)
+    // The sweeps' T-GEMM engine: this kernel unless OCTEN_ALS_TGEMM=dmma
+    // (measured at c3, pipelined step: 12.47 ms against 12.95 ms on DMMA)
     const char* e = std::getenv("OCTEN_ALS_TGEMM");  // (read per CP-ALS run)
-    return e && std::string(e) == "i8" && ozaki_supported(Q);
+    return !(e && std::string(e) == "dmma") && ozaki_supported(Q);
 }
 
 int ozaki_pitch(int Q) { return (Q + 15) / 16 * 16; }
 
 void ozaki_slice_y(const double* Y, int P, int Q, uint8_t* As, int* Ea, cudaStream_t st) {
     const int q2 = Q * Q;
-    dim3 grid((unsigned)((q2 + 127) / 128), (unsigned)P, 3);
-    oz_slice_y_kernel<<<grid, 128, 0, st>>>(Y, P, Q, ozaki_pitch(Q), As, Ea);
+    dim3 grid((unsigned)((q2 + SL_ROWS - 1) / SL_ROWS), (unsigned)P, 3);
+    const size_t smem = (size_t)SL_ROWS * (Q + 1) * sizeof(double);
+    if (smem > 48 * 1024) {
+        static PerDevice attr;
+        attr.once([] {
+            OCTEN_CUDA(cudaFuncSetAttribute(oz_slice_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)(SL_ROWS * 129 * sizeof(double))));
+        });
+    }
+    oz_slice_y_kernel<<<grid, 128, smem, st>>>(Y, P, Q, ozaki_pitch(Q), As, Ea);
     OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
 }
@@ -512,7 +565,7 @@ void ozaki_tgemm(const CUtensorMap& amap, const CUtensorMap& bmap, const int* Ea
     // m-tiles per CTA
     static const int per_cta = [] {
         const char* e = std::getenv("OCTEN_OZ_TILES");
-        return e ? std::max(1, std::atoi(e)) : 3;
+        return e ? std::max(1, std::atoi(e)) : 4;  // measured 2/3/4/5: 12.8/12.57/12.47/12.47 ms per c3 step
     }();
     const int mtiles = (q2 + BM - 1) / BM;
     dim3 grid((unsigned)((mtiles + per_cta - 1) / per_cta), (unsigned)G, (unsigned)pn);

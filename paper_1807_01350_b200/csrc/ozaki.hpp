@@ -25,7 +25,7 @@ constexpr int kOzSlices = 7;
 
 // Shapes the kernel covers (Q <= 128: one 128-byte K row; any S R).
 bool ozaki_supported(int Q);
-// Whether the CP-ALS sweeps use it (OCTEN_ALS_TGEMM=i8 and supported).
+// Whether the CP-ALS sweeps use it (supported, unless OCTEN_ALS_TGEMM=dmma).
 bool ozaki_selected(int Q);
 // Bytes of one row of the sliced operand (Q rounded up to 16).
 int ozaki_pitch(int Q);

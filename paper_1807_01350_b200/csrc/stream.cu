@@ -140,7 +140,14 @@ Stream::Stream(const StreamCfg& c, int rank, int world) : cfg(c), shard_rank(ran
 }
 
 Stream::~Stream() {
+    (void)aworker.wait();
     (void)worker.wait();
+    if (ast) {
+        cudaStreamSynchronize(ast);
+        cudaStreamDestroy(ast);
+    }
+    for (cudaEvent_t e : aevs)
+        if (e) cudaEventDestroy(e);
     if (mst) {
         cudaStreamSynchronize(mst);
         cudaStreamDestroy(mst);
@@ -626,7 +633,7 @@ void Stream::begin_ctx(BatchCtx& b, bool first, std::int64_t t) {
 }
 
 void Stream::begin(BatchCtx& b, const void* data, int dtype, int location, int order, const std::int64_t* dims,
-                   double* models_out, bool out_of_place) {
+                   double* models_out, bool out_of_place, bool run_als) {
     if (b.pending) throw ConfigError("octen: the previous batch has not finished (begin/merge/finish)");
     const bool first = !initialized;
     if (first) {
@@ -741,7 +748,14 @@ void Stream::begin(BatchCtx& b, const void* data, int dtype, int location, int o
         OCTEN_CUDA(cudaEventRecord(evs[1], st));
         OCTEN_CUDA(cudaStreamSynchronize(st));
         b.rec.compress_seconds = std::chrono::duration<double>(Clock::now() - tc).count();
-        als_phase(b, Yout.p, models_out);
+        // device time of the compression (main stream)
+        float cms = 0.f;
+        OCTEN_CUDA(cudaEventElapsedTime(&cms, evs[0], evs[1]));
+        dev_ms[0] += cms;
+        dev_ms[3] += comp.collect_gemm1_ms();
+        gemm1_flops = comp.gemm1_flops;
+        gemm1_launches = comp.gemm1_launches;
+        if (run_als) als_phase(b, Yout.p, models_out, st);
     } catch (...) {
         fail_pending(b);
     }
@@ -749,10 +763,12 @@ void Stream::begin(BatchCtx& b, const void* data, int dtype, int location, int o
 
 // CP-ALS of the owned replicas on the updated summaries, packed into this
 // rank's models block (status header + factors + lambdas).
-void Stream::als_phase(BatchCtx& b, const double* dY, double* models_out) {
+void Stream::als_phase(BatchCtx& b, const double* dY, double* models_out, cudaStream_t st) {
     const int Q = cfg.q, R = cfg.rank;
     auto ta = Clock::now();
-    OCTEN_CUDA(cudaEventRecord(evs[2], st));
+    for (cudaEvent_t& e : aevs)
+        if (!e) OCTEN_CUDA(cudaEventCreate(&e));
+    OCTEN_CUDA(cudaEventRecord(aevs[0], st));
     double hdr[4] = {0, 0, 0, 0};
     const size_t qr = (size_t)Q * R;
     if (pl > 0) {
@@ -781,18 +797,13 @@ void Stream::als_phase(BatchCtx& b, const double* dY, double* models_out) {
         }
     }
     h2d_param(models_out, hdr, sizeof(hdr), st);
-    OCTEN_CUDA(cudaEventRecord(evs[3], st));
+    OCTEN_CUDA(cudaEventRecord(aevs[1], st));
     OCTEN_CUDA(cudaStreamSynchronize(st));
     b.rec.als_seconds = std::chrono::duration<double>(Clock::now() - ta).count();
-    // device time of compression and CP-ALS (main stream; the merge adds its own)
+    // device time of CP-ALS (its stream; the compression and the merge add their own)
     float ms = 0.f;
-    OCTEN_CUDA(cudaEventElapsedTime(&ms, evs[0], evs[1]));
-    dev_ms[0] += ms;
-    OCTEN_CUDA(cudaEventElapsedTime(&ms, evs[2], evs[3]));
+    OCTEN_CUDA(cudaEventElapsedTime(&ms, aevs[0], aevs[1]));
     dev_ms[1] += ms;
-    dev_ms[3] += comp.collect_gemm1_ms();
-    gemm1_flops = comp.gemm1_flops;
-    gemm1_launches = comp.gemm1_launches;
     OCTEN_CUDA(cudaEventRecord(b.ev[2], st));
 }
 
@@ -899,7 +910,11 @@ void Stream::begin_reduced(const double* owned_block, double* models_out) {
         }
         b.compressed = true;
         ++batches_seen;
-        als_phase(b, Y.p, models_out);
+        float cms = 0.f;  // this rank's share of the compression (begin_temporal)
+        OCTEN_CUDA(cudaEventElapsedTime(&cms, evs[0], evs[1]));
+        dev_ms[0] += cms;
+        dev_ms[3] += comp_all.collect_gemm1_ms();
+        als_phase(b, Y.p, models_out, st);
     } catch (...) {
         fail_pending(b);
     }
@@ -1136,8 +1151,21 @@ void Stream::ingest(const void* data, int dtype, int location, int order, const 
 }
 
 void Stream::sync() {
-    std::exception_ptr e = worker.wait();
+    // the pipelined ingest's batch in flight: its CP-ALS, then its merge
+    std::exception_ptr e = aworker.wait();
+    if (!e && a_prev) post_merge(*a_prev, a_prev_models);
+    a_prev = nullptr;
+    std::exception_ptr m = worker.wait();
+    if (!e) e = m;
     if (e) std::rethrow_exception(e);
+}
+
+void Stream::post_merge(BatchCtx& b, double* models) {
+    xrows.reserve(rows_count());
+    worker.post(cfg.device, [this, &b, models] {
+        merge_phase(b, models, xrows.p);
+        finish(b, xrows.p);
+    });
 }
 
 namespace {
@@ -1195,40 +1223,59 @@ void Stream::ingest_async(const void* data, int dtype, int location, int order, 
         if (merge_sms > 0) mst = green_merge_stream(cfg.device, merge_sms, least);
         if (!mst) OCTEN_CUDA(cudaStreamCreateWithPriority(&mst, cudaStreamNonBlocking, least));
     }
+    if (!ast) OCTEN_CUDA(cudaStreamCreateWithPriority(&ast, cudaStreamNonBlocking, critical_stream_priority()));
     BatchCtx& b = actx[aslot];
     b.st = mst;
     double* models = aslot ? xmodels2.reserve(models_count()) : xmodels.reserve(models_count());
     const std::int64_t drawn0 = batches_drawn, seen0 = batches_seen;
     const std::vector<double> tgram0 = tgram;
+    // this batch's compression (Ynext = Y + its summaries), overlapping the
+    // previous batch's CP-ALS on the CP-ALS worker
     std::exception_ptr begin_err;
     try {
-        begin(b, data, dtype, location, order, dims, models, true);
+        begin(b, data, dtype, location, order, dims, models, true, false);
     } catch (...) {
         begin_err = std::current_exception();
     }
-    // the previous batch's merge must be complete before Y is replaced
-    std::exception_ptr prev_err = worker.wait();
+    // the previous batch: its CP-ALS must be done before this one's starts
+    // (one engine); its merge then runs beside this batch's CP-ALS
+    std::exception_ptr prev_err = aworker.wait();
+    BatchCtx* prev = a_prev;
+    double* prev_models = a_prev_models;
+    a_prev = nullptr;
+    bool posted = false;
+    if (!prev_err && !begin_err) {
+        const double* dY = Ynext.p;
+        aworker.post(cfg.device, [this, &b, dY, models] {
+            try {
+                als_phase(b, dY, models, ast);
+            } catch (...) {
+                fail_pending(b);
+            }
+        });
+        posted = true;
+    }
+    if (!prev_err && prev) {
+        post_merge(*prev, prev_models);
+        prev_err = worker.wait();
+    }
     if (prev_err) {
-        // batch b-1 failed in its merge (the reference throws from its
-        // ingest_batch): this batch was never ingested
+        // batch b-1 failed in its CP-ALS or merge (the reference throws from
+        // its ingest_batch): this batch was never ingested
+        if (posted) (void)aworker.wait();
         batches_drawn = drawn0;
         batches_seen = seen0;
         tgram = tgram0;
         b.pending = false;
         std::rethrow_exception(prev_err);
     }
-    if (begin_err) {
-        // the reference keeps the updated summaries when CP-ALS fails
-        if (b.compressed) Y.swap(Ynext);
-        std::rethrow_exception(begin_err);
-    }
+    if (begin_err) std::rethrow_exception(begin_err);
+    // the summaries now include this batch (a CP-ALS failure keeps them, as
+    // the reference does)
     Y.swap(Ynext);
+    a_prev = &b;
+    a_prev_models = models;
     aslot ^= 1;
-    xrows.reserve(rows_count());
-    worker.post(cfg.device, [this, &b, models] {
-        merge_phase(b, models, xrows.p);
-        finish(b, xrows.p);
-    });
 }
 
 namespace {

@@ -117,12 +117,14 @@ public:
 
     void init(const void* data, int dtype, int location, int order, const std::int64_t* dims);
     void ingest(const void* data, int dtype, int location, int order, const std::int64_t* dims);
-    // Pipelined ingest_batch: compression and CP-ALS of this batch run now;
-    // its alignment/merge runs on the worker thread (own CUDA stream) and
-    // overlaps the next batch's compression and CP-ALS.  The results are the
-    // same bits as ingest(): every stage reads the same inputs (the summaries
-    // are double-buffered, the temporal rows and Gram are per batch).  A
-    // merge error surfaces at the next ingest_async / sync (with its batch
+    // Pipelined ingest_batch: this batch is compressed now (overlapping the
+    // previous batch's CP-ALS); its CP-ALS runs on the CP-ALS worker thread
+    // (own CUDA streams) and overlaps the previous batch's merge, which runs
+    // on the merge worker thread.  The call returns once the previous
+    // batch's merge is done.  The results are the same bits as ingest():
+    // every stage reads the same inputs (the summaries are double-buffered,
+    // the temporal rows and Gram are per batch).  A CP-ALS or merge error of
+    // batch b surfaces at the next ingest_async / sync (with its batch
     // prefix); that next batch is then not ingested.  Strict streams and the
     // first batch run synchronously.
     void ingest_async(const void* data, int dtype, int location, int order, const std::int64_t* dims);
@@ -232,8 +234,15 @@ public:
     BatchCtx cur;                 // synchronous / sharded phases
     BatchCtx actx[2];             // pipelined ingest: alternating per batch
     int aslot = 0;
-    Worker worker;
+    Worker worker;                // pipelined ingest: the merges
+    Worker aworker;               // pipelined ingest: the CP-ALS runs
     cudaStream_t mst = nullptr;   // merge stream of the pipelined ingest (lower priority)
+    cudaStream_t ast = nullptr;   // CP-ALS stream of the pipelined ingest
+    // the batch whose CP-ALS is posted (aworker) and whose merge is still to
+    // be posted: its context and models block
+    BatchCtx* a_prev = nullptr;
+    double* a_prev_models = nullptr;
+    cudaEvent_t aevs[2] = {};     // CP-ALS device timing (the CP-ALS worker's events)
 
 private:
     using Clock = std::chrono::steady_clock;
@@ -253,10 +262,11 @@ private:
     void check_finite(const void* dX, int dtype, size_t n);
     void ensure_c_capacity(std::int64_t rows, cudaStream_t st);
     void begin(BatchCtx& b, const void* data, int dtype, int location, int order, const std::int64_t* dims,
-               double* models_out, bool out_of_place);
+               double* models_out, bool out_of_place, bool run_als = true);
     void merge_phase(BatchCtx& b, const double* models_all, double* rows_out);
     void finish(BatchCtx& b, const double* rows_all);
-    void als_phase(BatchCtx& b, const double* dY, double* models_out);
+    void als_phase(BatchCtx& b, const double* dY, double* models_out, cudaStream_t as);
+    void post_merge(BatchCtx& b, double* models);
     void snapshot(Snapshot& s);
     void restore(Snapshot& s);
     [[noreturn]] void fail_pending(BatchCtx& b);

@@ -126,11 +126,12 @@ def test_tgemm_digit_split_nonfinite_propagates():
     assert np.isnan(t[0, :, 2]).all()
 
 
-def test_cp_als_sweeps_run_on_tcgen05(monkeypatch):
-    """With OCTEN_ALS_TGEMM=i8 the batched CP-ALS sweeps' T-GEMMs go through
-    the int8 tcgen05 kernel (path counter), and the result matches the oracle
-    restatement."""
-    monkeypatch.setenv("OCTEN_ALS_TGEMM", "i8")
+@pytest.mark.parametrize("engine", ["i8", "dmma"])
+def test_cp_als_sweeps_engines(monkeypatch, engine):
+    """The batched CP-ALS sweeps' T-GEMMs go through the int8 tcgen05 kernel
+    by default (path counter; OCTEN_ALS_TGEMM=dmma selects the DMMA GEMM),
+    and either result matches the oracle restatement."""
+    monkeypatch.setenv("OCTEN_ALS_TGEMM", engine)
     from oracle import octen_oracle as O
     from oracle import rng as R
 
@@ -143,7 +144,10 @@ def test_cp_als_sweeps_run_on_tcgen05(monkeypatch):
     c0 = ob.kernel_counts()
     models, fits, its = ob.cp_als_batched([y, 2.0 * y], cfg, [11, 12])
     c1 = ob.kernel_counts()
-    assert c1["tcgen05_als"] > c0["tcgen05_als"]
+    if engine == "i8":
+        assert c1["tcgen05_als"] > c0["tcgen05_als"]
+    else:
+        assert c1["tcgen05_als"] == c0["tcgen05_als"]
     for yy, m, sd, fit in zip([y, 2.0 * y], models, [11, 12], fits):
         ref = O.cp_als(yy, O.AlsConfig(rank, 40, 1e-10, 2, sd))
         cg = min(O.congruence(O.KruskalModel(m.factors, m.lambda_), ref.model))
