@@ -58,14 +58,16 @@ def peaks():
 def pipe_peaks():
     """Measured arithmetic peaks of the pipes the path uses
     (scripts/micro/peaks.cu on this pool's B200, profiles/peaks_b200.json):
-    tcgen05 kind::tf32, DMMA fp64, FFMA fp32."""
+    tcgen05 kind::tf32 and kind::i8 (scripts/micro/i8_rate.cu), DMMA fp64,
+    FFMA fp32."""
     try:
         with open(os.path.join(ROOT, "profiles", "peaks_b200.json")) as f:
             d = json.load(f)
         return {"tf32": float(d["tcgen05_tf32_tflops"]), "dmma": float(d["dmma_f64_tflops"]),
-                "ffma": float(d["ffma_f32_tflops"]), "source": "measured (profiles/peaks_b200.json)"}
+                "ffma": float(d["ffma_f32_tflops"]), "i8": float(d.get("tcgen05_i8_tops", 4500.0)),
+                "source": "measured (profiles/peaks_b200.json)"}
     except Exception:
-        return {"tf32": 1100.0, "dmma": 37.0, "ffma": 72.0, "source": "nominal (peaks file missing)"}
+        return {"tf32": 1100.0, "dmma": 37.0, "ffma": 72.0, "i8": 4500.0, "source": "nominal (peaks file missing)"}
 
 
 def ref_backend():
@@ -847,14 +849,31 @@ def main():
     if kd and kd["gemm_launches"] > 0:
         gms = kd["gemm_ms"] / kd["gemm_launches"]
         gfl = kd["gemm_flops"] / kd["gemm_launches"]
-        rooflines["als_tgemm"] = {
-            "kernel": "gemm_dmma_pipe_kernel (CP-ALS partial contractions T = Y x_n F, all restarts of a lane's "
-                      "replicas)", "bound": "FP64 tensor (DMMA)", "achieved": gfl / (gms * 1e-3) / 1e12,
-            "peak": pk["dmma"], "unit": "TFLOP/s", "frac": gfl / (gms * 1e-3) / 1e12 / pk["dmma"],
-            "flops_per_launch": gfl, "ms_per_launch": gms, "sampled_launches": kd["gemm_launches"],
-            "peak_source": pk["source"],
-            "note": "duration from CUDA events on the launching lane stream (sampled: lane 0, every fifth sweep) "
-                    "while the other lanes and the pipelined merge share the GPU"}
+        live_note = ("duration from CUDA events on the launching lane stream (sampled: lane 0, every fifth sweep) "
+                     "while the other lanes, the next batch's compression and the pipelined merge share the GPU")
+        if os.environ.get("OCTEN_ALS_TGEMM") == "dmma" or Q > 128:
+            rooflines["als_tgemm"] = {
+                "kernel": "gemm_dmma_pipe_kernel (CP-ALS partial contractions T = Y x_n F, all restarts of a lane's "
+                          "replicas)", "bound": "FP64 tensor (DMMA)", "achieved": gfl / (gms * 1e-3) / 1e12,
+                "peak": pk["dmma"], "unit": "TFLOP/s", "frac": gfl / (gms * 1e-3) / 1e12 / pk["dmma"],
+                "flops_per_launch": gfl, "ms_per_launch": gms, "sampled_launches": kd["gemm_launches"],
+                "peak_source": pk["source"], "note": live_note}
+        else:
+            # issued int8 tensor work of one lane launch (csrc/ozaki.cu): per
+            # 128-row tile and 64-column group, 34 slice pairs (i + j <= 9, i, j
+            # <= 7) x 64 columns x 128 rows x 32 ceil(Q / 32) K bytes
+            lane_p = P / 4.0
+            tiles = lane_p * -(-Q * Q // 128) * -(-(cfg["restarts"] * R) // 64)
+            iops = 2.0 * 34 * 64 * 128 * 32 * -(-Q // 32) * tiles
+            rooflines["als_tgemm"] = {
+                "kernel": "oz_tgemm_kernel (CP-ALS partial contractions T = Y x_n F in fp64 on the int8 tensor cores "
+                          "by exact digit splitting, all restarts of a lane's replicas; csrc/ozaki.cu)",
+                "bound": "tensor (tcgen05 kind::i8)", "achieved": iops / (gms * 1e-3) / 1e12, "peak": pk["i8"],
+                "unit": "TOP/s", "frac": iops / (gms * 1e-3) / 1e12 / pk["i8"], "issued_ops_per_launch": iops,
+                "fp64_flops_per_launch": gfl, "fp64_equiv_tflops": gfl / (gms * 1e-3) / 1e12,
+                "fp64_equiv_frac_of_dmma_peak": gfl / (gms * 1e-3) / 1e12 / pk["dmma"],
+                "ms_per_launch": gms, "sampled_launches": kd["gemm_launches"], "peak_source": pk["source"],
+                "note": live_note}
     if kd and kd["mttkrp_launches"] > 0:
         mms = kd["mttkrp_ms"] / kd["mttkrp_launches"]
         mby = kd["mttkrp_bytes"] / kd["mttkrp_launches"]
@@ -867,7 +886,8 @@ def main():
     if kd and kd["sweeps"] > 0:
         # every sweep: 1.5 T-GEMMs of 2 Q^3 S R flops per replica
         als_flops = kd["sweeps"] / args.steps * 1.5 * 2.0 * Q ** 3 * cfg["restarts"] * R * P
-        rooflines["als_stage"] = {"bound": "FP64 tensor (DMMA)", "achieved": als_flops / (dt[1] / args.steps * 1e-3) / 1e12,
+        rooflines["als_stage"] = {"bound": "FP64 (fp64 T-GEMM flops vs the DMMA peak)",
+                                  "achieved": als_flops / (dt[1] / args.steps * 1e-3) / 1e12,
                                   "peak": pk["dmma"], "unit": "TFLOP/s",
                                   "frac": als_flops / (dt[1] / args.steps * 1e-3) / 1e12 / pk["dmma"],
                                   "flops_per_step": als_flops, "sweeps_per_step": kd["sweeps"] / args.steps,
