@@ -1268,9 +1268,27 @@ AlsEngine::~AlsEngine() {
         if (e) cudaEventDestroy(e);
 }
 
+namespace {
+// What run_init hands to run_sweeps.
+struct AlsPending {
+    AlsDev d;
+    int P, S, Q, R, max_iters;
+    double rel_tol;
+    const double* dY;
+    std::vector<int> used;  // GEVD attempt per problem (-1: random start)
+};
+}  // namespace
+
 void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, const double* dY,
                     const std::vector<std::uint64_t>& seeds, cudaStream_t st) {
+    run_init(P, S, Q, R, max_iters, rel_tol, dY, seeds, st);
+    run_sweeps(st);
+}
+
+void AlsEngine::run_init(int P, int S, int Q, int R, int max_iters, double rel_tol, const double* dY,
+                         const std::vector<std::uint64_t>& seeds, cudaStream_t st) {
     failure = {};
+    pend.reset();
     if (R < 1) throw ConfigError("cp_als: rank must be >= 1");
     if (max_iters < 1) throw ConfigError("cp_als: max_iters must be >= 1");
     if (!(rel_tol > 0.0)) throw ConfigError("cp_als: rel_tol must be > 0");
@@ -1517,6 +1535,22 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
     als_init_state_kernel<<<NP, 128, 0, st>>>(d); OCTEN_LAUNCHED(1);
     OCTEN_CUDA(cudaGetLastError());
     OCTEN_PROF("init", st);
+    pend = std::make_shared<AlsPending>(AlsPending{d, P, S, Q, R, max_iters, rel_tol, dY, used});
+}
+
+// The sweeps of the run prepared by run_init (on `st`, which must be ordered
+// after run_init's stream), best restart selection and the results.
+void AlsEngine::run_sweeps(cudaStream_t st) {
+    if (!pend) throw ConfigError("octen: CP-ALS sweeps without an initialised run");
+    const AlsPending pd = *static_cast<const AlsPending*>(pend.get());
+    pend.reset();
+    AlsDev d = pd.d;
+    const int P = pd.P, S = pd.S, Q = pd.Q, R = pd.R, max_iters = pd.max_iters;
+    const double rel_tol = pd.rel_tol;
+    const double* dY = pd.dY;
+    (void)rel_tol;
+    const int NP = P * S;
+    const size_t q2 = (size_t)Q * Q, q3 = q2 * Q;
 
     // ---- sweeps
     const int SR = S * R;
@@ -1937,7 +1971,7 @@ void AlsEngine::run(int P, int S, int Q, int R, int max_iters, double rel_tol, c
         r.restart = hb[p];
         r.iterations = hs[prob].iterations;
         r.rescued = hs[prob].rescued != 0;
-        r.gevd_attempt = used[prob];
+        r.gevd_attempt = pd.used[prob];
         r.fit_history.assign(fh + (size_t)prob * max_iters, fh + (size_t)prob * max_iters + r.iterations);
         r.residual_history.assign(rh + (size_t)prob * max_iters, rh + (size_t)prob * max_iters + r.iterations);
         r.fit = r.fit_history.empty() ? -INFINITY : r.fit_history.back();

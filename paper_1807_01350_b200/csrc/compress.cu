@@ -140,7 +140,12 @@ void run_project(CompressEngine& e, const T* dX, std::int64_t t, T* Z1, T* Z2, c
         const long long N1 = e.J * tc;
         const T* Xc = dX + (size_t)e.I * e.J * k0;
         if (ready) OCTEN_CUDA(cudaStreamWaitEvent(st, ready[ci], 0));
-        if (flag) {
+        // the non-finite scan: fused into the tcgen05 GEMM1's conversion
+        // warps when it runs, else a separate pass
+        bool scanned = false;
+        auto scan = [&] {
+            if (!flag || scanned) return;
+            scanned = true;
             const size_t n = (size_t)e.I * e.J * tc;
             size_t blocks = (n + 255) / 256;
             if (blocks > 148 * 8) blocks = 148 * 8;
@@ -149,7 +154,7 @@ void run_project(CompressEngine& e, const T* dX, std::int64_t t, T* Z1, T* Z2, c
             else
                 nonfinite_chunk_kernel<<<(int)blocks, 256, 0, st>>>(nullptr, Xc, n, flag);
             OCTEN_LAUNCHED(1);
-        }
+        };
         bool done = false;
         OCTEN_CUDA(cudaEventRecord(e.event(2 * e.g1_used), st));
         if constexpr (std::is_same<T, float>::value) {
@@ -162,7 +167,8 @@ void run_project(CompressEngine& e, const T* dX, std::int64_t t, T* Z1, T* Z2, c
                                         "(sm_100a required; set OCTEN_ALLOW_SIMT=1 to run the SIMT GEMMs)");
                 } else {
                     done = tc_gemm_tf32x3(e.Ahi.p, e.Alo.p, e.lda_tc, Xc, Z1, (int)e.Meff, (long long)N1, (int)e.I,
-                                          st, P, Q, e.shared);
+                                          st, P, Q, e.shared, flag);
+                    if (done) scanned = true;
                     if (done)
                         path_counter(kTcgen05Launches).fetch_add(1);
                     else
@@ -172,6 +178,7 @@ void run_project(CompressEngine& e, const T* dX, std::int64_t t, T* Z1, T* Z2, c
             e.used_tc = done;
         }
         if (!done) {
+            scan();
             if constexpr (std::is_same<T, double>::value) {
                 gemm_f64<true, true>(1, (int)e.Meff, (int)N1, (int)e.I, G1A<T>{A, e.I}, G1B<T>{Xc, e.I},
                                      G1C<T>{Z1, N1}, st);

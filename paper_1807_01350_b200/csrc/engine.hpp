@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <string>
 #include <future>
+#include <memory>
 #include <vector>
 
 #include "devbuf.hpp"
@@ -69,6 +70,13 @@ public:
     // Y: P x Q^3 device summaries.  seeds: per replica AlsConfig.seed.
     void run(int P, int S, int Q, int R, int max_iters, double rel_tol, const double* dY,
              const std::vector<std::uint64_t>& seeds, cudaStream_t st);
+    // run() in two parts: the start (norms, GEVD attempts, initial factors;
+    // host syncs on `st`) and the sweeps with the results (on a stream
+    // ordered after the start).  The pipelined ingest runs the next batch's
+    // start on another engine while this one sweeps.
+    void run_init(int P, int S, int Q, int R, int max_iters, double rel_tol, const double* dY,
+                  const std::vector<std::uint64_t>& seeds, cudaStream_t st);
+    void run_sweeps(cudaStream_t st);
     // Draw the host RNG of a later run() with these seeds now (helper thread).
     void prefetch_host_draws(const std::vector<std::uint64_t>& seeds, int S, int Q);
 
@@ -121,6 +129,7 @@ private:
     DevBuf<Mt64> rngs;
     DevBuf<std::uint64_t> rescue_seed;
     std::future<AlsHostDraws> next_draws;
+    std::shared_ptr<void> pend;  // run_init -> run_sweeps (als.cu)
     unsigned char* res_pin = nullptr;  // pinned landing area of run()'s results (one read)
     size_t res_cap = 0;
 };

@@ -392,10 +392,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         double* Tp = T + (size_t)p * q2 * SR + (size_t)q2 * (n0 + h * NH);
         const double* cs = sCs + h * NH;
         int it = 0;
+        // the row exponent of the next tile is loaded one tile ahead
+        int ea_next = (int)blockIdx.x * BM + r < q2 ? __ldg(Ea + (size_t)p * q2 + blockIdx.x * BM + r) : 0;
 #pragma unroll 1
         for (int mt = blockIdx.x; mt < mtiles; mt += cpg, ++it) {
             const int m = mt * BM + r;
-            const int ea = m < q2 ? __ldg(Ea + (size_t)p * q2 + m) : 0;
+            const int ea = ea_next;
+            if (mt + cpg < mtiles)
+                ea_next = m + cpg * BM < q2 ? __ldg(Ea + (size_t)p * q2 + m + cpg * BM) : 0;
             // row weights: the two Horner groups weigh 2^(ea - 36), 2^(ea - 68)
             const bool fast = ea >= -1022 + 68 && ea <= 1023 + 36;  // (false for kBadExp)
             const double w0 = fast ? pow2i(ea - 36) : 0.0;
@@ -451,9 +455,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                 }
                 if (row_ok) {
+                    double* o = trow_out + (size_t)q2 * c0;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        if (c0 + j < ncol) trow_out[(size_t)q2 * (c0 + j)] = val[j];
+                    for (int j = 0; j < 8; ++j) {
+                        if (c0 + j < ncol) *o = val[j];
+                        o += q2;
+                    }
                 }
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             }

@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(G1P_THREADS, 1)
                                      const __grid_constant__ CUtensorMap map_alo,
                                      const __grid_constant__ CUtensorMap map_x, float* __restrict__ Z, int M,
                                      long long N, int K, long long ldz, int scP, int scQ, int scSh, int mt,
-                                     long long ntiles, int two_mma) {
+                                     long long ntiles, int two_mma, int* __restrict__ nonfinite) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full_bar = (uint64_t*)(smem + STAGES * STAGE_BYTES);
@@ -413,9 +413,12 @@ __global__ void __launch_bounds__(G1P_THREADS, 1)
             }
         }
     } else if (warp < G1P_EPI_WARP0) {
-        // ---- X hi/lo split (warps 2..7) ----
+        // ---- X hi/lo split (warps 2..7); with `nonfinite` the batch's
+        // non-finite scan rides along (every X element passes through here) ----
         const int ct = threadIdx.x - CONVERT_WARP0 * 32;
         uint32_t it = 0;
+        uint32_t bad = 0;
+        auto nf = [](float f) { return (__float_as_uint(f) & 0x7f800000u) == 0x7f800000u ? 1u : 0u; };
         for (long long L = blockIdx.x; L < ntiles; L += gridDim.x) {
             for (int kb = 0; kb < num_kb; ++kb, ++it) {
                 const int s = it % STAGES;
@@ -430,6 +433,7 @@ __global__ void __launch_bounds__(G1P_THREADS, 1)
                     // magnitude bits
                     for (int i = ct; i < B_BYTES / 16; i += CONVERT_WARPS * 32) {
                         const float4 v = bx[i];
+                        bad |= nf(v.x) | nf(v.y) | nf(v.z) | nf(v.w);
                         float4 h;
                         h.x = __uint_as_float((__float_as_uint(v.x) + 0x1000u) & 0xFFFFE000u);
                         h.y = __uint_as_float((__float_as_uint(v.y) + 0x1000u) & 0xFFFFE000u);
@@ -440,6 +444,7 @@ __global__ void __launch_bounds__(G1P_THREADS, 1)
                 } else {
                     for (int i = ct; i < B_BYTES / 16; i += CONVERT_WARPS * 32) {
                         const float4 v = bx[i];
+                        bad |= nf(v.x) | nf(v.y) | nf(v.z) | nf(v.w);
                         float4 l;
                         l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
                         l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
@@ -452,6 +457,7 @@ __global__ void __launch_bounds__(G1P_THREADS, 1)
                 mbar_arrive(&conv_bar[s]);
             }
         }
+        if (nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(nonfinite, 1);
     } else {
         // ---- epilogue (warps 8..11) ----
         const int q = warp & 3;
@@ -748,7 +754,7 @@ bool tc_gemm_available() {
 }
 
 bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X, float* Z, int M, long long N, int K,
-                    cudaStream_t st, int scatter_p, int scatter_q, int scatter_sh) {
+                    cudaStream_t st, int scatter_p, int scatter_q, int scatter_sh, int* nonfinite) {
     if (!tc_gemm_available()) return false;
     if ((K % 4) != 0 || (lda % 4) != 0 || ((uintptr_t)X % 16) != 0 || ((uintptr_t)Ahi % 16) != 0 ||
         ((uintptr_t)Alo % 16) != 0 || N > (1LL << 31) - 1 || M <= 0 || N <= 0 || K <= 0)
@@ -781,7 +787,7 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
         // A_hi X_lo + A_lo X_hi split
         static const int two_mma = std::getenv("OCTEN_G1_3MMA") ? 0 : 1;
         tc_gemm_tf32x3_persistent_kernel<<<grid, G1P_THREADS, smem + G1P_EPI_BYTES, st>>>(
-            mhi, mlo, mx, Z, M, N, K, N, scatter_p, scatter_q, scatter_sh, mt, ntiles, two_mma);
+            mhi, mlo, mx, Z, M, N, K, N, scatter_p, scatter_q, scatter_sh, mt, ntiles, two_mma, nonfinite);
         OCTEN_LAUNCHED(1);
         OCTEN_CUDA(cudaGetLastError());
         return true;
@@ -790,7 +796,7 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
     attr.once([&] {
         OCTEN_CUDA(cudaFuncSetAttribute(tc_gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     });
-    if ((N + BN - 1) / BN > 65535) return false;
+    if ((N + BN - 1) / BN > 65535 || nonfinite) return false;  // (diagnostics path: no fused scan)
     dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
     tc_gemm_tf32x3_kernel<<<grid, NUM_THREADS, smem, st>>>(mhi, mlo, mx, Z, M, N, K, N, scatter_p, scatter_q,
                                                            scatter_sh);

@@ -18,8 +18,10 @@ void* tc_tensor_map_encoder();
 // scatter_p > 0: output row m of the deduplicated stack is written to the
 // replica rows p * scatter_q + a (shared rows m < scatter_sh to every replica),
 // so Z is scatter_p * scatter_q x N.
+// nonfinite (optional): set to 1 when X holds a non-finite value (the
+// conversion warps check every element they pass).
 bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X, float* Z, int M, long long N, int K,
-                    cudaStream_t st, int scatter_p = 0, int scatter_q = 0, int scatter_sh = 0);
+                    cudaStream_t st, int scatter_p = 0, int scatter_q = 0, int scatter_sh = 0, int* nonfinite = nullptr);
 // Mode-2 contraction batched over (replica, slice):
 //   Z2[p * zstride + a + Q b + Q^2 k] = sum_j Z1[p Q + a][k J + j] V_p[j, b]
 // Z1: P*Q x N1 row-major (N1 = J * tc); Vhi/Vlo: TF32 hi/lo split of V,

@@ -113,13 +113,17 @@ def test_async_merge_error_reported_by_next_call(ob):
     _same_state(a, b)
 
 
-def test_async_non_finite_batch(ob):
-    x = _data([20, 18, 40], 2, 6, 0.0)
+@pytest.mark.parametrize("dtype,val,pos", [(np.float64, np.inf, (1, 2, 3)), (np.float32, np.nan, (5, 7, 9)),
+                                           (np.float32, -np.inf, (19, 17, 0))])
+def test_async_non_finite_batch(ob, dtype, val, pos):
+    """fp64 batches take the separate non-finite scan; fp32 batches are checked
+    by the tcgen05 GEMM1's conversion warps (every X element passes them)."""
+    x = _data([20, 18, 40], 2, 6, 0.0).astype(dtype)
     cfg = ob.StreamConfig(rank=2, p=6, q=6, shared=2, seed=5, als=ob.AlsConfig(rank=2, max_iters=40))
     a = ob.init_stream(np.asfortranarray(x[:, :, :10]), cfg)
     b = ob.init_stream(np.asfortranarray(x[:, :, :10]), cfg)
     bad = np.array(x[:, :, 20:30], order="F")
-    bad[1, 2, 3] = np.inf
+    bad[pos] = val
     ob.ingest_batch(a, np.asfortranarray(x[:, :, 10:20]))
     with pytest.raises(ob.NumericError, match=r"^batch 2: DenseTensor: non-finite value"):
         ob.ingest_batch(a, bad)
