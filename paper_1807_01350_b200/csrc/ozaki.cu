@@ -53,7 +53,10 @@ constexpr int KB = 128;             // bytes of K per row (K <= 128)
 constexpr int KH = 64;              // bytes of K per A stage (64 B swizzle)
 constexpr int A_SLICE = BM * KH;    // 8 KB: one digit slice of a K-half A tile
 constexpr int A_STAGE = NS * A_SLICE;  // 56 KB
-constexpr int NSLOT = 3;            // A stages in flight (ring)
+#ifndef OCTEN_OZ_NSLOT
+#define OCTEN_OZ_NSLOT 3
+#endif
+constexpr int NSLOT = OCTEN_OZ_NSLOT;  // A stages in flight (ring)
 constexpr int BH_SLICE = NH * KB;   // 4 KB
 constexpr int EPI_WARPS = 8;        // one per (TMEM lane quarter, half)
 constexpr int PW = EPI_WARPS;       // the MMA warp
