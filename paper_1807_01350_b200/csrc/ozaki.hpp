@@ -5,7 +5,7 @@
 // the dimension-tree partial T of als.cu) are formed as
 //     A(m, k) = 2^ea(m) sum_i a_i(m, k) 2^(2 - 8 i),  F(k, n) = 2^eb(n) sum_j b_j(k, n) 2^(2 - 8 j)
 // with balanced signed byte digits a_i, b_j in [-128, 127], i, j = 1..7:
-// the digits hold floor(x 2^(54 - e)) exactly, 54 bits of each row's
+// the digits hold rint(x 2^(54 - e)) exactly, 54 bits of each row's
 // (column's) largest value (fp64 has 53), and every digit product is summed
 // in int32 with no rounding at all.  The pairs with i + j <= 9 are kept (the
 // first dropped diagonal weighs 2^-76 of the scale product, per K term); the

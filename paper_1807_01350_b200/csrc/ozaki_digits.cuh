@@ -31,15 +31,15 @@ __device__ __forceinline__ void oz_scales(int e, double& s1, double& s2) {
     s1 = pow2i(h);
     s2 = pow2i(k - h);
 }
-// Balanced signed base-256 digits of N = floor(x 2^(54 - e)), |x| < 2^e so
-// |N| < 2^54: N = sum_i d_i 256^(7 - i), every d_i in [-128, 127] (the top
-// one in [-65, 64]), i.e. y = x 2^-e = sum_i d_i 2^(2 - 8 i).  With
-// M = N + 128 (1 + 256 + ... + 256^5) the low six bytes of M are d_i + 128
-// and M >> 48 is the top digit, so byte 7 - i of M ^ 0x808080808080 is d_i
-// (two's complement): one exact scaling, one floor conversion, two integer
-// operations.
+// Balanced signed base-256 digits of N = rint(x 2^(54 - e)), |x| < 2^e so
+// |N| <= 2^54: N = sum_i d_i 256^(7 - i), every d_i in [-128, 127] (the top
+// one in [-65, 65]), i.e. y = x 2^-e = sum_i d_i 2^(2 - 8 i) up to half a
+// unit of 2^-54 (round to nearest: no bias).  With M = N + 128 (1 + 256 +
+// ... + 256^5) the low six bytes of M are d_i + 128 and M >> 48 is the top
+// digit, so byte 7 - i of M ^ 0x808080808080 is d_i (two's complement): one
+// exact scaling, one rounding conversion, two integer operations.
 __device__ __forceinline__ unsigned long long oz_digits(double x, double s1, double s2) {
-    const long long n = __double2ll_rd(x * s1 * s2);
+    const long long n = __double2ll_rn(x * s1 * s2);
     return (unsigned long long)(n + 0x808080808080LL) ^ 0x808080808080ULL;
 }
 

@@ -64,7 +64,8 @@ def _factors(rng, p, s, q, r, kind="unit"):
     return f
 
 
-@pytest.mark.parametrize("q,s,r", [(20, 3, 5), (50, 2, 10), (64, 3, 20), (100, 1, 7), (128, 1, 32)])
+@pytest.mark.parametrize("q,s,r", [(20, 3, 5), (50, 2, 10), (64, 3, 20), (100, 1, 7), (128, 1, 32),
+                                   (128, 3, 32), (100, 3, 30), (40, 5, 30)])
 @pytest.mark.parametrize("mode", [0, 1, 2])
 def test_tgemm_digit_split_vs_exact(q, s, r, mode):
     rng = np.random.default_rng(1000 * q + 10 * r + mode)
