@@ -58,7 +58,11 @@ constexpr int A_STAGE = NS * A_SLICE;  // 56 KB
 #endif
 constexpr int NSLOT = OCTEN_OZ_NSLOT;  // A stages in flight (ring)
 constexpr int BH_SLICE = NH * KB;   // 4 KB
-constexpr int EPI_WARPS = 8;        // one per (TMEM lane quarter, half)
+#ifndef OCTEN_OZ_EPI_WARPS
+#define OCTEN_OZ_EPI_WARPS 8
+#endif
+constexpr int EPI_WARPS = OCTEN_OZ_EPI_WARPS;  // 8: one per (TMEM lane quarter, half); 16: two, 16 columns each
+constexpr int EPI_COLS = NH * 8 / EPI_WARPS;  // columns of a half per epilogue warp
 constexpr int PW = EPI_WARPS;       // the MMA warp
 constexpr int LW = EPI_WARPS + 1;   // the TMA warp
 constexpr int THREADS = (EPI_WARPS + 2) * 32;
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         __syncwarp();
     } else {
-        const int q = warp & 3, h = warp >> 2;
+        const int q = warp & 3, h = (warp >> 2) & 1, sub = warp >> 3;
         const int r = q * 32 + lane;
         const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * ND * NH);
         const int ncol = min(NH, SR - n0 - h * NH);  // valid columns of this half
@@ -423,12 +427,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                                    "=r"(a[buf][d][4]), "=r"(a[buf][d][5]), "=r"(a[buf][d][6]), "=r"(a[buf][d][7])
                                  : "r"(trow + (uint32_t)(d * NH + c0)));
             };
-            tload(0, 0);
+            tload(0, sub * EPI_COLS);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int ch = 0; ch < NH / 8; ++ch) {
-                const int c0 = ch * 8, buf = ch & 1;
-                if (ch + 1 < NH / 8) tload(buf ^ 1, c0 + 8);
+            for (int ch = 0; ch < EPI_COLS / 8; ++ch) {
+                const int c0 = sub * EPI_COLS + ch * 8, buf = ch & 1;
+                if (ch + 1 < EPI_COLS / 8) tload(buf ^ 1, c0 + 8);
                 double val[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
