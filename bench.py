@@ -724,7 +724,9 @@ def main():
         # pipelined ingest: batch b's merge overlaps batch b+1's compression
         # and CP-ALS (same bits as ingest_batch; st.sync() drains it)
         ingest = st.ingest_async
-    pipelined = not sharded
+        if os.environ.get("OCTEN_BENCH_SYNC"):  # diagnostics: the stages one after another
+            ingest = lambda b: ob.ingest_batch(st, b)
+    pipelined = not sharded and not os.environ.get("OCTEN_BENCH_SYNC")
     t_init = time.perf_counter() - t_init
     del first
     batches = [syn.batch(K0 + i * t, t) for i in range(args.warmup + args.steps)]

@@ -249,10 +249,12 @@ inline void ingest_batch_f32(StreamState& st, const std::vector<std::int64_t>& d
     detail::refresh(st);
 }
 
-// Pipelined ingest (no reference counterpart; same results as ingest_batch):
-// the batch's merge overlaps the next call's compression and CP-ALS.  The
-// host model/log copies are refreshed by sync(); an error of the pending
-// merge is thrown by the next ingest_batch_async or sync.
+// Pipelined ingest (no reference counterpart; same results as ingest_batch),
+// two batches in flight: the CP-ALS sweeps and the merges run on library
+// worker threads beside the next batch's compression and CP-ALS start.  The
+// host model/log copies are refreshed by sync(); a CP-ALS error of batch b is
+// thrown by the call of batch b+1, a merge error by the call of batch b+2 or
+// sync (the later batches are then not ingested).
 inline void ingest_batch_async(StreamState& st, const DenseTensor& batch) {
     if (!st.handle) throw ConfigError("ingest_batch: stream is not initialised");
     check(octen_stream_ingest_async(st.handle.get(), batch.data.data(), OCTEN_F64, OCTEN_HOST, batch.order(),

@@ -119,19 +119,21 @@ int octen_stream_prefetch(octen_stream* s, const void* data, int dtype, int orde
  * batch I x J x t (dtype/location as octen_stream_ingest); computed on the
  * device without materialising the reconstruction. */
 /* Pipelined ingest_batch (no reference counterpart; same results as
- * octen_stream_ingest, bit for bit): the batch is compressed before the call
- * returns (beside the previous batch's CP-ALS); its CP-ALS runs on a library
- * worker thread and its alignment/merge on another, beside the next batch's
- * CP-ALS.  The call returns once the previous batch's merge is done.  A
- * CP-ALS or merge error of a batch is returned by the next
- * octen_stream_ingest_async / octen_stream_sync (or any getter), with the
- * reference's "batch N: " prefix; the batch passed to that call is then not
- * ingested.  The batch buffer may be reused when the call returns.  Strict
- * streams and the first batch run synchronously. */
+ * octen_stream_ingest, bit for bit), two batches in flight: the batch is
+ * compressed and its CP-ALS started (GEVD attempts) before the call returns,
+ * beside the previous batch's CP-ALS sweeps (library worker thread) and the
+ * merge before them (another worker); then the batch's sweeps and the
+ * previous batch's merge are posted.  A CP-ALS error of batch b is returned
+ * by the call of batch b+1, a merge error by the call of batch b+2 or
+ * octen_stream_sync (or any getter), with the reference's "batch N: "
+ * prefix; the later batches are rolled back (not ingested), so the state is
+ * the reference's after its failed ingest_batch.  The batch buffer may be
+ * reused when the call returns.  Strict streams and the first batch run
+ * synchronously. */
 int octen_stream_ingest_async(octen_stream* s, const void* data, int dtype, int location, int order,
                               const int64_t* dims);
-/* Finish the batch in flight of octen_stream_ingest_async (its CP-ALS, then
- * its merge); returns its error. */
+/* Finish the batches in flight of octen_stream_ingest_async (the sweeps and
+ * merges); returns the first error. */
 int octen_stream_sync(octen_stream* s);
 /* Model publication for pipelined callers: with on != 0 every finished batch
  * copies its model to host memory, readable with octen_stream_last_model

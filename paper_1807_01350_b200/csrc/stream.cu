@@ -148,6 +148,8 @@ Stream::~Stream() {
     }
     for (cudaEvent_t e : aevs)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ievs)
+        if (e) cudaEventDestroy(e);
     if (mst) {
         cudaStreamSynchronize(mst);
         cudaStreamDestroy(mst);
@@ -615,13 +617,17 @@ std::exception_ptr Worker::wait() {
     return e;
 }
 
-void Stream::next_w_slot() { wslot ^= 1; }
+void Stream::next_w_slot() { wslot = (wslot + 1) % 3; }
 
 void Stream::begin_ctx(BatchCtx& b, bool first, std::int64_t t) {
     b.context = first ? std::string() : "batch " + std::to_string(batches_seen) + ": ";
     b.pending = true;
     b.first = first;
     b.compressed = false;
+    b.init_failed = false;
+    b.als_init_ms = 0.f;
+    b.als_init_s = 0.0;
+    b.Yb = nullptr;
     b.t = t;
     b.t_start = Clock::now();
     b.rec = BatchRecordC{};
@@ -764,46 +770,74 @@ void Stream::begin(BatchCtx& b, const void* data, int dtype, int location, int o
 // CP-ALS of the owned replicas on the updated summaries, packed into this
 // rank's models block (status header + factors + lambdas).
 void Stream::als_phase(BatchCtx& b, const double* dY, double* models_out, cudaStream_t st) {
-    const int Q = cfg.q, R = cfg.rank;
+    als_init_phase(b, dY, als, st);
+    als_sweep_phase(b, models_out, als, st, 1);
+}
+
+// CP-ALS, part 1: norms, GEVD starts and initial factors of the owned
+// replicas on `e` (host syncs on `st`).
+void Stream::als_init_phase(BatchCtx& b, const double* dY, AlsEngine& e, cudaStream_t st) {
     auto ta = Clock::now();
-    for (cudaEvent_t& e : aevs)
-        if (!e) OCTEN_CUDA(cudaEventCreate(&e));
-    OCTEN_CUDA(cudaEventRecord(aevs[0], st));
-    double hdr[4] = {0, 0, 0, 0};
-    const size_t qr = (size_t)Q * R;
+    for (cudaEvent_t& ev : ievs)
+        if (!ev) OCTEN_CUDA(cudaEventCreate(&ev));
+    OCTEN_CUDA(cudaEventRecord(ievs[0], st));
     if (pl > 0) {
         std::vector<std::uint64_t> seeds(pl);
         for (int r = 0; r < pl; ++r)
             seeds[r] = rng::derive(cfg.seed, {rng::kStreamAls, (std::uint64_t)(p0 + r), (std::uint64_t)b.rec.batch_index});
+        e.run_init(pl, cfg.als_n_restarts, cfg.q, cfg.rank, cfg.als_max_iters, cfg.als_rel_tol, dY, seeds, st);
+    }
+    OCTEN_CUDA(cudaEventRecord(ievs[1], st));
+    OCTEN_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    OCTEN_CUDA(cudaEventElapsedTime(&ms, ievs[0], ievs[1]));
+    b.als_init_ms = ms;
+    b.als_init_s = std::chrono::duration<double>(Clock::now() - ta).count();
+}
+
+// CP-ALS, part 2: the sweeps on `e` (stream `st`, ordered after part 1),
+// packed into this rank's models block (status header + factors + lambdas).
+// `ahead`: how many batches later the engine runs again (its host draws are
+// prefetched for that batch).
+void Stream::als_sweep_phase(BatchCtx& b, double* models_out, AlsEngine& e, cudaStream_t st, int ahead) {
+    const int Q = cfg.q, R = cfg.rank;
+    auto ta = Clock::now();
+    for (cudaEvent_t& ev : aevs)
+        if (!ev) OCTEN_CUDA(cudaEventCreate(&ev));
+    OCTEN_CUDA(cudaEventRecord(aevs[0], st));
+    double hdr[4] = {0, 0, 0, 0};
+    const size_t qr = (size_t)Q * R;
+    if (pl > 0) {
         try {
-            als.run(pl, cfg.als_n_restarts, Q, R, cfg.als_max_iters, cfg.als_rel_tol, dY, seeds, st);
-            // the next batch's host draws, off its critical path
+            e.run_sweeps(st);
+            // the engine's next batch's host draws, off its critical path
+            std::vector<std::uint64_t> seeds(pl);
             for (int r = 0; r < pl; ++r)
-                seeds[r] = rng::derive(cfg.seed,
-                                       {rng::kStreamAls, (std::uint64_t)(p0 + r), (std::uint64_t)b.rec.batch_index + 1});
-            als.prefetch_host_draws(seeds, cfg.als_n_restarts, Q);
+                seeds[r] = rng::derive(cfg.seed, {rng::kStreamAls, (std::uint64_t)(p0 + r),
+                                                  (std::uint64_t)(b.rec.batch_index + ahead)});
+            e.prefetch_host_draws(seeds, cfg.als_n_restarts, Q);
         } catch (const NumericError&) {
             // a replica's CP-ALS failed: every rank raises it after the exchange
-            if (als.failure.kind == 0) throw;
-            hdr[0] = als.failure.kind;
-            hdr[1] = als.failure.a;
-            hdr[2] = als.failure.b;
+            if (e.failure.kind == 0) throw;
+            hdr[0] = e.failure.kind;
+            hdr[1] = e.failure.a;
+            hdr[2] = e.failure.b;
         }
         if (hdr[0] == 0.0) {
-            OCTEN_CUDA(cudaMemcpyAsync(models_out + 4, als.Mf.p, sizeof(double) * pl * 3 * qr,
+            OCTEN_CUDA(cudaMemcpyAsync(models_out + 4, e.Mf.p, sizeof(double) * pl * 3 * qr,
                                        cudaMemcpyDeviceToDevice, st));
-            OCTEN_CUDA(cudaMemcpyAsync(models_out + 4 + (size_t)chunk * 3 * qr, als.Mlam.p, sizeof(double) * pl * R,
+            OCTEN_CUDA(cudaMemcpyAsync(models_out + 4 + (size_t)chunk * 3 * qr, e.Mlam.p, sizeof(double) * pl * R,
                                        cudaMemcpyDeviceToDevice, st));
         }
     }
     h2d_param(models_out, hdr, sizeof(hdr), st);
     OCTEN_CUDA(cudaEventRecord(aevs[1], st));
     OCTEN_CUDA(cudaStreamSynchronize(st));
-    b.rec.als_seconds = std::chrono::duration<double>(Clock::now() - ta).count();
-    // device time of CP-ALS (its stream; the compression and the merge add their own)
+    b.rec.als_seconds = b.als_init_s + std::chrono::duration<double>(Clock::now() - ta).count();
+    // device time of CP-ALS (its streams; the compression and the merge add their own)
     float ms = 0.f;
     OCTEN_CUDA(cudaEventElapsedTime(&ms, aevs[0], aevs[1]));
-    dev_ms[1] += ms;
+    dev_ms[1] += ms + b.als_init_ms;
     OCTEN_CUDA(cudaEventRecord(b.ev[2], st));
 }
 
@@ -970,7 +1004,7 @@ void Stream::merge_phase(BatchCtx& b, const double* models_all, double* rows_out
         Bnew.reserve((size_t)J * R);
         merge.recover_ab(b.first ? nullptr : A.p, b.first ? nullptr : B.p, Anew.p, Bnew.p, st);
         sp.mark("recover_ab", st);
-        if (pl > 0) merge.temporal_stack(Y.p, p0, pl, Anew.p, Bnew.p, rows_out, true, st);
+        if (pl > 0) merge.temporal_stack(b.Yb ? b.Yb : Y.p, p0, pl, Anew.p, Bnew.p, rows_out, true, st);
         sp.mark("temporal_stack", st);
         sp.report("merge_phase");
         OCTEN_CUDA(cudaStreamSynchronize(st));
@@ -1151,13 +1185,29 @@ void Stream::ingest(const void* data, int dtype, int location, int order, const 
 }
 
 void Stream::sync() {
-    // the pipelined ingest's batch in flight: its CP-ALS, then its merge
-    std::exception_ptr e = aworker.wait();
-    if (!e && a_prev) post_merge(*a_prev, a_prev_models);
+    // the pipelined ingest's batches in flight: the last batch's sweeps and
+    // the merge before them, then the last batch's merge
+    std::exception_ptr a_err = aworker.wait();
+    BatchCtx* pa = a_prev;
     a_prev = nullptr;
-    std::exception_ptr m = worker.wait();
-    if (!e) e = m;
-    if (e) std::rethrow_exception(e);
+    std::exception_ptr m_err = worker.wait();
+    m_prev = nullptr;
+    if (m_err) {
+        // the earlier batch failed in its merge: the reference stops there
+        if (pa) {
+            rollback_to(*pa);
+            Y.swap(Yhold);
+            pa->pending = false;
+        }
+        std::rethrow_exception(m_err);
+    }
+    if (a_err) std::rethrow_exception(a_err);
+    if (pa) {
+        pa->Yb = Y.p;
+        post_merge(*pa, pa->models);
+        std::exception_ptr e = worker.wait();
+        if (e) std::rethrow_exception(e);
+    }
 }
 
 void Stream::post_merge(BatchCtx& b, double* models) {
@@ -1166,6 +1216,12 @@ void Stream::post_merge(BatchCtx& b, double* models) {
         merge_phase(b, models, xrows.p);
         finish(b, xrows.p);
     });
+}
+
+void Stream::rollback_to(const BatchCtx& b) {
+    batches_drawn = b.rb_drawn;
+    batches_seen = b.rb_seen;
+    tgram = b.rb_tgram;
 }
 
 namespace {
@@ -1224,58 +1280,94 @@ void Stream::ingest_async(const void* data, int dtype, int location, int order, 
         if (!mst) OCTEN_CUDA(cudaStreamCreateWithPriority(&mst, cudaStreamNonBlocking, least));
     }
     if (!ast) OCTEN_CUDA(cudaStreamCreateWithPriority(&ast, cudaStreamNonBlocking, critical_stream_priority()));
-    BatchCtx& b = actx[aslot];
-    b.st = mst;
-    double* models = aslot ? xmodels2.reserve(models_count()) : xmodels.reserve(models_count());
-    const std::int64_t drawn0 = batches_drawn, seen0 = batches_seen;
-    const std::vector<double> tgram0 = tgram;
-    // this batch's compression (Ynext = Y + its summaries), overlapping the
-    // previous batch's CP-ALS on the CP-ALS worker
+    // Two batches in flight: the previous batch's sweeps (CP-ALS worker) and
+    // the merge before them (merge worker) run while this batch is
+    // compressed and its CP-ALS start (GEVD attempts) runs on the other
+    // engine; then this batch's sweeps and the previous batch's merge are
+    // posted.  Errors of batch b surface in the call of batch b+1 (CP-ALS) or
+    // b+2 (merge), with the later batches rolled back.
+    BatchCtx& bc = actx[aslot];
+    bc.st = mst;
+    double* models = apar ? xmodels2.reserve(models_count()) : xmodels.reserve(models_count());
+    AlsEngine& eng = apar ? als_b : als;
+    bc.rb_drawn = batches_drawn;
+    bc.rb_seen = batches_seen;
+    bc.rb_tgram = tgram;
     std::exception_ptr begin_err;
     try {
-        begin(b, data, dtype, location, order, dims, models, true, false);
+        begin(bc, data, dtype, location, order, dims, models, true, false);
+        try {
+            als_init_phase(bc, Ynext.p, eng, st);
+        } catch (...) {
+            bc.init_failed = true;
+            fail_pending(bc);
+        }
     } catch (...) {
         begin_err = std::current_exception();
     }
-    // the previous batch: its CP-ALS must be done before this one's starts
-    // (one engine); its merge then runs beside this batch's CP-ALS
-    std::exception_ptr prev_err = aworker.wait();
-    BatchCtx* prev = a_prev;
-    double* prev_models = a_prev_models;
+    // the previous batch's sweeps, then the merge posted before them
+    std::exception_ptr a_err = aworker.wait();
+    BatchCtx* pa = a_prev;
     a_prev = nullptr;
-    bool posted = false;
-    if (!prev_err && !begin_err) {
-        const double* dY = Ynext.p;
-        aworker.post(cfg.device, [this, &b, dY, models] {
-            try {
-                als_phase(b, dY, models, ast);
-            } catch (...) {
-                fail_pending(b);
-            }
-        });
-        posted = true;
+    std::exception_ptr m_err = worker.wait();
+    m_prev = nullptr;
+    if (m_err) {
+        // the batch before pa failed in its merge (the reference throws from
+        // its ingest_batch): pa and this batch were never ingested; the
+        // summaries are the failed batch's (Yhold)
+        if (pa) {
+            rollback_to(*pa);
+            Y.swap(Yhold);
+            pa->pending = false;
+        } else {
+            rollback_to(bc);
+        }
+        bc.pending = false;
+        std::rethrow_exception(m_err);
     }
-    if (!prev_err && prev) {
-        post_merge(*prev, prev_models);
-        prev_err = worker.wait();
+    if (a_err) {
+        // pa failed in its CP-ALS: its summaries stay (as the reference's);
+        // this batch was never ingested
+        rollback_to(bc);
+        bc.pending = false;
+        std::rethrow_exception(a_err);
     }
-    if (prev_err) {
-        // batch b-1 failed in its CP-ALS or merge (the reference throws from
-        // its ingest_batch): this batch was never ingested
-        if (posted) (void)aworker.wait();
-        batches_drawn = drawn0;
-        batches_seen = seen0;
-        tgram = tgram0;
-        b.pending = false;
-        std::rethrow_exception(prev_err);
+    // the previous batch's merge (its models and summaries are final)
+    if (pa) {
+        pa->Yb = Y.p;
+        post_merge(*pa, pa->models);
+        m_prev = pa;
     }
-    if (begin_err) std::rethrow_exception(begin_err);
-    // the summaries now include this batch (a CP-ALS failure keeps them, as
-    // the reference does)
+    if (begin_err) {
+        // this batch's compression or CP-ALS start failed: the earlier
+        // batch's merge completes first (its error comes first)
+        std::exception_ptr e2 = worker.wait();
+        m_prev = nullptr;
+        if (e2) {
+            rollback_to(bc);
+            bc.pending = false;
+            std::rethrow_exception(e2);
+        }
+        if (bc.init_failed) Y.swap(Ynext);  // a CP-ALS failure keeps the updated summaries
+        std::rethrow_exception(begin_err);
+    }
+    // this batch's sweeps on its engine
+    bc.models = models;
+    AlsEngine* e = &eng;
+    aworker.post(cfg.device, [this, &bc, e, models] {
+        try {
+            als_sweep_phase(bc, models, *e, ast, 2);
+        } catch (...) {
+            fail_pending(bc);
+        }
+    });
+    a_prev = &bc;
+    // summaries: Yhold <- the previous batch's (its merge reads them), Y <-
+    // this batch's, Ynext <- the buffer the merge before released
+    Yhold.swap(Y);
     Y.swap(Ynext);
-    a_prev = &b;
-    a_prev_models = models;
-    aslot ^= 1;
+    aslot = (aslot + 1) % 3;
+    apar ^= 1;
 }
 
 namespace {

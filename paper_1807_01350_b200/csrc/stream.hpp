@@ -54,6 +54,15 @@ struct BatchCtx {
     cudaEvent_t ev[3] = {};            // merge start / end (device timing), inputs ready on the main stream
     std::vector<double> tgram;         // shared temporal Gram including this batch's rows (align)
     const double* dW = nullptr;        // this batch's temporal rows (P x t x Q)
+    // pipelined ingest: the summaries after this batch (read by its merge),
+    // its models block, and the stream counters before it (rollback)
+    const double* Yb = nullptr;
+    double* models = nullptr;
+    std::int64_t rb_drawn = 0, rb_seen = 0;
+    std::vector<double> rb_tgram;
+    bool init_failed = false;          // its CP-ALS start raised
+    float als_init_ms = 0.f;           // CP-ALS start: device ms, wall s
+    double als_init_s = 0.0;
     ~BatchCtx();
 };
 
@@ -117,16 +126,16 @@ public:
 
     void init(const void* data, int dtype, int location, int order, const std::int64_t* dims);
     void ingest(const void* data, int dtype, int location, int order, const std::int64_t* dims);
-    // Pipelined ingest_batch: this batch is compressed now (overlapping the
-    // previous batch's CP-ALS); its CP-ALS runs on the CP-ALS worker thread
-    // (own CUDA streams) and overlaps the previous batch's merge, which runs
-    // on the merge worker thread.  The call returns once the previous
-    // batch's merge is done.  The results are the same bits as ingest():
-    // every stage reads the same inputs (the summaries are double-buffered,
-    // the temporal rows and Gram are per batch).  A CP-ALS or merge error of
-    // batch b surfaces at the next ingest_async / sync (with its batch
-    // prefix); that next batch is then not ingested.  Strict streams and the
-    // first batch run synchronously.
+    // Pipelined ingest_batch, two batches in flight: this batch is compressed
+    // and its CP-ALS started (GEVD attempts, on the other of two engines)
+    // while the previous batch's sweeps (CP-ALS worker thread) and the merge
+    // before them (merge worker thread) run; then this batch's sweeps and
+    // the previous batch's merge are posted.  The results are the same bits
+    // as ingest(): every stage reads the same inputs (three summaries
+    // buffers, per-batch temporal rows and Gram).  A CP-ALS error of batch b
+    // surfaces at the call of batch b+1, a merge error at the call of batch
+    // b+2 or sync (with the batch prefix); the later batches are rolled back.
+    // Strict streams and the first batch run synchronously.
     void ingest_async(const void* data, int dtype, int location, int order, const std::int64_t* dims);
     // Wait for the pending merge; rethrows its error.
     void sync();
@@ -191,13 +200,14 @@ public:
     CompressEngine comp_all;  // every replica (temporal sharding)
     bool comp_all_ready = false;
     AlsEngine als;
+    AlsEngine als_b;  // pipelined ingest: batches alternate engines (one starts while the other sweeps)
     MergeEngine merge;
     // Y: pl x Q^3 (owned replicas); hist: P*Q x R (all replicas, kept redundantly)
     // Ynext: the pipelined ingest's summaries after the batch in flight
     // (Y + its compression, out of place: the merge of the previous batch
     // still reads Y); dWb: temporal rows of the last two batches
     DevBuf<double> Y, Ynext, hist, A, B, C, lam, Anew, Bnew, rows, X64;
-    DevBuf<double> dWb[2];
+    DevBuf<double> dWb[3];  // temporal rows of the last three batches (pipelined ingest)
     int wslot = 0;
     double* dW = nullptr;
     DevBuf<double> xmodels, xrows, MfAll, MlamAll, tstackAll;
@@ -232,17 +242,19 @@ public:
     cudaEvent_t evs[6] = {};
 
     BatchCtx cur;                 // synchronous / sharded phases
-    BatchCtx actx[2];             // pipelined ingest: alternating per batch
-    int aslot = 0;
+    BatchCtx actx[3];             // pipelined ingest: rotating per batch
+    int aslot = 0, apar = 0;      // context slot (mod 3); engine / models parity
     Worker worker;                // pipelined ingest: the merges
     Worker aworker;               // pipelined ingest: the CP-ALS runs
     cudaStream_t mst = nullptr;   // merge stream of the pipelined ingest (lower priority)
     cudaStream_t ast = nullptr;   // CP-ALS stream of the pipelined ingest
-    // the batch whose CP-ALS is posted (aworker) and whose merge is still to
-    // be posted: its context and models block
+    // pipelined ingest: the batch whose CP-ALS sweeps are posted (aworker),
+    // and the batch whose merge is posted (worker) and not yet waited for
     BatchCtx* a_prev = nullptr;
-    double* a_prev_models = nullptr;
-    cudaEvent_t aevs[2] = {};     // CP-ALS device timing (the CP-ALS worker's events)
+    BatchCtx* m_prev = nullptr;
+    DevBuf<double> Yhold;         // the summaries m_prev's merge reads
+    cudaEvent_t aevs[2] = {};     // CP-ALS sweeps device timing (the CP-ALS worker's events)
+    cudaEvent_t ievs[2] = {};     // CP-ALS start device timing (the caller's events)
 
 private:
     using Clock = std::chrono::steady_clock;
@@ -266,7 +278,10 @@ private:
     void merge_phase(BatchCtx& b, const double* models_all, double* rows_out);
     void finish(BatchCtx& b, const double* rows_all);
     void als_phase(BatchCtx& b, const double* dY, double* models_out, cudaStream_t as);
+    void als_init_phase(BatchCtx& b, const double* dY, AlsEngine& e, cudaStream_t st);
+    void als_sweep_phase(BatchCtx& b, double* models_out, AlsEngine& e, cudaStream_t st, int ahead);
     void post_merge(BatchCtx& b, double* models);
+    void rollback_to(const BatchCtx& b);
     void snapshot(Snapshot& s);
     void restore(Snapshot& s);
     [[noreturn]] void fail_pending(BatchCtx& b);

@@ -1,8 +1,11 @@
-"""Pipelined ingest (octen_stream_ingest_async): batch b's merge runs on a
-worker thread and overlaps batch b+1's compression and CP-ALS.  It must give
-the same bits as the synchronous ingest_batch (streaming.cpp:258-346) and the
-same error behaviour: a merge failure is reported (with the reference's
-"batch N: " prefix) by the next call, which does not ingest its own batch."""
+"""Pipelined ingest (octen_stream_ingest_async): two batches in flight.
+Batch b+1 is compressed and its CP-ALS started while batch b's sweeps (CP-ALS
+worker) and batch b-1's merge (merge worker) run.  It must give the same bits
+as the synchronous ingest_batch (streaming.cpp:258-346) and the reference's
+error behaviour: a CP-ALS failure of batch b is reported (with the
+reference's "batch N: " prefix) by the call of batch b+1, a merge failure by
+the call of batch b+2 or sync(), and the later batches are rolled back, so
+the state is the one the reference leaves after its failed ingest_batch."""
 import numpy as np
 import pytest
 
@@ -57,12 +60,16 @@ def test_async_ingest_bit_identical(ob, dtype, noise):
     for k in range(30, 90, 10):
         ob.ingest_batch(a, np.asfortranarray(x[:, :, k:k + 10]))
         b.ingest_async(np.asfortranarray(x[:, :, k:k + 10]))
-        m, nb = b.last_model()  # the model of the batch whose merge completed (none for the first)
+        m, nb = b.last_model()  # the model of the last batch whose merge completed (none at first)
         seen.append(nb)
     b.sync()
     _same_state(a, b)
     assert b.batches_seen == a.batches_seen == 7
-    assert seen == [0, 2, 3, 4, 5, 6]
+    # the call of batch j returns once batch j-2's merge is done (batch j-1's
+    # may be done too): batches merged so far, counting the initial block
+    assert seen[0] == 0 and all(u <= v for u, v in zip(seen, seen[1:]))
+    for j in range(3, 7):
+        assert j - 1 <= seen[j - 1] <= j, seen
     m, nb = b.last_model()
     assert nb == 7
     ma = a.model
@@ -103,14 +110,20 @@ def test_async_merge_error_reported_by_next_call(ob):
         ob.ingest_batch(a, np.asfortranarray(x[:, :, 20:60]))
     ob.ingest_batch(a, np.asfortranarray(x[:, :, 60:70]))
 
-    b.ingest_async(np.asfortranarray(x[:, :, 10:20]))
-    b.ingest_async(np.asfortranarray(x[:, :, 20:60]))  # compression + CP-ALS succeed
-    with pytest.raises(ob.NumericError, match=r"^batch 2: recover_temporal_append: p\*Q too small"):
-        b.ingest_async(np.asfortranarray(x[:, :, 60:70]))  # reports batch 2; this batch is not ingested
-    assert b.batches_seen == 3
-    b.ingest_async(np.asfortranarray(x[:, :, 60:70]))
-    b.sync()
-    _same_state(a, b)
+    for via in ("sync", "next"):
+        b = ob.init_stream(np.asfortranarray(x[:, :, :10]), cfg)
+        b.ingest_async(np.asfortranarray(x[:, :, 10:20]))
+        b.ingest_async(np.asfortranarray(x[:, :, 20:60]))  # compression + CP-ALS start succeed
+        b.ingest_async(np.asfortranarray(x[:, :, 60:70]))  # batch 2's sweeps succeed, its merge is posted
+        with pytest.raises(ob.NumericError, match=r"^batch 2: recover_temporal_append: p\*Q too small"):
+            if via == "sync":
+                b.sync()
+            else:  # reports batch 2; batches 3 and this one are rolled back
+                b.ingest_async(np.asfortranarray(x[:, :, 70:80]))
+        assert b.batches_seen == 3
+        b.ingest_async(np.asfortranarray(x[:, :, 60:70]))
+        b.sync()
+        _same_state(a, b)
 
 
 @pytest.mark.parametrize("dtype,val,pos", [(np.float64, np.inf, (1, 2, 3)), (np.float32, np.nan, (5, 7, 9)),
