@@ -418,7 +418,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             tc_fence_after();
             // chunks of 8 columns; the TMEM loads of chunk c + 1 are in flight
             // while chunk c is converted and stored
-            uint32_t a[2][ND][8];
+#ifndef OCTEN_OZ_TMEM_DB
+#define OCTEN_OZ_TMEM_DB 1
+#endif
+            constexpr int NBUF = OCTEN_OZ_TMEM_DB ? 2 : 1;  // TMEM load buffers (double: next chunk in flight)
+            uint32_t a[NBUF][ND][8];
             auto tload = [&](int buf, int c0) {
 #pragma unroll
                 for (int d = 0; d < ND; ++d)
@@ -431,8 +435,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int ch = 0; ch < EPI_COLS / 8; ++ch) {
-                const int c0 = sub * EPI_COLS + ch * 8, buf = ch & 1;
-                if (ch + 1 < EPI_COLS / 8) tload(buf ^ 1, c0 + 8);
+                const int c0 = sub * EPI_COLS + ch * 8, buf = NBUF == 2 ? (ch & 1) : 0;
+                if (NBUF == 2 && ch + 1 < EPI_COLS / 8) tload(buf ^ 1, c0 + 8);
+                if (NBUF == 1 && ch > 0) {
+                    tload(0, c0);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                }
                 double val[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
