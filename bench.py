@@ -629,7 +629,7 @@ def cpu_sample_sparse(batch, w, u, v, P, R, c, sample=50_000):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="octen", choices=["octen", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + ["c4"])

@@ -219,8 +219,11 @@ struct PanelC {
 // column-coalesced.
 constexpr int kTrailLD = kCholNB + 4;
 
+// With k0b >= 0 the update carries a second (earlier, delayed) panel of 64
+// columns at k0b as well: A(i, j) -= sum_k L(i, k0b + k) L(j, k0b + k) + ...,
+// one read-modify-write of A for both (rank-128 update).
 __global__ void __launch_bounds__(256, 3) chol_trail_kernel(double* A, int n, int lda, long long sA, int r0, int k0,
-                                                         int nb, int part, int ntiles, int ntasks) {
+                                                         int nb, int part, int ntiles, int ntasks, int k0b) {
     extern __shared__ double trail_smem[];
     double* Pi = trail_smem;                       // [64 k][kTrailLD m]
     double* Pj = trail_smem + kCholNB * kTrailLD;  // [64 k][kTrailLD m]
@@ -247,6 +250,17 @@ __global__ void __launch_bounds__(256, 3) chol_trail_kernel(double* A, int n, in
     double* a = A + (size_t)mat * sA;
     const int i0 = r0 + kCholNB * ti, j0 = r0 + kCholNB * tj;
     const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int pnl = k0b >= 0 ? 0 : 1; pnl < 2; ++pnl) {
+    const int kc = pnl == 0 ? k0b : k0;  // the delayed panel first, then this step's
+    const int nbp = pnl == 0 ? kCholNB : nb;
     // panels: batches of loads into registers, then shared stores
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -255,9 +269,9 @@ __global__ void __launch_bounds__(256, 3) chol_trail_kernel(double* A, int n, in
         for (int r = 0; r < 8; ++r) {
             const int e = tid + 256 * (8 * h + r);
             const int m = e & (kCholNB - 1), kk = e >> 6;
-            const bool kin = kk < nb;
-            pi[r] = (kin && i0 + m < n) ? a[(i0 + m) + (size_t)lda * (k0 + kk)] : 0.0;
-            pj[r] = (kin && j0 + m < n) ? a[(j0 + m) + (size_t)lda * (k0 + kk)] : 0.0;
+            const bool kin = kk < nbp;
+            pi[r] = (kin && i0 + m < n) ? a[(i0 + m) + (size_t)lda * (kc + kk)] : 0.0;
+            pj[r] = (kin && j0 + m < n) ? a[(j0 + m) + (size_t)lda * (kc + kk)] : 0.0;
         }
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -268,15 +282,7 @@ __global__ void __launch_bounds__(256, 3) chol_trail_kernel(double* A, int n, in
         }
     }
     __syncthreads();
-    const int lane = tid & 31, warp = tid >> 5;
-    const int g = lane >> 2, t4 = lane & 3;
-    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
-    double acc[4][2][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    const int kend = (nb + 3) & ~3;
+    const int kend = (nbp + 3) & ~3;
     for (int kk = 0; kk < kend; kk += 4) {
         double fa[4], fb[2];
 #pragma unroll
@@ -289,6 +295,7 @@ __global__ void __launch_bounds__(256, 3) chol_trail_kernel(double* A, int n, in
             for (int j = 0; j < 2; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
     }
     __syncthreads();
+    }  // panels
     // stage the 64 x 64 product column-major (ld 65) over the panel buffers
     double* Cs = trail_smem;
 #pragma unroll
@@ -371,6 +378,15 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
     OCTEN_CUDA(cudaEventRecord(ev_start, st));
     OCTEN_CUDA(cudaStreamWaitEvent(crit, ev_start, 0));
     int pending_rest = -1;  // step whose part 2 is in flight on `st`
+    // Delayed updates: every other step's part 2 is skipped and applied with
+    // the next step's panel in one rank-128 update (one read-modify-write of
+    // the trailing matrix for two panels); the next step's part 1 then
+    // carries both panels too.  OCTEN_CHOL_DELAY=0 turns it off.
+    static const bool delay_ok = [] {
+        const char* e = std::getenv("OCTEN_CHOL_DELAY");
+        return !(e && e[0] == '0');
+    }();
+    int delayed = -1;  // column offset of the panel whose trailing update is pending
     static thread_local EvProf cp;
     const bool prof = EvProf::enabled() && n >= 512;
     if (prof) cp.mark("begin", crit);
@@ -398,10 +414,12 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
         }
         if (prof) cp.mark("wait", crit);
         chol_trail_kernel<<<tiles * batch, 256, kTrailSmem, crit>>>(A, n, lda, sA, r0, k0, nb, 1, tiles,
-                                                                    tiles * batch);
+                                                                    tiles * batch, delayed);
         OCTEN_LAUNCHED(1);
         if (prof) cp.mark("part1", crit);
-        if (tiles > 1) {
+        if (tiles > 1 && delay_ok && delayed < 0 && nb == kCholNB) {
+            delayed = k0;  // this step's part 2 goes with the next step's
+        } else if (tiles > 1) {
             // OCTEN_TRAIL_CAP: cap the grid (tasks are strided over it) to
             // leave SM room for the critical chain (diagnostics)
             const int t2 = (tiles - 1) * tiles / 2;
@@ -411,10 +429,13 @@ inline void chol_batched(double* A, int n, int lda, long long sA, int batch, dou
             }();
             const int cap = cap_env > 0 ? cap_env : 1 << 30;
             chol_trail_kernel<<<std::min(t2 * batch, cap), 256, kTrailSmem, st>>>(A, n, lda, sA, r0, k0, nb, 2, t2,
-                                                                                  t2 * batch);
+                                                                                  t2 * batch, delayed);
             OCTEN_LAUNCHED(1);
             OCTEN_CUDA(cudaEventRecord(ev_rest[kb], st));
             pending_rest = kb;
+            delayed = -1;
+        } else {
+            delayed = -1;  // (no tile column beyond the next one: nothing was delayed)
         }
     }
     // join: everything on `st` after this waits for the critical chain

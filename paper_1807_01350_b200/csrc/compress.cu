@@ -167,7 +167,7 @@ void run_project(CompressEngine& e, const T* dX, std::int64_t t, T* Z1, T* Z2, c
                                         "(sm_100a required; set OCTEN_ALLOW_SIMT=1 to run the SIMT GEMMs)");
                 } else {
                     done = tc_gemm_tf32x3(e.Ahi.p, e.Alo.p, e.lda_tc, Xc, Z1, (int)e.Meff, (long long)N1, (int)e.I,
-                                          st, P, Q, e.shared, flag);
+                                          st, P, Q, e.shared, flag, e.g1_ctas);
                     if (done) scanned = true;
                     if (done)
                         path_counter(kTcgen05Launches).fetch_add(1);

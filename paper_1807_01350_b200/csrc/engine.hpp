@@ -179,6 +179,9 @@ public:
     int ldv_tc = 0;
     DevBuf<int> rowmap_id;   // identity row map (replica-contiguous Z1 of the tc path)
     bool used_tc = false;
+    // cap on GEMM1's persistent grid (0: one CTA per SM); the pipelined
+    // ingest sets it while the previous batch's CP-ALS sweeps run beside
+    int g1_ctas = 0;
     DevBuf<double> A64;  // Meff x I row-major
     DevBuf<float> V32;   // P x J x Q
     DevBuf<double> V64;  // P x J x Q

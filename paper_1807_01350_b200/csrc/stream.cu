@@ -1294,6 +1294,20 @@ void Stream::ingest_async(const void* data, int dtype, int location, int order, 
     bc.rb_seen = batches_seen;
     bc.rb_tgram = tgram;
     std::exception_ptr begin_err;
+    // GEMM1 on half the SMs while the previous batch's sweeps run beside it:
+    // its persistent CTAs would otherwise hold every SM for ~1.2 ms and
+    // stall the sweeps, the pipeline's critical chain.  Measured at c3 (ms
+    // per step, grid 148 / 128 / 100 / 74 / 48 / 32 CTAs): 11.70 / 11.64 /
+    // 11.60 / 11.55 / 11.67 / 11.95.  OCTEN_G1_SMS overrides (0: every SM).
+    static const int g1_env = [] {
+        const char* e = std::getenv("OCTEN_G1_SMS");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (a_prev) {
+        int nsm = 0;
+        OCTEN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg.device));
+        comp.g1_ctas = g1_env >= 0 ? g1_env : nsm / 2;
+    }
     try {
         begin(bc, data, dtype, location, order, dims, models, true, false);
         try {
@@ -1305,6 +1319,7 @@ void Stream::ingest_async(const void* data, int dtype, int location, int order, 
     } catch (...) {
         begin_err = std::current_exception();
     }
+    comp.g1_ctas = 0;
     // the previous batch's sweeps, then the merge posted before them
     std::exception_ptr a_err = aworker.wait();
     BatchCtx* pa = a_prev;

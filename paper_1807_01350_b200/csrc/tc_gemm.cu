@@ -754,7 +754,7 @@ bool tc_gemm_available() {
 }
 
 bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X, float* Z, int M, long long N, int K,
-                    cudaStream_t st, int scatter_p, int scatter_q, int scatter_sh, int* nonfinite) {
+                    cudaStream_t st, int scatter_p, int scatter_q, int scatter_sh, int* nonfinite, int max_ctas) {
     if (!tc_gemm_available()) return false;
     if ((K % 4) != 0 || (lda % 4) != 0 || ((uintptr_t)X % 16) != 0 || ((uintptr_t)Ahi % 16) != 0 ||
         ((uintptr_t)Alo % 16) != 0 || N > (1LL << 31) - 1 || M <= 0 || N <= 0 || K <= 0)
@@ -781,6 +781,7 @@ bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X,
         OCTEN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         const int mt = (M + BM - 1) / BM;
         const long long ntiles = (long long)mt * ((N + BN - 1) / BN);
+        if (max_ctas > 0) nsm = std::min(nsm, max_ctas);
         const int grid = (int)std::min<long long>(ntiles, nsm);
         // two MMAs per k-step (A_hi X_rn + A_lo X_rn, X rounded to the
         // nearest TF32) unless OCTEN_G1_3MMA asks for the A_hi X_hi +

@@ -20,8 +20,10 @@ void* tc_tensor_map_encoder();
 // so Z is scatter_p * scatter_q x N.
 // nonfinite (optional): set to 1 when X holds a non-finite value (the
 // conversion warps check every element they pass).
+// max_ctas > 0 caps the persistent grid (default: one CTA per SM).
 bool tc_gemm_tf32x3(const float* Ahi, const float* Alo, int lda, const float* X, float* Z, int M, long long N, int K,
-                    cudaStream_t st, int scatter_p = 0, int scatter_q = 0, int scatter_sh = 0, int* nonfinite = nullptr);
+                    cudaStream_t st, int scatter_p = 0, int scatter_q = 0, int scatter_sh = 0, int* nonfinite = nullptr,
+                    int max_ctas = 0);
 // Mode-2 contraction batched over (replica, slice):
 //   Z2[p * zstride + a + Q b + Q^2 k] = sum_j Z1[p Q + a][k J + j] V_p[j, b]
 // Z1: P*Q x N1 row-major (N1 = J * tc); Vhi/Vlo: TF32 hi/lo split of V,
