@@ -874,6 +874,17 @@ def main():
                                   "to the nearest TF32)" if n_mma == 2 else
                                   "split-TF32: 3 tcgen05 MMAs (hi*hi, hi*lo, lo*hi) per useful product"),
                   "tensor_pipe_active_pct_ncu": pipe_pct}}
+    if pipelined:  # GEMM1 runs on half the SMs beside the previous batch's sweeps
+        nsm = torch.cuda.get_device_properties(local).multi_processor_count
+        g1_env = os.environ.get("OCTEN_G1_SMS")
+        g1_ctas = int(g1_env) if g1_env is not None else nsm // 2
+        if 0 < g1_ctas < nsm:
+            rooflines["gemm1"].update({
+                "ctas": g1_ctas, "sms": nsm,
+                "frac_of_grid_sms": achieved / (tf32_peak * g1_ctas / nsm),
+                "grid_note": "the pipelined ingest caps GEMM1's persistent grid at %d of %d SMs so the previous "
+                             "batch's CP-ALS sweeps keep the rest (11.43 -> 11.17 ms per step); frac_of_grid_sms "
+                             "is the fraction of the peak those SMs give" % (g1_ctas, nsm)})
     if kd and kd["gemm_launches"] > 0:
         gms = kd["gemm_ms"] / kd["gemm_launches"]
         gfl = kd["gemm_flops"] / kd["gemm_launches"]
