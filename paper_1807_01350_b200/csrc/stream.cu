@@ -1288,7 +1288,10 @@ void Stream::ingest_async(const void* data, int dtype, int location, int order, 
     // b+2 (merge), with the later batches rolled back.
     BatchCtx& bc = actx[aslot];
     bc.st = mst;
-    double* models = apar ? xmodels2.reserve(models_count()) : xmodels.reserve(models_count());
+    // models per context slot: batch b-1's merge may still read its models
+    // while batch b+1's sweeps (same engine) write theirs
+    DevBuf<double>& mbuf = aslot == 0 ? xmodels : aslot == 1 ? xmodels2 : xmodels3;
+    double* models = mbuf.reserve(models_count());
     AlsEngine& eng = apar ? als_b : als;
     bc.rb_drawn = batches_drawn;
     bc.rb_seen = batches_seen;
@@ -1324,9 +1327,31 @@ void Stream::ingest_async(const void* data, int dtype, int location, int order, 
     std::exception_ptr a_err = aworker.wait();
     BatchCtx* pa = a_prev;
     a_prev = nullptr;
+    // This batch's sweeps are the pipeline's critical chain: when nothing
+    // has failed so far they are posted before waiting for the merge posted
+    // before them (which may still run; waiting for it first put its tail,
+    // ~1.2 ms at c3, between two batches' sweeps).  If that merge fails,
+    // the sweeps are drained and discarded with the rollback.
+    bc.models = models;
+    AlsEngine* e = &eng;
+    const bool early = !a_err && !begin_err;
+    if (early) {
+        aworker.post(cfg.device, [this, &bc, e, models] {
+            try {
+                als_sweep_phase(bc, models, *e, ast, 2);
+            } catch (...) {
+                fail_pending(bc);
+            }
+        });
+        a_prev = &bc;
+    }
     std::exception_ptr m_err = worker.wait();
     m_prev = nullptr;
     if (m_err) {
+        if (early) {
+            (void)aworker.wait();  // this batch is rolled back: its sweeps' outcome is moot
+            a_prev = nullptr;
+        }
         // the batch before pa failed in its merge (the reference throws from
         // its ingest_batch): pa and this batch were never ingested; the
         // summaries are the failed batch's (Yhold)
@@ -1366,17 +1391,6 @@ void Stream::ingest_async(const void* data, int dtype, int location, int order, 
         if (bc.init_failed) Y.swap(Ynext);  // a CP-ALS failure keeps the updated summaries
         std::rethrow_exception(begin_err);
     }
-    // this batch's sweeps on its engine
-    bc.models = models;
-    AlsEngine* e = &eng;
-    aworker.post(cfg.device, [this, &bc, e, models] {
-        try {
-            als_sweep_phase(bc, models, *e, ast, 2);
-        } catch (...) {
-            fail_pending(bc);
-        }
-    });
-    a_prev = &bc;
     // summaries: Yhold <- the previous batch's (its merge reads them), Y <-
     // this batch's, Ynext <- the buffer the merge before released
     Yhold.swap(Y);

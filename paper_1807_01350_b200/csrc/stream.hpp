@@ -212,6 +212,7 @@ public:
     double* dW = nullptr;
     DevBuf<double> xmodels, xrows, MfAll, MlamAll, tstackAll;
     DevBuf<double> xmodels2;     // pipelined ingest: models of the batch in flight (NCCL: all-gathered models)
+    DevBuf<double> xmodels3;     // pipelined ingest: one models buffer per context slot (three batches overlap)
     DevBuf<double> rows_all_buf, part_buf, owned_buf;  // NCCL exchange buffers
     DevBuf<float> X32, XT32;     // staged batch; its temporal-last reorder (temporal mode not last)
     DevBuf<double> XT64, MfSlot;
