@@ -72,11 +72,11 @@ def pipe_peaks():
 
 def isolated_launch_ms():
     """Mean per-launch duration (ms) of the CP-ALS kernels in the committed
-    ncu launch list of the c3 bench (profiles/r2s3_launches_c3.csv)."""
+    ncu launch list of the c3 bench (profiles/r2s4_launches_c3.csv)."""
     out = {}
     try:
         import csv
-        with open(os.path.join(ROOT, "profiles", "r2s3_launches_c3.csv")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2s4_launches_c3.csv")) as f:
             rows = [r for r in csv.reader(f)]
         h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
         hdr = rows[h]
@@ -963,7 +963,7 @@ def main():
             live = r["ms_per_launch"]
             r["isolated"] = {"ms_per_launch": iso[kname], "achieved": r["achieved"] * live / iso[kname],
                              "frac": r["frac"] * live / iso[kname],
-                             "source": "ncu launch list profiles/r2s3_launches_c3.csv (gpu__time_duration, "
+                             "source": "ncu launch list profiles/r2s4_launches_c3.csv (gpu__time_duration, "
                                        "serialised, cold caches)"}
             if "fp64_equiv_tflops" in r:
                 r["isolated"]["fp64_equiv_frac_of_dmma_peak"] = r["fp64_equiv_frac_of_dmma_peak"] * live / iso[kname]
