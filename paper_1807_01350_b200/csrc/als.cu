@@ -863,6 +863,19 @@ __device__ __forceinline__ void mttkrp_column_v2(const double* __restrict__ tcol
     }
 }
 
+// Diagnostics, compiled in with -DOCTEN_ALS_GT_STAMPS only (the stamps cost the
+// contraction kernel registers): %globaltimer marks (ns) of problem 0's V^-1
+// block, first column block and mode update within one MTTKRP launch.
+__device__ __forceinline__ void als_gt_stamp(const AlsDev& d, int i) {
+#ifdef OCTEN_ALS_GT_STAMPS
+    if (d.tsc && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        d.tsc[i] = (long long)t;
+    }
+#endif
+}
+
 // The first NP blocks instead form Vi of `mode` (als_vinv_block).  With
 // `fused`, the last of a problem's R + 1 blocks to finish (fence + counter)
 // runs the mode update for it (als_update_block), so the update needs no
@@ -878,7 +891,9 @@ __global__ void __launch_bounds__(256, 3) als_mttkrp_T_kernel(AlsDev d, int cont
     if ((int)blockIdx.x < d.NP) {
         prob = blockIdx.x;
         if (!d.state[prob].active) return;
+        if (prob == 0) als_gt_stamp(d, 32);
         als_vinv_block(d, prob, mode, vsm);
+        if (prob == 0) als_gt_stamp(d, 33);
     } else {
         const int bid = blockIdx.x - d.NP;
         prob = bid / R;
@@ -888,11 +903,15 @@ __global__ void __launch_bounds__(256, 3) als_mttkrp_T_kernel(AlsDev d, int cont
         const double* tcol = d.T + (size_t)p * d.q2() * d.S * R + (size_t)d.q2() * (s * R + r);
         double* M = d.Mb + (size_t)prob * Q * R + (size_t)Q * r;
         const double* w = d.f(prob, fsrc) + (size_t)Q * r;
+        if (bid == 0) als_gt_stamp(d, 34);
         if (NA == 0)
             mttkrp_column_v2(tcol, w, M, Q, contract_first);
         else
             mttkrp_column<NA == 0 ? 4 : NA>(tcol, w, M, Q, contract_first);
     }
+#ifdef OCTEN_ALS_GT_STAMPS
+    if (d.tsc && blockIdx.x == (unsigned)d.NP) { __syncthreads(); als_gt_stamp(d, 35); }
+#endif
     if (!fused) return;
     __shared__ int last;
     __syncthreads();
@@ -904,7 +923,11 @@ __global__ void __launch_bounds__(256, 3) als_mttkrp_T_kernel(AlsDev d, int cont
     if (!last) return;
     __threadfence();
     if (threadIdx.x == 0) d.mcount[prob] = 0;
+    if (prob == 0) als_gt_stamp(d, 36);
     als_update_block(d, prob, mode, sweep, vsm);
+#ifdef OCTEN_ALS_GT_STAMPS
+    if (prob == 0) { __syncthreads(); als_gt_stamp(d, 37); }
+#endif
 }
 
 
@@ -1929,6 +1952,11 @@ void AlsEngine::run_sweeps(cudaStream_t st) {
         for (int i = 1; i < 32; ++i)
             if (t[i]) std::fprintf(stderr, " [%d] %lld", i, t[i] - t[0]);
         std::fprintf(stderr, "\n");
+#ifdef OCTEN_ALS_GT_STAMPS
+        const long long b = t[32] ? t[32] : t[34];
+        std::fprintf(stderr, "octen als mttkrp launch, problem 0 (ns from the earlier start): vinv %lld..%lld, column block 0 %lld..%lld, update %lld..%lld\n",
+                     t[32] - b, t[33] - b, t[34] - b, t[35] - b, t[36] - b, t[37] - b);
+#endif
     }
     if (std::getenv("OCTEN_DEBUG_ALS")) {
         const std::vector<int> ed = eigdbg.to_host(1, st);
