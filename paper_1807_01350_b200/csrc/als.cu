@@ -1851,18 +1851,26 @@ void AlsEngine::run_sweeps(cudaStream_t st) {
             }
         }
         OCTEN_CUDA(cudaGetLastError());
-        if (seg == 1) OCTEN_CUDA(cudaEventRecord(lane_ev[kSweepEv + kMaxLanes * (sw & 1) + l], ss));
+        if (seg == 1) OCTEN_CUDA(cudaEventRecord(lane_ev[kSweepEv + kMaxLanes * (sw & 3) + l], ss));
     };
+    // The host stays `ahead` sweeps in front of the device (a ring of four
+    // sweep events): the sweeps queued past the one every problem stopped in
+    // find no active problem and return at once, so the results do not depend
+    // on the depth.
+    static const int ahead = [] {
+        const char* e = std::getenv("OCTEN_ALS_LOOKAHEAD");
+        return e ? std::max(1, std::min(3, std::atoi(e))) : 1;
+    }();
     int sweep = 0;
     for (; sweep < max_iters; ++sweep) {
         for (int seg = 0; seg < 2; ++seg)
             for (int l = 0; l < L; ++l) launch_seg(l, sweep, seg);
-        if (sweep >= 1) {
-            // problems still active after the previous sweep
+        if (sweep >= ahead) {
+            // problems still active after sweep `sweep - ahead`
             int left = 0;
             for (int l = 0; l < L; ++l) {
-                OCTEN_CUDA(cudaEventSynchronize(lane_ev[kSweepEv + kMaxLanes * ((sweep - 1) & 1) + l]));
-                left += reinterpret_cast<volatile int*>(hact)[(size_t)(sweep - 1) * kMaxLanes + l];
+                OCTEN_CUDA(cudaEventSynchronize(lane_ev[kSweepEv + kMaxLanes * ((sweep - ahead) & 3) + l]));
+                left += reinterpret_cast<volatile int*>(hact)[(size_t)(sweep - ahead) * kMaxLanes + l];
             }
             ++host_syncs;
             if (left == 0) {

@@ -108,9 +108,9 @@ private:
     cudaStream_t gemm_st = nullptr;         //   and the lanes' T-GEMMs (low priority)
     cudaStream_t lane_gemm[kMaxLanes] = {}; // OCTEN_ALS_GEMM_STREAM=2: one low-priority GEMM stream per lane
     // lane_ev: [0] fork/join, [kGin + l] lane -> GEMM stream, [kGout + l]
-    // GEMM stream -> lane, [kSweepEv + 4 (sweep & 1) + l] end of a sweep
+    // GEMM stream -> lane, [kSweepEv + kMaxLanes (sweep & 3) + l] end of a sweep
     static constexpr int kGin = 1, kGout = 1 + kMaxLanes, kSweepEv = 1 + 2 * kMaxLanes;
-    cudaEvent_t lane_ev[1 + 4 * kMaxLanes] = {};
+    cudaEvent_t lane_ev[1 + 6 * kMaxLanes] = {};
     std::vector<cudaEvent_t> kev;   // timing event pool: pairs (start, end)
     struct KevRec {
         int ev;        // index of the start event (end = ev + 1)
